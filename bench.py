@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""bench.py -- ops analysed per second for the Apophenia repeat-finding hot
+path (SA + LCP + non-overlapping repeat selection, Alg. 2) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C4|C3|C2|C5]
+
+One step = one apo_find_repeats_batched call over the whole workload batch
+(all stages: SA, LCP, candidates, ordering, greedy selection, dedup/output),
+inputs resident in HBM.  Multi-GPU (torchrun, one process per GPU): every rank
+analyses its own C4-shaped batch (weak scaling, no data-path collective); the
+time is the max over ranks.  Prints ONE JSON line on rank 0.
+
+--impl reference times the CPU oracle (tier 0, the literal Alg. 2) on the
+host cores on a bounded sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ops analysed/sec (SA+LCP+repeat select) at 1/2/4/8 B200; HBM GB/s vs peak"
+MIN_LEN = 25
+
+
+def make_workload(cfg: str, rank: int):
+    from workloads import gen
+    if cfg == "C4":
+        tok, off, _, _ = gen.c4(seed=4 + rank, with_streams=False)
+        desc = dict(workload="C4: batch of 4,096 independent 16,384-op windows (64 loop templates), min_len 25",
+                    windows=len(off) - 1, window=int(off[1] - off[0]), min_len=MIN_LEN,
+                    seed=4 + rank if rank else 4)
+    else:
+        S = gen.CONFIGS[cfg]["gen"]()
+        tok, off = S, np.array([0, len(S)], dtype=np.int64)
+        desc = dict(workload=f"{cfg}: single {len(S):,}-op window", windows=1, window=len(S), min_len=MIN_LEN)
+    return tok, off, desc
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.lines: list[str] = []
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+        return self
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed
+    `ncu --set full` summary (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
+def cpu_baseline_sample(tok, off, budget_s: float, max_windows: int | None = None):
+    """The oracle as it stands (tier 0: naive SA, direct LCP, literal Alg. 2),
+    one host thread, on the first windows of the workload until budget_s."""
+    import oracle
+    oracle.build()
+    t0 = time.perf_counter()
+    ops = 0
+    nwin = 0
+    W = len(off) - 1
+    for w in range(W):
+        S = tok[off[w]:off[w + 1]]
+        oracle.find_repeats(S, MIN_LEN, tier=0)
+        ops += len(S)
+        nwin += 1
+        if time.perf_counter() - t0 > budget_s or (max_windows and nwin >= max_windows):
+            break
+    dt = time.perf_counter() - t0
+    return ops / dt, nwin, ops, dt
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return 0
+    tok, off, desc = make_workload(args.config, 0)
+    W = len(off) - 1
+    per_step = 2 if W > 1 else 1
+    if W == 1 and len(tok) > 100_000:
+        # a single huge window: the bounded sample is a prefix window
+        tok, off = tok[:65536], np.array([0, 65536])
+        desc["sample_prefix"] = 65536
+    times, ops = [], 0
+    w = 0
+    for it in range(args.warmup + args.steps):
+        sl = [(w + j) % (len(off) - 1) for j in range(per_step)]
+        w += per_step
+        t0 = time.perf_counter()
+        n = 0
+        import oracle
+        for ww in sl:
+            S = tok[off[ww]:off[ww + 1]]
+            oracle.find_repeats(S, MIN_LEN, tier=0)
+            n += len(S)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+            ops += n
+    total = sum(times)
+    v = ops / total
+    out = {"metric": METRIC, "value": v, "unit": "ops/s", "impl": "reference", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+           "data": "synthetic", "config": desc,
+           "cpu_baseline": {"value": v, "unit": "ops/s", "cores": 1, "kind": "oracle",
+                            "sample": f"{per_step} window(s) of the workload per step, tier-0 oracle "
+                                      f"(naive comparison-sort SA, direct LCP, literal Alg. 2), one host thread"},
+           "e2e": {"value": v, "unit": "ops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4", choices=["C2", "C3", "C4", "C5"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2406_18111_b200 import Context
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    ctx = Context(local)
+    tok_np, off, desc = make_workload(args.config, rank)
+    N = int(off[-1])
+    tok = torch.from_numpy(tok_np).to(dev)
+    cap = N // MIN_LEN + 1
+    W = len(off) - 1
+    bufs = (torch.empty((cap, 4), dtype=torch.int32, device=dev), torch.empty(W + 1, dtype=torch.int64, device=dev),
+            torch.empty(cap, dtype=torch.int32, device=dev), torch.zeros(2, dtype=torch.int64, device=dev))
+
+    def step():
+        return ctx.find_repeats_batched(tok, off, MIN_LEN, sync=False, out=bufs)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device events on the launching stream) ----
+    s = torch.cuda.current_stream(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.profile(True)
+    l0 = ctx.launches
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(s)
+        for _ in range(args.steps):
+            step()
+        ev1.record(s)
+        torch.cuda.synchronize()
+        barrier()
+    launches = ctx.launches - l0
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    ctx.profile(False)
+    rp_ms, rp_n, rp_bytes = ctx.profile_read(ctx.PROF_RADIX_PASS)
+    sc_ms, sc_n, _ = ctx.profile_read(ctx.PROF_SCAN)
+    rh_ms, rh_n, _ = ctx.profile_read(ctx.PROF_RADIX_HIST)
+    counts = bufs[3].tolist()
+    value = N * world * args.steps / (ms / 1e3)
+
+    # ---- end to end through the public API with HOST buffers ----
+    e2e = None
+    if not args.no_e2e:
+        tok_host = torch.from_numpy(tok_np).pin_memory()
+        for _ in range(1):
+            ctx.find_repeats_batched_host(tok_host, off, MIN_LEN)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d2h = 0
+        e0.record(s)
+        for _ in range(args.steps):
+            rep, roff, occ = ctx.find_repeats_batched_host(tok_host, off, MIN_LEN)
+            d2h = rep.numel() * 4 + roff.numel() * 8 + occ.numel() * 4 + 16
+        e1.record(s)
+        torch.cuda.synchronize()
+        barrier()
+        ems = max_over_ranks(e0.elapsed_time(e1))
+        e2e = {"value": N * world * args.steps / (ems / 1e3), "unit": "ops/s",
+               "h2d_bytes_per_step": N * 8 + (W + 1) * 8, "d2h_bytes_per_step": int(d2h)}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    peak, peak_src = peak_hbm()
+    avg_pass_s = (rp_ms / rp_n) / 1e3 if rp_n else None
+    achieved = (rp_bytes / rp_n) / avg_pass_s / 1e9 if rp_n else None
+    tr = ncu_traffic()
+    roofline = {"bound": "hbm", "kernel": "k_onesweep (radix-sort digit pass)", "achieved": achieved,
+                "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                "traffic_source": tr.get("source") if tr else None,
+                "launches": rp_n, "bytes_per_launch": rp_bytes / rp_n if rp_n else None,
+                "share_of_step": (rp_ms / ms) if ms else None,
+                "scan_share_of_step": sc_ms / ms if ms else None,
+                "hist_share_of_step": rh_ms / ms if ms else None}
+    cpu = None
+    if world == 1:
+        v, nwin, ops, dt = cpu_baseline_sample(tok_np, off, args.cpu_budget)
+        cpu = {"value": v, "unit": "ops/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {nwin} window(s) ({ops:,} ops) of the same workload, tier-0 oracle (naive "
+                         f"comparison-sort SA, direct LCP, literal Alg. 2), one host thread, {dt:.1f} s"}
+    desc = dict(desc)
+    desc["l2"] = f"inputs ({N * 8 / 2**20:.0f} MiB of tokens per GPU) larger than the 126 MB L2; no flush"
+    desc["repeats_found"] = int(counts[0])
+    out = {"metric": METRIC, "value": value, "unit": "ops/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "u64", "data": "synthetic", "config": desc,
+           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+           "clocks": clk.summary()}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

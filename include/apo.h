@@ -1,0 +1,187 @@
+/*
+ * apo.h -- C ABI of the B200-native Apophenia repeat-finding hot path
+ * (arXiv 2406.18111, "Apophenia: automatic trace identification").
+ *
+ * Library: paper_2406_18111_b200/libapo.so (hand-written sm_100a CUDA).
+ * Citations "P:n" are lines of the paper text; R1..R17 are the
+ * readings of the paper listed in DESIGN.md §3.
+ *
+ * General conventions
+ *  - Every pointer named d_* is a caller-owned DEVICE pointer (e.g. a torch
+ *    tensor's data_ptr()) on the context's device; h_* pointers are host
+ *    memory.  The library never frees caller memory.  Opaque handles
+ *    (apo_ctx, apo_history, apo_trie) own their device workspace, released by
+ *    the matching *_destroy call.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  All device
+ *    work is enqueued on it.  Data-dependent loop trip counts (prefix-doubling
+ *    rounds, greedy rounds) are currently resolved with a small host read of a
+ *    device flag, so the calls return with their results complete on `stream`.
+ *  - Tokens are uint64 op hashes ordered as unsigned integers (R1).  A suffix
+ *    that is a proper prefix of another sorts first (R2).
+ *  - Positions, lengths and counts on the device are int32 unless stated.
+ *    Window/stream offsets are int64.  A single window has n <= 2^30 tokens.
+ *  - Capacity: when an output has more records than its capacity, the true
+ *    count is still written and only the first `cap` records are stored; the
+ *    caller detects this after synchronising and retries.
+ *  - Errors: APO_ERR_INVALID for bad arguments (NULL with n > 0, negative
+ *    sizes, min_len < 1); APO_ERR_NOMEM when device workspace cannot be
+ *    allocated; APO_ERR_CUDA for CUDA failures (text via apo_last_error).
+ *    n == 0 and n < 2*min_len are not errors: the result is empty.
+ *  - A context is not thread-safe: use one per host thread.  Results are
+ *    bit-identical across runs and batch compositions.
+ */
+#ifndef APO_H
+#define APO_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  APO_OK = 0,
+  APO_ERR_INVALID = 1,
+  APO_ERR_CAPACITY = 2,
+  APO_ERR_NOMEM = 3,
+  APO_ERR_CUDA = 4
+} apo_status;
+
+typedef struct apo_ctx apo_ctx;
+typedef struct apo_history apo_history;
+typedef struct apo_trie apo_trie;
+
+/* Analysis parameters (the paper's -lg:auto_trace flags). */
+typedef struct {
+  int32_t min_count; /* keep repeats selected >= min_count times; 1 = paper-literal (R10) */
+  int32_t max_len;   /* trie chunking "maximum trace length" (R15); 0 = unbounded */
+  uint32_t flags;    /* reserved, must be 0 */
+  int32_t reserved;  /* must be 0 */
+} apo_params;
+
+/* One deduplicated repeat of FindRepeats (Alg. 2; R10, R11):
+ * start = smallest selected start (window-local), length, count = number of
+ * selected non-overlapping occurrences, first_occ = index of its first
+ * occurrence in the occurrence array.  Repeats are ordered by
+ * (length desc, sub-string lexicographic asc) within a window. */
+typedef struct {
+  int32_t start, length, count, first_occ;
+} apo_repeat;
+
+/* [begin, end) in absolute history coordinates (global op count). */
+typedef struct {
+  int64_t begin, end;
+} apo_slice;
+
+/* One MATCH_ALL hit: trace `trace_id` ends at position `end_pos` of stream
+ * `stream` (Alg. 1 Advance/FilterCompleted; R14). */
+typedef struct {
+  int32_t stream, end_pos, trace_id, _pad;
+} apo_match_rec;
+
+int apo_version(void);
+apo_status apo_ctx_create(int cuda_device, apo_ctx **out);
+void apo_ctx_destroy(apo_ctx *ctx);
+/* Text of the last error on this context ("" if none).  Owned by ctx. */
+const char *apo_last_error(const apo_ctx *ctx);
+/* Number of CUDA kernels the library has launched on this context so far
+ * (introspection for benchmarks; monotone). */
+int64_t apo_launch_count(const apo_ctx *ctx);
+
+/* In-library profiler (for bench.py's roofline): when enabled, selected
+ * kernel launches are bracketed by CUDA events recorded on the launching
+ * stream.  apo_profile(ctx, 1) clears and starts recording, 0 stops.
+ * apo_profile_read synchronises on the recorded events and returns, for
+ * kernel class `kind` (0 = radix-sort digit pass, 1 = radix histogram,
+ * 2 = single-pass scans, 3 = other), the summed device time in ms, the
+ * number of launches and the summed ALGORITHMIC bytes (each element's
+ * key/value read once and written once).  Any output pointer may be NULL. */
+apo_status apo_profile(apo_ctx *ctx, int enable);
+apo_status apo_profile_read(apo_ctx *ctx, int kind, double *ms, int64_t *launches, double *bytes);
+
+/* ---------------------------------------------------------------------- */
+/* Alg. 2 building blocks (exposed for parity)                              */
+/* ---------------------------------------------------------------------- */
+
+/* "SA, LCP <- SuffixArray(S)".  d_tok: n tokens.  d_sa: n int32,
+ * receives the suffix array (start positions in increasing suffix order).
+ * d_lcp: n int32 or NULL; d_lcp[i] = LCP(SA[i], SA[i+1]) for i < n-1 (R3) and
+ * d_lcp[n-1] = 0. */
+apo_status apo_suffix_array(apo_ctx *ctx, const uint64_t *d_tok, int32_t n, int32_t *d_sa,
+                            int32_t *d_lcp, void *stream);
+
+/* Same for a CSR batch of independent windows (R16).  h_off: HOST
+ * int64[nwin+1], h_off[0] = 0, non-decreasing; window w is
+ * d_tok[h_off[w] .. h_off[w+1]).  d_sa / d_lcp: h_off[nwin] int32 each; the
+ * window's entries sit at the same offsets, in WINDOW-LOCAL coordinates; the
+ * last LCP slot of each window is 0. */
+apo_status apo_suffix_array_batched(apo_ctx *ctx, const uint64_t *d_tok, const int64_t *h_off,
+                                    int32_t nwin, int32_t *d_sa, int32_t *d_lcp, void *stream);
+
+/* Candidate list of Alg. 2 in the paper's sort order
+ * "by decreasing length and by increasing sub-string and start position",
+ * with the greedy decision of P:576-583 for each.  Per candidate i:
+ * d_len[i], d_id[i] (dense ordinal of the distinct sub-string in this order;
+ * equal sub-strings share an id), d_start[i], d_kept[i] (1 = selected).
+ * Candidates shorter than min_len are not generated (R7).  d_count (device
+ * int64[1]) receives the candidate count m; at most cap are stored. */
+apo_status apo_candidates(apo_ctx *ctx, const uint64_t *d_tok, int32_t n, int32_t min_len,
+                          int32_t *d_len, int32_t *d_id, int32_t *d_start, uint8_t *d_kept,
+                          int64_t cap, int64_t *d_count, void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* FindRepeats (Alg. 2) -- the north_star call                              */
+/* ---------------------------------------------------------------------- */
+
+/* One window d_win[0..n).  params may be NULL (defaults: min_count 1).
+ * d_out: cap apo_repeat records.  d_occ: occ_cap int32 occurrence starts
+ * (window-local; per repeat in increasing order) or NULL.  d_counts: device
+ * int64[2] <- {number of repeats, number of occurrences}. */
+apo_status apo_find_repeats(apo_ctx *ctx, const uint64_t *d_win, int32_t n, int32_t min_len,
+                            const apo_params *params, apo_repeat *d_out, int64_t cap,
+                            int32_t *d_occ, int64_t occ_cap, int64_t *d_counts, void *stream);
+
+/* CSR batch of independent windows (h_off as in apo_suffix_array_batched).
+ * Output is window-major; d_out_off: device int64[nwin+1], repeats of window
+ * w are d_out[d_out_off[w] .. d_out_off[w+1]) with window-local starts;
+ * first_occ indexes the batch-wide d_occ.  d_counts: device int64[2] <-
+ * {total repeats, total occurrences}.  Identical, window by window, to
+ * apo_find_repeats on each window (R16). */
+apo_status apo_find_repeats_batched(apo_ctx *ctx, const uint64_t *d_tok, const int64_t *h_off,
+                                    int32_t nwin, int32_t min_len, const apo_params *params,
+                                    apo_repeat *d_out, int64_t cap, int64_t *d_out_off,
+                                    int32_t *d_occ, int64_t occ_cap, int64_t *d_counts,
+                                    void *stream);
+
+/* ---------------------------------------------------------------------- */
+/* Alg. 1 TraceFinder: token history + ruler-function sampling (§4.4)       */
+/* ---------------------------------------------------------------------- */
+
+/* History ring of the last capacity_B tokens (R13); analyses are scheduled
+ * every scale_C tokens ("multiples of a larger constant (such as 250)",
+ * P:763-764).  capacity_B >= scale_C >= 1. */
+apo_status apo_history_create(apo_ctx *ctx, int64_t capacity_B, int32_t scale_C,
+                              apo_history **out);
+void apo_history_destroy(apo_history *h);
+
+/* "B <- B + [H]" (Alg. 1) for n tokens d_tokens[0..n), then the
+ * slices "ShouldAnalyzeHistory / GetAnalysisSubset" selects while the global
+ * op count k goes from k0+1 to k0+n: at every k with k % C == 0 the slice
+ * [k - min(2^ruler(k/C) * C, B), k) (R13).  h_slices receives up
+ * to cap slices in order; *h_nslices the true number (APO_ERR_CAPACITY if it
+ * exceeds cap; the tokens are still appended). */
+apo_status apo_ingest(apo_history *h, const uint64_t *d_tokens, int64_t n, apo_slice *h_slices,
+                      int64_t cap, int64_t *h_nslices, void *stream);
+
+/* Copy history tokens [begin, end) (absolute coordinates, must lie within
+ * the last capacity_B tokens) to d_out (end-begin tokens). */
+apo_status apo_history_window(apo_history *h, int64_t begin, int64_t end, uint64_t *d_out,
+                              void *stream);
+
+/* Total number of tokens ever ingested. */
+int64_t apo_history_count(const apo_history *h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* APO_H */

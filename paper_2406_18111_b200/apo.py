@@ -1,0 +1,322 @@
+"""Thin ctypes binding of libapo (include/apo.h) -- argument marshalling only.
+
+Every step of the path runs in the CUDA kernels of libapo.so; this module only
+passes torch device pointers, sizes and the current CUDA stream.  There is no
+CPU fallback: if libapo.so is missing or no CUDA device is present, calls
+raise.
+
+Names follow the C ABI: suffix_array, suffix_array_batched, candidates,
+find_repeats, find_repeats_batched, History.ingest / .window.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libapo.so")
+
+APO_OK, APO_ERR_INVALID, APO_ERR_CAPACITY, APO_ERR_NOMEM, APO_ERR_CUDA = range(5)
+_STATUS = {0: "APO_OK", 1: "APO_ERR_INVALID", 2: "APO_ERR_CAPACITY", 3: "APO_ERR_NOMEM", 4: "APO_ERR_CUDA"}
+
+
+class ApoError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class apo_params(ctypes.Structure):
+    _fields_ = [("min_count", ctypes.c_int32), ("max_len", ctypes.c_int32),
+                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_int32)]
+
+
+class apo_slice(ctypes.Structure):
+    _fields_ = [("begin", ctypes.c_int64), ("end", ctypes.c_int64)]
+
+
+_VP = ctypes.c_void_p
+_I32 = ctypes.c_int32
+_I64 = ctypes.c_int64
+_P_I64 = ctypes.POINTER(ctypes.c_int64)
+
+_SIGS = {
+    "apo_version": (ctypes.c_int, []),
+    "apo_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_VP)]),
+    "apo_ctx_destroy": (None, [_VP]),
+    "apo_last_error": (ctypes.c_char_p, [_VP]),
+    "apo_launch_count": (ctypes.c_int64, [_VP]),
+    "apo_profile": (ctypes.c_int, [_VP, ctypes.c_int]),
+    "apo_profile_read": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.POINTER(ctypes.c_double), _P_I64,
+                                        ctypes.POINTER(ctypes.c_double)]),
+    "apo_suffix_array": (ctypes.c_int, [_VP, _VP, _I32, _VP, _VP, _VP]),
+    "apo_suffix_array_batched": (ctypes.c_int, [_VP, _VP, _P_I64, _I32, _VP, _VP, _VP]),
+    "apo_candidates": (ctypes.c_int, [_VP, _VP, _I32, _I32, _VP, _VP, _VP, _VP, _I64, _VP, _VP]),
+    "apo_find_repeats": (ctypes.c_int, [_VP, _VP, _I32, _I32, ctypes.POINTER(apo_params), _VP, _I64, _VP,
+                                        _I64, _VP, _VP]),
+    "apo_find_repeats_batched": (ctypes.c_int, [_VP, _VP, _P_I64, _I32, _I32, ctypes.POINTER(apo_params), _VP,
+                                                _I64, _VP, _VP, _I64, _VP, _VP]),
+    "apo_history_create": (ctypes.c_int, [_VP, _I64, _I32, ctypes.POINTER(_VP)]),
+    "apo_history_destroy": (None, [_VP]),
+    "apo_ingest": (ctypes.c_int, [_VP, _VP, _I64, ctypes.POINTER(apo_slice), _I64, _P_I64, _VP]),
+    "apo_history_window": (ctypes.c_int, [_VP, _I64, _I64, _VP, _VP]),
+    "apo_history_count": (ctypes.c_int64, [_VP]),
+}
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libapo.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise ImportError(f"{path} not found: build it with `python -m paper_2406_18111_b200.build` "
+                              "(there is no CPU fallback)")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _check_tok(t: torch.Tensor, device) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError("token tensor must be on the CUDA device (use the *_host helpers for host buffers)")
+    if t.dtype not in (torch.uint64, torch.int64):
+        raise ValueError("tokens must be uint64 (or int64 bit patterns)")
+    return t.contiguous()
+
+
+def _host_off(off) -> np.ndarray:
+    if isinstance(off, torch.Tensor):
+        off = off.cpu().numpy()
+    return np.ascontiguousarray(np.asarray(off, dtype=np.int64))
+
+
+class Context:
+    """An apo_ctx on one CUDA device (not thread-safe; one per host thread)."""
+
+    def __init__(self, device: int | torch.device = 0):
+        if not torch.cuda.is_available():
+            raise RuntimeError("libapo needs a CUDA device (no CPU fallback)")
+        self.lib = load_library()
+        self.device = torch.device("cuda", device if isinstance(device, int) else device.index or 0)
+        h = ctypes.c_void_p()
+        torch.cuda.init()
+        st = self.lib.apo_ctx_create(self.device.index, ctypes.byref(h))
+        if st != APO_OK:
+            raise ApoError(st, "apo_ctx_create failed")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.apo_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _raise(self, st: int):
+        if st not in (APO_OK,):
+            msg = self.lib.apo_last_error(self.h)
+            raise ApoError(st, msg.decode() if msg else "")
+
+    @property
+    def launches(self) -> int:
+        """Kernel launches issued by libapo on this context so far."""
+        return int(self.lib.apo_launch_count(self.h))
+
+    # ----------------------------------------------------------- profiler --
+    PROF_RADIX_PASS, PROF_RADIX_HIST, PROF_SCAN, PROF_OTHER = range(4)
+
+    def profile(self, enable: bool):
+        self._raise(self.lib.apo_profile(self.h, 1 if enable else 0))
+
+    def profile_read(self, kind: int):
+        """-> (device ms, launches, algorithmic bytes) summed over the recorded launches of `kind`."""
+        ms, by = ctypes.c_double(), ctypes.c_double()
+        k = ctypes.c_int64()
+        self._raise(self.lib.apo_profile_read(self.h, int(kind), ctypes.byref(ms), ctypes.byref(k), ctypes.byref(by)))
+        return ms.value, k.value, by.value
+
+    # ---------------------------------------------------------- SA / LCP --
+    def suffix_array(self, tok: torch.Tensor, lcp: bool = True):
+        tok = _check_tok(tok, self.device)
+        n = tok.numel()
+        sa = torch.empty(n, dtype=torch.int32, device=self.device)
+        lc = torch.empty(n, dtype=torch.int32, device=self.device) if lcp else None
+        self._raise(self.lib.apo_suffix_array(self.h, _ptr(tok), n, _ptr(sa), _ptr(lc), _stream(self.device)))
+        return (sa, lc[:max(n - 1, 0)]) if lcp else sa
+
+    def suffix_array_batched(self, tok: torch.Tensor, off):
+        tok = _check_tok(tok, self.device)
+        o = _host_off(off)
+        n = int(o[-1])
+        sa = torch.empty(n, dtype=torch.int32, device=self.device)
+        lc = torch.empty(n, dtype=torch.int32, device=self.device)
+        self._raise(self.lib.apo_suffix_array_batched(self.h, _ptr(tok), o.ctypes.data_as(_P_I64), len(o) - 1,
+                                                      _ptr(sa), _ptr(lc), _stream(self.device)))
+        return sa, lc
+
+    # --------------------------------------------------------- candidates --
+    def candidates(self, tok: torch.Tensor, min_len: int):
+        tok = _check_tok(tok, self.device)
+        n = tok.numel()
+        cap = max(2 * (n - 1), 1)
+        d = self.device
+        ln = torch.empty(cap, dtype=torch.int32, device=d)
+        cid = torch.empty(cap, dtype=torch.int32, device=d)
+        st = torch.empty(cap, dtype=torch.int32, device=d)
+        kept = torch.empty(cap, dtype=torch.uint8, device=d)
+        cnt = torch.zeros(1, dtype=torch.int64, device=d)
+        self._raise(self.lib.apo_candidates(self.h, _ptr(tok), n, int(min_len), _ptr(ln), _ptr(cid), _ptr(st),
+                                            _ptr(kept), cap, _ptr(cnt), _stream(d)))
+        m = int(cnt.item())
+        return dict(cand_len=ln[:m], cand_id=cid[:m], cand_start=st[:m], keep=kept[:m])
+
+    # ------------------------------------------------------- FindRepeats --
+    @staticmethod
+    def _params(min_count: int) -> apo_params:
+        return apo_params(int(min_count), 0, 0, 0)
+
+    def find_repeats(self, win: torch.Tensor, min_len: int, min_count: int = 1, sync: bool = True):
+        """Alg. 2 on one window -> (repeats int32[k,4] (start,length,count,first_occ), occ int32[])."""
+        win = _check_tok(win, self.device)
+        n = win.numel()
+        cap = n // max(int(min_len), 1) + 1  # kept intervals are disjoint and >= min_len long
+        d = self.device
+        out = torch.empty((cap, 4), dtype=torch.int32, device=d)
+        occ = torch.empty(cap, dtype=torch.int32, device=d)
+        counts = torch.zeros(2, dtype=torch.int64, device=d)
+        prm = self._params(min_count)
+        self._raise(self.lib.apo_find_repeats(self.h, _ptr(win), n, int(min_len), ctypes.byref(prm), _ptr(out), cap,
+                                              _ptr(occ), cap, _ptr(counts), _stream(d)))
+        if not sync:
+            return out, occ, counts
+        r, o = (int(x) for x in counts.tolist())
+        return out[:r], occ[:o]
+
+    def find_repeats_batched(self, tok: torch.Tensor, off, min_len: int, min_count: int = 1, sync: bool = True,
+                             out=None):
+        """Independent windows -> (repeats int32[k,4], out_off int64[W+1], occ int32[])."""
+        tok = _check_tok(tok, self.device)
+        o = _host_off(off)
+        n = int(o[-1])
+        W = len(o) - 1
+        d = self.device
+        cap = n // max(int(min_len), 1) + 1
+        if out is None:
+            out = (torch.empty((cap, 4), dtype=torch.int32, device=d), torch.empty(W + 1, dtype=torch.int64, device=d),
+                   torch.empty(cap, dtype=torch.int32, device=d), torch.zeros(2, dtype=torch.int64, device=d))
+        rep, roff, occ, counts = out
+        prm = self._params(min_count)
+        self._raise(self.lib.apo_find_repeats_batched(self.h, _ptr(tok), o.ctypes.data_as(_P_I64), W, int(min_len),
+                                                      ctypes.byref(prm), _ptr(rep), rep.shape[0], _ptr(roff),
+                                                      _ptr(occ), occ.shape[0], _ptr(counts), _stream(d)))
+        if not sync:
+            return rep, roff, occ, counts
+        r, oc = (int(x) for x in counts.tolist())
+        return rep[:r], roff, occ[:oc]
+
+    def find_repeats_batched_host(self, tok_host: torch.Tensor, off, min_len: int, min_count: int = 1):
+        """End-to-end user call with HOST buffers: H2D copy of the tokens,
+        the batched analysis, D2H copy of the results (pinned host memory)."""
+        tok = tok_host.to(self.device, non_blocking=True)
+        rep, roff, occ, counts = self.find_repeats_batched(tok, off, min_len, min_count, sync=False)
+        c = counts.to("cpu")
+        r, oc = int(c[0]), int(c[1])
+        return rep[:r].to("cpu"), roff.to("cpu"), occ[:oc].to("cpu")
+
+    # ------------------------------------------------------------ history --
+    def history(self, capacity_B: int, scale_C: int) -> "History":
+        return History(self, capacity_B, scale_C)
+
+
+class History:
+    """Alg. 1 TraceFinder buffer with ruler-function sampling (§4.4)."""
+
+    def __init__(self, ctx: Context, capacity_B: int, scale_C: int):
+        self.ctx = ctx
+        h = ctypes.c_void_p()
+        st = ctx.lib.apo_history_create(ctx.h, int(capacity_B), int(scale_C), ctypes.byref(h))
+        ctx._raise(st)
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.ctx.lib.apo_history_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    @property
+    def count(self) -> int:
+        return int(self.ctx.lib.apo_history_count(self.h))
+
+    def ingest(self, tokens: torch.Tensor, cap: int = 4096) -> list[tuple[int, int]]:
+        tokens = _check_tok(tokens, self.ctx.device)
+        buf = (apo_slice * max(cap, 1))()
+        ns = ctypes.c_int64()
+        st = self.ctx.lib.apo_ingest(self.h, _ptr(tokens), tokens.numel(), buf, cap, ctypes.byref(ns),
+                                     _stream(self.ctx.device))
+        if st == APO_ERR_CAPACITY:
+            raise ApoError(st, f"{ns.value} slices > cap {cap}")
+        self.ctx._raise(st)
+        return [(buf[i].begin, buf[i].end) for i in range(ns.value)]
+
+    def window(self, begin: int, end: int) -> torch.Tensor:
+        out = torch.empty(max(end - begin, 0), dtype=torch.uint64, device=self.ctx.device)
+        self.ctx._raise(self.ctx.lib.apo_history_window(self.h, int(begin), int(end), _ptr(out),
+                                                        _stream(self.ctx.device)))
+        return out
+
+
+_default: dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default:
+        _default[device] = Context(device)
+    return _default[device]
+
+
+def suffix_array(tok, lcp=True):
+    return default_context(tok.device.index or 0).suffix_array(tok, lcp)
+
+
+def suffix_array_batched(tok, off):
+    return default_context(tok.device.index or 0).suffix_array_batched(tok, off)
+
+
+def candidates(tok, min_len):
+    return default_context(tok.device.index or 0).candidates(tok, min_len)
+
+
+def find_repeats(win, min_len, min_count=1):
+    return default_context(win.device.index or 0).find_repeats(win, min_len, min_count)
+
+
+def find_repeats_batched(tok, off, min_len, min_count=1):
+    return default_context(tok.device.index or 0).find_repeats_batched(tok, off, min_len, min_count)

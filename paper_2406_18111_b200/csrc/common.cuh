@@ -1,0 +1,301 @@
+// common.cuh -- shared device/host plumbing of libapo (product path only).
+//
+// Context, workspace arena, error reporting, and the decoupled look-back
+// primitive used by the single-pass scans and the onesweep radix sort.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/apo.h"
+
+namespace apo {
+
+using u8 = uint8_t;
+using u32 = uint32_t;
+using u64 = uint64_t;
+using i32 = int32_t;
+using i64 = int64_t;
+
+constexpr int kNumCounterSlots = 4096;
+
+// --------------------------------------------------------------- errors --
+struct Error {
+  apo_status code;
+  std::string msg;
+};
+
+#define APO_CUDA(call)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw ::apo::Error{APO_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_) + \
+                                           " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"}; \
+  } while (0)
+
+#define APO_CHECK_LAUNCH() APO_CUDA(cudaGetLastError())
+
+inline void require(bool ok, const char *what) {
+  if (!ok) throw Error{APO_ERR_INVALID, what};
+}
+
+// ------------------------------------------------------------ workspace --
+// One device arena per context.  A call plans all its buffers, then carves
+// them from the arena (grown on demand).  Calls on one context are serialised
+// on the caller's stream, so the arena is reused call after call.
+struct Arena {
+  char *base = nullptr;
+  size_t cap = 0;
+  size_t used = 0;
+  void reserve(size_t bytes, cudaStream_t s) {
+    if (bytes <= cap) return;
+    if (base) {
+      APO_CUDA(cudaStreamSynchronize(s));
+      APO_CUDA(cudaFree(base));
+      base = nullptr;
+      cap = 0;
+    }
+    size_t want = bytes + bytes / 8 + (64u << 20);
+    cudaError_t e = cudaMalloc(&base, want);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error{APO_ERR_NOMEM, "device workspace allocation of " + std::to_string(want) +
+                                      " bytes failed: " + cudaGetErrorString(e)};
+    }
+    cap = want;
+  }
+  void release() {
+    if (base) cudaFree(base);
+    base = nullptr;
+    cap = 0;
+  }
+};
+
+// Bump allocator used in two passes: plan (base == nullptr, only sums sizes)
+// then carve (returns pointers).
+struct Carver {
+  char *base;
+  size_t off = 0;
+  explicit Carver(char *b) : base(b) {}
+  template <class T>
+  T *take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+    off += sizeof(T) * (count ? count : 1);
+    return p;
+  }
+};
+
+// Kernel classes timed by the optional in-library profiler (apo_profile).
+enum ProfKind { kProfRadixPass = 0, kProfRadixHist = 1, kProfScan = 2, kProfOther = 3, kProfKinds = 4 };
+
+struct ProfRec {
+  int kind;
+  double bytes;
+  cudaEvent_t a, b;
+};
+
+struct Ctx {
+  int device = 0;
+  int num_sms = 148;
+  std::string err;
+  Arena arena;  // per-call scratch
+  // persistent look-back state (zeroed once; epoch-tagged so never reset)
+  u64 *status = nullptr;
+  size_t status_words = 0;
+  u32 *counters = nullptr;  // tile counters, one slot per launch
+  u32 next_counter = 0;
+  u32 epoch = 0;
+  u32 *h_flag = nullptr;  // pinned host mailbox
+  u64 *d_misc = nullptr;  // small device scratch (flags, counts)
+  cudaEvent_t ev = nullptr;
+  int64_t launches = 0;  // kernel launches issued by the library (for bench)
+  // profiler: CUDA events around selected launches, on the launching stream
+  bool prof = false;
+  std::vector<ProfRec> prof_recs;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  cudaEvent_t prof_event();
+  void prof_begin(int kind, double bytes, cudaStream_t s);
+  void prof_end(cudaStream_t s);
+
+  void ensure_status(size_t words, cudaStream_t s);
+  u32 next_epoch() {
+    epoch = (epoch + 1) & 0x3FFFFFFFu;
+    if (epoch == 0) epoch = 1;
+    return epoch;
+  }
+  u32 *take_counter(cudaStream_t s);
+  u32 read_u32(const u32 *d_ptr, cudaStream_t s);
+  u64 read_u64(const u64 *d_ptr, cudaStream_t s);
+};
+
+// ------------------------------------------------- decoupled look-back --
+// Status word: [epoch:30][flag:2][value:32].  flag 1 = aggregate of the
+// tile only, 2 = inclusive prefix through the tile.  A word from another
+// launch (different epoch) reads as "not yet published".
+constexpr u32 kFlagAgg = 1, kFlagInc = 2;
+
+__device__ __forceinline__ u64 lb_pack(u32 epoch, u32 flag, u32 v) {
+  return (u64(epoch) << 34) | (u64(flag) << 32) | u64(v);
+}
+__device__ __forceinline__ void lb_store(u64 *p, u64 w) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ u64 lb_load(const u64 *p) {
+  u64 w;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+  return w;
+}
+
+// Sum (IS_MAX = false) or max (IS_MAX = true) of the published values of
+// tiles [0, tile) for one lane of the status array (stride = lanes per tile).
+template <bool IS_MAX>
+__device__ __forceinline__ u32 lb_lookback(const u64 *status, size_t stride, size_t lane,
+                                           i64 tile, u32 epoch) {
+  u32 acc = 0;
+  i64 p = tile - 1;
+  while (p >= 0) {
+    u64 w = lb_load(status + size_t(p) * stride + lane);
+    u32 ep = u32(w >> 34), fl = u32(w >> 32) & 3u;
+    if (ep != epoch || fl == 0) continue;  // spin until tile p publishes
+    u32 v = u32(w);
+    acc = IS_MAX ? (v > acc ? v : acc) : acc + v;
+    if (fl == kFlagInc) break;
+    --p;
+  }
+  return acc;
+}
+
+__host__ __device__ inline int bits_for(u64 v) {  // bits needed to store values in [0, v]
+  int b = 0;
+  while (b < 64 && (v >> b) != 0) ++b;
+  return b;
+}
+
+inline int grid_for(i64 n, int per_block, int cap = 1 << 30) {
+  i64 g = (n + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return int(g);
+}
+
+// ------------------------------------------------------ single-pass scan --
+// Generic block-tile scan over u32 values with decoupled look-back.
+//   F::load(i) -> u32  (i < n)
+//   F::store(i, inclusive, exclusive) -> bool  (true raises *F::flag())
+//   F::flag() -> u32* or nullptr
+// Op: sum (IS_MAX=false) or max (IS_MAX=true).  One launch, one pass over
+// the data, tiles claimed in order through an atomic counter.
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+template <bool IS_MAX>
+__device__ __forceinline__ u32 scan_op(u32 a, u32 b) {
+  return IS_MAX ? (a > b ? a : b) : a + b;
+}
+
+template <bool IS_MAX, class F>
+__global__ void __launch_bounds__(kScanThreads) k_scan(i64 n, F f, u64 *status, u32 *counter,
+                                                       u32 epoch) {
+  __shared__ u32 s_warp[kScanThreads / 32];
+  __shared__ u32 s_prefix;
+  __shared__ u32 s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+  __syncthreads();
+  const i64 tile = s_tile;
+  const i64 base = tile * kScanTile + i64(threadIdx.x) * kScanItems;
+  u32 v[kScanItems];
+  u32 local = 0;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    i64 i = base + j;
+    v[j] = i < n ? f.load(i) : 0u;
+    local = scan_op<IS_MAX>(local, v[j]);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  u32 incl = local;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    u32 o = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl = scan_op<IS_MAX>(incl, o);
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    u32 w = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
+    u32 wi = w;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      u32 o = __shfl_up_sync(0xffffffffu, wi, d);
+      if (lane >= d) wi = scan_op<IS_MAX>(wi, o);
+    }
+    u32 wex = __shfl_up_sync(0xffffffffu, wi, 1);
+    u32 tile_total = __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
+    if (lane < kScanThreads / 32) s_warp[lane] = lane ? wex : 0u;  // exclusive warp prefix
+    if (lane == 0) {
+      if (tile == 0) {
+        lb_store(status, lb_pack(epoch, kFlagInc, tile_total));
+        s_prefix = 0;
+      } else {
+        lb_store(status + tile, lb_pack(epoch, kFlagAgg, tile_total));
+        u32 pre = lb_lookback<IS_MAX>(status, 1, 0, tile, epoch);
+        lb_store(status + tile, lb_pack(epoch, kFlagInc, scan_op<IS_MAX>(pre, tile_total)));
+        s_prefix = pre;
+      }
+    }
+  }
+  __syncthreads();
+  // exclusive prefix of this thread
+  u32 warp_excl_in = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) warp_excl_in = 0;
+  u32 run = scan_op<IS_MAX>(scan_op<IS_MAX>(s_prefix, s_warp[warp]), warp_excl_in);
+  bool any = false;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    i64 i = base + j;
+    u32 nx = scan_op<IS_MAX>(run, v[j]);
+    if (i < n) any |= f.store(i, nx, run);
+    run = nx;
+  }
+  u32 *fl = f.flag();
+  if (fl != nullptr) {
+    if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(fl, 1u);
+  }
+}
+
+template <bool IS_MAX, class F>
+void launch_scan(Ctx &c, i64 n, const F &f, cudaStream_t s) {
+  if (n <= 0) return;
+  i64 tiles = (n + kScanTile - 1) / kScanTile;
+  c.ensure_status(size_t(tiles), s);
+  u32 *ctr = c.take_counter(s);
+  u32 ep = c.next_epoch();
+  if (c.prof) c.prof_begin(kProfScan, 0.0, s);
+  k_scan<IS_MAX, F><<<int(tiles), kScanThreads, 0, s>>>(n, f, c.status, ctr, ep);
+  APO_CHECK_LAUNCH();
+  if (c.prof) c.prof_end(s);
+  c.launches++;
+}
+
+// ----------------------------------------------------- radix sort (K1) --
+// LSD onesweep radix sort of (u64 key, V value) pairs (V = u32, u64, or
+// void for keys only) over key bits [begin_bit, end_bit).  Stable.  Returns
+// true iff the result ended in the *_alt buffers.
+bool radix_sort_u64_u32(Ctx &c, u64 *keys, u32 *vals, u64 *keys_alt, u32 *vals_alt, i64 n,
+                        int begin_bit, int end_bit, cudaStream_t s);
+bool radix_sort_u64_keys(Ctx &c, u64 *keys, u64 *keys_alt, i64 n, int begin_bit, int end_bit,
+                         cudaStream_t s);
+bool radix_sort_u32_u64(Ctx &c, u32 *keys, u64 *vals, u32 *keys_alt, u64 *vals_alt, i64 n,
+                        int begin_bit, int end_bit, cudaStream_t s);
+size_t radix_status_words(i64 n);
+
+}  // namespace apo
+
+struct apo_ctx {
+  apo::Ctx c;
+};

@@ -1,0 +1,72 @@
+// pipeline.cuh -- stages of FindRepeats on the device (product path).
+#pragma once
+
+#include "common.cuh"
+
+namespace apo {
+
+// A CSR batch of independent windows laid out back to back in one token
+// array (a single window is W == 1).  Positions are global in [0, N).
+struct Batch {
+  i64 N = 0;
+  int W = 1;
+  i64 maxwin = 0;            // longest window
+  const i64 *off = nullptr;  // device int64[W+1] (nullptr when W == 1)
+  const i32 *wid = nullptr;  // device int32[N] window of each position (nullptr when W == 1)
+};
+
+__device__ __forceinline__ int b_wid(const Batch &b, i64 i) { return b.W == 1 ? 0 : b.wid[i]; }
+__device__ __forceinline__ i64 b_beg(const Batch &b, int w) { return b.W == 1 ? 0 : b.off[w]; }
+__device__ __forceinline__ i64 b_end(const Batch &b, int w) { return b.W == 1 ? b.N : b.off[w + 1]; }
+
+// ----- suffix array + LCP (K2 initial ranking, K3 doubling, K4 PLCP) -----
+struct SAWork {
+  u64 *keys, *keys_alt;   // N
+  u32 *vals, *vals_alt;   // N
+  u64 *tok_sorted;        // N (batched initial ranking)
+  i32 *levels[40];        // rank levels 0..R (each N)
+  int max_levels;
+  i32 *phi, *plcp;        // N
+  // results
+  i32 *sa;                // N (global positions, window-major suffix order)
+  i32 *lcp;               // N (pair k = (k, k+1); 0 at the end of each window)
+  int R;                  // final level index (ranks all distinct)
+};
+
+void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp);
+void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s);
+
+// ----- candidate generation, ordering, greedy, output (K5-K8) -----
+struct SelWork {
+  u32 *k1, *k1_alt;       // 2N sort-1 keys (window, length desc)
+  u64 *v1, *v1_alt;       // 2N sort-1 values (pair rank << 32 | start)
+  u64 *k2, *k2_alt;       // 2N sort-2 keys (group, start)
+  i32 *rmq[32];           // sparse table over LCP, levels 1..J (level 0 = lcp)
+  int rmq_levels;
+  i32 *glen;              // 2N per-group length
+  i32 *cl, *cs, *cg;      // 2N per candidate (final order): length, start (global), group
+  u8 *state;              // 2N 0 undecided, 1 kept, 2 rejected
+  u32 *tab[32];           // greedy first-cover table levels (N each)
+  int tab_levels;
+  u32 *diff;              // N+1 coverage difference array
+  u32 *cov;               // N+1 coverage
+  u32 *gcnt, *gfirst;     // 2N per group
+  u32 *oidx;              // 2N occurrence index per candidate
+  u32 *wcnt;              // W+1 repeats per window
+  u64 *scal;              // small device scalars
+  i64 m = 0, G = 0;       // host copies of candidate / group counts
+};
+
+void plan_select(Carver &cv, const Batch &b, SelWork &w);
+// Runs K5..K7 (candidates, ordering, greedy).  After return, w.m and w.G are
+// valid and w.cl/cs/cg/state hold the candidates in the paper's order.
+void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa, int min_len,
+                       SelWork &w, cudaStream_t s);
+// K8: dedup + output.
+void emit_repeats(Ctx &c, const Batch &b, SelWork &w, int min_count, apo_repeat *out, i64 cap,
+                  i64 *out_off, i32 *occ, i64 occ_cap, i64 *counts, cudaStream_t s);
+// Parity view of the candidate list (single window).
+void emit_candidates(Ctx &c, const Batch &b, const SelWork &w, i32 *len, i32 *id, i32 *start, u8 *kept,
+                     i64 cap, i64 *count, cudaStream_t s);
+
+}  // namespace apo

@@ -1,0 +1,446 @@
+// select.cu -- K5..K8: Alg. 2 after the suffix array.
+//
+// K5 candidate generation.  For every rank-adjacent pair k of a
+//    window: s1, s2, p = SA[k], SA[k+1], LCP[k]; disjoint (|s2-s1| >= p,
+//    reading R4) -> (p, s1), (p, s2); otherwise d = |s2-s1|,
+//    l = floor((p+d)/2), l -= l % d -> (l, m), (l, m+l) with m = min(s1,s2)
+//    (R5, R6).  Kept iff l >= min_len (R7).  Compacted with a single-pass
+//    scan; emitted in pair order.
+// K6 ordering.  The paper sorts by (length desc,
+//    sub-string asc, start asc).  For equal length, the sub-string of pair k
+//    is the l-prefix of the suffix of rank k, so sub-string order is rank
+//    order: a STABLE radix sort of the pair-ordered candidates by
+//    (window, length desc) already yields sub-string order.  Two neighbours
+//    of pairs k1 <= k2 are the same sub-string iff k1 == k2 or
+//    min LCP[k1..k2-1] >= l (O(1) range-minimum over a sparse table).  The
+//    dense group ordinal is the paper's sub-string ID; a second radix sort by
+//    (ID, start) puts each group in start order.
+// K7 greedy non-overlap selection computed EXACTLY in rounds
+//    (lexicographically-first independent set): with priority = position in
+//    the sorted order, an undecided candidate is selected when no undecided
+//    candidate of higher priority covers its first or last position (any
+//    earlier -- hence not shorter -- overlapping interval must cover one of
+//    them), and rejected once a selected interval covers its first or last
+//    position (the paper's marked-array test).  firstcov(x) comes
+//    from a reverse sparse table (two atomicMin per interval, then a pull-down
+//    over levels); coverage from a +/-1 difference array and a scan.
+// K8 dedup/output (R10, R11).
+#include "pipeline.cuh"
+
+namespace apo {
+
+namespace {
+
+constexpr int T = 256;
+
+struct CandF {
+  Batch b;
+  const i32 *sa;
+  const i32 *lcp;
+  i32 min_len;
+  int bl;
+  i64 maxl;
+  i64 npairs;
+  u32 *k1;
+  u64 *v1;
+  i64 *m_out;
+  __device__ __forceinline__ bool pair(i64 k, i64 &l, i64 &a, i64 &bb, int &w) const {
+    i64 s1 = sa[k];
+    w = b_wid(b, s1);
+    if (k + 1 >= b_end(b, w)) return false;
+    i64 s2 = sa[k + 1];
+    i64 p = lcp[k];
+    i64 lo = s1 < s2 ? s1 : s2, d = s1 < s2 ? s2 - s1 : s1 - s2;
+    if (d >= p) {
+      l = p;
+      a = s1;
+      bb = s2;
+    } else {
+      i64 L = (p + d) / 2;
+      L -= L % d;
+      l = L;
+      a = lo;
+      bb = lo + L;
+    }
+    return l >= min_len;
+  }
+  __device__ u32 load(i64 k) const {
+    i64 l, a, bb;
+    int w;
+    return pair(k, l, a, bb, w) ? 1u : 0u;
+  }
+  __device__ bool store(i64 k, u32 incl, u32 excl) const {
+    i64 l, a, bb;
+    int w;
+    if (pair(k, l, a, bb, w)) {
+      u32 key = (u32(w) << bl) | u32(maxl - l);
+      i64 o = 2 * i64(excl);
+      k1[o] = key;
+      k1[o + 1] = key;
+      v1[o] = (u64(k) << 32) | u64(a);
+      v1[o + 1] = (u64(k) << 32) | u64(bb);
+    }
+    if (k == npairs - 1) *m_out = 2 * i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+struct Rmq {
+  const i32 *lv[32];
+  __device__ __forceinline__ i32 min(i64 a, i64 b) const {  // inclusive, a <= b
+    i64 len = b - a + 1;
+    int j = 63 - __clzll(len);
+    i32 x = lv[j][a], y = lv[j][b - (i64(1) << j) + 1];
+    return x < y ? x : y;
+  }
+};
+
+__global__ void k_rmq_level(const i32 *__restrict__ prev, i32 *__restrict__ next, i64 n, i64 half) {
+  i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  i32 x = prev[k];
+  if (k + half < n) {
+    i32 y = prev[k + half];
+    x = y < x ? y : x;
+  }
+  next[k] = x;
+}
+
+struct HeadF {
+  const u32 *k1;
+  const u64 *v1;
+  Rmq rmq;
+  i64 maxl;
+  u32 lmask;
+  int bN;
+  i64 m;
+  u64 *k2;
+  i32 *glen;
+  i64 *G_out;
+  __device__ u32 load(i64 c) const {
+    if (c == 0) return 1;
+    if (k1[c] != k1[c - 1]) return 1;
+    i64 kc = i64(v1[c] >> 32), kp = i64(v1[c - 1] >> 32);
+    if (kc == kp) return 0;
+    i64 l = maxl - i64(k1[c] & lmask);
+    return rmq.min(kp, kc - 1) < l ? 1u : 0u;
+  }
+  __device__ bool store(i64 c, u32 incl, u32 excl) const {
+    u64 g = u64(incl - 1);
+    u64 s = v1[c] & 0xffffffffull;
+    k2[c] = (g << bN) | s;
+    if (incl != excl) glen[g] = i32(maxl - i64(k1[c] & lmask));
+    if (c == m - 1) *G_out = i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+__global__ void k_unpack(const u64 *__restrict__ k2, i64 m, int bN, const i32 *__restrict__ glen,
+                         i32 *__restrict__ cl, i32 *__restrict__ cs, i32 *__restrict__ cg, u8 *__restrict__ state) {
+  i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  u64 key = k2[c];
+  i32 g = i32(key >> bN);
+  cs[c] = i32(key & ((1ull << bN) - 1));
+  cg[c] = g;
+  cl[c] = glen[g];
+  state[c] = 0;
+}
+
+struct Tab {
+  u32 *lv[32];
+};
+
+__global__ void k_mark(const i32 *__restrict__ cl, const i32 *__restrict__ cs, const u8 *__restrict__ state, i64 m,
+                       Tab tab) {
+  i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= m || state[c] != 0) return;
+  i64 l = cl[c], s = cs[c];
+  int q = 63 - __clzll(l);
+  u32 *t = tab.lv[q];
+  atomicMin(&t[s], u32(c));
+  atomicMin(&t[s + l - (i64(1) << q)], u32(c));
+}
+
+__global__ void k_pull(const u32 *__restrict__ up, u32 *__restrict__ down, i64 n, i64 half) {
+  i64 y = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (y >= n) return;
+  u32 v = up[y];
+  if (y >= half) {
+    u32 o = up[y - half];
+    v = o < v ? o : v;
+  }
+  if (v < down[y]) down[y] = v;
+}
+
+__global__ void k_select(const i32 *__restrict__ cl, const i32 *__restrict__ cs, u8 *__restrict__ state, i64 m,
+                         const u32 *__restrict__ first, u32 *__restrict__ diff) {
+  i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= m || state[c] != 0) return;
+  i64 l = cl[c], s = cs[c];
+  if (first[s] == u32(c) && first[s + l - 1] == u32(c)) {
+    state[c] = 1;
+    atomicAdd(&diff[s], 1u);
+    atomicAdd(&diff[s + l], 0xffffffffu);
+  }
+}
+
+struct CovF {
+  const u32 *diff;
+  u32 *cov;
+  __device__ u32 load(i64 i) const { return diff[i]; }
+  __device__ bool store(i64 i, u32 incl, u32) const {
+    cov[i] = incl;
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+__global__ void k_reject(const i32 *__restrict__ cl, const i32 *__restrict__ cs, u8 *__restrict__ state, i64 m,
+                         const u32 *__restrict__ cov, u32 *__restrict__ undecided) {
+  i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool und = false;
+  if (c < m && state[c] == 0) {
+    i64 l = cl[c], s = cs[c];
+    if (cov[s] != 0 || cov[s + l - 1] != 0)
+      state[c] = 2;
+    else
+      und = true;
+  }
+  if (__syncthreads_or(und) && threadIdx.x == 0) atomicOr(undecided, 1u);
+}
+
+__global__ void k_gstats(const i32 *__restrict__ cg, const u8 *__restrict__ state, i64 m, u32 *__restrict__ gcnt,
+                         u32 *__restrict__ gfirst) {
+  i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= m || state[c] != 1) return;
+  i32 g = cg[c];
+  atomicAdd(&gcnt[g], 1u);
+  atomicMin(&gfirst[g], u32(c));
+}
+
+struct OccF {
+  Batch b;
+  const i32 *cg, *cs;
+  const u8 *state;
+  const u32 *gcnt;
+  u32 minc;
+  u32 *oidx;
+  i32 *occ;
+  i64 occ_cap;
+  i64 m;
+  i64 *total;
+  __device__ u32 load(i64 c) const { return (state[c] == 1 && gcnt[cg[c]] >= minc) ? 1u : 0u; }
+  __device__ bool store(i64 c, u32 incl, u32 excl) const {
+    if (incl != excl) {
+      oidx[c] = excl;
+      if (occ != nullptr && i64(excl) < occ_cap) {
+        i64 s = cs[c];
+        occ[excl] = i32(s - b_beg(b, b_wid(b, s)));
+      }
+    }
+    if (c == m - 1) *total = i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+struct RepF {
+  Batch b;
+  const u32 *gcnt, *gfirst, *oidx;
+  const i32 *glen, *cs;
+  u32 minc;
+  apo_repeat *out;
+  i64 cap;
+  u32 *wcnt;
+  i64 G;
+  i64 *total;
+  __device__ u32 load(i64 g) const { return gcnt[g] >= minc ? 1u : 0u; }
+  __device__ bool store(i64 g, u32 incl, u32 excl) const {
+    if (incl != excl) {
+      u32 c0 = gfirst[g];
+      i64 s = cs[c0];
+      int w = b_wid(b, s);
+      if (i64(excl) < cap && out != nullptr) {
+        apo_repeat r;
+        r.start = i32(s - b_beg(b, w));
+        r.length = glen[g];
+        r.count = i32(gcnt[g]);
+        r.first_occ = i32(oidx[c0]);
+        out[excl] = r;
+      }
+      atomicAdd(&wcnt[w], 1u);
+    }
+    if (g == G - 1) *total = i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+struct OffF {
+  const u32 *wcnt;
+  i64 *out_off;
+  __device__ u32 load(i64 w) const { return wcnt[w]; }
+  __device__ bool store(i64 w, u32, u32 excl) const {
+    out_off[w] = i64(excl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+__global__ void k_emit_cands(Batch b, const i32 *__restrict__ cl, const i32 *__restrict__ cs,
+                             const i32 *__restrict__ cg, const u8 *__restrict__ state, i64 m, i64 cap,
+                             i32 *len, i32 *id, i32 *start, u8 *kept) {
+  i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= m || c >= cap) return;
+  i64 s = cs[c];
+  if (len) len[c] = cl[c];
+  if (id) id[c] = cg[c];
+  if (start) start[c] = i32(s - b_beg(b, b_wid(b, s)));
+  if (kept) kept[c] = state[c] == 1 ? 1 : 0;
+}
+
+}  // namespace
+
+void plan_select(Carver &cv, const Batch &b, SelWork &w) {
+  const i64 N = b.N, M = N > 1 ? 2 * (N - 1) : 1;
+  w.k1 = cv.take<u32>(M);
+  w.k1_alt = cv.take<u32>(M);
+  w.v1 = cv.take<u64>(M);
+  w.v1_alt = cv.take<u64>(M);
+  w.k2 = cv.take<u64>(M);
+  w.k2_alt = cv.take<u64>(M);
+  // sparse table over LCP: queries span < maxwin entries
+  w.rmq_levels = bits_for(u64(b.maxwin > 1 ? b.maxwin : 1));
+  if (w.rmq_levels > 31) w.rmq_levels = 31;
+  for (int j = 1; j < w.rmq_levels; ++j) w.rmq[j] = cv.take<i32>(N);
+  w.glen = cv.take<i32>(M);
+  w.cl = cv.take<i32>(M);
+  w.cs = cv.take<i32>(M);
+  w.cg = cv.take<i32>(M);
+  w.state = cv.take<u8>(M);
+  const i64 maxl = b.maxwin / 2;
+  w.tab_levels = maxl >= 1 ? bits_for(u64(maxl)) : 1;
+  for (int q = 0; q < w.tab_levels; ++q) w.tab[q] = cv.take<u32>(N);
+  w.diff = cv.take<u32>(N + 1);
+  w.cov = cv.take<u32>(N + 1);
+  w.gcnt = cv.take<u32>(M);
+  w.gfirst = cv.take<u32>(M);
+  w.oidx = cv.take<u32>(M);
+  w.wcnt = cv.take<u32>(size_t(b.W) + 1);
+  w.scal = cv.take<u64>(16);
+}
+
+void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa, int min_len, SelWork &w,
+                       cudaStream_t s) {
+  (void)tok;
+  const i64 N = b.N;
+  w.m = 0;
+  w.G = 0;
+  if (N < 2) return;
+  const i64 maxl = b.maxwin / 2;
+  const int bl = bits_for(u64(maxl));
+  const int bw = bits_for(u64(b.W - 1));
+  if (bl + bw > 32) throw Error{APO_ERR_INVALID, "batch too wide for 32-bit candidate keys"};
+  i64 *m_dev = reinterpret_cast<i64 *>(w.scal);
+  i64 *G_dev = reinterpret_cast<i64 *>(w.scal + 1);
+  u32 *undecided = reinterpret_cast<u32 *>(w.scal + 2);
+  APO_CUDA(cudaMemsetAsync(w.scal, 0, sizeof(u64) * 16, s));
+
+  // ---- K5 ----
+  {
+    CandF f{b, sa.sa, sa.lcp, min_len, bl, maxl, N - 1, w.k1, w.v1, m_dev};
+    launch_scan<false>(c, N - 1, f, s);
+  }
+  const i64 m = i64(c.read_u64(reinterpret_cast<u64 *>(m_dev), s));
+  w.m = m;
+  if (m == 0) return;
+
+  // ---- K6: sort by (window, length desc), stable in pair order ----
+  bool a = radix_sort_u32_u64(c, w.k1, w.v1, w.k1_alt, w.v1_alt, m, 0, bl + bw, s);
+  const u32 *k1 = a ? w.k1_alt : w.k1;
+  const u64 *v1 = a ? w.v1_alt : w.v1;
+  Rmq rmq{};
+  rmq.lv[0] = sa.lcp;
+  for (int j = 1; j < w.rmq_levels; ++j) {
+    k_rmq_level<<<grid_for(N, T), T, 0, s>>>(rmq.lv[j - 1], w.rmq[j], N, i64(1) << (j - 1));
+    APO_CHECK_LAUNCH();
+    c.launches++;
+    rmq.lv[j] = w.rmq[j];
+  }
+  const int bN = bits_for(u64(N - 1));
+  {
+    HeadF f{k1, v1, rmq, maxl, (1u << bl) - 1u, bN, m, w.k2, w.glen, G_dev};
+    launch_scan<false>(c, m, f, s);
+  }
+  const i64 G = i64(c.read_u64(reinterpret_cast<u64 *>(G_dev), s));
+  w.G = G;
+  bool a2 = radix_sort_u64_keys(c, w.k2, w.k2_alt, m, 0, bN + bits_for(u64(G - 1)), s);
+  const u64 *k2 = a2 ? w.k2_alt : w.k2;
+  k_unpack<<<grid_for(m, T), T, 0, s>>>(k2, m, bN, w.glen, w.cl, w.cs, w.cg, w.state);
+  APO_CHECK_LAUNCH();
+  c.launches++;
+
+  // ---- K7: exact round-parallel greedy ----
+  APO_CUDA(cudaMemsetAsync(w.diff, 0, sizeof(u32) * (N + 1), s));
+  Tab tab{};
+  for (int q = 0; q < w.tab_levels; ++q) tab.lv[q] = w.tab[q];
+  const int gm = grid_for(m, T), gn = grid_for(N, T);
+  for (int round = 0;; ++round) {
+    if (round > 100000) throw Error{APO_ERR_CUDA, "greedy selection did not converge"};
+    for (int q = 0; q < w.tab_levels; ++q) APO_CUDA(cudaMemsetAsync(w.tab[q], 0xff, sizeof(u32) * N, s));
+    k_mark<<<gm, T, 0, s>>>(w.cl, w.cs, w.state, m, tab);
+    APO_CHECK_LAUNCH();
+    for (int q = w.tab_levels - 1; q >= 1; --q) {
+      k_pull<<<gn, T, 0, s>>>(w.tab[q], w.tab[q - 1], N, i64(1) << (q - 1));
+      APO_CHECK_LAUNCH();
+    }
+    k_select<<<gm, T, 0, s>>>(w.cl, w.cs, w.state, m, w.tab[0], w.diff);
+    APO_CHECK_LAUNCH();
+    CovF cf{w.diff, w.cov};
+    launch_scan<false>(c, N, cf, s);
+    APO_CUDA(cudaMemsetAsync(undecided, 0, sizeof(u32), s));
+    k_reject<<<gm, T, 0, s>>>(w.cl, w.cs, w.state, m, w.cov, undecided);
+    APO_CHECK_LAUNCH();
+    c.launches += 3 + (w.tab_levels - 1);
+    if (c.read_u32(undecided, s) == 0) break;
+  }
+}
+
+void emit_repeats(Ctx &c, const Batch &b, SelWork &w, int min_count, apo_repeat *out, i64 cap, i64 *out_off,
+                  i32 *occ, i64 occ_cap, i64 *counts, cudaStream_t s) {
+  const i64 m = w.m, G = w.G;
+  APO_CUDA(cudaMemsetAsync(counts, 0, sizeof(i64) * 2, s));
+  APO_CUDA(cudaMemsetAsync(w.wcnt, 0, sizeof(u32) * (b.W + 1), s));
+  if (m > 0) {
+    APO_CUDA(cudaMemsetAsync(w.gcnt, 0, sizeof(u32) * G, s));
+    APO_CUDA(cudaMemsetAsync(w.gfirst, 0xff, sizeof(u32) * G, s));
+    k_gstats<<<grid_for(m, T), T, 0, s>>>(w.cg, w.state, m, w.gcnt, w.gfirst);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+    const u32 minc = u32(min_count < 1 ? 1 : min_count);
+    OccF of{b, w.cg, w.cs, w.state, w.gcnt, minc, w.oidx, occ, occ_cap, m, counts + 1};
+    launch_scan<false>(c, m, of, s);
+    RepF rf{b, w.gcnt, w.gfirst, w.oidx, w.glen, w.cs, minc, out, cap, w.wcnt, G, counts};
+    launch_scan<false>(c, G, rf, s);
+  }
+  if (out_off != nullptr) {
+    OffF f{w.wcnt, out_off};
+    launch_scan<false>(c, i64(b.W) + 1, f, s);
+  }
+}
+
+void emit_candidates(Ctx &c, const Batch &b, const SelWork &w, i32 *len, i32 *id, i32 *start, u8 *kept, i64 cap,
+                     i64 *count, cudaStream_t s) {
+  APO_CUDA(cudaMemcpyAsync(count, &w.m, sizeof(i64), cudaMemcpyHostToDevice, s));
+  if (w.m > 0) {
+    k_emit_cands<<<grid_for(w.m, T), T, 0, s>>>(b, w.cl, w.cs, w.cg, w.state, w.m, cap, len, id, start, kept);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+  }
+  APO_CUDA(cudaStreamSynchronize(s));  // w.m is a host value copied asynchronously
+}
+
+}  // namespace apo

@@ -1,0 +1,259 @@
+// suffix_array.cu -- K2/K3/K4: suffix array by prefix doubling and the LCP
+// array by the phi/PLCP (Kasai-style) method, for a batch of windows.
+//
+// "SA, LCP <- SuffixArray(S)" (Alg. 2); "Linear time
+// algorithms exist for suffix array and LCP array construction".
+//
+// SA (prefix doubling, Manber-Myers style, all windows at once):
+//   level 0   rank[i] = group start of token S[i] in (window, token) order
+//   level r   rank_r[i] orders suffixes by their first 2^r tokens (padded
+//             with an end marker that sorts first, reading R2)
+//   round h   key(i) = rank[i] << lob | (i+h < end(window) ? rank[i+h]-beg+1 : 0)
+//             LSD radix sort of (key, i); a sorted position k starts a new
+//             group iff key[k] != key[k-1]; new rank = max-scan of group
+//             starts, scattered to rank_next[sa[k]].  Stop when all distinct.
+// Keys are built in POSITION order (coalesced reads of rank[i], rank[i+h]),
+// so no gather through SA is needed; every level is kept for the LCP stage.
+//
+// LCP: phi[sa[k]] = sa[k-1]; PLCP[i] = lcp(i, phi[i]) computed in chunks of
+// consecutive i per thread with the Kasai bound PLCP[i] >= PLCP[i-1]-1; each
+// chunk's first value is found in O(log n) by galloping over the saved rank
+// levels (equal level-r ranks <=> equal 2^r-token prefixes); LCP[k] =
+// PLCP[sa[k+1]].
+#include "pipeline.cuh"
+
+namespace apo {
+
+namespace {
+
+__global__ void k_init_pairs(const u64 *__restrict__ tok, i64 n, u64 *__restrict__ keys,
+                             u32 *__restrict__ vals) {
+  i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) {
+    keys[i] = tok[i];
+    vals[i] = u32(i);
+  }
+}
+
+// batched: sort key = window id of the position (stable over (token, i) order)
+__global__ void k_wid_keys(const u32 *__restrict__ idx, const i32 *__restrict__ wid, i64 n,
+                           u64 *__restrict__ keys) {
+  i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) keys[k] = u64(u32(wid[idx[k]]));
+}
+
+__global__ void k_gather_tok(const u32 *__restrict__ idx, const u64 *__restrict__ tok, i64 n,
+                             u64 *__restrict__ out) {
+  i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < n) out[k] = tok[idx[k]];
+}
+
+// Level-0 ranks: head of a (window, token) group -> group start, max-scanned.
+struct InitRankF {
+  const u64 *tok_sorted;  // tokens in sorted order
+  const u32 *sa;
+  const i32 *wid;         // nullptr if single window
+  i32 *rank;
+  __device__ u32 load(i64 k) const {
+    if (k == 0) return 0;
+    bool head = tok_sorted[k] != tok_sorted[k - 1];
+    if (wid && !head) head = wid[sa[k]] != wid[sa[k - 1]];
+    return head ? u32(k) : 0u;
+  }
+  __device__ bool store(i64 k, u32 incl, u32) const {
+    rank[sa[k]] = i32(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+__global__ void k_double_keys(const i32 *__restrict__ rank, Batch b, i64 h, int lob, u64 *__restrict__ keys,
+                              u32 *__restrict__ vals) {
+  i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= b.N) return;
+  int w = b_wid(b, i);
+  i64 beg = b_beg(b, w), end = b_end(b, w);
+  u64 lo = (i + h < end) ? u64(rank[i + h] - beg + 1) : 0ull;
+  keys[i] = (u64(u32(rank[i])) << lob) | lo;
+  vals[i] = u32(i);
+}
+
+// Next rank level from the sorted keys; flags "not done" if any group has
+// more than one member.
+struct DoubleRankF {
+  const u64 *key;
+  const u32 *sa;
+  i32 *rank_next;
+  u32 *notdone;
+  __device__ u32 load(i64 k) const { return (k == 0 || key[k] != key[k - 1]) ? u32(k) : 0u; }
+  __device__ bool store(i64 k, u32 incl, u32) const {
+    rank_next[sa[k]] = i32(incl);
+    return incl != u32(k);
+  }
+  __device__ u32 *flag() const { return notdone; }
+};
+
+__global__ void k_phi(const u32 *__restrict__ sa, Batch b, i32 *__restrict__ phi) {
+  i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= b.N) return;
+  i64 i = sa[k];
+  int w = b_wid(b, i);
+  phi[i] = (k == b_beg(b, w)) ? -1 : i32(sa[k - 1]);
+}
+
+struct Levels {
+  const i32 *p[40];
+};
+
+// lcp(i, j) (same window, both < end) by galloping over rank levels R-1..0.
+__device__ __forceinline__ i64 gallop_lcp(const Levels &L, int R, i64 i, i64 j, i64 end) {
+  i64 l = 0;
+  for (int r = R - 1; r >= 0; --r) {
+    if (i + l >= end || j + l >= end) break;
+    const i32 *lv = L.p[r];
+    if (lv[i + l] == lv[j + l]) l += (i64(1) << r);
+  }
+  return l;
+}
+
+constexpr int kPlcpChunk = 32;
+
+__global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi, Levels L, int R, Batch b,
+                       i32 *__restrict__ plcp) {
+  i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  i64 i0 = t * kPlcpChunk;
+  if (i0 >= b.N) return;
+  i64 i1 = i0 + kPlcpChunk < b.N ? i0 + kPlcpChunk : b.N;
+  i64 h = -1;  // -1: no Kasai lower bound available
+  int cur_w = -1;
+  i64 end = 0;
+  for (i64 i = i0; i < i1; ++i) {
+    int w = b_wid(b, i);
+    if (w != cur_w) {
+      cur_w = w;
+      end = b_end(b, w);
+      h = -1;
+    }
+    i64 j = phi[i];
+    if (j < 0) {
+      plcp[i] = 0;
+      h = 0;
+      continue;
+    }
+    if (h < 0) {
+      h = gallop_lcp(L, R, i, j, end);
+    } else {
+      h = h > 0 ? h - 1 : 0;
+      while (i + h < end && j + h < end && tok[i + h] == tok[j + h]) ++h;
+    }
+    plcp[i] = i32(h);
+  }
+}
+
+__global__ void k_lcp_gather(const u32 *__restrict__ sa, const i32 *__restrict__ plcp, Batch b,
+                             i32 *__restrict__ lcp) {
+  i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= b.N) return;
+  int w = b_wid(b, sa[k]);
+  lcp[k] = (k + 1 < b_end(b, w)) ? plcp[sa[k + 1]] : 0;
+}
+
+}  // namespace
+
+void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp) {
+  const i64 N = b.N;
+  w.keys = cv.take<u64>(N);
+  w.keys_alt = cv.take<u64>(N);
+  w.vals = cv.take<u32>(N);
+  w.vals_alt = cv.take<u32>(N);
+  w.tok_sorted = b.W > 1 ? cv.take<u64>(N) : nullptr;
+  w.max_levels = bits_for(u64(b.maxwin > 1 ? b.maxwin - 1 : 1)) + 2;
+  if (w.max_levels > 40) w.max_levels = 40;
+  for (int r = 0; r < w.max_levels; ++r) w.levels[r] = cv.take<i32>(N);
+  w.sa = cv.take<i32>(N);
+  if (want_lcp) {
+    w.phi = cv.take<i32>(N);
+    w.plcp = cv.take<i32>(N);
+    w.lcp = cv.take<i32>(N);
+  } else {
+    w.phi = w.plcp = w.lcp = nullptr;
+  }
+}
+
+void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s) {
+  const i64 N = b.N;
+  const int T = 256;
+  const int G = grid_for(N, T);
+  w.R = 0;
+  if (N == 0) return;
+
+  // ---- K2: level-0 ranks (group start in (window, token) order) ----
+  k_init_pairs<<<G, T, 0, s>>>(tok, N, w.keys, w.vals);
+  APO_CHECK_LAUNCH();
+  c.launches++;
+  bool alt = radix_sort_u64_u32(c, w.keys, w.vals, w.keys_alt, w.vals_alt, N, 0, 64, s);
+  u64 *sk = alt ? w.keys_alt : w.keys;
+  u32 *sv = alt ? w.vals_alt : w.vals;
+  u64 *ok = alt ? w.keys : w.keys_alt;
+  u32 *ov = alt ? w.vals : w.vals_alt;
+  const u64 *tok_sorted = sk;
+  if (b.W > 1) {
+    k_wid_keys<<<G, T, 0, s>>>(sv, b.wid, N, ok);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+    // copy values so the (key, value) pair lives in (ok, ov)
+    APO_CUDA(cudaMemcpyAsync(ov, sv, sizeof(u32) * N, cudaMemcpyDeviceToDevice, s));
+    bool a2 = radix_sort_u64_u32(c, ok, ov, sk, sv, N, 0, bits_for(u64(b.W - 1)), s);
+    u32 *idx = a2 ? sv : ov;
+    k_gather_tok<<<G, T, 0, s>>>(idx, tok, N, w.tok_sorted);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+    tok_sorted = w.tok_sorted;
+    sv = idx;
+  }
+  {
+    InitRankF f{tok_sorted, sv, b.W > 1 ? b.wid : nullptr, w.levels[0]};
+    launch_scan<true>(c, N, f, s);
+  }
+
+  // ---- K3: doubling rounds ----
+  const int lob = bits_for(u64(b.maxwin));
+  const int hib = bits_for(u64(N - 1));
+  u32 *notdone = reinterpret_cast<u32 *>(c.d_misc);
+  const u32 *final_sa = sv;
+  int r = 0;
+  for (i64 h = 1;; h <<= 1) {
+    if (r + 1 >= w.max_levels) throw Error{APO_ERR_INVALID, "prefix doubling exceeded its level budget"};
+    APO_CUDA(cudaMemsetAsync(notdone, 0, sizeof(u32), s));
+    k_double_keys<<<G, T, 0, s>>>(w.levels[r], b, h, lob, w.keys, w.vals);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+    bool a = radix_sort_u64_u32(c, w.keys, w.vals, w.keys_alt, w.vals_alt, N, 0, hib + lob, s);
+    const u64 *key = a ? w.keys_alt : w.keys;
+    const u32 *sa = a ? w.vals_alt : w.vals;
+    DoubleRankF f{key, sa, w.levels[r + 1], notdone};
+    launch_scan<true>(c, N, f, s);
+    ++r;
+    final_sa = sa;
+    if (c.read_u32(notdone, s) == 0) break;
+    if (h > b.maxwin) throw Error{APO_ERR_CUDA, "prefix doubling did not converge"};
+  }
+  w.R = r;
+  APO_CUDA(cudaMemcpyAsync(w.sa, final_sa, sizeof(i32) * N, cudaMemcpyDeviceToDevice, s));
+
+  if (!want_lcp) return;
+  // ---- K4: phi, PLCP, LCP ----
+  const u32 *sa = reinterpret_cast<const u32 *>(w.sa);
+  k_phi<<<G, T, 0, s>>>(sa, b, w.phi);
+  APO_CHECK_LAUNCH();
+  Levels L{};
+  for (int q = 0; q <= w.R && q < 40; ++q) L.p[q] = w.levels[q];
+  i64 chunks = (N + kPlcpChunk - 1) / kPlcpChunk;
+  k_plcp<<<grid_for(chunks, 128), 128, 0, s>>>(tok, w.phi, L, w.R, b, w.plcp);
+  APO_CHECK_LAUNCH();
+  k_lcp_gather<<<G, T, 0, s>>>(sa, w.plcp, b, w.lcp);
+  APO_CHECK_LAUNCH();
+  c.launches += 3;
+}
+
+}  // namespace apo

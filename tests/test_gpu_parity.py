@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element
+by element, on seeded synthetic inputs.  Everything is integer, so the bar is
+bit-exact equality.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2406_18111_b200 import build
+    build.build()
+    from paper_2406_18111_b200 import Context
+    return Context(0)
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint64)).cuda()
+
+
+def small_cases():
+    cases = [gen.from_text("aabcbcbaa"), gen.from_text("ababab"), gen.from_text("aaaaaaa"),
+             gen.from_text("abababa"), np.array([5], np.uint64), np.array([5, 5], np.uint64),
+             np.array([1 << 63, 0, 1 << 63, 0], np.uint64), np.full(300, 7, np.uint64)]
+    for seed in range(12):
+        cases.append(gen.random_string(seed, 1 + (seed * 97) % 700, 1 + seed % 6))
+    for seed in range(4):
+        cases.append(gen.high_bit_string(seed, 500, 6))
+    cases.append(gen.periodic(3, 5000, 37, 4, noise=0.01))
+    cases.append(gen.fibonacci_word(3000))
+    cases.append(gen.c1())
+    return cases
+
+
+def multi_tile_cases():
+    # several 4,096-key sort tiles plus a ragged tail
+    return [gen.random_string(77, 9000, 3), gen.periodic(5, 13001, 64, 3, noise=0.02),
+            gen.c2()[:20000], gen.c3()[:17000]]
+
+
+@pytest.mark.parametrize("case", range(len(small_cases())))
+def test_sa_lcp_small(ctx, case):
+    S = small_cases()[case]
+    sa, lcp = ctx.suffix_array(dev(S))
+    want = oracle.sa_naive(S)
+    assert np.array_equal(sa.cpu().numpy(), want)
+    assert np.array_equal(lcp.cpu().numpy(), oracle.lcp_naive(S, want))
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_sa_lcp_multi_tile(ctx, case):
+    S = multi_tile_cases()[case]
+    sa, lcp = ctx.suffix_array(dev(S))
+    want = oracle.sa_doubling(S)
+    assert np.array_equal(sa.cpu().numpy(), want)
+    assert np.array_equal(lcp.cpu().numpy(), oracle.lcp_kasai(S, want))
+
+
+def check_find(ctx, S, min_len, min_count=1, tier=0):
+    want = oracle.find_repeats(S, min_len, min_count, tier=tier)
+    if len(S) >= 2:
+        c = ctx.candidates(dev(S), min_len)
+        assert np.array_equal(c["cand_len"].cpu().numpy(), want["cand_len"])
+        assert np.array_equal(c["cand_start"].cpu().numpy(), want["cand_start"])
+        assert np.array_equal(c["cand_id"].cpu().numpy(), want["cand_id"])
+        assert np.array_equal(c["keep"].cpu().numpy(), want["keep"])
+    rep, occ = ctx.find_repeats(dev(S), min_len, min_count)
+    assert np.array_equal(rep.cpu().numpy(), want["repeats"])
+    assert np.array_equal(occ.cpu().numpy(), want["occ"])
+
+
+@pytest.mark.parametrize("case", range(len(small_cases())))
+@pytest.mark.parametrize("min_len", [1, 2, 5])
+def test_find_repeats_small(ctx, case, min_len):
+    check_find(ctx, small_cases()[case], min_len)
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_find_repeats_multi_tile(ctx, case):
+    check_find(ctx, multi_tile_cases()[case], 3, tier=1)
+    check_find(ctx, multi_tile_cases()[case], 25, tier=1)
+
+
+def test_min_count(ctx):
+    for S in (gen.from_text("aabcbcbaa"), gen.c1()):
+        check_find(ctx, S, 2, min_count=2)
+
+
+def test_edge_cases(ctx):
+    from paper_2406_18111_b200 import ApoError
+    rep, occ = ctx.find_repeats(dev(np.zeros(0, np.uint64)), 1)
+    assert rep.shape[0] == 0 and occ.shape[0] == 0
+    rep, occ = ctx.find_repeats(dev(gen.c1()[:9]), 5)      # n < 2 * min_len
+    assert rep.shape[0] == 0
+    with pytest.raises(ApoError):
+        ctx.find_repeats(dev(gen.c1()[:9]), 0)
+    sa, lcp = ctx.suffix_array(dev(np.array([3], np.uint64)))
+    assert sa.tolist() == [0] and lcp.numel() == 0
+
+
+def test_config_c1_full(ctx):
+    check_find(ctx, gen.c1(), 5, tier=0)
+
+
+def test_config_c2_full(ctx):
+    S = gen.c2()
+    sa, lcp = ctx.suffix_array(dev(S))
+    want = oracle.sa_doubling(S)
+    assert oracle.sa_check(S, sa.cpu().numpy())
+    assert np.array_equal(sa.cpu().numpy(), want)
+    assert np.array_equal(lcp.cpu().numpy(), oracle.lcp_kasai(S, want))
+    check_find(ctx, S, 25, tier=1)
+
+
+def test_config_c3_full(ctx):
+    S = gen.c3()
+    sa, lcp = ctx.suffix_array(dev(S))
+    sa = sa.cpu().numpy()
+    assert oracle.sa_check(S, sa)                      # O(n) certificate: SA is unique
+    want = oracle.sa_doubling(S)
+    assert np.array_equal(sa, want)
+    assert np.array_equal(lcp.cpu().numpy(), oracle.lcp_kasai(S, want))
+    check_find(ctx, S, 25, tier=1)
+
+
+def batch_case(windows=24, window=2048, seed=11):
+    tok, off, _, _ = gen.c4(seed=seed, windows=windows, window=window, templates=8, with_streams=False)
+    # ragged: cut some windows short, include an empty and a tiny window
+    lens = [window] * windows
+    lens[1] = 0
+    lens[2] = 7
+    lens[5] = window // 3
+    parts = [tok[off[w]:off[w] + lens[w]] for w in range(windows)]
+    new_off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    return np.concatenate(parts), new_off
+
+
+def test_batched_sa_equals_per_window(ctx):
+    tok, off = batch_case()
+    sa, lcp = ctx.suffix_array_batched(dev(tok), off)
+    sa, lcp = sa.cpu().numpy(), lcp.cpu().numpy()
+    for w in range(len(off) - 1):
+        S = tok[off[w]:off[w + 1]]
+        want = oracle.sa_doubling(S)
+        assert np.array_equal(sa[off[w]:off[w + 1]], want)
+        wl = oracle.lcp_kasai(S, want)
+        got = lcp[off[w]:off[w + 1]]
+        assert np.array_equal(got[:max(len(S) - 1, 0)], wl)
+        if len(S):
+            assert got[-1] == 0
+
+
+def test_batched_find_equals_per_window(ctx):
+    tok, off = batch_case()
+    for min_len in (5, 25):
+        rep, roff, occ = ctx.find_repeats_batched(dev(tok), off, min_len)
+        rep, roff, occ = rep.cpu().numpy(), roff.cpu().numpy(), occ.cpu().numpy()
+        assert roff[0] == 0 and roff[-1] == len(rep)
+        for w in range(len(off) - 1):
+            want = oracle.find_repeats(tok[off[w]:off[w + 1]], min_len, tier=1)
+            got = rep[roff[w]:roff[w + 1]]
+            assert np.array_equal(got[:, :3], want["repeats"][:, :3]), w
+            for row, wrow in zip(got, want["repeats"]):
+                assert np.array_equal(occ[row[3]:row[3] + row[2]], want["occ"][wrow[3]:wrow[3] + wrow[2]])
+
+
+def test_c4_full_batch_sampled(ctx):
+    """C4 at full size, in the bench's launch configuration; 24 sampled
+    windows are compared with the oracle one by one, every window is checked
+    for the output invariants."""
+    tok, off, _, _ = gen.c4(with_streams=False)
+    rep, roff, occ = ctx.find_repeats_batched(dev(tok), off, 25)
+    rep, roff, occ = rep.cpu().numpy(), roff.cpu().numpy(), occ.cpu().numpy()
+    W = len(off) - 1
+    rng = gen.Rng(123)
+    sample = sorted({int(rng.below(W)) for _ in range(24)} | {0, W - 1})
+    for w in sample:
+        want = oracle.find_repeats(tok[off[w]:off[w + 1]], 25, tier=1)
+        got = rep[roff[w]:roff[w + 1]]
+        assert np.array_equal(got[:, :3], want["repeats"][:, :3]), w
+    # invariants everywhere: disjoint occurrences, equal contents, length >= 25
+    for w in range(0, W, 97):
+        S = tok[off[w]:off[w + 1]]
+        cov = np.zeros(len(S), np.int32)
+        for st, ln, cnt, f in rep[roff[w]:roff[w + 1]]:
+            assert ln >= 25
+            for o in occ[f:f + cnt]:
+                assert np.array_equal(S[o:o + ln], S[st:st + ln])
+                cov[o:o + ln] += 1
+        assert cov.max(initial=0) <= 1
+
+
+def test_determinism(ctx):
+    S = gen.c3()[:200000]
+    a = ctx.find_repeats(dev(S), 25)
+    b = ctx.find_repeats(dev(S), 25)
+    assert all(torch.equal(x, y) for x, y in zip(a, b))
+
+
+def test_history_ingest_and_window(ctx):
+    S = gen.c3()[:20000]
+    h = ctx.history(5000, 500)
+    got = []
+    pos = 0
+    for chunk in (1, 499, 500, 1234, 7766, 10000):
+        got += h.ingest(dev(S[pos:pos + chunk]))
+        pos += chunk
+    assert got == oracle.ruler_slices(0, 20000, 500, 5000)
+    assert h.count == 20000
+    for b, e in got[-5:]:
+        assert np.array_equal(h.window(b, e).cpu().numpy(), S[b:e])
