@@ -181,6 +181,52 @@ apo_status apo_history_window(apo_history *h, int64_t begin, int64_t end, uint64
 /* Total number of tokens ever ingested. */
 int64_t apo_history_count(const apo_history *h);
 
+/* ---------------------------------------------------------------------- */
+/* Alg. 1 TraceReplayer: candidate trace set and batched matching           */
+/* ---------------------------------------------------------------------- */
+
+/* IngestCandidates (Alg. 1): build the candidate trace set
+ * from the output of apo_find_repeats_batched.  d_tok/h_off: the analysed
+ * batch (as passed to apo_find_repeats_batched); d_rep/d_rep_off: its
+ * repeats and DEVICE int64[nwin+1] offsets.  Each repeat's content is cut
+ * into consecutive max_len pieces ("recorded traces are broken into pieces
+ * of a given maximum size"; R15: the tail is kept iff >= min_len;
+ * max_len = 0: no cut).  Identical contents are merged; trace ids are ranks
+ * in (length desc, content lexicographic asc) order (R1).  The returned
+ * handle owns the traces on the device; free with apo_trie_destroy.
+ * Synchronises `stream`. */
+apo_status apo_trie_build(apo_ctx *ctx, const uint64_t *d_tok, const int64_t *h_off, int32_t nwin,
+                          const apo_repeat *d_rep, const int64_t *d_rep_off, int32_t min_len,
+                          int32_t max_len, apo_trie **out, void *stream);
+
+/* Same, from explicit trace contents (e.g. the union of candidate lists
+ * gathered from several GPUs): trace t is d_tr[h_tr_off[t] .. h_tr_off[t+1])
+ * (host int64 offsets, non-empty traces).  Duplicates are merged. */
+apo_status apo_trie_build_traces(apo_ctx *ctx, const uint64_t *d_tr, const int64_t *h_tr_off,
+                                 int32_t ntraces, apo_trie **out, void *stream);
+
+void apo_trie_destroy(apo_trie *trie);
+
+/* Sizes of the trace set: number of traces, total tokens, longest trace. */
+apo_status apo_trie_info(const apo_trie *trie, int64_t *h_ntraces, int64_t *h_ntokens,
+                         int64_t *h_maxlen);
+
+/* Copy the traces out in id order: d_tokens (device, ntokens) and h_off
+ * (host int64[ntraces+1]); either may be NULL. */
+apo_status apo_trie_copy(const apo_trie *trie, uint64_t *d_tokens, int64_t *h_off, void *stream);
+
+/* Batched matching of independent op streams against the trace set
+ * (Alg. 1 AdvanceActiveCandidates / FilterInvalidCandidates /
+ * FilterCompletedCandidates).  mode 0 = MATCH_ALL
+ * (reading R14): every (stream, end_pos, trace_id) with
+ * stream[end_pos-|t|+1 .. end_pos] == trace t, sorted by (stream, end_pos,
+ * trace_id); end_pos is stream-local.  Other modes: APO_ERR_INVALID.
+ * h_off: HOST int64[nstreams+1] CSR offsets into d_streams.  d_count
+ * (device int64[1]) <- number of hits; at most cap records are stored. */
+apo_status apo_match(apo_ctx *ctx, const apo_trie *trie, const uint64_t *d_streams,
+                     const int64_t *h_off, int32_t nstreams, int32_t mode, apo_match_rec *d_out,
+                     int64_t cap, int64_t *d_count, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -64,6 +64,12 @@ _SIGS = {
     "apo_ingest": (ctypes.c_int, [_VP, _VP, _I64, ctypes.POINTER(apo_slice), _I64, _P_I64, _VP]),
     "apo_history_window": (ctypes.c_int, [_VP, _I64, _I64, _VP, _VP]),
     "apo_history_count": (ctypes.c_int64, [_VP]),
+    "apo_trie_build": (ctypes.c_int, [_VP, _VP, _P_I64, _I32, _VP, _VP, _I32, _I32, ctypes.POINTER(_VP), _VP]),
+    "apo_trie_build_traces": (ctypes.c_int, [_VP, _VP, _P_I64, _I32, ctypes.POINTER(_VP), _VP]),
+    "apo_trie_destroy": (None, [_VP]),
+    "apo_trie_info": (ctypes.c_int, [_VP, _P_I64, _P_I64, _P_I64]),
+    "apo_trie_copy": (ctypes.c_int, [_VP, _VP, _P_I64, _VP]),
+    "apo_match": (ctypes.c_int, [_VP, _VP, _VP, _P_I64, _I32, _I32, _VP, _I64, _VP, _VP]),
 }
 
 _lib = None
@@ -248,6 +254,47 @@ class Context:
         r, oc = int(c[0]), int(c[1])
         return rep[:r].to("cpu"), roff.to("cpu"), occ[:oc].to("cpu")
 
+    # --------------------------------------------------------- trie/match --
+    def trie_build(self, tok: torch.Tensor, off, repeats: torch.Tensor, rep_off: torch.Tensor, min_len: int,
+                   max_len: int = 0) -> "Trie":
+        """IngestCandidates from apo_find_repeats_batched output (repeats int32[k,4], rep_off int64[W+1])."""
+        tok = _check_tok(tok, self.device)
+        o = _host_off(off)
+        repeats = repeats.contiguous()
+        rep_off = rep_off.to(self.device, torch.int64).contiguous()
+        h = ctypes.c_void_p()
+        self._raise(self.lib.apo_trie_build(self.h, _ptr(tok), o.ctypes.data_as(_P_I64), len(o) - 1, _ptr(repeats),
+                                            _ptr(rep_off), int(min_len), int(max_len), ctypes.byref(h),
+                                            _stream(self.device)))
+        return Trie(self, h)
+
+    def trie_build_traces(self, traces: torch.Tensor, tr_off) -> "Trie":
+        """Trace set from explicit contents (e.g. a gathered union); duplicates merged."""
+        o = _host_off(tr_off)
+        traces = _check_tok(traces, self.device) if traces.numel() else traces
+        h = ctypes.c_void_p()
+        self._raise(self.lib.apo_trie_build_traces(self.h, _ptr(traces) if traces.numel() else None,
+                                                   o.ctypes.data_as(_P_I64), len(o) - 1, ctypes.byref(h),
+                                                   _stream(self.device)))
+        return Trie(self, h)
+
+    def match(self, trie: "Trie", streams: torch.Tensor, off, cap: int | None = None):
+        """MATCH_ALL -> int32[h,3] rows (stream, end_pos, trace_id) sorted."""
+        streams = _check_tok(streams, self.device)
+        o = _host_off(off)
+        d = self.device
+        if cap is None:
+            cap = 1 << 22
+        while True:
+            out = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=d)
+            cnt = torch.zeros(1, dtype=torch.int64, device=d)
+            self._raise(self.lib.apo_match(self.h, trie.h, _ptr(streams), o.ctypes.data_as(_P_I64), len(o) - 1, 0,
+                                           _ptr(out), cap, _ptr(cnt), _stream(d)))
+            n = int(cnt.item())
+            if n <= cap:
+                return out[:n, :3]
+            cap = n
+
     # ------------------------------------------------------------ history --
     def history(self, capacity_B: int, scale_C: int) -> "History":
         return History(self, capacity_B, scale_C)
@@ -291,6 +338,36 @@ class History:
         self.ctx._raise(self.ctx.lib.apo_history_window(self.h, int(begin), int(end), _ptr(out),
                                                         _stream(self.ctx.device)))
         return out
+
+
+class Trie:
+    """The candidate trace set (apo_trie): traces in id order (length desc, lexicographic asc)."""
+
+    def __init__(self, ctx: Context, h):
+        self.ctx = ctx
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.ctx.lib.apo_trie_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def info(self):
+        t, n, m = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        self.ctx._raise(self.ctx.lib.apo_trie_info(self.h, ctypes.byref(t), ctypes.byref(n), ctypes.byref(m)))
+        return t.value, n.value, m.value
+
+    def traces(self):
+        """-> (tokens uint64 device tensor, host int64 offsets[T+1])."""
+        T, n, _ = self.info()
+        tok = torch.empty(max(n, 1), dtype=torch.uint64, device=self.ctx.device)
+        off = np.zeros(T + 1, dtype=np.int64)
+        self.ctx._raise(self.ctx.lib.apo_trie_copy(self.h, _ptr(tok), off.ctypes.data_as(_P_I64),
+                                                   _stream(self.ctx.device)))
+        return tok[:n], off
 
 
 _default: dict[int, Context] = {}

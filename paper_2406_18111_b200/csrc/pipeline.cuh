@@ -13,6 +13,10 @@ struct Batch {
   i64 maxwin = 0;            // longest window
   const i64 *off = nullptr;  // device int64[W+1] (nullptr when W == 1)
   const i32 *wid = nullptr;  // device int32[N] window of each position (nullptr when W == 1)
+  // Generalized mode: one suffix array over ALL windows (window w ends with
+  // its own sentinel $_w, $_0 < $_1 < ... < every token) instead of one
+  // suffix array per window.  Used by the trie build and the matcher.
+  bool gen = false;
 };
 
 __device__ __forceinline__ int b_wid(const Batch &b, i64 i) { return b.W == 1 ? 0 : b.wid[i]; }

@@ -52,21 +52,19 @@ __global__ void __launch_bounds__(kSortThreads) k_hist(const K *__restrict__ key
   __shared__ u32 sh[kMaxPasses * kMaxRadix];
   for (int i = threadIdx.x; i < plan.npass * kMaxRadix; i += kSortThreads) sh[i] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
+  int shift[kMaxPasses];
+  u32 mask[kMaxPasses];
+#pragma unroll
+  for (int p = 0; p < kMaxPasses; ++p) {
+    shift[p] = p < plan.npass ? plan.shift[p] : 0;
+    mask[p] = p < plan.npass ? (1u << plan.bits[p]) - 1u : 0u;
+  }
   const i64 stride = i64(gridDim.x) * kSortThreads;
-  // loop trip count is warp-uniform so match_any can use the full mask
-  const i64 nround = (n + stride - 1) / stride;
-  for (i64 r = 0; r < nround; ++r) {
-    i64 i = r * stride + i64(blockIdx.x) * kSortThreads + threadIdx.x;
-    bool valid = i < n;
-    u32 vmask = __ballot_sync(0xffffffffu, valid);
-    if (!valid) continue;
+  for (i64 i = i64(blockIdx.x) * kSortThreads + threadIdx.x; i < n; i += stride) {
     K k = keys[i];
-    for (int p = 0; p < plan.npass; ++p) {
-      u32 d = u32(u64(k) >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u);
-      u32 peers = __match_any_sync(vmask, d);
-      if (lane == __ffs(peers) - 1) atomicAdd(&sh[p * kMaxRadix + d], __popc(peers));
-    }
+#pragma unroll
+    for (int p = 0; p < kMaxPasses; ++p)
+      if (p < plan.npass) atomicAdd(&sh[p * kMaxRadix + (u32(u64(k) >> shift[p]) & mask[p])], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < plan.npass * kMaxRadix; i += kSortThreads)
@@ -101,7 +99,7 @@ __device__ __forceinline__ void block_excl_scan_bins(const u32 (&v)[BPT], u32 (&
 }
 
 template <class K, class V, int BITS>
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__ kin, K *__restrict__ kout,
+__global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(const K *__restrict__ kin, K *__restrict__ kout,
                                                            const V *__restrict__ vin, V *__restrict__ vout,
                                                            i64 n, int shift, int pbits,
                                                            const u32 *__restrict__ ghist, u64 *status,
@@ -128,15 +126,11 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__
   const u32 dmask = (1u << pbits) - 1u;
 
   K key[kSortItems];
-  V val[kSortItems];
   u32 rk[kSortItems];
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     i64 idx = wbase + j * 32 + lane;
-    if (idx < n) {
-      key[j] = kin[idx];
-      if constexpr (HAS_V) val[j] = vin[idx];
-    }
+    if (idx < n) key[j] = kin[idx];
   }
   u32 *wh = s_whist + warp * RADIX;
   const u32 lt = lanemask_lt();
@@ -198,9 +192,22 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__
     i64 idx = wbase + j * 32 + lane;
     if (idx < n) {
       u32 d = u32(u64(key[j]) >> shift) & dmask;
-      u32 pos = s_start[d] + wh[d] + rk[j];
-      s_keys[pos] = key[j];
-      if constexpr (HAS_V) s_vals[pos] = val[j];
+      rk[j] += s_start[d] + wh[d];  // block-local sorted position
+      s_keys[rk[j]] = key[j];
+    }
+  }
+  if constexpr (HAS_V) {
+    // values are loaded only now (keeps registers low during ranking)
+    V val[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+      i64 idx = wbase + j * 32 + lane;
+      if (idx < n) val[j] = vin[idx];
+    }
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+      i64 idx = wbase + j * 32 + lane;
+      if (idx < n) s_vals[rk[j]] = val[j];
     }
   }
   __syncthreads();

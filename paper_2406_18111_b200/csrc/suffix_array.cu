@@ -73,7 +73,11 @@ __global__ void k_double_keys(const i32 *__restrict__ rank, Batch b, i64 h, int 
   if (i >= b.N) return;
   int w = b_wid(b, i);
   i64 beg = b_beg(b, w), end = b_end(b, w);
-  u64 lo = (i + h < end) ? u64(rank[i + h] - beg + 1) : 0ull;
+  u64 lo;
+  if (b.gen)  // sentinel $_w = w, real ranks shifted above all sentinels
+    lo = (i + h < end) ? u64(rank[i + h]) + u64(b.W) : u64(w);
+  else        // window-local rank + 1, end of window = 0
+    lo = (i + h < end) ? u64(rank[i + h] - beg + 1) : 0ull;
   keys[i] = (u64(u32(rank[i])) << lob) | lo;
   vals[i] = u32(i);
 }
@@ -97,19 +101,21 @@ __global__ void k_phi(const u32 *__restrict__ sa, Batch b, i32 *__restrict__ phi
   i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= b.N) return;
   i64 i = sa[k];
-  int w = b_wid(b, i);
-  phi[i] = (k == b_beg(b, w)) ? -1 : i32(sa[k - 1]);
+  bool first = b.gen ? (k == 0) : (k == b_beg(b, b_wid(b, i)));
+  phi[i] = first ? -1 : i32(sa[k - 1]);
 }
 
 struct Levels {
   const i32 *p[40];
 };
 
-// lcp(i, j) (same window, both < end) by galloping over rank levels R-1..0.
-__device__ __forceinline__ i64 gallop_lcp(const Levels &L, int R, i64 i, i64 j, i64 end) {
+// lcp(i, j) (i < end_i, j < end_j) by galloping over rank levels R-1..0:
+// equal level-r ranks <=> equal 2^r-token prefixes (padded with the end
+// marker of the suffix's own window).
+__device__ __forceinline__ i64 gallop_lcp(const Levels &L, int R, i64 i, i64 j, i64 end_i, i64 end_j) {
   i64 l = 0;
   for (int r = R - 1; r >= 0; --r) {
-    if (i + l >= end || j + l >= end) break;
+    if (i + l >= end_i || j + l >= end_j) break;
     const i32 *lv = L.p[r];
     if (lv[i + l] == lv[j + l]) l += (i64(1) << r);
   }
@@ -140,11 +146,12 @@ __global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi,
       h = 0;
       continue;
     }
+    const i64 end_j = b.gen ? b_end(b, b_wid(b, j)) : end;
     if (h < 0) {
-      h = gallop_lcp(L, R, i, j, end);
+      h = gallop_lcp(L, R, i, j, end, end_j);
     } else {
       h = h > 0 ? h - 1 : 0;
-      while (i + h < end && j + h < end && tok[i + h] == tok[j + h]) ++h;
+      while (i + h < end && j + h < end_j && tok[i + h] == tok[j + h]) ++h;
     }
     plcp[i] = i32(h);
   }
@@ -154,8 +161,8 @@ __global__ void k_lcp_gather(const u32 *__restrict__ sa, const i32 *__restrict__
                              i32 *__restrict__ lcp) {
   i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= b.N) return;
-  int w = b_wid(b, sa[k]);
-  lcp[k] = (k + 1 < b_end(b, w)) ? plcp[sa[k + 1]] : 0;
+  i64 lim = b.gen ? b.N : b_end(b, b_wid(b, sa[k]));
+  lcp[k] = (k + 1 < lim) ? plcp[sa[k + 1]] : 0;
 }
 
 }  // namespace
@@ -197,7 +204,7 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   u64 *ok = alt ? w.keys : w.keys_alt;
   u32 *ov = alt ? w.vals : w.vals_alt;
   const u64 *tok_sorted = sk;
-  if (b.W > 1) {
+  if (b.W > 1 && !b.gen) {
     k_wid_keys<<<G, T, 0, s>>>(sv, b.wid, N, ok);
     APO_CHECK_LAUNCH();
     c.launches++;
@@ -212,13 +219,14 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
     sv = idx;
   }
   {
-    InitRankF f{tok_sorted, sv, b.W > 1 ? b.wid : nullptr, w.levels[0]};
+    InitRankF f{tok_sorted, sv, (b.W > 1 && !b.gen) ? b.wid : nullptr, w.levels[0]};
     launch_scan<true>(c, N, f, s);
   }
 
   // ---- K3: doubling rounds ----
-  const int lob = bits_for(u64(b.maxwin));
+  const int lob = b.gen ? bits_for(u64(N - 1) + u64(b.W)) : bits_for(u64(b.maxwin));
   const int hib = bits_for(u64(N - 1));
+  if (lob + hib > 64) throw Error{APO_ERR_INVALID, "batch too large for 64-bit doubling keys"};
   u32 *notdone = reinterpret_cast<u32 *>(c.d_misc);
   const u32 *final_sa = sv;
   int r = 0;

@@ -1,0 +1,629 @@
+// trie.cu -- a10/a11: the candidate trace set and the batched matcher.
+//
+// IngestCandidates (Alg. 1):
+//   * materialise every repeat's content S[start : start+length) from its
+//     window; "recorded traces are broken into pieces of a given maximum
+//     size" (reading R15): consecutive max_len pieces, the tail
+//     kept iff >= min_len;
+//   * order the pieces by (length desc, content lexicographic asc) and merge
+//     identical contents -> trace ids 0..T-1 in that order.
+//   The content order comes from ONE generalized suffix array over all
+//   pieces (each piece ends with its own sentinel $_w, $_0 < $_1 < ... <
+//   every token): the rank of a piece's full suffix orders it among all
+//   pieces; identical neighbours are merged after a warp-parallel direct
+//   comparison.  The sorted, deduplicated trace list is the trie in array
+//   form (a node = an LCP interval of it).
+//
+// Matching (Alg. 1 AdvanceActiveCandidates / FilterInvalid /
+// FilterCompleted; MATCH_ALL, reading R14):
+//   report every (stream, end, trace) with stream[end-|t|+1 .. end] == t.
+//   One generalized suffix array over streams + traces: the stream suffixes
+//   that start with trace t form the LCP interval around t's own full suffix
+//   (maximal rank range with LCP >= |t|), found in O(log n) with a sparse
+//   table; the interval is enumerated with a load-balanced scan and the hits
+//   are radix-sorted by (stream, end, trace).
+#include <algorithm>
+#include <vector>
+
+#include "pipeline.cuh"
+
+struct apo_trie {
+  apo_ctx *ctx;
+  apo::i64 T = 0;      // distinct traces
+  apo::i64 ntok = 0;   // total tokens
+  apo::i64 maxlen = 0;
+  apo::u64 *d_tok = nullptr;  // traces in id order, back to back
+  apo::i64 *d_off = nullptr;  // T+1
+  std::vector<apo::i64> h_off;
+};
+
+namespace apo {
+namespace {
+
+constexpr int T256 = 256;
+
+// ------------------------------------------------------------ pieces ----
+struct SrcRep {
+  const apo_repeat *rep;
+  const i64 *rep_off;  // device, nwin+1
+  const i64 *src_off;  // device, nwin+1 (source windows)
+  int nwin;
+  i64 nrep;
+  i32 min_len, max_len;
+};
+
+__device__ __forceinline__ int rep_window(const SrcRep &s, i64 r) {
+  int lo = 0, hi = s.nwin - 1;  // last w with rep_off[w] <= r
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (s.rep_off[mid] <= r)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ i64 n_pieces(i64 len, i32 min_len, i32 max_len) {
+  if (max_len <= 0 || len <= max_len) return 1;
+  i64 full = len / max_len, tail = len % max_len;
+  return full + ((tail > 0 && tail >= min_len) ? 1 : 0);
+}
+
+struct PieceCountF {
+  SrcRep s;
+  u32 *piece_base;
+  i64 *total;
+  __device__ u32 load(i64 r) const { return u32(n_pieces(s.rep[r].length, s.min_len, s.max_len)); }
+  __device__ bool store(i64 r, u32 incl, u32 excl) const {
+    piece_base[r] = excl;
+    if (r == s.nrep - 1) *total = i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+__global__ void k_pieces(SrcRep s, const u32 *__restrict__ piece_base, i64 *__restrict__ p_src,
+                         i32 *__restrict__ p_len) {
+  i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= s.nrep) return;
+  apo_repeat rp = s.rep[r];
+  int w = rep_window(s, r);
+  i64 src = s.src_off[w] + rp.start;
+  i64 np = n_pieces(rp.length, s.min_len, s.max_len);
+  i64 step = (s.max_len > 0 && rp.length > s.max_len) ? s.max_len : rp.length;
+  for (i64 q = 0; q < np; ++q) {
+    i64 a = q * step;
+    i64 ln = rp.length - a < step ? rp.length - a : step;
+    p_src[piece_base[r] + q] = src + a;
+    p_len[piece_base[r] + q] = i32(ln);
+  }
+}
+
+// one warp per piece: copy its tokens
+__global__ void k_copy_pieces(const u64 *__restrict__ src_tok, const i64 *__restrict__ p_src,
+                              const i64 *__restrict__ p_off, i64 np, u64 *__restrict__ dst) {
+  i64 p = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (p >= np) return;
+  i64 a = p_src[p], o = p_off[p], n = p_off[p + 1] - o;
+  for (i64 k = lane; k < n; k += 32) dst[o + k] = src_tok[a + k];
+}
+
+// ------------------------------------------------ order + dedup ----
+__global__ void k_trace_keys(const i64 *__restrict__ off, i64 ntr, i64 maxlen, int bN,
+                             const i32 *__restrict__ final_rank, u64 *__restrict__ keys, u32 *__restrict__ vals) {
+  i64 w = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (w >= ntr) return;
+  i64 len = off[w + 1] - off[w];
+  keys[w] = (u64(maxlen - len) << bN) | u64(u32(final_rank[off[w]]));
+  vals[w] = u32(w);
+}
+
+// warp per sorted neighbour pair: same length and same content -> not a head
+__global__ void k_trace_heads(const u64 *__restrict__ tok, const i64 *__restrict__ off, const u32 *__restrict__ order,
+                              i64 ntr, u32 *__restrict__ head) {
+  i64 c = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (c >= ntr) return;
+  if (c == 0) {
+    if (lane == 0) head[0] = 1;
+    return;
+  }
+  i64 a = order[c - 1], b = order[c];
+  i64 la = off[a + 1] - off[a], lb = off[b + 1] - off[b];
+  bool same = la == lb;
+  for (i64 k = lane; same && k < la; k += 32) {
+    bool eq = tok[off[a] + k] == tok[off[b] + k];
+    same = __all_sync(__activemask(), eq);
+  }
+  same = __shfl_sync(0xffffffffu, same ? 1 : 0, 0) != 0;
+  if (lane == 0) head[c] = same ? 0u : 1u;
+}
+
+struct TraceIdF {
+  const u32 *head;
+  const u32 *order;
+  const i64 *off;
+  u32 *uniq;    // uniq[id] = source piece
+  i32 *ulen;    // ulen[id] = length
+  i64 n;
+  i64 *T_out;
+  __device__ u32 load(i64 c) const { return head[c]; }
+  __device__ bool store(i64 c, u32 incl, u32 excl) const {
+    if (incl != excl) {
+      u32 w = order[c];
+      uniq[excl] = w;
+      ulen[excl] = i32(off[w + 1] - off[w]);
+    }
+    if (c == n - 1) *T_out = i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+// ---------------------------------------------------------- matching ----
+__global__ void k_rmq_level_t(const i32 *__restrict__ prev, i32 *__restrict__ next, i64 n, i64 half) {
+  i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  i32 x = prev[k];
+  if (k + half < n) {
+    i32 y = prev[k + half];
+    x = y < x ? y : x;
+  }
+  next[k] = x;
+}
+
+struct Sparse {
+  const i32 *lv[32];
+  int levels;
+};
+
+// maximal rank interval [lo, hi] around r with LCP >= L between neighbours
+__device__ __forceinline__ void lcp_interval(const Sparse &sp, i64 n, i64 r, i32 L, i64 &lo, i64 &hi) {
+  // left: largest jump such that min LCP[lo-2^j .. lo-1] >= L
+  i64 a = r;
+  for (int j = sp.levels - 1; j >= 0; --j) {
+    i64 w = i64(1) << j;
+    if (a - w >= 0 && sp.lv[j][a - w] >= L) a -= w;
+  }
+  i64 b = r;  // right: min LCP[b .. b+2^j-1] >= L  (LCP[k] links k and k+1)
+  for (int j = sp.levels - 1; j >= 0; --j) {
+    i64 w = i64(1) << j;
+    if (b + w <= n - 1 && sp.lv[j][b] >= L) b += w;
+  }
+  lo = a;
+  hi = b;
+}
+
+struct MatchSetup {
+  Sparse sp;
+  i64 N, Ns;             // total positions, stream positions
+  int S;                 // streams
+  i64 T;                 // traces
+  const i64 *off;        // combined offsets (streams then traces)
+  const i32 *wid;
+  const i32 *final_rank;
+  const i32 *sa;
+};
+
+struct IntervalF {
+  MatchSetup m;
+  i64 *ilo;
+  u32 *ibase;
+  i64 *total;
+  __device__ u32 load(i64 t) const {
+    i64 p = m.off[m.S + t];
+    i32 L = i32(m.off[m.S + t + 1] - p);
+    i64 lo, hi;
+    lcp_interval(m.sp, m.N, m.final_rank[p], L, lo, hi);
+    ilo[t] = lo;
+    return u32(hi - lo + 1);
+  }
+  __device__ bool store(i64 t, u32 incl, u32 excl) const {
+    ibase[t] = excl;
+    if (t == m.T - 1) *total = i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+__global__ void k_enumerate(MatchSetup m, const i64 *__restrict__ ilo, const u32 *__restrict__ ibase, i64 Z,
+                            int bE, int bT, u64 *__restrict__ keys, u32 *__restrict__ nvalid) {
+  i64 z = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool valid = false;
+  if (z < Z) {
+    // trace owning slot z: last t with ibase[t] <= z
+    i64 lo = 0, hi = m.T - 1;
+    while (lo < hi) {
+      i64 mid = (lo + hi + 1) >> 1;
+      if (i64(ibase[mid]) <= z)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    i64 t = lo;
+    i64 k = ilo[t] + (z - i64(ibase[t]));
+    i64 p = m.sa[k];
+    u64 key = ~0ull;
+    if (p < m.Ns) {
+      int q = m.wid[p];
+      i64 L = m.off[m.S + t + 1] - m.off[m.S + t];
+      i64 end = p - m.off[q] + L - 1;
+      key = (u64(q) << (bE + bT)) | (u64(end) << bT) | u64(t);
+      valid = true;
+    }
+    keys[z] = key;
+  }
+  unsigned b = __ballot_sync(0xffffffffu, valid);
+  if ((threadIdx.x & 31) == 0 && b) atomicAdd(nvalid, u32(__popc(b)));
+}
+
+__global__ void k_write_hits(const u64 *__restrict__ keys, i64 nhits, i64 cap, int bE, int bT,
+                             apo_match_rec *__restrict__ out) {
+  i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nhits || i >= cap) return;
+  u64 k = keys[i];
+  apo_match_rec r;
+  r.trace_id = i32(k & ((1ull << bT) - 1));
+  r.end_pos = i32((k >> bT) & ((1ull << bE) - 1));
+  r.stream = i32(k >> (bE + bT));
+  r._pad = 0;
+  out[i] = r;
+}
+
+__global__ void k_fill_wid_t(const i64 *__restrict__ off, int W, i64 N, i32 *__restrict__ wid) {
+  i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int lo = 0, hi = W - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= i)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  wid[i] = lo;
+}
+
+// Generalized SA setup for a host-described batch; returns the carved work.
+struct GenPlan {
+  SAWork sa{};
+  i64 *d_off = nullptr;
+  i32 *d_wid = nullptr;
+};
+
+void plan_gen(Carver &cv, Batch &b, GenPlan &g, bool lcp) {
+  g.d_off = cv.take<i64>(size_t(b.W) + 1);
+  g.d_wid = cv.take<i32>(size_t(b.N));
+  plan_sa(cv, b, g.sa, lcp);
+}
+
+void upload_batch(Ctx &c, Batch &b, GenPlan &g, const std::vector<i64> &h_off, cudaStream_t s) {
+  APO_CUDA(cudaMemcpyAsync(g.d_off, h_off.data(), sizeof(i64) * h_off.size(), cudaMemcpyHostToDevice, s));
+  k_fill_wid_t<<<grid_for(b.N, T256), T256, 0, s>>>(g.d_off, b.W, b.N, g.d_wid);
+  APO_CHECK_LAUNCH();
+  c.launches++;
+  b.off = g.d_off;
+  b.wid = g.d_wid;
+}
+
+// Builds the trace set from pieces d_ptok / h_poff (host offsets).
+void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<i64> &h_poff, cudaStream_t s) {
+  const i64 np = i64(h_poff.size()) - 1;
+  const i64 N = h_poff.back();
+  tr->T = 0;
+  tr->ntok = 0;
+  tr->maxlen = 0;
+  tr->h_off.assign(1, 0);
+  if (np <= 0 || N <= 0) return;
+  Batch b;
+  b.N = N;
+  b.W = int(np);
+  b.gen = true;
+  for (i64 w = 0; w < np; ++w) b.maxwin = std::max<i64>(b.maxwin, h_poff[w + 1] - h_poff[w]);
+  const i64 maxlen = b.maxwin;
+  // plan: generalized SA (no LCP) + ordering buffers
+  GenPlan g;
+  u64 *keys, *keys_alt;
+  u32 *vals, *vals_alt, *head, *uniq;
+  i32 *ulen;
+  i64 *scal;
+  auto plan = [&](Carver &cv) {
+    plan_gen(cv, b, g, false);
+    keys = cv.take<u64>(np);
+    keys_alt = cv.take<u64>(np);
+    vals = cv.take<u32>(np);
+    vals_alt = cv.take<u32>(np);
+    head = cv.take<u32>(np);
+    uniq = cv.take<u32>(np);
+    ulen = cv.take<i32>(np);
+    scal = cv.take<i64>(4);
+  };
+  Carver dry(nullptr);
+  plan(dry);
+  c.arena.reserve(dry.off, s);
+  Carver cv(c.arena.base);
+  plan(cv);
+  upload_batch(c, b, g, h_poff, s);
+  build_sa(c, d_ptok, b, g.sa, false, s);
+  const i32 *final_rank = g.sa.levels[g.sa.R];
+  const int bN = bits_for(u64(N - 1));
+  k_trace_keys<<<grid_for(np, T256), T256, 0, s>>>(g.d_off, np, maxlen, bN, final_rank, keys, vals);
+  APO_CHECK_LAUNCH();
+  bool a = radix_sort_u64_u32(c, keys, vals, keys_alt, vals_alt, np, 0, bN + bits_for(u64(maxlen)), s);
+  const u32 *order = a ? vals_alt : vals;
+  k_trace_heads<<<grid_for(np * 32, T256), T256, 0, s>>>(d_ptok, g.d_off, order, np, head);
+  APO_CHECK_LAUNCH();
+  c.launches += 2;
+  TraceIdF f{head, order, g.d_off, uniq, ulen, np, scal};
+  launch_scan<false>(c, np, f, s);
+  const i64 T = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
+  // offsets of the distinct traces (host prefix sums of the lengths)
+  std::vector<i64> h_uoff(size_t(T) + 1, 0);
+  {
+    std::vector<i32> hl(static_cast<size_t>(T));
+    APO_CUDA(cudaMemcpyAsync(hl.data(), ulen, sizeof(i32) * T, cudaMemcpyDeviceToHost, s));
+    APO_CUDA(cudaStreamSynchronize(s));
+    for (i64 t = 0; t < T; ++t) h_uoff[t + 1] = h_uoff[t] + hl[t];
+  }
+  const i64 ntok = h_uoff[T];
+  APO_CUDA(cudaMalloc(&tr->d_tok, sizeof(u64) * std::max<i64>(ntok, 1)));
+  APO_CUDA(cudaMalloc(&tr->d_off, sizeof(i64) * (T + 1)));
+  APO_CUDA(cudaMemcpyAsync(tr->d_off, h_uoff.data(), sizeof(i64) * (T + 1), cudaMemcpyHostToDevice, s));
+  // source start of each distinct trace = piece offset of uniq[id]
+  i64 *d_src = reinterpret_cast<i64 *>(keys);  // reuse
+  {
+    std::vector<u32> hu(static_cast<size_t>(T));
+    APO_CUDA(cudaMemcpyAsync(hu.data(), uniq, sizeof(u32) * T, cudaMemcpyDeviceToHost, s));
+    APO_CUDA(cudaStreamSynchronize(s));
+    std::vector<i64> hs(static_cast<size_t>(T));
+    for (i64 t = 0; t < T; ++t) hs[t] = h_poff[hu[t]];
+    APO_CUDA(cudaMemcpyAsync(d_src, hs.data(), sizeof(i64) * T, cudaMemcpyHostToDevice, s));
+    k_copy_pieces<<<grid_for(T * 32, T256), T256, 0, s>>>(d_ptok, d_src, tr->d_off, T, tr->d_tok);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+    APO_CUDA(cudaStreamSynchronize(s));
+  }
+  tr->T = T;
+  tr->ntok = ntok;
+  tr->maxlen = maxlen;
+  tr->h_off = std::move(h_uoff);
+}
+
+}  // namespace
+}  // namespace apo
+
+using namespace apo;
+
+namespace {
+template <class Fn>
+apo_status trie_guard(apo_ctx *ctx, Fn &&fn) {
+  if (!ctx) return APO_ERR_INVALID;
+  ctx->c.err.clear();
+  try {
+    cudaSetDevice(ctx->c.device);
+    fn(ctx->c);
+    return APO_OK;
+  } catch (const Error &e) {
+    ctx->c.err = e.msg;
+    return e.code;
+  } catch (const std::exception &e) {
+    ctx->c.err = e.what();
+    return APO_ERR_CUDA;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+apo_status apo_trie_build(apo_ctx *ctx, const uint64_t *d_tok, const int64_t *h_off, int32_t nwin,
+                          const apo_repeat *d_rep, const int64_t *d_rep_off, int32_t min_len, int32_t max_len,
+                          apo_trie **out, void *stream) {
+  if (!out) return APO_ERR_INVALID;
+  *out = nullptr;
+  apo_trie *tr = new apo_trie();
+  tr->ctx = ctx;
+  apo_status st = trie_guard(ctx, [&](Ctx &c) {
+    require(nwin >= 1 && h_off != nullptr && d_rep_off != nullptr && min_len >= 1 && max_len >= 0,
+            "invalid argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    i64 nrep = 0;
+    APO_CUDA(cudaMemcpyAsync(&nrep, d_rep_off + nwin, sizeof(i64), cudaMemcpyDeviceToHost, s));
+    APO_CUDA(cudaStreamSynchronize(s));
+    if (nrep == 0) {
+      tr->h_off.assign(1, 0);
+      return;
+    }
+    require(d_tok != nullptr && d_rep != nullptr, "NULL device pointer");
+    // pieces
+    i64 *d_src_off = nullptr, *scal = nullptr, *p_src = nullptr, *p_off = nullptr;
+    u32 *pbase = nullptr;
+    i32 *p_len = nullptr;
+    APO_CUDA(cudaMalloc(&d_src_off, sizeof(i64) * (nwin + 1)));
+    APO_CUDA(cudaMalloc(&scal, sizeof(i64) * 4));
+    APO_CUDA(cudaMalloc(&pbase, sizeof(u32) * nrep));
+    APO_CUDA(cudaMemcpyAsync(d_src_off, h_off, sizeof(i64) * (nwin + 1), cudaMemcpyHostToDevice, s));
+    SrcRep sr{d_rep, d_rep_off, d_src_off, nwin, nrep, min_len, max_len};
+    PieceCountF pf{sr, pbase, scal};
+    launch_scan<false>(c, nrep, pf, s);
+    const i64 np = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
+    APO_CUDA(cudaMalloc(&p_src, sizeof(i64) * np));
+    APO_CUDA(cudaMalloc(&p_len, sizeof(i32) * np));
+    APO_CUDA(cudaMalloc(&p_off, sizeof(i64) * (np + 1)));
+    k_pieces<<<grid_for(nrep, T256), T256, 0, s>>>(sr, pbase, p_src, p_len);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+    std::vector<i32> hl(static_cast<size_t>(np));
+    APO_CUDA(cudaMemcpyAsync(hl.data(), p_len, sizeof(i32) * np, cudaMemcpyDeviceToHost, s));
+    APO_CUDA(cudaStreamSynchronize(s));
+    std::vector<i64> h_poff(size_t(np) + 1, 0);
+    for (i64 q = 0; q < np; ++q) h_poff[q + 1] = h_poff[q] + hl[q];
+    APO_CUDA(cudaMemcpyAsync(p_off, h_poff.data(), sizeof(i64) * (np + 1), cudaMemcpyHostToDevice, s));
+    u64 *ptok = nullptr;
+    APO_CUDA(cudaMalloc(&ptok, sizeof(u64) * std::max<i64>(h_poff[np], 1)));
+    k_copy_pieces<<<grid_for(np * 32, T256), T256, 0, s>>>(d_tok, p_src, p_off, np, ptok);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+    build_trace_set(c, tr, ptok, h_poff, s);
+    APO_CUDA(cudaStreamSynchronize(s));
+    cudaFree(ptok);
+    cudaFree(p_off);
+    cudaFree(p_len);
+    cudaFree(p_src);
+    cudaFree(pbase);
+    cudaFree(scal);
+    cudaFree(d_src_off);
+  });
+  if (st != APO_OK) {
+    apo_trie_destroy(tr);
+    return st;
+  }
+  *out = tr;
+  return APO_OK;
+}
+
+apo_status apo_trie_build_traces(apo_ctx *ctx, const uint64_t *d_tr, const int64_t *h_tr_off, int32_t ntraces,
+                                 apo_trie **out, void *stream) {
+  if (!out) return APO_ERR_INVALID;
+  *out = nullptr;
+  apo_trie *tr = new apo_trie();
+  tr->ctx = ctx;
+  apo_status st = trie_guard(ctx, [&](Ctx &c) {
+    require(ntraces >= 0 && (ntraces == 0 || h_tr_off != nullptr), "invalid argument");
+    std::vector<i64> h(size_t(ntraces) + 1, 0);
+    for (int t = 0; t <= ntraces; ++t) h[t] = ntraces ? h_tr_off[t] : 0;
+    for (int t = 0; t < ntraces; ++t) require(h[t + 1] > h[t], "traces must be non-empty");
+    require(h[0] == 0, "h_tr_off[0] must be 0");
+    require(ntraces == 0 || d_tr != nullptr, "NULL device pointer");
+    build_trace_set(c, tr, d_tr, h, static_cast<cudaStream_t>(stream));
+  });
+  if (st != APO_OK) {
+    apo_trie_destroy(tr);
+    return st;
+  }
+  *out = tr;
+  return APO_OK;
+}
+
+void apo_trie_destroy(apo_trie *tr) {
+  if (!tr) return;
+  if (tr->ctx) cudaSetDevice(tr->ctx->c.device);
+  if (tr->d_tok) cudaFree(tr->d_tok);
+  if (tr->d_off) cudaFree(tr->d_off);
+  delete tr;
+}
+
+apo_status apo_trie_info(const apo_trie *tr, int64_t *h_ntraces, int64_t *h_ntokens, int64_t *h_maxlen) {
+  if (!tr) return APO_ERR_INVALID;
+  if (h_ntraces) *h_ntraces = tr->T;
+  if (h_ntokens) *h_ntokens = tr->ntok;
+  if (h_maxlen) *h_maxlen = tr->maxlen;
+  return APO_OK;
+}
+
+apo_status apo_trie_copy(const apo_trie *tr, uint64_t *d_tokens, int64_t *h_off, void *stream) {
+  if (!tr) return APO_ERR_INVALID;
+  if (h_off) std::copy(tr->h_off.begin(), tr->h_off.end(), h_off);
+  if (tr->ntok > 0 && d_tokens) {
+    cudaError_t e = cudaMemcpyAsync(d_tokens, tr->d_tok, sizeof(u64) * tr->ntok, cudaMemcpyDeviceToDevice,
+                                    static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return APO_ERR_CUDA;
+  }
+  return APO_OK;
+}
+
+apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams, const int64_t *h_off,
+                     int32_t nstreams, int32_t mode, apo_match_rec *d_out, int64_t cap, int64_t *d_count,
+                     void *stream) {
+  return trie_guard(ctx, [&](Ctx &c) {
+    require(tr != nullptr && d_count != nullptr && cap >= 0 && nstreams >= 1 && h_off != nullptr, "invalid argument");
+    require(mode == 0, "only MATCH_ALL (mode 0) is implemented");
+    require(cap == 0 || d_out != nullptr, "d_out is NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    APO_CUDA(cudaMemsetAsync(d_count, 0, sizeof(i64), s));
+    const i64 Ns = h_off[nstreams];
+    require(h_off[0] == 0, "h_off[0] must be 0");
+    i64 maxs = 0;
+    for (int q = 0; q < nstreams; ++q) {
+      require(h_off[q + 1] >= h_off[q], "h_off must be non-decreasing");
+      maxs = std::max<i64>(maxs, h_off[q + 1] - h_off[q]);
+    }
+    if (tr->T == 0 || Ns == 0) return;
+    require(d_streams != nullptr, "NULL device pointer");
+    const i64 T = tr->T;
+    const i64 N = Ns + tr->ntok;
+    require(N < (i64(1) << 31) - 1, "streams + traces longer than 2^31-1 tokens");
+    const int bT = bits_for(u64(T - 1)), bE = bits_for(u64(maxs - 1)), bS = bits_for(u64(nstreams - 1));
+    require(bT + bE + bS <= 63, "match key does not fit 63 bits");
+    std::vector<i64> h_all(size_t(nstreams) + size_t(T) + 1);
+    for (int q = 0; q <= nstreams; ++q) h_all[q] = h_off[q];
+    for (i64 t = 1; t <= T; ++t) h_all[nstreams + t] = Ns + tr->h_off[t];
+    Batch b;
+    b.N = N;
+    b.W = int(nstreams + T);
+    b.gen = true;
+    b.maxwin = std::max<i64>(maxs, tr->maxlen);
+    GenPlan g;
+    u64 *tok = nullptr, *keys = nullptr, *keys_alt = nullptr;
+    i64 *ilo = nullptr, *scal = nullptr;
+    u32 *ibase = nullptr;
+    i32 *sp_lv[32] = {};
+    const int levels = bits_for(u64(N));
+    auto plan = [&](Carver &cv) {
+      plan_gen(cv, b, g, true);
+      tok = cv.take<u64>(N);
+      for (int j = 1; j < levels; ++j) sp_lv[j] = cv.take<i32>(N);
+      ilo = cv.take<i64>(T);
+      ibase = cv.take<u32>(T);
+      scal = cv.take<i64>(4);
+    };
+    Carver dry(nullptr);
+    plan(dry);
+    c.arena.reserve(dry.off, s);
+    Carver cv(c.arena.base);
+    plan(cv);
+    APO_CUDA(cudaMemcpyAsync(tok, d_streams, sizeof(u64) * Ns, cudaMemcpyDeviceToDevice, s));
+    APO_CUDA(cudaMemcpyAsync(tok + Ns, tr->d_tok, sizeof(u64) * tr->ntok, cudaMemcpyDeviceToDevice, s));
+    upload_batch(c, b, g, h_all, s);
+    build_sa(c, tok, b, g.sa, true, s);
+    Sparse sp{};
+    sp.levels = levels;
+    sp.lv[0] = g.sa.lcp;
+    for (int j = 1; j < levels; ++j) {
+      k_rmq_level_t<<<grid_for(N, T256), T256, 0, s>>>(sp.lv[j - 1], sp_lv[j], N, i64(1) << (j - 1));
+      APO_CHECK_LAUNCH();
+      c.launches++;
+      sp.lv[j] = sp_lv[j];
+    }
+    MatchSetup m{sp, N, Ns, nstreams, T, g.d_off, g.d_wid, g.sa.levels[g.sa.R], g.sa.sa};
+    APO_CUDA(cudaMemsetAsync(scal, 0, sizeof(i64) * 4, s));
+    IntervalF itf{m, ilo, ibase, scal};
+    launch_scan<false>(c, T, itf, s);
+    const i64 Z = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
+    if (Z == 0) return;
+    // hit keys (invalid slots = ~0 sort last); reuse the SA key buffers when large enough
+    size_t need = sizeof(u64) * size_t(Z) * 2;
+    u64 *kbuf = nullptr;
+    APO_CUDA(cudaMalloc(&kbuf, need));
+    keys = kbuf;
+    keys_alt = kbuf + Z;
+    u32 *nvalid = reinterpret_cast<u32 *>(scal + 1);
+    k_enumerate<<<grid_for(Z, T256), T256, 0, s>>>(m, ilo, ibase, Z, bE, bT, keys, nvalid);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+    const i64 nh = i64(c.read_u32(nvalid, s));
+    bool a = radix_sort_u64_keys(c, keys, keys_alt, Z, 0, 64, s);
+    const u64 *sorted = a ? keys_alt : keys;
+    if (nh > 0 && cap > 0) {
+      k_write_hits<<<grid_for(std::min(nh, cap), T256), T256, 0, s>>>(sorted, nh, cap, bE, bT, d_out);
+      APO_CHECK_LAUNCH();
+      c.launches++;
+    }
+    APO_CUDA(cudaMemcpyAsync(d_count, &nh, sizeof(i64), cudaMemcpyHostToDevice, s));
+    APO_CUDA(cudaStreamSynchronize(s));
+    cudaFree(kbuf);
+  });
+}
+
+}  // extern "C"

@@ -215,3 +215,47 @@ def test_history_ingest_and_window(ctx):
     assert h.count == 20000
     for b, e in got[-5:]:
         assert np.array_equal(h.window(b, e).cpu().numpy(), S[b:e])
+
+
+def test_config_c5_proxy(ctx):
+    """C5's structure (4-token alphabet, 1,000-op period) at 2^20: full parity."""
+    S = gen.c5(n=1 << 20)
+    sa, lcp = ctx.suffix_array(dev(S))
+    want = oracle.sa_doubling(S)
+    assert np.array_equal(sa.cpu().numpy(), want)
+    assert np.array_equal(lcp.cpu().numpy(), oracle.lcp_kasai(S, want))
+    check_find(ctx, S, 25, tier=1)
+
+
+def test_config_c5_full(ctx):
+    """C5 at 2^26 (64M): the O(n) suffix-array certificate (the SA is unique),
+    sampled LCP entries by direct comparison, and the repeat invariants."""
+    S = gen.c5()
+    d = dev(S)
+    sa, lcp = ctx.suffix_array(d)
+    sa_h = sa.cpu().numpy()
+    assert oracle.sa_check(S, sa_h)
+    lcp_h = lcp.cpu().numpy()
+    rng = gen.Rng(55)
+    for _ in range(8):
+        k = int(rng.below(len(S) - 1))
+        a, b = int(sa_h[k]), int(sa_h[k + 1])
+        L = int(lcp_h[k])
+        m = min(len(S) - a, len(S) - b)
+        assert L <= m and np.array_equal(S[a:a + L], S[b:b + L])
+        assert L == m or S[a + L] != S[b + L]
+    del sa, lcp
+    rep, occ = ctx.find_repeats(d, 25)
+    rep, occ = rep.cpu().numpy(), occ.cpu().numpy()
+    assert len(rep) >= 1
+    # the longest candidate is always kept first (R12, valid form): a pair of
+    # same-phase suffixes 1,000 apart gives l = ((p+d)/2) rounded down to a multiple of d
+    st, ln, cnt, f = rep[0]
+    assert ln % 1000 == 0 and cnt >= 2
+    cov = np.zeros(len(S), np.int8)
+    for st, ln, cnt, f in rep:
+        o = occ[f:f + cnt]
+        for x in o:
+            assert cov[x:x + ln].max() == 0
+            cov[x:x + ln] = 1
+        assert np.array_equal(S[o[0]:o[0] + min(ln, 4096)], S[o[-1]:o[-1] + min(ln, 4096)])

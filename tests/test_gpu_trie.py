@@ -1,0 +1,106 @@
+"""GPU parity for the trace set (IngestCandidates) and MATCH_ALL matching
+against the CPU oracle (oracle/traces.py, or_match_brute): bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from workloads import gen
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2406_18111_b200 import build
+    build.build()
+    from paper_2406_18111_b200 import Context
+    return Context(0)
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint64)).cuda()
+
+
+def trace_list(tok, off):
+    return [tuple(int(x) for x in tok[off[i]:off[i + 1]]) for i in range(len(off) - 1)]
+
+
+def small_batch(windows=12, window=1500, seed=21):
+    tok, off, st, so = gen.c4(seed=seed, windows=windows, window=window, templates=6)
+    return tok, off, st, so
+
+
+@pytest.mark.parametrize("max_len", [0, 40, 7])
+def test_trie_from_repeats(ctx, max_len):
+    tok, off, _, _ = small_batch()
+    min_len = 5
+    rep, roff, occ = ctx.find_repeats_batched(dev(tok), off, min_len)
+    trie = ctx.trie_build(dev(tok), off, rep, roff, min_len, max_len)
+    got_tok, got_off = trie.traces()
+    got = trace_list(got_tok.cpu().numpy(), got_off)
+    # oracle: per-window repeats, then IngestCandidates
+    srcs = [tok[off[w]:off[w + 1]] for w in range(len(off) - 1)]
+    reps = [oracle.find_repeats(s, min_len, tier=1)["repeats"] for s in srcs]
+    wt, wo = oracle.traces_from_repeats(srcs, reps, min_len, max_len)
+    want = trace_list(wt, wo)
+    assert got == want
+    T, n, m = trie.info()
+    assert T == len(want) and n == sum(len(t) for t in want)
+
+
+def test_trie_from_traces_order_dedup(ctx):
+    rng = gen.Rng(5)
+    base = [tuple(int(x) for x in gen.random_string(i, 1 + rng.below(9), 3)) for i in range(60)]
+    # add duplicates, prefixes of others and high-bit tokens
+    extra = [base[3], base[7], base[3][:2] or base[3], (1 << 63, 1), (1 << 63, 1), (5,), (5,)]
+    allt = [t for t in base + extra if len(t)]
+    flat = np.array([x for t in allt for x in t], dtype=np.uint64)
+    toff = np.cumsum([0] + [len(t) for t in allt]).astype(np.int64)
+    trie = ctx.trie_build_traces(dev(flat), toff)
+    got_tok, got_off = trie.traces()
+    got = trace_list(got_tok.cpu().numpy(), got_off)
+    assert got == sorted(set(allt), key=lambda t: (-len(t), t))
+
+
+def test_match_small_examples(ctx):
+    # trie {abc} on stream "ababc" completes at the last token
+    tr = gen.from_text("abc")
+    trie = ctx.trie_build_traces(dev(tr), np.array([0, 3]))
+    st = gen.from_text("ababc")
+    hits = ctx.match(trie, dev(st), np.array([0, 5]))
+    assert hits.cpu().tolist() == [[0, 4, 0]]
+    # nested traces (a prefix of another) all reported (R14)
+    traces = [gen.from_text(x) for x in ("ab", "abab", "b", "ba")]
+    flat = np.concatenate(traces)
+    toff = np.cumsum([0] + [len(t) for t in traces]).astype(np.int64)
+    trie = ctx.trie_build_traces(dev(flat), toff)
+    tt, to = trie.traces()
+    streams = [gen.from_text("ababab"), gen.from_text("xbab"), gen.from_text("q")]
+    sflat = np.concatenate(streams)
+    soff = np.cumsum([0] + [len(s) for s in streams]).astype(np.int64)
+    hits = ctx.match(trie, dev(sflat), soff).cpu().numpy()
+    want, cnt = oracle.match_brute(sflat, soff, tt.cpu().numpy(), to)
+    assert np.array_equal(hits, want)
+
+
+def test_match_batch_vs_oracle(ctx):
+    tok, off, st, so = small_batch(windows=10, window=1200, seed=31)
+    min_len = 5
+    rep, roff, occ = ctx.find_repeats_batched(dev(tok), off, min_len)
+    trie = ctx.trie_build(dev(tok), off, rep, roff, min_len, 0)
+    tt, to = trie.traces()
+    hits = ctx.match(trie, dev(st), so).cpu().numpy()
+    want, cnt = oracle.match_brute(st, so, tt.cpu().numpy(), to)
+    assert cnt == len(hits)
+    assert np.array_equal(hits, want)
+
+
+def test_match_no_hits_and_empty(ctx):
+    trie = ctx.trie_build_traces(dev(np.array([1, 2, 3], np.uint64)), np.array([0, 3]))
+    hits = ctx.match(trie, dev(np.array([4, 5, 6, 1, 2], np.uint64)), np.array([0, 5]))
+    assert hits.shape[0] == 0
+    empty = ctx.trie_build_traces(torch.zeros(0, dtype=torch.uint64, device="cuda"), np.array([0]))
+    assert empty.info()[0] == 0
+    hits = ctx.match(empty, dev(np.array([4, 5], np.uint64)), np.array([0, 2]))
+    assert hits.shape[0] == 0
