@@ -5,10 +5,14 @@ path (SA + LCP + non-overlapping repeat selection, Alg. 2) on B200.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config C4|C3|C2|C5]
 
-One step = one apo_find_repeats_batched call over the whole workload batch
-(all stages: SA, LCP, candidates, ordering, greedy selection, dedup/output),
-inputs resident in HBM.  Multi-GPU (torchrun, one process per GPU): every rank
-analyses its own C4-shaped batch (weak scaling, no data-path collective); the
+One step = one pass of the whole hot path over
+one batch, inputs resident in HBM: apo_find_repeats_batched over every window
+(SA, LCP, candidates, ordering, greedy selection, dedup/output), the
+candidate trace set (apo_trie_build), and MATCH_ALL matching of every
+window's next 16,384 ops (apo_match).  Multi-GPU (torchrun, one process per
+GPU): every rank analyses its own C4-shaped batch (weak scaling); the only
+exchange is the NCCL all-gather of the candidate trace lists, after which
+every rank builds the same union trace set and matches its own streams.  The
 time is the max over ranks.  Prints ONE JSON line on rank 0.
 
 --impl reference times the CPU oracle (tier 0, the literal Alg. 2) on the
@@ -34,18 +38,19 @@ METRIC = "ops analysed/sec (SA+LCP+repeat select) at 1/2/4/8 B200; HBM GB/s vs p
 MIN_LEN = 25
 
 
-def make_workload(cfg: str, rank: int):
+def make_workload(cfg: str, rank: int, streams: bool = True):
+    """-> (tokens, offsets, match streams or None, stream offsets or None, description)"""
     from workloads import gen
     if cfg == "C4":
-        tok, off, _, _ = gen.c4(seed=4 + rank, with_streams=False)
-        desc = dict(workload="C4: batch of 4,096 independent 16,384-op windows (64 loop templates), min_len 25",
-                    windows=len(off) - 1, window=int(off[1] - off[0]), min_len=MIN_LEN,
-                    seed=4 + rank if rank else 4)
-    else:
-        S = gen.CONFIGS[cfg]["gen"]()
-        tok, off = S, np.array([0, len(S)], dtype=np.int64)
-        desc = dict(workload=f"{cfg}: single {len(S):,}-op window", windows=1, window=len(S), min_len=MIN_LEN)
-    return tok, off, desc
+        tok, off, st, so = gen.c4(seed=4 + rank, with_streams=streams)
+        desc = dict(workload="C4: batch of 4,096 independent 16,384-op windows (64 loop templates) + batched "
+                             "trace matching of the next 16,384 ops of each, min_len 25",
+                    windows=len(off) - 1, window=int(off[1] - off[0]), min_len=MIN_LEN, seed=4 + rank)
+        return tok, off, st, so, desc
+    S = gen.CONFIGS[cfg]["gen"]()
+    desc = dict(workload=f"{cfg}: single {len(S):,}-op window (analysis only)", windows=1, window=len(S),
+                min_len=MIN_LEN)
+    return S, np.array([0, len(S)], dtype=np.int64), None, None, desc
 
 
 class ClockSampler:
@@ -144,7 +149,7 @@ def cpu_baseline_sample(tok, off, budget_s: float, max_windows: int | None = Non
 def run_reference(args, rank):
     if rank != 0:
         return 0
-    tok, off, desc = make_workload(args.config, 0)
+    tok, off, _, _, desc = make_workload(args.config, 0, streams=False)
     W = len(off) - 1
     per_step = 2 if W > 1 else 1
     if W == 1 and len(tok) > 100_000:
@@ -205,18 +210,47 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2406_18111_b200.dist import gather_traces
     dev = torch.device("cuda", local)
     ctx = Context(local)
-    tok_np, off, desc = make_workload(args.config, rank)
+    tok_np, off, st_np, soff, desc = make_workload(args.config, rank)
     N = int(off[-1])
-    tok = torch.from_numpy(tok_np).to(dev)
-    cap = N // MIN_LEN + 1
     W = len(off) - 1
+    cap = N // MIN_LEN + 1
     bufs = (torch.empty((cap, 4), dtype=torch.int32, device=dev), torch.empty(W + 1, dtype=torch.int64, device=dev),
             torch.empty(cap, dtype=torch.int32, device=dev), torch.zeros(2, dtype=torch.int64, device=dev))
+    s = torch.cuda.current_stream(dev)
+    stage_names = ["analysis", "trace_set", "gather", "match"]
+    stage_ms = {k: 0.0 for k in stage_names}
+    last = {}
 
-    def step():
-        return ctx.find_repeats_batched(tok, off, MIN_LEN, sync=False, out=bufs)
+    def step(tok, streams, timed=False):
+        """One pass of the whole hot path: FindRepeats on every window, the
+        candidate trace set (+ the cross-GPU union), batched matching."""
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if timed else None
+        if timed:
+            evs[0].record(s)
+        rep, roff, occ, counts = ctx.find_repeats_batched(tok, off, MIN_LEN, sync=False, out=bufs)
+        if timed:
+            evs[1].record(s)
+        hits = None
+        if streams is not None:
+            trie = ctx.trie_build(tok, off, rep, roff, MIN_LEN, 0)
+            if timed:
+                evs[2].record(s)
+            if world > 1:
+                tt, to = trie.traces()
+                at, ao = gather_traces(tt, to)
+                trie = ctx.trie_build_traces(at, ao)
+            if timed:
+                evs[3].record(s)
+            hits = ctx.match(trie, streams, soff, cap=last.get("hits", 1 << 22))
+            last["hits"] = max(int(hits.shape[0]), 1)
+            last["traces"] = trie.info()[0]
+        if timed:
+            evs[4].record(s)
+            return evs
+        return counts, hits
 
     def barrier():
         if world > 1:
@@ -229,26 +263,34 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    tok = torch.from_numpy(tok_np).to(dev)
+    streams = torch.from_numpy(st_np).to(dev) if st_np is not None else None
     for _ in range(args.warmup):
-        step()
+        step(tok, streams)
     torch.cuda.synchronize()
 
     # ---- timed region (device events on the launching stream) ----
-    s = torch.cuda.current_stream(dev)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ctx.profile(True)
     l0 = ctx.launches
+    marks = []
     with ClockSampler(local) as clk:
         barrier()
         torch.cuda.synchronize()
         ev0.record(s)
         for _ in range(args.steps):
-            step()
+            marks.append(step(tok, streams, timed=True))
         ev1.record(s)
         torch.cuda.synchronize()
         barrier()
     launches = ctx.launches - l0
     ms = max_over_ranks(ev0.elapsed_time(ev1))
+    for ev in marks:
+        if streams is None:
+            stage_ms["analysis"] += ev[0].elapsed_time(ev[1])
+        else:
+            for k, name in enumerate(stage_names):
+                stage_ms[name] += ev[k].elapsed_time(ev[k + 1])
     ctx.profile(False)
     rp_ms, rp_n, rp_bytes = ctx.profile_read(ctx.PROF_RADIX_PASS)
     sc_ms, sc_n, _ = ctx.profile_read(ctx.PROF_SCAN)
@@ -260,22 +302,35 @@ def main():
     e2e = None
     if not args.no_e2e:
         tok_host = torch.from_numpy(tok_np).pin_memory()
-        for _ in range(1):
-            ctx.find_repeats_batched_host(tok_host, off, MIN_LEN)
+        st_host = torch.from_numpy(st_np).pin_memory() if st_np is not None else None
+
+        def e2e_step():
+            t = tok_host.to(dev, non_blocking=True)
+            q = st_host.to(dev, non_blocking=True) if st_host is not None else None
+            c, h = step(t, q)
+            r, o = (int(x) for x in c.tolist())
+            rep_h = bufs[0][:r].cpu()
+            roff_h = bufs[1].cpu()
+            occ_h = bufs[2][:o].cpu()
+            hits_h = h.cpu() if h is not None else None
+            return rep_h.numel() * 4 + roff_h.numel() * 8 + occ_h.numel() * 4 + 16 + \
+                (hits_h.numel() * 4 if hits_h is not None else 0)
+
+        e2e_step()
         torch.cuda.synchronize()
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        d2h = 0
         e0.record(s)
+        d2h = 0
         for _ in range(args.steps):
-            rep, roff, occ = ctx.find_repeats_batched_host(tok_host, off, MIN_LEN)
-            d2h = rep.numel() * 4 + roff.numel() * 8 + occ.numel() * 4 + 16
+            d2h = e2e_step()
         e1.record(s)
         torch.cuda.synchronize()
         barrier()
         ems = max_over_ranks(e0.elapsed_time(e1))
+        h2d = N * 8 + (W + 1) * 8 + (int(soff[-1]) * 8 + len(soff) * 8 if soff is not None else 0)
         e2e = {"value": N * world * args.steps / (ems / 1e3), "unit": "ops/s",
-               "h2d_bytes_per_step": N * 8 + (W + 1) * 8, "d2h_bytes_per_step": int(d2h)}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
     if rank != 0:
         if world > 1:
@@ -304,6 +359,10 @@ def main():
     desc = dict(desc)
     desc["l2"] = f"inputs ({N * 8 / 2**20:.0f} MiB of tokens per GPU) larger than the 126 MB L2; no flush"
     desc["repeats_found"] = int(counts[0])
+    if streams is not None:
+        desc["traces"] = int(last.get("traces", 0))
+        desc["match_hits"] = int(last.get("hits", 0))
+    desc["stage_ms_per_step"] = {k: round(v / args.steps, 3) for k, v in stage_ms.items()}
     out = {"metric": METRIC, "value": value, "unit": "ops/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "u64", "data": "synthetic", "config": desc,

@@ -1,0 +1,54 @@
+"""Multi-GPU plumbing: gather every rank's candidate trace list.
+
+The only data-path exchange of the sharded C4 workload:
+each rank analyses its own windows, builds its local trace set, and the
+ranks all-gather their trace lists (NCCL over NVLink on GPUs; gloo in the CPU
+tests) so that every rank builds the same union trace set
+(apo_trie_build_traces merges duplicates and orders ids by content, so the
+union is independent of the gather order and of the number of ranks).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def gather_traces(tokens: torch.Tensor, off: np.ndarray, group=None):
+    """All-gather (tokens uint64[n], host offsets int64[T+1]) from every rank.
+
+    Returns (all_tokens on tokens.device, host offsets int64[sum T + 1]) with
+    rank 0's traces first, then rank 1's, ...
+    """
+    world = dist.get_world_size(group)
+    dev = tokens.device
+    off = np.asarray(off, dtype=np.int64)
+    n_tok, n_tr = int(off[-1]), len(off) - 1
+    sizes = torch.tensor([n_tok, n_tr], dtype=torch.int64, device=dev)
+    all_sizes = torch.empty(world * 2, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(all_sizes, sizes, group=group)
+    all_sizes = all_sizes.view(world, 2).cpu().numpy()
+    max_tok = max(int(all_sizes[:, 0].max()), 1)
+    max_tr = max(int(all_sizes[:, 1].max()), 1)
+    # padded payloads (uint64 travels as its int64 bit pattern)
+    pt = torch.zeros(max_tok, dtype=torch.int64, device=dev)
+    if n_tok:
+        pt[:n_tok] = tokens[:n_tok].view(torch.int64)
+    lens = torch.zeros(max_tr, dtype=torch.int64, device=dev)
+    if n_tr:
+        lens[:n_tr] = torch.from_numpy(np.diff(off)).to(dev)
+    gt = torch.empty(world * max_tok, dtype=torch.int64, device=dev)
+    gl = torch.empty(world * max_tr, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(gt, pt, group=group)
+    dist.all_gather_into_tensor(gl, lens, group=group)
+    gt = gt.view(world, max_tok)
+    gl = gl.view(world, max_tr).cpu().numpy()
+    parts, lengths = [], []
+    for r in range(world):
+        nt, nr = int(all_sizes[r, 0]), int(all_sizes[r, 1])
+        parts.append(gt[r, :nt])
+        lengths.append(gl[r, :nr])
+    all_tok = torch.cat(parts).view(torch.uint64) if parts else torch.zeros(0, dtype=torch.uint64, device=dev)
+    all_len = np.concatenate(lengths) if lengths else np.zeros(0, np.int64)
+    all_off = np.concatenate([[0], np.cumsum(all_len)]).astype(np.int64)
+    return all_tok, all_off
