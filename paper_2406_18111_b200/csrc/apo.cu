@@ -220,6 +220,8 @@ void apo_ctx_destroy(apo_ctx *ctx) {
   cudaSetDevice(c.device);
   cudaDeviceSynchronize();
   c.arena.release();
+  c.aux.release();
+  for (auto &b : c.pool) cudaFree(b.first);
   for (auto e : c.ev_pool) cudaEventDestroy(e);
   if (c.status) cudaFree(c.status);
   if (c.counters) cudaFree(c.counters);

@@ -103,6 +103,30 @@ struct Ctx {
   int num_sms = 148;
   std::string err;
   Arena arena;  // per-call scratch
+  Arena aux;    // second per-call scratch (trie pieces, match hit keys)
+  // cached device blocks for objects that outlive a call (trie storage):
+  // reused instead of cudaMalloc/cudaFree every step
+  std::vector<std::pair<void *, size_t>> pool;
+  void *pool_get(size_t bytes) {
+    size_t best = pool.size();
+    for (size_t i = 0; i < pool.size(); ++i)
+      if (pool[i].second >= bytes && (best == pool.size() || pool[i].second < pool[best].second)) best = i;
+    if (best < pool.size()) {
+      void *p = pool[best].first;
+      pool.erase(pool.begin() + long(best));
+      return p;
+    }
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes ? bytes : 1);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      throw Error{APO_ERR_NOMEM, "device allocation failed"};
+    }
+    return p;
+  }
+  void pool_put(void *p, size_t bytes) {
+    if (p) pool.emplace_back(p, bytes);
+  }
   // persistent look-back state (zeroed once; epoch-tagged so never reset)
   u64 *status = nullptr;
   size_t status_words = 0;
@@ -156,16 +180,33 @@ __device__ __forceinline__ u64 lb_load(const u64 *p) {
 template <bool IS_MAX>
 __device__ __forceinline__ u32 lb_lookback(const u64 *status, size_t stride, size_t lane,
                                            i64 tile, u32 epoch) {
+  // Spin with ONE load on the nearest unresolved predecessor; once it has
+  // published, fetch the next seven predecessors' words together (independent
+  // loads in flight at once) so a walk over k "aggregate only" tiles costs
+  // ~k/8 dependent L2 round trips instead of k.
+  constexpr int kLB = 8;
   u32 acc = 0;
   i64 p = tile - 1;
   while (p >= 0) {
-    u64 w = lb_load(status + size_t(p) * stride + lane);
-    u32 ep = u32(w >> 34), fl = u32(w >> 32) & 3u;
+    u64 w0 = lb_load(status + size_t(p) * stride + lane);
+    u32 ep = u32(w0 >> 34), fl = u32(w0 >> 32) & 3u;
     if (ep != epoch || fl == 0) continue;  // spin until tile p publishes
-    u32 v = u32(w);
-    acc = IS_MAX ? (v > acc ? v : acc) : acc + v;
-    if (fl == kFlagInc) break;
+    acc = IS_MAX ? (u32(w0) > acc ? u32(w0) : acc) : acc + u32(w0);
+    if (fl == kFlagInc) return acc;
     --p;
+    u64 w[kLB - 1];
+#pragma unroll
+    for (int k = 0; k < kLB - 1; ++k) w[k] = (p - k >= 0) ? lb_load(status + size_t(p - k) * stride + lane) : 0ull;
+    int k = 0;
+    for (; k < kLB - 1 && p - k >= 0; ++k) {
+      ep = u32(w[k] >> 34);
+      fl = u32(w[k] >> 32) & 3u;
+      if (ep != epoch || fl == 0) break;  // not published yet: spin on it next
+      u32 v = u32(w[k]);
+      acc = IS_MAX ? (v > acc ? v : acc) : acc + v;
+      if (fl == kFlagInc) return acc;
+    }
+    p -= k;
   }
   return acc;
 }

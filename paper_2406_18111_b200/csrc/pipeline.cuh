@@ -23,6 +23,10 @@ __device__ __forceinline__ int b_wid(const Batch &b, i64 i) { return b.W == 1 ? 
 __device__ __forceinline__ i64 b_beg(const Batch &b, int w) { return b.W == 1 ? 0 : b.off[w]; }
 __device__ __forceinline__ i64 b_end(const Batch &b, int w) { return b.W == 1 ? b.N : b.off[w + 1]; }
 
+struct LevelPtrs {
+  i32 *p[40];
+};
+
 // ----- suffix array + LCP (K2 initial ranking, K3 doubling, K4 PLCP) -----
 struct SAWork {
   u64 *keys, *keys_alt;   // N
@@ -31,6 +35,7 @@ struct SAWork {
   i32 *levels[40];        // rank levels 0..R (each N)
   int max_levels;
   i32 *phi, *plcp;        // N
+  i32 *rw;                // W: rounds per window (K9 path) or nullptr
   // results
   i32 *sa;                // N (global positions, window-major suffix order)
   i32 *lcp;               // N (pair k = (k, k+1); 0 at the end of each window)
@@ -38,6 +43,9 @@ struct SAWork {
 };
 
 void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp);
+// K9: per-window on-chip doubling (windows <= 16,384 ops, not generalized).
+bool window_sa_supported(const Batch &b);
+void run_window_sa(Ctx &c, const Batch &b, SAWork &w, cudaStream_t s);
 void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s);
 
 // ----- candidate generation, ordering, greedy, output (K5-K8) -----

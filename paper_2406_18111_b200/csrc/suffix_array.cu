@@ -124,8 +124,8 @@ __device__ __forceinline__ i64 gallop_lcp(const Levels &L, int R, i64 i, i64 j, 
 
 constexpr int kPlcpChunk = 32;
 
-__global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi, Levels L, int R, Batch b,
-                       i32 *__restrict__ plcp) {
+__global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi, Levels L, int R,
+                       const i32 *__restrict__ rw, Batch b, i32 *__restrict__ plcp) {
   i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   i64 i0 = t * kPlcpChunk;
   if (i0 >= b.N) return;
@@ -133,12 +133,14 @@ __global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi,
   i64 h = -1;  // -1: no Kasai lower bound available
   int cur_w = -1;
   i64 end = 0;
+  int Rcur = R;
   for (i64 i = i0; i < i1; ++i) {
     int w = b_wid(b, i);
     if (w != cur_w) {
       cur_w = w;
       end = b_end(b, w);
       h = -1;
+      if (rw) Rcur = rw[w];  // K9 path: per-window number of rounds
     }
     i64 j = phi[i];
     if (j < 0) {
@@ -148,7 +150,7 @@ __global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi,
     }
     const i64 end_j = b.gen ? b_end(b, b_wid(b, j)) : end;
     if (h < 0) {
-      h = gallop_lcp(L, R, i, j, end, end_j);
+      h = gallop_lcp(L, Rcur, i, j, end, end_j);
     } else {
       h = h > 0 ? h - 1 : 0;
       while (i + h < end && j + h < end_j && tok[i + h] == tok[j + h]) ++h;
@@ -178,6 +180,7 @@ void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp) {
   if (w.max_levels > 40) w.max_levels = 40;
   for (int r = 0; r < w.max_levels; ++r) w.levels[r] = cv.take<i32>(N);
   w.sa = cv.take<i32>(N);
+  w.rw = window_sa_supported(b) ? cv.take<i32>(size_t(b.W)) : nullptr;
   if (want_lcp) {
     w.phi = cv.take<i32>(N);
     w.plcp = cv.take<i32>(N);
@@ -223,6 +226,11 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
     launch_scan<true>(c, N, f, s);
   }
 
+  if (w.rw != nullptr) {
+    // ---- K9: every window's doubling loop on chip ----
+    run_window_sa(c, b, w, s);
+    w.R = w.max_levels - 1;  // upper bound; the LCP stage uses the per-window count
+  } else {
   // ---- K3: doubling rounds ----
   const int lob = b.gen ? bits_for(u64(N - 1) + u64(b.W)) : bits_for(u64(b.maxwin));
   const int hib = bits_for(u64(N - 1));
@@ -248,6 +256,7 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   }
   w.R = r;
   APO_CUDA(cudaMemcpyAsync(w.sa, final_sa, sizeof(i32) * N, cudaMemcpyDeviceToDevice, s));
+  }
 
   if (!want_lcp) return;
   // ---- K4: phi, PLCP, LCP ----
@@ -255,9 +264,9 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   k_phi<<<G, T, 0, s>>>(sa, b, w.phi);
   APO_CHECK_LAUNCH();
   Levels L{};
-  for (int q = 0; q <= w.R && q < 40; ++q) L.p[q] = w.levels[q];
+  for (int q = 0; q < w.max_levels && q < 40; ++q) L.p[q] = w.levels[q];
   i64 chunks = (N + kPlcpChunk - 1) / kPlcpChunk;
-  k_plcp<<<grid_for(chunks, 128), 128, 0, s>>>(tok, w.phi, L, w.R, b, w.plcp);
+  k_plcp<<<grid_for(chunks, 128), 128, 0, s>>>(tok, w.phi, L, w.R, w.rw, b, w.plcp);
   APO_CHECK_LAUNCH();
   k_lcp_gather<<<G, T, 0, s>>>(sa, w.plcp, b, w.lcp);
   APO_CHECK_LAUNCH();

@@ -34,6 +34,7 @@ struct apo_trie {
   apo::i64 maxlen = 0;
   apo::u64 *d_tok = nullptr;  // traces in id order, back to back
   apo::i64 *d_off = nullptr;  // T+1
+  size_t tok_bytes = 0, off_bytes = 0;  // pooled blocks (returned to the context on destroy)
   std::vector<apo::i64> h_off;
 };
 
@@ -111,15 +112,6 @@ __global__ void k_copy_pieces(const u64 *__restrict__ src_tok, const i64 *__rest
 }
 
 // ------------------------------------------------ order + dedup ----
-__global__ void k_trace_keys(const i64 *__restrict__ off, i64 ntr, i64 maxlen, int bN,
-                             const i32 *__restrict__ final_rank, u64 *__restrict__ keys, u32 *__restrict__ vals) {
-  i64 w = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (w >= ntr) return;
-  i64 len = off[w + 1] - off[w];
-  keys[w] = (u64(maxlen - len) << bN) | u64(u32(final_rank[off[w]]));
-  vals[w] = u32(w);
-}
-
 // warp per sorted neighbour pair: same length and same content -> not a head
 __global__ void k_trace_heads(const u64 *__restrict__ tok, const i64 *__restrict__ off, const u32 *__restrict__ order,
                               i64 ntr, u32 *__restrict__ head) {
@@ -229,7 +221,7 @@ struct IntervalF {
 };
 
 __global__ void k_enumerate(MatchSetup m, const i64 *__restrict__ ilo, const u32 *__restrict__ ibase, i64 Z,
-                            int bE, int bT, u64 *__restrict__ keys, u32 *__restrict__ nvalid) {
+                            int bE, int bT, u64 invalid, u64 *__restrict__ keys, u32 *__restrict__ nvalid) {
   i64 z = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   bool valid = false;
   if (z < Z) {
@@ -245,7 +237,7 @@ __global__ void k_enumerate(MatchSetup m, const i64 *__restrict__ ilo, const u32
     i64 t = lo;
     i64 k = ilo[t] + (z - i64(ibase[t]));
     i64 p = m.sa[k];
-    u64 key = ~0ull;
+    u64 key = invalid;  // sorts after every hit
     if (p < m.Ns) {
       int q = m.wid[p];
       i64 L = m.off[m.S + t + 1] - m.off[m.S + t];
@@ -308,7 +300,57 @@ void upload_batch(Ctx &c, Batch &b, GenPlan &g, const std::vector<i64> &h_off, c
   b.wid = g.d_wid;
 }
 
-// Builds the trace set from pieces d_ptok / h_poff (host offsets).
+// Total order on pieces: length desc, then content (unsigned tokens, R1),
+// then piece index (indices >= n are padding and sort last).
+struct TraceCmp {
+  const u64 *tok;
+  const i64 *off;
+  i64 n;
+  __device__ __forceinline__ int cmp(u32 a, u32 b) const {
+    if (a == b) return 0;
+    const bool pa = a >= n, pb = b >= n;
+    if (pa || pb) return (pa && pb) ? (a < b ? -1 : 1) : (pa ? 1 : -1);
+    const i64 oa = off[a], ob = off[b];
+    const i64 la = off[a + 1] - oa, lb = off[b + 1] - ob;
+    if (la != lb) return la > lb ? -1 : 1;
+    for (i64 k = 0; k < la; ++k) {
+      u64 x = tok[oa + k], y = tok[ob + k];
+      if (x != y) return x < y ? -1 : 1;
+    }
+    return a < b ? -1 : 1;
+  }
+};
+
+__global__ void k_iota(u32 *__restrict__ idx, i64 n) {
+  i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) idx[i] = u32(i);
+}
+
+// one compare-exchange stage (k, j) of a bitonic sorting network
+__global__ void k_bitonic(u32 *__restrict__ idx, i64 P, i64 j, i64 k, TraceCmp c) {
+  i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  i64 l = i ^ j;
+  if (l <= i) return;
+  u32 a = idx[i], b = idx[l];
+  int r = c.cmp(a, b);
+  bool asc = (i & k) == 0;
+  if ((asc && r > 0) || (!asc && r < 0)) {
+    idx[i] = b;
+    idx[l] = a;
+  }
+}
+
+__global__ void k_src_of(const u32 *__restrict__ uniq, const i64 *__restrict__ poff, i64 T, i64 *__restrict__ src) {
+  i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < T) src[t] = poff[uniq[t]];
+}
+
+// Builds the trace set from pieces d_ptok / h_poff (host offsets): order the
+// pieces by (length desc, content lexicographic asc) with a comparison sort
+// (a bitonic network whose comparator walks the two token sequences; almost
+// every comparison ends at the first differing token), merge identical
+// neighbours, and copy the distinct traces out in id order.
 void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<i64> &h_poff, cudaStream_t s) {
   const i64 np = i64(h_poff.size()) - 1;
   const i64 N = h_poff.back();
@@ -317,27 +359,20 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
   tr->maxlen = 0;
   tr->h_off.assign(1, 0);
   if (np <= 0 || N <= 0) return;
-  Batch b;
-  b.N = N;
-  b.W = int(np);
-  b.gen = true;
-  for (i64 w = 0; w < np; ++w) b.maxwin = std::max<i64>(b.maxwin, h_poff[w + 1] - h_poff[w]);
-  const i64 maxlen = b.maxwin;
-  // plan: generalized SA (no LCP) + ordering buffers
-  GenPlan g;
-  u64 *keys, *keys_alt;
-  u32 *vals, *vals_alt, *head, *uniq;
+  i64 maxlen = 0;
+  for (i64 w = 0; w < np; ++w) maxlen = std::max<i64>(maxlen, h_poff[w + 1] - h_poff[w]);
+  i64 P = 1;
+  while (P < np) P <<= 1;
+  i64 *d_poff, *scal, *d_src;
+  u32 *order, *head, *uniq;
   i32 *ulen;
-  i64 *scal;
   auto plan = [&](Carver &cv) {
-    plan_gen(cv, b, g, false);
-    keys = cv.take<u64>(np);
-    keys_alt = cv.take<u64>(np);
-    vals = cv.take<u32>(np);
-    vals_alt = cv.take<u32>(np);
+    d_poff = cv.take<i64>(np + 1);
+    order = cv.take<u32>(P);
     head = cv.take<u32>(np);
     uniq = cv.take<u32>(np);
     ulen = cv.take<i32>(np);
+    d_src = cv.take<i64>(np);
     scal = cv.take<i64>(4);
   };
   Carver dry(nullptr);
@@ -345,18 +380,21 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
   c.arena.reserve(dry.off, s);
   Carver cv(c.arena.base);
   plan(cv);
-  upload_batch(c, b, g, h_poff, s);
-  build_sa(c, d_ptok, b, g.sa, false, s);
-  const i32 *final_rank = g.sa.levels[g.sa.R];
-  const int bN = bits_for(u64(N - 1));
-  k_trace_keys<<<grid_for(np, T256), T256, 0, s>>>(g.d_off, np, maxlen, bN, final_rank, keys, vals);
+  APO_CUDA(cudaMemcpyAsync(d_poff, h_poff.data(), sizeof(i64) * (np + 1), cudaMemcpyHostToDevice, s));
+  k_iota<<<grid_for(P, T256), T256, 0, s>>>(order, P);
   APO_CHECK_LAUNCH();
-  bool a = radix_sort_u64_u32(c, keys, vals, keys_alt, vals_alt, np, 0, bN + bits_for(u64(maxlen)), s);
-  const u32 *order = a ? vals_alt : vals;
-  k_trace_heads<<<grid_for(np * 32, T256), T256, 0, s>>>(d_ptok, g.d_off, order, np, head);
+  c.launches++;
+  TraceCmp cmp{d_ptok, d_poff, np};
+  for (i64 k = 2; k <= P; k <<= 1)
+    for (i64 j = k >> 1; j > 0; j >>= 1) {
+      k_bitonic<<<grid_for(P, T256), T256, 0, s>>>(order, P, j, k, cmp);
+      APO_CHECK_LAUNCH();
+      c.launches++;
+    }
+  k_trace_heads<<<grid_for(np * 32, T256), T256, 0, s>>>(d_ptok, d_poff, order, np, head);
   APO_CHECK_LAUNCH();
-  c.launches += 2;
-  TraceIdF f{head, order, g.d_off, uniq, ulen, np, scal};
+  c.launches++;
+  TraceIdF f{head, order, d_poff, uniq, ulen, np, scal};
   launch_scan<false>(c, np, f, s);
   const i64 T = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
   // offsets of the distinct traces (host prefix sums of the lengths)
@@ -368,23 +406,16 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
     for (i64 t = 0; t < T; ++t) h_uoff[t + 1] = h_uoff[t] + hl[t];
   }
   const i64 ntok = h_uoff[T];
-  APO_CUDA(cudaMalloc(&tr->d_tok, sizeof(u64) * std::max<i64>(ntok, 1)));
-  APO_CUDA(cudaMalloc(&tr->d_off, sizeof(i64) * (T + 1)));
+  tr->tok_bytes = sizeof(u64) * size_t(std::max<i64>(ntok, 1));
+  tr->off_bytes = sizeof(i64) * size_t(T + 1);
+  tr->d_tok = static_cast<u64 *>(c.pool_get(tr->tok_bytes));
+  tr->d_off = static_cast<i64 *>(c.pool_get(tr->off_bytes));
   APO_CUDA(cudaMemcpyAsync(tr->d_off, h_uoff.data(), sizeof(i64) * (T + 1), cudaMemcpyHostToDevice, s));
-  // source start of each distinct trace = piece offset of uniq[id]
-  i64 *d_src = reinterpret_cast<i64 *>(keys);  // reuse
-  {
-    std::vector<u32> hu(static_cast<size_t>(T));
-    APO_CUDA(cudaMemcpyAsync(hu.data(), uniq, sizeof(u32) * T, cudaMemcpyDeviceToHost, s));
-    APO_CUDA(cudaStreamSynchronize(s));
-    std::vector<i64> hs(static_cast<size_t>(T));
-    for (i64 t = 0; t < T; ++t) hs[t] = h_poff[hu[t]];
-    APO_CUDA(cudaMemcpyAsync(d_src, hs.data(), sizeof(i64) * T, cudaMemcpyHostToDevice, s));
-    k_copy_pieces<<<grid_for(T * 32, T256), T256, 0, s>>>(d_ptok, d_src, tr->d_off, T, tr->d_tok);
-    APO_CHECK_LAUNCH();
-    c.launches++;
-    APO_CUDA(cudaStreamSynchronize(s));
-  }
+  k_src_of<<<grid_for(T, T256), T256, 0, s>>>(uniq, d_poff, T, d_src);
+  k_copy_pieces<<<grid_for(T * 32, T256), T256, 0, s>>>(d_ptok, d_src, tr->d_off, T, tr->d_tok);
+  APO_CHECK_LAUNCH();
+  c.launches += 2;
+  APO_CUDA(cudaStreamSynchronize(s));
   tr->T = T;
   tr->ntok = ntok;
   tr->maxlen = maxlen;
@@ -436,21 +467,36 @@ apo_status apo_trie_build(apo_ctx *ctx, const uint64_t *d_tok, const int64_t *h_
       return;
     }
     require(d_tok != nullptr && d_rep != nullptr, "NULL device pointer");
-    // pieces
-    i64 *d_src_off = nullptr, *scal = nullptr, *p_src = nullptr, *p_off = nullptr;
-    u32 *pbase = nullptr;
-    i32 *p_len = nullptr;
-    APO_CUDA(cudaMalloc(&d_src_off, sizeof(i64) * (nwin + 1)));
-    APO_CUDA(cudaMalloc(&scal, sizeof(i64) * 4));
-    APO_CUDA(cudaMalloc(&pbase, sizeof(u32) * nrep));
+    // pieces, carved from the aux arena with upper bounds: the repeats'
+    // representative occurrences are disjoint kept intervals, so their
+    // total length is <= the batch length; each repeat yields at most
+    // ceil(length / max_len) pieces.
+    const i64 Nsrc = h_off[nwin];
+    const i64 np_max = max_len > 0 ? nrep + Nsrc / max_len + 1 : nrep;
+    i64 *d_src_off, *scal, *p_src, *p_off;
+    u32 *pbase;
+    i32 *p_len;
+    u64 *ptok;
+    auto plan = [&](Carver &cv) {
+      d_src_off = cv.take<i64>(size_t(nwin) + 1);
+      scal = cv.take<i64>(4);
+      pbase = cv.take<u32>(nrep);
+      p_src = cv.take<i64>(np_max);
+      p_len = cv.take<i32>(np_max);
+      p_off = cv.take<i64>(np_max + 1);
+      ptok = cv.take<u64>(Nsrc);
+    };
+    Carver dry(nullptr);
+    plan(dry);
+    c.aux.reserve(dry.off, s);
+    Carver cv(c.aux.base);
+    plan(cv);
     APO_CUDA(cudaMemcpyAsync(d_src_off, h_off, sizeof(i64) * (nwin + 1), cudaMemcpyHostToDevice, s));
     SrcRep sr{d_rep, d_rep_off, d_src_off, nwin, nrep, min_len, max_len};
     PieceCountF pf{sr, pbase, scal};
     launch_scan<false>(c, nrep, pf, s);
     const i64 np = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
-    APO_CUDA(cudaMalloc(&p_src, sizeof(i64) * np));
-    APO_CUDA(cudaMalloc(&p_len, sizeof(i32) * np));
-    APO_CUDA(cudaMalloc(&p_off, sizeof(i64) * (np + 1)));
+    require(np <= np_max, "piece count exceeds its bound");
     k_pieces<<<grid_for(nrep, T256), T256, 0, s>>>(sr, pbase, p_src, p_len);
     APO_CHECK_LAUNCH();
     c.launches++;
@@ -459,21 +505,12 @@ apo_status apo_trie_build(apo_ctx *ctx, const uint64_t *d_tok, const int64_t *h_
     APO_CUDA(cudaStreamSynchronize(s));
     std::vector<i64> h_poff(size_t(np) + 1, 0);
     for (i64 q = 0; q < np; ++q) h_poff[q + 1] = h_poff[q] + hl[q];
+    require(h_poff[np] <= Nsrc, "piece tokens exceed their bound");
     APO_CUDA(cudaMemcpyAsync(p_off, h_poff.data(), sizeof(i64) * (np + 1), cudaMemcpyHostToDevice, s));
-    u64 *ptok = nullptr;
-    APO_CUDA(cudaMalloc(&ptok, sizeof(u64) * std::max<i64>(h_poff[np], 1)));
     k_copy_pieces<<<grid_for(np * 32, T256), T256, 0, s>>>(d_tok, p_src, p_off, np, ptok);
     APO_CHECK_LAUNCH();
     c.launches++;
     build_trace_set(c, tr, ptok, h_poff, s);
-    APO_CUDA(cudaStreamSynchronize(s));
-    cudaFree(ptok);
-    cudaFree(p_off);
-    cudaFree(p_len);
-    cudaFree(p_src);
-    cudaFree(pbase);
-    cudaFree(scal);
-    cudaFree(d_src_off);
   });
   if (st != APO_OK) {
     apo_trie_destroy(tr);
@@ -508,9 +545,10 @@ apo_status apo_trie_build_traces(apo_ctx *ctx, const uint64_t *d_tr, const int64
 
 void apo_trie_destroy(apo_trie *tr) {
   if (!tr) return;
-  if (tr->ctx) cudaSetDevice(tr->ctx->c.device);
-  if (tr->d_tok) cudaFree(tr->d_tok);
-  if (tr->d_off) cudaFree(tr->d_off);
+  if (tr->ctx) {
+    tr->ctx->c.pool_put(tr->d_tok, tr->tok_bytes);
+    tr->ctx->c.pool_put(tr->d_off, tr->off_bytes);
+  }
   delete tr;
 }
 
@@ -603,17 +641,17 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
     const i64 Z = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
     if (Z == 0) return;
     // hit keys (invalid slots = ~0 sort last); reuse the SA key buffers when large enough
-    size_t need = sizeof(u64) * size_t(Z) * 2;
-    u64 *kbuf = nullptr;
-    APO_CUDA(cudaMalloc(&kbuf, need));
+    c.aux.reserve(sizeof(u64) * size_t(Z) * 2 + 1024, s);
+    u64 *kbuf = reinterpret_cast<u64 *>(c.aux.base);
     keys = kbuf;
     keys_alt = kbuf + Z;
     u32 *nvalid = reinterpret_cast<u32 *>(scal + 1);
-    k_enumerate<<<grid_for(Z, T256), T256, 0, s>>>(m, ilo, ibase, Z, bE, bT, keys, nvalid);
+    const int kb = bS + bE + bT;  // hit key bits; invalid slots get bit kb set
+    k_enumerate<<<grid_for(Z, T256), T256, 0, s>>>(m, ilo, ibase, Z, bE, bT, u64(1) << kb, keys, nvalid);
     APO_CHECK_LAUNCH();
     c.launches++;
     const i64 nh = i64(c.read_u32(nvalid, s));
-    bool a = radix_sort_u64_keys(c, keys, keys_alt, Z, 0, 64, s);
+    bool a = radix_sort_u64_keys(c, keys, keys_alt, Z, 0, kb + 1, s);
     const u64 *sorted = a ? keys_alt : keys;
     if (nh > 0 && cap > 0) {
       k_write_hits<<<grid_for(std::min(nh, cap), T256), T256, 0, s>>>(sorted, nh, cap, bE, bT, d_out);
@@ -622,7 +660,6 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
     }
     APO_CUDA(cudaMemcpyAsync(d_count, &nh, sizeof(i64), cudaMemcpyHostToDevice, s));
     APO_CUDA(cudaStreamSynchronize(s));
-    cudaFree(kbuf);
   });
 }
 

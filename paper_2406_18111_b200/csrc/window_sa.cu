@@ -1,0 +1,218 @@
+// window_sa.cu -- K9: prefix doubling of one window per CTA, on chip.
+//
+// For batches whose windows hold <= 16,384 ops (the C4 workload, and every
+// small single window) the whole doubling loop of a window runs inside one
+// 1024-thread CTA.  Per round:
+//   * keys (rank[i] << 15 | (i+h < n ? rank[i+h]+1 : 0), 29 bits) and
+//     positions are built from the u16 ranks held in shared memory;
+//   * four stable LSD digit passes (8,7,7,7 bits) move (key u32, position
+//     u16) between two shared-memory buffers: each warp ranks its 512 items
+//     with __match_any_sync into a per-warp u16 histogram, one block scan
+//     gives the digit starts, and every item is scattered to its slot;
+//   * a block-wide max-scan of group starts gives the new ranks;
+//   * the new level is streamed to HBM (4 B/op) for the LCP stage's galloping.
+// The loop ends per window as soon as all its ranks are distinct.  HBM
+// traffic per round is the level write only, instead of ~140 B/op for a
+// round of the global onesweep path.  The result is the same suffix array
+// (it is unique).
+#include "pipeline.cuh"
+
+namespace apo {
+
+namespace {
+
+constexpr int kWT = 1024;
+constexpr int kWWarps = kWT / 32;
+constexpr int kWItems = 16;
+constexpr int kWMax = kWT * kWItems;  // 16384
+constexpr u32 kPadKey = (1u << 29) - 1;
+
+struct WinBuf {
+  u32 key[kWMax];
+  unsigned short pos[kWMax];
+};
+
+struct WinSmem {
+  WinBuf a, b;  // ping-pong; the u16 rank array aliases b.key while a holds the items
+  unsigned short hist[kWWarps][256];
+  u32 start[256];
+  u32 scan[kWWarps];
+};
+
+__device__ __forceinline__ u32 lanemask_lt_w() {
+  u32 m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// One stable LSD digit pass: items of `src` (sorted position q = index) go to
+// `dst`.  Warp w ranks the contiguous sub-tile [w*512, w*512+512) in
+// (j, lane) order, which is index order, so the pass is stable.
+template <int SHIFT, int BITS>
+__device__ __forceinline__ void lsd_pass(const WinBuf &src, WinBuf &dst, WinSmem &S) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr u32 mask = (1u << BITS) - 1u;
+  for (int i = tid; i < kWWarps * 256; i += kWT) (&S.hist[0][0])[i] = 0;
+  __syncthreads();
+  unsigned short *wh = S.hist[warp];
+  const u32 lt = lanemask_lt_w();
+  const int base = warp * (32 * kWItems) + lane;
+  u32 rk[kWItems / 2];  // two u16 in-warp ranks per register
+#pragma unroll
+  for (int j = 0; j < kWItems; ++j) {
+    u32 d = (src.key[base + j * 32] >> SHIFT) & mask;
+    u32 peers = __match_any_sync(0xffffffffu, d);
+    u32 old = wh[d];
+    __syncwarp();
+    if (lane == __ffs(peers) - 1) wh[d] = (unsigned short)(old + __popc(peers));
+    __syncwarp();
+    u32 r = old + __popc(peers & lt);
+    if (j & 1)
+      rk[j >> 1] |= r << 16;
+    else
+      rk[j >> 1] = r;
+  }
+  __syncthreads();
+  // per digit: exclusive prefix over warps (in place) and the digit total
+  u32 total = 0;
+  if (tid < 256) {
+#pragma unroll 8
+    for (int w = 0; w < kWWarps; ++w) {
+      u32 c = S.hist[w][tid];
+      S.hist[w][tid] = (unsigned short)total;
+      total += c;
+    }
+  }
+  u32 incl = total;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    u32 v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (tid < 256 && lane == 31) S.scan[warp] = incl;
+  __syncthreads();
+  if (tid < 256) {
+    u32 pre = 0;
+    for (int w = 0; w < warp; ++w) pre += S.scan[w];
+    S.start[tid] = pre + incl - total;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kWItems; ++j) {
+    const int q = base + j * 32;
+    u32 k = src.key[q];
+    u32 d = (k >> SHIFT) & mask;
+    u32 r = (rk[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+    u32 p = S.start[d] + wh[d] + r;
+    dst.key[p] = k;
+    dst.pos[p] = src.pos[q];
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const i32 *__restrict__ level0, LevelPtrs lv,
+                                                      int max_levels, i32 *__restrict__ sa_out,
+                                                      i32 *__restrict__ rw) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WinSmem &S = *reinterpret_cast<WinSmem *>(smem_raw);
+  unsigned short *rank = reinterpret_cast<unsigned short *>(S.b.key);  // aliases b while a holds items
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int w = blockIdx.x;
+  const i64 beg = b_beg(b, w), n = b_end(b, w) - beg;
+  if (n == 0) {
+    if (tid == 0) rw[w] = 0;
+    return;
+  }
+  for (int i = tid; i < n; i += kWT) rank[i] = (unsigned short)(level0[beg + i] - beg);
+  int r = 0;
+  for (i64 h = 1;; h <<= 1) {
+    __syncthreads();
+    for (int q = tid; q < kWMax; q += kWT) {
+      u32 key = kPadKey;
+      if (q < n) {
+        u32 lo = (q + h < n) ? u32(rank[q + h]) + 1u : 0u;
+        key = (u32(rank[q]) << 15) | lo;
+      }
+      S.a.key[q] = key;
+      S.a.pos[q] = (unsigned short)q;
+    }
+    __syncthreads();
+    lsd_pass<0, 8>(S.a, S.b, S);
+    lsd_pass<8, 7>(S.b, S.a, S);
+    lsd_pass<15, 7>(S.a, S.b, S);
+    lsd_pass<22, 7>(S.b, S.a, S);
+    // S.a is sorted.  New rank of sorted position q = start of its key group
+    // (blocked max-scan; thread t owns positions [16t, 16t+16)).
+    const int q0 = tid * kWItems;
+    u32 run = 0;
+    {
+      u32 prev = q0 > 0 ? S.a.key[q0 - 1] : 0xffffffffu;
+#pragma unroll
+      for (int j = 0; j < kWItems; ++j) {
+        u32 k = S.a.key[q0 + j];
+        if (k != prev) run = u32(q0 + j);
+        prev = k;
+      }
+    }
+    u32 incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      u32 v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl = v > incl ? v : incl;
+    }
+    if (lane == 31) S.scan[warp] = incl;
+    __syncthreads();
+    u32 before = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) before = 0;
+    for (int ww = 0; ww < warp; ++ww) before = S.scan[ww] > before ? S.scan[ww] : before;
+    bool notdone = false;
+    {
+      u32 g = before;
+      u32 prev = q0 > 0 ? S.a.key[q0 - 1] : 0xffffffffu;
+#pragma unroll
+      for (int j = 0; j < kWItems; ++j) {
+        const int q = q0 + j;
+        u32 k = S.a.key[q];
+        if (k != prev) g = u32(q);
+        prev = k;
+        if (q < n) {
+          rank[S.a.pos[q]] = (unsigned short)g;
+          notdone |= (g != u32(q));
+        }
+      }
+    }
+    bool any = __syncthreads_or(notdone);
+    ++r;
+    if (r < max_levels) {
+      i32 *out = lv.p[r];
+      for (int i = tid; i < n; i += kWT) out[beg + i] = i32(rank[i]) + i32(beg);
+    }
+    if (!any || r + 1 >= max_levels) {
+      for (int q = tid; q < n; q += kWT) sa_out[beg + q] = i32(beg) + i32(S.a.pos[q]);
+      if (tid == 0) rw[w] = any ? -1 : r;  // -1: level budget exhausted (cannot happen for n <= 2^14)
+      return;
+    }
+  }
+}
+
+}  // namespace
+
+bool window_sa_supported(const Batch &b) { return !b.gen && b.maxwin <= kWMax; }
+
+void run_window_sa(Ctx &c, const Batch &b, SAWork &w, cudaStream_t s) {
+  const size_t smem = sizeof(WinSmem);
+  static bool attr = false;
+  if (!attr) {
+    APO_CUDA(cudaFuncSetAttribute(k_window_sa, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  LevelPtrs lv{};
+  for (int r = 0; r < w.max_levels && r < 40; ++r) lv.p[r] = w.levels[r];
+  if (c.prof) c.prof_begin(kProfOther, 0.0, s);
+  k_window_sa<<<b.W, kWT, smem, s>>>(b, w.levels[0], lv, w.max_levels, w.sa, w.rw);
+  APO_CHECK_LAUNCH();
+  if (c.prof) c.prof_end(s);
+  c.launches++;
+}
+
+}  // namespace apo
