@@ -129,6 +129,13 @@ apo_status apo_candidates(apo_ctx *ctx, const uint64_t *d_tok, int32_t n, int32_
                           int32_t *d_len, int32_t *d_id, int32_t *d_start, uint8_t *d_kept,
                           int64_t cap, int64_t *d_count, void *stream);
 
+/* K1, the LSD radix sort every sort of the path runs on (SA rounds P:552,
+ * "Sort(C)" P:574-575): stable sort of (d_keys[i], d_vals[i]) pairs by key
+ * bits [begin_bit, end_bit), in place.  d_vals may be NULL (keys only).
+ * Exposed for parity tests and kernel benchmarks. */
+apo_status apo_radix_sort(apo_ctx *ctx, uint64_t *d_keys, uint32_t *d_vals, int64_t n,
+                          int32_t begin_bit, int32_t end_bit, void *stream);
+
 /* ---------------------------------------------------------------------- */
 /* FindRepeats (Alg. 2) -- the north_star call                              */
 /* ---------------------------------------------------------------------- */

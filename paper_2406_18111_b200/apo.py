@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libapo.so")
+LIB_PATH = os.environ.get("APO_LIB", os.path.join(_HERE, "libapo.so"))
 
 APO_OK, APO_ERR_INVALID, APO_ERR_CAPACITY, APO_ERR_NOMEM, APO_ERR_CUDA = range(5)
 _STATUS = {0: "APO_OK", 1: "APO_ERR_INVALID", 2: "APO_ERR_CAPACITY", 3: "APO_ERR_NOMEM", 4: "APO_ERR_CUDA"}
@@ -52,6 +52,7 @@ _SIGS = {
     "apo_profile": (ctypes.c_int, [_VP, ctypes.c_int]),
     "apo_profile_read": (ctypes.c_int, [_VP, ctypes.c_int, ctypes.POINTER(ctypes.c_double), _P_I64,
                                         ctypes.POINTER(ctypes.c_double)]),
+    "apo_radix_sort": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I32, _I32, _VP]),
     "apo_suffix_array": (ctypes.c_int, [_VP, _VP, _I32, _VP, _VP, _VP]),
     "apo_suffix_array_batched": (ctypes.c_int, [_VP, _VP, _P_I64, _I32, _VP, _VP, _VP]),
     "apo_candidates": (ctypes.c_int, [_VP, _VP, _I32, _I32, _VP, _VP, _VP, _VP, _I64, _VP, _VP]),
@@ -165,6 +166,18 @@ class Context:
         k = ctypes.c_int64()
         self._raise(self.lib.apo_profile_read(self.h, int(kind), ctypes.byref(ms), ctypes.byref(k), ctypes.byref(by)))
         return ms.value, k.value, by.value
+
+    # ------------------------------------------------------------------ K1 --
+    def radix_sort(self, keys: torch.Tensor, vals: torch.Tensor | None = None, begin_bit: int = 0,
+                   end_bit: int = 64):
+        """Stable in-place sort of (uint64 keys, uint32/int32 values) by key bits [begin, end)."""
+        if not keys.is_cuda or keys.dtype not in (torch.uint64, torch.int64) or not keys.is_contiguous():
+            raise ValueError("keys must be a contiguous CUDA uint64 tensor")
+        if vals is not None and (vals.numel() != keys.numel() or vals.element_size() != 4 or not vals.is_contiguous()):
+            raise ValueError("vals must be a contiguous 32-bit tensor of the same length")
+        self._raise(self.lib.apo_radix_sort(self.h, _ptr(keys), _ptr(vals), keys.numel(), int(begin_bit), int(end_bit),
+                                            _stream(self.device)))
+        return keys, vals
 
     # ---------------------------------------------------------- SA / LCP --
     def suffix_array(self, tok: torch.Tensor, lcp: bool = True):

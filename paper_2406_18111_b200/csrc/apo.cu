@@ -293,6 +293,32 @@ apo_status apo_suffix_array_batched(apo_ctx *ctx, const uint64_t *d_tok, const i
   return sa_common(ctx, d_tok, h_off, nwin, d_sa, d_lcp, stream);
 }
 
+apo_status apo_radix_sort(apo_ctx *ctx, uint64_t *d_keys, uint32_t *d_vals, int64_t n, int32_t begin_bit,
+                          int32_t end_bit, void *stream) {
+  return guarded(ctx, [&](Ctx &c) {
+    require(n >= 0 && begin_bit >= 0 && end_bit <= 64 && begin_bit <= end_bit, "invalid argument");
+    require(n < (i64(1) << 32), "n must be < 2^32");
+    if (n <= 1 || begin_bit == end_bit) return;
+    require(d_keys != nullptr, "NULL device pointer");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    u64 *ka;
+    u32 *va = nullptr;
+    Carver dry(nullptr);
+    dry.take<u64>(n);
+    if (d_vals) dry.take<u32>(n);
+    c.arena.reserve(dry.off, s);
+    Carver cv(c.arena.base);
+    ka = cv.take<u64>(n);
+    if (d_vals) va = cv.take<u32>(n);
+    bool alt = d_vals ? radix_sort_u64_u32(c, d_keys, d_vals, ka, va, n, begin_bit, end_bit, s)
+                      : radix_sort_u64_keys(c, d_keys, ka, n, begin_bit, end_bit, s);
+    if (alt) {
+      APO_CUDA(cudaMemcpyAsync(d_keys, ka, sizeof(u64) * n, cudaMemcpyDeviceToDevice, s));
+      if (d_vals) APO_CUDA(cudaMemcpyAsync(d_vals, va, sizeof(u32) * n, cudaMemcpyDeviceToDevice, s));
+    }
+  });
+}
+
 apo_status apo_candidates(apo_ctx *ctx, const uint64_t *d_tok, int32_t n, int32_t min_len, int32_t *d_len,
                           int32_t *d_id, int32_t *d_start, uint8_t *d_kept, int64_t cap, int64_t *d_count,
                           void *stream) {

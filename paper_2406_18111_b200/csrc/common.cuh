@@ -190,7 +190,10 @@ __device__ __forceinline__ u32 lb_lookback(const u64 *status, size_t stride, siz
   while (p >= 0) {
     u64 w0 = lb_load(status + size_t(p) * stride + lane);
     u32 ep = u32(w0 >> 34), fl = u32(w0 >> 32) & 3u;
-    if (ep != epoch || fl == 0) continue;  // spin until tile p publishes
+    if (ep != epoch || fl == 0) {  // spin (with backoff) until tile p publishes
+      __nanosleep(32);
+      continue;
+    }
     acc = IS_MAX ? (u32(w0) > acc ? u32(w0) : acc) : acc + u32(w0);
     if (fl == kFlagInc) return acc;
     --p;

@@ -7,7 +7,7 @@
 //     positions are built from the u16 ranks held in shared memory;
 //   * four stable LSD digit passes (8,7,7,7 bits) move (key u32, position
 //     u16) between two shared-memory buffers: each warp ranks its 512 items
-//     with __match_any_sync into a per-warp u16 histogram, one block scan
+//     (peer masks from ballots) into a per-warp u16 histogram, one block scan
 //     gives the digit starts, and every item is scattered to its slot;
 //   * a block-wide max-scan of group starts gives the new ranks;
 //   * the new level is streamed to HBM (4 B/op) for the LCP stage's galloping.
@@ -39,6 +39,18 @@ struct WinSmem {
   u32 scan[kWWarps];
 };
 
+template <int BITS>
+__device__ __forceinline__ u32 peers_ballot_w(u32 d) {
+  u32 peers = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const u32 m = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? m : ~m;
+  }
+  return peers;
+}
+
 __device__ __forceinline__ u32 lanemask_lt_w() {
   u32 m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -61,7 +73,7 @@ __device__ __forceinline__ void lsd_pass(const WinBuf &src, WinBuf &dst, WinSmem
 #pragma unroll
   for (int j = 0; j < kWItems; ++j) {
     u32 d = (src.key[base + j * 32] >> SHIFT) & mask;
-    u32 peers = __match_any_sync(0xffffffffu, d);
+    u32 peers = peers_ballot_w<BITS>(d);
     u32 old = wh[d];
     __syncwarp();
     if (lane == __ffs(peers) - 1) wh[d] = (unsigned short)(old + __popc(peers));
