@@ -155,100 +155,110 @@ struct TraceIdF {
 };
 
 // ---------------------------------------------------------- matching ----
-__global__ void k_rmq_level_t(const i32 *__restrict__ prev, i32 *__restrict__ next, i64 n, i64 half) {
-  i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  i32 x = prev[k];
-  if (k + half < n) {
-    i32 y = prev[k + half];
-    x = y < x ? y : x;
-  }
-  next[k] = x;
-}
-
-struct Sparse {
-  const i32 *lv[32];
-  int levels;
-};
-
-// maximal rank interval [lo, hi] around r with LCP >= L between neighbours
-__device__ __forceinline__ void lcp_interval(const Sparse &sp, i64 n, i64 r, i32 L, i64 &lo, i64 &hi) {
-  // left: largest jump such that min LCP[lo-2^j .. lo-1] >= L
-  i64 a = r;
-  for (int j = sp.levels - 1; j >= 0; --j) {
-    i64 w = i64(1) << j;
-    if (a - w >= 0 && sp.lv[j][a - w] >= L) a -= w;
-  }
-  i64 b = r;  // right: min LCP[b .. b+2^j-1] >= L  (LCP[k] links k and k+1)
-  for (int j = sp.levels - 1; j >= 0; --j) {
-    i64 w = i64(1) << j;
-    if (b + w <= n - 1 && sp.lv[j][b] >= L) b += w;
-  }
-  lo = a;
-  hi = b;
-}
-
 struct MatchSetup {
-  Sparse sp;
-  i64 N, Ns;             // total positions, stream positions
+  i64 N;                 // stream positions
   int S;                 // streams
   i64 T;                 // traces
-  const i64 *off;        // combined offsets (streams then traces)
+  const i64 *off;        // stream offsets (device)
   const i32 *wid;
-  const i32 *final_rank;
-  const i32 *sa;
+  const i32 *sa;         // generalized suffix array of the streams
+  const u64 *tok;        // stream tokens
+  const u64 *ttok;       // trace tokens (id order)
+  const i64 *toff;       // trace offsets (device)
 };
 
-struct IntervalF {
-  MatchSetup m;
-  i64 *ilo;
-  u32 *ibase;
-  i64 *total;
-  __device__ u32 load(i64 t) const {
-    i64 p = m.off[m.S + t];
-    i32 L = i32(m.off[m.S + t + 1] - p);
-    i64 lo, hi;
-    lcp_interval(m.sp, m.N, m.final_rank[p], L, lo, hi);
-    ilo[t] = lo;
-    return u32(hi - lo + 1);
+// Compare trace t[0..L) with the stream suffix at p (ending at e), from
+// offset `from` (known equal prefix).  Returns 0 if t is a prefix of the
+// suffix, <0 if t sorts before it, >0 if after (a suffix that ends first is
+// smaller, reading R2); *lcp receives the matched length.
+__device__ __forceinline__ int cmp_trace_suffix(const u64 *__restrict__ S, i64 p, i64 e, const u64 *__restrict__ t,
+                                                i64 L, i64 from, i64 *lcp) {
+  for (i64 k = from; k < L; ++k) {
+    if (p + k >= e) {
+      *lcp = k;
+      return 1;
+    }
+    const u64 x = t[k], y = S[p + k];
+    if (x != y) {
+      *lcp = k;
+      return x < y ? -1 : 1;
+    }
   }
-  __device__ bool store(i64 t, u32 incl, u32 excl) const {
-    ibase[t] = excl;
-    if (t == m.T - 1) *total = i64(incl);
+  *lcp = L;
+  return 0;
+}
+
+// First suffix rank r in [0, N) with cmp(t, s_r) <= 0 (STRICT = false: the
+// first suffix that has t as a prefix or sorts after t) or < 0 (STRICT =
+// true: the first suffix after every suffix that has t as a prefix).
+// Manber-Myers binary search: comparisons start at min(lcp with the two
+// bracketing suffixes), so a search costs O(|t| + log N) token reads in
+// the usual case.
+template <bool STRICT>
+__device__ __forceinline__ i64 trace_bound(const MatchSetup &m, const u64 *t, i64 L) {
+  i64 lo = -1, hi = m.N, llo = 0, lhi = 0;
+  while (hi - lo > 1) {
+    const i64 mid = lo + ((hi - lo) >> 1);
+    const i64 p = m.sa[mid];
+    const i64 e = m.off[m.wid[p] + 1];
+    i64 l;
+    const int c = cmp_trace_suffix(m.tok, p, e, t, L, llo < lhi ? llo : lhi, &l);
+    if (STRICT ? (c < 0) : (c <= 0)) {
+      hi = mid;
+      lhi = l;
+    } else {
+      lo = mid;
+      llo = l;
+    }
+  }
+  return hi;
+}
+
+// Each trace's interval of stream suffixes that start with it.
+__global__ void k_trace_search(MatchSetup m, i64 *__restrict__ ilo, u32 *__restrict__ icnt) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= m.T) return;
+  const u64 *tt = m.ttok + m.toff[t];
+  const i64 L = m.toff[t + 1] - m.toff[t];
+  const i64 a = trace_bound<false>(m, tt, L);
+  const i64 b = trace_bound<true>(m, tt, L);
+  ilo[t] = a;
+  icnt[t] = u32(b - a);
+}
+
+struct CountScanF {
+  const u32 *cnt;
+  u32 *base;
+  i64 n;
+  i64 *total;
+  __device__ u32 load(i64 i) const { return cnt[i]; }
+  __device__ bool store(i64 i, u32 incl, u32 excl) const {
+    base[i] = excl;
+    if (i == n - 1) *total = i64(incl);
     return false;
   }
   __device__ u32 *flag() const { return nullptr; }
 };
 
 __global__ void k_enumerate(MatchSetup m, const i64 *__restrict__ ilo, const u32 *__restrict__ ibase, i64 Z,
-                            int bE, int bT, u64 invalid, u64 *__restrict__ keys, u32 *__restrict__ nvalid) {
+                            int bE, int bT, u64 *__restrict__ keys) {
   i64 z = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  bool valid = false;
-  if (z < Z) {
-    // trace owning slot z: last t with ibase[t] <= z
-    i64 lo = 0, hi = m.T - 1;
-    while (lo < hi) {
-      i64 mid = (lo + hi + 1) >> 1;
-      if (i64(ibase[mid]) <= z)
-        lo = mid;
-      else
-        hi = mid - 1;
-    }
-    i64 t = lo;
-    i64 k = ilo[t] + (z - i64(ibase[t]));
-    i64 p = m.sa[k];
-    u64 key = invalid;  // sorts after every hit
-    if (p < m.Ns) {
-      int q = m.wid[p];
-      i64 L = m.off[m.S + t + 1] - m.off[m.S + t];
-      i64 end = p - m.off[q] + L - 1;
-      key = (u64(q) << (bE + bT)) | (u64(end) << bT) | u64(t);
-      valid = true;
-    }
-    keys[z] = key;
+  if (z >= Z) return;
+  // trace owning slot z: last t with ibase[t] <= z
+  i64 lo = 0, hi = m.T - 1;
+  while (lo < hi) {
+    i64 mid = (lo + hi + 1) >> 1;
+    if (i64(ibase[mid]) <= z)
+      lo = mid;
+    else
+      hi = mid - 1;
   }
-  unsigned b = __ballot_sync(0xffffffffu, valid);
-  if ((threadIdx.x & 31) == 0 && b) atomicAdd(nvalid, u32(__popc(b)));
+  const i64 t = lo;
+  const i64 p = m.sa[ilo[t] + (z - i64(ibase[t]))];
+  const int q = m.wid[p];
+  const i64 L = m.toff[t + 1] - m.toff[t];
+  const i64 end = p - m.off[q] + L - 1;
+  keys[z] = (u64(q) << (bE + bT)) | (u64(end) << bT) | u64(t);
 }
 
 __global__ void k_write_hits(const u64 *__restrict__ keys, i64 nhits, i64 cap, int bE, int bT,
@@ -590,30 +600,24 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
     if (tr->T == 0 || Ns == 0) return;
     require(d_streams != nullptr, "NULL device pointer");
     const i64 T = tr->T;
-    const i64 N = Ns + tr->ntok;
-    require(N < (i64(1) << 31) - 1, "streams + traces longer than 2^31-1 tokens");
+    require(Ns < (i64(1) << 31) - 1, "streams longer than 2^31-1 tokens");
     const int bT = bits_for(u64(T - 1)), bE = bits_for(u64(maxs - 1)), bS = bits_for(u64(nstreams - 1));
-    require(bT + bE + bS <= 63, "match key does not fit 63 bits");
-    std::vector<i64> h_all(size_t(nstreams) + size_t(T) + 1);
-    for (int q = 0; q <= nstreams; ++q) h_all[q] = h_off[q];
-    for (i64 t = 1; t <= T; ++t) h_all[nstreams + t] = Ns + tr->h_off[t];
+    require(bT + bE + bS <= 64, "match key does not fit 64 bits");
+    std::vector<i64> h_s(h_off, h_off + nstreams + 1);
+    // one generalized suffix array over the streams (no LCP needed)
     Batch b;
-    b.N = N;
-    b.W = int(nstreams + T);
+    b.N = Ns;
+    b.W = nstreams;
     b.gen = true;
-    b.maxwin = std::max<i64>(maxs, tr->maxlen);
+    b.maxwin = maxs;
     GenPlan g;
-    u64 *tok = nullptr, *keys = nullptr, *keys_alt = nullptr;
     i64 *ilo = nullptr, *scal = nullptr;
-    u32 *ibase = nullptr;
-    i32 *sp_lv[32] = {};
-    const int levels = bits_for(u64(N));
+    u32 *ibase = nullptr, *icnt = nullptr;
     auto plan = [&](Carver &cv) {
-      plan_gen(cv, b, g, true);
-      tok = cv.take<u64>(N);
-      for (int j = 1; j < levels; ++j) sp_lv[j] = cv.take<i32>(N);
+      plan_gen(cv, b, g, false);
       ilo = cv.take<i64>(T);
       ibase = cv.take<u32>(T);
+      icnt = cv.take<u32>(T);
       scal = cv.take<i64>(4);
     };
     Carver dry(nullptr);
@@ -621,39 +625,27 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
     c.arena.reserve(dry.off, s);
     Carver cv(c.arena.base);
     plan(cv);
-    APO_CUDA(cudaMemcpyAsync(tok, d_streams, sizeof(u64) * Ns, cudaMemcpyDeviceToDevice, s));
-    APO_CUDA(cudaMemcpyAsync(tok + Ns, tr->d_tok, sizeof(u64) * tr->ntok, cudaMemcpyDeviceToDevice, s));
-    upload_batch(c, b, g, h_all, s);
-    build_sa(c, tok, b, g.sa, true, s);
-    Sparse sp{};
-    sp.levels = levels;
-    sp.lv[0] = g.sa.lcp;
-    for (int j = 1; j < levels; ++j) {
-      k_rmq_level_t<<<grid_for(N, T256), T256, 0, s>>>(sp.lv[j - 1], sp_lv[j], N, i64(1) << (j - 1));
-      APO_CHECK_LAUNCH();
-      c.launches++;
-      sp.lv[j] = sp_lv[j];
-    }
-    MatchSetup m{sp, N, Ns, nstreams, T, g.d_off, g.d_wid, g.sa.levels[g.sa.R], g.sa.sa};
-    APO_CUDA(cudaMemsetAsync(scal, 0, sizeof(i64) * 4, s));
-    IntervalF itf{m, ilo, ibase, scal};
-    launch_scan<false>(c, T, itf, s);
-    const i64 Z = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
-    if (Z == 0) return;
-    // hit keys (invalid slots = ~0 sort last); reuse the SA key buffers when large enough
-    c.aux.reserve(sizeof(u64) * size_t(Z) * 2 + 1024, s);
-    u64 *kbuf = reinterpret_cast<u64 *>(c.aux.base);
-    keys = kbuf;
-    keys_alt = kbuf + Z;
-    u32 *nvalid = reinterpret_cast<u32 *>(scal + 1);
-    const int kb = bS + bE + bT;  // hit key bits; invalid slots get bit kb set
-    k_enumerate<<<grid_for(Z, T256), T256, 0, s>>>(m, ilo, ibase, Z, bE, bT, u64(1) << kb, keys, nvalid);
+    upload_batch(c, b, g, h_s, s);
+    build_sa(c, d_streams, b, g.sa, false, s);
+    MatchSetup m{Ns, nstreams, T, g.d_off, g.d_wid, g.sa.sa, d_streams, tr->d_tok, tr->d_off};
+    k_trace_search<<<grid_for(T, 128), 128, 0, s>>>(m, ilo, icnt);
     APO_CHECK_LAUNCH();
     c.launches++;
-    const i64 nh = i64(c.read_u32(nvalid, s));
-    bool a = radix_sort_u64_keys(c, keys, keys_alt, Z, 0, kb + 1, s);
+    APO_CUDA(cudaMemsetAsync(scal, 0, sizeof(i64) * 4, s));
+    CountScanF cf{icnt, ibase, T, scal};
+    launch_scan<false>(c, T, cf, s);
+    const i64 nh = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
+    if (nh == 0) return;
+    c.aux.reserve(sizeof(u64) * size_t(nh) * 2 + 1024, s);
+    u64 *keys = reinterpret_cast<u64 *>(c.aux.base);
+    u64 *keys_alt = keys + nh;
+    k_enumerate<<<grid_for(nh, T256), T256, 0, s>>>(m, ilo, ibase, nh, bE, bT, keys);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+    const int kb = bS + bE + bT;
+    bool a = radix_sort_u64_keys(c, keys, keys_alt, nh, 0, kb, s);
     const u64 *sorted = a ? keys_alt : keys;
-    if (nh > 0 && cap > 0) {
+    if (cap > 0) {
       k_write_hits<<<grid_for(std::min(nh, cap), T256), T256, 0, s>>>(sorted, nh, cap, bE, bT, d_out);
       APO_CHECK_LAUNCH();
       c.launches++;
