@@ -167,21 +167,30 @@ struct MatchSetup {
   const i64 *toff;       // trace offsets (device)
 };
 
-// Compare trace t[0..L) with the stream suffix at p (ending at e), from
-// offset `from` (known equal prefix).  Returns 0 if t is a prefix of the
-// suffix, <0 if t sorts before it, >0 if after (a suffix that ends first is
-// smaller, reading R2); *lcp receives the matched length.
-__device__ __forceinline__ int cmp_trace_suffix(const u64 *__restrict__ S, i64 p, i64 e, const u64 *__restrict__ t,
-                                                i64 L, i64 from, i64 *lcp) {
-  for (i64 k = from; k < L; ++k) {
-    if (p + k >= e) {
-      *lcp = k;
-      return 1;
+// Warp-cooperative comparison of trace t[0..L) with the stream suffix at p
+// (ending at e), from offset `from` (a known equal prefix), 32 tokens per
+// step.  Returns 0 if t is a prefix of the suffix, <0 if t sorts before it,
+// >0 if after (a suffix that ends first is smaller, reading R2); *lcp gets
+// the matched length.  All lanes return the same values.
+__device__ __forceinline__ int warp_cmp_trace_suffix(const u64 *__restrict__ S, i64 p, i64 e,
+                                                     const u64 *__restrict__ t, i64 L, i64 from, i64 *lcp) {
+  const int lane = threadIdx.x & 31;
+  for (i64 base = from; base < L; base += 32) {
+    const i64 k = base + lane;
+    int res = 0;
+    if (k < L) {
+      if (p + k >= e) {
+        res = 1;
+      } else {
+        const u64 x = t[k], y = S[p + k];
+        res = x == y ? 0 : (x < y ? -1 : 1);
+      }
     }
-    const u64 x = t[k], y = S[p + k];
-    if (x != y) {
-      *lcp = k;
-      return x < y ? -1 : 1;
+    const u32 m = __ballot_sync(0xffffffffu, res != 0);
+    if (m) {
+      const int f = __ffs(m) - 1;
+      *lcp = base + f;
+      return __shfl_sync(0xffffffffu, res, f);
     }
   }
   *lcp = L;
@@ -192,8 +201,7 @@ __device__ __forceinline__ int cmp_trace_suffix(const u64 *__restrict__ S, i64 p
 // first suffix that has t as a prefix or sorts after t) or < 0 (STRICT =
 // true: the first suffix after every suffix that has t as a prefix).
 // Manber-Myers binary search: comparisons start at min(lcp with the two
-// bracketing suffixes), so a search costs O(|t| + log N) token reads in
-// the usual case.
+// bracketing suffixes).  One warp per search.
 template <bool STRICT>
 __device__ __forceinline__ i64 trace_bound(const MatchSetup &m, const u64 *t, i64 L) {
   i64 lo = -1, hi = m.N, llo = 0, lhi = 0;
@@ -202,7 +210,7 @@ __device__ __forceinline__ i64 trace_bound(const MatchSetup &m, const u64 *t, i6
     const i64 p = m.sa[mid];
     const i64 e = m.off[m.wid[p] + 1];
     i64 l;
-    const int c = cmp_trace_suffix(m.tok, p, e, t, L, llo < lhi ? llo : lhi, &l);
+    const int c = warp_cmp_trace_suffix(m.tok, p, e, t, L, llo < lhi ? llo : lhi, &l);
     if (STRICT ? (c < 0) : (c <= 0)) {
       hi = mid;
       lhi = l;
@@ -214,16 +222,18 @@ __device__ __forceinline__ i64 trace_bound(const MatchSetup &m, const u64 *t, i6
   return hi;
 }
 
-// Each trace's interval of stream suffixes that start with it.
+// Each trace's interval of stream suffixes that start with it (warp per trace).
 __global__ void k_trace_search(MatchSetup m, i64 *__restrict__ ilo, u32 *__restrict__ icnt) {
-  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 t = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (t >= m.T) return;
   const u64 *tt = m.ttok + m.toff[t];
   const i64 L = m.toff[t + 1] - m.toff[t];
   const i64 a = trace_bound<false>(m, tt, L);
   const i64 b = trace_bound<true>(m, tt, L);
-  ilo[t] = a;
-  icnt[t] = u32(b - a);
+  if ((threadIdx.x & 31) == 0) {
+    ilo[t] = a;
+    icnt[t] = u32(b - a);
+  }
 }
 
 struct CountScanF {
@@ -311,10 +321,13 @@ void upload_batch(Ctx &c, Batch &b, GenPlan &g, const std::vector<i64> &h_off, c
 }
 
 // Total order on pieces: length desc, then content (unsigned tokens, R1),
-// then piece index (indices >= n are padding and sort last).
+// then piece index (indices >= n are padding and sort last).  The first three
+// tokens come from compact prefix-key arrays, so most comparisons never touch
+// the token array.
 struct TraceCmp {
   const u64 *tok;
   const i64 *off;
+  const u64 *pk;  // pk[3*i + j] = token j of piece i (j < min(3, len))
   i64 n;
   __device__ __forceinline__ int cmp(u32 a, u32 b) const {
     if (a == b) return 0;
@@ -323,7 +336,12 @@ struct TraceCmp {
     const i64 oa = off[a], ob = off[b];
     const i64 la = off[a + 1] - oa, lb = off[b + 1] - ob;
     if (la != lb) return la > lb ? -1 : 1;
-    for (i64 k = 0; k < la; ++k) {
+    const i64 np = la < 3 ? la : 3;
+    for (i64 k = 0; k < np; ++k) {
+      u64 x = pk[3 * i64(a) + k], y = pk[3 * i64(b) + k];
+      if (x != y) return x < y ? -1 : 1;
+    }
+    for (i64 k = 3; k < la; ++k) {
       u64 x = tok[oa + k], y = tok[ob + k];
       if (x != y) return x < y ? -1 : 1;
     }
@@ -331,9 +349,9 @@ struct TraceCmp {
   }
 };
 
-__global__ void k_iota(u32 *__restrict__ idx, i64 n) {
+__global__ void k_iota_list(const u32 *__restrict__ list, i64 U, u32 *__restrict__ idx, i64 P, u32 pad) {
   i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) idx[i] = u32(i);
+  if (i < P) idx[i] = i < U ? list[i] : pad + u32(i);
 }
 
 // one compare-exchange stage (k, j) of a bitonic sorting network
@@ -351,16 +369,88 @@ __global__ void k_bitonic(u32 *__restrict__ idx, i64 P, i64 j, i64 k, TraceCmp c
   }
 }
 
+__device__ __forceinline__ u64 mix64(u64 z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// warp per piece: a position-keyed content hash (only used to bring equal
+// contents together; equality is always verified token by token) and the
+// piece's first three tokens.  keys = (maxlen - len) << 0 handled by a
+// second sort; here keys[i] = hash, vals[i] = i.
+__global__ void k_piece_hash(const u64 *__restrict__ tok, const i64 *__restrict__ off, i64 np,
+                             u64 *__restrict__ hkey, u32 *__restrict__ hval, u64 *__restrict__ pk) {
+  const i64 p = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= np) return;
+  const i64 o = off[p], L = off[p + 1] - o;
+  u64 h = 0;
+  for (i64 k = lane; k < L; k += 32) h += mix64(tok[o + k] ^ mix64(u64(k) + 0x9E3779B97F4A7C15ull));
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) h += __shfl_xor_sync(0xffffffffu, h, d);
+  if (lane == 0) {
+    hkey[p] = h;
+    hval[p] = u32(p);
+  }
+  if (lane < 3) pk[3 * p + lane] = lane < L ? tok[o + lane] : 0ull;
+}
+
+__global__ void k_len_keys(const u32 *__restrict__ order, const i64 *__restrict__ off, i64 np, i64 maxlen,
+                           u64 *__restrict__ keys) {
+  i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= np) return;
+  const u32 p = order[c];
+  keys[c] = u64(maxlen - (off[p + 1] - off[p]));
+}
+
+// warp per neighbour pair in (length, hash) order: 1 = keep (first of its
+// content), 0 = exact duplicate of the previous piece
+__global__ void k_dup_keep(const u64 *__restrict__ tok, const i64 *__restrict__ off, const u32 *__restrict__ order,
+                           const u64 *__restrict__ hk, i64 np, u32 *__restrict__ keep) {
+  const i64 c = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= np) return;
+  if (c == 0) {
+    if (lane == 0) keep[0] = 1;
+    return;
+  }
+  const u32 a = order[c - 1], b = order[c];
+  const i64 la = off[a + 1] - off[a], lb = off[b + 1] - off[b];
+  bool same = la == lb && hk[a] == hk[b];
+  for (i64 k = lane; same && k < la; k += 32) same = __all_sync(__activemask(), tok[off[a] + k] == tok[off[b] + k]);
+  same = __shfl_sync(0xffffffffu, same ? 1 : 0, 0) != 0;
+  if (lane == 0) keep[c] = same ? 0u : 1u;
+}
+
+struct CompactF {
+  const u32 *keepf;
+  const u32 *order;
+  u32 *out;
+  i64 n;
+  i64 *total;
+  __device__ u32 load(i64 i) const { return keepf[i]; }
+  __device__ bool store(i64 i, u32 incl, u32 excl) const {
+    if (incl != excl) out[excl] = order[i];
+    if (i == n - 1) *total = i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
 __global__ void k_src_of(const u32 *__restrict__ uniq, const i64 *__restrict__ poff, i64 T, i64 *__restrict__ src) {
   i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t < T) src[t] = poff[uniq[t]];
 }
 
-// Builds the trace set from pieces d_ptok / h_poff (host offsets): order the
-// pieces by (length desc, content lexicographic asc) with a comparison sort
-// (a bitonic network whose comparator walks the two token sequences; almost
-// every comparison ends at the first differing token), merge identical
-// neighbours, and copy the distinct traces out in id order.
+// Builds the trace set from pieces d_ptok / h_poff (host offsets):
+//  1. merge identical pieces: radix-sort by (length, content hash), verify
+//     neighbours token by token, keep the first of each content;
+//  2. order the distinct pieces by (length desc, content lexicographic asc)
+//     with a bitonic comparison network (comparisons almost always end within
+//     the three prefix tokens kept in a compact array);
+//  3. an exact neighbour comparison in that order (catches any content that
+//     step 1 left split by a hash collision), ids, copy-out in id order.
 void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<i64> &h_poff, cudaStream_t s) {
   const i64 np = i64(h_poff.size()) - 1;
   const i64 N = h_poff.back();
@@ -374,10 +464,19 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
   i64 P = 1;
   while (P < np) P <<= 1;
   i64 *d_poff, *scal, *d_src;
-  u32 *order, *head, *uniq;
+  u32 *order, *head, *uniq, *hv, *hv_alt, *keep, *surv;
+  u64 *hk, *hk_alt, *hk_keep, *pk;
   i32 *ulen;
   auto plan = [&](Carver &cv) {
     d_poff = cv.take<i64>(np + 1);
+    hk = cv.take<u64>(np);
+    hk_alt = cv.take<u64>(np);
+    hk_keep = cv.take<u64>(np);
+    hv = cv.take<u32>(np);
+    hv_alt = cv.take<u32>(np);
+    pk = cv.take<u64>(3 * np);
+    keep = cv.take<u32>(np);
+    surv = cv.take<u32>(np);
     order = cv.take<u32>(P);
     head = cv.take<u32>(np);
     uniq = cv.take<u32>(np);
@@ -391,21 +490,44 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
   Carver cv(c.arena.base);
   plan(cv);
   APO_CUDA(cudaMemcpyAsync(d_poff, h_poff.data(), sizeof(i64) * (np + 1), cudaMemcpyHostToDevice, s));
-  k_iota<<<grid_for(P, T256), T256, 0, s>>>(order, P);
+  // 1. merge identical pieces
+  k_piece_hash<<<grid_for(np * 32, T256), T256, 0, s>>>(d_ptok, d_poff, np, hk, hv, pk);
+  APO_CHECK_LAUNCH();
+  APO_CUDA(cudaMemcpyAsync(hk_keep, hk, sizeof(u64) * np, cudaMemcpyDeviceToDevice, s));
+  bool a1 = radix_sort_u64_u32(c, hk, hv, hk_alt, hv_alt, np, 0, 64, s);
+  u64 *k1 = a1 ? hk_alt : hk;
+  u32 *o1 = a1 ? hv_alt : hv;
+  u64 *k2 = a1 ? hk : hk_alt;
+  u32 *o2 = a1 ? hv : hv_alt;
+  k_len_keys<<<grid_for(np, T256), T256, 0, s>>>(o1, d_poff, np, maxlen, k1);
+  APO_CHECK_LAUNCH();
+  bool a2 = radix_sort_u64_u32(c, k1, o1, k2, o2, np, 0, bits_for(u64(maxlen)), s);
+  const u32 *by_hash = a2 ? o2 : o1;
+  k_dup_keep<<<grid_for(np * 32, T256), T256, 0, s>>>(d_ptok, d_poff, by_hash, hk_keep, np, keep);
+  APO_CHECK_LAUNCH();
+  c.launches += 3;
+  CompactF cf{keep, by_hash, surv, np, scal};
+  launch_scan<false>(c, np, cf, s);
+  const i64 U = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
+  // 2. lexicographic order of the distinct pieces
+  i64 PU = 1;
+  while (PU < U) PU <<= 1;
+  k_iota_list<<<grid_for(PU, T256), T256, 0, s>>>(surv, U, order, PU, u32(np));
   APO_CHECK_LAUNCH();
   c.launches++;
-  TraceCmp cmp{d_ptok, d_poff, np};
-  for (i64 k = 2; k <= P; k <<= 1)
+  TraceCmp cmp{d_ptok, d_poff, pk, np};
+  for (i64 k = 2; k <= PU; k <<= 1)
     for (i64 j = k >> 1; j > 0; j >>= 1) {
-      k_bitonic<<<grid_for(P, T256), T256, 0, s>>>(order, P, j, k, cmp);
+      k_bitonic<<<grid_for(PU, T256), T256, 0, s>>>(order, PU, j, k, cmp);
       APO_CHECK_LAUNCH();
       c.launches++;
     }
-  k_trace_heads<<<grid_for(np * 32, T256), T256, 0, s>>>(d_ptok, d_poff, order, np, head);
+  // 3. exact neighbour check, ids
+  k_trace_heads<<<grid_for(U * 32, T256), T256, 0, s>>>(d_ptok, d_poff, order, U, head);
   APO_CHECK_LAUNCH();
   c.launches++;
-  TraceIdF f{head, order, d_poff, uniq, ulen, np, scal};
-  launch_scan<false>(c, np, f, s);
+  TraceIdF f{head, order, d_poff, uniq, ulen, U, scal};
+  launch_scan<false>(c, U, f, s);
   const i64 T = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
   // offsets of the distinct traces (host prefix sums of the lengths)
   std::vector<i64> h_uoff(size_t(T) + 1, 0);
@@ -628,7 +750,7 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
     upload_batch(c, b, g, h_s, s);
     build_sa(c, d_streams, b, g.sa, false, s);
     MatchSetup m{Ns, nstreams, T, g.d_off, g.d_wid, g.sa.sa, d_streams, tr->d_tok, tr->d_off};
-    k_trace_search<<<grid_for(T, 128), 128, 0, s>>>(m, ilo, icnt);
+    k_trace_search<<<grid_for(T * 32, 256), 256, 0, s>>>(m, ilo, icnt);
     APO_CHECK_LAUNCH();
     c.launches++;
     APO_CUDA(cudaMemsetAsync(scal, 0, sizeof(i64) * 4, s));
