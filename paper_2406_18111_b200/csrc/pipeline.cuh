@@ -17,6 +17,11 @@ struct Batch {
   // its own sentinel $_w, $_0 < $_1 < ... < every token) instead of one
   // suffix array per window.  Used by the trie build and the matcher.
   bool gen = false;
+  // Stop prefix doubling once suffixes are ordered by their first
+  // `sort_depth` tokens (0 = fully sorted).  Suffixes still tied then share
+  // that prefix; the matcher, which only compares against traces no longer
+  // than sort_depth, cannot tell them apart.  Not valid with LCP.
+  i64 sort_depth = 0;
 };
 
 __device__ __forceinline__ int b_wid(const Batch &b, i64 i) { return b.W == 1 ? 0 : b.wid[i]; }
@@ -36,6 +41,10 @@ struct SAWork {
   int max_levels;
   i32 *phi, *plcp;        // N
   i32 *rw;                // W: rounds per window (K9 path) or nullptr
+  u32 *ids;               // N dense token ids (K2 hash path)
+  bool ids_valid;
+  char *ht_scratch;       // hash-table scratch of dense_token_ids
+  u32 ht_cap;
   // results
   i32 *sa;                // N (global positions, window-major suffix order)
   i32 *lcp;               // N (pair k = (k, k+1); 0 at the end of each window)
@@ -43,6 +52,10 @@ struct SAWork {
 };
 
 void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp);
+// K2 (hash path): dense order-preserving token ids; returns K or -1 when
+// the distinct count exceeds cap / 2.
+size_t token_ids_scratch_bytes(i64 n, u32 cap);
+i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scratch, cudaStream_t s);
 // K9: per-window on-chip doubling (windows <= 16,384 ops, not generalized).
 bool window_sa_supported(const Batch &b);
 void run_window_sa(Ctx &c, const Batch &b, SAWork &w, cudaStream_t s);

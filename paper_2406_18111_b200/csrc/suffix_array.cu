@@ -67,6 +67,27 @@ struct InitRankF {
   __device__ u32 *flag() const { return nullptr; }
 };
 
+__global__ void k_count_ids(const u32 *__restrict__ ids, i64 n, u32 *__restrict__ cnt) {
+  i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) atomicAdd(&cnt[ids[i]], 1u);
+}
+
+struct ExclF {  // in-place exclusive sum
+  u32 *a;
+  __device__ u32 load(i64 i) const { return a[i]; }
+  __device__ bool store(i64 i, u32, u32 excl) const {
+    a[i] = excl;
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+__global__ void k_rank_from_ids(const u32 *__restrict__ ids, i64 n, const u32 *__restrict__ start,
+                                i32 *__restrict__ rank) {
+  i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) rank[i] = i32(start[ids[i]]);
+}
+
 __global__ void k_double_keys(const i32 *__restrict__ rank, Batch b, i64 h, int lob, u64 *__restrict__ keys,
                               u32 *__restrict__ vals) {
   i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -181,6 +202,11 @@ void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp) {
   for (int r = 0; r < w.max_levels; ++r) w.levels[r] = cv.take<i32>(N);
   w.sa = cv.take<i32>(N);
   w.rw = window_sa_supported(b) ? cv.take<i32>(size_t(b.W)) : nullptr;
+  w.ids = cv.take<u32>(N);
+  w.ids_valid = false;
+  w.ht_cap = 1u << 21;  // up to 1M distinct tokens; 24 MB of L2-friendly tables
+  while (w.ht_cap > 4096 && u64(w.ht_cap) > 4 * u64(N)) w.ht_cap >>= 1;
+  w.ht_scratch = cv.take<char>(token_ids_scratch_bytes(N, w.ht_cap));
   if (want_lcp) {
     w.phi = cv.take<i32>(N);
     w.plcp = cv.take<i32>(N);
@@ -197,7 +223,31 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   w.R = 0;
   if (N == 0) return;
 
-  // ---- K2: level-0 ranks (group start in (window, token) order) ----
+  // ---- K2: level-0 ranks ----
+  // Dense token ids from the hash table whenever the level-0 ranks do not
+  // depend on the window (generalized mode, a single window) or K9 computes
+  // its window-local ranks itself; otherwise (or if the vocabulary is too
+  // large) the 64-bit radix sort of (token, position).
+  w.ids_valid = false;
+  if (b.gen || b.W == 1 || w.rw != nullptr) {
+    const i64 K = dense_token_ids(c, tok, N, w.ids, w.ht_cap, w.ht_scratch, s);
+    if (K >= 0) {
+      w.ids_valid = true;
+      if (w.rw == nullptr) {
+        // group start of a token = number of positions holding smaller tokens
+        u32 *cnt = w.vals;  // K <= N counters, then exclusive starts in place
+        APO_CUDA(cudaMemsetAsync(cnt, 0, sizeof(u32) * K, s));
+        k_count_ids<<<G, T, 0, s>>>(w.ids, N, cnt);
+        APO_CHECK_LAUNCH();
+        ExclF ef{cnt};
+        launch_scan<false>(c, K, ef, s);
+        k_rank_from_ids<<<G, T, 0, s>>>(w.ids, N, cnt, w.levels[0]);
+        APO_CHECK_LAUNCH();
+        c.launches += 2;
+      }
+    }
+  }
+  if (!w.ids_valid) {
   k_init_pairs<<<G, T, 0, s>>>(tok, N, w.keys, w.vals);
   APO_CHECK_LAUNCH();
   c.launches++;
@@ -225,6 +275,7 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
     InitRankF f{tok_sorted, sv, (b.W > 1 && !b.gen) ? b.wid : nullptr, w.levels[0]};
     launch_scan<true>(c, N, f, s);
   }
+  }
 
   if (w.rw != nullptr) {
     // ---- K9: every window's doubling loop on chip ----
@@ -236,7 +287,7 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   const int hib = bits_for(u64(N - 1));
   if (lob + hib > 64) throw Error{APO_ERR_INVALID, "batch too large for 64-bit doubling keys"};
   u32 *notdone = reinterpret_cast<u32 *>(c.d_misc);
-  const u32 *final_sa = sv;
+  const u32 *final_sa = nullptr;  // set by the first round (there is always one)
   int r = 0;
   for (i64 h = 1;; h <<= 1) {
     if (r + 1 >= w.max_levels) throw Error{APO_ERR_INVALID, "prefix doubling exceeded its level budget"};
@@ -252,6 +303,7 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
     ++r;
     final_sa = sa;
     if (c.read_u32(notdone, s) == 0) break;
+    if (b.sort_depth > 0 && 2 * h >= b.sort_depth) break;  // ordered deeply enough
     if (h > b.maxwin) throw Error{APO_ERR_CUDA, "prefix doubling did not converge"};
   }
   w.R = r;

@@ -1,0 +1,149 @@
+// token_ids.cu -- K2: dense, order-preserving ids of the distinct tokens.
+//
+// ids[i] in [0, K) with ids[i] < ids[j] iff tok[i] < tok[j] (unsigned, R1).
+// The op-hash streams of the paper's workloads reuse a small vocabulary (a
+// loop body's task kinds), so instead of radix-sorting all N 64-bit tokens
+// (8 passes over N) the distinct values are collected in an open-addressing
+// hash table sized to stay L2-resident, only those K values are sorted, and
+// every position maps to its value's rank: two passes over N plus a sort of
+// K << N keys.  When the table would exceed its budget the caller falls back
+// to the full sort.
+#include "pipeline.cuh"
+
+namespace apo {
+
+namespace {
+
+constexpr u64 kEmpty = ~0ull;  // the token value ~0 itself is handled aside
+
+__device__ __forceinline__ u64 ht_mix(u64 z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// ids[i] <- table slot of tok[i] (cap = the ~0 token); counts new keys.
+__global__ void k_ht_insert(const u64 *__restrict__ tok, i64 n, u64 *__restrict__ table, u32 cap, u32 *__restrict__ ids,
+                            u32 *__restrict__ nkeys, u32 *__restrict__ flags) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u64 key = tok[i];
+  if (key == kEmpty) {
+    ids[i] = cap;
+    flags[0] = 1;  // the ~0 token occurs
+    return;
+  }
+  u32 h = u32(ht_mix(key)) & (cap - 1);
+  for (u32 probe = 0; probe < cap; ++probe) {
+    u64 cur = table[h];
+    if (cur == key) {
+      ids[i] = h;
+      return;
+    }
+    if (cur == kEmpty) {
+      u64 old = atomicCAS(reinterpret_cast<unsigned long long *>(&table[h]), kEmpty, key);
+      if (old == kEmpty) {
+        u32 k = atomicAdd(nkeys, 1u);
+        if (k + 1 > cap / 2) flags[1] = 1;  // over budget: caller retries or falls back
+        ids[i] = h;
+        return;
+      }
+      if (old == key) {
+        ids[i] = h;
+        return;
+      }
+    }
+    h = (h + 1) & (cap - 1);
+  }
+  flags[1] = 1;
+}
+
+struct HtCompactF {
+  const u64 *table;
+  u64 *keys;
+  u32 *slots;
+  i64 n;
+  i64 *total;
+  __device__ u32 load(i64 i) const { return table[i] != kEmpty ? 1u : 0u; }
+  __device__ bool store(i64 i, u32 incl, u32 excl) const {
+    if (incl != excl) {
+      keys[excl] = table[i];
+      slots[excl] = u32(i);
+    }
+    if (i == n - 1) *total = i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+__global__ void k_slot_rank(const u32 *__restrict__ slots_sorted, i64 K, u32 *__restrict__ slot_rank) {
+  const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r < K) slot_rank[slots_sorted[r]] = u32(r);
+}
+
+__global__ void k_ids_from_slots(u32 *__restrict__ ids, i64 n, const u32 *__restrict__ slot_rank) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) ids[i] = slot_rank[ids[i]];
+}
+
+}  // namespace
+
+size_t token_ids_scratch_bytes(i64 n, u32 cap) {
+  Carver cv(nullptr);
+  cv.take<u64>(cap);        // table
+  cv.take<u32>(cap + 1);    // slot -> rank
+  cv.take<u64>(cap / 2);    // distinct keys
+  cv.take<u64>(cap / 2);    // ... alt
+  cv.take<u32>(cap / 2);    // slots
+  cv.take<u32>(cap / 2);    // ... alt
+  cv.take<u32>(8);          // counters / flags
+  cv.take<i64>(2);
+  (void)n;
+  return cv.off;
+}
+
+// Returns K (number of distinct tokens) or -1 if more than cap/2 distinct
+// tokens were found (ids are then undefined).  `scratch` must hold
+// token_ids_scratch_bytes(n, cap) bytes.
+i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scratch, cudaStream_t s) {
+  Carver cv(scratch);
+  u64 *table = cv.take<u64>(cap);
+  u32 *slot_rank = cv.take<u32>(cap + 1);
+  u64 *dk = cv.take<u64>(cap / 2), *dk_alt = cv.take<u64>(cap / 2);
+  u32 *ds = cv.take<u32>(cap / 2), *ds_alt = cv.take<u32>(cap / 2);
+  u32 *cnt = cv.take<u32>(8);
+  i64 *tot = cv.take<i64>(2);
+  APO_CUDA(cudaMemsetAsync(table, 0xff, sizeof(u64) * cap, s));
+  APO_CUDA(cudaMemsetAsync(cnt, 0, sizeof(u32) * 8, s));
+  k_ht_insert<<<grid_for(n, 256), 256, 0, s>>>(tok, n, table, cap, ids, cnt, cnt + 1);
+  APO_CHECK_LAUNCH();
+  c.launches++;
+  APO_CUDA(cudaMemcpyAsync(c.h_flag, cnt, sizeof(u32) * 3, cudaMemcpyDeviceToHost, s));
+  APO_CUDA(cudaStreamSynchronize(s));
+  const u32 nkeys = c.h_flag[0], has_max = c.h_flag[1], over = c.h_flag[2];
+  if (over) return -1;
+  HtCompactF f{table, dk, ds, i64(cap), tot};
+  launch_scan<false>(c, i64(cap), f, s);
+  i64 K = nkeys;
+  if (K > 1) {
+    bool a = radix_sort_u64_u32(c, dk, ds, dk_alt, ds_alt, K, 0, 64, s);
+    if (a) ds = ds_alt;
+  }
+  if (K > 0) {
+    k_slot_rank<<<grid_for(K, 256), 256, 0, s>>>(ds, K, slot_rank);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+  }
+  if (has_max) {  // the token ~0 is the largest value
+    const u32 r = u32(K);
+    APO_CUDA(cudaMemcpyAsync(slot_rank + cap, &r, sizeof(u32), cudaMemcpyHostToDevice, s));
+    ++K;
+  }
+  k_ids_from_slots<<<grid_for(n, 256), 256, 0, s>>>(ids, n, slot_rank);
+  APO_CHECK_LAUNCH();
+  c.launches++;
+  APO_CUDA(cudaStreamSynchronize(s));  // `r` above lives on the host stack
+  return K;
+}
+
+}  // namespace apo

@@ -732,6 +732,7 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
     b.W = nstreams;
     b.gen = true;
     b.maxwin = maxs;
+    b.sort_depth = tr->maxlen;  // binary search compares at most maxlen tokens
     GenPlan g;
     i64 *ilo = nullptr, *scal = nullptr;
     u32 *ibase = nullptr, *icnt = nullptr;

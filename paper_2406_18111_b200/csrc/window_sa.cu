@@ -122,22 +122,93 @@ __device__ __forceinline__ void lsd_pass(const WinBuf &src, WinBuf &dst, WinSmem
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const i32 *__restrict__ level0, LevelPtrs lv,
+// Sort the items in S.a (keys < 2^29, positions) with four LSD passes, then
+// set rank[pos] = start of the item's key group (blocked max-scan; thread t
+// owns sorted positions [16t, 16t+16)).  Returns true if some group still
+// has more than one member.
+__device__ __forceinline__ bool sort_and_rank(WinSmem &S, unsigned short *rank, i64 n) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  lsd_pass<0, 8>(S.a, S.b, S);
+  lsd_pass<8, 7>(S.b, S.a, S);
+  lsd_pass<15, 7>(S.a, S.b, S);
+  lsd_pass<22, 7>(S.b, S.a, S);
+  const int q0 = tid * kWItems;
+  u32 run = 0;
+  {
+    u32 prev = q0 > 0 ? S.a.key[q0 - 1] : 0xffffffffu;
+#pragma unroll
+    for (int j = 0; j < kWItems; ++j) {
+      u32 k = S.a.key[q0 + j];
+      if (k != prev) run = u32(q0 + j);
+      prev = k;
+    }
+  }
+  u32 incl = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    u32 v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = v > incl ? v : incl;
+  }
+  if (lane == 31) S.scan[warp] = incl;
+  __syncthreads();
+  u32 before = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) before = 0;
+  for (int ww = 0; ww < warp; ++ww) before = S.scan[ww] > before ? S.scan[ww] : before;
+  bool notdone = false;
+  u32 g = before;
+  u32 prev = q0 > 0 ? S.a.key[q0 - 1] : 0xffffffffu;
+#pragma unroll
+  for (int j = 0; j < kWItems; ++j) {
+    const int q = q0 + j;
+    u32 k = S.a.key[q];
+    if (k != prev) g = u32(q);
+    prev = k;
+    if (q < n) {
+      rank[S.a.pos[q]] = (unsigned short)g;
+      notdone |= (g != u32(q));
+    }
+  }
+  return __syncthreads_or(notdone);
+}
+
+// ids: dense token ids (level 0 is computed here: window-local group starts
+// of the tokens), or nullptr to take level 0 from levels[0].
+__global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__restrict__ ids, LevelPtrs lv,
                                                       int max_levels, i32 *__restrict__ sa_out,
                                                       i32 *__restrict__ rw) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WinSmem &S = *reinterpret_cast<WinSmem *>(smem_raw);
   unsigned short *rank = reinterpret_cast<unsigned short *>(S.b.key);  // aliases b while a holds items
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int w = blockIdx.x;
   const i64 beg = b_beg(b, w), n = b_end(b, w) - beg;
   if (n == 0) {
     if (tid == 0) rw[w] = 0;
     return;
   }
-  for (int i = tid; i < n; i += kWT) rank[i] = (unsigned short)(level0[beg + i] - beg);
+  bool any;
+  if (ids != nullptr) {
+    // level 0: sort the window's token ids on chip
+    for (int q = tid; q < kWMax; q += kWT) {
+      S.a.key[q] = q < n ? ids[beg + q] : kPadKey;
+      S.a.pos[q] = (unsigned short)q;
+    }
+    __syncthreads();
+    any = sort_and_rank(S, rank, n);
+    i32 *out = lv.p[0];
+    for (int i = tid; i < n; i += kWT) out[beg + i] = i32(rank[i]) + i32(beg);
+  } else {
+    const i32 *level0 = lv.p[0];
+    for (int i = tid; i < n; i += kWT) rank[i] = (unsigned short)(level0[beg + i] - beg);
+    any = true;
+  }
   int r = 0;
   for (i64 h = 1;; h <<= 1) {
+    if (!any) {  // already distinct (e.g. all tokens different)
+      for (int q = tid; q < n; q += kWT) sa_out[beg + q] = i32(beg) + i32(S.a.pos[q]);
+      if (tid == 0) rw[w] = r;
+      return;
+    }
     __syncthreads();
     for (int q = tid; q < kWMax; q += kWT) {
       u32 key = kPadKey;
@@ -149,59 +220,14 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const i32 *__rest
       S.a.pos[q] = (unsigned short)q;
     }
     __syncthreads();
-    lsd_pass<0, 8>(S.a, S.b, S);
-    lsd_pass<8, 7>(S.b, S.a, S);
-    lsd_pass<15, 7>(S.a, S.b, S);
-    lsd_pass<22, 7>(S.b, S.a, S);
-    // S.a is sorted.  New rank of sorted position q = start of its key group
-    // (blocked max-scan; thread t owns positions [16t, 16t+16)).
-    const int q0 = tid * kWItems;
-    u32 run = 0;
-    {
-      u32 prev = q0 > 0 ? S.a.key[q0 - 1] : 0xffffffffu;
-#pragma unroll
-      for (int j = 0; j < kWItems; ++j) {
-        u32 k = S.a.key[q0 + j];
-        if (k != prev) run = u32(q0 + j);
-        prev = k;
-      }
-    }
-    u32 incl = run;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      u32 v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl = v > incl ? v : incl;
-    }
-    if (lane == 31) S.scan[warp] = incl;
-    __syncthreads();
-    u32 before = __shfl_up_sync(0xffffffffu, incl, 1);
-    if (lane == 0) before = 0;
-    for (int ww = 0; ww < warp; ++ww) before = S.scan[ww] > before ? S.scan[ww] : before;
-    bool notdone = false;
-    {
-      u32 g = before;
-      u32 prev = q0 > 0 ? S.a.key[q0 - 1] : 0xffffffffu;
-#pragma unroll
-      for (int j = 0; j < kWItems; ++j) {
-        const int q = q0 + j;
-        u32 k = S.a.key[q];
-        if (k != prev) g = u32(q);
-        prev = k;
-        if (q < n) {
-          rank[S.a.pos[q]] = (unsigned short)g;
-          notdone |= (g != u32(q));
-        }
-      }
-    }
-    bool any = __syncthreads_or(notdone);
+    any = sort_and_rank(S, rank, n);
     ++r;
     if (r < max_levels) {
       i32 *out = lv.p[r];
       for (int i = tid; i < n; i += kWT) out[beg + i] = i32(rank[i]) + i32(beg);
     }
-    if (!any || r + 1 >= max_levels) {
-      for (int q = tid; q < n; q += kWT) sa_out[beg + q] = i32(beg) + i32(S.a.pos[q]);
-      if (tid == 0) rw[w] = any ? -1 : r;  // -1: level budget exhausted (cannot happen for n <= 2^14)
+    if (r + 1 >= max_levels && any) {  // level budget exhausted (cannot happen for n <= 2^14)
+      if (tid == 0) rw[w] = -1;
       return;
     }
   }
@@ -221,7 +247,7 @@ void run_window_sa(Ctx &c, const Batch &b, SAWork &w, cudaStream_t s) {
   LevelPtrs lv{};
   for (int r = 0; r < w.max_levels && r < 40; ++r) lv.p[r] = w.levels[r];
   if (c.prof) c.prof_begin(kProfOther, 0.0, s);
-  k_window_sa<<<b.W, kWT, smem, s>>>(b, w.levels[0], lv, w.max_levels, w.sa, w.rw);
+  k_window_sa<<<b.W, kWT, smem, s>>>(b, w.ids_valid ? w.ids : nullptr, lv, w.max_levels, w.sa, w.rw);
   APO_CHECK_LAUNCH();
   if (c.prof) c.prof_end(s);
   c.launches++;
