@@ -133,8 +133,11 @@ struct Levels {
 // lcp(i, j) (i < end_i, j < end_j) by galloping over rank levels R-1..0:
 // equal level-r ranks <=> equal 2^r-token prefixes (padded with the end
 // marker of the suffix's own window).
-__device__ __forceinline__ i64 gallop_lcp(const Levels &L, int R, i64 i, i64 j, i64 end_i, i64 end_j) {
-  i64 l = 0;
+__device__ __forceinline__ i64 gallop_lcp(const Levels &L, int R, i64 i, i64 j, i64 end_i, i64 end_j,
+                                          i64 from) {
+  // from: a known lower bound of the lcp; lcp - from < 2^R, so descending
+  // powers of two from 2^(R-1) reach it exactly
+  i64 l = from;
   for (int r = R - 1; r >= 0; --r) {
     if (i + l >= end_i || j + l >= end_j) break;
     const i32 *lv = L.p[r];
@@ -144,6 +147,7 @@ __device__ __forceinline__ i64 gallop_lcp(const Levels &L, int R, i64 i, i64 j, 
 }
 
 constexpr int kPlcpChunk = 32;
+constexpr int kKasaiSteps = 16;
 
 __global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi, Levels L, int R,
                        const i32 *__restrict__ rw, Batch b, i32 *__restrict__ plcp) {
@@ -171,10 +175,21 @@ __global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi,
     }
     const i64 end_j = b.gen ? b_end(b, b_wid(b, j)) : end;
     if (h < 0) {
-      h = gallop_lcp(L, Rcur, i, j, end, end_j);
+      h = gallop_lcp(L, Rcur, i, j, end, end_j, 0);
     } else {
+      // Kasai: PLCP[i] >= PLCP[i-1] - 1.  Extend by direct comparison for a
+      // few tokens; a longer extension (after a sharp drop) is finished by
+      // galloping from the current bound, so no thread walks thousands of
+      // tokens one at a time.
       h = h > 0 ? h - 1 : 0;
-      while (i + h < end && j + h < end_j && tok[i + h] == tok[j + h]) ++h;
+      int steps = 0;
+      while (i + h < end && j + h < end_j && tok[i + h] == tok[j + h]) {
+        ++h;
+        if (++steps == kKasaiSteps) {
+          h = gallop_lcp(L, Rcur, i, j, end, end_j, h);
+          break;
+        }
+      }
     }
     plcp[i] = i32(h);
   }
