@@ -235,31 +235,45 @@ inline int grid_for(i64 n, int per_block, int cap = 1 << 30) {
 // Op: sum (IS_MAX=false) or max (IS_MAX=true).  One launch, one pass over
 // the data, tiles claimed in order through an atomic counter.
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
-constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;  // 4096
 
 template <bool IS_MAX>
 __device__ __forceinline__ u32 scan_op(u32 a, u32 b) {
   return IS_MAX ? (a > b ? a : b) : a + b;
 }
 
+// F::load and F::store are called in a warp-STRIPED order (consecutive
+// threads touch consecutive elements, so the functors' own memory accesses
+// coalesce); the values are transposed through shared memory so each thread
+// scans a contiguous run of kScanItems elements.
 template <bool IS_MAX, class F>
-__global__ void __launch_bounds__(kScanThreads) k_scan(i64 n, F f, u64 *status, u32 *counter,
-                                                       u32 epoch) {
+__global__ void __launch_bounds__(kScanThreads) k_scan(i64 n, F f, u64 *status, u32 *counter, u32 epoch) {
+  // one pad word per 16 keeps both the striped and the blocked accesses
+  // bank-conflict free
+  __shared__ u32 s_v[kScanTile + kScanTile / 16];  // values
+  __shared__ u32 s_e[kScanTile + kScanTile / 16];  // exclusive prefixes
   __shared__ u32 s_warp[kScanThreads / 32];
   __shared__ u32 s_prefix;
   __shared__ u32 s_tile;
   if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
   __syncthreads();
   const i64 tile = s_tile;
-  const i64 base = tile * kScanTile + i64(threadIdx.x) * kScanItems;
-  u32 v[kScanItems];
-  u32 local = 0;
+  const i64 tbase = tile * kScanTile;
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
-    i64 i = base + j;
-    v[j] = i < n ? f.load(i) : 0u;
-    local = scan_op<IS_MAX>(local, v[j]);
+    const int q = j * kScanThreads + threadIdx.x;
+    const i64 i = tbase + q;
+    s_v[q + (q >> 4)] = i < n ? f.load(i) : 0u;
+  }
+  __syncthreads();
+  u32 w[kScanItems];
+  u32 local = 0;
+  const int b0 = threadIdx.x * kScanItems;
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    w[j] = s_v[b0 + j + ((b0 + j) >> 4)];
+    local = scan_op<IS_MAX>(local, w[j]);
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   u32 incl = local;
@@ -271,8 +285,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(i64 n, F f, u64 *status, 
   if (lane == 31) s_warp[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    u32 w = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
-    u32 wi = w;
+    u32 x = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
+    u32 wi = x;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       u32 o = __shfl_up_sync(0xffffffffu, wi, d);
@@ -294,17 +308,25 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(i64 n, F f, u64 *status, 
     }
   }
   __syncthreads();
-  // exclusive prefix of this thread
+  // exclusive prefix of each element back into shared memory (blocked)
   u32 warp_excl_in = __shfl_up_sync(0xffffffffu, incl, 1);
   if (lane == 0) warp_excl_in = 0;
   u32 run = scan_op<IS_MAX>(scan_op<IS_MAX>(s_prefix, s_warp[warp]), warp_excl_in);
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    s_e[b0 + j + ((b0 + j) >> 4)] = run;  // exclusive prefix of element b0 + j
+    run = scan_op<IS_MAX>(run, w[j]);
+  }
+  __syncthreads();
   bool any = false;
 #pragma unroll
   for (int j = 0; j < kScanItems; ++j) {
-    i64 i = base + j;
-    u32 nx = scan_op<IS_MAX>(run, v[j]);
-    if (i < n) any |= f.store(i, nx, run);
-    run = nx;
+    const int q = j * kScanThreads + threadIdx.x;
+    const i64 i = tbase + q;
+    if (i < n) {
+      const u32 ex = s_e[q + (q >> 4)];
+      any |= f.store(i, scan_op<IS_MAX>(ex, s_v[q + (q >> 4)]), ex);
+    }
   }
   u32 *fl = f.flag();
   if (fl != nullptr) {

@@ -766,7 +766,9 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
     APO_CHECK_LAUNCH();
     c.launches++;
     const int kb = bS + bE + bT;
-    bool a = radix_sort_u64_keys(c, keys, keys_alt, nh, 0, kb, s);
+    // hits were enumerated in trace-id order, so a STABLE sort on the
+    // (stream, end) bits alone leaves equal (stream, end) in trace order
+    bool a = radix_sort_u64_keys(c, keys, keys_alt, nh, bT, kb, s);
     const u64 *sorted = a ? keys_alt : keys;
     if (cap > 0) {
       k_write_hits<<<grid_for(std::min(nh, cap), T256), T256, 0, s>>>(sorted, nh, cap, bE, bT, d_out);

@@ -21,7 +21,7 @@ def main():
     shutil.copytree(src, tmp)
     shutil.copytree(os.path.join(ROOT, "include"), os.path.join(base, "include"))
     for spec in sys.argv[2:]:
-        f, old, new = spec.split("::")
+        f, old, new = spec.split("@@") if "@@" in spec else spec.split("::")
         p = os.path.join(tmp, f)
         s = open(p).read()
         assert old in s, (f, old)
