@@ -24,6 +24,10 @@
 //    position (the paper's marked-array test).  firstcov(x) comes
 //    from a reverse sparse table (two atomicMin per interval, then a pull-down
 //    over levels); coverage from a +/-1 difference array and a scan.
+//    For batches of small windows (<= 16,384 ops) the paper's own sequential
+//    loop is faster: one warp per window walks the window's sorted
+//    candidates with the marked array as a shared-memory bitset
+//    (k_greedy_window), every window at once.
 // K8 dedup/output (R10, R11).
 #include "pipeline.cuh"
 
@@ -302,6 +306,74 @@ __global__ void k_emit_cands(Batch b, const i32 *__restrict__ cl, const i32 *__r
   if (kept) kept[c] = state[c] == 1 ? 1 : 0;
 }
 
+// K7 for batches of small windows: the sequential greedy of P:576-583 with
+// the marked array of P:613-619, one WARP per window.  The window's
+// candidates are contiguous in the sorted order; the marks are a bitset in
+// shared memory (kGreedyMaxWin bits); a candidate is kept iff the bits of
+// its first and last positions are clear, then the warp sets its interval's
+// bits 32 words at a time.  Candidates are staged 32 at a time by the warp.
+constexpr int kGreedyMaxWin = 16384;
+constexpr int kGreedyWarps = 8;
+
+__global__ void __launch_bounds__(kGreedyWarps * 32) k_greedy_window(Batch b, const i32 *__restrict__ cl,
+                                                                     const i32 *__restrict__ cs, i64 m,
+                                                                     u8 *__restrict__ state) {
+  __shared__ u32 marks[kGreedyWarps][kGreedyMaxWin / 32];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const i64 w = i64(blockIdx.x) * kGreedyWarps + wl;
+  if (w >= b.W) return;
+  u32 *mk = marks[wl];
+  const i64 beg = b_beg(b, int(w)), len = b_end(b, int(w)) - beg;
+  for (int i = lane; i < (len + 31) / 32; i += 32) mk[i] = 0;
+  // windows are contiguous in position space and candidates are window-major,
+  // so a plain lower bound on the window id of each candidate's start works
+  i64 c0, c1;
+  {
+    i64 lo = 0, hi = m;
+    while (lo < hi) {
+      i64 mid = (lo + hi) >> 1;
+      if (b_wid(b, cs[mid]) < w) lo = mid + 1; else hi = mid;
+    }
+    c0 = lo;
+    hi = m;
+    while (lo < hi) {
+      i64 mid = (lo + hi) >> 1;
+      if (b_wid(b, cs[mid]) <= w) lo = mid + 1; else hi = mid;
+    }
+    c1 = lo;
+  }
+  __syncwarp();
+  for (i64 base = c0; base < c1; base += 32) {
+    const i64 my = base + lane;
+    i32 ml = 0, ms = 0;
+    if (my < c1) {
+      ml = cl[my];
+      ms = i32(cs[my] - beg);
+    }
+    const int cnt = int(c1 - base < 32 ? c1 - base : 32);
+    u32 keep_bits = 0;
+    for (int k = 0; k < cnt; ++k) {
+      const i32 l = __shfl_sync(0xffffffffu, ml, k);
+      const i32 st = __shfl_sync(0xffffffffu, ms, k);
+      const i32 en = st + l - 1;
+      const bool free_ = !((mk[st >> 5] >> (st & 31)) & 1u) && !((mk[en >> 5] >> (en & 31)) & 1u);
+      if (free_) {
+        keep_bits |= 1u << k;
+        // set bits [st, en]
+        const int w0 = st >> 5, w1 = en >> 5;
+        for (int x = w0 + lane; x <= w1; x += 32) {
+          u32 bits = 0xffffffffu;
+          if (x == w0) bits &= 0xffffffffu << (st & 31);
+          if (x == w1) bits &= 0xffffffffu >> (31 - (en & 31));
+          mk[x] |= bits;
+        }
+      }
+      __syncwarp();
+    }
+    if (my < c1) state[my] = ((keep_bits >> lane) & 1u) ? 1 : 2;
+  }
+}
+
 }  // namespace
 
 void plan_select(Carver &cv, const Batch &b, SelWork &w) {
@@ -383,7 +455,16 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
   APO_CHECK_LAUNCH();
   c.launches++;
 
-  // ---- K7: exact round-parallel greedy ----
+  // ---- K7 ----
+  if (b.maxwin <= kGreedyMaxWin && b.W >= 8) {
+    // many small windows: the paper's sequential marked-array greedy, one
+    // warp per window, all windows at once
+    k_greedy_window<<<grid_for(b.W, kGreedyWarps), kGreedyWarps * 32, 0, s>>>(b, w.cl, w.cs, m, w.state);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+    return;
+  }
+  // large windows: exact round-parallel greedy
   APO_CUDA(cudaMemsetAsync(w.diff, 0, sizeof(u32) * (N + 1), s));
   Tab tab{};
   for (int q = 0; q < w.tab_levels; ++q) tab.lv[q] = w.tab[q];
