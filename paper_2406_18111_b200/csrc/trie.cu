@@ -320,6 +320,159 @@ void upload_batch(Ctx &c, Batch &b, GenPlan &g, const std::vector<i64> &h_off, c
   b.wid = g.d_wid;
 }
 
+
+// ------------------------------------------- per-stream matching path ----
+// Every stream gets its own suffix array (K9 on chip for streams <= 16K);
+// each stream's SA is cut into buckets of equal first token; a trace is
+// binary-searched only in the buckets whose first token equals its own first
+// token (an exact filter: elsewhere it cannot occur).
+struct StreamMatch {
+  const i64 *off;   // stream offsets
+  const i32 *wid;
+  const i32 *sa;    // per-stream (window-major) suffix arrays, global positions
+  const u64 *tok;   // stream tokens
+  const u64 *ttok;  // trace tokens
+  const i64 *toff;  // trace offsets
+  i64 N, T;
+};
+
+struct BucketF {
+  StreamMatch m;
+  u64 *e_tok;
+  u32 *e_lo, *e_q;
+  i64 *total;
+  __device__ u32 load(i64 k) const {
+    const i64 p = m.sa[k];
+    const int q = m.wid[p];
+    if (k == m.off[q]) return 1;
+    return m.tok[p] != m.tok[m.sa[k - 1]] ? 1u : 0u;
+  }
+  __device__ bool store(i64 k, u32 incl, u32 excl) const {
+    if (incl != excl) {
+      const i64 p = m.sa[k];
+      e_tok[excl] = m.tok[p];
+      e_lo[excl] = u32(k);
+      e_q[excl] = u32(m.wid[p]);
+    }
+    if (k == m.N - 1) *total = i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+__global__ void k_bucket_hi(const u32 *__restrict__ e_lo, const u32 *__restrict__ e_q, i64 E,
+                            const i64 *__restrict__ off, u32 *__restrict__ e_hi, u32 *__restrict__ e_idx) {
+  const i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  e_hi[e] = (e + 1 < E && e_q[e + 1] == e_q[e]) ? e_lo[e + 1] : u32(off[e_q[e] + 1]);
+  e_idx[e] = u32(e);
+}
+
+// per trace: range [ea, eb) of token-sorted buckets with the trace's first token
+__global__ void k_trace_buckets(StreamMatch m, const u64 *__restrict__ sorted_tok, i64 E, u32 *__restrict__ ea,
+                                u32 *__restrict__ ecnt) {
+  const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= m.T) return;
+  const u64 a = m.ttok[m.toff[t]];
+  i64 lo = 0, hi = E;
+  while (lo < hi) {
+    i64 mid = (lo + hi) >> 1;
+    if (sorted_tok[mid] < a) lo = mid + 1; else hi = mid;
+  }
+  const i64 first = lo;
+  hi = E;
+  while (lo < hi) {
+    i64 mid = (lo + hi) >> 1;
+    if (sorted_tok[mid] <= a) lo = mid + 1; else hi = mid;
+  }
+  ea[t] = u32(first);
+  ecnt[t] = u32(lo - first);
+}
+
+struct PairBaseF {  // exclusive scan of per-trace pair counts (u32)
+  const u32 *cnt;
+  u32 *base;
+  i64 n;
+  i64 *total;
+  __device__ u32 load(i64 i) const { return cnt[i]; }
+  __device__ bool store(i64 i, u32 incl, u32 excl) const {
+    base[i] = excl;
+    if (i == n - 1) *total = i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+// first rank r in [lo0, hi0) of one stream's SA with cmp(t, s_r) <= 0
+// (STRICT: < 0); comparisons start at `from` (a known common prefix)
+template <bool STRICT>
+__device__ __forceinline__ i64 range_bound(const StreamMatch &m, i64 lo0, i64 hi0, i64 e, const u64 *t, i64 L,
+                                           i64 from) {
+  i64 lo = lo0 - 1, hi = hi0, llo = from, lhi = from;
+  while (hi - lo > 1) {
+    const i64 mid = lo + ((hi - lo) >> 1);
+    i64 l;
+    const int c = warp_cmp_trace_suffix(m.tok, m.sa[mid], e, t, L, llo < lhi ? llo : lhi, &l);
+    if (STRICT ? (c < 0) : (c <= 0)) {
+      hi = mid;
+      lhi = l;
+    } else {
+      lo = mid;
+      llo = l;
+    }
+  }
+  return hi;
+}
+
+// warp per (trace, bucket) pair: the trace's interval inside the bucket
+__global__ void k_pair_search(StreamMatch m, const u32 *__restrict__ pbase, const u32 *__restrict__ ea, i64 P,
+                              const u32 *__restrict__ e_order, const u32 *__restrict__ e_lo,
+                              const u32 *__restrict__ e_hi, const u32 *__restrict__ e_q, i64 *__restrict__ ilo,
+                              u32 *__restrict__ icnt, u32 *__restrict__ ptrace) {
+  const i64 z = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (z >= P) return;
+  i64 lo = 0, hi = m.T - 1;  // trace owning pair z: last t with pbase[t] <= z
+  while (lo < hi) {
+    i64 mid = (lo + hi + 1) >> 1;
+    if (i64(pbase[mid]) <= z) lo = mid; else hi = mid - 1;
+  }
+  const i64 t = lo;
+  const u32 e = e_order[ea[t] + (z - i64(pbase[t]))];
+  const i64 q = e_q[e];
+  const u64 *tt = m.ttok + m.toff[t];
+  const i64 L = m.toff[t + 1] - m.toff[t];
+  const i64 end = m.off[q + 1];
+  const i64 a = range_bound<false>(m, e_lo[e], e_hi[e], end, tt, L, 1);
+  const i64 b = range_bound<true>(m, e_lo[e], e_hi[e], end, tt, L, 1);
+  if ((threadIdx.x & 31) == 0) {
+    ilo[z] = a;
+    icnt[z] = u32(b - a);
+    ptrace[z] = u32(t);
+  }
+}
+
+// warp per pair: its hits are the contiguous SA range [ilo, ilo + cnt) of
+// one stream; written to [hbase, hbase + cnt) of the key array
+__global__ void k_enumerate_pairs(StreamMatch m, const i64 *__restrict__ ilo, const u32 *__restrict__ hbase,
+                                  const u32 *__restrict__ ptrace, i64 P, i64 H, int bE, int bT,
+                                  u64 *__restrict__ keys) {
+  const i64 z = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (z >= P) return;
+  const int lane = threadIdx.x & 31;
+  const i64 base = hbase[z];
+  const i64 cnt = (z + 1 < P ? i64(hbase[z + 1]) : H) - base;
+  if (cnt == 0) return;
+  const i64 t = ptrace[z];
+  const i64 L = m.toff[t + 1] - m.toff[t];
+  const i64 r0 = ilo[z];
+  for (i64 i = lane; i < cnt; i += 32) {
+    const i64 p = m.sa[r0 + i];
+    const int q = m.wid[p];
+    const i64 end = p - m.off[q] + L - 1;
+    keys[base + i] = (u64(q) << (bE + bT)) | (u64(end) << bT) | u64(t);
+  }
+}
+
 // Total order on pieces: length desc, then content (unsigned tokens, R1),
 // then piece index (indices >= n are padding and sort last).  The first three
 // tokens come from compact prefix-key arrays, so most comparisons never touch
@@ -726,7 +879,109 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
     const int bT = bits_for(u64(T - 1)), bE = bits_for(u64(maxs - 1)), bS = bits_for(u64(nstreams - 1));
     require(bT + bE + bS <= 64, "match key does not fit 64 bits");
     std::vector<i64> h_s(h_off, h_off + nstreams + 1);
-    // one generalized suffix array over the streams (no LCP needed)
+    u64 *keys = nullptr, *keys_alt = nullptr;
+    i64 nh = -1;
+    {
+      // ---- per-stream path: each stream's own SA, bucketed by first token ----
+      Batch b;
+      b.N = Ns;
+      b.W = nstreams;
+      b.maxwin = maxs;
+      GenPlan g;
+      u64 *e_tok, *e_tok_alt;
+      u32 *e_lo, *e_q, *e_hi, *e_idx, *e_idx_alt, *ea, *ecnt, *pbase;
+      i64 *scal;
+      auto plan = [&](Carver &cv) {
+        plan_gen(cv, b, g, false);
+        e_tok = cv.take<u64>(Ns);
+        e_tok_alt = cv.take<u64>(Ns);
+        e_lo = cv.take<u32>(Ns);
+        e_q = cv.take<u32>(Ns);
+        e_hi = cv.take<u32>(Ns);
+        e_idx = cv.take<u32>(Ns);
+        e_idx_alt = cv.take<u32>(Ns);
+        ea = cv.take<u32>(T);
+        ecnt = cv.take<u32>(T);
+        pbase = cv.take<u32>(T);
+        scal = cv.take<i64>(4);
+      };
+      Carver dry(nullptr);
+      plan(dry);
+      c.arena.reserve(dry.off, s);
+      Carver cv(c.arena.base);
+      plan(cv);
+      upload_batch(c, b, g, h_s, s);
+      build_sa(c, d_streams, b, g.sa, false, s);
+      StreamMatch sm{g.d_off, g.d_wid, g.sa.sa, d_streams, tr->d_tok, tr->d_off, Ns, T};
+      APO_CUDA(cudaMemsetAsync(scal, 0, sizeof(i64) * 4, s));
+      BucketF bf{sm, e_tok, e_lo, e_q, scal};
+      launch_scan<false>(c, Ns, bf, s);
+      const i64 E = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
+      k_bucket_hi<<<grid_for(E, T256), T256, 0, s>>>(e_lo, e_q, E, g.d_off, e_hi, e_idx);
+      APO_CHECK_LAUNCH();
+      bool ae = radix_sort_u64_u32(c, e_tok, e_idx, e_tok_alt, e_idx_alt, E, 0, 64, s);
+      const u64 *stok = ae ? e_tok_alt : e_tok;
+      const u32 *sord = ae ? e_idx_alt : e_idx;
+      k_trace_buckets<<<grid_for(T, T256), T256, 0, s>>>(sm, stok, E, ea, ecnt);
+      APO_CHECK_LAUNCH();
+      c.launches += 2;
+      PairBaseF pf{ecnt, pbase, T, scal + 1};
+      launch_scan<false>(c, T, pf, s);
+      const i64 P = i64(c.read_u64(reinterpret_cast<const u64 *>(scal + 1), s));
+      // exact filter; fall back to the generalized SA when the pairs explode
+      // (e.g. a tiny alphabet where every trace's first token is everywhere)
+      if (P <= std::max<i64>(Ns / 4, 4 * T)) {
+        nh = 0;
+        if (P > 0) {
+          i64 *ilo;
+          u32 *icnt, *hbase, *ptr;
+          Carver cx(nullptr);
+          cx.take<i64>(P);
+          cx.take<u32>(P);
+          cx.take<u32>(P);
+          cx.take<u32>(P);
+          c.aux.reserve(cx.off, s);
+          Carver ca(c.aux.base);
+          ilo = ca.take<i64>(P);
+          icnt = ca.take<u32>(P);
+          hbase = ca.take<u32>(P);
+          ptr = ca.take<u32>(P);
+          k_pair_search<<<grid_for(P * 32, 256), 256, 0, s>>>(sm, pbase, ea, P, sord, e_lo, e_hi, e_q, ilo, icnt,
+                                                                ptr);
+          APO_CHECK_LAUNCH();
+          c.launches++;
+          PairBaseF hf{icnt, hbase, P, scal + 2};
+          launch_scan<false>(c, P, hf, s);
+          nh = i64(c.read_u64(reinterpret_cast<const u64 *>(scal + 2), s));
+          if (nh > 0) {
+            // keys after the pair tables in the aux arena (grown if needed:
+            // reserve() keeps nothing, so re-carve the pair tables first)
+            const size_t need = cx.off + 256 + sizeof(u64) * size_t(nh) * 2;
+            if (need > c.aux.cap) {
+              // move the pair tables aside in the main arena's key buffers
+              i64 *ilo2 = reinterpret_cast<i64 *>(e_tok);
+              u32 *hb2 = e_lo, *pt2 = e_q;
+              APO_CUDA(cudaMemcpyAsync(ilo2, ilo, sizeof(i64) * P, cudaMemcpyDeviceToDevice, s));
+              APO_CUDA(cudaMemcpyAsync(hb2, hbase, sizeof(u32) * P, cudaMemcpyDeviceToDevice, s));
+              APO_CUDA(cudaMemcpyAsync(pt2, ptr, sizeof(u32) * P, cudaMemcpyDeviceToDevice, s));
+              c.aux.reserve(need, s);
+              ilo = ilo2;
+              hbase = hb2;
+              ptr = pt2;
+              keys = reinterpret_cast<u64 *>(c.aux.base);
+            } else {
+              keys = reinterpret_cast<u64 *>(c.aux.base + ((cx.off + 255) & ~size_t(255)));
+            }
+            keys_alt = keys + nh;
+            k_enumerate_pairs<<<grid_for(P * 32, T256), T256, 0, s>>>(sm, ilo, hbase, ptr, P, nh, bE, bT, keys);
+            APO_CHECK_LAUNCH();
+            c.launches++;
+          }
+        }
+      }
+    }
+    if (nh < 0) {
+    // ---- fallback: one generalized suffix array over the streams ----
     Batch b;
     b.N = Ns;
     b.W = nstreams;
@@ -757,17 +1012,20 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
     APO_CUDA(cudaMemsetAsync(scal, 0, sizeof(i64) * 4, s));
     CountScanF cf{icnt, ibase, T, scal};
     launch_scan<false>(c, T, cf, s);
-    const i64 nh = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
+    nh = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
+    if (nh > 0) {
+      c.aux.reserve(sizeof(u64) * size_t(nh) * 2 + 1024, s);
+      keys = reinterpret_cast<u64 *>(c.aux.base);
+      keys_alt = keys + nh;
+      k_enumerate<<<grid_for(nh, T256), T256, 0, s>>>(m, ilo, ibase, nh, bE, bT, keys);
+      APO_CHECK_LAUNCH();
+      c.launches++;
+    }
+    }
     if (nh == 0) return;
-    c.aux.reserve(sizeof(u64) * size_t(nh) * 2 + 1024, s);
-    u64 *keys = reinterpret_cast<u64 *>(c.aux.base);
-    u64 *keys_alt = keys + nh;
-    k_enumerate<<<grid_for(nh, T256), T256, 0, s>>>(m, ilo, ibase, nh, bE, bT, keys);
-    APO_CHECK_LAUNCH();
-    c.launches++;
     const int kb = bS + bE + bT;
-    // hits were enumerated in trace-id order, so a STABLE sort on the
-    // (stream, end) bits alone leaves equal (stream, end) in trace order
+    // hits were enumerated in trace-id order (both paths), so a STABLE sort
+    // on the (stream, end) bits alone leaves equal (stream, end) in trace order
     bool a = radix_sort_u64_keys(c, keys, keys_alt, nh, bT, kb, s);
     const u64 *sorted = a ? keys_alt : keys;
     if (cap > 0) {

@@ -104,3 +104,22 @@ def test_match_no_hits_and_empty(ctx):
     assert empty.info()[0] == 0
     hits = ctx.match(empty, dev(np.array([4, 5], np.uint64)), np.array([0, 2]))
     assert hits.shape[0] == 0
+
+
+def test_match_both_paths(ctx):
+    """Tiny alphabet: every trace's first token occurs in every stream, so the
+    per-stream bucket filter gives up and the generalized-SA path runs; a
+    large-alphabet case takes the per-stream path.  Both vs the oracle."""
+    for alpha, nstreams in ((2, 40), (64, 12)):
+        streams = [gen.random_string(1000 + q, 30 + (q * 7) % 50, alpha) for q in range(nstreams)]
+        traces = sorted({tuple(int(x) for x in gen.random_string(2000 + j, 1 + j % 6, alpha)) for j in range(60)},
+                        key=lambda t: (-len(t), t))
+        flat = np.array([x for t in traces for x in t], dtype=np.uint64)
+        toff = np.cumsum([0] + [len(t) for t in traces]).astype(np.int64)
+        trie = ctx.trie_build_traces(dev(flat), toff)
+        tt, to = trie.traces()
+        sflat = np.concatenate(streams)
+        soff = np.cumsum([0] + [len(x) for x in streams]).astype(np.int64)
+        hits = ctx.match(trie, dev(sflat), soff).cpu().numpy()
+        want, cnt = oracle.match_brute(sflat, soff, tt.cpu().numpy(), to)
+        assert np.array_equal(hits, want), alpha
