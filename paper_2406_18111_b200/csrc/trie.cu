@@ -330,6 +330,7 @@ struct StreamMatch {
   const i64 *off;   // stream offsets
   const i32 *wid;
   const i32 *sa;    // per-stream (window-major) suffix arrays, global positions
+  const i32 *lcp;   // per-stream LCP (lcp[k] = LCP(sa[k], sa[k+1]), 0 at a stream end)
   const u64 *tok;   // stream tokens
   const u64 *ttok;  // trace tokens
   const i64 *toff;  // trace offsets
@@ -407,12 +408,15 @@ struct PairBaseF {  // exclusive scan of per-trace pair counts (u32)
 // (STRICT: < 0); comparisons start at `from` (a known common prefix)
 template <bool STRICT>
 __device__ __forceinline__ i64 range_bound(const StreamMatch &m, i64 lo0, i64 hi0, i64 e, const u64 *t, i64 L,
-                                           i64 from) {
-  i64 lo = lo0 - 1, hi = hi0, llo = from, lhi = from;
+                                           i64 from, i64 *lcp_hi) {
+  i64 lo = lo0 - 1, hi = hi0, llo = from, lhi = -1;  // lhi < 0: hi is the range end (not compared)
   while (hi - lo > 1) {
     const i64 mid = lo + ((hi - lo) >> 1);
     i64 l;
-    const int c = warp_cmp_trace_suffix(m.tok, m.sa[mid], e, t, L, llo < lhi ? llo : lhi, &l);
+    // Manber-Myers skip: lcp(t, S_mid) >= min(lcp(t, S_lo), lcp(t, S_hi)) holds only
+    // once BOTH brackets were compared; before that only `from` is known
+    const i64 st = lhi < 0 ? from : (llo < lhi ? llo : lhi);
+    const int c = warp_cmp_trace_suffix(m.tok, m.sa[mid], e, t, L, st, &l);
     if (STRICT ? (c < 0) : (c <= 0)) {
       hi = mid;
       lhi = l;
@@ -421,6 +425,7 @@ __device__ __forceinline__ i64 range_bound(const StreamMatch &m, i64 lo0, i64 hi
       llo = l;
     }
   }
+  *lcp_hi = lhi;
   return hi;
 }
 
@@ -442,11 +447,29 @@ __global__ void k_pair_search(StreamMatch m, const u32 *__restrict__ pbase, cons
   const u64 *tt = m.ttok + m.toff[t];
   const i64 L = m.toff[t + 1] - m.toff[t];
   const i64 end = m.off[q + 1];
-  const i64 a = range_bound<false>(m, e_lo[e], e_hi[e], end, tt, L, 1);
-  const i64 b = range_bound<true>(m, e_lo[e], e_hi[e], end, tt, L, 1);
+  i64 la;
+  const i64 a = range_bound<false>(m, e_lo[e], e_hi[e], end, tt, L, 1, &la);
+  // the interval: from the lower bound (if it has t as a prefix) while the
+  // LCP with the next suffix stays >= |t| (32 LCP entries per step)
+  i64 cnt = 0;
+  if (la >= L) {
+    const int lane = threadIdx.x & 31;
+    const i64 lim = e_hi[e];
+    cnt = 1;
+    for (i64 k0 = a; k0 + 1 < lim; k0 += 32) {
+      const i64 k = k0 + lane;
+      const bool ok = (k + 1 < lim) && m.lcp[k] >= L;
+      const u32 bad = __ballot_sync(0xffffffffu, !ok);
+      if (bad) {
+        cnt += __ffs(bad) - 1;
+        break;
+      }
+      cnt += 32;
+    }
+  }
   if ((threadIdx.x & 31) == 0) {
     ilo[z] = a;
-    icnt[z] = u32(b - a);
+    icnt[z] = u32(cnt);
     ptrace[z] = u32(t);
   }
 }
@@ -892,7 +915,7 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
       u32 *e_lo, *e_q, *e_hi, *e_idx, *e_idx_alt, *ea, *ecnt, *pbase;
       i64 *scal;
       auto plan = [&](Carver &cv) {
-        plan_gen(cv, b, g, false);
+        plan_gen(cv, b, g, true);
         e_tok = cv.take<u64>(Ns);
         e_tok_alt = cv.take<u64>(Ns);
         e_lo = cv.take<u32>(Ns);
@@ -911,8 +934,8 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
       Carver cv(c.arena.base);
       plan(cv);
       upload_batch(c, b, g, h_s, s);
-      build_sa(c, d_streams, b, g.sa, false, s);
-      StreamMatch sm{g.d_off, g.d_wid, g.sa.sa, d_streams, tr->d_tok, tr->d_off, Ns, T};
+      build_sa(c, d_streams, b, g.sa, true, s);
+      StreamMatch sm{g.d_off, g.d_wid, g.sa.sa, g.sa.lcp, d_streams, tr->d_tok, tr->d_off, Ns, T};
       APO_CUDA(cudaMemsetAsync(scal, 0, sizeof(i64) * 4, s));
       BucketF bf{sm, e_tok, e_lo, e_q, scal};
       launch_scan<false>(c, Ns, bf, s);

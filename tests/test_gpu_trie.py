@@ -123,3 +123,23 @@ def test_match_both_paths(ctx):
         hits = ctx.match(trie, dev(sflat), soff).cpu().numpy()
         want, cnt = oracle.match_brute(sflat, soff, tt.cpu().numpy(), to)
         assert np.array_equal(hits, want), alpha
+
+
+def test_match_medium_batches_sampled_streams(ctx):
+    """Mid-size C4-shaped batches (the per-stream matcher with its bucket
+    binary searches and LCP interval extension): sampled streams against the
+    brute-force oracle."""
+    for (W, win, seed) in ((64, 4096, 7), (96, 16384, 4)):
+        tok, off, st, so = gen.c4(seed=seed, windows=W, window=win, templates=16)
+        d = dev(tok)
+        rep, roff, occ = ctx.find_repeats_batched(d, off, 25)
+        trie = ctx.trie_build(d, off, rep, roff, 25, 0)
+        tt, to = trie.traces()
+        tth = tt.cpu().numpy()
+        hits = ctx.match(trie, dev(st), so).cpu().numpy()
+        for q in (0, 30, 42, W - 1):
+            s1 = st[so[q]:so[q + 1]]
+            want, _ = oracle.match_brute(s1, [0, len(s1)], tth, to)
+            got = hits[hits[:, 0] == q].copy()
+            got[:, 0] = 0
+            assert np.array_equal(got, want), (W, q)
