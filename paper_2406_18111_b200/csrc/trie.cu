@@ -545,6 +545,51 @@ __global__ void k_bitonic(u32 *__restrict__ idx, i64 P, i64 j, i64 k, TraceCmp c
   }
 }
 
+// keys for the LSD passes of the trace order: which = 2: token 1, 1: token 0,
+// 0: maxlen - length (length descending); vals (optional) = piece ids
+__global__ void k_prefix_keys(const u32 *__restrict__ ids, i64 U, const u64 *__restrict__ pk,
+                              const i64 *__restrict__ off, i64 maxlen, int which, u64 *__restrict__ keys,
+                              u32 *__restrict__ vals) {
+  const i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= U) return;
+  const u32 p = ids[c];
+  if (which == 0)
+    keys[c] = u64(maxlen - (off[p + 1] - off[p]));
+  else
+    keys[c] = pk[3 * i64(p) + (which == 1 ? 0 : 1)];
+  if (vals) vals[c] = p;
+}
+
+constexpr int kMaxTie = 256;
+
+// Insertion sort of each run of equal (length, token 0, token 1) with the
+// full comparator (one thread per run, started at the run's first element).
+// *worst receives the largest run length; runs longer than kMaxTie are left
+// unsorted (the caller then falls back to the bitonic network).
+__global__ void k_tie_sort(u32 *__restrict__ order, i64 U, TraceCmp cmp, u32 *__restrict__ worst) {
+  const i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= U) return;
+  auto same = [&](u32 a, u32 b) {
+    const i64 la = cmp.off[a + 1] - cmp.off[a], lb = cmp.off[b + 1] - cmp.off[b];
+    return la == lb && cmp.pk[3 * i64(a)] == cmp.pk[3 * i64(b)] && cmp.pk[3 * i64(a) + 1] == cmp.pk[3 * i64(b) + 1];
+  };
+  if (c > 0 && same(order[c - 1], order[c])) return;  // not a run start
+  i64 e = c + 1;
+  while (e < U && same(order[c], order[e])) ++e;
+  const i64 g = e - c;
+  if (g > 1) atomicMax(worst, u32(g));
+  if (g < 2 || g > kMaxTie) return;
+  for (i64 i = c + 1; i < e; ++i) {
+    const u32 x = order[i];
+    i64 j = i - 1;
+    while (j >= c && cmp.cmp(order[j], x) > 0) {
+      order[j + 1] = order[j];
+      --j;
+    }
+    order[j + 1] = x;
+  }
+}
+
 __device__ __forceinline__ u64 mix64(u64 z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
@@ -685,19 +730,49 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
   CompactF cf{keep, by_hash, surv, np, scal};
   launch_scan<false>(c, np, cf, s);
   const i64 U = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
-  // 2. lexicographic order of the distinct pieces
-  i64 PU = 1;
-  while (PU < U) PU <<= 1;
-  k_iota_list<<<grid_for(PU, T256), T256, 0, s>>>(surv, U, order, PU, u32(np));
-  APO_CHECK_LAUNCH();
-  c.launches++;
+  // 2. lexicographic order of the distinct pieces: LSD radix sort by
+  //    (length desc, token 0, token 1) -- every sort is over U << N keys --
+  //    then the rare tie groups (same length and first two tokens) are
+  //    finished by an insertion sort with the full comparator.  A tie group
+  //    larger than kMaxTie falls back to the bitonic network.
   TraceCmp cmp{d_ptok, d_poff, pk, np};
-  for (i64 k = 2; k <= PU; k <<= 1)
-    for (i64 j = k >> 1; j > 0; j >>= 1) {
-      k_bitonic<<<grid_for(PU, T256), T256, 0, s>>>(order, PU, j, k, cmp);
+  {
+    u64 *rk = hk, *rk_alt = hk_alt;
+    u32 *rv = hv, *rv_alt = hv_alt;
+    const int lenbits = bits_for(u64(maxlen));
+    k_prefix_keys<<<grid_for(U, T256), T256, 0, s>>>(surv, U, pk, d_poff, maxlen, 2, rk, rv);
+    APO_CHECK_LAUNCH();
+    bool x = radix_sort_u64_u32(c, rk, rv, rk_alt, rv_alt, U, 0, 64, s);
+    if (x) { std::swap(rk, rk_alt); std::swap(rv, rv_alt); }
+    k_prefix_keys<<<grid_for(U, T256), T256, 0, s>>>(rv, U, pk, d_poff, maxlen, 1, rk, nullptr);
+    APO_CHECK_LAUNCH();
+    x = radix_sort_u64_u32(c, rk, rv, rk_alt, rv_alt, U, 0, 64, s);
+    if (x) { std::swap(rk, rk_alt); std::swap(rv, rv_alt); }
+    k_prefix_keys<<<grid_for(U, T256), T256, 0, s>>>(rv, U, pk, d_poff, maxlen, 0, rk, nullptr);
+    APO_CHECK_LAUNCH();
+    x = radix_sort_u64_u32(c, rk, rv, rk_alt, rv_alt, U, 0, lenbits, s);
+    if (x) { std::swap(rk, rk_alt); std::swap(rv, rv_alt); }
+    APO_CUDA(cudaMemsetAsync(scal + 2, 0, sizeof(i64), s));
+    k_tie_sort<<<grid_for(U, T256), T256, 0, s>>>(rv, U, cmp, reinterpret_cast<u32 *>(scal + 2));
+    APO_CHECK_LAUNCH();
+    c.launches += 4;
+    const u32 worst = c.read_u32(reinterpret_cast<const u32 *>(scal + 2), s);
+    if (worst <= u32(kMaxTie)) {
+      APO_CUDA(cudaMemcpyAsync(order, rv, sizeof(u32) * U, cudaMemcpyDeviceToDevice, s));
+    } else {
+      i64 PU = 1;
+      while (PU < U) PU <<= 1;
+      k_iota_list<<<grid_for(PU, T256), T256, 0, s>>>(surv, U, order, PU, u32(np));
       APO_CHECK_LAUNCH();
       c.launches++;
+      for (i64 k = 2; k <= PU; k <<= 1)
+        for (i64 j = k >> 1; j > 0; j >>= 1) {
+          k_bitonic<<<grid_for(PU, T256), T256, 0, s>>>(order, PU, j, k, cmp);
+          APO_CHECK_LAUNCH();
+          c.launches++;
+        }
     }
+  }
   // 3. exact neighbour check, ids
   k_trace_heads<<<grid_for(U * 32, T256), T256, 0, s>>>(d_ptok, d_poff, order, U, head);
   APO_CHECK_LAUNCH();
