@@ -430,47 +430,56 @@ __device__ __forceinline__ i64 range_bound(const StreamMatch &m, i64 lo0, i64 hi
 }
 
 // warp per (trace, bucket) pair: the trace's interval inside the bucket
+// One warp per chunk of kPairChunk consecutive (trace, bucket) pairs: one
+// trace lookup per chunk, then the pairs in order (pairs are grouped by
+// trace), each: the trace's lower bound in the bucket (warp-cooperative
+// Manber-Myers search), then the interval extended while the stream LCP stays
+// >= |t| (32 LCP entries per step).
+constexpr int kPairChunk = 16;
+
 __global__ void k_pair_search(StreamMatch m, const u32 *__restrict__ pbase, const u32 *__restrict__ ea, i64 P,
                               const u32 *__restrict__ e_order, const u32 *__restrict__ e_lo,
                               const u32 *__restrict__ e_hi, const u32 *__restrict__ e_q, i64 *__restrict__ ilo,
                               u32 *__restrict__ icnt, u32 *__restrict__ ptrace) {
-  const i64 z = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  if (z >= P) return;
-  i64 lo = 0, hi = m.T - 1;  // trace owning pair z: last t with pbase[t] <= z
+  const i64 z0 = ((i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * kPairChunk;
+  if (z0 >= P) return;
+  const int lane = threadIdx.x & 31;
+  i64 lo = 0, hi = m.T - 1;  // trace owning pair z0: last t with pbase[t] <= z0
   while (lo < hi) {
     i64 mid = (lo + hi + 1) >> 1;
-    if (i64(pbase[mid]) <= z) lo = mid; else hi = mid - 1;
+    if (i64(pbase[mid]) <= z0) lo = mid; else hi = mid - 1;
   }
-  const i64 t = lo;
-  const u32 e = e_order[ea[t] + (z - i64(pbase[t]))];
-  const i64 q = e_q[e];
-  const u64 *tt = m.ttok + m.toff[t];
-  const i64 L = m.toff[t + 1] - m.toff[t];
-  const i64 end = m.off[q + 1];
-  i64 la;
-  const i64 a = range_bound<false>(m, e_lo[e], e_hi[e], end, tt, L, 1, &la);
-  // the interval: from the lower bound (if it has t as a prefix) while the
-  // LCP with the next suffix stays >= |t| (32 LCP entries per step)
-  i64 cnt = 0;
-  if (la >= L) {
-    const int lane = threadIdx.x & 31;
-    const i64 lim = e_hi[e];
-    cnt = 1;
-    for (i64 k0 = a; k0 + 1 < lim; k0 += 32) {
-      const i64 k = k0 + lane;
-      const bool ok = (k + 1 < lim) && m.lcp[k] >= L;
-      const u32 bad = __ballot_sync(0xffffffffu, !ok);
-      if (bad) {
-        cnt += __ffs(bad) - 1;
-        break;
+  i64 t = lo;
+  const i64 z1 = z0 + kPairChunk < P ? z0 + kPairChunk : P;
+  for (i64 z = z0; z < z1; ++z) {
+    while (t + 1 < m.T && i64(pbase[t + 1]) <= z) ++t;
+    const u32 e = e_order[ea[t] + (z - i64(pbase[t]))];
+    const i64 q = e_q[e];
+    const u64 *tt = m.ttok + m.toff[t];
+    const i64 L = m.toff[t + 1] - m.toff[t];
+    const i64 end = m.off[q + 1];
+    i64 la;
+    const i64 a = range_bound<false>(m, e_lo[e], e_hi[e], end, tt, L, 1, &la);
+    i64 cnt = 0;
+    if (la >= L) {
+      const i64 lim = e_hi[e];
+      cnt = 1;
+      for (i64 k0 = a; k0 + 1 < lim; k0 += 32) {
+        const i64 k = k0 + lane;
+        const bool ok = (k + 1 < lim) && m.lcp[k] >= L;
+        const u32 bad = __ballot_sync(0xffffffffu, !ok);
+        if (bad) {
+          cnt += __ffs(bad) - 1;
+          break;
+        }
+        cnt += 32;
       }
-      cnt += 32;
     }
-  }
-  if ((threadIdx.x & 31) == 0) {
-    ilo[z] = a;
-    icnt[z] = u32(cnt);
-    ptrace[z] = u32(t);
+    if (lane == 0) {
+      ilo[z] = a;
+      icnt[z] = u32(cnt);
+      ptrace[z] = u32(t);
+    }
   }
 }
 
@@ -1044,8 +1053,9 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
           icnt = ca.take<u32>(P);
           hbase = ca.take<u32>(P);
           ptr = ca.take<u32>(P);
-          k_pair_search<<<grid_for(P * 32, 256), 256, 0, s>>>(sm, pbase, ea, P, sord, e_lo, e_hi, e_q, ilo, icnt,
-                                                                ptr);
+          const i64 chunks = (P + kPairChunk - 1) / kPairChunk;
+          k_pair_search<<<grid_for(chunks * 32, 256), 256, 0, s>>>(sm, pbase, ea, P, sord, e_lo, e_hi, e_q, ilo,
+                                                                     icnt, ptr);
           APO_CHECK_LAUNCH();
           c.launches++;
           PairBaseF hf{icnt, hbase, P, scal + 2};
