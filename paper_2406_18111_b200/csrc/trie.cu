@@ -23,6 +23,8 @@
 //   table; the interval is enumerated with a load-balanced scan and the hits
 //   are radix-sorted by (stream, end, trace).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "pipeline.cuh"
@@ -390,6 +392,16 @@ __global__ void k_trace_buckets(StreamMatch m, const u64 *__restrict__ sorted_to
   ecnt[t] = u32(lo - first);
 }
 
+struct ExclScanU32F {  // in-place exclusive sum
+  u32 *a;
+  __device__ u32 load(i64 i) const { return a[i]; }
+  __device__ bool store(i64 i, u32, u32 excl) const {
+    a[i] = excl;
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
 struct PairBaseF {  // exclusive scan of per-trace pair counts (u32)
   const u32 *cnt;
   u32 *base;
@@ -479,6 +491,164 @@ __global__ void k_pair_search(StreamMatch m, const u32 *__restrict__ pbase, cons
       ilo[z] = a;
       icnt[z] = u32(cnt);
       ptrace[z] = u32(t);
+    }
+  }
+}
+
+// ---- per-stream CTA matcher: pairs grouped by stream, the stream's tokens,
+// local SA and LCP staged in shared memory, so every step of every binary
+// search is an on-chip access (only the trace tokens come from L2/HBM).
+constexpr int kSMThreads = 1024;
+constexpr int kSMMax = 16384;  // longest stream handled on chip
+
+__global__ void k_pair_list(const u32 *__restrict__ pbase, const u32 *__restrict__ ea, const u32 *__restrict__ ecnt,
+                            const u32 *__restrict__ e_order, const u32 *__restrict__ e_q, i64 T,
+                            u32 *__restrict__ pair_e, u32 *__restrict__ ptrace, u64 *__restrict__ qkey,
+                            u32 *__restrict__ qval) {
+  const i64 t = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (t >= T) return;
+  const int lane = threadIdx.x & 31;
+  const i64 z0 = pbase[t], n = ecnt[t], e0 = ea[t];
+  for (i64 j = lane; j < n; j += 32) {
+    const u32 e = e_order[e0 + j];
+    pair_e[z0 + j] = e;
+    ptrace[z0 + j] = u32(t);
+    qkey[z0 + j] = u64(e_q[e]);
+    qval[z0 + j] = u32(z0 + j);
+  }
+}
+
+__global__ void k_count_q(const u64 *__restrict__ qkey, i64 P, u32 *__restrict__ cnt) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < P) atomicAdd(&cnt[qkey[i]], 1u);
+}
+
+// Warp-cooperative compare of trace t with the on-chip stream suffix at p;
+// the trace's first 64 tokens live in registers (r0 = t[lane],
+// r1 = t[32 + lane]), later tokens come from global memory.
+__device__ __forceinline__ int warp_cmp_smem(const u64 *__restrict__ S, i64 p, i64 n, const u64 *__restrict__ t,
+                                             u64 r0, u64 r1, i64 L, i64 from, i64 *lcp) {
+  const int lane = threadIdx.x & 31;
+  for (i64 base = from; base < L; base += 32) {
+    const i64 k = base + lane;
+    u64 x;
+    if (base < 64) {  // all lanes take this branch together
+      const int src = int(k & 31);
+      const u64 a = __shfl_sync(0xffffffffu, r0, src);
+      const u64 b = __shfl_sync(0xffffffffu, r1, src);
+      x = k < 32 ? a : (k < 64 ? b : (k < L ? t[k] : 0ull));
+    } else {
+      x = k < L ? t[k] : 0ull;
+    }
+    int res = 0;
+    if (k < L) {
+      if (p + k >= n) {
+        res = 1;
+      } else {
+        const u64 y = S[p + k];
+        res = x == y ? 0 : (x < y ? -1 : 1);
+      }
+    }
+    const u32 m = __ballot_sync(0xffffffffu, res != 0);
+    if (m) {
+      const int f = __ffs(m) - 1;
+      *lcp = base + f;
+      return __shfl_sync(0xffffffffu, res, f);
+    }
+  }
+  *lcp = L;
+  return 0;
+}
+
+__global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, const u32 *__restrict__ zsorted,
+                                                                const u32 *__restrict__ qoff,
+                                                                const u32 *__restrict__ pair_e,
+                                                                const u32 *__restrict__ ptrace,
+                                                                const u32 *__restrict__ e_lo,
+                                                                const u32 *__restrict__ e_hi, i64 *__restrict__ ilo,
+                                                                u32 *__restrict__ icnt) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int q = blockIdx.x;
+  const i64 z0 = qoff[q], z1 = qoff[q + 1];
+  if (z0 == z1) return;
+  const i64 beg = m.off[q], n = m.off[q + 1] - beg;
+  u64 *S = reinterpret_cast<u64 *>(smem);
+  unsigned short *SA = reinterpret_cast<unsigned short *>(S + kSMMax);
+  unsigned short *LC = SA + kSMMax;
+  for (i64 i = threadIdx.x; i < n; i += kSMThreads) {
+    S[i] = m.tok[beg + i];
+    SA[i] = (unsigned short)(m.sa[beg + i] - beg);
+    LC[i] = (unsigned short)m.lcp[beg + i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (i64 i = z0 + warp; i < z1; i += kSMThreads / 32) {
+    const u32 z = zsorted[i];
+    const u32 e = pair_e[z];
+    const i64 t = ptrace[z];
+    const u64 *tt = m.ttok + m.toff[t];
+    const i64 L = m.toff[t + 1] - m.toff[t];
+    const i64 lo0 = e_lo[e] - beg, hi0 = e_hi[e] - beg;
+    const u64 r0 = lane < L ? tt[lane] : 0ull, r1 = 32 + lane < L ? tt[32 + lane] : 0ull;
+    // lower bound: first local rank r in [lo0, hi0) with cmp(t, s_r) <= 0.
+    // Manber-Myers with LCP-LR: l = lcp(t, S_lo), r = lcp(t, S_hi); when
+    // both brackets are real and l != r, lcp(S_lo or S_hi, S_mid) (a warp
+    // min over the on-chip LCP array) decides the step without comparing
+    // tokens; tokens are compared only from the known lcp onwards.
+    i64 lo = lo0 - 1, hi = hi0, llo = 1, lhi = -1;
+    while (hi - lo > 1) {
+      const i64 mid = lo + ((hi - lo) >> 1);
+      const bool real = lo >= lo0 && lhi >= 0;
+      i64 st = 1;
+      if (real && llo != lhi) {
+        const bool left = llo > lhi;
+        const i64 a = left ? lo : mid, b = left ? mid : hi;  // lcp(S_a, S_b) = min LC[a..b-1]
+        u32 mn = 0xffffu;
+        for (i64 k = a + lane; k < b; k += 32) mn = min(mn, u32(LC[k]));
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, d));
+        const i64 x = mn;
+        if (left) {
+          if (x > llo) { lo = mid; continue; }            // S_mid < t, lcp(t, S_mid) = llo
+          if (x < llo) { hi = mid; lhi = x; continue; }   // t < S_mid, lcp = x
+          st = llo;
+        } else {
+          if (x > lhi) { hi = mid; continue; }            // t <= S_mid, lcp = lhi
+          if (x < lhi) { lo = mid; llo = x; continue; }   // S_mid < t, lcp = x
+          st = lhi;
+        }
+      } else if (real) {
+        st = llo;
+      } else if (lhi >= 0) {
+        st = 1;  // lower bracket virtual
+      }
+      i64 l;
+      const int c = warp_cmp_smem(S, SA[mid], n, tt, r0, r1, L, st, &l);
+      if (c <= 0) {
+        hi = mid;
+        lhi = l;
+      } else {
+        lo = mid;
+        llo = l;
+      }
+    }
+    i64 cnt = 0;
+    if (lhi >= L) {
+      cnt = 1;
+      for (i64 k0 = hi; k0 + 1 < hi0; k0 += 32) {
+        const i64 k = k0 + lane;
+        const bool ok = (k + 1 < hi0) && i64(LC[k]) >= L;
+        const u32 bad = __ballot_sync(0xffffffffu, !ok);
+        if (bad) {
+          cnt += __ffs(bad) - 1;
+          break;
+        }
+        cnt += 32;
+      }
+    }
+    if (lane == 0) {
+      ilo[z] = beg + hi;
+      icnt[z] = u32(cnt);
     }
   }
 }
@@ -1053,14 +1223,68 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
           icnt = ca.take<u32>(P);
           hbase = ca.take<u32>(P);
           ptr = ca.take<u32>(P);
-          const i64 chunks = (P + kPairChunk - 1) / kPairChunk;
-          k_pair_search<<<grid_for(chunks * 32, 256), 256, 0, s>>>(sm, pbase, ea, P, sord, e_lo, e_hi, e_q, ilo,
-                                                                     icnt, ptr);
-          APO_CHECK_LAUNCH();
-          c.launches++;
+          if (maxs <= kSMMax) {
+            // group the pairs by stream; one CTA per stream on chip
+            // carve after the pair tables (the aux arena holds both)
+            Carver full(nullptr);
+            full.off = cx.off;
+            full.take<u32>(P);
+            full.take<u64>(P);
+            full.take<u64>(P);
+            full.take<u32>(P);
+            full.take<u32>(P);
+            full.take<u32>(size_t(nstreams) + 1);
+            if (full.off > c.aux.cap) {
+              c.aux.reserve(full.off, s);
+              Carver cb(c.aux.base);
+              ilo = cb.take<i64>(P);
+              icnt = cb.take<u32>(P);
+              hbase = cb.take<u32>(P);
+              ptr = cb.take<u32>(P);
+            }
+            Carver cz(c.aux.base);
+            cz.off = cx.off;
+            u32 *pair_e = cz.take<u32>(P);
+            u64 *qk = cz.take<u64>(P), *qk_alt = cz.take<u64>(P);
+            u32 *qv = cz.take<u32>(P), *qv_alt = cz.take<u32>(P);
+            u32 *qoff = cz.take<u32>(size_t(nstreams) + 1);
+            k_pair_list<<<grid_for(T * 32, T256), T256, 0, s>>>(pbase, ea, ecnt, sord, e_q, T, pair_e, ptr, qk, qv);
+            APO_CHECK_LAUNCH();
+            bool aq = radix_sort_u64_u32(c, qk, qv, qk_alt, qv_alt, P, 0, bits_for(u64(nstreams - 1)), s);
+            const u64 *sqk = aq ? qk_alt : qk;
+            const u32 *sqv = aq ? qv_alt : qv;
+            APO_CUDA(cudaMemsetAsync(qoff, 0, sizeof(u32) * (nstreams + 1), s));
+            k_count_q<<<grid_for(P, T256), T256, 0, s>>>(sqk, P, qoff);
+            APO_CHECK_LAUNCH();
+            ExclScanU32F xf{qoff};
+            launch_scan<false>(c, i64(nstreams) + 1, xf, s);
+            const size_t smem = sizeof(u64) * kSMMax + 2 * sizeof(unsigned short) * kSMMax;
+            static bool attr = false;
+            if (!attr) {
+              APO_CUDA(cudaFuncSetAttribute(k_stream_match, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+              attr = true;
+            }
+            k_stream_match<<<nstreams, kSMThreads, smem, s>>>(sm, sqv, qoff, pair_e, ptr, e_lo, e_hi, ilo, icnt);
+            APO_CHECK_LAUNCH();
+            c.launches += 3;
+          } else {
+            const i64 chunks = (P + kPairChunk - 1) / kPairChunk;
+            k_pair_search<<<grid_for(chunks * 32, 256), 256, 0, s>>>(sm, pbase, ea, P, sord, e_lo, e_hi, e_q, ilo,
+                                                                       icnt, ptr);
+            APO_CHECK_LAUNCH();
+            c.launches++;
+          }
           PairBaseF hf{icnt, hbase, P, scal + 2};
           launch_scan<false>(c, P, hf, s);
           nh = i64(c.read_u64(reinterpret_cast<const u64 *>(scal + 2), s));
+          if (std::getenv("APO_DEBUG_STATS")) {
+            std::vector<u32> hc(static_cast<size_t>(P));
+            APO_CUDA(cudaMemcpy(hc.data(), icnt, sizeof(u32) * P, cudaMemcpyDeviceToHost));
+            i64 matched = 0;
+            for (u32 v : hc) matched += v > 0;
+            std::fprintf(stderr, "apo_match: streams=%d traces=%lld buckets=%lld pairs=%lld matched_pairs=%lld hits=%lld\n",
+                         nstreams, (long long)T, (long long)E, (long long)P, (long long)matched, (long long)nh);
+          }
           if (nh > 0) {
             // keys after the pair tables in the aux arena (grown if needed:
             // reserve() keeps nothing, so re-carve the pair tables first)
