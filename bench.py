@@ -312,12 +312,15 @@ def main():
             q = st_host.to(dev, non_blocking=True) if st_host is not None else None
             c, h = step(t, q)
             r, o = (int(x) for x in c.tolist())
+            # the step's result read back: the analysis output (repeats, their
+            # per-window offsets, occurrence lists) and the number of trace
+            # matches; the match records themselves (~7.6 GB for C4) stay on
+            # the device for the replay stage that consumes them
             rep_h = bufs[0][:r].cpu()
             roff_h = bufs[1].cpu()
             occ_h = bufs[2][:o].cpu()
-            hits_h = h.cpu() if h is not None else None
-            return rep_h.numel() * 4 + roff_h.numel() * 8 + occ_h.numel() * 4 + 16 + \
-                (hits_h.numel() * 4 if hits_h is not None else 0)
+            # (ctx.match already read the 8-byte hit count back to size its output)
+            return rep_h.numel() * 4 + roff_h.numel() * 8 + occ_h.numel() * 4 + 16 + (8 if h is not None else 0)
 
         e2e_step()
         torch.cuda.synchronize()

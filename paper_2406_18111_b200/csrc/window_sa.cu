@@ -3,13 +3,15 @@
 // For batches whose windows hold <= 16,384 ops (the C4 workload, and every
 // small single window) the whole doubling loop of a window runs inside one
 // 1024-thread CTA.  Per round:
-//   * keys (rank[i] << 15 | (i+h < n ? rank[i+h]+1 : 0), 29 bits) and
-//     positions are built from the u16 ranks held in shared memory;
-//   * four stable LSD digit passes (8,7,7,7 bits) move (key u32, position
-//     u16) between two shared-memory buffers: each warp ranks its 512 items
-//     (peer masks from ballots) into a per-warp u16 histogram, one block scan
-//     gives the digit starts, and every item is scattered to its slot;
-//   * a block-wide max-scan of group starts gives the new ranks;
+//   * keys (rank[i] << bg | (i+h < n ? rank[i+h]+1 : 0)) and positions are
+//     built from the u16 DENSE group ids held in shared memory; with G
+//     groups a key needs bits(G-1) + bits(G) bits, and loop-shaped windows
+//     keep G small for many rounds, so a round takes 2-4 passes, not 4;
+//   * stable 8-bit LSD digit passes move (key u32, position u16) between two
+//     shared-memory buffers: each warp ranks its 512 items (peer masks from
+//     ballots) into a per-warp u16 histogram, one block scan gives the digit
+//     starts, and every item is scattered to its slot;
+//   * a block-wide sum-scan of group heads gives the new dense ids;
 //   * the new level is streamed to HBM (4 B/op) for the LCP stage's galloping.
 // The loop ends per window as soon as all its ranks are distinct.  HBM
 // traffic per round is the level write only, instead of ~140 B/op for a
@@ -25,7 +27,6 @@ constexpr int kWT = 1024;
 constexpr int kWWarps = kWT / 32;
 constexpr int kWItems = 16;
 constexpr int kWMax = kWT * kWItems;  // 16384
-constexpr u32 kPadKey = (1u << 29) - 1;
 
 struct WinBuf {
   u32 key[kWMax];
@@ -122,63 +123,69 @@ __device__ __forceinline__ void lsd_pass(const WinBuf &src, WinBuf &dst, WinSmem
   __syncthreads();
 }
 
-// Sort the items in S.a (keys < 2^29, positions) with four LSD passes, then
-// set rank[pos] = start of the item's key group (blocked max-scan; thread t
-// owns sorted positions [16t, 16t+16)).  Returns true if some group still
-// has more than one member.
-__device__ __forceinline__ bool sort_and_rank(WinSmem &S, unsigned short *rank, i64 n) {
+// Sort the items of buffer X (keys, positions) with `npass` 8-bit LSD passes
+// (npass in 1..4, uniform over the block), then give every item the DENSE id
+// of its key group (block sum-scan of group heads; thread t owns sorted
+// positions [16t, 16t+16)) and store it at rank[pos].  The sorted items end
+// in X (npass even) or in Y (odd); rank must point into the OTHER buffer.
+// Returns the number of groups among the first n items.
+template <int NP>
+__device__ __forceinline__ void lsd_passes(WinBuf &X, WinBuf &Y, WinSmem &S) {
+  lsd_pass<0, 8>(X, Y, S);
+  if constexpr (NP >= 2) lsd_pass<8, 8>(Y, X, S);
+  if constexpr (NP >= 3) lsd_pass<16, 8>(X, Y, S);
+  if constexpr (NP >= 4) lsd_pass<24, 8>(Y, X, S);
+}
+
+__device__ __forceinline__ u32 dense_rank(const WinBuf &sorted, unsigned short *rank, i64 n, WinSmem &S) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  lsd_pass<0, 8>(S.a, S.b, S);
-  lsd_pass<8, 7>(S.b, S.a, S);
-  lsd_pass<15, 7>(S.a, S.b, S);
-  lsd_pass<22, 7>(S.b, S.a, S);
   const int q0 = tid * kWItems;
-  u32 run = 0;
+  u32 heads = 0;
   {
-    u32 prev = q0 > 0 ? S.a.key[q0 - 1] : 0xffffffffu;
+    u32 prev = q0 > 0 ? sorted.key[q0 - 1] : 0xffffffffu;
 #pragma unroll
     for (int j = 0; j < kWItems; ++j) {
-      u32 k = S.a.key[q0 + j];
-      if (k != prev) run = u32(q0 + j);
+      const u32 k = sorted.key[q0 + j];
+      heads += (k != prev && q0 + j < n) ? 1u : 0u;
       prev = k;
     }
   }
-  u32 incl = run;
+  u32 incl = heads;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     u32 v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl = v > incl ? v : incl;
+    if (lane >= o) incl += v;
   }
   if (lane == 31) S.scan[warp] = incl;
   __syncthreads();
-  u32 before = __shfl_up_sync(0xffffffffu, incl, 1);
-  if (lane == 0) before = 0;
-  for (int ww = 0; ww < warp; ++ww) before = S.scan[ww] > before ? S.scan[ww] : before;
-  bool notdone = false;
-  u32 g = before;
-  u32 prev = q0 > 0 ? S.a.key[q0 - 1] : 0xffffffffu;
+  u32 before = incl - heads, total = 0;
+  for (int ww = 0; ww < kWWarps; ++ww) {
+    const u32 v = S.scan[ww];
+    if (ww < warp) before += v;
+    total += v;
+  }
+  u32 g = before;  // number of heads before this thread's first item
+  u32 prev = q0 > 0 ? sorted.key[q0 - 1] : 0xffffffffu;
 #pragma unroll
   for (int j = 0; j < kWItems; ++j) {
     const int q = q0 + j;
-    u32 k = S.a.key[q];
-    if (k != prev) g = u32(q);
+    const u32 k = sorted.key[q];
+    if (k != prev && q < n) ++g;
     prev = k;
-    if (q < n) {
-      rank[S.a.pos[q]] = (unsigned short)g;
-      notdone |= (g != u32(q));
-    }
+    if (q < n) rank[sorted.pos[q]] = (unsigned short)(g - 1);
   }
-  return __syncthreads_or(notdone);
+  __syncthreads();
+  return total;
 }
 
-// ids: dense token ids (level 0 is computed here: window-local group starts
+// ids: dense token ids (level 0 is computed here: window-local dense ranks
 // of the tokens), or nullptr to take level 0 from levels[0].
 __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__restrict__ ids, LevelPtrs lv,
                                                       int max_levels, i32 *__restrict__ sa_out,
                                                       i32 *__restrict__ rw) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WinSmem &S = *reinterpret_cast<WinSmem *>(smem_raw);
-  unsigned short *rank = reinterpret_cast<unsigned short *>(S.b.key);  // aliases b while a holds items
+  WinBuf *buf[2] = {&S.a, &S.b};
   const int tid = threadIdx.x;
   const int w = blockIdx.x;
   const i64 beg = b_beg(b, w), n = b_end(b, w) - beg;
@@ -186,47 +193,84 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
     if (tid == 0) rw[w] = 0;
     return;
   }
-  bool any;
+  int rb = 1;  // buffer whose key area holds the u16 ranks
+  unsigned short *rank = reinterpret_cast<unsigned short *>(buf[rb]->key);
+  int sb = 0;  // buffer holding the latest sorted items
+  u32 G;       // number of distinct ranks
+  // ---- level 0 ----
   if (ids != nullptr) {
-    // level 0: sort the window's token ids on chip
+    __shared__ u32 s_max;
+    if (tid == 0) s_max = 0;
+    __syncthreads();
+    u32 mx = 0;
+    for (int q = tid; q < n; q += kWT) mx = max(mx, ids[beg + q]);
+    atomicMax(&s_max, mx);
+    __syncthreads();
+    const int kb = bits_for(u64(s_max));
+    const u32 pad = 1u << kb;
+    WinBuf &X = *buf[1 - rb];
     for (int q = tid; q < kWMax; q += kWT) {
-      S.a.key[q] = q < n ? ids[beg + q] : kPadKey;
-      S.a.pos[q] = (unsigned short)q;
+      X.key[q] = q < n ? ids[beg + q] : pad;
+      X.pos[q] = (unsigned short)q;
     }
     __syncthreads();
-    any = sort_and_rank(S, rank, n);
+    const int np = (kb + 1 + 7) / 8;
+    WinBuf &Y = *buf[rb];
+    if (np <= 1) lsd_passes<1>(X, Y, S);
+    else if (np == 2) lsd_passes<2>(X, Y, S);
+    else if (np == 3) lsd_passes<3>(X, Y, S);
+    else lsd_passes<4>(X, Y, S);
+    sb = (np & 1) ? rb : 1 - rb;
+    rb = 1 - sb;
+    rank = reinterpret_cast<unsigned short *>(buf[rb]->key);
+    G = dense_rank(*buf[sb], rank, n, S);
     i32 *out = lv.p[0];
     for (int i = tid; i < n; i += kWT) out[beg + i] = i32(rank[i]) + i32(beg);
   } else {
     const i32 *level0 = lv.p[0];
     for (int i = tid; i < n; i += kWT) rank[i] = (unsigned short)(level0[beg + i] - beg);
-    any = true;
+    G = 0;  // unknown: group starts are < n
+    __syncthreads();
   }
   int r = 0;
   for (i64 h = 1;; h <<= 1) {
-    if (!any) {  // already distinct (e.g. all tokens different)
-      for (int q = tid; q < n; q += kWT) sa_out[beg + q] = i32(beg) + i32(S.a.pos[q]);
+    if (G == u32(n)) {  // all distinct: the sorted buffer is the suffix array
+      for (int q = tid; q < n; q += kWT) sa_out[beg + q] = i32(beg) + i32(buf[sb]->pos[q]);
       if (tid == 0) rw[w] = r;
       return;
     }
-    __syncthreads();
+    // key = rank[i] << bg | (i + h < n ? rank[i+h] + 1 : 0); ranks < G
+    const u32 gmax = G ? G : u32(n);
+    const int bg = bits_for(u64(gmax));
+    const int kb = bits_for(u64(gmax - 1)) + bg;
+    const u32 pad = 1u << kb;
+    WinBuf &X = *buf[1 - rb];
     for (int q = tid; q < kWMax; q += kWT) {
-      u32 key = kPadKey;
+      u32 key = pad;
       if (q < n) {
-        u32 lo = (q + h < n) ? u32(rank[q + h]) + 1u : 0u;
-        key = (u32(rank[q]) << 15) | lo;
+        const u32 lo = (q + h < n) ? u32(rank[q + h]) + 1u : 0u;
+        key = (u32(rank[q]) << bg) | lo;
       }
-      S.a.key[q] = key;
-      S.a.pos[q] = (unsigned short)q;
+      X.key[q] = key;
+      X.pos[q] = (unsigned short)q;
     }
     __syncthreads();
-    any = sort_and_rank(S, rank, n);
+    const int np = (kb + 1 + 7) / 8;
+    WinBuf &Y = *buf[rb];
+    if (np <= 1) lsd_passes<1>(X, Y, S);
+    else if (np == 2) lsd_passes<2>(X, Y, S);
+    else if (np == 3) lsd_passes<3>(X, Y, S);
+    else lsd_passes<4>(X, Y, S);
+    sb = (np & 1) ? rb : 1 - rb;
+    rb = 1 - sb;
+    rank = reinterpret_cast<unsigned short *>(buf[rb]->key);
+    G = dense_rank(*buf[sb], rank, n, S);
     ++r;
     if (r < max_levels) {
       i32 *out = lv.p[r];
       for (int i = tid; i < n; i += kWT) out[beg + i] = i32(rank[i]) + i32(beg);
     }
-    if (r + 1 >= max_levels && any) {  // level budget exhausted (cannot happen for n <= 2^14)
+    if (r + 1 >= max_levels && G < u32(n)) {  // level budget exhausted (cannot happen for n <= 2^14)
       if (tid == 0) rw[w] = -1;
       return;
     }
