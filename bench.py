@@ -298,6 +298,8 @@ def main():
     rp_ms, rp_n, rp_bytes = ctx.profile_read(ctx.PROF_RADIX_PASS)
     sc_ms, sc_n, _ = ctx.profile_read(ctx.PROF_SCAN)
     rh_ms, rh_n, _ = ctx.profile_read(ctx.PROF_RADIX_HIST)
+    ws_ms, ws_n, ws_bytes = ctx.profile_read(ctx.PROF_WINDOW_SA)
+    mt_ms, mt_n, _ = ctx.profile_read(ctx.PROF_MATCH)
     counts = bufs[3].tolist()
     value = N * world * args.steps / (ms / 1e3)
 
@@ -347,15 +349,38 @@ def main():
     avg_pass_s = (rp_ms / rp_n) / 1e3 if rp_n else None
     achieved = (rp_bytes / rp_n) / avg_pass_s / 1e9 if rp_n else None
     tr = ncu_traffic()
-    roofline = {"bound": "hbm", "kernel": "k_onesweep (radix-sort digit pass)", "achieved": achieved,
+    roof_hbm = {"bound": "hbm", "kernel": "k_onesweep (K1 radix-sort digit pass)", "achieved": achieved,
                 "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None,
-                "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                "traffic": tr.get("k_onesweep_dram_bytes_per_launch") if tr else None,
                 "traffic_source": tr.get("source") if tr else None,
                 "launches": rp_n, "bytes_per_launch": rp_bytes / rp_n if rp_n else None,
-                "share_of_step": (rp_ms / ms) if ms else None,
-                "scan_share_of_step": sc_ms / ms if ms else None,
-                "hist_share_of_step": rh_ms / ms if ms else None}
+                "share_of_step": (rp_ms / ms) if ms else None}
+    roofline = roof_hbm
+    if ws_n and ws_ms > rp_ms:
+        # K9 (per-window on-chip suffix sort) dominates: it is bound by shared
+        # memory, so its roofline is algorithmic shared-memory bytes (counted
+        # by the kernel: 20 B/item/LSD pass + 18 B/item/round) over the
+        # shared-memory crossbar peak, 128 B/clk/SM (B300_MICROARCH.md "LDS/STS")
+        # x SMs x max SM clock (MEASURED_PEAKS.json sm_max_mhz)
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        try:
+            fmax = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
+        except Exception:
+            fmax = 1965.0
+        speak = 128.0 * nsm * fmax * 1e6 / 1e9
+        sach = (ws_bytes / ws_n) / ((ws_ms / ws_n) / 1e3) / 1e9
+        roofline = {"bound": "smem", "kernel": "k_window_sa (K9 per-window on-chip prefix doubling)",
+                    "achieved": sach, "peak": speak,
+                    "peak_source": f"derived: 128 B/clk/SM x {nsm} SMs x {fmax:.0f} MHz", "unit": "GB/s",
+                    "frac": sach / speak,
+                    "traffic": tr.get("k_window_sa_dram_bytes_per_launch") if tr else None,
+                    "traffic_source": tr.get("source") if tr else None,
+                    "launches": ws_n, "bytes_per_launch": ws_bytes / ws_n, "share_of_step": ws_ms / ms}
+    roofline["shares_of_step"] = {"k_window_sa": ws_ms / ms if ms else None,
+                                  "k_onesweep": rp_ms / ms if ms else None,
+                                  "k_stream_match": mt_ms / ms if ms else None,
+                                  "k_scan": sc_ms / ms if ms else None, "k_hist": rh_ms / ms if ms else None}
     cpu = None
     if world == 1:
         v, nwin, ops, dt = cpu_baseline_sample(tok_np, off, args.cpu_budget)
@@ -373,7 +398,8 @@ def main():
     out = {"metric": METRIC, "value": value, "unit": "ops/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "u64", "data": "synthetic", "config": desc,
-           "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+           "roofline": roofline, "roofline_hbm": roof_hbm, "cpu_baseline": cpu, "e2e": e2e,
+           "gpu_launches": int(launches),
            "clocks": clk.summary()}
     print(json.dumps(out), flush=True)
     if world > 1:

@@ -93,9 +93,12 @@ int64_t apo_launch_count(const apo_ctx *ctx);
  * stream.  apo_profile(ctx, 1) clears and starts recording, 0 stops.
  * apo_profile_read synchronises on the recorded events and returns, for
  * kernel class `kind` (0 = radix-sort digit pass, 1 = radix histogram,
- * 2 = single-pass scans, 3 = other), the summed device time in ms, the
- * number of launches and the summed ALGORITHMIC bytes (each element's
- * key/value read once and written once).  Any output pointer may be NULL. */
+ * 2 = single-pass scans, 3 = other, 4 = per-window on-chip suffix sort K9,
+ * 5 = per-stream trace search), the summed device time in ms, the number
+ * of launches and the summed ALGORITHMIC bytes: HBM bytes for kind 0 (each
+ * key/value read once and written once), shared-memory bytes for kind 4
+ * (20 B per item per LSD pass + 18 B per item per round, counted by the
+ * kernel).  Any output pointer may be NULL. */
 apo_status apo_profile(apo_ctx *ctx, int enable);
 apo_status apo_profile_read(apo_ctx *ctx, int kind, double *ms, int64_t *launches, double *bytes);
 

@@ -155,7 +155,7 @@ class Context:
         return int(self.lib.apo_launch_count(self.h))
 
     # ----------------------------------------------------------- profiler --
-    PROF_RADIX_PASS, PROF_RADIX_HIST, PROF_SCAN, PROF_OTHER = range(4)
+    PROF_RADIX_PASS, PROF_RADIX_HIST, PROF_SCAN, PROF_OTHER, PROF_WINDOW_SA, PROF_MATCH = range(6)
 
     def profile(self, enable: bool):
         self._raise(self.lib.apo_profile(self.h, 1 if enable else 0))

@@ -240,6 +240,7 @@ apo_status apo_profile(apo_ctx *ctx, int enable) {
     if (c.prof) {
       c.prof_recs.clear();
       c.ev_used = 0;
+      APO_CUDA(cudaMemset(c.d_misc + kProfDevSlot, 0, sizeof(u64) * kProfKinds));
     }
   });
 }
@@ -258,6 +259,9 @@ apo_status apo_profile_read(apo_ctx *ctx, int kind, double *ms, int64_t *launche
       by += r.bytes;
       ++k;
     }
+    u64 dev_bytes = 0;  // bytes counted by the kernels themselves
+    APO_CUDA(cudaMemcpy(&dev_bytes, c.d_misc + kProfDevSlot + kind, sizeof(u64), cudaMemcpyDeviceToHost));
+    by += double(dev_bytes);
     if (ms) *ms = t;
     if (launches) *launches = k;
     if (bytes) *bytes = by;

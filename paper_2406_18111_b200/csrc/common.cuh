@@ -90,7 +90,17 @@ struct Carver {
 };
 
 // Kernel classes timed by the optional in-library profiler (apo_profile).
-enum ProfKind { kProfRadixPass = 0, kProfRadixHist = 1, kProfScan = 2, kProfOther = 3, kProfKinds = 4 };
+enum ProfKind {
+  kProfRadixPass = 0,  // K1 digit pass (algorithmic HBM bytes known at launch)
+  kProfRadixHist = 1,
+  kProfScan = 2,
+  kProfOther = 3,
+  kProfWindowSA = 4,   // K9 (algorithmic shared-memory bytes counted on the device)
+  kProfMatch = 5,      // per-stream trace search
+  kProfKinds = 6
+};
+// device-side byte counters of the profiler live in d_misc[kProfDevSlot + kind]
+constexpr int kProfDevSlot = 4096;
 
 struct ProfRec {
   int kind;

@@ -1264,8 +1264,10 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
               APO_CUDA(cudaFuncSetAttribute(k_stream_match, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
               attr = true;
             }
+            if (c.prof) c.prof_begin(kProfMatch, 0.0, s);
             k_stream_match<<<nstreams, kSMThreads, smem, s>>>(sm, sqv, qoff, pair_e, ptr, e_lo, e_hi, ilo, icnt);
             APO_CHECK_LAUNCH();
+            if (c.prof) c.prof_end(s);
             c.launches += 3;
           } else {
             const i64 chunks = (P + kPairChunk - 1) / kPairChunk;

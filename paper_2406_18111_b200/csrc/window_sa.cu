@@ -180,9 +180,17 @@ __device__ __forceinline__ u32 dense_rank(const WinBuf &sorted, unsigned short *
 
 // ids: dense token ids (level 0 is computed here: window-local dense ranks
 // of the tokens), or nullptr to take level 0 from levels[0].
+// Algorithmic shared-memory traffic (profiling only): every LSD pass reads
+// and writes each item once (key 4 B + position 2 B, each way) and reads its
+// digit + updates a counter (8 B): 20 B per item per pass; building a round's
+// items reads two ranks and writes one item (10 B); the dense ranks read the
+// sorted item and write a rank (8 B).
+constexpr u64 kSmemPassBytes = 20, kSmemRoundBytes = 18;
+
 __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__restrict__ ids, LevelPtrs lv,
                                                       int max_levels, i32 *__restrict__ sa_out,
-                                                      i32 *__restrict__ rw) {
+                                                      i32 *__restrict__ rw, unsigned long long *smem_bytes) {
+  u64 prof = 0;  // thread 0 only
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WinSmem &S = *reinterpret_cast<WinSmem *>(smem_raw);
   WinBuf *buf[2] = {&S.a, &S.b};
@@ -224,6 +232,7 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
     rb = 1 - sb;
     rank = reinterpret_cast<unsigned short *>(buf[rb]->key);
     G = dense_rank(*buf[sb], rank, n, S);
+    prof += u64(n) * (kSmemPassBytes * np + kSmemRoundBytes);
     i32 *out = lv.p[0];
     for (int i = tid; i < n; i += kWT) out[beg + i] = i32(rank[i]) + i32(beg);
   } else {
@@ -236,7 +245,10 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
   for (i64 h = 1;; h <<= 1) {
     if (G == u32(n)) {  // all distinct: the sorted buffer is the suffix array
       for (int q = tid; q < n; q += kWT) sa_out[beg + q] = i32(beg) + i32(buf[sb]->pos[q]);
-      if (tid == 0) rw[w] = r;
+      if (tid == 0) {
+        rw[w] = r;
+        if (smem_bytes) atomicAdd(smem_bytes, (unsigned long long)prof);
+      }
       return;
     }
     // key = rank[i] << bg | (i + h < n ? rank[i+h] + 1 : 0); ranks < G
@@ -265,6 +277,7 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
     rb = 1 - sb;
     rank = reinterpret_cast<unsigned short *>(buf[rb]->key);
     G = dense_rank(*buf[sb], rank, n, S);
+    prof += u64(n) * (kSmemPassBytes * np + kSmemRoundBytes);
     ++r;
     if (r < max_levels) {
       i32 *out = lv.p[r];
@@ -290,8 +303,10 @@ void run_window_sa(Ctx &c, const Batch &b, SAWork &w, cudaStream_t s) {
   }
   LevelPtrs lv{};
   for (int r = 0; r < w.max_levels && r < 40; ++r) lv.p[r] = w.levels[r];
-  if (c.prof) c.prof_begin(kProfOther, 0.0, s);
-  k_window_sa<<<b.W, kWT, smem, s>>>(b, w.ids_valid ? w.ids : nullptr, lv, w.max_levels, w.sa, w.rw);
+  if (c.prof) c.prof_begin(kProfWindowSA, 0.0, s);
+  unsigned long long *cnt =
+      c.prof ? reinterpret_cast<unsigned long long *>(c.d_misc + kProfDevSlot + kProfWindowSA) : nullptr;
+  k_window_sa<<<b.W, kWT, smem, s>>>(b, w.ids_valid ? w.ids : nullptr, lv, w.max_levels, w.sa, w.rw, cnt);
   APO_CHECK_LAUNCH();
   if (c.prof) c.prof_end(s);
   c.launches++;
