@@ -137,49 +137,70 @@ __device__ __forceinline__ void lsd_passes(WinBuf &X, WinBuf &Y, WinSmem &S) {
   if constexpr (NP >= 4) lsd_pass<24, 8>(Y, X, S);
 }
 
+// Dense id of every sorted item's key group, stored at rank[pos].  Warp w
+// owns the sorted items [512w, 512w+512) and walks them in 16 rows of 32
+// consecutive items (conflict-free shared-memory access): a row's group heads
+// come from one ballot, the running count from popc.  Returns the number of
+// groups among the first n items.
 __device__ __forceinline__ u32 dense_rank(const WinBuf &sorted, unsigned short *rank, i64 n, WinSmem &S) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int q0 = tid * kWItems;
-  u32 heads = 0;
-  {
-    u32 prev = q0 > 0 ? sorted.key[q0 - 1] : 0xffffffffu;
-#pragma unroll
-    for (int j = 0; j < kWItems; ++j) {
-      const u32 k = sorted.key[q0 + j];
-      heads += (k != prev && q0 + j < n) ? 1u : 0u;
-      prev = k;
-    }
+  const int wbase = warp * (32 * kWItems);
+  const u32 lt = lanemask_lt_w();
+  // pass 1: heads of this warp's segment
+  u32 cnt = 0;
+#pragma unroll 4
+  for (int j = 0; j < kWItems; ++j) {
+    const int q = wbase + j * 32 + lane;
+    const u32 k = sorted.key[q];
+    const u32 pk = q > 0 ? sorted.key[q - 1] : 0xffffffffu;
+    cnt += __popc(__ballot_sync(0xffffffffu, k != pk && q < n));
   }
-  u32 incl = heads;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    u32 v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) S.scan[warp] = incl;
+  if (lane == 0) S.scan[warp] = cnt;
   __syncthreads();
-  u32 before = incl - heads, total = 0;
+  u32 before = 0, total = 0;
   for (int ww = 0; ww < kWWarps; ++ww) {
     const u32 v = S.scan[ww];
     if (ww < warp) before += v;
     total += v;
   }
-  u32 g = before;  // number of heads before this thread's first item
-  u32 prev = q0 > 0 ? sorted.key[q0 - 1] : 0xffffffffu;
-#pragma unroll
+  // pass 2: ids
+  u32 run = before;  // heads before the current row
+#pragma unroll 4
   for (int j = 0; j < kWItems; ++j) {
-    const int q = q0 + j;
+    const int q = wbase + j * 32 + lane;
     const u32 k = sorted.key[q];
-    if (k != prev && q < n) ++g;
-    prev = k;
-    if (q < n) rank[sorted.pos[q]] = (unsigned short)(g - 1);
+    const u32 pk = q > 0 ? sorted.key[q - 1] : 0xffffffffu;
+    const u32 hb = __ballot_sync(0xffffffffu, k != pk && q < n);
+    const u32 id = run + __popc(hb & lt) + ((hb >> lane) & 1u);  // heads up to and including q
+    if (q < n) rank[sorted.pos[q]] = (unsigned short)(id - 1);
+    run += __popc(hb);
   }
   __syncthreads();
   return total;
 }
 
-// ids: dense token ids (level 0 is computed here: window-local dense ranks
-// of the tokens), or nullptr to take level 0 from levels[0].
+template <int NP, bool XA>  // XA: items in S.a, other buffer S.b
+__device__ __forceinline__ void sort_round(WinSmem &S) {
+  if constexpr (XA)
+    lsd_passes<NP>(S.a, S.b, S);
+  else
+    lsd_passes<NP>(S.b, S.a, S);
+}
+
+__device__ __forceinline__ void sort_items(WinSmem &S, int np, bool xa) {
+  if (xa) {
+    if (np <= 1) sort_round<1, true>(S);
+    else if (np == 2) sort_round<2, true>(S);
+    else if (np == 3) sort_round<3, true>(S);
+    else sort_round<4, true>(S);
+  } else {
+    if (np <= 1) sort_round<1, false>(S);
+    else if (np == 2) sort_round<2, false>(S);
+    else if (np == 3) sort_round<3, false>(S);
+    else sort_round<4, false>(S);
+  }
+}
+
 // Algorithmic shared-memory traffic (profiling only): every LSD pass reads
 // and writes each item once (key 4 B + position 2 B, each way) and reads its
 // digit + updates a counter (8 B): 20 B per item per pass; building a round's
@@ -187,13 +208,13 @@ __device__ __forceinline__ u32 dense_rank(const WinBuf &sorted, unsigned short *
 // sorted item and write a rank (8 B).
 constexpr u64 kSmemPassBytes = 20, kSmemRoundBytes = 18;
 
+// ids: dense token ids (level 0 is computed here: window-local dense ranks
+// of the tokens), or nullptr to take level 0 from levels[0].
 __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__restrict__ ids, LevelPtrs lv,
                                                       int max_levels, i32 *__restrict__ sa_out,
                                                       i32 *__restrict__ rw, unsigned long long *smem_bytes) {
-  u64 prof = 0;  // thread 0 only
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WinSmem &S = *reinterpret_cast<WinSmem *>(smem_raw);
-  WinBuf *buf[2] = {&S.a, &S.b};
   const int tid = threadIdx.x;
   const int w = blockIdx.x;
   const i64 beg = b_beg(b, w), n = b_end(b, w) - beg;
@@ -201,10 +222,14 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
     if (tid == 0) rw[w] = 0;
     return;
   }
-  int rb = 1;  // buffer whose key area holds the u16 ranks
-  unsigned short *rank = reinterpret_cast<unsigned short *>(buf[rb]->key);
-  int sb = 0;  // buffer holding the latest sorted items
-  u32 G;       // number of distinct ranks
+  u64 prof = 0;
+  // The items of a round are built in buffer X and sorted with np passes;
+  // they end in X (np even) or in the other buffer.  The u16 ranks live in
+  // the key area of the buffer NOT holding the sorted items.
+  bool rank_in_b = true;  // ranks in S.b.key, items built in S.a
+  bool sorted_in_a = true;
+  u32 G;  // number of distinct ranks
+  auto rank_ptr = [&]() { return reinterpret_cast<unsigned short *>(rank_in_b ? S.b.key : S.a.key); };
   // ---- level 0 ----
   if (ids != nullptr) {
     __shared__ u32 s_max;
@@ -216,27 +241,23 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
     __syncthreads();
     const int kb = bits_for(u64(s_max));
     const u32 pad = 1u << kb;
-    WinBuf &X = *buf[1 - rb];
-    for (int q = tid; q < kWMax; q += kWT) {
-      X.key[q] = q < n ? ids[beg + q] : pad;
-      X.pos[q] = (unsigned short)q;
+    for (int q = tid; q < kWMax; q += kWT) {  // items into S.a
+      S.a.key[q] = q < n ? ids[beg + q] : pad;
+      S.a.pos[q] = (unsigned short)q;
     }
     __syncthreads();
     const int np = (kb + 1 + 7) / 8;
-    WinBuf &Y = *buf[rb];
-    if (np <= 1) lsd_passes<1>(X, Y, S);
-    else if (np == 2) lsd_passes<2>(X, Y, S);
-    else if (np == 3) lsd_passes<3>(X, Y, S);
-    else lsd_passes<4>(X, Y, S);
-    sb = (np & 1) ? rb : 1 - rb;
-    rb = 1 - sb;
-    rank = reinterpret_cast<unsigned short *>(buf[rb]->key);
-    G = dense_rank(*buf[sb], rank, n, S);
+    sort_items(S, np, true);
+    sorted_in_a = (np & 1) == 0;
+    rank_in_b = sorted_in_a;
+    G = dense_rank(sorted_in_a ? S.a : S.b, rank_ptr(), n, S);
     prof += u64(n) * (kSmemPassBytes * np + kSmemRoundBytes);
+    unsigned short *rank = rank_ptr();
     i32 *out = lv.p[0];
     for (int i = tid; i < n; i += kWT) out[beg + i] = i32(rank[i]) + i32(beg);
   } else {
     const i32 *level0 = lv.p[0];
+    unsigned short *rank = rank_ptr();
     for (int i = tid; i < n; i += kWT) rank[i] = (unsigned short)(level0[beg + i] - beg);
     G = 0;  // unknown: group starts are < n
     __syncthreads();
@@ -244,7 +265,8 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
   int r = 0;
   for (i64 h = 1;; h <<= 1) {
     if (G == u32(n)) {  // all distinct: the sorted buffer is the suffix array
-      for (int q = tid; q < n; q += kWT) sa_out[beg + q] = i32(beg) + i32(buf[sb]->pos[q]);
+      const unsigned short *pos = sorted_in_a ? S.a.pos : S.b.pos;
+      for (int q = tid; q < n; q += kWT) sa_out[beg + q] = i32(beg) + i32(pos[q]);
       if (tid == 0) {
         rw[w] = r;
         if (smem_bytes) atomicAdd(smem_bytes, (unsigned long long)prof);
@@ -256,32 +278,31 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
     const int bg = bits_for(u64(gmax));
     const int kb = bits_for(u64(gmax - 1)) + bg;
     const u32 pad = 1u << kb;
-    WinBuf &X = *buf[1 - rb];
+    const unsigned short *rank = rank_ptr();
+    const bool xa = rank_in_b;  // items go to the buffer without the ranks
+    u32 *xk = xa ? S.a.key : S.b.key;
+    unsigned short *xp = xa ? S.a.pos : S.b.pos;
     for (int q = tid; q < kWMax; q += kWT) {
       u32 key = pad;
       if (q < n) {
         const u32 lo = (q + h < n) ? u32(rank[q + h]) + 1u : 0u;
         key = (u32(rank[q]) << bg) | lo;
       }
-      X.key[q] = key;
-      X.pos[q] = (unsigned short)q;
+      xk[q] = key;
+      xp[q] = (unsigned short)q;
     }
     __syncthreads();
     const int np = (kb + 1 + 7) / 8;
-    WinBuf &Y = *buf[rb];
-    if (np <= 1) lsd_passes<1>(X, Y, S);
-    else if (np == 2) lsd_passes<2>(X, Y, S);
-    else if (np == 3) lsd_passes<3>(X, Y, S);
-    else lsd_passes<4>(X, Y, S);
-    sb = (np & 1) ? rb : 1 - rb;
-    rb = 1 - sb;
-    rank = reinterpret_cast<unsigned short *>(buf[rb]->key);
-    G = dense_rank(*buf[sb], rank, n, S);
+    sort_items(S, np, xa);
+    sorted_in_a = ((np & 1) == 0) == xa;
+    rank_in_b = sorted_in_a;
+    unsigned short *nrank = rank_ptr();
+    G = dense_rank(sorted_in_a ? S.a : S.b, nrank, n, S);
     prof += u64(n) * (kSmemPassBytes * np + kSmemRoundBytes);
     ++r;
     if (r < max_levels) {
       i32 *out = lv.p[r];
-      for (int i = tid; i < n; i += kWT) out[beg + i] = i32(rank[i]) + i32(beg);
+      for (int i = tid; i < n; i += kWT) out[beg + i] = i32(nrank[i]) + i32(beg);
     }
     if (r + 1 >= max_levels && G < u32(n)) {  // level budget exhausted (cannot happen for n <= 2^14)
       if (tid == 0) rw[w] = -1;
