@@ -392,16 +392,6 @@ __global__ void k_trace_buckets(StreamMatch m, const u64 *__restrict__ sorted_to
   ecnt[t] = u32(lo - first);
 }
 
-struct ExclScanU32F {  // in-place exclusive sum
-  u32 *a;
-  __device__ u32 load(i64 i) const { return a[i]; }
-  __device__ bool store(i64 i, u32, u32 excl) const {
-    a[i] = excl;
-    return false;
-  }
-  __device__ u32 *flag() const { return nullptr; }
-};
-
 struct PairBaseF {  // exclusive scan of per-trace pair counts (u32)
   const u32 *cnt;
   u32 *base;
@@ -518,9 +508,16 @@ __global__ void k_pair_list(const u32 *__restrict__ pbase, const u32 *__restrict
   }
 }
 
-__global__ void k_count_q(const u64 *__restrict__ qkey, i64 P, u32 *__restrict__ cnt) {
-  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < P) atomicAdd(&cnt[qkey[i]], 1u);
+// qoff[q] = first index of stream q in the stream-sorted pair list
+__global__ void k_q_offsets(const u64 *__restrict__ qkey, i64 P, int S, u32 *__restrict__ qoff) {
+  const i64 q = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q > S) return;
+  i64 lo = 0, hi = P;
+  while (lo < hi) {
+    const i64 mid = (lo + hi) >> 1;
+    if (i64(qkey[mid]) < q) lo = mid + 1; else hi = mid;
+  }
+  qoff[q] = u32(lo);
 }
 
 // Warp-cooperative compare of trace t with the on-chip stream suffix at p;
@@ -529,31 +526,42 @@ __global__ void k_count_q(const u64 *__restrict__ qkey, i64 P, u32 *__restrict__
 __device__ __forceinline__ int warp_cmp_smem(const u64 *__restrict__ S, i64 p, i64 n, const u64 *__restrict__ t,
                                              u64 r0, u64 r1, i64 L, i64 from, i64 *lcp) {
   const int lane = threadIdx.x & 31;
-  for (i64 base = from; base < L; base += 32) {
+  i64 base = from;
+  // tokens 0..63 of the trace come from registers
+  for (; base < L && base < 64; base += 32) {
     const i64 k = base + lane;
-    u64 x;
-    if (base < 64) {  // all lanes take this branch together
-      const int src = int(k & 31);
-      const u64 a = __shfl_sync(0xffffffffu, r0, src);
-      const u64 b = __shfl_sync(0xffffffffu, r1, src);
-      x = k < 32 ? a : (k < 64 ? b : (k < L ? t[k] : 0ull));
-    } else {
-      x = k < L ? t[k] : 0ull;
-    }
+    const int src = int(k & 31);
+    const u64 a = __shfl_sync(0xffffffffu, r0, src);
+    const u64 b = __shfl_sync(0xffffffffu, r1, src);
+    const u64 x = k < 32 ? a : (k < 64 ? b : (k < L ? t[k] : 0ull));
     int res = 0;
-    if (k < L) {
-      if (p + k >= n) {
-        res = 1;
-      } else {
-        const u64 y = S[p + k];
-        res = x == y ? 0 : (x < y ? -1 : 1);
-      }
-    }
+    if (k < L) res = (p + k >= n) ? 1 : (x == S[p + k] ? 0 : (x < S[p + k] ? -1 : 1));
     const u32 m = __ballot_sync(0xffffffffu, res != 0);
     if (m) {
       const int f = __ffs(m) - 1;
       *lcp = base + f;
       return __shfl_sync(0xffffffffu, res, f);
+    }
+  }
+  // later tokens: four 32-token chunks per round trip to L2/HBM
+  for (; base < L; base += 128) {
+    u64 x[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const i64 k = base + c * 32 + lane;
+      x[c] = k < L ? t[k] : 0ull;
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const i64 k = base + c * 32 + lane;
+      int res = 0;
+      if (k < L) res = (p + k >= n) ? 1 : (x[c] == S[p + k] ? 0 : (x[c] < S[p + k] ? -1 : 1));
+      const u32 m = __ballot_sync(0xffffffffu, res != 0);
+      if (m) {
+        const int f = __ffs(m) - 1;
+        *lcp = base + c * 32 + f;
+        return __shfl_sync(0xffffffffu, res, f);
+      }
     }
   }
   *lcp = L;
@@ -1253,11 +1261,8 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             bool aq = radix_sort_u64_u32(c, qk, qv, qk_alt, qv_alt, P, 0, bits_for(u64(nstreams - 1)), s);
             const u64 *sqk = aq ? qk_alt : qk;
             const u32 *sqv = aq ? qv_alt : qv;
-            APO_CUDA(cudaMemsetAsync(qoff, 0, sizeof(u32) * (nstreams + 1), s));
-            k_count_q<<<grid_for(P, T256), T256, 0, s>>>(sqk, P, qoff);
+            k_q_offsets<<<grid_for(i64(nstreams) + 1, T256), T256, 0, s>>>(sqk, P, nstreams, qoff);
             APO_CHECK_LAUNCH();
-            ExclScanU32F xf{qoff};
-            launch_scan<false>(c, i64(nstreams) + 1, xf, s);
             const size_t smem = sizeof(u64) * kSMMax + 2 * sizeof(unsigned short) * kSMMax;
             static bool attr = false;
             if (!attr) {
