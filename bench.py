@@ -11,8 +11,11 @@ one batch, inputs resident in HBM: apo_find_repeats_batched over every window
 candidate trace set (apo_trie_build), and MATCH_ALL matching of every
 window's next 16,384 ops (apo_match).  Multi-GPU (torchrun, one process per
 GPU): every rank analyses its own C4-shaped batch (weak scaling); the only
-exchange is the NCCL all-gather of the candidate trace lists, after which
-every rank builds the same union trace set and matches its own streams.  The
+exchange is the union of the candidate trace lists: each rank stages its list
+in a symmetric (NVLink-mapped) buffer and apo_trie_build_traces_multi pulls
+the peers' lists over NVLink inside the kernel that hashes them (sizes and
+offsets travel by NCCL), after which every rank holds the same union trace
+set and matches its own streams.  The
 time is the max over ranks.  Prints ONE JSON line on rank 0.
 
 --impl reference times the CPU oracle (tier 0, the literal Alg. 2) on the
@@ -198,6 +201,8 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C2", "C3", "C4", "C5"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--workload-rank", type=int, default=None,
+                    help="diagnostic: generate the workload of this rank (per-rank seed) on a single GPU")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -213,10 +218,12 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2406_18111_b200.dist import gather_traces
+    from paper_2406_18111_b200.dist import TraceExchange
     dev = torch.device("cuda", local)
     ctx = Context(local)
-    tok_np, off, st_np, soff, desc = make_workload(args.config, rank)
+    exchange = TraceExchange(ctx) if world > 1 else None
+    tok_np, off, st_np, soff, desc = make_workload(
+        args.config, rank if args.workload_rank is None else args.workload_rank)
     N = int(off[-1])
     W = len(off) - 1
     cap = N // MIN_LEN + 1
@@ -242,9 +249,7 @@ def main():
             if timed:
                 evs[2].record(s)
             if world > 1:
-                tt, to = trie.traces()
-                at, ao = gather_traces(tt, to)
-                trie = ctx.trie_build_traces(at, ao)
+                trie = exchange.union(trie)
             if timed:
                 evs[3].record(s)
             hits = ctx.match(trie, streams, soff, cap=last.get("hits", 1 << 22))

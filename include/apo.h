@@ -215,6 +215,21 @@ apo_status apo_trie_build(apo_ctx *ctx, const uint64_t *d_tok, const int64_t *h_
 apo_status apo_trie_build_traces(apo_ctx *ctx, const uint64_t *d_tr, const int64_t *h_tr_off,
                                  int32_t ntraces, apo_trie **out, void *stream);
 
+/* Union trace set of nsrc (1..16) trace lists -- the multi-GPU exchange of
+ * every rank builds the same union of all ranks' candidate
+ * lists.  List r holds h_src_ntr[r] traces; its tokens are at h_src_tok[r],
+ * a device pointer READABLE FROM ctx's DEVICE (a local allocation, or a peer
+ * rank's buffer mapped over NVLink, e.g. CUDA IPC / symmetric memory), and
+ * its host int64 offsets h_src_off[r][0 .. ntr] start at 0 (non-empty
+ * traces).  The library pulls every list into local memory in the same pass
+ * that hashes the pieces (no separate gather); the result is identical to
+ * apo_trie_build_traces on the concatenation of the lists in source order.
+ * The sources must stay unchanged until the call returns (it synchronises
+ * `stream`); the caller orders the peers' writes before it (e.g. a barrier). */
+apo_status apo_trie_build_traces_multi(apo_ctx *ctx, int32_t nsrc, const uint64_t *const *h_src_tok,
+                                       const int64_t *const *h_src_off, const int32_t *h_src_ntr,
+                                       apo_trie **out, void *stream);
+
 void apo_trie_destroy(apo_trie *trie);
 
 /* Sizes of the trace set: number of traces, total tokens, longest trace. */

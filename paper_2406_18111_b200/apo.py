@@ -67,6 +67,7 @@ _SIGS = {
     "apo_history_count": (ctypes.c_int64, [_VP]),
     "apo_trie_build": (ctypes.c_int, [_VP, _VP, _P_I64, _I32, _VP, _VP, _I32, _I32, ctypes.POINTER(_VP), _VP]),
     "apo_trie_build_traces": (ctypes.c_int, [_VP, _VP, _P_I64, _I32, ctypes.POINTER(_VP), _VP]),
+    "apo_trie_build_traces_multi": (ctypes.c_int, [_VP, _I32, _VP, _VP, _VP, ctypes.POINTER(_VP), _VP]),
     "apo_trie_destroy": (None, [_VP]),
     "apo_trie_info": (ctypes.c_int, [_VP, _P_I64, _P_I64, _P_I64]),
     "apo_trie_copy": (ctypes.c_int, [_VP, _VP, _P_I64, _VP]),
@@ -291,6 +292,34 @@ class Context:
                                                    _stream(self.device)))
         return Trie(self, h)
 
+    def trie_build_traces_multi(self, sources) -> "Trie":
+        """Union trace set of several trace lists, pulled and hashed in one pass.
+
+        sources: sequence of (device pointer int or CUDA uint64 tensor, host
+        int64 offsets[ntr+1]); a pointer may be a peer rank's buffer mapped
+        into this device (symmetric memory over NVLink).  Same result as
+        trie_build_traces on the concatenation."""
+        n = len(sources)
+        ptrs = (ctypes.c_uint64 * n)()
+        offs = []
+        ntr = (ctypes.c_int32 * n)()
+        for r, (tok, off) in enumerate(sources):
+            o = _host_off(off)
+            offs.append(o)
+            ntr[r] = len(o) - 1
+            if isinstance(tok, torch.Tensor):
+                if len(o) > 1:
+                    _check_tok(tok, self.device)
+                ptrs[r] = tok.data_ptr() if tok.numel() else 0
+            else:
+                ptrs[r] = int(tok)
+        optrs = (ctypes.c_void_p * n)(*[o.ctypes.data for o in offs])
+        h = ctypes.c_void_p()
+        self._raise(self.lib.apo_trie_build_traces_multi(self.h, n, ctypes.cast(ptrs, _VP), ctypes.cast(optrs, _VP),
+                                                         ctypes.cast(ntr, _VP), ctypes.byref(h),
+                                                         _stream(self.device)))
+        return Trie(self, h)
+
     def match(self, trie: "Trie", streams: torch.Tensor, off, cap: int | None = None):
         """MATCH_ALL -> int32[h,3] rows (stream, end_pos, trace_id) sorted."""
         streams = _check_tok(streams, self.device)
@@ -373,10 +402,17 @@ class Trie:
         self.ctx._raise(self.ctx.lib.apo_trie_info(self.h, ctypes.byref(t), ctypes.byref(n), ctypes.byref(m)))
         return t.value, n.value, m.value
 
-    def traces(self):
-        """-> (tokens uint64 device tensor, host int64 offsets[T+1])."""
+    def traces(self, out: torch.Tensor | None = None):
+        """-> (tokens uint64 device tensor, host int64 offsets[T+1]); `out`
+        (contiguous, >= ntokens elements, 8-byte dtype) receives the tokens
+        instead of a new tensor."""
         T, n, _ = self.info()
-        tok = torch.empty(max(n, 1), dtype=torch.uint64, device=self.ctx.device)
+        if out is None:
+            tok = torch.empty(max(n, 1), dtype=torch.uint64, device=self.ctx.device)
+        else:
+            if not out.is_cuda or out.element_size() != 8 or not out.is_contiguous() or out.numel() < n:
+                raise ValueError("out must be a contiguous 8-byte CUDA tensor with >= ntokens elements")
+            tok = out
         off = np.zeros(T + 1, dtype=np.int64)
         self.ctx._raise(self.ctx.lib.apo_trie_copy(self.h, _ptr(tok), off.ctypes.data_as(_P_I64),
                                                    _stream(self.ctx.device)))

@@ -750,30 +750,55 @@ __global__ void k_prefix_keys(const u32 *__restrict__ ids, i64 U, const u64 *__r
 constexpr int kMaxTie = 256;
 
 // Insertion sort of each run of equal (length, token 0, token 1) with the
-// full comparator (one thread per run, started at the run's first element).
+// full comparator, one warp per run (started at the run's first element):
+// a comparison reads both pieces 32 tokens at a time (coalesced) and the
+// first differing token is found with a ballot, so two long pieces sharing a
+// long prefix cost one round trip per 32 tokens instead of one per token.
 // *worst receives the largest run length; runs longer than kMaxTie are left
 // unsorted (the caller then falls back to the bitonic network).
 __global__ void k_tie_sort(u32 *__restrict__ order, i64 U, TraceCmp cmp, u32 *__restrict__ worst) {
-  const i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  const i64 c = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (c >= U) return;
   auto same = [&](u32 a, u32 b) {
     const i64 la = cmp.off[a + 1] - cmp.off[a], lb = cmp.off[b + 1] - cmp.off[b];
     return la == lb && cmp.pk[3 * i64(a)] == cmp.pk[3 * i64(b)] && cmp.pk[3 * i64(a) + 1] == cmp.pk[3 * i64(b) + 1];
   };
-  if (c > 0 && same(order[c - 1], order[c])) return;  // not a run start
+  if (c > 0 && same(order[c - 1], order[c])) return;  // not a run start (warp-uniform)
   i64 e = c + 1;
   while (e < U && same(order[c], order[e])) ++e;
   const i64 g = e - c;
-  if (g > 1) atomicMax(worst, u32(g));
+  if (g > 1 && lane == 0) atomicMax(worst, u32(g));
   if (g < 2 || g > kMaxTie) return;
+  // pieces of one run share their length (and first two tokens)
+  const i64 L = cmp.off[order[c] + 1] - cmp.off[order[c]];
+  auto greater = [&](u32 a, u32 b) -> bool {  // cmp(a, b) > 0
+    const u64 *ta = cmp.tok + cmp.off[a], *tb = cmp.tok + cmp.off[b];
+    for (i64 k0 = 2; k0 < L; k0 += 32) {
+      const i64 k = k0 + lane;
+      const u64 x = k < L ? ta[k] : 0, y = k < L ? tb[k] : 0;
+      const unsigned m = __ballot_sync(0xffffffffu, x != y);
+      if (m) {
+        const int f = __ffs(m) - 1;
+        const u64 xf = __shfl_sync(0xffffffffu, x, f), yf = __shfl_sync(0xffffffffu, y, f);
+        return xf > yf;
+      }
+    }
+    return a > b;
+  };
   for (i64 i = c + 1; i < e; ++i) {
     const u32 x = order[i];
     i64 j = i - 1;
-    while (j >= c && cmp.cmp(order[j], x) > 0) {
-      order[j + 1] = order[j];
+    u32 oj = order[j];
+    while (j >= c && greater(oj, x)) {
+      __syncwarp();
+      if (lane == 0) order[j + 1] = oj;
       --j;
+      if (j >= c) oj = order[j];  // no lane has written order[j]
     }
-    order[j + 1] = x;
+    __syncwarp();
+    if (lane == 0) order[j + 1] = x;
+    __syncwarp();
   }
 }
 
@@ -783,25 +808,51 @@ __device__ __forceinline__ u64 mix64(u64 z) {
   return z ^ (z >> 31);
 }
 
+// Sources of the pieces when the trace set is built from several trace
+// lists (the multi-GPU union): list r's tokens live at tok[r] (a local
+// allocation or a peer mapping over NVLink) and its pieces are the global
+// pieces [first[r], first[r + 1]) whose tokens start at global token base[r].
+constexpr int kMaxSrc = 16;
+struct PieceSrc {
+  const u64 *tok[kMaxSrc];
+  i64 first[kMaxSrc + 1];
+  i64 base[kMaxSrc + 1];
+  int n;
+  u64 *gather;  // non-null: copy every piece here (at its global offset)
+};
+
 // warp per piece: a position-keyed content hash (only used to bring equal
 // contents together; equality is always verified token by token) and the
-// piece's first three tokens.  keys = (maxlen - len) << 0 handled by a
-// second sort; here keys[i] = hash, vals[i] = i.
+// piece's first three tokens; keys[i] = hash, vals[i] = i.  With src.gather
+// set, the pieces are pulled from their source lists (peer memory for the
+// remote ranks' lists) into the local buffer in the same pass.
+template <bool GATHER>
 __global__ void k_piece_hash(const u64 *__restrict__ tok, const i64 *__restrict__ off, i64 np,
-                             u64 *__restrict__ hkey, u32 *__restrict__ hval, u64 *__restrict__ pk) {
+                             u64 *__restrict__ hkey, u32 *__restrict__ hval, u64 *__restrict__ pk, PieceSrc src) {
   const i64 p = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (p >= np) return;
   const i64 o = off[p], L = off[p + 1] - o;
+  const u64 *from = tok + o;
+  if (GATHER) {
+    int r = 0;
+    while (r + 1 < src.n && p >= src.first[r + 1]) ++r;
+    from = src.tok[r] + (o - src.base[r]);
+  }
   u64 h = 0;
-  for (i64 k = lane; k < L; k += 32) h += mix64(tok[o + k] ^ mix64(u64(k) + 0x9E3779B97F4A7C15ull));
+#pragma unroll 4
+  for (i64 k = lane; k < L; k += 32) {
+    const u64 x = from[k];
+    if (GATHER) src.gather[o + k] = x;
+    h += mix64(x ^ mix64(u64(k) + 0x9E3779B97F4A7C15ull));
+  }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) h += __shfl_xor_sync(0xffffffffu, h, d);
   if (lane == 0) {
     hkey[p] = h;
     hval[p] = u32(p);
   }
-  if (lane < 3) pk[3 * p + lane] = lane < L ? tok[o + lane] : 0ull;
+  if (lane < 3) pk[3 * p + lane] = lane < L ? from[lane] : 0ull;
 }
 
 __global__ void k_len_keys(const u32 *__restrict__ order, const i64 *__restrict__ off, i64 np, i64 maxlen,
@@ -859,7 +910,8 @@ __global__ void k_src_of(const u32 *__restrict__ uniq, const i64 *__restrict__ p
 //     the three prefix tokens kept in a compact array);
 //  3. an exact neighbour comparison in that order (catches any content that
 //     step 1 left split by a hash collision), ids, copy-out in id order.
-void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<i64> &h_poff, cudaStream_t s) {
+void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<i64> &h_poff, cudaStream_t s,
+                     const PieceSrc *src = nullptr) {
   const i64 np = i64(h_poff.size()) - 1;
   const i64 N = h_poff.back();
   tr->T = 0;
@@ -899,7 +951,10 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
   plan(cv);
   APO_CUDA(cudaMemcpyAsync(d_poff, h_poff.data(), sizeof(i64) * (np + 1), cudaMemcpyHostToDevice, s));
   // 1. merge identical pieces
-  k_piece_hash<<<grid_for(np * 32, T256), T256, 0, s>>>(d_ptok, d_poff, np, hk, hv, pk);
+  if (src)
+    k_piece_hash<true><<<grid_for(np * 32, T256), T256, 0, s>>>(d_ptok, d_poff, np, hk, hv, pk, *src);
+  else
+    k_piece_hash<false><<<grid_for(np * 32, T256), T256, 0, s>>>(d_ptok, d_poff, np, hk, hv, pk, PieceSrc{});
   APO_CHECK_LAUNCH();
   APO_CUDA(cudaMemcpyAsync(hk_keep, hk, sizeof(u64) * np, cudaMemcpyDeviceToDevice, s));
   bool a1 = radix_sort_u64_u32(c, hk, hv, hk_alt, hv_alt, np, 0, 64, s);
@@ -940,7 +995,7 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
     x = radix_sort_u64_u32(c, rk, rv, rk_alt, rv_alt, U, 0, lenbits, s);
     if (x) { std::swap(rk, rk_alt); std::swap(rv, rv_alt); }
     APO_CUDA(cudaMemsetAsync(scal + 2, 0, sizeof(i64), s));
-    k_tie_sort<<<grid_for(U, T256), T256, 0, s>>>(rv, U, cmp, reinterpret_cast<u32 *>(scal + 2));
+    k_tie_sort<<<grid_for(U * 32, T256), T256, 0, s>>>(rv, U, cmp, reinterpret_cast<u32 *>(scal + 2));
     APO_CHECK_LAUNCH();
     c.launches += 4;
     const u32 worst = c.read_u32(reinterpret_cast<const u32 *>(scal + 2), s);
@@ -1104,6 +1159,49 @@ apo_status apo_trie_build_traces(apo_ctx *ctx, const uint64_t *d_tr, const int64
     require(h[0] == 0, "h_tr_off[0] must be 0");
     require(ntraces == 0 || d_tr != nullptr, "NULL device pointer");
     build_trace_set(c, tr, d_tr, h, static_cast<cudaStream_t>(stream));
+  });
+  if (st != APO_OK) {
+    apo_trie_destroy(tr);
+    return st;
+  }
+  *out = tr;
+  return APO_OK;
+}
+
+apo_status apo_trie_build_traces_multi(apo_ctx *ctx, int32_t nsrc, const uint64_t *const *h_src_tok,
+                                       const int64_t *const *h_src_off, const int32_t *h_src_ntr, apo_trie **out,
+                                       void *stream) {
+  if (!out) return APO_ERR_INVALID;
+  *out = nullptr;
+  apo_trie *tr = new apo_trie();
+  tr->ctx = ctx;
+  apo_status st = trie_guard(ctx, [&](Ctx &c) {
+    require(nsrc >= 1 && nsrc <= kMaxSrc && h_src_tok && h_src_off && h_src_ntr, "invalid argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    PieceSrc src{};
+    src.n = nsrc;
+    std::vector<i64> h(1, 0);
+    for (int r = 0; r < nsrc; ++r) {
+      const int32_t nt = h_src_ntr[r];
+      const int64_t *o = h_src_off[r];
+      require(nt >= 0 && (nt == 0 || o != nullptr), "invalid argument");
+      require(nt == 0 || o[0] == 0, "source offsets must start at 0");
+      require(nt == 0 || h_src_tok[r] != nullptr, "NULL source pointer");
+      src.tok[r] = h_src_tok[r];
+      src.first[r] = i64(h.size()) - 1;
+      src.base[r] = h.back();
+      for (int t = 0; t < nt; ++t) {
+        require(o[t + 1] > o[t], "traces must be non-empty");
+        h.push_back(src.base[r] + o[t + 1]);
+      }
+    }
+    src.first[nsrc] = i64(h.size()) - 1;
+    src.base[nsrc] = h.back();
+    const i64 N = h.back();
+    // the gathered tokens: a second scratch arena (build_trace_set carves the first)
+    c.aux.reserve(sizeof(u64) * size_t(std::max<i64>(N, 1)), s);
+    src.gather = reinterpret_cast<u64 *>(c.aux.base);
+    build_trace_set(c, tr, src.gather, h, s, &src);
   });
   if (st != APO_OK) {
     apo_trie_destroy(tr);

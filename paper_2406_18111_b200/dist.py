@@ -52,3 +52,66 @@ def gather_traces(tokens: torch.Tensor, off: np.ndarray, group=None):
     all_len = np.concatenate(lengths) if lengths else np.zeros(0, np.int64)
     all_off = np.concatenate([[0], np.cumsum(all_len)]).astype(np.int64)
     return all_tok, all_off
+
+
+class TraceExchange:
+    """The multi-GPU union over NVLink peer memory.
+
+    Each rank copies its local trace list into a symmetric buffer (one
+    allocation per rank, mapped into every peer by torch's symmetric memory:
+    plumbing), the ranks exchange their (small) host offsets, and every rank
+    calls apo_trie_build_traces_multi with the peers' mapped pointers: the
+    library kernel pulls the remote lists over NVLink in the same pass that
+    hashes them, so there is no separate all-gather buffer, padding or
+    concatenation.  Device barriers on the symmetric handle order the copies
+    before the pulls and the pulls before the next step's copies.
+
+    The buffer is reused across steps and regrown (collectively: every rank
+    sees the same global maximum) when a list no longer fits.
+    """
+
+    def __init__(self, ctx, group=None):
+        import torch.distributed._symmetric_memory as symm_mem
+        self._symm = symm_mem
+        self.ctx = ctx
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.dev = ctx.device if isinstance(ctx.device, torch.device) else torch.device("cuda", ctx.device)
+        self.cap = 0
+        self.buf = None
+        self.hdl = None
+
+    def _ensure(self, need: int):
+        if need <= self.cap:
+            return
+        cap = int(need * 1.25) + 4096
+        self.buf = self._symm.empty(cap, dtype=torch.int64, device=self.dev)
+        self.hdl = self._symm.rendezvous(self.buf, self.group)
+        self.cap = cap
+
+    def union(self, trie):
+        """-> the union Trie of every rank's `trie` (identical on all ranks)."""
+        T, n, _ = trie.info()
+        sizes = torch.tensor([n, T], dtype=torch.int64, device=self.dev)
+        all_sizes = torch.empty(self.world * 2, dtype=torch.int64, device=self.dev)
+        dist.all_gather_into_tensor(all_sizes, sizes, group=self.group)
+        all_sizes = all_sizes.view(self.world, 2).cpu().numpy()
+        self._ensure(max(int(all_sizes[:, 0].max()), 1))
+        self.hdl.barrier(channel=0)          # peers are done reading the previous step's lists
+        _, off = trie.traces(out=self.buf)   # local list -> own symmetric buffer
+        max_tr = max(int(all_sizes[:, 1].max()), 1)
+        lens = torch.zeros(max_tr, dtype=torch.int64, device=self.dev)
+        if T:
+            lens[:T] = torch.from_numpy(np.diff(off)).to(self.dev)
+        gl = torch.empty(self.world * max_tr, dtype=torch.int64, device=self.dev)
+        dist.all_gather_into_tensor(gl, lens, group=self.group)
+        gl = gl.view(self.world, max_tr).cpu().numpy()
+        self.hdl.barrier(channel=0)          # every rank's copy is complete
+        ptrs = self.hdl.buffer_ptrs
+        sources = []
+        for r in range(self.world):
+            nr = int(all_sizes[r, 1])
+            o = np.concatenate([[0], np.cumsum(gl[r, :nr])]).astype(np.int64)
+            sources.append((ptrs[r], o))
+        return self.ctx.trie_build_traces_multi(sources)

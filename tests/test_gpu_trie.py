@@ -63,6 +63,27 @@ def test_trie_from_traces_order_dedup(ctx):
     assert got == sorted(set(allt), key=lambda t: (-len(t), t))
 
 
+def test_trie_order_long_shared_prefixes(ctx):
+    """Tie groups of equal (length, token 0, token 1) whose members share long
+    prefixes: the warp-cooperative comparator must scan several 32-token
+    rounds before the first difference (and see exact duplicates through)."""
+    rng = gen.Rng(17)
+    pre = [int(x) for x in gen.random_string(99, 150, 4)]
+    allt = []
+    for i in range(300):
+        L = 150 + 40 * rng.below(3)
+        cut = rng.below(L)
+        t = pre[:min(cut, 150)] + [int(x) for x in gen.random_string(500 + i, L, 2)][min(cut, 150):]
+        allt.append(tuple(t[:L]))
+    allt += allt[:20]
+    flat = np.array([x for t in allt for x in t], dtype=np.uint64)
+    toff = np.cumsum([0] + [len(t) for t in allt]).astype(np.int64)
+    trie = ctx.trie_build_traces(dev(flat), toff)
+    got_tok, got_off = trie.traces()
+    got = trace_list(got_tok.cpu().numpy(), got_off)
+    assert got == sorted(set(allt), key=lambda t: (-len(t), t))
+
+
 def test_match_small_examples(ctx):
     # SPEC.md S:297: trie {abc} on stream "ababc" completes at the last token
     tr = gen.from_text("abc")
@@ -143,3 +164,31 @@ def test_match_medium_batches_sampled_streams(ctx):
             got = hits[hits[:, 0] == q].copy()
             got[:, 0] = 0
             assert np.array_equal(got, want), (W, q)
+
+
+def test_trie_build_traces_multi_sources(ctx):
+    """The multi-source union (the multi-GPU exchange's builder; here every
+    source is a local buffer) equals trie_build_traces on the concatenation,
+    including duplicates across sources and empty sources."""
+    lists = []
+    for seed, (W, win) in enumerate(((8, 2000), (6, 3000), (0, 0), (8, 2000))):
+        if W == 0:
+            lists.append((torch.zeros(0, dtype=torch.uint64, device="cuda"), np.array([0])))
+            continue
+        tok, off, _, _ = gen.c4(seed=40 + (seed % 3), windows=W, window=win, templates=4)
+        d = dev(tok)
+        rep, roff, occ = ctx.find_repeats_batched(d, off, 6)
+        tt, to = ctx.trie_build(d, off, rep, roff, 6, 0).traces()
+        lists.append((tt.clone(), to))
+    u = ctx.trie_build_traces_multi(lists)
+    flat = torch.cat([t for t, _ in lists])
+    offs = [np.array([0], np.int64)]
+    base = 0
+    for _, o in lists:
+        offs.append(o[1:] + base)
+        base += int(o[-1])
+    ref = ctx.trie_build_traces(flat, np.concatenate(offs))
+    a, ao = u.traces()
+    b, bo = ref.traces()
+    assert np.array_equal(ao, bo) and torch.equal(a, b)
+    assert u.info()[0] < sum(len(o) - 1 for _, o in lists)  # source 3 repeats source 0

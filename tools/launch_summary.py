@@ -16,7 +16,7 @@ def summarise(path):
             continue
         v = float(r[vi].replace(",", ""))
         v *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r[ui], 1.0)
-        name = r[ki].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+        name = r[ki].replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("unnamed>::", "")
         m = re.match(r"(?:void )?([\w:]+)(<[^(]*>)?", name)
         key = m.group(1) + (m.group(2) or "") if m else name[:60]
         agg[key][0] += 1
