@@ -574,11 +574,16 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
                                                                 const u32 *__restrict__ ptrace,
                                                                 const u32 *__restrict__ e_lo,
                                                                 const u32 *__restrict__ e_hi, i64 *__restrict__ ilo,
-                                                                u32 *__restrict__ icnt) {
+                                                                u32 *__restrict__ icnt, u32 *__restrict__ qtot) {
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ u32 s_tot;
   const int q = blockIdx.x;
   const i64 z0 = qoff[q], z1 = qoff[q + 1];
-  if (z0 == z1) return;
+  if (z0 == z1) {
+    if (threadIdx.x == 0) qtot[q] = 0;
+    return;
+  }
+  if (threadIdx.x == 0) s_tot = 0;
   const i64 beg = m.off[q], n = m.off[q + 1] - beg;
   u64 *S = reinterpret_cast<u64 *>(smem);
   unsigned short *SA = reinterpret_cast<unsigned short *>(S + kSMMax);
@@ -657,6 +662,180 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
     if (lane == 0) {
       ilo[z] = beg + hi;
       icnt[z] = u32(cnt);
+      if (cnt) atomicAdd(&s_tot, u32(cnt));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) qtot[q] = s_tot;
+}
+
+// ---- ordered hit emission, one CTA per stream (on-chip path) ----
+// Output order is (stream, end, trace id).  The CTA counts its stream's hits
+// per end position (shared atomics over the stream's local SA) and scans the
+// counts into bin starts; then it places every hit straight at its final
+// index with a STABLE scatter in trace order: the stream's pairs (already in
+// trace-id order) are cut into units of <= 32 hits of one pair, and rounds of
+// 32 consecutive units run one unit per warp.  A unit's hits have distinct
+// end positions (one trace, one length), so within a round the only order to
+// settle is between warps: each hit sets its warp's bit in a per-end mask,
+// its index is the end's cursor plus the number of lower warps in the mask,
+// and the highest warp advances the cursor.  No global sort, no second pass
+// over the hits.
+constexpr int kEmitThreads = 1024;
+constexpr int kEmitBatch = 1024;  // pairs staged on chip per batch
+
+// exclusive scan of one u32 per thread over the CTA; returns the total
+__device__ __forceinline__ u32 cta_excl_scan(u32 v, u32 *s_warp, u32 *out_excl) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  u32 incl = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u32 o = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += o;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const u32 x = s_warp[lane];
+    u32 wi = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u32 o = __shfl_up_sync(0xffffffffu, wi, d);
+      if (lane >= d) wi += o;
+    }
+    s_warp[lane] = wi - x;
+    if (lane == 31) s_warp[32] = wi;
+  }
+  __syncthreads();
+  *out_excl = s_warp[warp] + incl - v;
+  const u32 total = s_warp[32];
+  __syncthreads();  // s_warp may be reused
+  return total;
+}
+
+__global__ void __launch_bounds__(kEmitThreads, 1) k_stream_emit(StreamMatch m, const u32 *__restrict__ zsorted,
+                                                                 const u32 *__restrict__ qoff,
+                                                                 const u32 *__restrict__ ptrace,
+                                                                 const i64 *__restrict__ ilo,
+                                                                 const u32 *__restrict__ icnt,
+                                                                 const u32 *__restrict__ qbase, i64 cap,
+                                                                 apo_match_rec *__restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ u32 s_warp[33];
+  const int q = blockIdx.x;
+  const i64 z0 = qoff[q], z1 = qoff[q + 1];
+  if (z0 == z1) return;
+  const i64 beg = m.off[q], n = m.off[q + 1] - beg;
+  u32 *st = reinterpret_cast<u32 *>(smem);  // [kSMMax] bin counts -> cursors
+  u32 *mask = st + kSMMax;                  // [kSMMax] warps of the round with a hit at this end
+  u32 *pc = mask + kSMMax;                  // [kEmitBatch] staged pairs: hit count
+  u32 *plo = pc + kEmitBatch;               //   first local SA rank
+  u32 *pl1 = plo + kEmitBatch;              //   trace length - 1
+  u32 *ptr = pl1 + kEmitBatch;              //   trace id
+  u32 *ub = ptr + kEmitBatch;               // [kEmitBatch + 1] unit prefix
+  unsigned short *SA = reinterpret_cast<unsigned short *>(ub + kEmitBatch + 1);  // [kSMMax]
+  for (i64 i = threadIdx.x; i < n; i += kEmitThreads) {
+    SA[i] = (unsigned short)(m.sa[beg + i] - beg);
+    st[i] = 0;
+    mask[i] = 0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // 1. hits per end position (pair metadata loaded lane-parallel)
+  for (i64 gbase = z0 + i64(warp) * 32; gbase < z1; gbase += i64(kEmitThreads)) {
+    const i64 i = gbase + lane;
+    u32 c = 0, lo = 0, L1 = 0;
+    if (i < z1) {
+      const u32 z = zsorted[i];
+      c = icnt[z];
+      if (c) {
+        const u32 t = ptrace[z];
+        L1 = u32(m.toff[t + 1] - m.toff[t]) - 1u;
+        lo = u32(ilo[z] - beg);
+      }
+    }
+    u32 live = __ballot_sync(0xffffffffu, c != 0);
+    while (live) {
+      const int src = __ffs(live) - 1;
+      live &= live - 1;
+      const u32 cc = __shfl_sync(0xffffffffu, c, src), ll = __shfl_sync(0xffffffffu, lo, src),
+                l1 = __shfl_sync(0xffffffffu, L1, src);
+      for (u32 k = lane; k < cc; k += 32) atomicAdd(&st[u32(SA[ll + k]) + l1], 1u);
+    }
+  }
+  __syncthreads();
+  // 2. exclusive scan of the n bin counts (16 per thread) -> cursors
+  constexpr int kPer = kSMMax / kEmitThreads;
+  {
+    u32 v[kPer];
+    u32 sum = 0;
+    const int b0 = threadIdx.x * kPer;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      v[j] = b0 + j < n ? st[b0 + j] : 0u;
+      sum += v[j];
+    }
+    u32 run;
+    cta_excl_scan(sum, s_warp, &run);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      if (b0 + j < n) st[b0 + j] = run;
+      run += v[j];
+    }
+  }
+  __syncthreads();
+  const i64 qb = qbase[q];
+  // 3. stable placement, batch by batch of pairs, round by round of units
+  for (i64 bz = z0; bz < z1; bz += kEmitBatch) {
+    const int nb = int(min(i64(kEmitBatch), z1 - bz));
+    u32 units = 0;
+    if (threadIdx.x < nb) {
+      const u32 z = zsorted[bz + threadIdx.x];
+      const u32 c = icnt[z];
+      pc[threadIdx.x] = c;
+      if (c) {
+        const u32 t = ptrace[z];
+        ptr[threadIdx.x] = t;
+        pl1[threadIdx.x] = u32(m.toff[t + 1] - m.toff[t]) - 1u;
+        plo[threadIdx.x] = u32(ilo[z] - beg);
+      }
+      units = (c + 31) >> 5;
+    }
+    u32 ex;
+    const u32 U = cta_excl_scan(units, s_warp, &ex);
+    if (threadIdx.x < nb) ub[threadIdx.x] = ex;
+    if (threadIdx.x == 0) ub[nb] = U;
+    __syncthreads();
+    for (u32 r0 = 0; r0 < U; r0 += kEmitThreads / 32) {
+      const u32 u = r0 + warp;
+      int e = -1;
+      u32 t = 0;
+      if (u < U) {
+        int lo = 0, hi = nb - 1;  // pair j: last with ub[j] <= u
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (ub[mid] <= u) lo = mid; else hi = mid - 1;
+        }
+        const u32 k = ((u - ub[lo]) << 5) + lane;
+        if (k < pc[lo]) {
+          e = int(u32(SA[plo[lo] + k]) + pl1[lo]);
+          t = ptr[lo];
+        }
+      }
+      if (e >= 0) atomicOr(&mask[e], 1u << warp);
+      __syncthreads();
+      u32 mm = 0;
+      if (e >= 0) {
+        mm = mask[e];
+        const i64 pos = qb + st[e] + __popc(mm & ((1u << warp) - 1u));
+        if (pos < cap) reinterpret_cast<int4 *>(out)[pos] = make_int4(q, e, i32(t), 0);  // one 16-B store
+      }
+      __syncthreads();
+      if (e >= 0 && warp == 31 - __clz(mm)) {
+        st[e] += __popc(mm);
+        mask[e] = 0;
+      }
+      __syncthreads();
     }
   }
 }
@@ -1246,6 +1425,7 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
     require(tr != nullptr && d_count != nullptr && cap >= 0 && nstreams >= 1 && h_off != nullptr, "invalid argument");
     require(mode == 0, "only MATCH_ALL (mode 0) is implemented");
     require(cap == 0 || d_out != nullptr, "d_out is NULL");
+    require((reinterpret_cast<uintptr_t>(d_out) & 15) == 0, "d_out must be 16-byte aligned");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     APO_CUDA(cudaMemsetAsync(d_count, 0, sizeof(i64), s));
     const i64 Ns = h_off[nstreams];
@@ -1264,6 +1444,7 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
     std::vector<i64> h_s(h_off, h_off + nstreams + 1);
     u64 *keys = nullptr, *keys_alt = nullptr;
     i64 nh = -1;
+    bool emitted = false;  // hits already written in final order
     {
       // ---- per-stream path: each stream's own SA, bucketed by first token ----
       Batch b;
@@ -1340,6 +1521,8 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             full.take<u32>(P);
             full.take<u32>(P);
             full.take<u32>(size_t(nstreams) + 1);
+            full.take<u32>(size_t(nstreams));
+            full.take<u32>(size_t(nstreams));
             if (full.off > c.aux.cap) {
               c.aux.reserve(full.off, s);
               Carver cb(c.aux.base);
@@ -1354,6 +1537,8 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             u64 *qk = cz.take<u64>(P), *qk_alt = cz.take<u64>(P);
             u32 *qv = cz.take<u32>(P), *qv_alt = cz.take<u32>(P);
             u32 *qoff = cz.take<u32>(size_t(nstreams) + 1);
+            u32 *qtot = cz.take<u32>(size_t(nstreams));
+            u32 *qbase = cz.take<u32>(size_t(nstreams));
             k_pair_list<<<grid_for(T * 32, T256), T256, 0, s>>>(pbase, ea, ecnt, sord, e_q, T, pair_e, ptr, qk, qv);
             APO_CHECK_LAUNCH();
             bool aq = radix_sort_u64_u32(c, qk, qv, qk_alt, qv_alt, P, 0, bits_for(u64(nstreams - 1)), s);
@@ -1368,10 +1553,28 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
               attr = true;
             }
             if (c.prof) c.prof_begin(kProfMatch, 0.0, s);
-            k_stream_match<<<nstreams, kSMThreads, smem, s>>>(sm, sqv, qoff, pair_e, ptr, e_lo, e_hi, ilo, icnt);
+            k_stream_match<<<nstreams, kSMThreads, smem, s>>>(sm, sqv, qoff, pair_e, ptr, e_lo, e_hi, ilo, icnt,
+                                                              qtot);
             APO_CHECK_LAUNCH();
             if (c.prof) c.prof_end(s);
             c.launches += 3;
+            // hits in final order straight from the per-stream emitter
+            PairBaseF qf{qtot, qbase, nstreams, scal + 3};
+            launch_scan<false>(c, nstreams, qf, s);
+            nh = i64(c.read_u64(reinterpret_cast<const u64 *>(scal + 3), s));
+            emitted = true;
+            if (nh > 0 && cap > 0) {
+              const size_t esmem = sizeof(u32) * (2 * kSMMax + 5 * kEmitBatch + 1) + sizeof(unsigned short) * kSMMax;
+              static bool eattr = false;
+              if (!eattr) {
+                APO_CUDA(cudaFuncSetAttribute(k_stream_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              int(esmem)));
+                eattr = true;
+              }
+              k_stream_emit<<<nstreams, kEmitThreads, esmem, s>>>(sm, sqv, qoff, ptr, ilo, icnt, qbase, cap, d_out);
+              APO_CHECK_LAUNCH();
+              c.launches++;
+            }
           } else {
             const i64 chunks = (P + kPairChunk - 1) / kPairChunk;
             k_pair_search<<<grid_for(chunks * 32, 256), 256, 0, s>>>(sm, pbase, ea, P, sord, e_lo, e_hi, e_q, ilo,
@@ -1379,6 +1582,7 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             APO_CHECK_LAUNCH();
             c.launches++;
           }
+          if (!emitted) {
           PairBaseF hf{icnt, hbase, P, scal + 2};
           launch_scan<false>(c, P, hf, s);
           nh = i64(c.read_u64(reinterpret_cast<const u64 *>(scal + 2), s));
@@ -1413,6 +1617,7 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             k_enumerate_pairs<<<grid_for(P * 32, T256), T256, 0, s>>>(sm, ilo, hbase, ptr, P, nh, bE, bT, keys);
             APO_CHECK_LAUNCH();
             c.launches++;
+          }
           }
         }
       }
@@ -1458,6 +1663,11 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
       APO_CHECK_LAUNCH();
       c.launches++;
     }
+    }
+    if (emitted) {
+      APO_CUDA(cudaMemcpyAsync(d_count, &nh, sizeof(i64), cudaMemcpyHostToDevice, s));
+      APO_CUDA(cudaStreamSynchronize(s));
+      return;
     }
     if (nh == 0) return;
     const int kb = bS + bE + bT;

@@ -192,3 +192,23 @@ def test_trie_build_traces_multi_sources(ctx):
     b, bo = ref.traces()
     assert np.array_equal(ao, bo) and torch.equal(a, b)
     assert u.info()[0] < sum(len(o) - 1 for _, o in lists)  # source 3 repeats source 0
+
+
+def test_match_large_end_bins(ctx):
+    """Many traces ending at the same stream position (nested runs of one
+    token): end bins far larger than the per-hit ranking threshold take the
+    warp bitonic path of the ordered emitter; order (stream, end, id) and
+    content vs the brute-force oracle."""
+    a, b = 7, 9
+    traces = sorted({(a,) * L for L in range(1, 120)} | {(a,) * L + (b,) for L in range(1, 40)},
+                    key=lambda t: (-len(t), t))
+    flat = np.array([x for t in traces for x in t], dtype=np.uint64)
+    toff = np.cumsum([0] + [len(t) for t in traces]).astype(np.int64)
+    trie = ctx.trie_build_traces(dev(flat), toff)
+    tt, to = trie.traces()
+    streams = [np.full(3000, a, np.uint64), np.array([a] * 500 + [b] + [a] * 200, np.uint64)]
+    sflat = np.concatenate(streams)
+    soff = np.cumsum([0] + [len(x) for x in streams]).astype(np.int64)
+    hits = ctx.match(trie, dev(sflat), soff).cpu().numpy()
+    want, cnt = oracle.match_brute(sflat, soff, tt.cpu().numpy(), to)
+    assert cnt == len(hits) and np.array_equal(hits, want)
