@@ -674,8 +674,8 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
 // per end position (shared atomics over the stream's local SA) and scans the
 // counts into bin starts; then it places every hit straight at its final
 // index with a STABLE scatter in trace order: the stream's pairs (already in
-// trace-id order) are cut into units of <= 32 hits of one pair, and rounds of
-// 32 consecutive units run one unit per warp.  A unit's hits have distinct
+// trace-id order) are cut into units of <= 32 * kEmitK hits of one pair, and
+// rounds of 32 consecutive units run one unit per warp.  A unit's hits have distinct
 // end positions (one trace, one length), so within a round the only order to
 // settle is between warps: each hit sets its warp's bit in a per-end mask,
 // its index is the end's cursor plus the number of lower warps in the mask,
@@ -683,6 +683,7 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
 // over the hits.
 constexpr int kEmitThreads = 1024;
 constexpr int kEmitBatch = 1024;  // pairs staged on chip per batch
+constexpr int kEmitK = 4;         // hits per lane per round: a unit is <= 128 hits of one pair
 
 // exclusive scan of one u32 per thread over the CTA; returns the total
 __device__ __forceinline__ u32 cta_excl_scan(u32 v, u32 *s_warp, u32 *out_excl) {
@@ -799,7 +800,7 @@ __global__ void __launch_bounds__(kEmitThreads, 1) k_stream_emit(StreamMatch m, 
         pl1[threadIdx.x] = u32(m.toff[t + 1] - m.toff[t]) - 1u;
         plo[threadIdx.x] = u32(ilo[z] - beg);
       }
-      units = (c + 31) >> 5;
+      units = (c + 32 * kEmitK - 1) / (32 * kEmitK);
     }
     u32 ex;
     const u32 U = cta_excl_scan(units, s_warp, &ex);
@@ -808,32 +809,45 @@ __global__ void __launch_bounds__(kEmitThreads, 1) k_stream_emit(StreamMatch m, 
     __syncthreads();
     for (u32 r0 = 0; r0 < U; r0 += kEmitThreads / 32) {
       const u32 u = r0 + warp;
-      int e = -1;
+      int e[kEmitK];
       u32 t = 0;
+#pragma unroll
+      for (int j = 0; j < kEmitK; ++j) e[j] = -1;
       if (u < U) {
         int lo = 0, hi = nb - 1;  // pair j: last with ub[j] <= u
         while (lo < hi) {
           const int mid = (lo + hi + 1) >> 1;
           if (ub[mid] <= u) lo = mid; else hi = mid - 1;
         }
-        const u32 k = ((u - ub[lo]) << 5) + lane;
-        if (k < pc[lo]) {
-          e = int(u32(SA[plo[lo] + k]) + pl1[lo]);
-          t = ptr[lo];
+        const u32 k0 = (u - ub[lo]) * u32(32 * kEmitK) + lane, c = pc[lo], sa0 = plo[lo], l1 = pl1[lo];
+        t = ptr[lo];
+#pragma unroll
+        for (int j = 0; j < kEmitK; ++j) {
+          const u32 k = k0 + 32 * j;
+          if (k < c) e[j] = int(u32(SA[sa0 + k]) + l1);
         }
       }
-      if (e >= 0) atomicOr(&mask[e], 1u << warp);
+#pragma unroll
+      for (int j = 0; j < kEmitK; ++j)
+        if (e[j] >= 0) atomicOr(&mask[e[j]], 1u << warp);
       __syncthreads();
-      u32 mm = 0;
-      if (e >= 0) {
-        mm = mask[e];
-        const i64 pos = qb + st[e] + __popc(mm & ((1u << warp) - 1u));
-        if (pos < cap) reinterpret_cast<int4 *>(out)[pos] = make_int4(q, e, i32(t), 0);  // one 16-B store
+      u32 mine = 0;  // bit j: this lane advances the cursor of e[j]
+#pragma unroll
+      for (int j = 0; j < kEmitK; ++j) {
+        if (e[j] >= 0) {
+          const u32 mm = mask[e[j]];
+          if (warp == 31 - __clz(mm)) mine |= 1u << j;
+          const i64 pos = qb + st[e[j]] + __popc(mm & ((1u << warp) - 1u));
+          if (pos < cap) reinterpret_cast<int4 *>(out)[pos] = make_int4(q, e[j], i32(t), 0);  // one 16-B store
+        }
       }
       __syncthreads();
-      if (e >= 0 && warp == 31 - __clz(mm)) {
-        st[e] += __popc(mm);
-        mask[e] = 0;
+#pragma unroll
+      for (int j = 0; j < kEmitK; ++j) {
+        if (mine >> j & 1u) {
+          st[e[j]] += __popc(mask[e[j]]);
+          mask[e[j]] = 0;
+        }
       }
       __syncthreads();
     }
