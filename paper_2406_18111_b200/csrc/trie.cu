@@ -35,6 +35,7 @@ struct apo_trie {
   apo::i64 ntok = 0;   // total tokens
   apo::i64 maxlen = 0;
   apo::u64 *d_tok = nullptr;  // traces in id order, back to back
+  mutable apo::u64 *d_rtok = nullptr;  // the same traces, each reversed (built by the first apo_match)
   apo::i64 *d_off = nullptr;  // T+1
   size_t tok_bytes = 0, off_bytes = 0;  // pooled blocks (returned to the context on destroy)
   std::vector<apo::i64> h_off;
@@ -323,6 +324,24 @@ void upload_batch(Ctx &c, Batch &b, GenPlan &g, const std::vector<i64> &h_off, c
 }
 
 
+// reversed copies for the on-chip matcher: dst[off[w] + j] = src[off[w+1] - 1 - j]
+__global__ void k_reverse_by_wid(const u64 *__restrict__ src, const i64 *__restrict__ off,
+                                 const i32 *__restrict__ wid, i64 N, u64 *__restrict__ dst) {
+  const i64 p = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= N) return;
+  const int w = wid[p];
+  dst[p] = src[off[w] + off[w + 1] - 1 - p];
+}
+
+__global__ void k_reverse_traces(const u64 *__restrict__ src, const i64 *__restrict__ off, i64 T,
+                                 u64 *__restrict__ dst) {
+  const i64 t = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (t >= T) return;
+  const int lane = threadIdx.x & 31;
+  const i64 o = off[t], L = off[t + 1] - o;
+  for (i64 k = lane; k < L; k += 32) dst[o + k] = src[o + L - 1 - k];
+}
+
 // ------------------------------------------- per-stream matching path ----
 // Every stream gets its own suffix array (K9 on chip for streams <= 16K);
 // each stream's SA is cut into buckets of equal first token; a trace is
@@ -508,6 +527,19 @@ __global__ void k_pair_list(const u32 *__restrict__ pbase, const u32 *__restrict
   }
 }
 
+// Launch order of the per-stream CTAs: streams keyed by the trace of their
+// first pair (the longest candidate trace whose first token the stream
+// holds).  Streams that share traces get neighbouring CTAs, so the CTAs
+// resident at any moment read overlapping trace sets and the trace tokens
+// (the matcher's HBM stream) are served from L2 instead of re-read from HBM.
+__global__ void k_stream_keys(const u32 *__restrict__ qoff, const u32 *__restrict__ zsorted,
+                              const u32 *__restrict__ ptrace, int S, u64 *__restrict__ key, u32 *__restrict__ val) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= S) return;
+  key[q] = qoff[q] < qoff[q + 1] ? u64(ptrace[zsorted[qoff[q]]]) : ~0ull;
+  val[q] = u32(q);
+}
+
 // qoff[q] = first index of stream q in the stream-sorted pair list
 __global__ void k_q_offsets(const u64 *__restrict__ qkey, i64 P, int S, u32 *__restrict__ qoff) {
   const i64 q = i64(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -574,10 +606,11 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
                                                                 const u32 *__restrict__ ptrace,
                                                                 const u32 *__restrict__ e_lo,
                                                                 const u32 *__restrict__ e_hi, i64 *__restrict__ ilo,
-                                                                u32 *__restrict__ icnt, u32 *__restrict__ qtot) {
+                                                                u32 *__restrict__ icnt, u32 *__restrict__ qtot,
+                                                                const u32 *__restrict__ qorder) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ u32 s_tot;
-  const int q = blockIdx.x;
+  const int q = int(qorder[blockIdx.x]);
   const i64 z0 = qoff[q], z1 = qoff[q + 1];
   if (z0 == z1) {
     if (threadIdx.x == 0) qtot[q] = 0;
@@ -670,20 +703,26 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
 }
 
 // ---- ordered hit emission, one CTA per stream (on-chip path) ----
-// Output order is (stream, end, trace id).  The CTA counts its stream's hits
-// per end position (shared atomics over the stream's local SA) and scans the
-// counts into bin starts; then it places every hit straight at its final
-// index with a STABLE scatter in trace order: the stream's pairs (already in
-// trace-id order) are cut into units of <= 32 * kEmitK hits of one pair, and
-// rounds of 32 consecutive units run one unit per warp.  A unit's hits have distinct
-// end positions (one trace, one length), so within a round the only order to
-// settle is between warps: each hit sets its warp's bit in a per-end mask,
-// its index is the end's cursor plus the number of lower warps in the mask,
-// and the highest warp advances the cursor.  No global sort, no second pass
-// over the hits.
+// The on-chip path matches REVERSED traces against the suffix arrays of the
+// REVERSED streams: reversed trace t occurs at reversed position i of stream
+// q exactly when t ends at e = n - 1 - i.  In that suffix array the hit
+// intervals [lo, hi) of the stream's traces form a laminar family (two
+// intervals that meet belong to a trace and a suffix of it -- a prefix in
+// reversed order -- and the longer trace's interval lies inside), so the
+// traces ending at one position e are exactly the chain of intervals that
+// contain its rank r = RISA[n-1-e], from the deepest (longest trace,
+// smallest id) outwards: precisely the required (end, trace id) order.
+//  * k_tree_keys / radix sort / k_tree_sweep: per stream, the matched
+//    intervals in preorder (lo asc, hi desc, shorter first) and a stack sweep
+//    give every interval its parent (the next enclosing interval);
+//  * k_stream_emit: paints the deepest interval of every rank (shared
+//    atomicMin over the local pair index, which is the trace order), counts
+//    chain lengths with a difference array, scans them in end order and
+//    walks each end's chain, writing its records back to back -- every hit
+//    goes straight to its final place, and the writes of a warp stay within
+//    a few KB, so no partial-sector read-modify-write reaches HBM.
 constexpr int kEmitThreads = 1024;
-constexpr int kEmitBatch = 1024;  // pairs staged on chip per batch
-constexpr int kEmitK = 4;         // hits per lane per round: a unit is <= 128 hits of one pair
+constexpr u32 kNoPar = 0xffffffffu;
 
 // exclusive scan of one u32 per thread over the CTA; returns the total
 __device__ __forceinline__ u32 cta_excl_scan(u32 v, u32 *s_warp, u32 *out_excl) {
@@ -714,143 +753,198 @@ __device__ __forceinline__ u32 cta_excl_scan(u32 v, u32 *s_warp, u32 *out_excl) 
   return total;
 }
 
+// Preorder keys of the matched intervals: (stream, lo asc, hi desc); written
+// in reverse pair order so that the stable sort leaves equal intervals with
+// the larger pair index (shorter trace, the enclosing one) first.  Unmatched
+// pairs get a key above every stream.
+__global__ void k_tree_keys(const u64 *__restrict__ sqk, const u32 *__restrict__ zsorted,
+                            const i64 *__restrict__ ilo, const u32 *__restrict__ icnt, const i64 *__restrict__ off,
+                            const u32 *__restrict__ ptrace, i64 P, int bS, u64 *__restrict__ key,
+                            u32 *__restrict__ val, u32 *__restrict__ gtr) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const u32 z = zsorted[i];
+  gtr[i] = ptrace[z];
+  const u32 c = icnt[z];
+  const u64 q = sqk[i];
+  const i64 k = P - 1 - i;
+  if (c) {
+    const u64 lo = u64(ilo[z] - off[q]), hi = lo + c;
+    key[k] = (q << 30) | (lo << 15) | (32767u - hi);
+  } else {
+    key[k] = u64(1) << (bS + 30);
+  }
+  val[k] = u32(i);
+}
+
+// toff[q] = first index of stream q's intervals in the preorder list
+__global__ void k_tree_offsets(const u64 *__restrict__ key, i64 P, int S, u32 *__restrict__ toff) {
+  const i64 q = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q > S) return;
+  i64 lo = 0, hi = P;
+  while (lo < hi) {
+    const i64 mid = (lo + hi) >> 1;
+    if ((key[mid] >> 30) < u64(q)) lo = mid + 1; else hi = mid;
+  }
+  toff[q] = u32(lo);
+}
+
+// Stack sweep of one stream's intervals in preorder, one warp per stream:
+// the warp stages the sorted list in shared memory chunk by chunk and lane 0
+// sweeps it with the open-interval stack in shared memory (a ring of the top
+// kTreeDepth entries; deeper entries are recovered through the parent links
+// already written to global memory).  gpar[i] = parent's local pair index
+// (i - qoff[q]) or kNoPar, ghi[i] = interval end.
+constexpr int kTreeChunk = 1024;
+constexpr int kTreeDepth = 1024;
+
+__global__ void __launch_bounds__(32) k_tree_sweep(const u64 *__restrict__ key, const u32 *__restrict__ val,
+                                                   const u32 *__restrict__ toff, const u32 *__restrict__ qoff,
+                                                   u32 *__restrict__ gpar, u32 *__restrict__ ghi) {
+  __shared__ u64 s_key[kTreeChunk];
+  __shared__ u32 s_val[kTreeChunk];
+  __shared__ u32 s_idx[kTreeDepth], s_hi[kTreeDepth];
+  const int q = blockIdx.x, lane = threadIdx.x;
+  const u32 a = toff[q], b = toff[q + 1], z0 = qoff[q];
+  u32 cur = kNoPar, curhi = 0, depth = 0, held = 0;  // held: stack entries below the top kept in the ring
+  for (u32 c0 = a; c0 < b; c0 += kTreeChunk) {
+    const u32 m = min(u32(kTreeChunk), b - c0);
+    for (u32 k = lane; k < m; k += 32) {
+      s_key[k] = key[c0 + k];
+      s_val[k] = val[c0 + k];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      for (u32 k = 0; k < m; ++k) {
+        const u64 kk = s_key[k];
+        const u32 i = s_val[k];
+        const u32 lo = u32(kk >> 15) & 32767u, hi = 32767u - (u32(kk) & 32767u);
+        while (cur != kNoPar && curhi <= lo) {  // the open interval ends before this one starts: pop
+          if (depth == 0) {
+            cur = kNoPar;
+            break;
+          }
+          --depth;
+          if (held) {
+            --held;
+            cur = s_idx[depth % kTreeDepth];
+            curhi = s_hi[depth % kTreeDepth];
+          } else {
+            cur = gpar[z0 + cur];
+            curhi = cur != kNoPar ? ghi[z0 + cur] : 0;
+          }
+        }
+        gpar[i] = cur;
+        ghi[i] = hi;
+        if (cur != kNoPar) {  // push the open interval below the new one
+          s_idx[depth % kTreeDepth] = cur;
+          s_hi[depth % kTreeDepth] = curhi;
+          held = min(held + 1, u32(kTreeDepth));
+          ++depth;
+        }
+        cur = i - z0;
+        curhi = hi;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void __launch_bounds__(kEmitThreads, 1) k_stream_emit(StreamMatch m, const u32 *__restrict__ zsorted,
                                                                  const u32 *__restrict__ qoff,
-                                                                 const u32 *__restrict__ ptrace,
                                                                  const i64 *__restrict__ ilo,
                                                                  const u32 *__restrict__ icnt,
                                                                  const u32 *__restrict__ qbase, i64 cap,
-                                                                 apo_match_rec *__restrict__ out) {
+                                                                 apo_match_rec *__restrict__ out,
+                                                                 const u32 *__restrict__ qorder,
+                                                                 const u32 *__restrict__ gpar,
+                                                                 const u32 *__restrict__ gtr) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ u32 s_warp[33];
-  const int q = blockIdx.x;
+  const int q = int(qorder[blockIdx.x]);
   const i64 z0 = qoff[q], z1 = qoff[q + 1];
   if (z0 == z1) return;
   const i64 beg = m.off[q], n = m.off[q + 1] - beg;
-  u32 *st = reinterpret_cast<u32 *>(smem);  // [kSMMax] bin counts -> cursors
-  u32 *mask = st + kSMMax;                  // [kSMMax] warps of the round with a hit at this end
-  u32 *pc = mask + kSMMax;                  // [kEmitBatch] staged pairs: hit count
-  u32 *plo = pc + kEmitBatch;               //   first local SA rank
-  u32 *pl1 = plo + kEmitBatch;              //   trace length - 1
-  u32 *ptr = pl1 + kEmitBatch;              //   trace id
-  u32 *ub = ptr + kEmitBatch;               // [kEmitBatch + 1] unit prefix
-  unsigned short *SA = reinterpret_cast<unsigned short *>(ub + kEmitBatch + 1);  // [kSMMax]
-  for (i64 i = threadIdx.x; i < n; i += kEmitThreads) {
-    SA[i] = (unsigned short)(m.sa[beg + i] - beg);
-    st[i] = 0;
-    mask[i] = 0;
+  u32 *deep = reinterpret_cast<u32 *>(smem);  // [kSMMax] deepest interval (local pair index) at each rank
+  u32 *cnt = deep + kSMMax;                   // [kSMMax + 1] chain length at each rank (difference array first)
+  unsigned short *RISA = reinterpret_cast<unsigned short *>(cnt + kSMMax + 1);  // [kSMMax]
+  for (i64 r = threadIdx.x; r < n; r += kEmitThreads) {
+    deep[r] = kNoPar;
+    cnt[r] = 0;
+    RISA[m.sa[beg + r] - beg] = (unsigned short)r;
   }
+  if (threadIdx.x == 0) cnt[n] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // 1. hits per end position (pair metadata loaded lane-parallel)
+  // 1. deepest interval per rank and chain-length differences (pair metadata
+  //    loaded lane-parallel, each pair painted by the whole warp)
   for (i64 gbase = z0 + i64(warp) * 32; gbase < z1; gbase += i64(kEmitThreads)) {
     const i64 i = gbase + lane;
-    u32 c = 0, lo = 0, L1 = 0;
+    u32 c = 0, lo = 0;
     if (i < z1) {
       const u32 z = zsorted[i];
       c = icnt[z];
-      if (c) {
-        const u32 t = ptrace[z];
-        L1 = u32(m.toff[t + 1] - m.toff[t]) - 1u;
-        lo = u32(ilo[z] - beg);
-      }
+      if (c) lo = u32(ilo[z] - beg);
+    }
+    if (c) {
+      atomicAdd(&cnt[lo], 1u);
+      atomicSub(&cnt[lo + c], 1u);
     }
     u32 live = __ballot_sync(0xffffffffu, c != 0);
     while (live) {
       const int src = __ffs(live) - 1;
       live &= live - 1;
-      const u32 cc = __shfl_sync(0xffffffffu, c, src), ll = __shfl_sync(0xffffffffu, lo, src),
-                l1 = __shfl_sync(0xffffffffu, L1, src);
-      for (u32 k = lane; k < cc; k += 32) atomicAdd(&st[u32(SA[ll + k]) + l1], 1u);
+      const u32 cc = __shfl_sync(0xffffffffu, c, src), ll = __shfl_sync(0xffffffffu, lo, src);
+      const u32 li = u32(gbase + src - z0);
+      for (u32 k = lane; k < cc; k += 32) atomicMin(&deep[ll + k], li);
     }
   }
   __syncthreads();
-  // 2. exclusive scan of the n bin counts (16 per thread) -> cursors
+  // 2. chain lengths per rank: prefix sum of the differences (16 per thread)
   constexpr int kPer = kSMMax / kEmitThreads;
+  const int b0 = threadIdx.x * kPer;
   {
     u32 v[kPer];
     u32 sum = 0;
-    const int b0 = threadIdx.x * kPer;
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
-      v[j] = b0 + j < n ? st[b0 + j] : 0u;
+      v[j] = b0 + j < n ? cnt[b0 + j] : 0u;
       sum += v[j];
     }
     u32 run;
     cta_excl_scan(sum, s_warp, &run);
 #pragma unroll
     for (int j = 0; j < kPer; ++j) {
-      if (b0 + j < n) st[b0 + j] = run;
       run += v[j];
+      if (b0 + j < n) cnt[b0 + j] = run;
     }
   }
   __syncthreads();
-  const i64 qb = qbase[q];
-  // 3. stable placement, batch by batch of pairs, round by round of units
-  for (i64 bz = z0; bz < z1; bz += kEmitBatch) {
-    const int nb = int(min(i64(kEmitBatch), z1 - bz));
-    u32 units = 0;
-    if (threadIdx.x < nb) {
-      const u32 z = zsorted[bz + threadIdx.x];
-      const u32 c = icnt[z];
-      pc[threadIdx.x] = c;
-      if (c) {
-        const u32 t = ptrace[z];
-        ptr[threadIdx.x] = t;
-        pl1[threadIdx.x] = u32(m.toff[t + 1] - m.toff[t]) - 1u;
-        plo[threadIdx.x] = u32(ilo[z] - beg);
-      }
-      units = (c + 32 * kEmitK - 1) / (32 * kEmitK);
+  // 3. ends in order: thread t owns ends [16t, 16t + 16); record offsets by a
+  //    scan of the chain lengths, then each end's chain is walked and written
+  u32 ce[kPer];
+  u32 sum = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const i64 e = b0 + j;
+    ce[j] = e < n ? cnt[RISA[n - 1 - e]] : 0u;
+    sum += ce[j];
+  }
+  u32 run;
+  cta_excl_scan(sum, s_warp, &run);
+  const i64 qb = i64(qbase[q]);
+#pragma unroll 1
+  for (int j = 0; j < kPer; ++j) {
+    if (!ce[j]) continue;
+    const i64 e = b0 + j;
+    u32 z = deep[RISA[n - 1 - e]];
+    i64 pos = qb + run;
+    for (u32 k = 0; k < ce[j]; ++k, ++pos) {
+      const u32 t = gtr[z0 + z];
+      if (pos < cap) reinterpret_cast<int4 *>(out)[pos] = make_int4(q, i32(e), i32(t), 0);  // one 16-B store
+      z = gpar[z0 + z];
     }
-    u32 ex;
-    const u32 U = cta_excl_scan(units, s_warp, &ex);
-    if (threadIdx.x < nb) ub[threadIdx.x] = ex;
-    if (threadIdx.x == 0) ub[nb] = U;
-    __syncthreads();
-    for (u32 r0 = 0; r0 < U; r0 += kEmitThreads / 32) {
-      const u32 u = r0 + warp;
-      int e[kEmitK];
-      u32 t = 0;
-#pragma unroll
-      for (int j = 0; j < kEmitK; ++j) e[j] = -1;
-      if (u < U) {
-        int lo = 0, hi = nb - 1;  // pair j: last with ub[j] <= u
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (ub[mid] <= u) lo = mid; else hi = mid - 1;
-        }
-        const u32 k0 = (u - ub[lo]) * u32(32 * kEmitK) + lane, c = pc[lo], sa0 = plo[lo], l1 = pl1[lo];
-        t = ptr[lo];
-#pragma unroll
-        for (int j = 0; j < kEmitK; ++j) {
-          const u32 k = k0 + 32 * j;
-          if (k < c) e[j] = int(u32(SA[sa0 + k]) + l1);
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < kEmitK; ++j)
-        if (e[j] >= 0) atomicOr(&mask[e[j]], 1u << warp);
-      __syncthreads();
-      u32 mine = 0;  // bit j: this lane advances the cursor of e[j]
-#pragma unroll
-      for (int j = 0; j < kEmitK; ++j) {
-        if (e[j] >= 0) {
-          const u32 mm = mask[e[j]];
-          if (warp == 31 - __clz(mm)) mine |= 1u << j;
-          const i64 pos = qb + st[e[j]] + __popc(mm & ((1u << warp) - 1u));
-          if (pos < cap) reinterpret_cast<int4 *>(out)[pos] = make_int4(q, e[j], i32(t), 0);  // one 16-B store
-        }
-      }
-      __syncthreads();
-#pragma unroll
-      for (int j = 0; j < kEmitK; ++j) {
-        if (mine >> j & 1u) {
-          st[e[j]] += __popc(mask[e[j]]);
-          mask[e[j]] = 0;
-        }
-      }
-      __syncthreads();
-    }
+    run += ce[j];
   }
 }
 
@@ -1408,6 +1502,7 @@ void apo_trie_destroy(apo_trie *tr) {
   if (!tr) return;
   if (tr->ctx) {
     tr->ctx->c.pool_put(tr->d_tok, tr->tok_bytes);
+    if (tr->d_rtok) tr->ctx->c.pool_put(tr->d_rtok, tr->tok_bytes);
     tr->ctx->c.pool_put(tr->d_off, tr->off_bytes);
   }
   delete tr;
@@ -1466,11 +1561,14 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
       b.W = nstreams;
       b.maxwin = maxs;
       GenPlan g;
-      u64 *e_tok, *e_tok_alt;
+      u64 *e_tok, *e_tok_alt, *d_rs = nullptr;
       u32 *e_lo, *e_q, *e_hi, *e_idx, *e_idx_alt, *ea, *ecnt, *pbase;
       i64 *scal;
+      // streams that fit on chip are matched in reversed form (see k_stream_emit)
+      const bool rev = maxs <= kSMMax;
       auto plan = [&](Carver &cv) {
         plan_gen(cv, b, g, true);
+        if (rev) d_rs = cv.take<u64>(Ns);
         e_tok = cv.take<u64>(Ns);
         e_tok_alt = cv.take<u64>(Ns);
         e_lo = cv.take<u32>(Ns);
@@ -1489,8 +1587,20 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
       Carver cv(c.arena.base);
       plan(cv);
       upload_batch(c, b, g, h_s, s);
-      build_sa(c, d_streams, b, g.sa, true, s);
-      StreamMatch sm{g.d_off, g.d_wid, g.sa.sa, g.sa.lcp, d_streams, tr->d_tok, tr->d_off, Ns, T};
+      if (rev) {
+        k_reverse_by_wid<<<grid_for(Ns, T256), T256, 0, s>>>(d_streams, g.d_off, g.d_wid, Ns, d_rs);
+        APO_CHECK_LAUNCH();
+        c.launches++;
+        if (!tr->d_rtok) {
+          tr->d_rtok = static_cast<u64 *>(c.pool_get(tr->tok_bytes));
+          k_reverse_traces<<<grid_for(T * 32, T256), T256, 0, s>>>(tr->d_tok, tr->d_off, T, tr->d_rtok);
+          APO_CHECK_LAUNCH();
+          c.launches++;
+        }
+      }
+      const u64 *mtok = rev ? d_rs : d_streams;
+      build_sa(c, mtok, b, g.sa, true, s);
+      StreamMatch sm{g.d_off, g.d_wid, g.sa.sa, g.sa.lcp, mtok, rev ? tr->d_rtok : tr->d_tok, tr->d_off, Ns, T};
       APO_CUDA(cudaMemsetAsync(scal, 0, sizeof(i64) * 4, s));
       BucketF bf{sm, e_tok, e_lo, e_q, scal};
       launch_scan<false>(c, Ns, bf, s);
@@ -1537,6 +1647,18 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             full.take<u32>(size_t(nstreams) + 1);
             full.take<u32>(size_t(nstreams));
             full.take<u32>(size_t(nstreams));
+            full.take<u64>(size_t(nstreams));
+            full.take<u64>(size_t(nstreams));
+            full.take<u32>(size_t(nstreams));
+            full.take<u32>(size_t(nstreams));
+            full.take<u64>(P);
+            full.take<u64>(P);
+            full.take<u32>(P);
+            full.take<u32>(P);
+            full.take<u32>(size_t(nstreams) + 1);
+            full.take<u32>(P);
+            full.take<u32>(P);
+            full.take<u32>(P);
             if (full.off > c.aux.cap) {
               c.aux.reserve(full.off, s);
               Carver cb(c.aux.base);
@@ -1553,6 +1675,12 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             u32 *qoff = cz.take<u32>(size_t(nstreams) + 1);
             u32 *qtot = cz.take<u32>(size_t(nstreams));
             u32 *qbase = cz.take<u32>(size_t(nstreams));
+            u64 *sk = cz.take<u64>(size_t(nstreams)), *sk_alt = cz.take<u64>(size_t(nstreams));
+            u32 *sv = cz.take<u32>(size_t(nstreams)), *sv_alt = cz.take<u32>(size_t(nstreams));
+            u64 *tk = cz.take<u64>(P), *tk_alt = cz.take<u64>(P);
+            u32 *tv = cz.take<u32>(P), *tv_alt = cz.take<u32>(P);
+            u32 *tof = cz.take<u32>(size_t(nstreams) + 1);
+            u32 *gpar = cz.take<u32>(P), *ghi = cz.take<u32>(P), *gtr = cz.take<u32>(P);
             k_pair_list<<<grid_for(T * 32, T256), T256, 0, s>>>(pbase, ea, ecnt, sord, e_q, T, pair_e, ptr, qk, qv);
             APO_CHECK_LAUNCH();
             bool aq = radix_sort_u64_u32(c, qk, qv, qk_alt, qv_alt, P, 0, bits_for(u64(nstreams - 1)), s);
@@ -1560,6 +1688,11 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             const u32 *sqv = aq ? qv_alt : qv;
             k_q_offsets<<<grid_for(i64(nstreams) + 1, T256), T256, 0, s>>>(sqk, P, nstreams, qoff);
             APO_CHECK_LAUNCH();
+            k_stream_keys<<<grid_for(nstreams, T256), T256, 0, s>>>(qoff, sqv, ptr, nstreams, sk, sv);
+            APO_CHECK_LAUNCH();
+            c.launches += 2;
+            const bool as = radix_sort_u64_u32(c, sk, sv, sk_alt, sv_alt, nstreams, 0, 64, s);
+            const u32 *qorder = as ? sv_alt : sv;
             const size_t smem = sizeof(u64) * kSMMax + 2 * sizeof(unsigned short) * kSMMax;
             static bool attr = false;
             if (!attr) {
@@ -1568,7 +1701,7 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             }
             if (c.prof) c.prof_begin(kProfMatch, 0.0, s);
             k_stream_match<<<nstreams, kSMThreads, smem, s>>>(sm, sqv, qoff, pair_e, ptr, e_lo, e_hi, ilo, icnt,
-                                                              qtot);
+                                                              qtot, qorder);
             APO_CHECK_LAUNCH();
             if (c.prof) c.prof_end(s);
             c.launches += 3;
@@ -1578,16 +1711,27 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             nh = i64(c.read_u64(reinterpret_cast<const u64 *>(scal + 3), s));
             emitted = true;
             if (nh > 0 && cap > 0) {
-              const size_t esmem = sizeof(u32) * (2 * kSMMax + 5 * kEmitBatch + 1) + sizeof(unsigned short) * kSMMax;
+              // interval forest of every stream (preorder sort + stack sweep)
+              k_tree_keys<<<grid_for(P, T256), T256, 0, s>>>(sqk, sqv, ilo, icnt, g.d_off, ptr, P, bS, tk, tv, gtr);
+              APO_CHECK_LAUNCH();
+              const bool at = radix_sort_u64_u32(c, tk, tv, tk_alt, tv_alt, P, 0, bS + 31, s);
+              const u64 *stk = at ? tk_alt : tk;
+              const u32 *stv = at ? tv_alt : tv;
+              k_tree_offsets<<<grid_for(i64(nstreams) + 1, T256), T256, 0, s>>>(stk, P, nstreams, tof);
+              APO_CHECK_LAUNCH();
+              k_tree_sweep<<<nstreams, 32, 0, s>>>(stk, stv, tof, qoff, gpar, ghi);
+              APO_CHECK_LAUNCH();
+              const size_t esmem = sizeof(u32) * (2 * kSMMax + 1) + sizeof(unsigned short) * kSMMax;
               static bool eattr = false;
               if (!eattr) {
                 APO_CUDA(cudaFuncSetAttribute(k_stream_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               int(esmem)));
                 eattr = true;
               }
-              k_stream_emit<<<nstreams, kEmitThreads, esmem, s>>>(sm, sqv, qoff, ptr, ilo, icnt, qbase, cap, d_out);
+              k_stream_emit<<<nstreams, kEmitThreads, esmem, s>>>(sm, sqv, qoff, ilo, icnt, qbase, cap, d_out, qorder,
+                                                                  gpar, gtr);
               APO_CHECK_LAUNCH();
-              c.launches++;
+              c.launches += 4;
             }
           } else {
             const i64 chunks = (P + kPairChunk - 1) / kPairChunk;

@@ -212,3 +212,24 @@ def test_match_large_end_bins(ctx):
     hits = ctx.match(trie, dev(sflat), soff).cpu().numpy()
     want, cnt = oracle.match_brute(sflat, soff, tt.cpu().numpy(), to)
     assert cnt == len(hits) and np.array_equal(hits, want)
+
+
+def test_match_deep_nesting():
+    """More nested traces at one end than the sweep's on-chip stack ring and
+    more matched traces in one stream than one staging chunk (1,100 runs of
+    one token): the interval-forest sweep must fall back to its parent links
+    exactly; compared with the brute-force oracle."""
+    from paper_2406_18111_b200 import Context
+    ctx = Context(0)
+    a = 11
+    traces = [(a,) * L for L in range(1100, 0, -1)]
+    flat = np.array([x for t in traces for x in t], dtype=np.uint64)
+    toff = np.cumsum([0] + [len(t) for t in traces]).astype(np.int64)
+    trie = ctx.trie_build_traces(dev(flat), toff)
+    tt, to = trie.traces()
+    streams = [np.full(2500, a, np.uint64), np.array([a] * 1200 + [3] + [a] * 50, np.uint64)]
+    sflat = np.concatenate(streams)
+    soff = np.cumsum([0] + [len(x) for x in streams]).astype(np.int64)
+    hits = ctx.match(trie, dev(sflat), soff).cpu().numpy()
+    want, cnt = oracle.match_brute(sflat, soff, tt.cpu().numpy(), to)
+    assert cnt == len(hits) and np.array_equal(hits, want)
