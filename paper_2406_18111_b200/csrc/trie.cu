@@ -722,6 +722,7 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
 //    goes straight to its final place, and the writes of a warp stay within
 //    a few KB, so no partial-sector read-modify-write reaches HBM.
 constexpr int kEmitThreads = 1024;
+constexpr int kEmitPairs = 8192;  // interval links kept on chip when the stream has at most this many
 constexpr u32 kNoPar = 0xffffffffu;
 
 // exclusive scan of one u32 per thread over the CTA; returns the total
@@ -793,31 +794,30 @@ __global__ void k_tree_offsets(const u64 *__restrict__ key, i64 P, int S, u32 *_
 // the warp stages the sorted list in shared memory chunk by chunk and lane 0
 // sweeps it with the open-interval stack in shared memory (a ring of the top
 // kTreeDepth entries; deeper entries are recovered through the parent links
-// already written to global memory).  gpar[i] = parent's local pair index
-// (i - qoff[q]) or kNoPar, ghi[i] = interval end.
+// already written to global memory).  Interval ids are preorder positions
+// local to the stream (k - toff[q]); per preorder position k:
+// opar[k] = parent id or kNoPar, ohi[k] = interval end, odep[k] = number of
+// intervals containing it (itself included), otr[k] = its trace id.
 constexpr int kTreeChunk = 1024;
 constexpr int kTreeDepth = 1024;
 
 __global__ void __launch_bounds__(32) k_tree_sweep(const u64 *__restrict__ key, const u32 *__restrict__ val,
-                                                   const u32 *__restrict__ toff, const u32 *__restrict__ qoff,
-                                                   u32 *__restrict__ gpar, u32 *__restrict__ ghi) {
+                                                   const u32 *__restrict__ toff, const u32 *__restrict__ gtr,
+                                                   u32 *__restrict__ opar, u32 *__restrict__ ohi,
+                                                   u32 *__restrict__ odep, u32 *__restrict__ otr) {
   __shared__ u64 s_key[kTreeChunk];
-  __shared__ u32 s_val[kTreeChunk];
   __shared__ u32 s_idx[kTreeDepth], s_hi[kTreeDepth];
   const int q = blockIdx.x, lane = threadIdx.x;
-  const u32 a = toff[q], b = toff[q + 1], z0 = qoff[q];
+  const u32 a = toff[q], b = toff[q + 1];
+  for (u32 k = a + lane; k < b; k += 32) otr[k] = gtr[val[k]];
   u32 cur = kNoPar, curhi = 0, depth = 0, held = 0;  // held: stack entries below the top kept in the ring
   for (u32 c0 = a; c0 < b; c0 += kTreeChunk) {
     const u32 m = min(u32(kTreeChunk), b - c0);
-    for (u32 k = lane; k < m; k += 32) {
-      s_key[k] = key[c0 + k];
-      s_val[k] = val[c0 + k];
-    }
+    for (u32 k = lane; k < m; k += 32) s_key[k] = key[c0 + k];
     __syncwarp();
     if (lane == 0) {
       for (u32 k = 0; k < m; ++k) {
         const u64 kk = s_key[k];
-        const u32 i = s_val[k];
         const u32 lo = u32(kk >> 15) & 32767u, hi = 32767u - (u32(kk) & 32767u);
         while (cur != kNoPar && curhi <= lo) {  // the open interval ends before this one starts: pop
           if (depth == 0) {
@@ -830,19 +830,21 @@ __global__ void __launch_bounds__(32) k_tree_sweep(const u64 *__restrict__ key, 
             cur = s_idx[depth % kTreeDepth];
             curhi = s_hi[depth % kTreeDepth];
           } else {
-            cur = gpar[z0 + cur];
-            curhi = cur != kNoPar ? ghi[z0 + cur] : 0;
+            cur = opar[a + cur];
+            curhi = cur != kNoPar ? ohi[a + cur] : 0;
           }
         }
-        gpar[i] = cur;
-        ghi[i] = hi;
+        const u32 id = c0 + k - a;
+        opar[a + id] = cur;
+        ohi[a + id] = hi;
+        odep[a + id] = cur != kNoPar ? depth + 2 : 1;
         if (cur != kNoPar) {  // push the open interval below the new one
           s_idx[depth % kTreeDepth] = cur;
           s_hi[depth % kTreeDepth] = curhi;
           held = min(held + 1, u32(kTreeDepth));
           ++depth;
         }
-        cur = i - z0;
+        cur = id;
         curhi = hi;
       }
     }
@@ -850,101 +852,88 @@ __global__ void __launch_bounds__(32) k_tree_sweep(const u64 *__restrict__ key, 
   }
 }
 
-__global__ void __launch_bounds__(kEmitThreads, 1) k_stream_emit(StreamMatch m, const u32 *__restrict__ zsorted,
-                                                                 const u32 *__restrict__ qoff,
-                                                                 const i64 *__restrict__ ilo,
-                                                                 const u32 *__restrict__ icnt,
+__global__ void __launch_bounds__(kEmitThreads, 1) k_stream_emit(StreamMatch m, const u64 *__restrict__ tkey,
+                                                                 const u32 *__restrict__ toff,
                                                                  const u32 *__restrict__ qbase, i64 cap,
                                                                  apo_match_rec *__restrict__ out,
                                                                  const u32 *__restrict__ qorder,
-                                                                 const u32 *__restrict__ gpar,
-                                                                 const u32 *__restrict__ gtr) {
+                                                                 const u32 *__restrict__ opar,
+                                                                 const u32 *__restrict__ otr,
+                                                                 const u32 *__restrict__ odep) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ u32 s_warp[33];
   const int q = int(qorder[blockIdx.x]);
-  const i64 z0 = qoff[q], z1 = qoff[q + 1];
-  if (z0 == z1) return;
+  const i64 a = toff[q], M = i64(toff[q + 1]) - a;  // the stream's matched intervals, in preorder
+  if (M == 0) return;
   const i64 beg = m.off[q], n = m.off[q + 1] - beg;
-  u32 *deep = reinterpret_cast<u32 *>(smem);  // [kSMMax] deepest interval (local pair index) at each rank
-  u32 *cnt = deep + kSMMax;                   // [kSMMax + 1] chain length at each rank (difference array first)
-  unsigned short *RISA = reinterpret_cast<unsigned short *>(cnt + kSMMax + 1);  // [kSMMax]
+  u32 *deep = reinterpret_cast<u32 *>(smem);  // [kSMMax] 1 + deepest interval (preorder id) at each rank, 0 = none
+  u32 *spar = deep + kSMMax;                  // [kEmitPairs] parent, trace id and depth of every
+  u32 *str = spar + kEmitPairs;               //   interval of the stream when they fit on chip
+  u32 *sdep = str + kEmitPairs;
+  unsigned short *RISA = reinterpret_cast<unsigned short *>(sdep + kEmitPairs);  // [kSMMax]
   for (i64 r = threadIdx.x; r < n; r += kEmitThreads) {
-    deep[r] = kNoPar;
-    cnt[r] = 0;
+    deep[r] = 0;
     RISA[m.sa[beg + r] - beg] = (unsigned short)r;
   }
-  if (threadIdx.x == 0) cnt[n] = 0;
+  const bool onchip = M <= kEmitPairs;
+  if (onchip) {
+    for (i64 i = threadIdx.x; i < M; i += kEmitThreads) {
+      spar[i] = opar[a + i];
+      str[i] = otr[a + i];
+      sdep[i] = odep[a + i];
+    }
+  }
+  const u32 *par = onchip ? spar : opar + a, *trs = onchip ? str : otr + a, *dep = onchip ? sdep : odep + a;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // 1. deepest interval per rank and chain-length differences (pair metadata
-  //    loaded lane-parallel, each pair painted by the whole warp)
-  for (i64 gbase = z0 + i64(warp) * 32; gbase < z1; gbase += i64(kEmitThreads)) {
-    const i64 i = gbase + lane;
-    u32 c = 0, lo = 0;
-    if (i < z1) {
-      const u32 z = zsorted[i];
-      c = icnt[z];
-      if (c) lo = u32(ilo[z] - beg);
+  // 1. deepest interval per rank: in preorder a descendant follows its
+  //    ancestors, so the deepest interval containing a rank has the largest id
+  for (i64 kb = i64(warp) * 32; kb < M; kb += i64(kEmitThreads)) {
+    const i64 k = kb + lane;
+    u32 lo = 0, hi = 0;
+    if (k < M) {
+      const u64 kk = tkey[a + k];
+      lo = u32(kk >> 15) & 32767u;
+      hi = 32767u - (u32(kk) & 32767u);
     }
-    if (c) {
-      atomicAdd(&cnt[lo], 1u);
-      atomicSub(&cnt[lo + c], 1u);
-    }
-    u32 live = __ballot_sync(0xffffffffu, c != 0);
+    u32 live = __ballot_sync(0xffffffffu, hi > lo);
     while (live) {
       const int src = __ffs(live) - 1;
       live &= live - 1;
-      const u32 cc = __shfl_sync(0xffffffffu, c, src), ll = __shfl_sync(0xffffffffu, lo, src);
-      const u32 li = u32(gbase + src - z0);
-      for (u32 k = lane; k < cc; k += 32) atomicMin(&deep[ll + k], li);
+      const u32 l0 = __shfl_sync(0xffffffffu, lo, src), h0 = __shfl_sync(0xffffffffu, hi, src);
+      const u32 id1 = u32(kb + src) + 1u;
+      for (u32 r = l0 + lane; r < h0; r += 32)
+        if (deep[r] < id1) atomicMax(&deep[r], id1);
     }
   }
   __syncthreads();
-  // 2. chain lengths per rank: prefix sum of the differences (16 per thread)
+  // 2. ends in order: thread t owns ends [16t, 16t + 16); an end's record
+  //    count is the depth of its deepest interval; record offsets by a CTA
+  //    scan, then each end's chain is walked and written back to back (a
+  //    warp's writes stay within a few KB, so sectors fill in L2).
   constexpr int kPer = kSMMax / kEmitThreads;
   const int b0 = threadIdx.x * kPer;
-  {
-    u32 v[kPer];
-    u32 sum = 0;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      v[j] = b0 + j < n ? cnt[b0 + j] : 0u;
-      sum += v[j];
-    }
-    u32 run;
-    cta_excl_scan(sum, s_warp, &run);
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      run += v[j];
-      if (b0 + j < n) cnt[b0 + j] = run;
-    }
-  }
-  __syncthreads();
-  // 3. ends in order: thread t owns ends [16t, 16t + 16); record offsets by a
-  //    scan of the chain lengths, then each end's chain is walked and written
   u32 ce[kPer];
-  u32 sum = 0;
+  u32 tsum = 0;
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
     const i64 e = b0 + j;
-    ce[j] = e < n ? cnt[RISA[n - 1 - e]] : 0u;
-    sum += ce[j];
+    const u32 d1 = e < n ? deep[RISA[n - 1 - e]] : 0u;
+    ce[j] = d1 ? dep[d1 - 1] : 0u;
+    tsum += ce[j];
   }
   u32 run;
-  cta_excl_scan(sum, s_warp, &run);
-  const i64 qb = i64(qbase[q]);
+  cta_excl_scan(tsum, s_warp, &run);
+  i64 pos = i64(qbase[q]) + run;
 #pragma unroll 1
   for (int j = 0; j < kPer; ++j) {
     if (!ce[j]) continue;
     const i64 e = b0 + j;
-    u32 z = deep[RISA[n - 1 - e]];
-    i64 pos = qb + run;
+    u32 z = deep[RISA[n - 1 - e]] - 1u;
     for (u32 k = 0; k < ce[j]; ++k, ++pos) {
-      const u32 t = gtr[z0 + z];
-      if (pos < cap) reinterpret_cast<int4 *>(out)[pos] = make_int4(q, i32(e), i32(t), 0);  // one 16-B store
-      z = gpar[z0 + z];
+      if (pos < cap) reinterpret_cast<int4 *>(out)[pos] = make_int4(q, i32(e), i32(trs[z]), 0);  // one 16-B store
+      z = par[z];
     }
-    run += ce[j];
   }
 }
 
@@ -1659,6 +1648,8 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             full.take<u32>(P);
             full.take<u32>(P);
             full.take<u32>(P);
+            full.take<u32>(P);
+            full.take<u32>(P);
             if (full.off > c.aux.cap) {
               c.aux.reserve(full.off, s);
               Carver cb(c.aux.base);
@@ -1680,7 +1671,8 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             u64 *tk = cz.take<u64>(P), *tk_alt = cz.take<u64>(P);
             u32 *tv = cz.take<u32>(P), *tv_alt = cz.take<u32>(P);
             u32 *tof = cz.take<u32>(size_t(nstreams) + 1);
-            u32 *gpar = cz.take<u32>(P), *ghi = cz.take<u32>(P), *gtr = cz.take<u32>(P);
+            u32 *gpar = cz.take<u32>(P), *ghi = cz.take<u32>(P), *gtr = cz.take<u32>(P), *gdep = cz.take<u32>(P);
+            u32 *otr = cz.take<u32>(P);
             k_pair_list<<<grid_for(T * 32, T256), T256, 0, s>>>(pbase, ea, ecnt, sord, e_q, T, pair_e, ptr, qk, qv);
             APO_CHECK_LAUNCH();
             bool aq = radix_sort_u64_u32(c, qk, qv, qk_alt, qv_alt, P, 0, bits_for(u64(nstreams - 1)), s);
@@ -1719,17 +1711,17 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
               const u32 *stv = at ? tv_alt : tv;
               k_tree_offsets<<<grid_for(i64(nstreams) + 1, T256), T256, 0, s>>>(stk, P, nstreams, tof);
               APO_CHECK_LAUNCH();
-              k_tree_sweep<<<nstreams, 32, 0, s>>>(stk, stv, tof, qoff, gpar, ghi);
+              k_tree_sweep<<<nstreams, 32, 0, s>>>(stk, stv, tof, gtr, gpar, ghi, gdep, otr);
               APO_CHECK_LAUNCH();
-              const size_t esmem = sizeof(u32) * (2 * kSMMax + 1) + sizeof(unsigned short) * kSMMax;
+              const size_t esmem = sizeof(u32) * (kSMMax + 3 * kEmitPairs) + sizeof(unsigned short) * kSMMax;
               static bool eattr = false;
               if (!eattr) {
                 APO_CUDA(cudaFuncSetAttribute(k_stream_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               int(esmem)));
                 eattr = true;
               }
-              k_stream_emit<<<nstreams, kEmitThreads, esmem, s>>>(sm, sqv, qoff, ilo, icnt, qbase, cap, d_out, qorder,
-                                                                  gpar, gtr);
+              k_stream_emit<<<nstreams, kEmitThreads, esmem, s>>>(sm, stk, tof, qbase, cap, d_out, qorder, gpar, otr,
+                                                                  gdep);
               APO_CHECK_LAUNCH();
               c.launches += 4;
             }
