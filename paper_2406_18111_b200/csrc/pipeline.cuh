@@ -69,6 +69,7 @@ struct SelWork {
   i32 *rmq[32];           // sparse table over LCP, levels 1..J (level 0 = lcp)
   int rmq_levels;
   i32 *glen;              // 2N per-group length
+  i32 *gbase;             // 2N per-group window base (global position of the window start)
   i32 *cl, *cs, *cg;      // 2N per candidate (final order): length, start (global), group
   u8 *state;              // 2N 0 undecided, 1 kept, 2 rejected
   u32 *tab[32];           // greedy first-cover table levels (N each)

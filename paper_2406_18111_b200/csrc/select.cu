@@ -111,17 +111,23 @@ __global__ void k_rmq_level(const i32 *__restrict__ prev, i32 *__restrict__ next
   next[k] = x;
 }
 
+// sort-2 keys (group, window-local start): a group never spans windows, so
+// the local start orders it as the global one does, in bits(maxwin) bits
+// instead of bits(N); the group's window base is kept aside (gbase)
 struct HeadF {
   const u32 *k1;
   const u64 *v1;
   Rmq rmq;
   i64 maxl;
   u32 lmask;
-  int bN;
+  int bL;
   i64 m;
   u64 *k2;
   i32 *glen;
   i64 *G_out;
+  const i64 *off;
+  const i32 *wid;  // NULL for one window
+  i32 *gbase;
   __device__ u32 load(i64 c) const {
     if (c == 0) return 1;
     if (k1[c] != k1[c - 1]) return 1;
@@ -132,22 +138,27 @@ struct HeadF {
   }
   __device__ bool store(i64 c, u32 incl, u32 excl) const {
     u64 g = u64(incl - 1);
-    u64 s = v1[c] & 0xffffffffull;
-    k2[c] = (g << bN) | s;
-    if (incl != excl) glen[g] = i32(maxl - i64(k1[c] & lmask));
+    const i64 s = i64(v1[c] & 0xffffffffull);
+    const i64 base = wid ? off[wid[s]] : 0;
+    k2[c] = (g << bL) | u64(s - base);
+    if (incl != excl) {
+      glen[g] = i32(maxl - i64(k1[c] & lmask));
+      gbase[g] = i32(base);
+    }
     if (c == m - 1) *G_out = i64(incl);
     return false;
   }
   __device__ u32 *flag() const { return nullptr; }
 };
 
-__global__ void k_unpack(const u64 *__restrict__ k2, i64 m, int bN, const i32 *__restrict__ glen,
-                         i32 *__restrict__ cl, i32 *__restrict__ cs, i32 *__restrict__ cg, u8 *__restrict__ state) {
+__global__ void k_unpack(const u64 *__restrict__ k2, i64 m, int bL, const i32 *__restrict__ glen,
+                         const i32 *__restrict__ gbase, i32 *__restrict__ cl, i32 *__restrict__ cs,
+                         i32 *__restrict__ cg, u8 *__restrict__ state) {
   i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= m) return;
   u64 key = k2[c];
-  i32 g = i32(key >> bN);
-  cs[c] = i32(key & ((1ull << bN) - 1));
+  i32 g = i32(key >> bL);
+  cs[c] = gbase[g] + i32(key & ((1ull << bL) - 1));
   cg[c] = g;
   cl[c] = glen[g];
   state[c] = 0;
@@ -389,6 +400,7 @@ void plan_select(Carver &cv, const Batch &b, SelWork &w) {
   if (w.rmq_levels > 31) w.rmq_levels = 31;
   for (int j = 1; j < w.rmq_levels; ++j) w.rmq[j] = cv.take<i32>(N);
   w.glen = cv.take<i32>(M);
+  w.gbase = cv.take<i32>(M);
   w.cl = cv.take<i32>(M);
   w.cs = cv.take<i32>(M);
   w.cg = cv.take<i32>(M);
@@ -442,16 +454,17 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
     c.launches++;
     rmq.lv[j] = w.rmq[j];
   }
-  const int bN = bits_for(u64(N - 1));
+  const int bL = bits_for(u64(b.maxwin > 1 ? b.maxwin - 1 : 1));
   {
-    HeadF f{k1, v1, rmq, maxl, (1u << bl) - 1u, bN, m, w.k2, w.glen, G_dev};
+    HeadF f{k1, v1, rmq, maxl, (1u << bl) - 1u, bL, m, w.k2, w.glen, G_dev, b.off, b.W > 1 ? b.wid : nullptr,
+            w.gbase};
     launch_scan<false>(c, m, f, s);
   }
   const i64 G = i64(c.read_u64(reinterpret_cast<u64 *>(G_dev), s));
   w.G = G;
-  bool a2 = radix_sort_u64_keys(c, w.k2, w.k2_alt, m, 0, bN + bits_for(u64(G - 1)), s);
+  bool a2 = radix_sort_u64_keys(c, w.k2, w.k2_alt, m, 0, bL + bits_for(u64(G - 1)), s);
   const u64 *k2 = a2 ? w.k2_alt : w.k2;
-  k_unpack<<<grid_for(m, T), T, 0, s>>>(k2, m, bN, w.glen, w.cl, w.cs, w.cg, w.state);
+  k_unpack<<<grid_for(m, T), T, 0, s>>>(k2, m, bL, w.glen, w.gbase, w.cl, w.cs, w.cg, w.state);
   APO_CHECK_LAUNCH();
   c.launches++;
 
