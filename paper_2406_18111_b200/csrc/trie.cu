@@ -552,6 +552,8 @@ __global__ void k_q_offsets(const u64 *__restrict__ qkey, i64 P, int S, u32 *__r
   qoff[q] = u32(lo);
 }
 
+constexpr int kCmpChunks = 8;  // trace tokens fetched per round trip: 8 x 32
+
 // Warp-cooperative compare of trace t with the on-chip stream suffix at p;
 // the trace's first 64 tokens live in registers (r0 = t[lane],
 // r1 = t[32 + lane]), later tokens come from global memory.
@@ -575,16 +577,16 @@ __device__ __forceinline__ int warp_cmp_smem(const u64 *__restrict__ S, i64 p, i
       return __shfl_sync(0xffffffffu, res, f);
     }
   }
-  // later tokens: four 32-token chunks per round trip to L2/HBM
-  for (; base < L; base += 128) {
-    u64 x[4];
+  // later tokens: kCmpChunks 32-token chunks per round trip to L2/HBM
+  for (; base < L; base += 32 * kCmpChunks) {
+    u64 x[kCmpChunks];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < kCmpChunks; ++c) {
       const i64 k = base + c * 32 + lane;
       x[c] = k < L ? t[k] : 0ull;
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < kCmpChunks; ++c) {
       const i64 k = base + c * 32 + lane;
       int res = 0;
       if (k < L) res = (p + k >= n) ? 1 : (x[c] == S[p + k] ? 0 : (x[c] < S[p + k] ? -1 : 1));
