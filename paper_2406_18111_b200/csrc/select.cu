@@ -322,7 +322,9 @@ __global__ void k_emit_cands(Batch b, const i32 *__restrict__ cl, const i32 *__r
 // candidates are contiguous in the sorted order; the marks are a bitset in
 // shared memory (kGreedyMaxWin bits); a candidate is kept iff the bits of
 // its first and last positions are clear, then the warp sets its interval's
-// bits 32 words at a time.  Candidates are staged 32 at a time by the warp.
+// bits 32 words at a time.  Candidates are staged 32 at a time by the warp;
+// the lanes first reject in parallel every staged candidate that already
+// overlaps a mark, and only the rest are decided one by one, in order.
 constexpr int kGreedyMaxWin = 16384;
 constexpr int kGreedyWarps = 8;
 
@@ -361,9 +363,19 @@ __global__ void __launch_bounds__(kGreedyWarps * 32) k_greedy_window(Batch b, co
       ml = cl[my];
       ms = i32(cs[my] - beg);
     }
-    const int cnt = int(c1 - base < 32 ? c1 - base : 32);
+    // marks only grow, so a candidate whose end bits are already set now is
+    // rejected whatever the earlier candidates of this batch do: only the
+    // survivors of this parallel pre-check are walked in order
+    bool maybe = false;
+    if (my < c1) {
+      const i32 en = ms + ml - 1;
+      maybe = !((mk[ms >> 5] >> (ms & 31)) & 1u) && !((mk[en >> 5] >> (en & 31)) & 1u);
+    }
+    u32 pend = __ballot_sync(0xffffffffu, maybe);
     u32 keep_bits = 0;
-    for (int k = 0; k < cnt; ++k) {
+    while (pend) {
+      const int k = __ffs(pend) - 1;
+      pend &= pend - 1;
       const i32 l = __shfl_sync(0xffffffffu, ml, k);
       const i32 st = __shfl_sync(0xffffffffu, ms, k);
       const i32 en = st + l - 1;
