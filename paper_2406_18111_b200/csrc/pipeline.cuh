@@ -66,7 +66,7 @@ struct SelWork {
   u32 *k1, *k1_alt;       // 2N sort-1 keys (window, length desc)
   u64 *v1, *v1_alt;       // 2N sort-1 values (pair rank << 32 | start)
   u64 *k2, *k2_alt;       // 2N sort-2 keys (group, start)
-  i32 *rmq[32];           // sparse table over LCP, levels 1..J (level 0 = lcp)
+  i32 *rmq[32];           // LCP range minima: [0] in-block prefix, [1] in-block suffix, [2..] block-min sparse table
   int rmq_levels;
   i32 *glen;              // 2N per-group length
   i32 *gbase;             // 2N per-group window base (global position of the window start)

@@ -90,15 +90,53 @@ struct CandF {
   __device__ u32 *flag() const { return nullptr; }
 };
 
+// Range minimum over the LCP array for the group-head test of K6: blocks of
+// 32 entries with in-block prefix / suffix minima (one warp scan per block)
+// and a sparse table over the block minima only, so the table costs
+// ~bits(maxwin/32) passes over N/32 entries instead of bits(maxwin) passes
+// over N; a query inside one block scans it directly (<= 32 L1-resident
+// entries).
 struct Rmq {
-  const i32 *lv[32];
+  const i32 *lcp;
+  const i32 *pre, *suf;  // min of LCP[block start .. j], LCP[j .. block end]
+  const i32 *lv[32];     // lv[0] = block minima, lv[j] = min over 2^j blocks
   __device__ __forceinline__ i32 min(i64 a, i64 b) const {  // inclusive, a <= b
-    i64 len = b - a + 1;
-    int j = 63 - __clzll(len);
-    i32 x = lv[j][a], y = lv[j][b - (i64(1) << j) + 1];
-    return x < y ? x : y;
+    const i64 ba = a >> 5, bb = b >> 5;
+    if (ba == bb) {
+      i32 x = lcp[a];
+      for (i64 j = a + 1; j <= b; ++j) x = lcp[j] < x ? lcp[j] : x;
+      return x;
+    }
+    i32 x = suf[a] < pre[b] ? suf[a] : pre[b];
+    if (bb - ba > 1) {
+      const i64 l = ba + 1, r = bb - 1;
+      const int j = 63 - __clzll(r - l + 1);
+      const i32 y = lv[j][l], z = lv[j][r - (i64(1) << j) + 1];
+      x = y < x ? y : x;
+      x = z < x ? z : x;
+    }
+    return x;
   }
 };
+
+__global__ void k_rmq_blocks(const i32 *__restrict__ lcp, i64 n, i32 *__restrict__ pre, i32 *__restrict__ suf,
+                             i32 *__restrict__ bmin) {
+  const i64 j = i64(blockIdx.x) * blockDim.x + threadIdx.x;  // blockDim is a multiple of 32
+  const int lane = threadIdx.x & 31;
+  const i32 v = j < n ? lcp[j] : 0x7fffffff;
+  i32 up = v, dn = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const i32 a = __shfl_up_sync(0xffffffffu, up, d), b = __shfl_down_sync(0xffffffffu, dn, d);
+    if (lane >= d) up = a < up ? a : up;
+    if (lane + d < 32) dn = b < dn ? b : dn;
+  }
+  if (j < n) {
+    pre[j] = up;
+    suf[j] = dn;
+  }
+  if (lane == 31 && (j - 31) < n) bmin[j >> 5] = up;
+}
 
 __global__ void k_rmq_level(const i32 *__restrict__ prev, i32 *__restrict__ next, i64 n, i64 half) {
   i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -407,10 +445,14 @@ void plan_select(Carver &cv, const Batch &b, SelWork &w) {
   w.v1_alt = cv.take<u64>(M);
   w.k2 = cv.take<u64>(M);
   w.k2_alt = cv.take<u64>(M);
-  // sparse table over LCP: queries span < maxwin entries
-  w.rmq_levels = bits_for(u64(b.maxwin > 1 ? b.maxwin : 1));
-  if (w.rmq_levels > 31) w.rmq_levels = 31;
-  for (int j = 1; j < w.rmq_levels; ++j) w.rmq[j] = cv.take<i32>(N);
+  // range minima over LCP: in-block prefix/suffix minima (N each) and a
+  // sparse table over the N/32 block minima (queries span < maxwin entries)
+  const i64 nb = (N + 31) / 32;
+  w.rmq_levels = bits_for(u64(b.maxwin / 32 + 2));
+  if (w.rmq_levels > 29) w.rmq_levels = 29;
+  w.rmq[0] = cv.take<i32>(N);
+  w.rmq[1] = cv.take<i32>(N);
+  for (int j = 0; j < w.rmq_levels; ++j) w.rmq[j + 2] = cv.take<i32>(nb);
   w.glen = cv.take<i32>(M);
   w.gbase = cv.take<i32>(M);
   w.cl = cv.take<i32>(M);
@@ -459,12 +501,21 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
   const u32 *k1 = a ? w.k1_alt : w.k1;
   const u64 *v1 = a ? w.v1_alt : w.v1;
   Rmq rmq{};
-  rmq.lv[0] = sa.lcp;
-  for (int j = 1; j < w.rmq_levels; ++j) {
-    k_rmq_level<<<grid_for(N, T), T, 0, s>>>(rmq.lv[j - 1], w.rmq[j], N, i64(1) << (j - 1));
+  {
+    const i64 nb = (N + 31) / 32;
+    rmq.lcp = sa.lcp;
+    rmq.pre = w.rmq[0];
+    rmq.suf = w.rmq[1];
+    k_rmq_blocks<<<grid_for(nb * 32, T), T, 0, s>>>(sa.lcp, N, w.rmq[0], w.rmq[1], w.rmq[2]);
     APO_CHECK_LAUNCH();
     c.launches++;
-    rmq.lv[j] = w.rmq[j];
+    rmq.lv[0] = w.rmq[2];
+    for (int j = 1; j < w.rmq_levels; ++j) {
+      k_rmq_level<<<grid_for(nb, T), T, 0, s>>>(rmq.lv[j - 1], w.rmq[j + 2], nb, i64(1) << (j - 1));
+      APO_CHECK_LAUNCH();
+      c.launches++;
+      rmq.lv[j] = w.rmq[j + 2];
+    }
   }
   const int bL = bits_for(u64(b.maxwin > 1 ? b.maxwin - 1 : 1));
   {
