@@ -166,6 +166,7 @@ struct HeadF {
   const i64 *off;
   const i32 *wid;  // NULL for one window
   i32 *gbase;
+  u32 *gpos;       // position of the group's first member in sort-1 order
   __device__ u32 load(i64 c) const {
     if (c == 0) return 1;
     if (k1[c] != k1[c - 1]) return 1;
@@ -182,6 +183,7 @@ struct HeadF {
     if (incl != excl) {
       glen[g] = i32(maxl - i64(k1[c] & lmask));
       gbase[g] = i32(base);
+      gpos[g] = u32(c);
     }
     if (c == m - 1) *G_out = i64(incl);
     return false;
@@ -200,6 +202,41 @@ __global__ void k_unpack(const u64 *__restrict__ k2, i64 m, int bL, const i32 *_
   cg[c] = g;
   cl[c] = glen[g];
   state[c] = 0;
+}
+
+// Sort-2 without a radix sort when every group is small (the common case:
+// ~2 members per group on C4).  In sort-1 order the members of a group are
+// already contiguous (same window and length, SA ranks of one LCP interval),
+// so only the members of each group need ordering by start: an item's place
+// is its group's first position plus the number of members with a smaller
+// (local start, position) -- and the unpacking of k_unpack happens in the
+// same pass.  A group larger than kSegMax sets *big and the caller falls
+// back to the radix sort.
+constexpr u32 kSegMax = 64;
+
+__global__ void k_seg_unpack(const u64 *__restrict__ k2, i64 m, i64 G, int bL, const u32 *__restrict__ gpos,
+                             const i32 *__restrict__ glen, const i32 *__restrict__ gbase, i32 *__restrict__ cl,
+                             i32 *__restrict__ cs, i32 *__restrict__ cg, u8 *__restrict__ state,
+                             u32 *__restrict__ big) {
+  const i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  const u64 key = k2[c];
+  const i64 g = i64(key >> bL);
+  const i64 gs = gpos[g], ge = g + 1 < G ? i64(gpos[g + 1]) : m;
+  if (ge - gs > kSegMax) {
+    atomicOr(big, 1u);
+    return;
+  }
+  i64 r = 0;
+  for (i64 j = gs; j < ge; ++j) {
+    const u64 o = k2[j];
+    r += (o < key) || (o == key && j < c);
+  }
+  const i64 p = gs + r;
+  cs[p] = gbase[g] + i32(key & ((1ull << bL) - 1));
+  cg[p] = i32(g);
+  cl[p] = glen[g];
+  state[p] = 0;
 }
 
 struct Tab {
@@ -455,6 +492,7 @@ void plan_select(Carver &cv, const Batch &b, SelWork &w) {
   for (int j = 0; j < w.rmq_levels; ++j) w.rmq[j + 2] = cv.take<i32>(nb);
   w.glen = cv.take<i32>(M);
   w.gbase = cv.take<i32>(M);
+  w.gpos = cv.take<u32>(M);
   w.cl = cv.take<i32>(M);
   w.cs = cv.take<i32>(M);
   w.cg = cv.take<i32>(M);
@@ -520,16 +558,22 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
   const int bL = bits_for(u64(b.maxwin > 1 ? b.maxwin - 1 : 1));
   {
     HeadF f{k1, v1, rmq, maxl, (1u << bl) - 1u, bL, m, w.k2, w.glen, G_dev, b.off, b.W > 1 ? b.wid : nullptr,
-            w.gbase};
+            w.gbase, w.gpos};
     launch_scan<false>(c, m, f, s);
   }
   const i64 G = i64(c.read_u64(reinterpret_cast<u64 *>(G_dev), s));
   w.G = G;
-  bool a2 = radix_sort_u64_keys(c, w.k2, w.k2_alt, m, 0, bL + bits_for(u64(G - 1)), s);
-  const u64 *k2 = a2 ? w.k2_alt : w.k2;
-  k_unpack<<<grid_for(m, T), T, 0, s>>>(k2, m, bL, w.glen, w.gbase, w.cl, w.cs, w.cg, w.state);
+  u32 *big = reinterpret_cast<u32 *>(w.scal + 3);
+  k_seg_unpack<<<grid_for(m, T), T, 0, s>>>(w.k2, m, G, bL, w.gpos, w.glen, w.gbase, w.cl, w.cs, w.cg, w.state, big);
   APO_CHECK_LAUNCH();
   c.launches++;
+  if (c.read_u32(big, s) != 0) {  // a large group somewhere: sort all keys instead
+    bool a2 = radix_sort_u64_keys(c, w.k2, w.k2_alt, m, 0, bL + bits_for(u64(G - 1)), s);
+    const u64 *k2 = a2 ? w.k2_alt : w.k2;
+    k_unpack<<<grid_for(m, T), T, 0, s>>>(k2, m, bL, w.glen, w.gbase, w.cl, w.cs, w.cg, w.state);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+  }
 
   // ---- K7 ----
   if (b.maxwin <= kGreedyMaxWin && b.W >= 8) {
