@@ -556,7 +556,13 @@ constexpr int kCmpChunks = 8;  // trace tokens fetched per round trip: 8 x 32
 
 // Warp-cooperative compare of trace t with the on-chip stream suffix at p;
 // the trace's first 64 tokens live in registers (r0 = t[lane],
-// r1 = t[32 + lane]), later tokens come from global memory.
+// r1 = t[32 + lane]), later tokens come from global memory.  Each 32-token
+// step only tests inequality (one ballot); the order of the first differing
+// token is resolved once, at the end.
+__device__ __forceinline__ int cmp_at(u64 x, const u64 *__restrict__ S, i64 pk, i64 n) {
+  return pk >= n ? 1 : (x < S[pk] ? -1 : 1);  // called for a differing (or past-the-end) position only
+}
+
 __device__ __forceinline__ int warp_cmp_smem(const u64 *__restrict__ S, i64 p, i64 n, const u64 *__restrict__ t,
                                              u64 r0, u64 r1, i64 L, i64 from, i64 *lcp) {
   const int lane = threadIdx.x & 31;
@@ -568,13 +574,12 @@ __device__ __forceinline__ int warp_cmp_smem(const u64 *__restrict__ S, i64 p, i
     const u64 a = __shfl_sync(0xffffffffu, r0, src);
     const u64 b = __shfl_sync(0xffffffffu, r1, src);
     const u64 x = k < 32 ? a : (k < 64 ? b : (k < L ? t[k] : 0ull));
-    int res = 0;
-    if (k < L) res = (p + k >= n) ? 1 : (x == S[p + k] ? 0 : (x < S[p + k] ? -1 : 1));
-    const u32 m = __ballot_sync(0xffffffffu, res != 0);
+    const bool ne = k < L && (p + k >= n || x != S[p + k]);
+    const u32 m = __ballot_sync(0xffffffffu, ne);
     if (m) {
       const int f = __ffs(m) - 1;
       *lcp = base + f;
-      return __shfl_sync(0xffffffffu, res, f);
+      return __shfl_sync(0xffffffffu, ne ? cmp_at(x, S, p + k, n) : 0, f);
     }
   }
   // later tokens: kCmpChunks 32-token chunks per round trip to L2/HBM
@@ -588,13 +593,12 @@ __device__ __forceinline__ int warp_cmp_smem(const u64 *__restrict__ S, i64 p, i
 #pragma unroll
     for (int c = 0; c < kCmpChunks; ++c) {
       const i64 k = base + c * 32 + lane;
-      int res = 0;
-      if (k < L) res = (p + k >= n) ? 1 : (x[c] == S[p + k] ? 0 : (x[c] < S[p + k] ? -1 : 1));
-      const u32 m = __ballot_sync(0xffffffffu, res != 0);
+      const bool ne = k < L && (p + k >= n || x[c] != S[p + k]);
+      const u32 m = __ballot_sync(0xffffffffu, ne);
       if (m) {
         const int f = __ffs(m) - 1;
         *lcp = base + c * 32 + f;
-        return __shfl_sync(0xffffffffu, res, f);
+        return __shfl_sync(0xffffffffu, ne ? cmp_at(x[c], S, p + k, n) : 0, f);
       }
     }
   }
@@ -611,26 +615,56 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
                                                                 u32 *__restrict__ icnt, u32 *__restrict__ qtot,
                                                                 const u32 *__restrict__ qorder) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ u32 s_tot;
+  __shared__ u32 s_tot, s_next;
+  __shared__ unsigned short s_bmin[kSMMax / 32];  // minima of LC over 32-entry blocks
   const int q = int(qorder[blockIdx.x]);
   const i64 z0 = qoff[q], z1 = qoff[q + 1];
   if (z0 == z1) {
     if (threadIdx.x == 0) qtot[q] = 0;
     return;
   }
-  if (threadIdx.x == 0) s_tot = 0;
+  if (threadIdx.x == 0) {
+    s_tot = 0;
+    s_next = kSMThreads / 32;
+  }
   const i64 beg = m.off[q], n = m.off[q + 1] - beg;
   u64 *S = reinterpret_cast<u64 *>(smem);
   unsigned short *SA = reinterpret_cast<unsigned short *>(S + kSMMax);
   unsigned short *LC = SA + kSMMax;
-  for (i64 i = threadIdx.x; i < n; i += kSMThreads) {
-    S[i] = m.tok[beg + i];
-    SA[i] = (unsigned short)(m.sa[beg + i] - beg);
-    LC[i] = (unsigned short)m.lcp[beg + i];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (i64 i = threadIdx.x; i < ((n + 31) & ~i64(31)); i += kSMThreads) {
+    u32 v = 0xffffu;
+    if (i < n) {
+      S[i] = m.tok[beg + i];
+      SA[i] = (unsigned short)(m.sa[beg + i] - beg);
+      v = u32(m.lcp[beg + i]);
+      LC[i] = (unsigned short)v;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, d));
+    if (lane == 0) s_bmin[i >> 5] = (unsigned short)v;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (i64 i = z0 + warp; i < z1; i += kSMThreads / 32) {
+  // lcp(S_a, S_b) = min LC[a .. b-1]: partial blocks directly, whole blocks
+  // from their minima
+  auto range_min = [&](i64 a, i64 b) -> u32 {
+    u32 mn = 0xffffu;
+    const i64 ba = (a + 31) >> 5, bb = b >> 5;
+    if (ba >= bb) {
+      for (i64 k = a + lane; k < b; k += 32) mn = min(mn, u32(LC[k]));
+    } else {
+      const i64 k1 = a + lane, k2 = (bb << 5) + lane;
+      if (k1 < (ba << 5)) mn = min(mn, u32(LC[k1]));
+      if (k2 < b) mn = min(mn, u32(LC[k2]));
+      for (i64 k = ba + lane; k < bb; k += 32) mn = min(mn, u32(s_bmin[k]));
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, d));
+    return mn;
+  };
+  // pairs are handed out one at a time (the first 32 statically), so a few
+  // long searches do not leave the other warps idle at the end
+  for (i64 i = z0 + warp; i < z1;) {
     const u32 z = zsorted[i];
     const u32 e = pair_e[z];
     const i64 t = ptrace[z];
@@ -651,11 +685,7 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
       if (real && llo != lhi) {
         const bool left = llo > lhi;
         const i64 a = left ? lo : mid, b = left ? mid : hi;  // lcp(S_a, S_b) = min LC[a..b-1]
-        u32 mn = 0xffffu;
-        for (i64 k = a + lane; k < b; k += 32) mn = min(mn, u32(LC[k]));
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, d));
-        const i64 x = mn;
+        const i64 x = range_min(a, b);
         if (left) {
           if (x > llo) { lo = mid; continue; }            // S_mid < t, lcp(t, S_mid) = llo
           if (x < llo) { hi = mid; lhi = x; continue; }   // t < S_mid, lcp = x
@@ -694,11 +724,14 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
         cnt += 32;
       }
     }
+    u32 nx = 0;
     if (lane == 0) {
       ilo[z] = beg + hi;
       icnt[z] = u32(cnt);
       if (cnt) atomicAdd(&s_tot, u32(cnt));
+      nx = atomicAdd(&s_next, 1u);
     }
+    i = z0 + __shfl_sync(0xffffffffu, nx, 0);
   }
   __syncthreads();
   if (threadIdx.x == 0) qtot[q] = s_tot;
