@@ -137,22 +137,27 @@ __device__ __forceinline__ void lsd_passes(WinBuf &X, WinBuf &Y, WinSmem &S) {
   if constexpr (NP >= 4) lsd_pass<24, 8>(Y, X, S);
 }
 
-// Dense id of every sorted item's key group, stored at rank[pos].  Warp w
-// owns the sorted items [512w, 512w+512) and walks them in 16 rows of 32
-// consecutive items (conflict-free shared-memory access): a row's group heads
-// come from one ballot, the running count from popc.  Returns the number of
-// groups among the first n items.
-__device__ __forceinline__ u32 dense_rank(const WinBuf &sorted, unsigned short *rank, i64 n, WinSmem &S) {
+// Dense id of every sorted item's key group, stored at rank[pos], and the
+// sorted index of every group's first item at gstart[id] (gstart = rank +
+// kWMax: the upper half of the same key area).  Warp w owns the sorted items
+// [512w, 512w+512) and walks them in 16 rows of 32 consecutive items
+// (conflict-free shared-memory access): a row's group heads come from one
+// ballot, the running count from popc.  KeyAt(q) gives the key of sorted
+// item q.  Returns the number of groups among the first n items.
+template <class KeyAt>
+__device__ __forceinline__ u32 dense_rank_by(KeyAt key_at, const unsigned short *spos, unsigned short *rank, i64 n,
+                                             WinSmem &S) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wbase = warp * (32 * kWItems);
   const u32 lt = lanemask_lt_w();
+  unsigned short *gstart = rank + kWMax;
   // pass 1: heads of this warp's segment
   u32 cnt = 0;
 #pragma unroll 4
   for (int j = 0; j < kWItems; ++j) {
     const int q = wbase + j * 32 + lane;
-    const u32 k = sorted.key[q];
-    const u32 pk = q > 0 ? sorted.key[q - 1] : 0xffffffffu;
+    const u32 k = q < n ? key_at(q) : 0u;
+    const u32 pk = (q > 0 && q < n) ? key_at(q - 1) : 0xffffffffu;
     cnt += __popc(__ballot_sync(0xffffffffu, k != pk && q < n));
   }
   if (lane == 0) S.scan[warp] = cnt;
@@ -168,15 +173,76 @@ __device__ __forceinline__ u32 dense_rank(const WinBuf &sorted, unsigned short *
 #pragma unroll 4
   for (int j = 0; j < kWItems; ++j) {
     const int q = wbase + j * 32 + lane;
-    const u32 k = sorted.key[q];
-    const u32 pk = q > 0 ? sorted.key[q - 1] : 0xffffffffu;
-    const u32 hb = __ballot_sync(0xffffffffu, k != pk && q < n);
+    const u32 k = q < n ? key_at(q) : 0u;
+    const u32 pk = (q > 0 && q < n) ? key_at(q - 1) : 0xffffffffu;
+    const bool head = k != pk && q < n;
+    const u32 hb = __ballot_sync(0xffffffffu, head);
     const u32 id = run + __popc(hb & lt) + ((hb >> lane) & 1u);  // heads up to and including q
-    if (q < n) rank[sorted.pos[q]] = (unsigned short)(id - 1);
+    if (q < n) rank[spos[q]] = (unsigned short)(id - 1);
+    if (head) gstart[id - 1] = (unsigned short)q;
     run += __popc(hb);
   }
   __syncthreads();
   return total;
+}
+
+__device__ __forceinline__ u32 dense_rank(const WinBuf &sorted, unsigned short *rank, i64 n, WinSmem &S) {
+  return dense_rank_by([&](int q) { return sorted.key[q]; }, sorted.pos, rank, n, S);
+}
+
+// Largest group of the current ranking (group starts from dense_rank).
+__device__ __forceinline__ u32 max_group(const unsigned short *rank, u32 G, i64 n) {
+  __shared__ u32 s_mx;
+  if (threadIdx.x == 0) s_mx = 0;
+  __syncthreads();
+  const unsigned short *gstart = rank + kWMax;
+  u32 mx = 0;
+  for (u32 g = threadIdx.x; g < G; g += kWT) {
+    const u32 e = g + 1 < G ? u32(gstart[g + 1]) : u32(n);
+    mx = max(mx, e - u32(gstart[g]));
+  }
+  atomicMax(&s_mx, mx);
+  __syncthreads();
+  const u32 r = s_mx;
+  __syncthreads();
+  return r;
+}
+
+// One doubling round when every current group holds at most kSmallGroup
+// items (late rounds of loop-shaped windows): the items are still in sorted
+// order of their current rank, so only each group's members need ordering by
+// rank[i + h]; an item's new sorted index is its group's start plus the
+// number of members ordered before it (by rank[i+h], ties by current index).
+// Reads sorted positions P.pos and ranks R.key; writes the new order to
+// R.pos, then the new ranks (and group starts) to P.key.  No LSD pass.
+constexpr u32 kSmallGroup = 32;
+
+__device__ __forceinline__ u32 small_group_round(WinBuf &P, WinBuf &R, u32 G, i64 n, i64 h, int bg, WinSmem &S) {
+  const unsigned short *rank = reinterpret_cast<const unsigned short *>(R.key);
+  const unsigned short *gstart = rank + kWMax;
+  auto r2 = [&](u32 p) -> u32 { return (i64(p) + h < n) ? u32(rank[p + h]) + 1u : 0u; };
+  for (int q = threadIdx.x; q < n; q += kWT) {
+    const u32 p = P.pos[q];
+    const u32 g = rank[p];
+    const u32 a = gstart[g], b = g + 1 < G ? u32(gstart[g + 1]) : u32(n);
+    u32 nq = u32(q);
+    if (b - a > 1) {
+      const u32 mine = r2(p);
+      u32 c = 0;
+      for (u32 j = a; j < b; ++j) {
+        const u32 o = r2(P.pos[j]);
+        c += (o < mine) || (o == mine && j < u32(q));
+      }
+      nq = a + c;
+    }
+    R.pos[nq] = (unsigned short)p;
+  }
+  __syncthreads();
+  unsigned short *nrank = reinterpret_cast<unsigned short *>(P.key);
+  return dense_rank_by([&](int q) {
+    const u32 p = R.pos[q];
+    return (u32(rank[p]) << bg) | r2(p);
+  }, R.pos, nrank, n, S);
 }
 
 template <int NP, bool XA>  // XA: items in S.a, other buffer S.b
@@ -228,7 +294,8 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
   // the key area of the buffer NOT holding the sorted items.
   bool rank_in_b = true;  // ranks in S.b.key, items built in S.a
   bool sorted_in_a = true;
-  u32 G;  // number of distinct ranks
+  u32 G;                 // number of distinct ranks
+  u32 maxg = 0xffffffffu;  // largest group (unknown: the first round sorts)
   auto rank_ptr = [&]() { return reinterpret_cast<unsigned short *>(rank_in_b ? S.b.key : S.a.key); };
   // ---- level 0 ----
   if (ids != nullptr) {
@@ -251,6 +318,7 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
     sorted_in_a = (np & 1) == 0;
     rank_in_b = sorted_in_a;
     G = dense_rank(sorted_in_a ? S.a : S.b, rank_ptr(), n, S);
+    maxg = max_group(rank_ptr(), G, n);
     prof += u64(n) * (kSmemPassBytes * np + kSmemRoundBytes);
     unsigned short *rank = rank_ptr();
     i32 *out = lv.p[0];
@@ -276,29 +344,39 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
     // key = rank[i] << bg | (i + h < n ? rank[i+h] + 1 : 0); ranks < G
     const u32 gmax = G ? G : u32(n);
     const int bg = bits_for(u64(gmax));
-    const int kb = bits_for(u64(gmax - 1)) + bg;
-    const u32 pad = 1u << kb;
-    const unsigned short *rank = rank_ptr();
-    const bool xa = rank_in_b;  // items go to the buffer without the ranks
-    u32 *xk = xa ? S.a.key : S.b.key;
-    unsigned short *xp = xa ? S.a.pos : S.b.pos;
-    for (int q = tid; q < kWMax; q += kWT) {
-      u32 key = pad;
-      if (q < n) {
-        const u32 lo = (q + h < n) ? u32(rank[q + h]) + 1u : 0u;
-        key = (u32(rank[q]) << bg) | lo;
+    if (G && maxg <= kSmallGroup) {
+      // small groups only: order each group's members in place of a sort
+      WinBuf &P = sorted_in_a ? S.a : S.b, &R = sorted_in_a ? S.b : S.a;
+      G = small_group_round(P, R, G, n, h, bg, S);
+      sorted_in_a = !sorted_in_a;
+      rank_in_b = sorted_in_a;
+      prof += u64(n) * kSmemRoundBytes * 2;
+    } else {
+      const int kb = bits_for(u64(gmax - 1)) + bg;
+      const u32 pad = 1u << kb;
+      const unsigned short *rank = rank_ptr();
+      const bool xa = rank_in_b;  // items go to the buffer without the ranks
+      u32 *xk = xa ? S.a.key : S.b.key;
+      unsigned short *xp = xa ? S.a.pos : S.b.pos;
+      for (int q = tid; q < kWMax; q += kWT) {
+        u32 key = pad;
+        if (q < n) {
+          const u32 lo = (q + h < n) ? u32(rank[q + h]) + 1u : 0u;
+          key = (u32(rank[q]) << bg) | lo;
+        }
+        xk[q] = key;
+        xp[q] = (unsigned short)q;
       }
-      xk[q] = key;
-      xp[q] = (unsigned short)q;
+      __syncthreads();
+      const int np = (kb + 1 + 7) / 8;
+      sort_items(S, np, xa);
+      sorted_in_a = ((np & 1) == 0) == xa;
+      rank_in_b = sorted_in_a;
+      G = dense_rank(sorted_in_a ? S.a : S.b, rank_ptr(), n, S);
+      prof += u64(n) * (kSmemPassBytes * np + kSmemRoundBytes);
     }
-    __syncthreads();
-    const int np = (kb + 1 + 7) / 8;
-    sort_items(S, np, xa);
-    sorted_in_a = ((np & 1) == 0) == xa;
-    rank_in_b = sorted_in_a;
     unsigned short *nrank = rank_ptr();
-    G = dense_rank(sorted_in_a ? S.a : S.b, nrank, n, S);
-    prof += u64(n) * (kSmemPassBytes * np + kSmemRoundBytes);
+    maxg = max_group(nrank, G, n);
     ++r;
     if (r < max_levels) {
       i32 *out = lv.p[r];
