@@ -208,29 +208,32 @@ __device__ __forceinline__ u32 max_group(const unsigned short *rank, u32 G, i64 
   return r;
 }
 
-// One doubling round when every current group holds at most kSmallGroup
+// One doubling round when every current group holds at most kSmallGroup (64)
 // items (late rounds of loop-shaped windows): the items are still in sorted
 // order of their current rank, so only each group's members need ordering by
 // rank[i + h]; an item's new sorted index is its group's start plus the
 // number of members ordered before it (by rank[i+h], ties by current index).
 // Reads sorted positions P.pos and ranks R.key; writes the new order to
 // R.pos, then the new ranks (and group starts) to P.key.  No LSD pass.
-constexpr u32 kSmallGroup = 32;
+constexpr u32 kSmallGroup = 64;
 
 __device__ __forceinline__ u32 small_group_round(WinBuf &P, WinBuf &R, u32 G, i64 n, i64 h, int bg, WinSmem &S) {
   const unsigned short *rank = reinterpret_cast<const unsigned short *>(R.key);
   const unsigned short *gstart = rank + kWMax;
   auto r2 = [&](u32 p) -> u32 { return (i64(p) + h < n) ? u32(rank[p + h]) + 1u : 0u; };
+  u32 *R2 = P.key;  // second keys in current sorted order (P.key is free until the new ranks)
+  for (int q = threadIdx.x; q < n; q += kWT) R2[q] = r2(P.pos[q]);
+  __syncthreads();
   for (int q = threadIdx.x; q < n; q += kWT) {
     const u32 p = P.pos[q];
     const u32 g = rank[p];
     const u32 a = gstart[g], b = g + 1 < G ? u32(gstart[g + 1]) : u32(n);
     u32 nq = u32(q);
     if (b - a > 1) {
-      const u32 mine = r2(p);
+      const u32 mine = R2[q];
       u32 c = 0;
       for (u32 j = a; j < b; ++j) {
-        const u32 o = r2(P.pos[j]);
+        const u32 o = R2[j];
         c += (o < mine) || (o == mine && j < u32(q));
       }
       nq = a + c;
