@@ -357,8 +357,13 @@ def main():
     roof_hbm = {"bound": "hbm", "kernel": "k_onesweep (K1 radix-sort digit pass)", "achieved": achieved,
                 "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None,
-                "traffic": tr.get("k_onesweep_dram_bytes_per_launch") if tr else None,
-                "traffic_source": tr.get("source") if tr else None,
+                # the captured pass's DRAM/algorithmic ratio applied to this run's
+                # average pass (passes differ in size; all read and write each
+                # element once)
+                "traffic": (tr["k_onesweep_dram_over_algorithmic"] * rp_bytes / rp_n)
+                if tr and rp_n and "k_onesweep_dram_over_algorithmic" in tr else None,
+                "traffic_source": (tr.get("source", "") + "; " + tr.get("k_onesweep_capture", "")
+                                   + " DRAM/algorithmic ratio x this run's average pass") if tr else None,
                 "launches": rp_n, "bytes_per_launch": rp_bytes / rp_n if rp_n else None,
                 "share_of_step": (rp_ms / ms) if ms else None}
     roofline = roof_hbm
