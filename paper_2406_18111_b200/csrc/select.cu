@@ -49,9 +49,11 @@ struct CandF {
   u64 *v1;
   i64 *m_out;
   __device__ __forceinline__ bool pair(i64 k, i64 &l, i64 &a, i64 &bb, int &w) const {
-    i64 s1 = sa[k];
-    w = b_wid(b, s1);
+    // the SA is window-major: rank k belongs to the window of position k
+    // (a sequential read, not a random one at SA[k])
+    w = b_wid(b, k);
     if (k + 1 >= b_end(b, w)) return false;
+    i64 s1 = sa[k];
     i64 s2 = sa[k + 1];
     i64 p = lcp[k];
     i64 lo = s1 < s2 ? s1 : s2, d = s1 < s2 ? s2 - s1 : s1 - s2;
@@ -165,6 +167,7 @@ struct HeadF {
   i64 *G_out;
   const i64 *off;
   const i32 *wid;  // NULL for one window
+  int bW;          // window field of the sort-1 key starts at bit bW
   i32 *gbase;
   u32 *gpos;       // position of the group's first member in sort-1 order
   __device__ u32 load(i64 c) const {
@@ -178,7 +181,7 @@ struct HeadF {
   __device__ bool store(i64 c, u32 incl, u32 excl) const {
     u64 g = u64(incl - 1);
     const i64 s = i64(v1[c] & 0xffffffffull);
-    const i64 base = wid ? off[wid[s]] : 0;
+    const i64 base = wid ? off[k1[c] >> bW] : 0;  // the window is the key's high field
     k2[c] = (g << bL) | u64(s - base);
     if (incl != excl) {
       glen[g] = i32(maxl - i64(k1[c] & lmask));
@@ -558,7 +561,7 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
   const int bL = bits_for(u64(b.maxwin > 1 ? b.maxwin - 1 : 1));
   {
     HeadF f{k1, v1, rmq, maxl, (1u << bl) - 1u, bL, m, w.k2, w.glen, G_dev, b.off, b.W > 1 ? b.wid : nullptr,
-            w.gbase, w.gpos};
+            bl, w.gbase, w.gpos};
     launch_scan<false>(c, m, f, s);
   }
   const i64 G = i64(c.read_u64(reinterpret_cast<u64 *>(G_dev), s));
