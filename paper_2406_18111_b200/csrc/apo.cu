@@ -98,18 +98,12 @@ apo_status guarded(apo_ctx *ctx, Fn &&fn) {
   }
 }
 
+// position -> window map: one CTA per window fills its range (coalesced)
 __global__ void k_fill_wid(const i64 *__restrict__ off, int W, i64 N, i32 *__restrict__ wid) {
-  i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= N) return;
-  int lo = 0, hi = W - 1;  // last w with off[w] <= i
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (off[mid] <= i)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  wid[i] = lo;
+  const int w = blockIdx.x;
+  if (w >= W) return;
+  const i64 e = off[w + 1];
+  for (i64 i = off[w] + threadIdx.x; i < e; i += blockDim.x) wid[i] = w;
 }
 
 __global__ void k_localize_sa(const i32 *__restrict__ sa, Batch b, i32 *__restrict__ out) {
@@ -173,7 +167,7 @@ Plan setup(Ctx &c, Batch &b, const i64 *h_off, bool want_lcp, bool want_select, 
   plan_all(cv, b, p, want_lcp, want_select);
   if (b.W > 1) {
     APO_CUDA(cudaMemcpyAsync(p.d_off, h_off, sizeof(i64) * (b.W + 1), cudaMemcpyHostToDevice, s));
-    k_fill_wid<<<grid_for(b.N, 256), 256, 0, s>>>(p.d_off, b.W, b.N, p.d_wid);
+    k_fill_wid<<<b.W, 256, 0, s>>>(p.d_off, b.W, b.N, p.d_wid);
     APO_CHECK_LAUNCH();
     c.launches++;
     b.off = p.d_off;

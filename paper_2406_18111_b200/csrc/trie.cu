@@ -287,18 +287,12 @@ __global__ void k_write_hits(const u64 *__restrict__ keys, i64 nhits, i64 cap, i
   out[i] = r;
 }
 
+// position -> window map: one CTA per window fills its range (coalesced)
 __global__ void k_fill_wid_t(const i64 *__restrict__ off, int W, i64 N, i32 *__restrict__ wid) {
-  i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= N) return;
-  int lo = 0, hi = W - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (off[mid] <= i)
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  wid[i] = lo;
+  const int w = blockIdx.x;
+  if (w >= W) return;
+  const i64 e = off[w + 1];
+  for (i64 i = off[w] + threadIdx.x; i < e; i += blockDim.x) wid[i] = w;
 }
 
 // Generalized SA setup for a host-described batch; returns the carved work.
@@ -316,7 +310,7 @@ void plan_gen(Carver &cv, Batch &b, GenPlan &g, bool lcp) {
 
 void upload_batch(Ctx &c, Batch &b, GenPlan &g, const std::vector<i64> &h_off, cudaStream_t s) {
   APO_CUDA(cudaMemcpyAsync(g.d_off, h_off.data(), sizeof(i64) * h_off.size(), cudaMemcpyHostToDevice, s));
-  k_fill_wid_t<<<grid_for(b.N, T256), T256, 0, s>>>(g.d_off, b.W, b.N, g.d_wid);
+  k_fill_wid_t<<<b.W, T256, 0, s>>>(g.d_off, b.W, b.N, g.d_wid);
   APO_CHECK_LAUNCH();
   c.launches++;
   b.off = g.d_off;
