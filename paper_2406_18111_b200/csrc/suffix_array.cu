@@ -122,7 +122,8 @@ __global__ void k_phi(const u32 *__restrict__ sa, Batch b, i32 *__restrict__ phi
   i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= b.N) return;
   i64 i = sa[k];
-  bool first = b.gen ? (k == 0) : (k == b_beg(b, b_wid(b, i)));
+  // the SA is window-major: rank k lies in the window of position k
+  bool first = b.gen ? (k == 0) : (k == b_beg(b, b_wid(b, k)));
   phi[i] = first ? -1 : i32(sa[k - 1]);
 }
 
@@ -199,7 +200,7 @@ __global__ void k_lcp_gather(const u32 *__restrict__ sa, const i32 *__restrict__
                              i32 *__restrict__ lcp) {
   i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= b.N) return;
-  i64 lim = b.gen ? b.N : b_end(b, b_wid(b, sa[k]));
+  i64 lim = b.gen ? b.N : b_end(b, b_wid(b, k));  // window-major SA: rank k is in the window of position k
   lcp[k] = (k + 1 < lim) ? plcp[sa[k + 1]] : 0;
 }
 
