@@ -151,6 +151,29 @@ __global__ void k_rmq_level(const i32 *__restrict__ prev, i32 *__restrict__ next
   next[k] = x;
 }
 
+// Group heads of the sort-1 order, one thread per candidate (all loads in
+// flight at once; the scan that numbers the groups then reads one byte per
+// candidate): a candidate starts a group unless the previous one has the same
+// (window, length) and the same sub-string -- the same pair, or pairs whose
+// SA ranks kp < kc have min LCP[kp .. kc-1] >= length.
+__global__ void k_head_flags(const u32 *__restrict__ k1, const u64 *__restrict__ v1, Rmq rmq, i64 maxl, u32 lmask,
+                             i64 m, u8 *__restrict__ head) {
+  const i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= m) return;
+  if (c == 0) {
+    head[0] = 1;
+    return;
+  }
+  const u32 a = k1[c], b = k1[c - 1];
+  const u64 va = v1[c], vb = v1[c - 1];
+  u8 h = 1;
+  if (a == b) {
+    const i64 kc = i64(va >> 32), kp = i64(vb >> 32);
+    h = (kc == kp) ? 0 : (rmq.min(kp, kc - 1) < maxl - i64(a & lmask) ? 1 : 0);
+  }
+  head[c] = h;
+}
+
 // sort-2 keys (group, window-local start): a group never spans windows, so
 // the local start orders it as the global one does, in bits(maxwin) bits
 // instead of bits(N); the group's window base is kept aside (gbase)
@@ -170,14 +193,8 @@ struct HeadF {
   int bW;          // window field of the sort-1 key starts at bit bW
   i32 *gbase;
   u32 *gpos;       // position of the group's first member in sort-1 order
-  __device__ u32 load(i64 c) const {
-    if (c == 0) return 1;
-    if (k1[c] != k1[c - 1]) return 1;
-    i64 kc = i64(v1[c] >> 32), kp = i64(v1[c - 1] >> 32);
-    if (kc == kp) return 0;
-    i64 l = maxl - i64(k1[c] & lmask);
-    return rmq.min(kp, kc - 1) < l ? 1u : 0u;
-  }
+  const u8 *head;  // group-head flags from k_head_flags
+  __device__ u32 load(i64 c) const { return head[c]; }
   __device__ bool store(i64 c, u32 incl, u32 excl) const {
     u64 g = u64(incl - 1);
     const i64 s = i64(v1[c] & 0xffffffffull);
@@ -560,8 +577,11 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
   }
   const int bL = bits_for(u64(b.maxwin > 1 ? b.maxwin - 1 : 1));
   {
+    k_head_flags<<<grid_for(m, T), T, 0, s>>>(k1, v1, rmq, maxl, (1u << bl) - 1u, m, w.state);
+    APO_CHECK_LAUNCH();
+    c.launches++;
     HeadF f{k1, v1, rmq, maxl, (1u << bl) - 1u, bL, m, w.k2, w.glen, G_dev, b.off, b.W > 1 ? b.wid : nullptr,
-            bl, w.gbase, w.gpos};
+            bl, w.gbase, w.gpos, w.state};
     launch_scan<false>(c, m, f, s);
   }
   const i64 G = i64(c.read_u64(reinterpret_cast<u64 *>(G_dev), s));
