@@ -35,8 +35,8 @@ struct WinBuf {
 
 struct WinSmem {
   WinBuf a, b;  // ping-pong; the u16 rank array aliases b.key while a holds the items
-  unsigned short hist[kWWarps][256];
-  u32 start[256];
+  unsigned short hist[kWWarps][512];  // per-warp digit counts (digits of up to 9 bits)
+  unsigned short start[512];  // digit starts (<= 16,384)
   u32 scan[kWWarps];
 };
 
@@ -64,8 +64,9 @@ __device__ __forceinline__ u32 lanemask_lt_w() {
 template <int SHIFT, int BITS>
 __device__ __forceinline__ void lsd_pass(const WinBuf &src, WinBuf &dst, WinSmem &S) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr u32 mask = (1u << BITS) - 1u;
-  for (int i = tid; i < kWWarps * 256; i += kWT) (&S.hist[0][0])[i] = 0;
+  constexpr int RADIX = 1 << BITS;
+  constexpr u32 mask = RADIX - 1u;
+  for (int i = tid; i < kWWarps * 512; i += kWT) (&S.hist[0][0])[i] = 0;
   __syncthreads();
   unsigned short *wh = S.hist[warp];
   const u32 lt = lanemask_lt_w();
@@ -88,7 +89,7 @@ __device__ __forceinline__ void lsd_pass(const WinBuf &src, WinBuf &dst, WinSmem
   __syncthreads();
   // per digit: exclusive prefix over warps (in place) and the digit total
   u32 total = 0;
-  if (tid < 256) {
+  if (tid < RADIX) {
 #pragma unroll 8
     for (int w = 0; w < kWWarps; ++w) {
       u32 c = S.hist[w][tid];
@@ -102,12 +103,12 @@ __device__ __forceinline__ void lsd_pass(const WinBuf &src, WinBuf &dst, WinSmem
     u32 v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;
   }
-  if (tid < 256 && lane == 31) S.scan[warp] = incl;
+  if (tid < RADIX && lane == 31) S.scan[warp] = incl;
   __syncthreads();
-  if (tid < 256) {
+  if (tid < RADIX) {
     u32 pre = 0;
     for (int w = 0; w < warp; ++w) pre += S.scan[w];
-    S.start[tid] = pre + incl - total;
+    S.start[tid] = (unsigned short)(pre + incl - total);
   }
   __syncthreads();
 #pragma unroll
@@ -116,25 +117,21 @@ __device__ __forceinline__ void lsd_pass(const WinBuf &src, WinBuf &dst, WinSmem
     u32 k = src.key[q];
     u32 d = (k >> SHIFT) & mask;
     u32 r = (rk[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
-    u32 p = S.start[d] + wh[d] + r;
+    u32 p = u32(S.start[d]) + wh[d] + r;
     dst.key[p] = k;
     dst.pos[p] = src.pos[q];
   }
   __syncthreads();
 }
 
-// Sort the items of buffer X (keys, positions) with `npass` 8-bit LSD passes
-// (npass in 1..4, uniform over the block), then give every item the DENSE id
-// of its key group (block sum-scan of group heads; thread t owns sorted
-// positions [16t, 16t+16)) and store it at rank[pos].  The sorted items end
-// in X (npass even) or in Y (odd); rank must point into the OTHER buffer.
-// Returns the number of groups among the first n items.
-template <int NP>
+// Sort the items of buffer X (keys, positions) with NP stable LSD passes of
+// W-bit digits (the sorted items end in X for even NP, in Y for odd NP).
+template <int NP, int W>
 __device__ __forceinline__ void lsd_passes(WinBuf &X, WinBuf &Y, WinSmem &S) {
-  lsd_pass<0, 8>(X, Y, S);
-  if constexpr (NP >= 2) lsd_pass<8, 8>(Y, X, S);
-  if constexpr (NP >= 3) lsd_pass<16, 8>(X, Y, S);
-  if constexpr (NP >= 4) lsd_pass<24, 8>(Y, X, S);
+  lsd_pass<0, W>(X, Y, S);
+  if constexpr (NP >= 2) lsd_pass<W, W>(Y, X, S);
+  if constexpr (NP >= 3) lsd_pass<2 * W, W>(X, Y, S);
+  if constexpr (NP >= 4) lsd_pass<3 * W, W>(Y, X, S);
 }
 
 // Dense id of every sorted item's key group, stored at rank[pos], and the
@@ -248,26 +245,32 @@ __device__ __forceinline__ u32 small_group_round(WinBuf &P, WinBuf &R, u32 G, i6
   }, R.pos, nrank, n, S);
 }
 
-template <int NP, bool XA>  // XA: items in S.a, other buffer S.b
+template <int NP, int W, bool XA>  // XA: items in S.a, other buffer S.b
 __device__ __forceinline__ void sort_round(WinSmem &S) {
   if constexpr (XA)
-    lsd_passes<NP>(S.a, S.b, S);
+    lsd_passes<NP, W>(S.a, S.b, S);
   else
-    lsd_passes<NP>(S.b, S.a, S);
+    lsd_passes<NP, W>(S.b, S.a, S);
 }
 
-__device__ __forceinline__ void sort_items(WinSmem &S, int np, bool xa) {
-  if (xa) {
-    if (np <= 1) sort_round<1, true>(S);
-    else if (np == 2) sort_round<2, true>(S);
-    else if (np == 3) sort_round<3, true>(S);
-    else sort_round<4, true>(S);
-  } else {
-    if (np <= 1) sort_round<1, false>(S);
-    else if (np == 2) sort_round<2, false>(S);
-    else if (np == 3) sort_round<3, false>(S);
-    else sort_round<4, false>(S);
-  }
+template <bool XA>
+__device__ __forceinline__ int sort_items_x(WinSmem &S, int bits) {
+  // fewest passes, 8-bit digits where that many passes suffice (8 ballots per
+  // item instead of 9): 8 | 9 | 16 | 18 | 24 | 27 | 32 bits
+  if (bits <= 8) { sort_round<1, 8, XA>(S); return 1; }
+  if (bits <= 9) { sort_round<1, 9, XA>(S); return 1; }
+  if (bits <= 16) { sort_round<2, 8, XA>(S); return 2; }
+  if (bits <= 18) { sort_round<2, 9, XA>(S); return 2; }
+  if (bits <= 24) { sort_round<3, 8, XA>(S); return 3; }
+  if (bits <= 27) { sort_round<3, 9, XA>(S); return 3; }
+  sort_round<4, 8, XA>(S);
+  return 4;
+}
+
+// Sort the items (keys of `bits` significant bits) built in S.a (xa) or
+// S.b; returns the number of passes (odd: the items end in the other buffer)
+__device__ __forceinline__ int sort_items(WinSmem &S, int bits, bool xa) {
+  return xa ? sort_items_x<true>(S, bits) : sort_items_x<false>(S, bits);
 }
 
 // Algorithmic shared-memory traffic (profiling only): every LSD pass reads
@@ -316,8 +319,7 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
       S.a.pos[q] = (unsigned short)q;
     }
     __syncthreads();
-    const int np = (kb + 1 + 7) / 8;
-    sort_items(S, np, true);
+    const int np = sort_items(S, kb + (n < kWMax ? 1 : 0), true);  // pad items need one more bit
     sorted_in_a = (np & 1) == 0;
     rank_in_b = sorted_in_a;
     G = dense_rank(sorted_in_a ? S.a : S.b, rank_ptr(), n, S);
@@ -371,8 +373,7 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
         xp[q] = (unsigned short)q;
       }
       __syncthreads();
-      const int np = (kb + 1 + 7) / 8;
-      sort_items(S, np, xa);
+      const int np = sort_items(S, kb + (n < kWMax ? 1 : 0), xa);  // pad items need one more bit
       sorted_in_a = ((np & 1) == 0) == xa;
       rank_in_b = sorted_in_a;
       G = dense_rank(sorted_in_a ? S.a : S.b, rank_ptr(), n, S);
