@@ -50,19 +50,20 @@ struct CandF {
   i64 *m_out;
   __device__ __forceinline__ bool pair(i64 k, i64 &l, i64 &a, i64 &bb, int &w) const {
     // the SA is window-major: rank k belongs to the window of position k
-    // (a sequential read, not a random one at SA[k])
+    // (a sequential read, not a random one at SA[k]); all loads are issued
+    // before any branch, and the arithmetic is 32-bit (positions < 2^31)
     w = b_wid(b, k);
-    if (k + 1 >= b_end(b, w)) return false;
-    i64 s1 = sa[k];
-    i64 s2 = sa[k + 1];
-    i64 p = lcp[k];
-    i64 lo = s1 < s2 ? s1 : s2, d = s1 < s2 ? s2 - s1 : s1 - s2;
+    const i64 e = b_end(b, w);
+    const bool ok = k + 1 < e;
+    const u32 s1 = u32(sa[k]), s2 = u32(sa[ok ? k + 1 : k]), p = u32(lcp[k]);
+    if (!ok) return false;
+    const u32 lo = s1 < s2 ? s1 : s2, d = s1 < s2 ? s2 - s1 : s1 - s2;
     if (d >= p) {
       l = p;
       a = s1;
       bb = s2;
     } else {
-      i64 L = (p + d) / 2;
+      u32 L = (p + d) >> 1;
       L -= L % d;
       l = L;
       a = lo;
