@@ -357,18 +357,20 @@ struct BucketF {
   u64 *e_tok;
   u32 *e_lo, *e_q;
   i64 *total;
+  // a bucket starts at a stream's first rank or where the first token
+  // changes, i.e. where the LCP with the previous suffix is 0 (sequential
+  // reads only: the SA is stream-major, so rank k is in the stream of
+  // position k)
   __device__ u32 load(i64 k) const {
-    const i64 p = m.sa[k];
-    const int q = m.wid[p];
+    const int q = m.wid[k];
     if (k == m.off[q]) return 1;
-    return m.tok[p] != m.tok[m.sa[k - 1]] ? 1u : 0u;
+    return m.lcp[k - 1] == 0 ? 1u : 0u;
   }
   __device__ bool store(i64 k, u32 incl, u32 excl) const {
     if (incl != excl) {
-      const i64 p = m.sa[k];
-      e_tok[excl] = m.tok[p];
+      e_tok[excl] = m.tok[m.sa[k]];
       e_lo[excl] = u32(k);
-      e_q[excl] = u32(m.wid[p]);
+      e_q[excl] = u32(m.wid[k]);
     }
     if (k == m.N - 1) *total = i64(incl);
     return false;
