@@ -835,10 +835,12 @@ constexpr int kTreeDepth = 1024;
 __global__ void __launch_bounds__(32) k_tree_sweep(const u64 *__restrict__ key, const u32 *__restrict__ val,
                                                    const u32 *__restrict__ toff, const u32 *__restrict__ gtr,
                                                    u32 *__restrict__ opar, u32 *__restrict__ ohi,
-                                                   u32 *__restrict__ odep, u32 *__restrict__ otr) {
+                                                   u32 *__restrict__ odep, u32 *__restrict__ otr,
+                                                   const u32 *__restrict__ only) {
   __shared__ u64 s_key[kTreeChunk];
   __shared__ u32 s_idx[kTreeDepth], s_hi[kTreeDepth];
   const int q = blockIdx.x, lane = threadIdx.x;
+  if (only && !only[q]) return;  // fallback run: only the streams k_tree_par flagged
   const u32 a = toff[q], b = toff[q + 1];
   for (u32 k = a + lane; k < b; k += 32) otr[k] = gtr[val[k]];
   u32 cur = kNoPar, curhi = 0, depth = 0, held = 0;  // held: stack entries below the top kept in the ring
@@ -881,6 +883,80 @@ __global__ void __launch_bounds__(32) k_tree_sweep(const u64 *__restrict__ key, 
     }
     __syncwarp();
   }
+}
+
+// The same forest, 32 intervals at a time (one warp per stream): in preorder
+// the parent of an interval is the nearest PRECEDING interval whose end is >=
+// its own (laminar family), so within a chunk it comes from 32 shuffles; if
+// it precedes the chunk it is on the chain of open intervals left by the
+// previous chunk, kept as a depth-indexed stack whose ends are non-increasing
+// (binary search).  Depths inside the chunk follow by pointer jumping, and
+// the stack is updated by "the last interval of the chunk at each depth" (the
+// ancestor of the chunk's last interval at depth d is the last interval of
+// depth d before it in preorder).  A stream nested deeper than the on-chip
+// stack is flagged in `big` and redone by k_tree_sweep.
+constexpr u32 kParDepth = 4096;
+
+__global__ void __launch_bounds__(32) k_tree_par(const u64 *__restrict__ key, const u32 *__restrict__ val,
+                                                 const u32 *__restrict__ toff, const u32 *__restrict__ gtr,
+                                                 u32 *__restrict__ opar, u32 *__restrict__ ohi,
+                                                 u32 *__restrict__ odep, u32 *__restrict__ otr,
+                                                 u32 *__restrict__ big) {
+  __shared__ u32 s_id[kParDepth + 1];
+  __shared__ unsigned short s_hi[kParDepth + 1];
+  const int q = blockIdx.x, lane = threadIdx.x;
+  const u32 a = toff[q], b = toff[q + 1];
+  u32 ssize = 0;  // the stack holds depths 1 .. ssize
+  bool deep_stream = false;
+  for (u32 c0 = a; c0 < b; c0 += 32) {
+    const u32 k = c0 + lane;
+    const bool v = k < b;
+    u32 hi = 0;
+    if (v) hi = 32767u - (u32(key[k]) & 32767u);
+    int P = -1;  // nearest preceding lane of the chunk that contains this interval
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const u32 hj = __shfl_sync(0xffffffffu, hi, j);
+      if (j < lane && hj >= hi) P = j;
+    }
+    u32 pid = kNoPar, acc = 1;
+    int ptr = P;
+    if (P < 0) {
+      u32 l = 0, h = min(ssize, kParDepth);  // deepest stack depth whose end is >= hi
+      while (l < h) {
+        const u32 mid = (l + h + 1) >> 1;
+        if (s_hi[mid] >= hi) l = mid; else h = mid - 1;
+      }
+      pid = l ? s_id[l] : kNoPar;
+      acc = l + 1;
+    }
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {  // depth = depth(parent) + 1 along in-chunk links
+      const int src = ptr >= 0 ? ptr : lane;
+      const u32 pacc = __shfl_sync(0xffffffffu, acc, src);
+      const int pptr = __shfl_sync(0xffffffffu, ptr, src);
+      if (ptr >= 0) {
+        acc += pacc;
+        ptr = pptr;
+      }
+    }
+    const u32 depth = acc;
+    if (v) {
+      opar[k] = P >= 0 ? c0 + u32(P) - a : pid;
+      ohi[k] = hi;
+      odep[k] = depth;
+      otr[k] = gtr[val[k]];
+      if (depth > kParDepth) deep_stream = true;
+    }
+    const u32 peers = __match_any_sync(0xffffffffu, v ? depth : 0xffffffffu);
+    if (v && depth <= kParDepth && lane == 31 - __clz(peers)) {
+      s_id[depth] = k - a;
+      s_hi[depth] = (unsigned short)hi;
+    }
+    ssize = __shfl_sync(0xffffffffu, depth, int(min(31u, b - c0 - 1)));
+    __syncwarp();
+  }
+  if (__any_sync(0xffffffffu, deep_stream) && lane == 0) big[q] = 1;
 }
 
 __global__ void __launch_bounds__(kEmitThreads, 1) k_stream_emit(StreamMatch m, const u64 *__restrict__ tkey,
@@ -1681,6 +1757,7 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             full.take<u32>(P);
             full.take<u32>(P);
             full.take<u32>(P);
+            full.take<u32>(size_t(nstreams));
             if (full.off > c.aux.cap) {
               c.aux.reserve(full.off, s);
               Carver cb(c.aux.base);
@@ -1704,6 +1781,7 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             u32 *tof = cz.take<u32>(size_t(nstreams) + 1);
             u32 *gpar = cz.take<u32>(P), *ghi = cz.take<u32>(P), *gtr = cz.take<u32>(P), *gdep = cz.take<u32>(P);
             u32 *otr = cz.take<u32>(P);
+            u32 *tbig = cz.take<u32>(size_t(nstreams));
             k_pair_list<<<grid_for(T * 32, T256), T256, 0, s>>>(pbase, ea, ecnt, sord, e_q, T, pair_e, ptr, qk, qv);
             APO_CHECK_LAUNCH();
             bool aq = radix_sort_u64_u32(c, qk, qv, qk_alt, qv_alt, P, 0, bits_for(u64(nstreams - 1)), s);
@@ -1742,8 +1820,16 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
               const u32 *stv = at ? tv_alt : tv;
               k_tree_offsets<<<grid_for(i64(nstreams) + 1, T256), T256, 0, s>>>(stk, P, nstreams, tof);
               APO_CHECK_LAUNCH();
-              k_tree_sweep<<<nstreams, 32, 0, s>>>(stk, stv, tof, gtr, gpar, ghi, gdep, otr);
+              // APO_TREE_SEQ=1 (tests) forces the sequential sweep on every stream
+              static const bool tree_seq = std::getenv("APO_TREE_SEQ") != nullptr;
+              APO_CUDA(cudaMemsetAsync(tbig, tree_seq ? 0xff : 0, sizeof(u32) * size_t(nstreams), s));
+              if (!tree_seq) {
+                k_tree_par<<<nstreams, 32, 0, s>>>(stk, stv, tof, gtr, gpar, ghi, gdep, otr, tbig);
+                APO_CHECK_LAUNCH();
+              }
+              k_tree_sweep<<<nstreams, 32, 0, s>>>(stk, stv, tof, gtr, gpar, ghi, gdep, otr, tbig);
               APO_CHECK_LAUNCH();
+              c.launches++;
               const size_t esmem = sizeof(u32) * (kSMMax + 3 * kEmitPairs) + sizeof(unsigned short) * kSMMax;
               static bool eattr = false;
               if (!eattr) {

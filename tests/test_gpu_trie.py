@@ -233,3 +233,19 @@ def test_match_deep_nesting():
     hits = ctx.match(trie, dev(sflat), soff).cpu().numpy()
     want, cnt = oracle.match_brute(sflat, soff, tt.cpu().numpy(), to)
     assert cnt == len(hits) and np.array_equal(hits, want)
+
+
+def test_match_tree_sweep_fallback():
+    """The sequential interval-forest sweep (the fallback for streams nested
+    deeper than the parallel builder's on-chip stack), forced for every
+    stream in a subprocess, gives the same hits as the brute-force oracle."""
+    import subprocess, sys, os
+    code = ("import importlib.util, sys; sys.path.insert(0, '.'); "
+            "spec = importlib.util.spec_from_file_location('tgt', 'tests/test_gpu_trie.py'); "
+            "t = importlib.util.module_from_spec(spec); spec.loader.exec_module(t); "
+            "from paper_2406_18111_b200 import Context; c = Context(0); "
+            "t.test_match_deep_nesting(); t.test_match_large_end_bins(c); t.test_match_batch_vs_oracle(c)")
+    env = dict(os.environ, APO_TREE_SEQ="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
