@@ -49,6 +49,7 @@ struct SAWork {
   i32 *sa;                // N (global positions, window-major suffix order)
   i32 *lcp;               // N (pair k = (k, k+1); 0 at the end of each window)
   int R;                  // final level index (ranks all distinct)
+  int unit = 1;           // level r ranks the (unit * 2^r)-token prefixes (token packing, K3)
 };
 
 void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp);

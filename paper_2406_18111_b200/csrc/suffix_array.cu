@@ -88,6 +88,20 @@ __global__ void k_rank_from_ids(const u32 *__restrict__ ids, i64 n, const u32 *_
   if (i < n) rank[i] = i32(start[ids[i]]);
 }
 
+// Token packing: the first sort orders the suffixes by their
+// first q tokens at once -- q dense ids of bt bits each (id + 1; 0 past the
+// end of the single window) in one 64-bit key -- so doubling starts at
+// h = q instead of 1 and saves log2(q) rounds.
+__global__ void k_pack_keys(const u32 *__restrict__ ids, i64 n, int q, int bt, u64 *__restrict__ keys,
+                            u32 *__restrict__ vals) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  u64 k = 0;
+  for (int t = 0; t < q; ++t) k = (k << bt) | (i + t < n ? u64(ids[i + t]) + 1u : 0ull);
+  keys[i] = k;
+  vals[i] = u32(i);
+}
+
 __global__ void k_double_keys(const i32 *__restrict__ rank, Batch b, i64 h, int lob, u64 *__restrict__ keys,
                               u32 *__restrict__ vals) {
   i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -132,25 +146,27 @@ struct Levels {
 };
 
 // lcp(i, j) (i < end_i, j < end_j) by galloping over rank levels R-1..0:
-// equal level-r ranks <=> equal 2^r-token prefixes (padded with the end
-// marker of the suffix's own window).
-__device__ __forceinline__ i64 gallop_lcp(const Levels &L, int R, i64 i, i64 j, i64 end_i, i64 end_j,
-                                          i64 from) {
-  // from: a known lower bound of the lcp; lcp - from < 2^R, so descending
-  // powers of two from 2^(R-1) reach it exactly
+// equal level-r ranks <=> equal (unit * 2^r)-token prefixes (padded with the
+// end marker of the suffix's own window); the last < unit tokens (token
+// packing) are compared directly.
+__device__ __forceinline__ i64 gallop_lcp(const Levels &L, int R, int unit, const u64 *__restrict__ tok, i64 i,
+                                          i64 j, i64 end_i, i64 end_j, i64 from) {
+  // from: a known lower bound of the lcp; lcp - from < unit * 2^R, so
+  // descending multiples unit * 2^r reach it to within unit - 1
   i64 l = from;
   for (int r = R - 1; r >= 0; --r) {
     if (i + l >= end_i || j + l >= end_j) break;
     const i32 *lv = L.p[r];
-    if (lv[i + l] == lv[j + l]) l += (i64(1) << r);
+    if (lv[i + l] == lv[j + l]) l += i64(unit) << r;
   }
+  for (int t = 1; t < unit && i + l < end_i && j + l < end_j && tok[i + l] == tok[j + l]; ++t) ++l;
   return l;
 }
 
 constexpr int kPlcpChunk = 32;
 constexpr int kKasaiSteps = 16;
 
-__global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi, Levels L, int R,
+__global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi, Levels L, int R, int unit,
                        const i32 *__restrict__ rw, Batch b, i32 *__restrict__ plcp) {
   i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   i64 i0 = t * kPlcpChunk;
@@ -176,7 +192,7 @@ __global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi,
     }
     const i64 end_j = b.gen ? b_end(b, b_wid(b, j)) : end;
     if (h < 0) {
-      h = gallop_lcp(L, Rcur, i, j, end, end_j, 0);
+      h = gallop_lcp(L, Rcur, unit, tok, i, j, end, end_j, 0);
     } else {
       // Kasai: PLCP[i] >= PLCP[i-1] - 1.  Extend by direct comparison for a
       // few tokens; a longer extension (after a sharp drop) is finished by
@@ -187,7 +203,7 @@ __global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi,
       while (i + h < end && j + h < end_j && tok[i + h] == tok[j + h]) {
         ++h;
         if (++steps == kKasaiSteps) {
-          h = gallop_lcp(L, Rcur, i, j, end, end_j, h);
+          h = gallop_lcp(L, Rcur, unit, tok, i, j, end, end_j, h);
           break;
         }
       }
@@ -245,11 +261,16 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   // its window-local ranks itself; otherwise (or if the vocabulary is too
   // large) the 64-bit radix sort of (token, position).
   w.ids_valid = false;
+  w.unit = 1;
+  i64 packK = -1;
   if (b.gen || b.W == 1 || w.rw != nullptr) {
     const i64 K = dense_token_ids(c, tok, N, w.ids, w.ht_cap, w.ht_scratch, s);
     if (K >= 0) {
       w.ids_valid = true;
-      if (w.rw == nullptr) {
+      packK = K;
+      const int bt0 = bits_for(u64(K));
+      const bool will_pack = !b.gen && b.W == 1 && w.rw == nullptr && b.sort_depth == 0 && 64 / bt0 >= 2;
+      if (w.rw == nullptr && !will_pack) {
         // group start of a token = number of positions holding smaller tokens
         u32 *cnt = w.vals;  // K <= N counters, then exclusive starts in place
         APO_CUDA(cudaMemsetAsync(cnt, 0, sizeof(u32) * K, s));
@@ -305,7 +326,28 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   u32 *notdone = reinterpret_cast<u32 *>(c.d_misc);
   const u32 *final_sa = nullptr;  // set by the first round (there is always one)
   int r = 0;
-  for (i64 h = 1;; h <<= 1) {
+  i64 h0 = 1;
+  bool done = false;
+  // token packing for a single window with dense ids (C2, C3, C5): level 0
+  // = ranks of the first q tokens
+  const int bt = packK >= 0 ? bits_for(u64(packK)) : 64;
+  const int q = 64 / bt;
+  if (w.ids_valid && !b.gen && b.W == 1 && w.rw == nullptr && q >= 2 && b.sort_depth == 0) {
+    APO_CUDA(cudaMemsetAsync(notdone, 0, sizeof(u32), s));
+    k_pack_keys<<<G, T, 0, s>>>(w.ids, N, q, bt, w.keys, w.vals);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+    bool a = radix_sort_u64_u32(c, w.keys, w.vals, w.keys_alt, w.vals_alt, N, 0, q * bt, s);
+    const u64 *key = a ? w.keys_alt : w.keys;
+    const u32 *sa = a ? w.vals_alt : w.vals;
+    DoubleRankF f{key, sa, w.levels[0], notdone};
+    launch_scan<true>(c, N, f, s);
+    final_sa = sa;
+    w.unit = q;
+    h0 = q;
+    done = c.read_u32(notdone, s) == 0;
+  }
+  for (i64 h = h0; !done; h <<= 1) {
     if (r + 1 >= w.max_levels) throw Error{APO_ERR_INVALID, "prefix doubling exceeded its level budget"};
     APO_CUDA(cudaMemsetAsync(notdone, 0, sizeof(u32), s));
     k_double_keys<<<G, T, 0, s>>>(w.levels[r], b, h, lob, w.keys, w.vals);
@@ -334,7 +376,7 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   Levels L{};
   for (int q = 0; q < w.max_levels && q < 40; ++q) L.p[q] = w.levels[q];
   i64 chunks = (N + kPlcpChunk - 1) / kPlcpChunk;
-  k_plcp<<<grid_for(chunks, 128), 128, 0, s>>>(tok, w.phi, L, w.R, w.rw, b, w.plcp);
+  k_plcp<<<grid_for(chunks, 128), 128, 0, s>>>(tok, w.phi, L, w.R, w.unit, w.rw, b, w.plcp);
   APO_CHECK_LAUNCH();
   k_lcp_gather<<<G, T, 0, s>>>(sa, w.plcp, b, w.lcp);
   APO_CHECK_LAUNCH();
