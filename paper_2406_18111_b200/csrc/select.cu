@@ -260,6 +260,139 @@ __global__ void k_seg_unpack(const u64 *__restrict__ k2, i64 m, i64 G, int bL, c
   state[p] = 0;
 }
 
+// K6 sort-1 for batches of small windows: the candidates come out of K5 in
+// pair order, i.e. already grouped by window, so only the length field needs
+// sorting, and only inside each window.  One 1,024-thread CTA per window runs
+// a stable two-pass LSD counting sort on the (maxl - length) field (7 + 7
+// bits for windows <= 16,384 ops) over its own segment: a histogram of both
+// digits, then per pass the segment's tiles of 4,096 in order, each ranked
+// with the ballot multisplit and scattered behind the previous tiles (no
+// global look-back, no window bits in the key).
+constexpr int kSegThreads = 1024;
+constexpr int kSegItems = 4;
+constexpr int kSegTile = kSegThreads * kSegItems;
+
+template <int BITS>
+__device__ __forceinline__ u32 peers_of(u32 d) {
+  u32 peers = 0xffffffffu;
+#pragma unroll
+  for (int b = 0; b < BITS; ++b) {
+    const bool bit = (d >> b) & 1u;
+    const u32 m = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? m : ~m;
+  }
+  return peers;
+}
+
+template <int SHIFT, int BITS>
+__device__ __forceinline__ void seg_pass(const u32 *__restrict__ kin, const u64 *__restrict__ vin,
+                                         u32 *__restrict__ kout, u64 *__restrict__ vout, i64 c0, i64 c1,
+                                         u32 lmask, u32 *s_base, unsigned short (*s_wh)[128], u32 *s_tot) {
+  constexpr u32 RADIX = 1u << BITS, mask = RADIX - 1u;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  u32 lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  for (i64 t0 = c0; t0 < c1; t0 += kSegTile) {
+    for (int i = tid; i < 32 * 128; i += kSegThreads) (&s_wh[0][0])[i] = 0;
+    __syncthreads();
+    u32 d[kSegItems], r[kSegItems];
+    bool v[kSegItems];
+#pragma unroll
+    for (int j = 0; j < kSegItems; ++j) {  // warp w owns tile items [128 w, 128 w + 128) in (j, lane) order
+      const i64 i = t0 + warp * (32 * kSegItems) + j * 32 + lane;
+      v[j] = i < c1;
+      d[j] = v[j] ? ((kin[i] & lmask) >> SHIFT) & mask : mask;
+      const u32 peers = peers_of<BITS>(d[j]) & __ballot_sync(0xffffffffu, v[j]);
+      const u32 old = s_wh[warp][d[j]];
+      __syncwarp();
+      if (v[j] && lane == __ffs(peers) - 1) s_wh[warp][d[j]] = (unsigned short)(old + __popc(peers));
+      __syncwarp();
+      r[j] = old + __popc(peers & lt);
+    }
+    __syncthreads();
+    if (tid < int(RADIX)) {  // per digit: exclusive prefix over warps, tile total
+      u32 tot = 0;
+      for (int w = 0; w < 32; ++w) {
+        const u32 c = s_wh[w][tid];
+        s_wh[w][tid] = (unsigned short)tot;
+        tot += c;
+      }
+      s_tot[tid] = tot;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSegItems; ++j) {
+      if (!v[j]) continue;
+      const i64 i = t0 + warp * (32 * kSegItems) + j * 32 + lane;
+      const i64 p = c0 + s_base[d[j]] + s_wh[warp][d[j]] + r[j];
+      kout[p] = kin[i];
+      vout[p] = vin[i];
+    }
+    __syncthreads();
+    if (tid < int(RADIX)) s_base[tid] += s_tot[tid];  // the next tile goes behind this one
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kSegThreads) k_seg_sort1(Batch b, u32 *__restrict__ k1, u64 *__restrict__ v1,
+                                                           u32 *__restrict__ k1a, u64 *__restrict__ v1a, i64 m,
+                                                           int bl, u32 lmask) {
+  __shared__ u32 s_h0[128], s_h1[128], s_tot[128];
+  __shared__ unsigned short s_wh[32][128];
+  const int w = blockIdx.x, tid = threadIdx.x;
+  // the window's candidate segment [c0, c1) (candidates are window-major)
+  i64 c0, c1;
+  {
+    i64 lo = 0, hi = m;
+    while (lo < hi) {
+      const i64 mid = (lo + hi) >> 1;
+      if (i64(k1[mid] >> bl) < w) lo = mid + 1; else hi = mid;
+    }
+    c0 = lo;
+    hi = m;
+    while (lo < hi) {
+      const i64 mid = (lo + hi) >> 1;
+      if (i64(k1[mid] >> bl) <= w) lo = mid + 1; else hi = mid;
+    }
+    c1 = lo;
+  }
+  if (c0 == c1) return;
+  if (tid < 128) {
+    s_h0[tid] = 0;
+    s_h1[tid] = 0;
+  }
+  __syncthreads();
+  for (i64 i = c0 + tid; i < c1; i += kSegThreads) {
+    const u32 f = k1[i] & lmask;
+    atomicAdd(&s_h0[f & 127u], 1u);
+    atomicAdd(&s_h1[(f >> 7) & 127u], 1u);
+  }
+  __syncthreads();
+  if (tid < 32) {  // exclusive digit starts (one warp, 4 + 4 digits per lane)
+    u32 a[4], t = 0;
+    for (int j = 0; j < 4; ++j) { a[j] = s_h0[tid * 4 + j]; t += a[j]; }
+    u32 incl = t;
+    for (int d = 1; d < 32; d <<= 1) {
+      const u32 o = __shfl_up_sync(0xffffffffu, incl, d);
+      if (tid >= d) incl += o;
+    }
+    u32 run = incl - t;
+    for (int j = 0; j < 4; ++j) { s_h0[tid * 4 + j] = run; run += a[j]; }
+    u32 b2[4], t2 = 0;
+    for (int j = 0; j < 4; ++j) { b2[j] = s_h1[tid * 4 + j]; t2 += b2[j]; }
+    incl = t2;
+    for (int d = 1; d < 32; d <<= 1) {
+      const u32 o = __shfl_up_sync(0xffffffffu, incl, d);
+      if (tid >= d) incl += o;
+    }
+    run = incl - t2;
+    for (int j = 0; j < 4; ++j) { s_h1[tid * 4 + j] = run; run += b2[j]; }
+  }
+  __syncthreads();
+  seg_pass<0, 7>(k1, v1, k1a, v1a, c0, c1, lmask, s_h0, s_wh, s_tot);
+  seg_pass<7, 7>(k1a, v1a, k1, v1, c0, c1, lmask, s_h1, s_wh, s_tot);
+}
+
 struct Tab {
   u32 *lv[32];
 };
@@ -556,9 +689,17 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
   if (m == 0) return;
 
   // ---- K6: sort by (window, length desc), stable in pair order ----
-  bool a = radix_sort_u32_u64(c, w.k1, w.v1, w.k1_alt, w.v1_alt, m, 0, bl + bw, s);
-  const u32 *k1 = a ? w.k1_alt : w.k1;
-  const u64 *v1 = a ? w.v1_alt : w.v1;
+  const u32 *k1 = w.k1;
+  const u64 *v1 = w.v1;
+  if (b.W > 1 && bl <= 14) {  // windows <= 16,384 ops: per-window two-pass sort (7 + 7 bits)
+    k_seg_sort1<<<b.W, kSegThreads, 0, s>>>(b, w.k1, w.v1, w.k1_alt, w.v1_alt, m, bl, (1u << bl) - 1u);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+  } else {
+    bool a = radix_sort_u32_u64(c, w.k1, w.v1, w.k1_alt, w.v1_alt, m, 0, bl + bw, s);
+    k1 = a ? w.k1_alt : w.k1;
+    v1 = a ? w.v1_alt : w.v1;
+  }
   Rmq rmq{};
   {
     const i64 nb = (N + 31) / 32;
