@@ -287,7 +287,8 @@ __device__ __forceinline__ u32 peers_of(u32 d) {
 template <int SHIFT, int BITS>
 __device__ __forceinline__ void seg_pass(const u32 *__restrict__ kin, const u64 *__restrict__ vin,
                                          u32 *__restrict__ kout, u64 *__restrict__ vout, i64 c0, i64 c1,
-                                         u32 lmask, u32 *s_base, unsigned short (*s_wh)[128], u32 *s_tot) {
+                                         u32 lmask, u32 *s_base, unsigned short (*s_wh)[128], u32 *s_tot,
+                                         u32 *s_tdig, u32 *s_sk, u64 *s_sv) {
   constexpr u32 RADIX = 1u << BITS, mask = RADIX - 1u;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   u32 lt;
@@ -320,13 +321,46 @@ __device__ __forceinline__ void seg_pass(const u32 *__restrict__ kin, const u64 
       s_tot[tid] = tot;
     }
     __syncthreads();
+    if (warp == 0) {  // exclusive digit starts inside the tile (RADIX <= 128: 4 per lane)
+      u32 a4[4], t = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int dd = lane * 4 + q;
+        a4[q] = dd < int(RADIX) ? s_tot[dd] : 0u;
+        t += a4[q];
+      }
+      u32 incl = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+      }
+      u32 run = incl - t;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int dd = lane * 4 + q;
+        if (dd < int(RADIX)) s_tdig[dd] = run;
+        run += a4[q];
+      }
+    }
+    __syncthreads();
+    // stage the tile in digit order, then write each digit's run contiguously
 #pragma unroll
     for (int j = 0; j < kSegItems; ++j) {
       if (!v[j]) continue;
       const i64 i = t0 + warp * (32 * kSegItems) + j * 32 + lane;
-      const i64 p = c0 + s_base[d[j]] + s_wh[warp][d[j]] + r[j];
-      kout[p] = kin[i];
-      vout[p] = vin[i];
+      const u32 tp = s_tdig[d[j]] + s_wh[warp][d[j]] + r[j];
+      s_sk[tp] = kin[i];
+      s_sv[tp] = vin[i];
+    }
+    __syncthreads();
+    const int tn = int(min(i64(kSegTile), c1 - t0));
+    for (int i = tid; i < tn; i += kSegThreads) {
+      const u32 kk = s_sk[i];
+      const u32 dd = ((kk & lmask) >> SHIFT) & mask;
+      const i64 p = c0 + s_base[dd] + (u32(i) - s_tdig[dd]);
+      kout[p] = kk;
+      vout[p] = s_sv[i];
     }
     __syncthreads();
     if (tid < int(RADIX)) s_base[tid] += s_tot[tid];  // the next tile goes behind this one
@@ -337,8 +371,11 @@ __device__ __forceinline__ void seg_pass(const u32 *__restrict__ kin, const u64 
 __global__ void __launch_bounds__(kSegThreads) k_seg_sort1(Batch b, u32 *__restrict__ k1, u64 *__restrict__ v1,
                                                            u32 *__restrict__ k1a, u64 *__restrict__ v1a, i64 m,
                                                            int bl, u32 lmask) {
-  __shared__ u32 s_h0[128], s_h1[128], s_tot[128];
+  __shared__ u32 s_h0[128], s_h1[128], s_tot[128], s_tdig[128];
   __shared__ unsigned short s_wh[32][128];
+  extern __shared__ __align__(16) unsigned char seg_smem[];
+  u64 *s_sv = reinterpret_cast<u64 *>(seg_smem);  // [kSegTile] staged values
+  u32 *s_sk = reinterpret_cast<u32 *>(s_sv + kSegTile);  // [kSegTile] staged keys
   const int w = blockIdx.x, tid = threadIdx.x;
   // the window's candidate segment [c0, c1) (candidates are window-major)
   i64 c0, c1;
@@ -389,8 +426,8 @@ __global__ void __launch_bounds__(kSegThreads) k_seg_sort1(Batch b, u32 *__restr
     for (int j = 0; j < 4; ++j) { s_h1[tid * 4 + j] = run; run += b2[j]; }
   }
   __syncthreads();
-  seg_pass<0, 7>(k1, v1, k1a, v1a, c0, c1, lmask, s_h0, s_wh, s_tot);
-  seg_pass<7, 7>(k1a, v1a, k1, v1, c0, c1, lmask, s_h1, s_wh, s_tot);
+  seg_pass<0, 7>(k1, v1, k1a, v1a, c0, c1, lmask, s_h0, s_wh, s_tot, s_tdig, s_sk, s_sv);
+  seg_pass<7, 7>(k1a, v1a, k1, v1, c0, c1, lmask, s_h1, s_wh, s_tot, s_tdig, s_sk, s_sv);
 }
 
 struct Tab {
@@ -692,7 +729,13 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
   const u32 *k1 = w.k1;
   const u64 *v1 = w.v1;
   if (b.W > 1 && bl <= 14) {  // windows <= 16,384 ops: per-window two-pass sort (7 + 7 bits)
-    k_seg_sort1<<<b.W, kSegThreads, 0, s>>>(b, w.k1, w.v1, w.k1_alt, w.v1_alt, m, bl, (1u << bl) - 1u);
+    const size_t ssm = size_t(kSegTile) * (sizeof(u64) + sizeof(u32));
+    static bool sattr = false;
+    if (!sattr) {
+      APO_CUDA(cudaFuncSetAttribute(k_seg_sort1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ssm)));
+      sattr = true;
+    }
+    k_seg_sort1<<<b.W, kSegThreads, ssm, s>>>(b, w.k1, w.v1, w.k1_alt, w.v1_alt, m, bl, (1u << bl) - 1u);
     APO_CHECK_LAUNCH();
     c.launches++;
   } else {
