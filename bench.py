@@ -67,6 +67,7 @@ class ClockSampler:
         self.index = index
         self.lines: list[str] = []
         self.p = None
+        self.post = False  # True: the only sample was taken right after the timed region
 
     def __enter__(self):
         try:
@@ -90,6 +91,14 @@ class ClockSampler:
                 self.p.wait(timeout=5)
             except Exception:
                 self.p.kill()
+        if not self.lines:  # a timed region shorter than nvidia-smi's first sample: query once right after it
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+                self.lines = [ln.strip() for ln in out.stdout.splitlines() if ln.strip()]
+                self.post = True
+            except Exception:
+                pass
 
     def summary(self):
         sm, mx, reasons = [], 0, set()
@@ -108,7 +117,10 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if self.post:
+            out["note"] = "timed region shorter than the 200 ms sampling period: sampled right after it"
+        return out
 
 
 def peak_hbm():
