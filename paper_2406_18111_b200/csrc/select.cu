@@ -181,7 +181,6 @@ __global__ void k_head_flags(const u32 *__restrict__ k1, const u64 *__restrict__
 struct HeadF {
   const u32 *k1;
   const u64 *v1;
-  Rmq rmq;
   i64 maxl;
   u32 lmask;
   int bL;
@@ -765,7 +764,7 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
     k_head_flags<<<grid_for(m, T), T, 0, s>>>(k1, v1, rmq, maxl, (1u << bl) - 1u, m, w.state);
     APO_CHECK_LAUNCH();
     c.launches++;
-    HeadF f{k1, v1, rmq, maxl, (1u << bl) - 1u, bL, m, w.k2, w.glen, G_dev, b.off, b.W > 1 ? b.wid : nullptr,
+    HeadF f{k1, v1, maxl, (1u << bl) - 1u, bL, m, w.k2, w.glen, G_dev, b.off, b.W > 1 ? b.wid : nullptr,
             bl, w.gbase, w.gpos, w.state};
     launch_scan<false>(c, m, f, s);
   }
