@@ -421,7 +421,9 @@ def main():
                     "frac": sach / speak,
                     "traffic": tr.get("k_window_sa_dram_bytes_per_launch") if tr else None,
                     "traffic_source": tr.get("source") if tr else None,
-                    "launches": ws_n, "bytes_per_launch": ws_bytes / ws_n, "share_of_step": ws_ms / ms}
+                    "launches": ws_n, "bytes_per_launch": ws_bytes / ws_n, "share_of_step": ws_ms / ms,
+                    "note": "the kernel's limiter is instruction issue (ballot multisplit): ncu shows ~2.5 IPC "
+                            "and ~63 % issue slots busy (profiles/r01_ncu_full_summary.txt)"}
     roofline["shares_of_step"] = {"k_window_sa": ws_ms / ms if ms else None,
                                   "k_onesweep": rp_ms / ms if ms else None,
                                   "k_stream_match": mt_ms / ms if ms else None,
