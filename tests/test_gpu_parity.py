@@ -259,3 +259,31 @@ def test_config_c5_full(ctx):
             assert cov[x:x + ln].max() == 0
             cov[x:x + ln] = 1
         assert np.array_equal(S[o[0]:o[0] + min(ln, 4096)], S[o[-1]:o[-1] + min(ln, 4096)])
+
+
+@pytest.mark.parametrize("B,C", [(16384, 256), (65536, 1024)])
+def test_ruler_multiscale_batch(ctx, B, C):
+    """SURVEY §8(f) NEXT 1, the paper's own workload shape: the
+    slices the ruler schedule emits while a stream is ingested (sizes
+    C * 2^j, capped at B) form one mixed-size batch for FindRepeats; every
+    window of the batch equals the oracle on that slice.  B = 16,384 keeps
+    every slice on the per-window on-chip path, B = 65,536 mixes in the
+    global path."""
+    S = gen.c3()[:4 * B]
+    h = ctx.history(B, C)
+    slices = []
+    for pos in range(0, len(S), 3000):
+        slices += h.ingest(dev(S[pos:pos + 3000]))
+    assert slices == oracle.ruler_slices(0, len(S), C, B)
+    wins = [S[b:e] for b, e in slices[-40:]]
+    toks = np.concatenate(wins)
+    off = np.cumsum([0] + [len(x) for x in wins]).astype(np.int64)
+    assert len(set(len(x) for x in wins)) > 2  # mixed sizes
+    rep, roff, occ = ctx.find_repeats_batched(dev(toks), off, 25)
+    rep, roff, occ = rep.cpu().numpy(), roff.cpu().numpy(), occ.cpu().numpy()
+    for w, x in enumerate(wins):
+        want = oracle.find_repeats(x, 25, tier=1)
+        got = rep[roff[w]:roff[w + 1]]
+        assert np.array_equal(got[:, :3], want["repeats"][:, :3]), w
+        for row, wrow in zip(got, want["repeats"]):
+            assert np.array_equal(occ[row[3]:row[3] + row[2]], want["occ"][wrow[3]:wrow[3] + wrow[2]])
