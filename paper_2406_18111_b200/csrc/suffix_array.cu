@@ -163,7 +163,7 @@ __device__ __forceinline__ i64 gallop_lcp(const Levels &L, int R, int unit, cons
   return l;
 }
 
-constexpr int kPlcpChunk = 32;
+constexpr int kPlcpChunk = 8;  // positions per thread (more independent Kasai chains in flight)
 constexpr int kKasaiSteps = 16;
 
 __global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi, Levels L, int R, int unit,
