@@ -245,8 +245,8 @@ inline int grid_for(i64 n, int per_block, int cap = 1 << 30) {
 // Op: sum (IS_MAX=false) or max (IS_MAX=true).  One launch, one pass over
 // the data, tiles claimed in order through an atomic counter.
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;
-constexpr int kScanTile = kScanThreads * kScanItems;  // 4096
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;  // 2048 (shorter dependent chains per thread)
 
 template <bool IS_MAX>
 __device__ __forceinline__ u32 scan_op(u32 a, u32 b) {
