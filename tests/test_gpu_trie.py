@@ -249,3 +249,26 @@ def test_match_tree_sweep_fallback():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+def test_match_many_intervals_one_stream(ctx):
+    """More matched traces in one stream than the emitter keeps on chip
+    (> 8,192 intervals): the global-table path of k_stream_emit, against the
+    brute-force oracle."""
+    rng = gen.Rng(77)
+    s = np.array([int(x) for x in gen.random_string(4242, 12000, 8)], dtype=np.uint64)
+    seen = set()
+    while len(seen) < 9000:
+        L = 5 + rng.below(6)
+        p = rng.below(len(s) - L)
+        seen.add(tuple(int(x) for x in s[p:p + L]))
+    traces = sorted(seen, key=lambda t: (-len(t), t))
+    flat = np.array([x for t in traces for x in t], dtype=np.uint64)
+    toff = np.cumsum([0] + [len(t) for t in traces]).astype(np.int64)
+    trie = ctx.trie_build_traces(dev(flat), toff)
+    tt, to = trie.traces()
+    sflat = np.concatenate([s, s[:3000]])
+    soff = np.array([0, len(s), len(s) + 3000], dtype=np.int64)
+    hits = ctx.match(trie, dev(sflat), soff).cpu().numpy()
+    want, cnt = oracle.match_brute(sflat, soff, tt.cpu().numpy(), to)
+    assert cnt == len(hits) and np.array_equal(hits, want)
