@@ -66,9 +66,13 @@ __device__ __forceinline__ void lsd_pass(const WinBuf &src, WinBuf &dst, WinSmem
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int RADIX = 1 << BITS;
   constexpr u32 mask = RADIX - 1u;
-  for (int i = tid; i < kWWarps * 512; i += kWT) (&S.hist[0][0])[i] = 0;
-  __syncthreads();
   unsigned short *wh = S.hist[warp];
+  {  // each warp clears its own histogram row (the previous pass ended with a barrier)
+    u32 *row = reinterpret_cast<u32 *>(wh);
+#pragma unroll
+    for (int i = lane; i < RADIX / 2; i += 32) row[i] = 0;
+    __syncwarp();
+  }
   const u32 lt = lanemask_lt_w();
   const int base = warp * (32 * kWItems) + lane;
   u32 rk[kWItems / 2];  // two u16 in-warp ranks per register
