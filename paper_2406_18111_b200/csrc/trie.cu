@@ -966,7 +966,7 @@ __global__ void __launch_bounds__(kEmitThreads, 1) k_stream_emit(StreamMatch m, 
                                                                  const u32 *__restrict__ qorder,
                                                                  const u32 *__restrict__ opar,
                                                                  const u32 *__restrict__ otr,
-                                                                 const u32 *__restrict__ odep) {
+                                                                 const u32 *__restrict__ odep, bool pair32) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ u32 s_warp[33];
   const int q = int(qorder[blockIdx.x]);
@@ -1032,16 +1032,45 @@ __global__ void __launch_bounds__(kEmitThreads, 1) k_stream_emit(StreamMatch m, 
   u32 run;
   cta_excl_scan(tsum, s_warp, &run);
   i64 pos = i64(qbase[q]) + run;
+  // a thread's records are consecutive: an even-indexed record waits for its
+  // successor and the pair goes out as one 32-B store (half the store
+  // transactions); odd starts and the last record use 16-B stores
+  int4 held = make_int4(0, 0, 0, 0);
+  bool have = false;
+  i64 hpos = 0;
+  auto put = [&](i64 p, int4 r) {
+    if (have) {  // the held record (even index hpos) pairs with its successor
+      if (p == hpos + 1 && p < cap) {
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(
+                         reinterpret_cast<int4 *>(out) + hpos),
+                     "r"(held.x), "r"(held.y), "r"(held.z), "r"(held.w), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w)
+                     : "memory");
+        have = false;
+        return;
+      }
+      reinterpret_cast<int4 *>(out)[hpos] = held;
+      have = false;
+    }
+    if (p >= cap) return;
+    if (pair32 && (p & 1) == 0) {
+      held = r;
+      hpos = p;
+      have = true;
+    } else {
+      reinterpret_cast<int4 *>(out)[p] = r;  // one 16-B store
+    }
+  };
 #pragma unroll 1
   for (int j = 0; j < kPer; ++j) {
     if (!ce[j]) continue;
     const i64 e = b0 + j;
     u32 z = deep[RISA[n - 1 - e]] - 1u;
     for (u32 k = 0; k < ce[j]; ++k, ++pos) {
-      if (pos < cap) reinterpret_cast<int4 *>(out)[pos] = make_int4(q, i32(e), i32(trs[z]), 0);  // one 16-B store
+      put(pos, make_int4(q, i32(e), i32(trs[z]), 0));
       z = par[z];
     }
   }
+  if (have) reinterpret_cast<int4 *>(out)[hpos] = held;
 }
 
 // warp per pair: its hits are the contiguous SA range [ilo, ilo + cnt) of
@@ -1837,8 +1866,9 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
                                               int(esmem)));
                 eattr = true;
               }
+              const bool pair32 = (reinterpret_cast<uintptr_t>(d_out) & 31) == 0;
               k_stream_emit<<<nstreams, kEmitThreads, esmem, s>>>(sm, stk, tof, qbase, cap, d_out, qorder, gpar, otr,
-                                                                  gdep);
+                                                                  gdep, pair32);
               APO_CHECK_LAUNCH();
               c.launches += 4;
             }
