@@ -81,11 +81,10 @@ struct CandF {
     int w;
     if (pair(k, l, a, bb, w)) {
       u32 key = (u32(w) << bl) | u32(maxl - l);
-      i64 o = 2 * i64(excl);
-      k1[o] = key;
-      k1[o + 1] = key;
-      v1[o] = (u64(k) << 32) | u64(a);
-      v1[o + 1] = (u64(k) << 32) | u64(bb);
+      i64 o = 2 * i64(excl);  // even: the pair's two records go out as one 8-B and one 16-B store
+      reinterpret_cast<uint2 *>(k1)[o >> 1] = make_uint2(key, key);
+      reinterpret_cast<ulonglong2 *>(v1)[o >> 1] =
+          make_ulonglong2((u64(k) << 32) | u64(a), (u64(k) << 32) | u64(bb));
     }
     if (k == npairs - 1) *m_out = 2 * i64(incl);
     return false;
