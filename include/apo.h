@@ -248,7 +248,8 @@ apo_status apo_trie_copy(const apo_trie *trie, uint64_t *d_tokens, int64_t *h_of
  * trace_id); end_pos is stream-local.  Other modes: APO_ERR_INVALID.
  * h_off: HOST int64[nstreams+1] CSR offsets into d_streams.  d_count
  * (device int64[1]) <- number of hits; at most cap records are stored
- * (d_out: device, 16-byte aligned, cap records). */
+ * (d_out: device, 16-byte aligned, cap records; 32-byte alignment lets the
+ * library store consecutive records in pairs).  Synchronises `stream`. */
 apo_status apo_match(apo_ctx *ctx, const apo_trie *trie, const uint64_t *d_streams,
                      const int64_t *h_off, int32_t nstreams, int32_t mode, apo_match_rec *d_out,
                      int64_t cap, int64_t *d_count, void *stream);
