@@ -529,10 +529,11 @@ __global__ void k_pair_list(const u32 *__restrict__ pbase, const u32 *__restrict
 // resident at any moment read overlapping trace sets and the trace tokens
 // (the matcher's HBM stream) are served from L2 instead of re-read from HBM.
 __global__ void k_stream_keys(const u32 *__restrict__ qoff, const u32 *__restrict__ zsorted,
-                              const u32 *__restrict__ ptrace, int S, u64 *__restrict__ key, u32 *__restrict__ val) {
+                              const u32 *__restrict__ ptrace, int S, i64 T, u64 *__restrict__ key,
+                              u32 *__restrict__ val) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= S) return;
-  key[q] = qoff[q] < qoff[q + 1] ? u64(ptrace[zsorted[qoff[q]]]) : ~0ull;
+  key[q] = qoff[q] < qoff[q + 1] ? u64(ptrace[zsorted[qoff[q]]]) : u64(T);  // streams without pairs last
   val[q] = u32(q);
 }
 
@@ -1369,7 +1370,9 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
     k_piece_hash<false><<<grid_for(np * 32, T256), T256, 0, s>>>(d_ptok, d_poff, np, hk, hv, pk, PieceSrc{});
   APO_CHECK_LAUNCH();
   APO_CUDA(cudaMemcpyAsync(hk_keep, hk, sizeof(u64) * np, cudaMemcpyDeviceToDevice, s));
-  bool a1 = radix_sort_u64_u32(c, hk, hv, hk_alt, hv_alt, np, 0, 64, s);
+  // grouping only needs equal hashes together: 32 hash bits suffice (a rare
+  // split group is caught by the exact neighbour check of step 3)
+  bool a1 = radix_sort_u64_u32(c, hk, hv, hk_alt, hv_alt, np, 0, 32, s);
   u64 *k1 = a1 ? hk_alt : hk;
   u32 *o1 = a1 ? hv_alt : hv;
   u64 *k2 = a1 ? hk : hk_alt;
@@ -1818,10 +1821,10 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             const u32 *sqv = aq ? qv_alt : qv;
             k_q_offsets<<<grid_for(i64(nstreams) + 1, T256), T256, 0, s>>>(sqk, P, nstreams, qoff);
             APO_CHECK_LAUNCH();
-            k_stream_keys<<<grid_for(nstreams, T256), T256, 0, s>>>(qoff, sqv, ptr, nstreams, sk, sv);
+            k_stream_keys<<<grid_for(nstreams, T256), T256, 0, s>>>(qoff, sqv, ptr, nstreams, T, sk, sv);
             APO_CHECK_LAUNCH();
             c.launches += 2;
-            const bool as = radix_sort_u64_u32(c, sk, sv, sk_alt, sv_alt, nstreams, 0, 64, s);
+            const bool as = radix_sort_u64_u32(c, sk, sv, sk_alt, sv_alt, nstreams, 0, bits_for(u64(T)), s);
             const u32 *qorder = as ? sv_alt : sv;
             const size_t smem = sizeof(u64) * kSMMax + 2 * sizeof(unsigned short) * kSMMax;
             static bool attr = false;
