@@ -371,8 +371,10 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   if (!want_lcp) return;
   // ---- K4: phi, PLCP, LCP ----
   const u32 *sa = reinterpret_cast<const u32 *>(w.sa);
-  k_phi<<<G, T, 0, s>>>(sa, b, w.phi);
-  APO_CHECK_LAUNCH();
+  if (w.rw == nullptr) {  // the K9 path writes phi itself
+    k_phi<<<G, T, 0, s>>>(sa, b, w.phi);
+    APO_CHECK_LAUNCH();
+  }
   Levels L{};
   for (int q = 0; q < w.max_levels && q < 40; ++q) L.p[q] = w.levels[q];
   i64 chunks = (N + kPlcpChunk - 1) / kPlcpChunk;

@@ -288,7 +288,8 @@ constexpr u64 kSmemPassBytes = 20, kSmemRoundBytes = 18;
 // of the tokens), or nullptr to take level 0 from levels[0].
 __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__restrict__ ids, LevelPtrs lv,
                                                       int max_levels, i32 *__restrict__ sa_out,
-                                                      i32 *__restrict__ rw, unsigned long long *smem_bytes) {
+                                                      i32 *__restrict__ rw, unsigned long long *smem_bytes,
+                                                      i32 *__restrict__ phi_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WinSmem &S = *reinterpret_cast<WinSmem *>(smem_raw);
   const int tid = threadIdx.x;
@@ -343,7 +344,11 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
   for (i64 h = 1;; h <<= 1) {
     if (G == u32(n)) {  // all distinct: the sorted buffer is the suffix array
       const unsigned short *pos = sorted_in_a ? S.a.pos : S.b.pos;
-      for (int q = tid; q < n; q += kWT) sa_out[beg + q] = i32(beg) + i32(pos[q]);
+      for (int q = tid; q < n; q += kWT) {
+        sa_out[beg + q] = i32(beg) + i32(pos[q]);
+        // phi of the LCP stage (K4): the suffix ranked just before, -1 for the first
+        if (phi_out) phi_out[beg + pos[q]] = q > 0 ? i32(beg) + i32(pos[q - 1]) : -1;
+      }
       if (tid == 0) {
         rw[w] = r;
         if (smem_bytes) atomicAdd(smem_bytes, (unsigned long long)prof);
@@ -413,7 +418,7 @@ void run_window_sa(Ctx &c, const Batch &b, SAWork &w, cudaStream_t s) {
   if (c.prof) c.prof_begin(kProfWindowSA, 0.0, s);
   unsigned long long *cnt =
       c.prof ? reinterpret_cast<unsigned long long *>(c.d_misc + kProfDevSlot + kProfWindowSA) : nullptr;
-  k_window_sa<<<b.W, kWT, smem, s>>>(b, w.ids_valid ? w.ids : nullptr, lv, w.max_levels, w.sa, w.rw, cnt);
+  k_window_sa<<<b.W, kWT, smem, s>>>(b, w.ids_valid ? w.ids : nullptr, lv, w.max_levels, w.sa, w.rw, cnt, w.phi);
   APO_CHECK_LAUNCH();
   if (c.prof) c.prof_end(s);
   c.launches++;
