@@ -166,8 +166,12 @@ __device__ __forceinline__ i64 gallop_lcp(const Levels &L, int R, int unit, cons
 constexpr int kPlcpChunk = 8;  // positions per thread (more independent Kasai chains in flight)
 constexpr int kKasaiSteps = 16;
 
+// With `lcp` set (windows fully sorted: the last rank level is the inverse
+// suffix array), PLCP[i] is scattered straight to lcp[ISA[i] - 1] and the
+// window's first suffix writes the window's last slot (0), so no gather pass
+// over the suffix array is needed; otherwise PLCP goes to `plcp`.
 __global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi, Levels L, int R, int unit,
-                       const i32 *__restrict__ rw, Batch b, i32 *__restrict__ plcp) {
+                       const i32 *__restrict__ rw, Batch b, i32 *__restrict__ plcp, i32 *__restrict__ lcp) {
   i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   i64 i0 = t * kPlcpChunk;
   if (i0 >= b.N) return;
@@ -186,7 +190,7 @@ __global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi,
     }
     i64 j = phi[i];
     if (j < 0) {
-      plcp[i] = 0;
+      if (lcp) lcp[end - 1] = 0; else plcp[i] = 0;
       h = 0;
       continue;
     }
@@ -208,7 +212,10 @@ __global__ void k_plcp(const u64 *__restrict__ tok, const i32 *__restrict__ phi,
         }
       }
     }
-    plcp[i] = i32(h);
+    if (lcp)
+      lcp[L.p[Rcur][i] - 1] = i32(h);  // the final level holds global ranks: ISA[i] - 1 is the predecessor pair
+    else
+      plcp[i] = i32(h);
   }
 }
 
@@ -378,10 +385,15 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   Levels L{};
   for (int q = 0; q < w.max_levels && q < 40; ++q) L.p[q] = w.levels[q];
   i64 chunks = (N + kPlcpChunk - 1) / kPlcpChunk;
-  k_plcp<<<grid_for(chunks, 128), 128, 0, s>>>(tok, w.phi, L, w.R, w.unit, w.rw, b, w.plcp);
+  // fully sorted per-window paths (K9, or K3 to the end): scatter directly
+  const bool direct = !b.gen && b.sort_depth == 0;
+  k_plcp<<<grid_for(chunks, 128), 128, 0, s>>>(tok, w.phi, L, w.R, w.unit, w.rw, b, w.plcp,
+                                                 direct ? w.lcp : nullptr);
   APO_CHECK_LAUNCH();
-  k_lcp_gather<<<G, T, 0, s>>>(sa, w.plcp, b, w.lcp);
-  APO_CHECK_LAUNCH();
+  if (!direct) {
+    k_lcp_gather<<<G, T, 0, s>>>(sa, w.plcp, b, w.lcp);
+    APO_CHECK_LAUNCH();
+  }
   c.launches += 3;
 }
 
