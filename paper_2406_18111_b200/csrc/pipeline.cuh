@@ -71,6 +71,7 @@ struct SelWork {
   int rmq_levels;
   i32 *glen;              // 2N per-group length
   i32 *gbase;             // 2N per-group window base (global position of the window start)
+  i32 *gwin;              // 2N per-group window index
   u32 *gpos;              // 2N per-group first position in sort-1 order
   i32 *cl, *cs, *cg;      // 2N per candidate (final order): length, start (global), group
   u8 *state;              // 2N 0 undecided, 1 kept, 2 rejected

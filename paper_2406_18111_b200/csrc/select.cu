@@ -191,6 +191,7 @@ struct HeadF {
   const i32 *wid;  // NULL for one window
   int bW;          // window field of the sort-1 key starts at bit bW
   i32 *gbase;
+  i32 *gwin;       // window of the group
   u32 *gpos;       // position of the group's first member in sort-1 order
   const u8 *head;  // group-head flags from k_head_flags
   __device__ u32 load(i64 c) const { return head[c]; }
@@ -202,6 +203,7 @@ struct HeadF {
     if (incl != excl) {
       glen[g] = i32(maxl - i64(k1[c] & lmask));
       gbase[g] = i32(base);
+      gwin[g] = wid ? i32(k1[c] >> bW) : 0;
       gpos[g] = u32(c);
     }
     if (c == m - 1) *G_out = i64(incl);
@@ -502,7 +504,7 @@ __global__ void k_gstats(const i32 *__restrict__ cg, const u8 *__restrict__ stat
 
 struct OccF {
   Batch b;
-  const i32 *cg, *cs;
+  const i32 *cg, *cs, *gbase;
   const u8 *state;
   const u32 *gcnt;
   u32 minc;
@@ -515,10 +517,7 @@ struct OccF {
   __device__ bool store(i64 c, u32 incl, u32 excl) const {
     if (incl != excl) {
       oidx[c] = excl;
-      if (occ != nullptr && i64(excl) < occ_cap) {
-        i64 s = cs[c];
-        occ[excl] = i32(s - b_beg(b, b_wid(b, s)));
-      }
+      if (occ != nullptr && i64(excl) < occ_cap) occ[excl] = cs[c] - gbase[cg[c]];  // window-local start
     }
     if (c == m - 1) *total = i64(incl);
     return false;
@@ -529,7 +528,7 @@ struct OccF {
 struct RepF {
   Batch b;
   const u32 *gcnt, *gfirst, *oidx;
-  const i32 *glen, *cs;
+  const i32 *glen, *cs, *gbase, *gwin;
   u32 minc;
   apo_repeat *out;
   i64 cap;
@@ -541,10 +540,10 @@ struct RepF {
     if (incl != excl) {
       u32 c0 = gfirst[g];
       i64 s = cs[c0];
-      int w = b_wid(b, s);
+      const int w = gwin[g];
       if (i64(excl) < cap && out != nullptr) {
         apo_repeat r;
-        r.start = i32(s - b_beg(b, w));
+        r.start = i32(s - gbase[g]);
         r.length = glen[g];
         r.count = i32(gcnt[g]);
         r.first_occ = i32(oidx[c0]);
@@ -681,6 +680,7 @@ void plan_select(Carver &cv, const Batch &b, SelWork &w) {
   for (int j = 0; j < w.rmq_levels; ++j) w.rmq[j + 2] = cv.take<i32>(nb);
   w.glen = cv.take<i32>(M);
   w.gbase = cv.take<i32>(M);
+  w.gwin = cv.take<i32>(M);
   w.gpos = cv.take<u32>(M);
   w.cl = cv.take<i32>(M);
   w.cs = cv.take<i32>(M);
@@ -764,7 +764,7 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
     APO_CHECK_LAUNCH();
     c.launches++;
     HeadF f{k1, v1, maxl, (1u << bl) - 1u, bL, m, w.k2, w.glen, G_dev, b.off, b.W > 1 ? b.wid : nullptr,
-            bl, w.gbase, w.gpos, w.state};
+            bl, w.gbase, w.gwin, w.gpos, w.state};
     launch_scan<false>(c, m, f, s);
   }
   const i64 G = i64(c.read_u64(reinterpret_cast<u64 *>(G_dev), s));
@@ -828,9 +828,9 @@ void emit_repeats(Ctx &c, const Batch &b, SelWork &w, int min_count, apo_repeat 
     APO_CHECK_LAUNCH();
     c.launches++;
     const u32 minc = u32(min_count < 1 ? 1 : min_count);
-    OccF of{b, w.cg, w.cs, w.state, w.gcnt, minc, w.oidx, occ, occ_cap, m, counts + 1};
+    OccF of{b, w.cg, w.cs, w.gbase, w.state, w.gcnt, minc, w.oidx, occ, occ_cap, m, counts + 1};
     launch_scan<false>(c, m, of, s);
-    RepF rf{b, w.gcnt, w.gfirst, w.oidx, w.glen, w.cs, minc, out, cap, w.wcnt, G, counts};
+    RepF rf{b, w.gcnt, w.gfirst, w.oidx, w.glen, w.cs, w.gbase, w.gwin, minc, out, cap, w.wcnt, G, counts};
     launch_scan<false>(c, G, rf, s);
   }
   if (out_off != nullptr) {
