@@ -272,3 +272,26 @@ def test_match_many_intervals_one_stream(ctx):
     hits = ctx.match(trie, dev(sflat), soff).cpu().numpy()
     want, cnt = oracle.match_brute(sflat, soff, tt.cpu().numpy(), to)
     assert cnt == len(hits) and np.array_equal(hits, want)
+
+
+def test_match_capacity_prefix(ctx):
+    """With cap < number of hits, apo_match stores exactly the first cap
+    records of the full sorted output (odd caps cut a 32-byte record pair),
+    reports the true count, and leaves the rest of the buffer untouched."""
+    from paper_2406_18111_b200.apo import _ptr, _P_I64, _stream
+    tok, off, st, so = gen.c4(seed=31, windows=10, window=1200, templates=6)
+    rep, roff, occ = ctx.find_repeats_batched(dev(tok), off, 5)
+    trie = ctx.trie_build(dev(tok), off, rep, roff, 5, 0)
+    ds = dev(st)
+    full = ctx.match(trie, ds, so)
+    nh = full.shape[0]
+    assert nh > 100
+    o = np.ascontiguousarray(so, dtype=np.int64)
+    for cap in (1, 7, nh // 3, nh // 2 + 1, nh - 1):
+        out = torch.full((cap + 8, 4), -5, dtype=torch.int32, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        ctx._raise(ctx.lib.apo_match(ctx.h, trie.h, _ptr(ds), o.ctypes.data_as(_P_I64), len(o) - 1, 0,
+                                     _ptr(out), cap, _ptr(cnt), _stream(ctx.device)))
+        assert int(cnt.item()) == nh
+        assert torch.equal(out[:cap, :3], full[:cap])
+        assert bool((out[cap:] == -5).all())
