@@ -287,3 +287,32 @@ def test_ruler_multiscale_batch(ctx, B, C):
         assert np.array_equal(got[:, :3], want["repeats"][:, :3]), w
         for row, wrow in zip(got, want["repeats"]):
             assert np.array_equal(occ[row[3]:row[3] + row[2]], want["occ"][wrow[3]:wrow[3] + wrow[2]])
+
+
+def test_batch_window_size_boundary(ctx):
+    """Windows straddling the on-chip limit (16,383 / 16,384 / 16,385 ops)
+    in one batch: the suffix arrays take the global path, candidate sorting
+    the per-window path; tokens include 0 and 2^64-1.  Every window equals
+    the oracle."""
+    wins = []
+    for i, n in enumerate((16383, 16384, 16385, 300)):
+        S = gen.c3()[i * 20000:i * 20000 + n].copy()
+        S[::997] = np.uint64((1 << 64) - 1)
+        S[5::1013] = np.uint64(0)
+        wins.append(S)
+    tok = np.concatenate(wins)
+    off = np.cumsum([0] + [len(x) for x in wins]).astype(np.int64)
+    rep, roff, occ = ctx.find_repeats_batched(dev(tok), off, 25)
+    rep, roff, occ = rep.cpu().numpy(), roff.cpu().numpy(), occ.cpu().numpy()
+    for w, S in enumerate(wins):
+        want = oracle.find_repeats(S, 25, tier=1)
+        got = rep[roff[w]:roff[w + 1]]
+        assert np.array_equal(got[:, :3], want["repeats"][:, :3]), w
+        for row, wrow in zip(got, want["repeats"]):
+            assert np.array_equal(occ[row[3]:row[3] + row[2]], want["occ"][wrow[3]:wrow[3] + wrow[2]])
+    sa, lcp = ctx.suffix_array_batched(dev(tok), off)
+    sa, lcp = sa.cpu().numpy(), lcp.cpu().numpy()
+    for w, S in enumerate(wins):
+        want = oracle.sa_doubling(S)
+        assert np.array_equal(sa[off[w]:off[w + 1]], want)
+        assert np.array_equal(lcp[off[w]:off[w + 1]][:len(S) - 1], oracle.lcp_kasai(S, want))
