@@ -295,3 +295,23 @@ def test_match_capacity_prefix(ctx):
         assert int(cnt.item()) == nh
         assert torch.equal(out[:cap, :3], full[:cap])
         assert bool((out[cap:] == -5).all())
+
+
+def test_match_long_streams(ctx):
+    """Streams longer than the on-chip limit (> 16,384 ops): the per-stream
+    path with global binary searches, hit enumeration and the (stream, end)
+    sort; against the brute-force oracle."""
+    S = gen.c3()[:60000]
+    wtok = S[:20000]
+    d = dev(wtok)
+    off = np.array([0, len(wtok)], dtype=np.int64)
+    rep, roff, occ = ctx.find_repeats_batched(d, off, 25)
+    trie = ctx.trie_build(d, off, rep, roff, 25, 0)
+    tt, to = trie.traces()
+    streams = [S[20000:40000], S[40000:57000], S[57000:60000]]
+    sflat = np.concatenate(streams)
+    soff = np.cumsum([0] + [len(x) for x in streams]).astype(np.int64)
+    hits = ctx.match(trie, dev(sflat), soff).cpu().numpy()
+    want, cnt = oracle.match_brute(sflat, soff, tt.cpu().numpy(), to)
+    assert cnt == len(hits) and np.array_equal(hits, want)
+    assert len(hits) > 0
