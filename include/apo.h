@@ -178,10 +178,20 @@ void apo_history_destroy(apo_history *h);
  * slices "ShouldAnalyzeHistory / GetAnalysisSubset" selects while the global
  * op count k goes from k0+1 to k0+n: at every k with k % C == 0 the slice
  * [k - min(2^ruler(k/C) * C, B), k) (R13).  h_slices receives up
- * to cap slices in order; *h_nslices the true number (APO_ERR_CAPACITY if it
- * exceeds cap; the tokens are still appended). */
+ * to cap slices in order; *h_nslices the true number.  If that number
+ * exceeds cap the call returns APO_ERR_CAPACITY WITHOUT ingesting anything
+ * (the schedule is pure arithmetic, so the count is known up front): the
+ * caller retries with *h_nslices slots. */
 apo_status apo_ingest(apo_history *h, const uint64_t *d_tokens, int64_t n, apo_slice *h_slices,
                       int64_t cap, int64_t *h_nslices, void *stream);
+
+/* The schedule apo_ingest applies, as a pure host function (no device, no
+ * state): the slices for op counts k in (k0, k0+n] (R13), into
+ * h_slices[0 .. cap); *h_nslices = the true number; APO_ERR_CAPACITY if it
+ * exceeds cap (the first cap slices are still written).  capacity_B >=
+ * scale_C >= 1, k0 >= 0, n >= 0. */
+apo_status apo_ruler_slices(int64_t k0, int64_t n, int32_t scale_C, int64_t capacity_B, apo_slice *h_slices,
+                            int64_t cap, int64_t *h_nslices);
 
 /* Copy history tokens [begin, end) (absolute coordinates, must lie within
  * the last capacity_B tokens) to d_out (end-begin tokens). */

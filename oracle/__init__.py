@@ -28,7 +28,7 @@ import threading
 import numpy as np
 
 from .ruler import ruler, ruler_slices  # noqa: F401
-from .traces import traces_from_repeats  # noqa: F401
+from .traces import traces_from_repeats, traces_from_repeats_np  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "apo_oracle.c")
@@ -48,7 +48,7 @@ def build(force: bool = False) -> str:
     """Compile the C oracle (gcc -O2).  Building the checker is not using it."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC", _SRC, "-o", tmp])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC", "-pthread", _SRC, "-o", tmp])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -71,6 +71,7 @@ def _load():
                 "or_sa_check": (ctypes.c_int, [P_U64, I64, P_I32]),
                 "or_lcp_kasai": (None, [P_U64, I64, P_I32, P_I32]),
                 "or_sort_and_id_rmq": (None, [P_U64, I64, P_I32, P_I32, I64, P_I32, P_I32, P_I32]),
+                "or_sort_and_id_rmq_mt": (None, [P_U64, I64, P_I32, P_I32, I64, P_I32, P_I32, P_I32, I32]),
                 "or_greedy_marks": (None, [I64, I64, P_I32, P_I32, P_U8]),
                 "or_match_brute": (I64, [P_U64, P_I64, I64, P_U64, P_I64, I64, P_I32, P_I32, P_I32, I64]),
             }
@@ -170,6 +171,22 @@ def sort_and_id_rmq(S, sa, lcp, cl, cs):
     if len(cl):
         _load().or_sort_and_id_rmq(_p(S, P_U64), len(S), _p(sa, P_I32), _p(lcp, P_I32), len(cl),
                                    _p(cl, P_I32), _p(cs, P_I32), _p(cid, P_I32))
+    return cl, cs, cid
+
+
+def sort_and_id_rmq_mt(S, sa, lcp, cl, cs, threads: int | None = None):
+    """sort_and_id_rmq with the same comparator, sorted on `threads` host
+    threads (chunk sorts + a merge tree); for ~10^8 candidates."""
+    S = _u64(S)
+    sa = np.ascontiguousarray(sa, dtype=np.int32)
+    lcp = np.ascontiguousarray(lcp, dtype=np.int32)
+    cl = np.array(cl, dtype=np.int32)
+    cs = np.array(cs, dtype=np.int32)
+    cid = np.empty(len(cl), dtype=np.int32)
+    t = int(threads or os.cpu_count() or 1)
+    if len(cl):
+        _load().or_sort_and_id_rmq_mt(_p(S, P_U64), len(S), _p(sa, P_I32), _p(lcp, P_I32), len(cl),
+                                      _p(cl, P_I32), _p(cs, P_I32), _p(cid, P_I32), t)
     return cl, cs, cid
 
 

@@ -20,6 +20,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <pthread.h>
 
 /* ------------------------------------------------------------------------ */
 /* R1: tokens compare as unsigned 64-bit integers.                            */
@@ -362,6 +363,89 @@ void or_sort_and_id_rmq(const uint64_t *S, int64_t n, const int32_t *sa, const i
     free(c); rmq_free(&r); free(isa);
 }
 
+/* The same O4 + IDs for inputs with ~10^8 candidates (C5 at 2^26): the SAME
+ * comparator (cmp_cand_rmq), the sort only spread over host threads -- each
+ * thread qsort_r's one chunk, then sorted runs are merged pairwise (a merge
+ * tree, each merge in its own thread; a merge keeps the left run first on
+ * ties, and ties are exact (l, s) duplicates, so the result is the sorted
+ * sequence qsort would give).  IDs as in or_sort_and_id_rmq, with the
+ * neighbour test evaluated in parallel.  Pinned against the single-thread
+ * version in tests/test_oracle_pins.py. */
+typedef struct { cand_t *a; int64_t lo, hi; const rmq_t *r; } sort_job_t;
+static void *sort_job(void *p) {
+    sort_job_t *j = (sort_job_t *)p;
+    qsort_r(j->a + j->lo, (size_t)(j->hi - j->lo), sizeof(cand_t), cmp_cand_rmq, (void *)j->r);
+    return NULL;
+}
+typedef struct { const cand_t *src; cand_t *dst; int64_t lo, mid, hi; const rmq_t *r; } merge_job_t;
+static void *merge_job(void *p) {
+    merge_job_t *j = (merge_job_t *)p;
+    int64_t a = j->lo, b = j->mid, o = j->lo;
+    while (a < j->mid && b < j->hi)
+        j->dst[o++] = cmp_cand_rmq(&j->src[b], &j->src[a], (void *)j->r) < 0 ? j->src[b++] : j->src[a++];
+    while (a < j->mid) j->dst[o++] = j->src[a++];
+    while (b < j->hi) j->dst[o++] = j->src[b++];
+    return NULL;
+}
+typedef struct { const cand_t *c; int64_t lo, hi; const rmq_t *r; uint8_t *same; } id_job_t;
+static void *id_job(void *p) {
+    id_job_t *j = (id_job_t *)p;
+    for (int64_t i = j->lo; i < j->hi; i++)
+        j->same[i] = i > 0 && j->c[i].l == j->c[i - 1].l && rmq_lcp(j->r, j->c[i].s, j->c[i - 1].s) >= j->c[i].l;
+    return NULL;
+}
+void or_sort_and_id_rmq_mt(const uint64_t *S, int64_t n, const int32_t *sa, const int32_t *lcp,
+                           int64_t m, int32_t *cl, int32_t *cs, int32_t *id, int32_t nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    int32_t *isa = (int32_t *)malloc(sizeof(int32_t) * (size_t)(n ? n : 1));
+    for (int64_t i = 0; i < n; i++) isa[sa[i]] = (int32_t)i;
+    rmq_t r;
+    rmq_build(&r, S, n, lcp, isa);
+    cand_t *c = (cand_t *)malloc(sizeof(cand_t) * (size_t)(m ? m : 1));
+    cand_t *t = (cand_t *)malloc(sizeof(cand_t) * (size_t)(m ? m : 1));
+    for (int64_t i = 0; i < m; i++) { c[i].l = cl[i]; c[i].s = cs[i]; }
+    int64_t runs = nthreads, *b = (int64_t *)malloc(sizeof(int64_t) * (size_t)(runs + 1));
+    for (int64_t k = 0; k <= runs; k++) b[k] = m * k / runs;
+    pthread_t th[256];
+    sort_job_t sj[256];
+    for (int64_t k = 0; k < runs; k++) {
+        sj[k] = (sort_job_t){c, b[k], b[k + 1], &r};
+        pthread_create(&th[k], NULL, sort_job, &sj[k]);
+    }
+    for (int64_t k = 0; k < runs; k++) pthread_join(th[k], NULL);
+    merge_job_t mj[256];
+    while (runs > 1) {
+        int64_t nr = 0;
+        for (int64_t k = 0; k < runs; k += 2) {
+            int64_t hi = k + 2 <= runs ? b[k + 2] : b[k + 1];
+            int64_t mid = k + 2 <= runs ? b[k + 1] : hi;
+            mj[nr] = (merge_job_t){c, t, b[k], mid, hi, &r};
+            pthread_create(&th[nr], NULL, merge_job, &mj[nr]);
+            b[nr] = b[k];
+            nr++;
+        }
+        for (int64_t k = 0; k < nr; k++) pthread_join(th[k], NULL);
+        b[nr] = m;
+        runs = nr;
+        cand_t *x = c; c = t; t = x;
+    }
+    uint8_t *same = (uint8_t *)malloc((size_t)(m ? m : 1));
+    id_job_t ij[256];
+    for (int64_t k = 0; k < nthreads; k++) {
+        ij[k] = (id_job_t){c, m * k / nthreads, m * (k + 1) / nthreads, &r, same};
+        pthread_create(&th[k], NULL, id_job, &ij[k]);
+    }
+    for (int64_t k = 0; k < nthreads; k++) pthread_join(th[k], NULL);
+    int32_t cur = -1;
+    for (int64_t i = 0; i < m; i++) {
+        cl[i] = c[i].l; cs[i] = c[i].s;
+        if (!same[i]) cur++;
+        id[i] = cur;
+    }
+    free(same); free(b); free(c); free(t); rmq_free(&r); free(isa);
+}
+
 /* O5' (tier-1): the greedy loop with the marked array of length |S|
  * (P:613-619): "as each candidate is selected, all positions covered by the
  * candidate are marked ... interval intersection can be checked by checking if
@@ -391,13 +475,23 @@ int64_t or_match_brute(const uint64_t *st, const int64_t *st_off, int64_t nstrea
                        const uint64_t *tr, const int64_t *tr_off, int64_t ntraces,
                        int32_t *out_stream, int32_t *out_end, int32_t *out_trace, int64_t cap) {
     int64_t cnt = 0;
+    /* per trace: length and last token in two small arrays, so the test of
+     * every (end, trace) pair reads them sequentially; the last token is
+     * compared first, then the whole content (the order of the token
+     * comparisons does not change which pairs are equal) */
+    int64_t *tlen = (int64_t *)malloc(sizeof(int64_t) * (size_t)(ntraces ? ntraces : 1));
+    uint64_t *tlast = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(ntraces ? ntraces : 1));
+    for (int64_t t = 0; t < ntraces; t++) {
+        tlen[t] = tr_off[t + 1] - tr_off[t];
+        tlast[t] = tlen[t] > 0 ? tr[tr_off[t + 1] - 1] : 0;
+    }
     for (int64_t q = 0; q < nstreams; q++) {
         const uint64_t *s = st + st_off[q];
         int64_t len = st_off[q + 1] - st_off[q];
         for (int64_t e = 0; e < len; e++) {
             for (int64_t t = 0; t < ntraces; t++) {
-                int64_t L = tr_off[t + 1] - tr_off[t];
-                if (L <= 0 || L > e + 1) continue;
+                int64_t L = tlen[t];
+                if (L <= 0 || L > e + 1 || tlast[t] != s[e]) continue;
                 if (memcmp(s + e - L + 1, tr + tr_off[t], sizeof(uint64_t) * (size_t)L) == 0) {
                     if (cnt < cap) { out_stream[cnt] = (int32_t)q; out_end[cnt] = (int32_t)e; out_trace[cnt] = (int32_t)t; }
                     cnt++;
@@ -405,5 +499,6 @@ int64_t or_match_brute(const uint64_t *st, const int64_t *st_off, int64_t nstrea
             }
         }
     }
+    free(tlen); free(tlast);
     return cnt;
 }

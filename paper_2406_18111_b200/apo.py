@@ -63,6 +63,7 @@ _SIGS = {
     "apo_history_create": (ctypes.c_int, [_VP, _I64, _I32, ctypes.POINTER(_VP)]),
     "apo_history_destroy": (None, [_VP]),
     "apo_ingest": (ctypes.c_int, [_VP, _VP, _I64, ctypes.POINTER(apo_slice), _I64, _P_I64, _VP]),
+    "apo_ruler_slices": (ctypes.c_int, [_I64, _I64, _I32, _I64, ctypes.POINTER(apo_slice), _I64, _P_I64]),
     "apo_history_window": (ctypes.c_int, [_VP, _I64, _I64, _VP, _VP]),
     "apo_history_count": (ctypes.c_int64, [_VP]),
     "apo_trie_build": (ctypes.c_int, [_VP, _VP, _P_I64, _I32, _VP, _VP, _I32, _I32, ctypes.POINTER(_VP), _VP]),
@@ -342,6 +343,23 @@ class Context:
         return History(self, capacity_B, scale_C)
 
 
+def ruler_slices(k0: int, n: int, scale_C: int, capacity_B: int) -> list[tuple[int, int]]:
+    """apo_ruler_slices: the analysis slices apo_ingest emits for op counts
+    (k0, k0+n] (host logic only; no device needed)."""
+    lib = load_library()
+    ns = ctypes.c_int64()
+    cap = 64
+    while True:
+        buf = (apo_slice * cap)()
+        st = lib.apo_ruler_slices(int(k0), int(n), int(scale_C), int(capacity_B), buf, cap, ctypes.byref(ns))
+        if st != APO_ERR_CAPACITY:
+            break
+        cap = int(ns.value)
+    if st != APO_OK:
+        raise ApoError(st, "apo_ruler_slices: invalid arguments")
+    return [(buf[i].begin, buf[i].end) for i in range(ns.value)]
+
+
 class History:
     """Alg. 1 TraceFinder buffer with ruler-function sampling (§4.4)."""
 
@@ -366,12 +384,14 @@ class History:
 
     def ingest(self, tokens: torch.Tensor, cap: int = 4096) -> list[tuple[int, int]]:
         tokens = _check_tok(tokens, self.ctx.device)
-        buf = (apo_slice * max(cap, 1))()
         ns = ctypes.c_int64()
-        st = self.ctx.lib.apo_ingest(self.h, _ptr(tokens), tokens.numel(), buf, cap, ctypes.byref(ns),
-                                     _stream(self.ctx.device))
-        if st == APO_ERR_CAPACITY:
-            raise ApoError(st, f"{ns.value} slices > cap {cap}")
+        while True:
+            buf = (apo_slice * max(cap, 1))()
+            st = self.ctx.lib.apo_ingest(self.h, _ptr(tokens), tokens.numel(), buf, cap, ctypes.byref(ns),
+                                         _stream(self.ctx.device))
+            if st != APO_ERR_CAPACITY:
+                break
+            cap = int(ns.value)  # nothing was ingested: retry with room for every slice
         self.ctx._raise(st)
         return [(buf[i].begin, buf[i].end) for i in range(ns.value)]
 

@@ -165,6 +165,16 @@ struct Ctx {
   u32 *take_counter(cudaStream_t s);
   u32 read_u32(const u32 *d_ptr, cudaStream_t s);
   u64 read_u64(const u64 *d_ptr, cudaStream_t s);
+  // dynamic shared-memory opt-ins already applied on THIS context's device
+  // (the attribute is per device, so it is tracked per context, not per
+  // process)
+  std::vector<std::pair<const void *, size_t>> smem_optins;
+  void smem_optin(const void *func, size_t bytes) {
+    for (auto &e : smem_optins)
+      if (e.first == func && e.second >= bytes) return;
+    APO_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    smem_optins.emplace_back(func, bytes);
+  }
 };
 
 // ------------------------------------------------- decoupled look-back --

@@ -68,10 +68,40 @@ void apo_history_destroy(apo_history *h) {
 
 int64_t apo_history_count(const apo_history *h) { return h ? h->count : -1; }
 
+apo_status apo_ruler_slices(int64_t k0, int64_t n, int32_t scale_C, int64_t capacity_B, apo_slice *h_slices,
+                            int64_t cap, int64_t *h_nslices) {
+  if (k0 < 0 || n < 0 || scale_C < 1 || capacity_B < scale_C || cap < 0 || (cap > 0 && !h_slices))
+    return APO_ERR_INVALID;
+  // ShouldAnalyzeHistory / GetAnalysisSubset (reading R13): at
+  // every op count k in (k0, k0+n] with k % C == 0, the last
+  // min(2^ruler(k/C) * C, B) tokens
+  const i64 C = scale_C, k1 = k0 + n;
+  i64 ns = 0;
+  for (i64 k = (k0 / C + 1) * C; k <= k1; k += C) {
+    if (ns < cap) {
+      const int r = ruler(k / C);
+      i64 len = r < 62 ? (i64(1) << r) * C : capacity_B;
+      if (len > capacity_B || len <= 0) len = capacity_B;
+      h_slices[ns] = apo_slice{k - len, k};
+    }
+    ++ns;
+  }
+  if (h_nslices) *h_nslices = ns;
+  return ns > cap ? APO_ERR_CAPACITY : APO_OK;
+}
+
 apo_status apo_ingest(apo_history *h, const uint64_t *d_tokens, int64_t n, apo_slice *h_slices, int64_t cap,
                       int64_t *h_nslices, void *stream) {
   if (!h || n < 0 || cap < 0 || (n > 0 && !d_tokens) || (cap > 0 && !h_slices)) return APO_ERR_INVALID;
   Ctx &c = h->ctx->c;
+  // The schedule is pure host arithmetic on the op count, so the slices are
+  // known before anything changes: too small a cap fails WITHOUT ingesting,
+  // and the caller retries with *h_nslices slots.
+  i64 ns = 0;
+  const apo_status st = apo_ruler_slices(h->count, n, h->C, h->B, h_slices, cap, &ns);
+  if (h_nslices) *h_nslices = ns;
+  if (st != APO_OK) return st;
+  const i64 k1 = h->count + n;
   cudaSetDevice(c.device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (n > 0) {
@@ -85,18 +115,8 @@ apo_status apo_ingest(apo_history *h, const uint64_t *d_tokens, int64_t n, apo_s
     }
     c.launches++;
   }
-  // ShouldAnalyzeHistory / GetAnalysisSubset (reading R13)
-  i64 ns = 0;
-  const i64 k0 = h->count, k1 = h->count + n;
-  for (i64 k = (k0 / h->C + 1) * h->C; k <= k1; k += h->C) {
-    i64 len = (i64(1) << ruler(k / h->C)) * h->C;
-    if (len > h->B || len <= 0) len = h->B;
-    if (ns < cap) h_slices[ns] = apo_slice{k - len, k};
-    ++ns;
-  }
   h->count = k1;
-  if (h_nslices) *h_nslices = ns;
-  return ns > cap ? APO_ERR_CAPACITY : APO_OK;
+  return APO_OK;
 }
 
 apo_status apo_history_window(apo_history *h, int64_t begin, int64_t end, uint64_t *d_out, void *stream) {

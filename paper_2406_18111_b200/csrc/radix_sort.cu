@@ -278,12 +278,7 @@ void launch_pass(Ctx &c, const K *kin, K *kout, const V *vin, V *vout, i64 n, in
   constexpr bool HAS_V = !std::is_same<V, NoVal>::value;
   constexpr int RADIX = 1 << BITS;
   const size_t smem = (sizeof(K) + (HAS_V ? sizeof(V) : 0)) * kSortTile + sizeof(u32) * kSortWarps * RADIX;
-  static bool attr_set = false;
-  if (!attr_set) {
-    APO_CUDA(cudaFuncSetAttribute(k_onesweep<K, V, BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  int(smem)));
-    attr_set = true;
-  }
+  c.smem_optin(reinterpret_cast<const void *>(k_onesweep<K, V, BITS>), smem);
   const i64 tiles = (n + kSortTile - 1) / kSortTile;
   c.ensure_status(size_t(tiles) * RADIX, s);
   u32 *ctr = c.take_counter(s);

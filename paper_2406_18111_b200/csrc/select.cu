@@ -728,11 +728,7 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
   const u64 *v1 = w.v1;
   if (b.W > 1 && bl <= 14) {  // windows <= 16,384 ops: per-window two-pass sort (7 + 7 bits)
     const size_t ssm = size_t(kSegTile) * (sizeof(u64) + sizeof(u32));
-    static bool sattr = false;
-    if (!sattr) {
-      APO_CUDA(cudaFuncSetAttribute(k_seg_sort1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ssm)));
-      sattr = true;
-    }
+    c.smem_optin(reinterpret_cast<const void *>(k_seg_sort1), ssm);
     k_seg_sort1<<<b.W, kSegThreads, ssm, s>>>(b, w.k1, w.v1, w.k1_alt, w.v1_alt, m, bl, (1u << bl) - 1u);
     APO_CHECK_LAUNCH();
     c.launches++;

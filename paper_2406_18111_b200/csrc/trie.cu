@@ -128,9 +128,12 @@ __global__ void k_trace_heads(const u64 *__restrict__ tok, const i64 *__restrict
   i64 a = order[c - 1], b = order[c];
   i64 la = off[a + 1] - off[a], lb = off[b + 1] - off[b];
   bool same = la == lb;
-  for (i64 k = lane; same && k < la; k += 32) {
-    bool eq = tok[off[a] + k] == tok[off[b] + k];
-    same = __all_sync(__activemask(), eq);
+  // warp-uniform trip count (c, la and same are uniform across the warp), so
+  // every lane takes part in every vote
+  for (i64 k0 = 0; same && k0 < la; k0 += 32) {
+    const i64 k = k0 + lane;
+    const bool eq = k >= la || tok[off[a] + k] == tok[off[b] + k];
+    same = __all_sync(0xffffffffu, eq);
   }
   same = __shfl_sync(0xffffffffu, same ? 1 : 0, 0) != 0;
   if (lane == 0) head[c] = same ? 0u : 1u;
@@ -1290,7 +1293,10 @@ __global__ void k_dup_keep(const u64 *__restrict__ tok, const i64 *__restrict__ 
   const u32 a = order[c - 1], b = order[c];
   const i64 la = off[a + 1] - off[a], lb = off[b + 1] - off[b];
   bool same = la == lb && hk[a] == hk[b];
-  for (i64 k = lane; same && k < la; k += 32) same = __all_sync(__activemask(), tok[off[a] + k] == tok[off[b] + k]);
+  for (i64 k0 = 0; same && k0 < la; k0 += 32) {  // warp-uniform trip count: every lane votes
+    const i64 k = k0 + lane;
+    same = __all_sync(0xffffffffu, k >= la || tok[off[a] + k] == tok[off[b] + k]);
+  }
   same = __shfl_sync(0xffffffffu, same ? 1 : 0, 0) != 0;
   if (lane == 0) keep[c] = same ? 0u : 1u;
 }
@@ -1744,6 +1750,8 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
       PairBaseF pf{ecnt, pbase, T, scal + 1};
       launch_scan<false>(c, T, pf, s);
       const i64 P = i64(c.read_u64(reinterpret_cast<const u64 *>(scal + 1), s));
+      void *spill = nullptr;  // pooled spill block of the pair tables (see below)
+      size_t spill_bytes = 0;
       // exact filter; fall back to the generalized SA when the pairs explode
       // (e.g. a tiny alphabet where every trace's first token is everywhere)
       if (P <= std::max<i64>(Ns / 4, 4 * T)) {
@@ -1827,11 +1835,7 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             const bool as = radix_sort_u64_u32(c, sk, sv, sk_alt, sv_alt, nstreams, 0, bits_for(u64(T)), s);
             const u32 *qorder = as ? sv_alt : sv;
             const size_t smem = sizeof(u64) * kSMMax + 2 * sizeof(unsigned short) * kSMMax;
-            static bool attr = false;
-            if (!attr) {
-              APO_CUDA(cudaFuncSetAttribute(k_stream_match, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-              attr = true;
-            }
+            c.smem_optin(reinterpret_cast<const void *>(k_stream_match), smem);
             if (c.prof) c.prof_begin(kProfMatch, 0.0, s);
             k_stream_match<<<nstreams, kSMThreads, smem, s>>>(sm, sqv, qoff, pair_e, ptr, e_lo, e_hi, ilo, icnt,
                                                               qtot, qorder);
@@ -1863,12 +1867,7 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
               APO_CHECK_LAUNCH();
               c.launches++;
               const size_t esmem = sizeof(u32) * (kSMMax + 3 * kEmitPairs) + sizeof(unsigned short) * kSMMax;
-              static bool eattr = false;
-              if (!eattr) {
-                APO_CUDA(cudaFuncSetAttribute(k_stream_emit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              int(esmem)));
-                eattr = true;
-              }
+              c.smem_optin(reinterpret_cast<const void *>(k_stream_emit), esmem);
               const bool pair32 = (reinterpret_cast<uintptr_t>(d_out) & 31) == 0;
               k_stream_emit<<<nstreams, kEmitThreads, esmem, s>>>(sm, stk, tof, qbase, cap, d_out, qorder, gpar, otr,
                                                                   gdep, pair32);
@@ -1899,9 +1898,19 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             // reserve() keeps nothing, so re-carve the pair tables first)
             const size_t need = cx.off + 256 + sizeof(u64) * size_t(nh) * 2;
             if (need > c.aux.cap) {
-              // move the pair tables aside in the main arena's key buffers
+              // move the pair tables aside: into the main arena's key buffers
+              // when they fit (P <= Ns), else into a pooled block that is
+              // returned once the enumeration is enqueued (later users of the
+              // pool run on the same stream, after it)
               i64 *ilo2 = reinterpret_cast<i64 *>(e_tok);
               u32 *hb2 = e_lo, *pt2 = e_q;
+              if (P > Ns) {
+                spill_bytes = (sizeof(i64) + 2 * sizeof(u32)) * size_t(P) + 256;
+                spill = c.pool_get(spill_bytes);
+                ilo2 = reinterpret_cast<i64 *>(spill);
+                hb2 = reinterpret_cast<u32 *>(ilo2 + P);
+                pt2 = hb2 + P;
+              }
               APO_CUDA(cudaMemcpyAsync(ilo2, ilo, sizeof(i64) * P, cudaMemcpyDeviceToDevice, s));
               APO_CUDA(cudaMemcpyAsync(hb2, hbase, sizeof(u32) * P, cudaMemcpyDeviceToDevice, s));
               APO_CUDA(cudaMemcpyAsync(pt2, ptr, sizeof(u32) * P, cudaMemcpyDeviceToDevice, s));
@@ -1917,6 +1926,7 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
             k_enumerate_pairs<<<grid_for(P * 32, T256), T256, 0, s>>>(sm, ilo, hbase, ptr, P, nh, bE, bT, keys);
             APO_CHECK_LAUNCH();
             c.launches++;
+            if (spill) c.pool_put(spill, spill_bytes);
           }
           }
         }

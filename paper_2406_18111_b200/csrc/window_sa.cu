@@ -408,11 +408,7 @@ bool window_sa_supported(const Batch &b) { return !b.gen && b.maxwin <= kWMax; }
 
 void run_window_sa(Ctx &c, const Batch &b, SAWork &w, cudaStream_t s) {
   const size_t smem = sizeof(WinSmem);
-  static bool attr = false;
-  if (!attr) {
-    APO_CUDA(cudaFuncSetAttribute(k_window_sa, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
-  }
+  c.smem_optin(reinterpret_cast<const void *>(k_window_sa), smem);
   LevelPtrs lv{};
   for (int r = 0; r < w.max_levels && r < 40; ++r) lv.p[r] = w.levels[r];
   if (c.prof) c.prof_begin(kProfWindowSA, 0.0, s);

@@ -66,10 +66,16 @@ def test_product_does_not_import_oracle():
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).replace("no CPU", ""), f
 
 
-def test_ruler_slices_host_logic():
-    """apo_ingest's schedule is host logic; check it against the oracle's
-    ruler on CPU through a tiny C shim is not possible without a device, so
-    the GPU test covers it; here check the oracle and the header agree on
-    the documented closed form for B=8, C=1."""
+def test_ruler_slices_host_logic(lib):
+    """apo_ingest's schedule (apo_ruler_slices, pure host code in libapo) vs
+    the oracle's ruler (P:750-755 and R13) for several (C, B), split points
+    and start counts; no device needed."""
     import oracle
-    assert oracle.ruler_slices(0, 8, 1, 8)[-1] == (0, 8)
+    from paper_2406_18111_b200.apo import ruler_slices
+    assert ruler_slices(0, 4, 1, 8) == [(0, 1), (0, 2), (2, 3), (0, 4)]   # P:750-753: 1, 2, 1, 4
+    for C, B in ((1, 8), (250, 5000), (500, 5000), (256, 16384), (3, 7)):
+        for k0, n in ((0, 20000), (7, 1), (C * 5 - 1, 2), (12345, 9876)):
+            assert ruler_slices(k0, n, C, B) == oracle.ruler_slices(k0, k0 + n, C, B), (C, B, k0, n)
+    from paper_2406_18111_b200.apo import ApoError
+    with pytest.raises(ApoError):
+        ruler_slices(0, 10, 0, 8)

@@ -387,3 +387,55 @@ def test_traces_order_and_dedup():
     tok, off = oracle.traces_from_repeats([S, S], reps, 1)
     ts = [tuple(tok[off[i]:off[i + 1]].tolist()) for i in range(len(off) - 1)]
     assert ts == [tuple(b"abc"), tuple(b"xy")]
+
+
+# ------------------------------------- tier-1 pinned at full window size ----
+
+def test_tier0_vs_tier1_full_c4_windows():
+    """Tier-1 (the oracle every full-size GPU comparison uses) equals tier-0
+    (the literal Alg. 2) on 8 full 16,384-op C4 windows."""
+    tok, off, _, _ = gen.c4(seed=4, windows=8 * 64, with_streams=False)
+    for w in range(0, 8 * 64, 64 + 1):
+        S = tok[off[w]:off[w + 1]]
+        a = oracle.find_repeats(S, 25, tier=0)
+        b = oracle.find_repeats(S, 25, tier=1)
+        for k in ("sa", "lcp", "cand_len", "cand_start", "cand_id", "keep", "repeats", "occ"):
+            assert np.array_equal(a[k], b[k]), (w, k)
+
+
+def test_tier0_vs_tier1_c2_full():
+    """... and on the full 65,536-op C2 window (Fig. 1b aliasing, maxLCP
+    64,768: the deepest doubling among the single windows that tier 0 can
+    still finish, ~15 s)."""
+    S = gen.c2()
+    a = oracle.find_repeats(S, 25, tier=0)
+    b = oracle.find_repeats(S, 25, tier=1)
+    for k in ("sa", "lcp", "cand_len", "cand_start", "cand_id", "keep", "repeats", "occ"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_sort_and_id_threads_equal_single():
+    """The multi-threaded tier-1 sort (same comparator; chunk sorts + merge
+    tree) gives the single-thread result, for any thread count."""
+    cases = [gen.c1(), gen.c2()[:30000], gen.random_string(3, 5000, 3), gen.periodic(4, 7000, 31, 3, 0.01)]
+    for S in cases:
+        sa = oracle.sa_doubling(S)
+        lcp = oracle.lcp_kasai(S, sa)
+        for ml in (1, 25):
+            cl, cs = oracle.candidates(sa, lcp, ml)
+            want = oracle.sort_and_id_rmq(S, sa, lcp, cl, cs)
+            for t in (1, 2, 5, 16):
+                got = oracle.sort_and_id_rmq_mt(S, sa, lcp, cl, cs, t)
+                assert all(np.array_equal(x, y) for x, y in zip(want, got)), t
+
+
+def test_traces_numpy_equals_python():
+    """The numpy trace-set builder (used at full C4 size) equals the Python
+    tuple version (IngestCandidates; R15 chunking) for max_len 0/7/40."""
+    tok, off, _, _ = gen.c4(seed=9, windows=12, window=2048, templates=4, with_streams=False)
+    srcs = [tok[off[w]:off[w + 1]] for w in range(12)]
+    reps = [oracle.find_repeats(s, 5, tier=1)["repeats"] for s in srcs]
+    for ml in (0, 7, 40):
+        a = oracle.traces_from_repeats(srcs, reps, 5, ml)
+        b = oracle.traces_from_repeats_np(srcs, reps, 5, ml)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), ml
