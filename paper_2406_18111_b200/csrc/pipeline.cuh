@@ -41,6 +41,7 @@ struct SAWork {
   int max_levels;
   i32 *phi, *plcp;        // N
   i32 *rw;                // W: rounds per window (K9 path) or nullptr
+  void *win_scratch;      // K9: per-CTA level scratch (L2-resident), or nullptr
   u32 *ids;               // N dense token ids (K2 hash path)
   bool ids_valid;
   char *ht_scratch;       // hash-table scratch of dense_token_ids
@@ -57,9 +58,13 @@ void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp);
 // the distinct count exceeds cap / 2.
 size_t token_ids_scratch_bytes(i64 n, u32 cap);
 i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scratch, cudaStream_t s);
-// K9: per-window on-chip doubling (windows <= 16,384 ops, not generalized).
+// K9: per-window on-chip suffix array + LCP (windows <= 16,384 ops, not
+// generalized): persistent CTAs (at most kWindowSACtasMax), each with its own
+// level scratch of window_sa_scratch_bytes(b) / CTAs bytes.
+constexpr int kWindowSACtasMax = 256;
 bool window_sa_supported(const Batch &b);
-void run_window_sa(Ctx &c, const Batch &b, SAWork &w, cudaStream_t s);
+size_t window_sa_scratch_bytes(const Batch &b);
+void run_window_sa(Ctx &c, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s);
 void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s);
 
 // ----- candidate generation, ordering, greedy, output (K5-K8) -----

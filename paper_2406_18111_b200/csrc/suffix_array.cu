@@ -236,19 +236,23 @@ void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp) {
   w.vals = cv.take<u32>(N);
   w.vals_alt = cv.take<u32>(N);
   w.tok_sorted = b.W > 1 ? cv.take<u64>(N) : nullptr;
-  w.max_levels = bits_for(u64(b.maxwin > 1 ? b.maxwin - 1 : 1)) + 2;
+  const bool k9 = window_sa_supported(b);
+  // K9 keeps its rank levels on chip / in a per-CTA L2 scratch: only level 0
+  // (the fallback initial ranking) is a per-position array there
+  w.max_levels = k9 ? 1 : bits_for(u64(b.maxwin > 1 ? b.maxwin - 1 : 1)) + 2;
   if (w.max_levels > 40) w.max_levels = 40;
   for (int r = 0; r < w.max_levels; ++r) w.levels[r] = cv.take<i32>(N);
   w.sa = cv.take<i32>(N);
-  w.rw = window_sa_supported(b) ? cv.take<i32>(size_t(b.W)) : nullptr;
+  w.rw = k9 ? cv.take<i32>(size_t(b.W)) : nullptr;
+  w.win_scratch = k9 ? cv.take<char>(window_sa_scratch_bytes(b)) : nullptr;
   w.ids = cv.take<u32>(N);
   w.ids_valid = false;
   w.ht_cap = 1u << 21;  // up to 1M distinct tokens; 24 MB of L2-friendly tables
   while (w.ht_cap > 4096 && u64(w.ht_cap) > 4 * u64(N)) w.ht_cap >>= 1;
   w.ht_scratch = cv.take<char>(token_ids_scratch_bytes(N, w.ht_cap));
   if (want_lcp) {
-    w.phi = cv.take<i32>(N);
-    w.plcp = cv.take<i32>(N);
+    w.phi = k9 ? nullptr : cv.take<i32>(N);
+    w.plcp = k9 ? nullptr : cv.take<i32>(N);
     w.lcp = cv.take<i32>(N);
   } else {
     w.phi = w.plcp = w.lcp = nullptr;
@@ -322,9 +326,9 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   }
 
   if (w.rw != nullptr) {
-    // ---- K9: every window's doubling loop on chip ----
-    run_window_sa(c, b, w, s);
-    w.R = w.max_levels - 1;  // upper bound; the LCP stage uses the per-window count
+    // ---- K9: every window's suffix array and LCP array on chip ----
+    run_window_sa(c, b, w, want_lcp, s);
+    return;
   } else {
   // ---- K3: doubling rounds ----
   const int lob = b.gen ? bits_for(u64(N - 1) + u64(b.W)) : bits_for(u64(b.maxwin));

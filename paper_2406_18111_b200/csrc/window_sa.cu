@@ -1,47 +1,88 @@
-// window_sa.cu -- K9: prefix doubling of one window per CTA, on chip.
+// window_sa.cu -- K9: suffix array AND LCP array of one window per CTA, on chip.
 //
-// For batches whose windows hold <= 16,384 ops (the C4 workload, and every
-// small single window) the whole doubling loop of a window runs inside one
-// 1024-thread CTA.  Per round:
-//   * keys (rank[i] << bg | (i+h < n ? rank[i+h]+1 : 0)) and positions are
-//     built from the u16 DENSE group ids held in shared memory; with G
-//     groups a key needs bits(G-1) + bits(G) bits, and loop-shaped windows
-//     keep G small for many rounds, so a round takes 2-4 passes, not 4;
-//   * stable 8-bit LSD digit passes move (key u32, position u16) between two
-//     shared-memory buffers: each warp ranks its 512 items (peer masks from
-//     ballots) into a per-warp u16 histogram, one block scan gives the digit
-//     starts, and every item is scattered to its slot;
-//   * a block-wide sum-scan of group heads gives the new dense ids;
-//   * the new level is streamed to HBM (4 B/op) for the LCP stage's galloping.
-// The loop ends per window as soon as all its ranks are distinct.  HBM
-// traffic per round is the level write only, instead of ~140 B/op for a
-// round of the global onesweep path.  The result is the same suffix array
-// (it is unique).
+// "SA, LCP <- SuffixArray(S)" (Alg. 2; "linear time algorithms
+// exist for suffix array and LCP array construction") for every window
+// of <= 16,384 ops of a batch (the C4 workload, the matcher's reversed
+// streams, every small single window).  One persistent 1,024-thread CTA per
+// SM takes windows from an atomic counter; the whole window lives in ~225 KB
+// of shared memory.
+//
+// Suffix array: prefix doubling in the Manber-Myers formulation.  Ranks are
+// Larsson-Sadakane style: rank[i] = sorted index of the first suffix of i's
+// group (equal first h tokens).  If the suffixes are in an order sorted by
+// their first h tokens (X), then walking that order and emitting i = X[q] - h
+// lists every suffix i sorted by its SECOND key rank[i+h]; a STABLE sort of
+// that list by the FIRST key rank[i] therefore orders the suffixes by their
+// first 2h tokens.  So a round sorts by the group alone, never by a
+// (rank, rank) pair: half the key bits.  Better still, only groups with more
+// than one member can change: a round's sort key is the ordinal k of the
+// item's NON-SINGLETON group (loop-shaped windows keep a few dozen to a few
+// thousand of them while thousands of groups are already singletons), so a
+// round is ONE stable LSD pass of bits(NS) <= 8 bits in most rounds (two
+// otherwise); singleton items keep their slot.  Suffixes i >= n - h (second
+// key "end of string") are singletons at level h and take the slots of the
+// suffixes j < h, which have no predecessor i = j - h.
+//
+// A pass ranks 512 items per warp with ballot-derived peer masks into a
+// per-warp u16 digit histogram, one block scan gives digit starts, and items
+// are scattered; the last pass of a round scatters straight to the item's new
+// slot (group start of its non-singleton group + rank inside it).  Group
+// heads of the new order compare (rank[i], rank[i+h]) of neighbours, a ballot
+// per row of 32 slots, and the new ranks, non-singleton ordinals and group
+// offsets come from popc prefix sums.
+//
+// Each level's ranks (u16) go to a per-CTA scratch in global memory that the
+// CTA rewrites window after window (L2-resident: ~448 KB per SM), never to a
+// per-position HBM array.  LCP: Kasai's bound PLCP[i] >= PLCP[i-1] - 1 over
+// chunks of 16 consecutive positions per thread, direct comparison of the
+// level-0 ranks (equal <=> equal tokens) in shared memory for up to 16 steps,
+// galloping over the saved levels (equal level-r ranks <=> equal 2^r-token
+// prefixes) for the chunk's first position and after long extensions.  The
+// CTA writes only the suffix array and the LCP array to HBM.
+//
+// The result is the unique suffix array and its LCP array; the per-window
+// arithmetic is exact integer arithmetic.
 #include "pipeline.cuh"
 
 namespace apo {
 
 namespace {
 
+using u16 = unsigned short;
+
 constexpr int kWT = 1024;
 constexpr int kWWarps = kWT / 32;
-constexpr int kWItems = 16;
+constexpr int kWItems = 16;           // slots per thread
 constexpr int kWMax = kWT * kWItems;  // 16384
+constexpr int kLvlSlots = 14;         // levels 0..13 (level 14, all distinct, is never needed)
+constexpr int kMaxBits = 8;           // digit width cap: per-warp histograms of 256 u16 bins
+constexpr u16 kSingleton = 0xFFFFu;
 
-struct WinBuf {
-  u32 key[kWMax];
-  unsigned short pos[kWMax];
-};
-
-struct WinSmem {
-  WinBuf a, b;  // ping-pong; the u16 rank array aliases b.key while a holds the items
-  unsigned short hist[kWWarps][512];  // per-warp digit counts (digits of up to 9 bits)
-  unsigned short start[512];  // digit starts (<= 16,384)
+struct Smem {
+  u32 X[kWMax];          // item buffer (sorted order: low 16 bits = position)
+  u32 Y[kWMax];          // item buffer
+  u16 rank[kWMax];       // rank[i] = sorted index of the first member of i's group
+  u16 nsk[kWMax];        // at a group start: ordinal of the non-singleton group, kSingleton otherwise
+  u16 delta[kWMax / 2];  // per non-singleton group k: number of singleton slots before its start
+  union {
+    u16 hist[kWWarps][1 << kMaxBits];  // LSD pass: per-warp digit counts
+    u32 bits[kWMax / 32];              // group phase: one head bit per slot
+  } u;
+  u16 start[1 << kMaxBits];  // digit starts of a pass
+  u32 wsum[kWWarps][2];      // per-warp (non-singleton heads, singleton slots)
+  int wlast[kWWarps];        // per-warp last head slot (-1 none)
   u32 scan[kWWarps];
+  int misc[4];
 };
+
+__device__ __forceinline__ u32 lanemask_lt() {
+  u32 m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
 
 template <int BITS>
-__device__ __forceinline__ u32 peers_ballot_w(u32 d) {
+__device__ __forceinline__ u32 peers_of(u32 d) {
   u32 peers = 0xffffffffu;
 #pragma unroll
   for (int b = 0; b < BITS; ++b) {
@@ -52,39 +93,28 @@ __device__ __forceinline__ u32 peers_ballot_w(u32 d) {
   return peers;
 }
 
-__device__ __forceinline__ u32 lanemask_lt_w() {
-  u32 m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
-// One stable LSD digit pass: items of `src` (sorted position q = index) go to
-// `dst`.  Warp w ranks the contiguous sub-tile [w*512, w*512+512) in
-// (j, lane) order, which is index order, so the pass is stable.
-template <int SHIFT, int BITS>
-__device__ __forceinline__ void lsd_pass(const WinBuf &src, WinBuf &dst, WinSmem &S) {
+// One stable LSD digit pass over all kWMax slots.  Warp w ranks the slots
+// [512w, 512w + 512) in (row, lane) order, which is slot order, so the pass is
+// stable.  digit(q): the item's digit; move(q, p): put slot q's item at rank p.
+template <int BITS, class DigitF, class MoveF>
+__device__ __forceinline__ void lsd_pass(Smem &S, DigitF digit, MoveF move) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int RADIX = 1 << BITS;
-  constexpr u32 mask = RADIX - 1u;
-  unsigned short *wh = S.hist[warp];
-  {  // each warp clears its own histogram row (the previous pass ended with a barrier)
-    u32 *row = reinterpret_cast<u32 *>(wh);
-#pragma unroll
-    for (int i = lane; i < RADIX / 2; i += 32) row[i] = 0;
-    __syncwarp();
-  }
-  const u32 lt = lanemask_lt_w();
+  u16 *wh = S.u.hist[warp];
+  for (int i = lane; i < (RADIX + 1) / 2; i += 32) reinterpret_cast<u32 *>(wh)[i] = 0;
+  __syncwarp();
+  const u32 lt = lanemask_lt();
   const int base = warp * (32 * kWItems) + lane;
   u32 rk[kWItems / 2];  // two u16 in-warp ranks per register
 #pragma unroll
   for (int j = 0; j < kWItems; ++j) {
-    u32 d = (src.key[base + j * 32] >> SHIFT) & mask;
-    u32 peers = peers_ballot_w<BITS>(d);
-    u32 old = wh[d];
+    const u32 d = digit(base + j * 32);
+    const u32 peers = peers_of<BITS>(d);
+    const u32 old = wh[d];
     __syncwarp();
-    if (lane == __ffs(peers) - 1) wh[d] = (unsigned short)(old + __popc(peers));
+    if (lane == __ffs(peers) - 1) wh[d] = u16(old + __popc(peers));
     __syncwarp();
-    u32 r = old + __popc(peers & lt);
+    const u32 r = old + __popc(peers & lt);
     if (j & 1)
       rk[j >> 1] |= r << 16;
     else
@@ -96,309 +126,331 @@ __device__ __forceinline__ void lsd_pass(const WinBuf &src, WinBuf &dst, WinSmem
   if (tid < RADIX) {
 #pragma unroll 8
     for (int w = 0; w < kWWarps; ++w) {
-      u32 c = S.hist[w][tid];
-      S.hist[w][tid] = (unsigned short)total;
+      const u32 c = S.u.hist[w][tid];
+      S.u.hist[w][tid] = u16(total);
       total += c;
     }
   }
   u32 incl = total;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    u32 v = __shfl_up_sync(0xffffffffu, incl, o);
+    const u32 v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;
   }
-  if (tid < RADIX && lane == 31) S.scan[warp] = incl;
+  if (tid < RADIX && lane == 31) S.scan[warp] = incl;  // (RADIX < 32: warp 0 alone, no prefix needed)
   __syncthreads();
   if (tid < RADIX) {
     u32 pre = 0;
     for (int w = 0; w < warp; ++w) pre += S.scan[w];
-    S.start[tid] = (unsigned short)(pre + incl - total);
+    S.start[tid] = u16(pre + incl - total);
   }
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kWItems; ++j) {
     const int q = base + j * 32;
-    u32 k = src.key[q];
-    u32 d = (k >> SHIFT) & mask;
-    u32 r = (rk[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
-    u32 p = u32(S.start[d]) + wh[d] + r;
-    dst.key[p] = k;
-    dst.pos[p] = src.pos[q];
+    const u32 d = digit(q);
+    const u32 r = (rk[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+    move(q, u32(S.start[d]) + wh[d] + r);
   }
   __syncthreads();
 }
 
-// Sort the items of buffer X (keys, positions) with NP stable LSD passes of
-// W-bit digits (the sorted items end in X for even NP, in Y for odd NP).
-template <int NP, int W>
-__device__ __forceinline__ void lsd_passes(WinBuf &X, WinBuf &Y, WinSmem &S) {
-  lsd_pass<0, W>(X, Y, S);
-  if constexpr (NP >= 2) lsd_pass<W, W>(Y, X, S);
-  if constexpr (NP >= 3) lsd_pass<2 * W, W>(X, Y, S);
-  if constexpr (NP >= 4) lsd_pass<3 * W, W>(Y, X, S);
+template <class DigitF, class MoveF>
+__device__ __forceinline__ void lsd_pass_bits(int bits, Smem &S, DigitF digit, MoveF move) {
+  switch (bits) {
+    case 1: lsd_pass<1>(S, digit, move); break;
+    case 2: lsd_pass<2>(S, digit, move); break;
+    case 3: lsd_pass<3>(S, digit, move); break;
+    case 4: lsd_pass<4>(S, digit, move); break;
+    case 5: lsd_pass<5>(S, digit, move); break;
+    case 6: lsd_pass<6>(S, digit, move); break;
+    case 7: lsd_pass<7>(S, digit, move); break;
+    default: lsd_pass<8>(S, digit, move); break;
+  }
 }
 
-// Dense id of every sorted item's key group, stored at rank[pos], and the
-// sorted index of every group's first item at gstart[id] (gstart = rank +
-// kWMax: the upper half of the same key area).  Warp w owns the sorted items
-// [512w, 512w+512) and walks them in 16 rows of 32 consecutive items
-// (conflict-free shared-memory access): a row's group heads come from one
-// ballot, the running count from popc.  KeyAt(q) gives the key of sorted
-// item q.  Returns the number of groups among the first n items.
-template <class KeyAt>
-__device__ __forceinline__ u32 dense_rank_by(KeyAt key_at, const unsigned short *spos, unsigned short *rank, i64 n,
-                                             WinSmem &S) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wbase = warp * (32 * kWItems);
-  const u32 lt = lanemask_lt_w();
-  unsigned short *gstart = rank + kWMax;
-  // pass 1: heads of this warp's segment
-  u32 cnt = 0;
+// Group phase A: one head bit per sorted slot q < n (head(q) = q starts a group).
+template <class HeadF>
+__device__ __forceinline__ void heads_phase(Smem &S, int n, HeadF head) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll 4
   for (int j = 0; j < kWItems; ++j) {
-    const int q = wbase + j * 32 + lane;
-    const u32 k = q < n ? key_at(q) : 0u;
-    const u32 pk = (q > 0 && q < n) ? key_at(q - 1) : 0xffffffffu;
-    cnt += __popc(__ballot_sync(0xffffffffu, k != pk && q < n));
+    const int q = warp * (32 * kWItems) + j * 32 + lane;
+    const bool h = q < n && head(q);
+    const u32 b = __ballot_sync(0xffffffffu, h);
+    if (lane == 0) S.u.bits[warp * kWItems + j] = b;
   }
-  if (lane == 0) S.scan[warp] = cnt;
   __syncthreads();
-  u32 before = 0, total = 0;
-  for (int ww = 0; ww < kWWarps; ++ww) {
-    const u32 v = S.scan[ww];
-    if (ww < warp) before += v;
-    total += v;
-  }
-  // pass 2: ids
-  u32 run = before;  // heads before the current row
+}
+
+// Group phases B + C: from the head bits and the sorted order ord (low 16
+// bits = position), the new ranks rank[ord[q]] = last head <= q, the non-singleton
+// ordinals at group starts (nsk) and each non-singleton group's number of
+// singleton slots before it (delta).  Returns NS, the number of
+// non-singleton groups.
+__device__ __forceinline__ int groups_phase(Smem &S, const u32 *ord, int n) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const u32 lt = lanemask_lt();
+  const u32 le = lt | (1u << lane);
+  auto next_head = [&](int q, u32 hb, int j) -> bool {  // head bit of slot q + 1 (1 past the end)
+    if (q + 1 >= n) return true;
+    if (lane < 31) return (hb >> (lane + 1)) & 1u;
+    return S.u.bits[warp * kWItems + j + 1] & 1u;  // first slot of the next row (or warp)
+  };
+  u32 cn = 0, cs = 0;
+  int last = -1;
 #pragma unroll 4
   for (int j = 0; j < kWItems; ++j) {
-    const int q = wbase + j * 32 + lane;
-    const u32 k = q < n ? key_at(q) : 0u;
-    const u32 pk = (q > 0 && q < n) ? key_at(q - 1) : 0xffffffffu;
-    const bool head = k != pk && q < n;
-    const u32 hb = __ballot_sync(0xffffffffu, head);
-    const u32 id = run + __popc(hb & lt) + ((hb >> lane) & 1u);  // heads up to and including q
-    if (q < n) rank[spos[q]] = (unsigned short)(id - 1);
-    if (head) gstart[id - 1] = (unsigned short)q;
-    run += __popc(hb);
+    const int q = warp * (32 * kWItems) + j * 32 + lane;
+    const u32 hb = S.u.bits[warp * kWItems + j];
+    const bool h = (hb >> lane) & 1u;
+    const bool nx = next_head(q, hb, j);
+    cs += __popc(__ballot_sync(0xffffffffu, h && nx));
+    cn += __popc(__ballot_sync(0xffffffffu, h && !nx));
+    if (hb) last = warp * (32 * kWItems) + j * 32 + 31 - __clz(hb);
+  }
+  if (lane == 0) {
+    S.wsum[warp][0] = cn;
+    S.wsum[warp][1] = cs;
+    S.wlast[warp] = last;
   }
   __syncthreads();
-  return total;
-}
-
-__device__ __forceinline__ u32 dense_rank(const WinBuf &sorted, unsigned short *rank, i64 n, WinSmem &S) {
-  return dense_rank_by([&](int q) { return sorted.key[q]; }, sorted.pos, rank, n, S);
-}
-
-// Largest group of the current ranking (group starts from dense_rank).
-__device__ __forceinline__ u32 max_group(const unsigned short *rank, u32 G, i64 n) {
-  __shared__ u32 s_mx;
-  if (threadIdx.x == 0) s_mx = 0;
-  __syncthreads();
-  const unsigned short *gstart = rank + kWMax;
-  u32 mx = 0;
-  for (u32 g = threadIdx.x; g < G; g += kWT) {
-    const u32 e = g + 1 < G ? u32(gstart[g + 1]) : u32(n);
-    mx = max(mx, e - u32(gstart[g]));
-  }
-  atomicMax(&s_mx, mx);
-  __syncthreads();
-  const u32 r = s_mx;
-  __syncthreads();
-  return r;
-}
-
-// One doubling round when every current group holds at most kSmallGroup (64)
-// items (late rounds of loop-shaped windows): the items are still in sorted
-// order of their current rank, so only each group's members need ordering by
-// rank[i + h]; an item's new sorted index is its group's start plus the
-// number of members ordered before it (by rank[i+h], ties by current index).
-// Reads sorted positions P.pos and ranks R.key; writes the new order to
-// R.pos, then the new ranks (and group starts) to P.key.  No LSD pass.
-constexpr u32 kSmallGroup = 64;
-
-__device__ __forceinline__ u32 small_group_round(WinBuf &P, WinBuf &R, u32 G, i64 n, i64 h, int bg, WinSmem &S) {
-  const unsigned short *rank = reinterpret_cast<const unsigned short *>(R.key);
-  const unsigned short *gstart = rank + kWMax;
-  auto r2 = [&](u32 p) -> u32 { return (i64(p) + h < n) ? u32(rank[p + h]) + 1u : 0u; };
-  u32 *R2 = P.key;  // second keys in current sorted order (P.key is free until the new ranks)
-  for (int q = threadIdx.x; q < n; q += kWT) R2[q] = r2(P.pos[q]);
-  __syncthreads();
-  for (int q = threadIdx.x; q < n; q += kWT) {
-    const u32 p = P.pos[q];
-    const u32 g = rank[p];
-    const u32 a = gstart[g], b = g + 1 < G ? u32(gstart[g + 1]) : u32(n);
-    u32 nq = u32(q);
-    if (b - a > 1) {
-      const u32 mine = R2[q];
-      u32 c = 0;
-      for (u32 j = a; j < b; ++j) {
-        const u32 o = R2[j];
-        c += (o < mine) || (o == mine && j < u32(q));
-      }
-      nq = a + c;
+  u32 nb = 0, sb = 0, NS = 0;
+  int carry = -1;
+  for (int w = 0; w < kWWarps; ++w) {
+    const u32 a = S.wsum[w][0], b = S.wsum[w][1];
+    if (w < warp) {
+      nb += a;
+      sb += b;
+      carry = max(carry, S.wlast[w]);
     }
-    R.pos[nq] = (unsigned short)p;
+    NS += a;
+  }
+#pragma unroll 4
+  for (int j = 0; j < kWItems; ++j) {
+    const int row = warp * (32 * kWItems) + j * 32;
+    const int q = row + lane;
+    const u32 hb = S.u.bits[warp * kWItems + j];
+    const bool h = (hb >> lane) & 1u;
+    const bool nx = next_head(q, hb, j);
+    const bool single = h && nx, nsh = h && !nx;
+    const u32 bn = __ballot_sync(0xffffffffu, nsh), bs = __ballot_sync(0xffffffffu, single);
+    if (nsh) {
+      const u32 k = nb + __popc(bn & lt);
+      S.nsk[q] = u16(k);
+      S.delta[k] = u16(sb + __popc(bs & lt));
+    }
+    if (single) S.nsk[q] = kSingleton;
+    const u32 hl = hb & le;
+    const int gs = hl ? row + 31 - __clz(hl) : carry;
+    if (q < n) S.rank[ord[q] & 0xffffu] = u16(gs);
+    nb += __popc(bn);
+    sb += __popc(bs);
+    if (hb) carry = row + 31 - __clz(hb);
   }
   __syncthreads();
-  unsigned short *nrank = reinterpret_cast<unsigned short *>(P.key);
-  return dense_rank_by([&](int q) {
-    const u32 p = R.pos[q];
-    return (u32(rank[p]) << bg) | r2(p);
-  }, R.pos, nrank, n, S);
+  return int(NS);
 }
 
-template <int NP, int W, bool XA>  // XA: items in S.a, other buffer S.b
-__device__ __forceinline__ void sort_round(WinSmem &S) {
-  if constexpr (XA)
-    lsd_passes<NP, W>(S.a, S.b, S);
-  else
-    lsd_passes<NP, W>(S.b, S.a, S);
+// Equal level-r ranks <=> equal 2^r-token prefixes: greedy descent over the
+// levels from a known lower bound l of lcp(i, j), valid because
+// lcp(i, j) - l < 2^R (level R is all distinct).
+__device__ __forceinline__ int gallop(const u16 *__restrict__ lv, int R, int n, int i, int j, int l) {
+  for (int r = R - 1; r >= 0; --r) {
+    if (i + l >= n || j + l >= n) break;
+    const u16 *L = lv + size_t(r) * kWMax;
+    if (__ldcg(L + i + l) == __ldcg(L + j + l)) l += 1 << r;
+  }
+  return l;
 }
 
-template <bool XA>
-__device__ __forceinline__ int sort_items_x(WinSmem &S, int bits) {
-  // fewest passes, 8-bit digits where that many passes suffice (8 ballots per
-  // item instead of 9): 8 | 9 | 16 | 18 | 24 | 27 | 32 bits
-  if (bits <= 8) { sort_round<1, 8, XA>(S); return 1; }
-  if (bits <= 9) { sort_round<1, 9, XA>(S); return 1; }
-  if (bits <= 16) { sort_round<2, 8, XA>(S); return 2; }
-  if (bits <= 18) { sort_round<2, 9, XA>(S); return 2; }
-  if (bits <= 24) { sort_round<3, 8, XA>(S); return 3; }
-  if (bits <= 27) { sort_round<3, 9, XA>(S); return 3; }
-  sort_round<4, 8, XA>(S);
-  return 4;
-}
+constexpr int kKasaiSteps = 16;
 
-// Sort the items (keys of `bits` significant bits) built in S.a (xa) or
-// S.b; returns the number of passes (odd: the items end in the other buffer)
-__device__ __forceinline__ int sort_items(WinSmem &S, int bits, bool xa) {
-  return xa ? sort_items_x<true>(S, bits) : sort_items_x<false>(S, bits);
-}
-
-// Algorithmic shared-memory traffic (profiling only): every LSD pass reads
-// and writes each item once (key 4 B + position 2 B, each way) and reads its
-// digit + updates a counter (8 B): 20 B per item per pass; building a round's
-// items reads two ranks and writes one item (10 B); the dense ranks read the
-// sorted item and write a rank (8 B).
-constexpr u64 kSmemPassBytes = 20, kSmemRoundBytes = 18;
-
-// ids: dense token ids (level 0 is computed here: window-local dense ranks
-// of the tokens), or nullptr to take level 0 from levels[0].
-__global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__restrict__ ids, LevelPtrs lv,
-                                                      int max_levels, i32 *__restrict__ sa_out,
-                                                      i32 *__restrict__ rw, unsigned long long *smem_bytes,
-                                                      i32 *__restrict__ phi_out) {
+// ids: global dense order-preserving token ids (K2), or nullptr: level 0
+// from level0 (global group starts of the (window, token) order).
+__global__ void __launch_bounds__(kWT, 1)
+    k_window_sa(Batch b, const u32 *__restrict__ ids, const i32 *__restrict__ level0, u16 *__restrict__ scratch,
+                u32 *__restrict__ next_win, i32 *__restrict__ sa_out, i32 *__restrict__ lcp_out,
+                i32 *__restrict__ rw) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WinSmem &S = *reinterpret_cast<WinSmem *>(smem_raw);
-  const int tid = threadIdx.x;
-  const int w = blockIdx.x;
-  const i64 beg = b_beg(b, w), n = b_end(b, w) - beg;
-  if (n == 0) {
-    if (tid == 0) rw[w] = 0;
-    return;
-  }
-  u64 prof = 0;
-  // The items of a round are built in buffer X and sorted with np passes;
-  // they end in X (np even) or in the other buffer.  The u16 ranks live in
-  // the key area of the buffer NOT holding the sorted items.
-  bool rank_in_b = true;  // ranks in S.b.key, items built in S.a
-  bool sorted_in_a = true;
-  u32 G;                 // number of distinct ranks
-  u32 maxg = 0xffffffffu;  // largest group (unknown: the first round sorts)
-  auto rank_ptr = [&]() { return reinterpret_cast<unsigned short *>(rank_in_b ? S.b.key : S.a.key); };
-  // ---- level 0 ----
-  if (ids != nullptr) {
-    __shared__ u32 s_max;
-    if (tid == 0) s_max = 0;
+  Smem &S = *reinterpret_cast<Smem *>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31;
+  u16 *lv = scratch + size_t(blockIdx.x) * kLvlSlots * kWMax;  // this CTA's level scratch
+  for (;;) {
+    if (tid == 0) S.misc[0] = int(atomicAdd(next_win, 1u));
     __syncthreads();
-    u32 mx = 0;
-    for (int q = tid; q < n; q += kWT) mx = max(mx, ids[beg + q]);
-    atomicMax(&s_max, mx);
+    const int w = S.misc[0];
     __syncthreads();
-    const int kb = bits_for(u64(s_max));
-    const u32 pad = 1u << kb;
-    for (int q = tid; q < kWMax; q += kWT) {  // items into S.a
-      S.a.key[q] = q < n ? ids[beg + q] : pad;
-      S.a.pos[q] = (unsigned short)q;
-    }
-    __syncthreads();
-    const int np = sort_items(S, kb + (n < kWMax ? 1 : 0), true);  // pad items need one more bit
-    sorted_in_a = (np & 1) == 0;
-    rank_in_b = sorted_in_a;
-    G = dense_rank(sorted_in_a ? S.a : S.b, rank_ptr(), n, S);
-    maxg = max_group(rank_ptr(), G, n);
-    prof += u64(n) * (kSmemPassBytes * np + kSmemRoundBytes);
-    unsigned short *rank = rank_ptr();
-    i32 *out = lv.p[0];
-    for (int i = tid; i < n; i += kWT) out[beg + i] = i32(rank[i]) + i32(beg);
-  } else {
-    const i32 *level0 = lv.p[0];
-    unsigned short *rank = rank_ptr();
-    for (int i = tid; i < n; i += kWT) rank[i] = (unsigned short)(level0[beg + i] - beg);
-    G = 0;  // unknown: group starts are < n
-    __syncthreads();
-  }
-  int r = 0;
-  for (i64 h = 1;; h <<= 1) {
-    if (G == u32(n)) {  // all distinct: the sorted buffer is the suffix array
-      const unsigned short *pos = sorted_in_a ? S.a.pos : S.b.pos;
-      for (int q = tid; q < n; q += kWT) {
-        sa_out[beg + q] = i32(beg) + i32(pos[q]);
-        // phi of the LCP stage (K4): the suffix ranked just before, -1 for the first
-        if (phi_out) phi_out[beg + pos[q]] = q > 0 ? i32(beg) + i32(pos[q - 1]) : -1;
+    if (w >= b.W) return;
+    const i64 beg = b_beg(b, w);
+    const int n = int(b_end(b, w) - beg);
+    if (n <= 1) {
+      if (n == 1 && tid == 0) {
+        sa_out[beg] = i32(beg);
+        if (lcp_out) lcp_out[beg] = 0;
       }
-      if (tid == 0) {
-        rw[w] = r;
-        if (smem_bytes) atomicAdd(smem_bytes, (unsigned long long)prof);
-      }
-      return;
+      if (tid == 0 && rw) rw[w] = 0;
+      continue;
     }
-    // key = rank[i] << bg | (i + h < n ? rank[i+h] + 1 : 0); ranks < G
-    const u32 gmax = G ? G : u32(n);
-    const int bg = bits_for(u64(gmax));
-    if (G && maxg <= kSmallGroup) {
-      // small groups only: order each group's members in place of a sort
-      WinBuf &P = sorted_in_a ? S.a : S.b, &R = sorted_in_a ? S.b : S.a;
-      G = small_group_round(P, R, G, n, h, bg, S);
-      sorted_in_a = !sorted_in_a;
-      rank_in_b = sorted_in_a;
-      prof += u64(n) * kSmemRoundBytes * 2;
-    } else {
-      const int kb = bits_for(u64(gmax - 1)) + bg;
-      const u32 pad = 1u << kb;
-      const unsigned short *rank = rank_ptr();
-      const bool xa = rank_in_b;  // items go to the buffer without the ranks
-      u32 *xk = xa ? S.a.key : S.b.key;
-      unsigned short *xp = xa ? S.a.pos : S.b.pos;
+    // ---------------- level 0: sort the window by token ----------------
+    if (ids != nullptr) {
+      // keys ping-pong X <-> Y, positions ping-pong rank <-> nsk
+      u32 mx = 0;
+      for (int q = tid; q < n; q += kWT) mx = max(mx, ids[beg + q]);
+      mx = __reduce_max_sync(0xffffffffu, mx);
+      if (tid == 0) S.misc[1] = 0;
+      __syncthreads();
+      if (lane == 0) atomicMax(reinterpret_cast<u32 *>(&S.misc[1]), mx);
+      __syncthreads();
+      const int kv = max(bits_for(u64(u32(S.misc[1]))), 1);
+      const int kb = kv + (n < kWMax ? 1 : 0);  // pad slots (key 2^kv, above every id) need one more bit
+      const u32 pad = 1u << kv;
       for (int q = tid; q < kWMax; q += kWT) {
-        u32 key = pad;
-        if (q < n) {
-          const u32 lo = (q + h < n) ? u32(rank[q + h]) + 1u : 0u;
-          key = (u32(rank[q]) << bg) | lo;
-        }
-        xk[q] = key;
-        xp[q] = (unsigned short)q;
+        S.X[q] = q < n ? ids[beg + q] : pad;
+        S.rank[q] = u16(q);
       }
       __syncthreads();
-      const int np = sort_items(S, kb + (n < kWMax ? 1 : 0), xa);  // pad items need one more bit
-      sorted_in_a = ((np & 1) == 0) == xa;
-      rank_in_b = sorted_in_a;
-      G = dense_rank(sorted_in_a ? S.a : S.b, rank_ptr(), n, S);
-      prof += u64(n) * (kSmemPassBytes * np + kSmemRoundBytes);
+      const int np = (kb + kMaxBits - 1) / kMaxBits;
+      const int bpp = (kb + np - 1) / np;
+      u32 *ks = S.X, *kd = S.Y;
+      u16 *ps = S.rank, *pd = S.nsk;
+      for (int p = 0; p < np; ++p) {
+        const int sh = p * bpp;
+        const u32 m = (1u << bpp) - 1u;
+        lsd_pass_bits(bpp, S, [&](int q) { return (ks[q] >> sh) & m; },
+                      [&](int q, u32 to) {
+                        kd[to] = ks[q];
+                        pd[to] = ps[q];
+                      });
+        u32 *t = ks; ks = kd; kd = t;
+        u16 *tp = ps; ps = pd; pd = tp;
+      }
+      heads_phase(S, n, [&](int q) { return q == 0 || ks[q] != ks[q - 1]; });
+      for (int q = tid; q < kWMax; q += kWT) S.X[q] = ps[q];  // sorted positions (pads: >= n, unused)
+      __syncthreads();
+    } else {
+      // level-0 group starts given: rank directly; slots by counting placement
+      u32 *cnt = S.Y;
+      for (int q = tid; q < kWMax; q += kWT) cnt[q] = 0;
+      __syncthreads();
+      for (int i = tid; i < n; i += kWT) {
+        const int g = int(level0[beg + i] - beg);
+        S.rank[i] = u16(g);
+        S.X[g + int(atomicAdd(&cnt[g], 1u))] = u32(i);
+      }
+      __syncthreads();
+      heads_phase(S, n, [&](int q) { return S.rank[S.X[q] & 0xffffu] == q; });
     }
-    unsigned short *nrank = rank_ptr();
-    maxg = max_group(nrank, G, n);
-    ++r;
-    if (r < max_levels) {
-      i32 *out = lv.p[r];
-      for (int i = tid; i < n; i += kWT) out[beg + i] = i32(nrank[i]) + i32(beg);
+    u32 *ord = S.X, *tmp = S.Y;  // ord: the current sorted order (low 16 bits = position)
+    int NS = groups_phase(S, ord, n);
+    // ---------------- doubling rounds ----------------
+    int r = 0;
+    while (NS > 0) {
+      // level r (prefix length h = 2^r) to the scratch for the LCP stage
+      {
+        const u32 *src = reinterpret_cast<const u32 *>(S.rank);
+        u32 *dst = reinterpret_cast<u32 *>(lv + size_t(r) * kWMax);
+        for (int q = tid; q < kWMax / 2; q += kWT) __stcg(dst + q, src[q]);
+      }
+      const int h = 1 << r;
+      // Manber-Myers order: slot q lists i = X[q] - h (suffixes sorted by
+      // their second key); the slots of j < h take the singletons i >= n - h.
+      // key = ordinal of i's non-singleton group, NS for singletons and pads
+      for (int q = tid; q < kWMax; q += kWT) {
+        u32 item = (u32(NS) << 16) | 0xffffu;
+        if (q < n) {
+          const int j = int(ord[q] & 0xffffu);
+          const int i = j >= h ? j - h : n - h + j;
+          const u16 k = S.nsk[S.rank[i]];
+          item = (u32(k == kSingleton ? NS : k) << 16) | u32(i);
+        }
+        tmp[q] = item;
+      }
+      __syncthreads();
+      const int kb = bits_for(u64(NS));
+      const int np = (kb + kMaxBits - 1) / kMaxBits;
+      const int bpp = (kb + np - 1) / np;
+      u32 *src = tmp, *dst = ord;
+      for (int p = 0; p < np; ++p) {
+        const int sh = 16 + p * bpp;
+        const u32 m = (1u << bpp) - 1u;
+        if (p + 1 < np) {
+          lsd_pass_bits(bpp, S, [&](int q) { return (src[q] >> sh) & m; },
+                        [&](int q, u32 to) { dst[to] = src[q]; });
+          u32 *t = src; src = dst; dst = t;
+        } else {
+          // last pass: scatter to the new slot.  Non-singleton group k's items
+          // come out contiguous in MM order; its slots start delta[k] later
+          // (the singleton slots before it); a singleton keeps its slot.
+          // (pads: position 0xffff, dropped)
+          lsd_pass_bits(bpp, S, [&](int q) { return (src[q] >> sh) & m; },
+                        [&](int q, u32 to) {
+                          const u32 v = src[q];
+                          const u32 k = v >> 16, i = v & 0xffffu;
+                          if (i == 0xffffu) return;
+                          const u32 at = k < u32(NS) ? to + S.delta[k] : u32(S.rank[i]);
+                          dst[at] = i;
+                        });
+          ord = dst;  // the new order (src's items are consumed)
+          tmp = src;
+        }
+      }
+      // heads of the new order: (rank[i], rank[i+h]) differs from the previous slot's
+      auto r2 = [&](int i) -> u32 { return i + h < n ? u32(S.rank[i + h]) + 1u : 0u; };
+      heads_phase(S, n, [&](int q) {
+        if (q == 0) return true;
+        const int i = int(ord[q] & 0xffffu), p = int(ord[q - 1] & 0xffffu);
+        return S.rank[i] != S.rank[p] || r2(i) != r2(p);
+      });
+      NS = groups_phase(S, ord, n);
+      ++r;
     }
-    if (r + 1 >= max_levels && G < u32(n)) {  // level budget exhausted (cannot happen for n <= 2^14)
-      if (tid == 0) rw[w] = -1;
-      return;
+    // ---------------- LCP (Kasai chunks + galloping over the levels) ----------------
+    // ord: suffix array (low 16 bits); rank: inverse suffix array; levels 0..r-1 in lv
+    u16 *tok0 = reinterpret_cast<u16 *>(tmp);  // level-0 ranks (equal <=> equal tokens)
+    u16 *lcps = tok0 + kWMax;                  // lcps[k] = LCP(SA[k], SA[k+1])
+    const int R = r;
+    if (lcp_out) {
+      if (R > 0) {
+        const u32 *src = reinterpret_cast<const u32 *>(lv);
+        u32 *dst = reinterpret_cast<u32 *>(tok0);
+        for (int q = tid; q < kWMax / 2; q += kWT) dst[q] = __ldcg(src + q);
+      }
+      __syncthreads();
+      const int i0 = tid * kWItems, i1 = min(i0 + kWItems, n);
+      int l = -1;
+      for (int i = i0; i < i1; ++i) {
+        const int q = S.rank[i];
+        if (q == 0) {
+          l = 0;
+          continue;
+        }
+        const int j = int(ord[q - 1] & 0xffffu);
+        if (R == 0) {
+          l = 0;  // all first tokens distinct
+        } else if (l < 0) {
+          l = gallop(lv, R, n, i, j, 0);
+        } else {
+          l = l > 0 ? l - 1 : 0;
+          int steps = 0;
+          while (i + l < n && j + l < n && tok0[i + l] == tok0[j + l]) {
+            ++l;
+            if (++steps == kKasaiSteps) {
+              l = gallop(lv, R, n, i, j, l);
+              break;
+            }
+          }
+        }
+        lcps[q - 1] = u16(l);
+      }
+      __syncthreads();
     }
+    for (int q = tid; q < n; q += kWT) {
+      sa_out[beg + q] = i32(beg) + i32(ord[q] & 0xffffu);
+      if (lcp_out) lcp_out[beg + q] = q + 1 < n ? i32(lcps[q]) : 0;
+    }
+    if (tid == 0 && rw) rw[w] = R;
+    __syncthreads();
   }
 }
 
@@ -406,15 +458,20 @@ __global__ void __launch_bounds__(kWT, 1) k_window_sa(Batch b, const u32 *__rest
 
 bool window_sa_supported(const Batch &b) { return !b.gen && b.maxwin <= kWMax; }
 
-void run_window_sa(Ctx &c, const Batch &b, SAWork &w, cudaStream_t s) {
-  const size_t smem = sizeof(WinSmem);
+size_t window_sa_scratch_bytes(const Batch &b) {
+  const i64 ctas = std::min<i64>(b.W, kWindowSACtasMax);
+  return size_t(ctas) * kLvlSlots * kWMax * sizeof(u16);
+}
+
+void run_window_sa(Ctx &c, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s) {
+  const size_t smem = sizeof(Smem);
   c.smem_optin(reinterpret_cast<const void *>(k_window_sa), smem);
-  LevelPtrs lv{};
-  for (int r = 0; r < w.max_levels && r < 40; ++r) lv.p[r] = w.levels[r];
+  const int grid = int(std::min<i64>(std::min<i64>(b.W, c.num_sms), kWindowSACtasMax));
+  u32 *ctr = c.take_counter(s);
   if (c.prof) c.prof_begin(kProfWindowSA, 0.0, s);
-  unsigned long long *cnt =
-      c.prof ? reinterpret_cast<unsigned long long *>(c.d_misc + kProfDevSlot + kProfWindowSA) : nullptr;
-  k_window_sa<<<b.W, kWT, smem, s>>>(b, w.ids_valid ? w.ids : nullptr, lv, w.max_levels, w.sa, w.rw, cnt, w.phi);
+  k_window_sa<<<grid, kWT, smem, s>>>(b, w.ids_valid ? w.ids : nullptr, w.levels[0],
+                                      reinterpret_cast<u16 *>(w.win_scratch), ctr, w.sa, want_lcp ? w.lcp : nullptr,
+                                      w.rw);
   APO_CHECK_LAUNCH();
   if (c.prof) c.prof_end(s);
   c.launches++;
