@@ -18,10 +18,11 @@
 // than one member can change: a round's sort key is the ordinal k of the
 // item's NON-SINGLETON group (loop-shaped windows keep a few dozen to a few
 // thousand of them while thousands of groups are already singletons), so a
-// round is ONE stable LSD pass of bits(NS) <= 8 bits in most rounds (two
-// otherwise); singleton items keep their slot.  Suffixes i >= n - h (second
-// key "end of string") are singletons at level h and take the slots of the
-// suffixes j < h, which have no predecessor i = j - h.
+// round is ONE stable LSD pass of bits(2 NS + 1) <= 8 bits in most rounds
+// (two otherwise); singleton items keep their slot.  Suffixes i >= n - h
+// (second key "end of string", the smallest) take the slots of the suffixes
+// j < h, which have no predecessor i = j - h; all but i = n - h are
+// singletons, and a low key bit of 0 puts i = n - h first in its group.
 //
 // A pass ranks 512 items per warp with ballot-derived peer masks into a
 // per-warp u16 digit histogram, one block scan gives digit starts, and items
@@ -346,6 +347,10 @@ __global__ void __launch_bounds__(kWT, 1)
     // ---------------- doubling rounds ----------------
     int r = 0;
     while (NS > 0) {
+      if (r >= kLvlSlots) {  // cannot happen for n <= 16,384 (see kLvlSlots)
+        if (tid == 0 && rw) rw[w] = -1;
+        break;
+      }
       // level r (prefix length h = 2^r) to the scratch for the LCP stage
       {
         const u32 *src = reinterpret_cast<const u32 *>(S.rank);
@@ -354,20 +359,26 @@ __global__ void __launch_bounds__(kWT, 1)
       }
       const int h = 1 << r;
       // Manber-Myers order: slot q lists i = X[q] - h (suffixes sorted by
-      // their second key); the slots of j < h take the singletons i >= n - h.
-      // key = ordinal of i's non-singleton group, NS for singletons and pads
+      // their second key); the slots of j < h take the suffixes i >= n - h,
+      // whose second key is "end of string", the smallest: they must precede
+      // every other member of their group (only i = n - h, exactly h tokens
+      // long, can share its group), so the key's low bit is 0 for them.
+      // key = 2 * ordinal of i's non-singleton group + that bit; 2 NS + 1 for
+      // singletons and pads (position 0xffff)
       for (int q = tid; q < kWMax; q += kWT) {
-        u32 item = (u32(NS) << 16) | 0xffffu;
+        u32 item = (u32(2 * NS + 1) << 16) | 0xffffu;
         if (q < n) {
           const int j = int(ord[q] & 0xffffu);
-          const int i = j >= h ? j - h : n - h + j;
+          const bool tail = j < h;
+          const int i = tail ? n - h + j : j - h;
           const u16 k = S.nsk[S.rank[i]];
-          item = (u32(k == kSingleton ? NS : k) << 16) | u32(i);
+          const u32 key = k == kSingleton ? u32(2 * NS + 1) : 2u * k + (tail ? 0u : 1u);
+          item = (key << 16) | u32(i);
         }
         tmp[q] = item;
       }
       __syncthreads();
-      const int kb = bits_for(u64(NS));
+      const int kb = bits_for(u64(2 * NS + 1));
       const int np = (kb + kMaxBits - 1) / kMaxBits;
       const int bpp = (kb + np - 1) / np;
       u32 *src = tmp, *dst = ord;
@@ -386,7 +397,7 @@ __global__ void __launch_bounds__(kWT, 1)
           lsd_pass_bits(bpp, S, [&](int q) { return (src[q] >> sh) & m; },
                         [&](int q, u32 to) {
                           const u32 v = src[q];
-                          const u32 k = v >> 16, i = v & 0xffffu;
+                          const u32 k = v >> 17, i = v & 0xffffu;
                           if (i == 0xffffu) return;
                           const u32 at = k < u32(NS) ? to + S.delta[k] : u32(S.rank[i]);
                           dst[at] = i;
