@@ -74,6 +74,8 @@ def _load():
                 "or_sort_and_id_rmq_mt": (None, [P_U64, I64, P_I32, P_I32, I64, P_I32, P_I32, P_I32, I32]),
                 "or_greedy_marks": (None, [I64, I64, P_I32, P_I32, P_U8]),
                 "or_match_brute": (I64, [P_U64, P_I64, I64, P_U64, P_I64, I64, P_I32, P_I32, P_I32, I64]),
+                "or_replay": (I64, [I64, P_I32, P_I32, P_I32, I64, P_I32, I32, I32, I32, I32, I32,
+                                    P_I32, P_I32, P_I32, P_I32, P_I32, I64]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(lib, name)
@@ -284,3 +286,26 @@ def match_brute(streams, st_off, traces_tok, tr_off, cap: int | None = None):
                              _p(a, P_I32), _p(b, P_I32), _p(c, P_I32), cap)
     k = min(cnt, cap)
     return np.stack([a[:k], b[:k], c[:k]], axis=1), cnt
+
+
+# REPLAY constants (P:694-713 names the mechanisms, not the values; SPEC's
+# declared defaults): count cap 100, decay 0.99 per 100 tasks (Q16:
+# round(0.99 * 65536) = 64881), replay bonus x 1.1 (11 / 10).
+REPLAY_DEFAULTS = dict(count_cap=100, decay_q16=64881, decay_period=100, bonus_num=11, bonus_den=10)
+
+
+def replay(hits, tlen, count_cap=100, decay_q16=64881, decay_period=100, bonus_num=11, bonus_den=10):
+    """REPLAY selection over MATCH_ALL hits (rows (stream, end, trace) sorted)
+    -> int32[r, 5] rows (stream, start, end, trace, first)."""
+    hits = np.ascontiguousarray(np.asarray(hits, dtype=np.int32).reshape(-1, 3))
+    hs, he, ht = (np.ascontiguousarray(hits[:, k]) for k in range(3))
+    tlen = np.ascontiguousarray(tlen, dtype=np.int32)
+    nh = len(hits)
+    cap = max(nh, 1)
+    out = [np.empty(cap, dtype=np.int32) for _ in range(5)]
+    n = 0
+    if nh:
+        n = _load().or_replay(nh, _p(hs, P_I32), _p(he, P_I32), _p(ht, P_I32), len(tlen), _p(tlen, P_I32),
+                              int(count_cap), int(decay_q16), int(decay_period), int(bonus_num), int(bonus_den),
+                              *[_p(o, P_I32) for o in out], cap)
+    return np.stack([o[:n] for o in out], axis=1) if n else np.zeros((0, 5), dtype=np.int32)

@@ -502,3 +502,88 @@ int64_t or_match_brute(const uint64_t *st, const int64_t *st_off, int64_t nstrea
     free(tlen); free(tlast);
     return cnt;
 }
+
+/* ======================================================================== */
+/* REPLAY selection (Alg. 1 SelectReplayTrace / ExecuteAndReplay,             */
+/* P:429-443; scoring P:694-713).  Readings R20-R24:              */
+/*  - input: every MATCH_ALL completion (stream, end, trace) of the stream,   */
+/*    sorted by (stream, end, trace); trace t has length tlen[t];             */
+/*  - "a count of the number of times the trace has appeared": appearances   */
+/*    = completions of t in this stream with end <= e (R21);                 */
+/*  - "impose a maximum value of the count": min(count, count_cap);          */
+/*  - "exponentially decay the value of the count by how many tasks have     */
+/*    been encountered since the trace last appeared": gap = e - end of the  */
+/*    previous appearance (0 at the first), factor decay^(gap / period) in   */
+/*    Q16 fixed point: d_0 = 65536, d_{k+1} = (d_k * decay_q16) >> 16 (R22); */
+/*  - "increase the score slightly if a trace has already been replayed":    */
+/*    score * bonus_num / bonus_den (integer division) (R22);               */
+/*    score = tlen * min(count, cap) * d_k, an unsigned 64-bit integer;      */
+/*  - at every end e, among completions whose start e - tlen + 1 is at or    */
+/*    after the first op not yet replayed (the "pending" tasks P), the one   */
+/*    with the highest score is replayed; ties: longer trace, then smaller   */
+/*    id (R23).  Replaying it executes the pending tasks before it, replays  */
+/*    it, and clears every pointer that started before its end (A), so the   */
+/*    next replay starts after it: replays never overlap (§3).    */
+/*  - out: per replay (stream, start, end, trace, first) with first = 1 the  */
+/*    first time the trace is replayed in this stream (a "record", SPEC's     */
+/*    record/replay distinction).  Returns the number of replays; only the   */
+/*    first cap are stored.                                                 */
+/* Plain per-stream sequential loop; per-trace state in calloc'ed arrays.    */
+/* ======================================================================== */
+int64_t or_replay(int64_t nh, const int32_t *h_stream, const int32_t *h_end, const int32_t *h_trace,
+                  int64_t ntraces, const int32_t *tlen, int32_t count_cap, int32_t decay_q16,
+                  int32_t decay_period, int32_t bonus_num, int32_t bonus_den,
+                  int32_t *r_stream, int32_t *r_start, int32_t *r_end, int32_t *r_trace, int32_t *r_first,
+                  int64_t cap) {
+    int64_t *count = (int64_t *)calloc((size_t)(ntraces ? ntraces : 1), sizeof(int64_t));
+    int64_t *last = (int64_t *)malloc(sizeof(int64_t) * (size_t)(ntraces ? ntraces : 1));
+    uint8_t *replayed = (uint8_t *)calloc((size_t)(ntraces ? ntraces : 1), 1);
+    int64_t nr = 0, i = 0;
+    while (i < nh) {
+        const int32_t q = h_stream[i];
+        int64_t j = i;
+        while (j < nh && h_stream[j] == q) j++;                /* [i, j): this stream's hits */
+        for (int64_t t = 0; t < ntraces; t++) { count[t] = 0; last[t] = -1; replayed[t] = 0; }
+        int64_t frontier = 0;                                   /* first op not yet replayed */
+        int64_t a = i;
+        while (a < j) {
+            const int64_t e = h_end[a];
+            int64_t b = a;
+            while (b < j && h_end[b] == e) b++;                 /* [a, b): completions at end e */
+            int64_t best = -1;
+            uint64_t best_s = 0;
+            for (int64_t k = a; k < b; k++) {
+                const int32_t t = h_trace[k];
+                const int64_t gap = last[t] < 0 ? 0 : e - last[t];
+                count[t] += 1;
+                last[t] = e;
+                const int64_t c = count[t] < count_cap ? count[t] : count_cap;
+                uint64_t d = 65536;
+                for (int64_t s = 0; s < gap / decay_period && d > 0; s++) d = (d * (uint64_t)decay_q16) >> 16;
+                uint64_t score = (uint64_t)tlen[t] * (uint64_t)c * d;
+                if (replayed[t]) score = score * (uint64_t)bonus_num / (uint64_t)bonus_den;
+                if (e - tlen[t] + 1 < frontier) continue;       /* pointer cleared by a replay */
+                if (best < 0 || score > best_s ||
+                    (score == best_s && (tlen[t] > tlen[h_trace[best]] ||
+                                         (tlen[t] == tlen[h_trace[best]] && t < h_trace[best])))) {
+                    best = k;
+                    best_s = score;
+                }
+            }
+            if (best >= 0) {
+                const int32_t t = h_trace[best];
+                if (nr < cap) {
+                    r_stream[nr] = q; r_start[nr] = (int32_t)(e - tlen[t] + 1); r_end[nr] = (int32_t)e;
+                    r_trace[nr] = t; r_first[nr] = replayed[t] ? 0 : 1;
+                }
+                nr++;
+                replayed[t] = 1;
+                frontier = e + 1;
+            }
+            a = b;
+        }
+        i = j;
+    }
+    free(count); free(last); free(replayed);
+    return nr;
+}

@@ -45,7 +45,29 @@
 // arithmetic is exact integer arithmetic.
 #include "pipeline.cuh"
 
+// Phase timing (diagnostics only; compiled out unless APO_K9_PHASES is 1):
+// thread 0 of every CTA adds clock64() deltas per phase to k9_phase_cycles.
+#ifndef APO_K9_PHASES
+#define APO_K9_PHASES 0
+#endif
+
 namespace apo {
+
+#if APO_K9_PHASES
+__device__ unsigned long long k9_phase_cycles[16];
+#define K9_T0() long long k9_t = clock64()
+#define K9_MARK(ph)                                                                    \
+  do {                                                                                 \
+    if (threadIdx.x == 0) {                                                            \
+      const long long k9_n = clock64();                                                \
+      atomicAdd(&k9_phase_cycles[ph], (unsigned long long)(k9_n - k9_t));               \
+      k9_t = k9_n;                                                                     \
+    }                                                                                  \
+  } while (0)
+#else
+#define K9_T0()
+#define K9_MARK(ph)
+#endif
 
 namespace {
 
@@ -293,6 +315,7 @@ __global__ void __launch_bounds__(kWT, 1)
       if (tid == 0 && rw) rw[w] = 0;
       continue;
     }
+    K9_T0();
     // ---------------- level 0: sort the window by token ----------------
     if (ids != nullptr) {
       // keys ping-pong X <-> Y, positions ping-pong rank <-> nsk
@@ -343,7 +366,9 @@ __global__ void __launch_bounds__(kWT, 1)
       heads_phase(S, n, [&](int q) { return S.rank[S.X[q] & 0xffffu] == q; });
     }
     u32 *ord = S.X, *tmp = S.Y;  // ord: the current sorted order (low 16 bits = position)
+    K9_MARK(0);
     int NS = groups_phase(S, ord, n);
+    K9_MARK(1);
     // ---------------- doubling rounds ----------------
     int r = 0;
     while (NS > 0) {
@@ -378,6 +403,7 @@ __global__ void __launch_bounds__(kWT, 1)
         tmp[q] = item;
       }
       __syncthreads();
+      K9_MARK(2);
       const int kb = bits_for(u64(2 * NS + 1));
       const int np = (kb + kMaxBits - 1) / kMaxBits;
       const int bpp = (kb + np - 1) / np;
@@ -406,6 +432,10 @@ __global__ void __launch_bounds__(kWT, 1)
           tmp = src;
         }
       }
+      K9_MARK(3);
+#if APO_K9_PHASES
+      if (threadIdx.x == 0) atomicAdd(&k9_phase_cycles[8 + np], 1ull);
+#endif
       // heads of the new order: (rank[i], rank[i+h]) differs from the previous slot's
       auto r2 = [&](int i) -> u32 { return i + h < n ? u32(S.rank[i + h]) + 1u : 0u; };
       heads_phase(S, n, [&](int q) {
@@ -413,7 +443,9 @@ __global__ void __launch_bounds__(kWT, 1)
         const int i = int(ord[q] & 0xffffu), p = int(ord[q - 1] & 0xffffu);
         return S.rank[i] != S.rank[p] || r2(i) != r2(p);
       });
+      K9_MARK(4);
       NS = groups_phase(S, ord, n);
+      K9_MARK(1);
       ++r;
     }
     // ---------------- LCP (Kasai chunks + galloping over the levels) ----------------
@@ -456,12 +488,14 @@ __global__ void __launch_bounds__(kWT, 1)
       }
       __syncthreads();
     }
+    K9_MARK(5);
     for (int q = tid; q < n; q += kWT) {
       sa_out[beg + q] = i32(beg) + i32(ord[q] & 0xffffu);
       if (lcp_out) lcp_out[beg + q] = q + 1 < n ? i32(lcps[q]) : 0;
     }
     if (tid == 0 && rw) rw[w] = R;
     __syncthreads();
+    K9_MARK(6);
   }
 }
 
@@ -489,3 +523,14 @@ void run_window_sa(Ctx &c, const Batch &b, SAWork &w, bool want_lcp, cudaStream_
 }
 
 }  // namespace apo
+
+#if APO_K9_PHASES
+extern "C" int apo_debug_k9_phases(unsigned long long *out, int reset) {
+  if (cudaMemcpyFromSymbol(out, apo::k9_phase_cycles, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(apo::k9_phase_cycles, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
