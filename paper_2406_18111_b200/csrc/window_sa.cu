@@ -87,16 +87,22 @@ struct Smem {
   u16 rank[kWMax];       // rank[i] = sorted index of the first member of i's group
   u16 nsk[kWMax];        // at a group start: ordinal of the non-singleton group, kSingleton otherwise
   u16 delta[kWMax / 2];  // per non-singleton group k: number of singleton slots before its start
+  u32 hbits[kWMax / 32]; // group-head bit of every slot of the current order
   union {
     u16 hist[kWWarps][1 << kMaxBits];  // LSD pass: per-warp digit counts
-    u32 bits[kWMax / 32];              // group phase: one head bit per slot
+    struct {
+      u32 sbits[kWMax / 32];  // group phase: singleton heads
+      u32 nbits[kWMax / 32];  // group phase: heads of non-singleton groups
+      u32 wsum[kWWarps][2];   // per-warp (non-singleton heads, singleton slots), then their exclusive prefix
+      int wlast[kWWarps];     // per-warp last head slot (-1 none), then the exclusive prefix max
+    } g;
   } u;
   u16 start[1 << kMaxBits];  // digit starts of a pass
-  u32 wsum[kWWarps][2];      // per-warp (non-singleton heads, singleton slots)
-  int wlast[kWWarps];        // per-warp last head slot (-1 none)
   u32 scan[kWWarps];
-  int misc[4];
+  u32 wfirst;                // head bit of the first slot of every warp's segment (bit w)
+  int misc[4];               // [0] window, [1] max id, [2] NS, [3] slot of suffix 0
 };
+static_assert(sizeof(Smem) <= 232448, "K9 shared memory exceeds the 227 KB opt-in limit");
 
 __device__ __forceinline__ u32 lanemask_lt() {
   u32 m;
@@ -192,87 +198,124 @@ __device__ __forceinline__ void lsd_pass_bits(int bits, Smem &S, DigitF digit, M
   }
 }
 
-// Group phase A: one head bit per sorted slot q < n (head(q) = q starts a group).
-template <class HeadF>
-__device__ __forceinline__ void heads_phase(Smem &S, int n, HeadF head) {
+// Group phase A: the group heads of the current order ord.  head(q) = q == 0,
+// or key(q) != key(q - 1), or (with OLD) q started a group before (the
+// previous head bits, still in hbits).  Per row of 32 slots: head bits,
+// singleton heads (a head followed by a head or the end) and non-singleton
+// heads, stored as bit rows; per warp: counts and the last head.
+template <bool OLD, class KeyF>
+__device__ __forceinline__ void heads_phase(Smem &S, int n, KeyF key) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll 4
-  for (int j = 0; j < kWItems; ++j) {
-    const int q = warp * (32 * kWItems) + j * 32 + lane;
-    const bool h = q < n && head(q);
-    const u32 b = __ballot_sync(0xffffffffu, h);
-    if (lane == 0) S.u.bits[warp * kWItems + j] = b;
+  const int wb = warp * (32 * kWItems);
+  // the first slot of the next warp's segment closes this warp's last row
+  bool nfirst = true;
+  {
+    const int qn = wb + 32 * kWItems;
+    if (qn < n) nfirst = (OLD && ((S.wfirst >> (warp + 1)) & 1u)) || key(qn) != key(qn - 1);
+  }
+  u32 prev_key = wb > 0 && wb < n ? key(wb - 1) : 0u;
+  u32 cn = 0, cs = 0;
+  int last = -1;
+  u32 hb_prev = 0;
+#pragma unroll 2
+  for (int j = 0; j <= kWItems; ++j) {
+    u32 hb = 0;
+    if (j < kWItems) {
+      const int q = wb + j * 32 + lane;
+      const u32 k = q < n ? key(q) : 0u;
+      u32 kp = __shfl_up_sync(0xffffffffu, k, 1);
+      if (lane == 0) kp = prev_key;
+      prev_key = __shfl_sync(0xffffffffu, k, 31);
+      bool h = q < n && (q == 0 || k != kp);
+      if (OLD && q < n) h = h || ((S.hbits[warp * kWItems + j] >> lane) & 1u);
+      hb = __ballot_sync(0xffffffffu, h);
+    }
+    if (j > 0) {  // classify row j - 1: its successor bits are known now
+      const int rb = wb + (j - 1) * 32;
+      const u32 nxt = j < kWItems ? (hb & 1u) : (nfirst ? 1u : 0u);
+      u32 nmask = (hb_prev >> 1) | (nxt << 31);
+      if (n - 1 >= rb && n - 1 < rb + 32) nmask |= 1u << ((n - 1) & 31);  // the last slot: end follows
+      const u32 single = hb_prev & nmask, nsh = hb_prev & ~nmask;
+      if (lane == 0) {
+        S.hbits[warp * kWItems + j - 1] = hb_prev;
+        S.u.g.sbits[warp * kWItems + j - 1] = single;
+        S.u.g.nbits[warp * kWItems + j - 1] = nsh;
+      }
+      cs += __popc(single);
+      cn += __popc(nsh);
+      if (hb_prev) last = rb + 31 - __clz(hb_prev);
+    }
+    hb_prev = hb;
+  }
+  if (lane == 0) {
+    S.u.g.wsum[warp][0] = cn;
+    S.u.g.wsum[warp][1] = cs;
+    S.u.g.wlast[warp] = last;
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive prefix over warps (sums; max for the last head)
+    const u32 a = S.u.g.wsum[lane][0], b = S.u.g.wsum[lane][1];
+    int l = S.u.g.wlast[lane];
+    u32 ia = a, ib = b;
+    int il = l;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 xa = __shfl_up_sync(0xffffffffu, ia, o), xb = __shfl_up_sync(0xffffffffu, ib, o);
+      const int xl = __shfl_up_sync(0xffffffffu, il, o);
+      if (lane >= o) {
+        ia += xa;
+        ib += xb;
+        il = max(il, xl);
+      }
+    }
+    const int el = __shfl_up_sync(0xffffffffu, il, 1);
+    S.u.g.wsum[lane][0] = ia - a;
+    S.u.g.wsum[lane][1] = ib - b;
+    S.u.g.wlast[lane] = lane ? el : -1;
+    if (lane == 31) S.misc[2] = int(ia);
+    const u32 fb = __ballot_sync(0xffffffffu, (S.hbits[lane * kWItems] & 1u) != 0u);
+    if (lane == 0) S.wfirst = fb;
   }
   __syncthreads();
 }
 
-// Group phases B + C: from the head bits and the sorted order ord (low 16
-// bits = position), the new ranks rank[ord[q]] = last head <= q, the non-singleton
-// ordinals at group starts (nsk) and each non-singleton group's number of
-// singleton slots before it (delta).  Returns NS, the number of
-// non-singleton groups.
+// Group phase C: from the bit rows, the new ranks rank[ord[q]] = last head
+// <= q, the non-singleton ordinals at group starts (nsk) and each
+// non-singleton group's number of singleton slots before it (delta); the
+// slot of suffix 0 goes to misc[3].  Returns NS, the number of non-singleton
+// groups.
 __device__ __forceinline__ int groups_phase(Smem &S, const u32 *ord, int n) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const u32 lt = lanemask_lt();
   const u32 le = lt | (1u << lane);
-  auto next_head = [&](int q, u32 hb, int j) -> bool {  // head bit of slot q + 1 (1 past the end)
-    if (q + 1 >= n) return true;
-    if (lane < 31) return (hb >> (lane + 1)) & 1u;
-    return S.u.bits[warp * kWItems + j + 1] & 1u;  // first slot of the next row (or warp)
-  };
-  u32 cn = 0, cs = 0;
-  int last = -1;
-#pragma unroll 4
-  for (int j = 0; j < kWItems; ++j) {
-    const int q = warp * (32 * kWItems) + j * 32 + lane;
-    const u32 hb = S.u.bits[warp * kWItems + j];
-    const bool h = (hb >> lane) & 1u;
-    const bool nx = next_head(q, hb, j);
-    cs += __popc(__ballot_sync(0xffffffffu, h && nx));
-    cn += __popc(__ballot_sync(0xffffffffu, h && !nx));
-    if (hb) last = warp * (32 * kWItems) + j * 32 + 31 - __clz(hb);
-  }
-  if (lane == 0) {
-    S.wsum[warp][0] = cn;
-    S.wsum[warp][1] = cs;
-    S.wlast[warp] = last;
-  }
-  __syncthreads();
-  u32 nb = 0, sb = 0, NS = 0;
-  int carry = -1;
-  for (int w = 0; w < kWWarps; ++w) {
-    const u32 a = S.wsum[w][0], b = S.wsum[w][1];
-    if (w < warp) {
-      nb += a;
-      sb += b;
-      carry = max(carry, S.wlast[w]);
-    }
-    NS += a;
-  }
+  u32 nb = S.u.g.wsum[warp][0], sb = S.u.g.wsum[warp][1];
+  int carry = S.u.g.wlast[warp];
 #pragma unroll 4
   for (int j = 0; j < kWItems; ++j) {
     const int row = warp * (32 * kWItems) + j * 32;
     const int q = row + lane;
-    const u32 hb = S.u.bits[warp * kWItems + j];
-    const bool h = (hb >> lane) & 1u;
-    const bool nx = next_head(q, hb, j);
-    const bool single = h && nx, nsh = h && !nx;
-    const u32 bn = __ballot_sync(0xffffffffu, nsh), bs = __ballot_sync(0xffffffffu, single);
-    if (nsh) {
+    const int rr = warp * kWItems + j;
+    const u32 hb = S.hbits[rr], bn = S.u.g.nbits[rr], bs = S.u.g.sbits[rr];
+    if ((bn >> lane) & 1u) {
       const u32 k = nb + __popc(bn & lt);
       S.nsk[q] = u16(k);
       S.delta[k] = u16(sb + __popc(bs & lt));
+    } else if ((bs >> lane) & 1u) {
+      S.nsk[q] = kSingleton;
     }
-    if (single) S.nsk[q] = kSingleton;
     const u32 hl = hb & le;
     const int gs = hl ? row + 31 - __clz(hl) : carry;
-    if (q < n) S.rank[ord[q] & 0xffffu] = u16(gs);
+    if (q < n) {
+      const u32 i = ord[q] & 0xffffu;
+      S.rank[i] = u16(gs);
+      if (i == 0) S.misc[3] = q;
+    }
     nb += __popc(bn);
     sb += __popc(bs);
     if (hb) carry = row + 31 - __clz(hb);
   }
   __syncthreads();
-  return int(NS);
+  return S.misc[2];
 }
 
 // Equal level-r ranks <=> equal 2^r-token prefixes: greedy descent over the
@@ -349,7 +392,7 @@ __global__ void __launch_bounds__(kWT, 1)
         u32 *t = ks; ks = kd; kd = t;
         u16 *tp = ps; ps = pd; pd = tp;
       }
-      heads_phase(S, n, [&](int q) { return q == 0 || ks[q] != ks[q - 1]; });
+      heads_phase<false>(S, n, [&](int q) { return ks[q]; });
       for (int q = tid; q < kWMax; q += kWT) S.X[q] = ps[q];  // sorted positions (pads: >= n, unused)
       __syncthreads();
     } else {
@@ -363,7 +406,7 @@ __global__ void __launch_bounds__(kWT, 1)
         S.X[g + int(atomicAdd(&cnt[g], 1u))] = u32(i);
       }
       __syncthreads();
-      heads_phase(S, n, [&](int q) { return S.rank[S.X[q] & 0xffffu] == q; });
+      heads_phase<false>(S, n, [&](int q) { return u32(S.rank[S.X[q] & 0xffffu]); });
     }
     u32 *ord = S.X, *tmp = S.Y;  // ord: the current sorted order (low 16 bits = position)
     K9_MARK(0);
@@ -383,28 +426,31 @@ __global__ void __launch_bounds__(kWT, 1)
         for (int q = tid; q < kWMax / 2; q += kWT) __stcg(dst + q, src[q]);
       }
       const int h = 1 << r;
-      // Manber-Myers order: slot q lists i = X[q] - h (suffixes sorted by
-      // their second key); the slots of j < h take the suffixes i >= n - h,
-      // whose second key is "end of string", the smallest: they must precede
-      // every other member of their group (only i = n - h, exactly h tokens
-      // long, can share its group), so the key's low bit is 0 for them.
-      // key = 2 * ordinal of i's non-singleton group + that bit; 2 NS + 1 for
-      // singletons and pads (position 0xffff)
-      for (int q = tid; q < kWMax; q += kWT) {
-        u32 item = (u32(2 * NS + 1) << 16) | 0xffffu;
-        if (q < n) {
-          const int j = int(ord[q] & 0xffffu);
-          const bool tail = j < h;
-          const int i = tail ? n - h + j : j - h;
-          const u16 k = S.nsk[S.rank[i]];
-          const u32 key = k == kSingleton ? u32(2 * NS + 1) : 2u * k + (tail ? 0u : 1u);
-          item = (key << 16) | u32(i);
+      // Manber-Myers order: the slots q of the current order list the
+      // suffixes i = ord[q] - h sorted by their SECOND key; the slots of
+      // j = ord[q] < h take the suffixes i = n - h + j >= n - h, whose second
+      // key is "end of string", the smallest.  All of those but i = n - h
+      // (exactly h tokens long) are singletons, so only i = n - h must come
+      // first among its group's members: it is listed first (from the slot
+      // q0 of suffix 0) and the slots before q0 move up by one.
+      // key = ordinal of i's non-singleton group, NS for singletons and pads
+      // (position 0xffff).
+      {
+        const int q0 = S.misc[3];
+        for (int q = tid; q < kWMax; q += kWT) {
+          if (q < n) {
+            const int j = int(ord[q] & 0xffffu);
+            const int i = j >= h ? j - h : n - h + j;
+            const u16 k = S.nsk[S.rank[i]];
+            tmp[q == q0 ? 0 : (q < q0 ? q + 1 : q)] = (u32(k == kSingleton ? NS : k) << 16) | u32(i);
+          } else {
+            tmp[q] = (u32(NS) << 16) | 0xffffu;
+          }
         }
-        tmp[q] = item;
       }
       __syncthreads();
       K9_MARK(2);
-      const int kb = bits_for(u64(2 * NS + 1));
+      const int kb = bits_for(u64(NS));
       const int np = (kb + kMaxBits - 1) / kMaxBits;
       const int bpp = (kb + np - 1) / np;
       u32 *src = tmp, *dst = ord;
@@ -418,15 +464,17 @@ __global__ void __launch_bounds__(kWT, 1)
         } else {
           // last pass: scatter to the new slot.  Non-singleton group k's items
           // come out contiguous in MM order; its slots start delta[k] later
-          // (the singleton slots before it); a singleton keeps its slot.
-          // (pads: position 0xffff, dropped)
+          // (the singleton slots before it); a singleton keeps its slot.  The
+          // item is stored with its second key r2 = rank[i+h] + 1 (0 past the
+          // end) in the high half, for the head test of the new order.
           lsd_pass_bits(bpp, S, [&](int q) { return (src[q] >> sh) & m; },
                         [&](int q, u32 to) {
                           const u32 v = src[q];
-                          const u32 k = v >> 17, i = v & 0xffffu;
+                          const u32 k = v >> 16, i = v & 0xffffu;
                           if (i == 0xffffu) return;
                           const u32 at = k < u32(NS) ? to + S.delta[k] : u32(S.rank[i]);
-                          dst[at] = i;
+                          const u32 r2 = int(i) + h < n ? u32(S.rank[i + h]) + 1u : 0u;
+                          dst[at] = (r2 << 16) | i;
                         });
           ord = dst;  // the new order (src's items are consumed)
           tmp = src;
@@ -436,13 +484,9 @@ __global__ void __launch_bounds__(kWT, 1)
 #if APO_K9_PHASES
       if (threadIdx.x == 0) atomicAdd(&k9_phase_cycles[8 + np], 1ull);
 #endif
-      // heads of the new order: (rank[i], rank[i+h]) differs from the previous slot's
-      auto r2 = [&](int i) -> u32 { return i + h < n ? u32(S.rank[i + h]) + 1u : 0u; };
-      heads_phase(S, n, [&](int q) {
-        if (q == 0) return true;
-        const int i = int(ord[q] & 0xffffu), p = int(ord[q - 1] & 0xffffu);
-        return S.rank[i] != S.rank[p] || r2(i) != r2(p);
-      });
+      // heads of the new order: an old group start, or the second key differs
+      // from the previous slot's (within an old group the first keys agree)
+      heads_phase<true>(S, n, [&](int q) { return ord[q] >> 16; });
       K9_MARK(4);
       NS = groups_phase(S, ord, n);
       K9_MARK(1);

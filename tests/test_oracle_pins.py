@@ -439,3 +439,107 @@ def test_traces_numpy_equals_python():
         a = oracle.traces_from_repeats(srcs, reps, 5, ml)
         b = oracle.traces_from_repeats_np(srcs, reps, 5, ml)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), ml
+
+
+# ------------------------------------------------------------- REPLAY ----
+
+def _replay_case(c):
+    if "stream" in c:
+        S = np.array(c["stream"], dtype=np.uint64)
+    else:  # "decay flips the choice"
+        S = np.array(list(range(1, 9)) + list(range(1000, 1300)) + [99, 5, 6, 7, 8] + list(range(1, 9)),
+                     dtype=np.uint64)
+    tr = [np.array(t, dtype=np.uint64) for t in c["traces"]]
+    tt = np.concatenate(tr)
+    to = np.cumsum([0] + [len(t) for t in tr]).astype(np.int64)
+    hits, _ = oracle.match_brute(S, np.array([0, len(S)], np.int64), tt, to)
+    return S, hits, [len(t) for t in tr]
+
+
+def test_replay_golden():
+    """Hand-derived REPLAY decisions (tests/golden/replay_examples.json)."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "replay_examples.json")))
+    for c in g["cases"]:
+        S, hits, tlen = _replay_case(c)
+        got = oracle.replay(hits, tlen, **c["params"]).tolist()
+        assert got == c["replays"], c["name"]
+        if "replays_no_decay" in c:
+            p = dict(c["params"], decay_q16=65536)
+            assert oracle.replay(hits, tlen, **p).tolist() == c["replays_no_decay"], c["name"]
+
+
+def test_replay_periodic_closed_form():
+    """S = u^k with the single trace u: every period is replayed back to back,
+    recorded the first time."""
+    for p, k in ((1, 9), (5, 7), (37, 12)):
+        u = gen.random_string(p, p, 1000)
+        S = np.tile(u, k)
+        hits, _ = oracle.match_brute(S, np.array([0, len(S)], np.int64), u, np.array([0, p], np.int64))
+        got = oracle.replay(hits, [p]).tolist()
+        assert got == [[0, i * p, (i + 1) * p - 1, 0, 1 if i == 0 else 0] for i in range(k)]
+
+
+def _replay_inputs():
+    out = []
+    for seed in range(40):
+        rng = gen.Rng(500 + seed)
+        nst = 1 + rng.below(3)
+        streams = [gen.periodic(seed * 7 + j, 40 + rng.below(200), 1 + rng.below(9), 2 + rng.below(3), noise=0.05)
+                   for j in range(nst)]
+        traces = {tuple(int(x) for x in s[a:a + 1 + rng.below(12)])
+                  for s in streams for a in [rng.below(max(len(s) - 12, 1)) for _ in range(6)]}
+        traces = sorted(traces, key=lambda t: (-len(t), t))
+        st = np.concatenate(streams)
+        so = np.cumsum([0] + [len(s) for s in streams]).astype(np.int64)
+        tt = np.array([x for t in traces for x in t], dtype=np.uint64)
+        to = np.cumsum([0] + [len(t) for t in traces]).astype(np.int64)
+        hits, _ = oracle.match_brute(st, so, tt, to)
+        out.append((streams, traces, hits))
+    return out
+
+
+def test_replay_special_case_longest_first():
+    """count_cap = 1, no decay, no bonus: every score is the trace length, so
+    REPLAY reduces to: at each end, the longest completion starting at or
+    after the first op not yet replayed."""
+    for streams, traces, hits in _replay_inputs():
+        got = oracle.replay(hits, [len(t) for t in traces], count_cap=1, decay_q16=65536, bonus_num=1,
+                            bonus_den=1).tolist()
+        want = []
+        for q in range(len(streams)):
+            frontier, best_at = 0, {}
+            for s, e, t in hits[hits[:, 0] == q].tolist():
+                best_at.setdefault(e, []).append(t)
+            seen = set()
+            for e in sorted(best_at):
+                ok = [t for t in best_at[e] if e - len(traces[t]) + 1 >= frontier]
+                if ok:
+                    t = min(ok, key=lambda t: (-len(traces[t]), t))
+                    want.append([q, e - len(traces[t]) + 1, e, t, 0 if t in seen else 1])
+                    seen.add(t)
+                    frontier = e + 1
+        assert got == want
+
+
+def test_replay_invariants():
+    """Default parameters: replays are MATCH_ALL hits, disjoint and in order;
+    no valid completion lies strictly between two replays (a completion is
+    replayed at the first end where one exists); `first` marks the first
+    replay of each trace in its stream."""
+    for streams, traces, hits in _replay_inputs():
+        got = oracle.replay(hits, [len(t) for t in traces])
+        hs = {tuple(h) for h in hits.tolist()}
+        for q in range(len(streams)):
+            rq = got[got[:, 0] == q]
+            prev_end, seen = -1, set()
+            for _, s, e, t, first in rq.tolist():
+                assert (q, e, t) in hs and s == e - len(traces[t]) + 1
+                assert s > prev_end
+                assert first == (0 if t in seen else 1)
+                seen.add(t)
+                hq = hits[(hits[:, 0] == q) & (hits[:, 1] < e) & (hits[:, 1] > prev_end)]
+                for _, e2, t2 in hq.tolist():
+                    assert e2 - len(traces[t2]) + 1 <= prev_end   # it was not valid
+                prev_end = e
