@@ -74,10 +74,31 @@ typedef struct {
 } apo_slice;
 
 /* One MATCH_ALL hit: trace `trace_id` ends at position `end_pos` of stream
- * `stream` (Alg. 1 Advance/FilterCompleted; R14). */
+ * `stream` (Alg. 1 Advance/FilterCompleted; R14).  `slot` is a
+ * per-stream key of the trace (within one stream: equal slots <=> equal
+ * trace ids; 0 <= slot < the number of traces), which apo_replay uses to
+ * index its per-stream trace state. */
 typedef struct {
-  int32_t stream, end_pos, trace_id, _pad;
+  int32_t stream, end_pos, trace_id, slot;
 } apo_match_rec;
+
+/* REPLAY scoring constants (P:694-713 names the mechanisms -- a count cap,
+ * an exponential decay of the count with the tasks since the trace last
+ * appeared, a replay bonus -- but no values; readings R20-R24).  Score of a
+ * completion of trace t at end e = len(t) * min(count, count_cap) * d_k with
+ * d_0 = 65536, d_{k+1} = (d_k * decay_q16) >> 16, k = gap / decay_period,
+ * times bonus_num / bonus_den (integer division) if t was replayed before in
+ * this stream.  NULL params = the defaults {100, 64881 (0.99), 100, 11, 10}. */
+typedef struct {
+  int32_t count_cap, decay_q16, decay_period, bonus_num, bonus_den, reserved;
+} apo_replay_params;
+
+/* One REPLAY decision: trace `trace_id` replayed over stream positions
+ * [end_pos - len + 1, end_pos]; first = 1 the first time this trace is
+ * replayed in this stream (the trace is recorded), else 0. */
+typedef struct {
+  int32_t stream, end_pos, trace_id, first;
+} apo_replay_rec;
 
 int apo_version(void);
 apo_status apo_ctx_create(int cuda_device, apo_ctx **out);
@@ -252,17 +273,37 @@ apo_status apo_trie_copy(const apo_trie *trie, uint64_t *d_tokens, int64_t *h_of
 
 /* Batched matching of independent op streams against the trace set
  * (Alg. 1 AdvanceActiveCandidates / FilterInvalidCandidates /
- * FilterCompletedCandidates).  mode 0 = MATCH_ALL
- * (reading R14): every (stream, end_pos, trace_id) with
- * stream[end_pos-|t|+1 .. end_pos] == trace t, sorted by (stream, end_pos,
- * trace_id); end_pos is stream-local.  Other modes: APO_ERR_INVALID.
- * h_off: HOST int64[nstreams+1] CSR offsets into d_streams.  d_count
- * (device int64[1]) <- number of hits; at most cap records are stored
- * (d_out: device, 16-byte aligned, cap records; 32-byte alignment lets the
- * library store consecutive records in pairs).  Synchronises `stream`. */
+ * FilterCompletedCandidates).  h_off: HOST
+ * int64[nstreams+1] CSR offsets into d_streams.
+ *  mode 0 = MATCH_ALL (reading R14): every (stream, end_pos, trace_id) with
+ *    stream[end_pos-|t|+1 .. end_pos] == trace t, sorted by (stream, end_pos,
+ *    trace_id); end_pos is stream-local.  d_out: apo_match_rec[cap] (device,
+ *    16-byte aligned; 32-byte alignment lets the library store consecutive
+ *    records in pairs); d_count: device int64[1] <- number of hits; at most
+ *    cap records are stored.
+ *  mode 1 = REPLAY: MATCH_ALL into library workspace, then apo_replay with
+ *    default parameters; d_out receives apo_replay_rec[cap] (cast), d_count:
+ *    device int64[2] <- {replays, MATCH_ALL hits}.
+ * Other modes: APO_ERR_INVALID.  Synchronises `stream`. */
 apo_status apo_match(apo_ctx *ctx, const apo_trie *trie, const uint64_t *d_streams,
                      const int64_t *h_off, int32_t nstreams, int32_t mode, apo_match_rec *d_out,
                      int64_t cap, int64_t *d_count, void *stream);
+
+/* REPLAY selection (Alg. 1 SelectReplayTrace / ExecuteAndReplay, P:429-443;
+ * scoring P:694-713; readings R20-R24) over MATCH_ALL hits d_hits[0..nhits)
+ * as apo_match mode 0 writes them (sorted by (stream, end_pos, trace_id),
+ * stream ids in [0, nstreams)).  Per stream, independently: walking the ends
+ * in order, every completion counts as an appearance of its trace; among the
+ * completions starting at or after the first op not yet replayed, the one
+ * with the highest score (ties: longer, then smaller id) is replayed, which
+ * clears every pointer that started before its end.  d_out: apo_replay_rec
+ * (device) sorted by (stream, end_pos); d_count: device int64[1] <- number
+ * of replays, at most cap stored.  h_len: HOST int64[nstreams] stream
+ * lengths (bounds the decay table and the per-stream staging).  Synchronises
+ * `stream`. */
+apo_status apo_replay(apo_ctx *ctx, const apo_trie *trie, const apo_match_rec *d_hits, int64_t nhits,
+                      const int64_t *h_len, int32_t nstreams, const apo_replay_params *params,
+                      apo_replay_rec *d_out, int64_t cap, int64_t *d_count, void *stream);
 
 #ifdef __cplusplus
 }

@@ -34,6 +34,14 @@ class apo_params(ctypes.Structure):
                 ("flags", ctypes.c_uint32), ("reserved", ctypes.c_int32)]
 
 
+class apo_replay_params(ctypes.Structure):
+    _fields_ = [("count_cap", ctypes.c_int32), ("decay_q16", ctypes.c_int32), ("decay_period", ctypes.c_int32),
+                ("bonus_num", ctypes.c_int32), ("bonus_den", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+REPLAY_DEFAULTS = dict(count_cap=100, decay_q16=64881, decay_period=100, bonus_num=11, bonus_den=10)
+
+
 class apo_slice(ctypes.Structure):
     _fields_ = [("begin", ctypes.c_int64), ("end", ctypes.c_int64)]
 
@@ -73,6 +81,7 @@ _SIGS = {
     "apo_trie_info": (ctypes.c_int, [_VP, _P_I64, _P_I64, _P_I64]),
     "apo_trie_copy": (ctypes.c_int, [_VP, _VP, _P_I64, _VP]),
     "apo_match": (ctypes.c_int, [_VP, _VP, _VP, _P_I64, _I32, _I32, _VP, _I64, _VP, _VP]),
+    "apo_replay": (ctypes.c_int, [_VP, _VP, _VP, _I64, _P_I64, _I32, _VP, _VP, _I64, _VP, _VP]),
 }
 
 _lib = None
@@ -321,21 +330,50 @@ class Context:
                                                          _stream(self.device)))
         return Trie(self, h)
 
-    def match(self, trie: "Trie", streams: torch.Tensor, off, cap: int | None = None):
-        """MATCH_ALL -> int32[h,3] rows (stream, end_pos, trace_id) sorted."""
+    def match(self, trie: "Trie", streams: torch.Tensor, off, cap: int | None = None, full: bool = False,
+              mode: int = 0):
+        """mode 0, MATCH_ALL -> int32[h,3] rows (stream, end_pos, trace_id) sorted
+        (full=True: [h,4] with the per-stream slot column).
+        mode 1, REPLAY -> (int32[r,4] rows (stream, end_pos, trace_id, first),
+        number of MATCH_ALL hits consumed on the device)."""
         streams = _check_tok(streams, self.device)
         o = _host_off(off)
         d = self.device
         if cap is None:
-            cap = 1 << 22
+            cap = 1 << 22 if mode == 0 else max(int(o[-1]) // 8, 1024)
+        while True:
+            out = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=d)
+            cnt = torch.zeros(2, dtype=torch.int64, device=d)
+            self._raise(self.lib.apo_match(self.h, trie.h, _ptr(streams), o.ctypes.data_as(_P_I64), len(o) - 1,
+                                           int(mode), _ptr(out), cap, _ptr(cnt), _stream(d)))
+            c = cnt.tolist()
+            n = int(c[0])
+            if n <= cap:
+                if mode == 1:
+                    return out[:n], int(c[1])
+                return out[:n] if full else out[:n, :3]
+            cap = n
+
+    def replay(self, trie: "Trie", hits: torch.Tensor, stream_lengths, cap: int | None = None, **params):
+        """REPLAY selection over MATCH_ALL hits (int32[h,4] from match(..., full=True))
+        -> int32[r,4] rows (stream, end_pos, trace_id, first)."""
+        if not hits.is_cuda or hits.dtype != torch.int32 or hits.dim() != 2 or hits.shape[1] != 4:
+            raise ValueError("hits must be a CUDA int32 [h, 4] tensor (match(..., full=True))")
+        hits = hits.contiguous()
+        lens = np.ascontiguousarray(np.asarray(stream_lengths, dtype=np.int64))
+        p = dict(REPLAY_DEFAULTS, **params)
+        prm = apo_replay_params(p["count_cap"], p["decay_q16"], p["decay_period"], p["bonus_num"], p["bonus_den"], 0)
+        d = self.device
+        if cap is None:
+            cap = max(int(lens.sum()) // 8, 1024)
         while True:
             out = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=d)
             cnt = torch.zeros(1, dtype=torch.int64, device=d)
-            self._raise(self.lib.apo_match(self.h, trie.h, _ptr(streams), o.ctypes.data_as(_P_I64), len(o) - 1, 0,
-                                           _ptr(out), cap, _ptr(cnt), _stream(d)))
+            self._raise(self.lib.apo_replay(self.h, trie.h, _ptr(hits), hits.shape[0], lens.ctypes.data_as(_P_I64),
+                                            len(lens), ctypes.byref(prm), _ptr(out), cap, _ptr(cnt), _stream(d)))
             n = int(cnt.item())
             if n <= cap:
-                return out[:n, :3]
+                return out[:n]
             cap = n
 
     # ------------------------------------------------------------ history --

@@ -215,6 +215,7 @@ void apo_ctx_destroy(apo_ctx *ctx) {
   cudaDeviceSynchronize();
   c.arena.release();
   c.aux.release();
+  if (c.hitbuf) cudaFree(c.hitbuf);
   for (auto &b : c.pool) cudaFree(b.first);
   for (auto e : c.ev_pool) cudaEventDestroy(e);
   if (c.status) cudaFree(c.status);

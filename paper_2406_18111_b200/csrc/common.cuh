@@ -137,6 +137,9 @@ struct Ctx {
   void pool_put(void *p, size_t bytes) {
     if (p) pool.emplace_back(p, bytes);
   }
+  // apo_match REPLAY mode: cached MATCH_ALL hit buffer (pooled)
+  void *hitbuf = nullptr;
+  size_t hitbuf_cap = 0;
   // persistent look-back state (zeroed once; epoch-tagged so never reset)
   u64 *status = nullptr;
   size_t status_words = 0;

@@ -29,17 +29,7 @@
 
 #include "pipeline.cuh"
 
-struct apo_trie {
-  apo_ctx *ctx;
-  apo::i64 T = 0;      // distinct traces
-  apo::i64 ntok = 0;   // total tokens
-  apo::i64 maxlen = 0;
-  apo::u64 *d_tok = nullptr;  // traces in id order, back to back
-  mutable apo::u64 *d_rtok = nullptr;  // the same traces, each reversed (built by the first apo_match)
-  apo::i64 *d_off = nullptr;  // T+1
-  size_t tok_bytes = 0, off_bytes = 0;  // pooled blocks (returned to the context on destroy)
-  std::vector<apo::i64> h_off;
-};
+#include "trie.cuh"
 
 namespace apo {
 namespace {
@@ -286,7 +276,7 @@ __global__ void k_write_hits(const u64 *__restrict__ keys, i64 nhits, i64 cap, i
   r.trace_id = i32(k & ((1ull << bT) - 1));
   r.end_pos = i32((k >> bT) & ((1ull << bE) - 1));
   r.stream = i32(k >> (bE + bT));
-  r._pad = 0;
+  r.slot = r.trace_id;  // this path's per-stream trace key is the trace id
   out[i] = r;
 }
 
@@ -1070,7 +1060,7 @@ __global__ void __launch_bounds__(kEmitThreads, 1) k_stream_emit(StreamMatch m, 
     const i64 e = b0 + j;
     u32 z = deep[RISA[n - 1 - e]] - 1u;
     for (u32 k = 0; k < ce[j]; ++k, ++pos) {
-      put(pos, make_int4(q, i32(e), i32(trs[z]), 0));
+      put(pos, make_int4(q, i32(e), i32(trs[z]), i32(z)));  // slot = stream-local interval id
       z = par[z];
     }
   }
@@ -1661,15 +1651,13 @@ apo_status apo_trie_copy(const apo_trie *tr, uint64_t *d_tokens, int64_t *h_off,
   return APO_OK;
 }
 
-apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams, const int64_t *h_off,
-                     int32_t nstreams, int32_t mode, apo_match_rec *d_out, int64_t cap, int64_t *d_count,
-                     void *stream) {
-  return trie_guard(ctx, [&](Ctx &c) {
-    require(tr != nullptr && d_count != nullptr && cap >= 0 && nstreams >= 1 && h_off != nullptr, "invalid argument");
-    require(mode == 0, "only MATCH_ALL (mode 0) is implemented");
-    require(cap == 0 || d_out != nullptr, "d_out is NULL");
-    require((reinterpret_cast<uintptr_t>(d_out) & 15) == 0, "d_out must be 16-byte aligned");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
+}  // extern "C"
+
+namespace {
+// MATCH_ALL (apo_match mode 0) into d_out[0..cap); *d_count <- hits.
+void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int64_t *h_off, int32_t nstreams,
+               apo_match_rec *d_out, int64_t cap, int64_t *d_count, cudaStream_t s) {
+  {
     APO_CUDA(cudaMemsetAsync(d_count, 0, sizeof(i64), s));
     const i64 Ns = h_off[nstreams];
     require(h_off[0] == 0, "h_off[0] must be 0");
@@ -1991,6 +1979,44 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
       c.launches++;
     }
     APO_CUDA(cudaMemcpyAsync(d_count, &nh, sizeof(i64), cudaMemcpyHostToDevice, s));
+    APO_CUDA(cudaStreamSynchronize(s));
+  }
+}
+}  // namespace
+
+extern "C" {
+
+apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams, const int64_t *h_off,
+                     int32_t nstreams, int32_t mode, apo_match_rec *d_out, int64_t cap, int64_t *d_count,
+                     void *stream) {
+  return trie_guard(ctx, [&](Ctx &c) {
+    require(tr != nullptr && d_count != nullptr && cap >= 0 && nstreams >= 1 && h_off != nullptr, "invalid argument");
+    require(mode == 0 || mode == 1, "mode must be 0 (MATCH_ALL) or 1 (REPLAY)");
+    require(cap == 0 || d_out != nullptr, "d_out is NULL");
+    require((reinterpret_cast<uintptr_t>(d_out) & 15) == 0, "d_out must be 16-byte aligned");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (mode == 0) {
+      match_all(c, tr, d_streams, h_off, nstreams, d_out, cap, d_count, s);
+      return;
+    }
+    // REPLAY: MATCH_ALL into a cached library buffer (grown and re-run if
+    // too small), then the replay selection consumes the hits on the device
+    i64 nh = 0;
+    for (;;) {
+      match_all(c, tr, d_streams, h_off, nstreams, static_cast<apo_match_rec *>(c.hitbuf),
+                i64(c.hitbuf_cap / sizeof(apo_match_rec)), d_count, s);
+      nh = i64(c.read_u64(reinterpret_cast<const u64 *>(d_count), s));
+      if (size_t(nh) * sizeof(apo_match_rec) <= c.hitbuf_cap) break;
+      if (c.hitbuf) c.pool_put(c.hitbuf, c.hitbuf_cap);
+      c.hitbuf_cap = (size_t(nh) + size_t(nh) / 16 + 1024) * sizeof(apo_match_rec);
+      c.hitbuf = c.pool_get(c.hitbuf_cap);
+    }
+    std::vector<i64> len(static_cast<size_t>(nstreams));
+    for (int q = 0; q < nstreams; ++q) len[q] = h_off[q + 1] - h_off[q];
+    const apo_replay_params prm{100, 64881, 100, 11, 10, 0};
+    run_replay(c, tr, static_cast<const apo_match_rec *>(c.hitbuf), nh, len.data(), nstreams, prm,
+               reinterpret_cast<apo_replay_rec *>(d_out), cap, d_count, s);
+    APO_CUDA(cudaMemcpyAsync(d_count + 1, &nh, sizeof(i64), cudaMemcpyHostToDevice, s));
     APO_CUDA(cudaStreamSynchronize(s));
   });
 }

@@ -71,6 +71,12 @@ def c4_gpu(ctx, c4):
     out["sample_hits"] = {s: hits[a:b].cpu().numpy() for s, a, b in zip(sample, lo, hi)}
     del hits, col
     torch.cuda.empty_cache()
+    # REPLAY over every stream (apo_match mode 1: the hits are consumed on the device)
+    rp, nh = ctx.match(trie, dev(st), so, mode=1)
+    rp = rp.cpu().numpy()
+    out["replay_nhits"] = nh
+    out["sample_replays"] = {q: rp[rp[:, 0] == q] for q in sample}
+    out["n_replays"] = len(rp)
     return out
 
 
@@ -141,12 +147,20 @@ def test_c4_sampled_full_streams_match(c4, c4_gpu):
     with ThreadPoolExecutor(min(THREADS, len(c4_gpu["sample"]))) as ex:
         res = list(ex.map(one, c4_gpu["sample"]))
     total = 0
+    tlen = np.diff(toff).astype(np.int32)
+    assert c4_gpu["replay_nhits"] == c4_gpu["nhits"]
     for q, h, cnt in res:
         got = c4_gpu["sample_hits"][q]
         assert got.shape[0] == cnt, q
         assert np.all(got[:, 0] == q)
-        assert np.array_equal(got[:, 1:], h[:, 1:]), q
+        assert np.array_equal(got[:, 1:3], h[:, 1:]), q
         total += cnt
+        # REPLAY of this stream (oracle on its own brute-force hits)
+        want = oracle.replay(h, tlen)
+        g = c4_gpu["sample_replays"][q]
+        assert len(want) > 0 and len(g) == len(want), q
+        assert np.array_equal(g[:, 1], want[:, 2]) and np.array_equal(g[:, 2], want[:, 3]), q
+        assert np.array_equal(g[:, 3], want[:, 4]), q
     assert total > 0
 
 
