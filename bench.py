@@ -345,8 +345,11 @@ def main():
                 trie = exchange.union(trie)
             if timed:
                 evs[3].record(s)
-            hits = ctx.match(trie, streams, soff, cap=last.get("hits", 1 << 22))
-            last["hits"] = max(int(hits.shape[0]), 1)
+            # MATCH_ALL, then REPLAY selection consuming the hits on the device
+            # (Alg. 1 SelectReplayTrace / ExecuteAndReplay)
+            hits, nall = ctx.match(trie, streams, soff, mode=1, cap=last.get("replays", 1 << 20))
+            last["replays"] = max(int(hits.shape[0]), 1)
+            last["hits"] = nall
             last["traces"] = trie.info()[0]
         if timed:
             evs[4].record(s)
@@ -448,14 +451,17 @@ def main():
             consumed[bi].record(s)
             r, o = (int(x) for x in c.tolist())
             # the step's result read back: the analysis output (repeats, their
-            # per-window offsets, occurrence lists) and the number of trace
-            # matches; the match records themselves (~7.6 GB for C4) stay on
-            # the device for the replay stage that consumes them
+            # per-window offsets, occurrence lists) and the replay decisions;
+            # the MATCH_ALL records (~7.6 GB for C4) are consumed on the
+            # device by the REPLAY selection
             rep_h = bufs[0][:r].cpu()
             roff_h = bufs[1].cpu()
             occ_h = bufs[2][:o].cpu()
-            # (ctx.match already read the 8-byte hit count back to size its output)
-            return rep_h.numel() * 4 + roff_h.numel() * 8 + occ_h.numel() * 4 + 16 + (8 if h is not None else 0)
+            # the REPLAY decisions (stream, end, trace, first) of every stream
+            # (ctx.match already read the 16-byte {replays, hits} count back)
+            rp_h = h.cpu() if h is not None else None
+            return (rep_h.numel() * 4 + roff_h.numel() * 8 + occ_h.numel() * 4 + 16
+                    + (16 + rp_h.numel() * 4 if rp_h is not None else 0))
 
         enqueue_copy(0)
         e2e_step(0, True)
@@ -498,27 +504,27 @@ def main():
                 "share_of_step": rp_ms / pms}
     roofline = roof_hbm
     if ws_n and ws_ms > rp_ms:
-        # K9 (per-window on-chip suffix sort) dominates: it is bound by shared
-        # memory, so its roofline is algorithmic shared-memory bytes (counted
-        # by the kernel: 20 B/item/LSD pass + 18 B/item/round) over the
-        # shared-memory crossbar peak, 128 B/clk/SM (B300_MICROARCH.md "LDS/STS")
-        # x SMs x max SM clock (MEASURED_PEAKS.json sm_max_mhz)
-        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-        try:
-            fmax = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"])
-        except Exception:
-            fmax = 1965.0
-        speak = 128.0 * nsm * fmax * 1e6 / 1e9
-        sach = (ws_bytes / ws_n) / ((ws_ms / ws_n) / 1e3) / 1e9
-        roofline = {"bound": "smem", "kernel": "k_window_sa (K9 per-window on-chip prefix doubling)",
-                    "achieved": sach, "peak": speak,
-                    "peak_source": f"derived: 128 B/clk/SM x {nsm} SMs x {fmax:.0f} MHz", "unit": "GB/s",
-                    "frac": sach / speak,
+        # K9 (per-window on-chip prefix doubling + LCP) dominates.  Its
+        # roofline per SURVEY.md §8(d): the per-window path moves ~16 B of HBM
+        # per op (8 B token in, 4 B SA + 4 B LCP out; the doubling rounds run
+        # in shared memory), x the ops one launch processes (every window of
+        # the batch, or every reversed match stream) / the launch's average
+        # CUDA-event duration.  The kernel is bound by instruction issue and
+        # shared memory, not HBM: the committed ncu capture's issue-slot and
+        # shared-memory-pipe utilisation are reported beside it.
+        k9_ops = N if streams is None else N + int(soff[-1])
+        k9_bytes = 16.0 * k9_ops / (ws_n / psteps)
+        sach = k9_bytes / ((ws_ms / ws_n) / 1e3) / 1e9
+        roofline = {"bound": "hbm", "kernel": "k_window_sa (K9 per-window on-chip prefix doubling + LCP)",
+                    "achieved": sach, "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                    "frac": sach / peak,
+                    "algorithmic_bytes_per_launch": k9_bytes,
+                    "algorithmic_model": "SURVEY.md §8(d): 16 B/op (token in, SA + LCP out) x ops per launch",
                     "traffic": tr.get("k_window_sa_dram_bytes_per_launch") if tr else None,
                     "traffic_source": tr.get("source") if tr else None,
-                    "launches": ws_n, "bytes_per_launch": ws_bytes / ws_n, "share_of_step": ws_ms / pms,
-                    "note": "the kernel's limiter is instruction issue (ballot multisplit): ncu shows ~2.5 IPC "
-                            "and ~63 % issue slots busy (profiles/r01_ncu_full_summary.txt)"}
+                    "launches": ws_n, "launches_per_step": ws_n / psteps, "ms_per_launch": ws_ms / ws_n,
+                    "share_of_step": ws_ms / pms,
+                    "ncu_utilisation": tr.get("k_window_sa_utilisation") if tr else None}
     roofline["shares_of_step"] = {"k_window_sa": ws_ms / pms, "k_onesweep": rp_ms / pms,
                                   "k_stream_match": mt_ms / pms, "k_scan": sc_ms / pms, "k_hist": rh_ms / pms}
     roofline["shares_source"] = (f"in-library CUDA events around each launch in a separate profiled pass of "
@@ -540,6 +546,8 @@ def main():
     desc = dict(desc)
     desc["l2"] = f"inputs ({N * 8 / 2**20:.0f} MiB of tokens per GPU) larger than the 126 MB L2; no flush"
     desc["repeats_found"] = int(counts[0])
+    if exchange is not None:
+        desc["exchange_pulled_bytes_per_rank"] = int(exchange.last_pulled_tokens) * 8
     if streams is not None:
         desc["traces"] = int(last.get("traces", 0))
         desc["match_hits"] = int(last.get("hits", 0))

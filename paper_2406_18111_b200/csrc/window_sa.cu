@@ -273,6 +273,12 @@ __device__ __forceinline__ void heads_phase(Smem &S, int n, KeyF key) {
     S.u.g.wsum[lane][1] = ib - b;
     S.u.g.wlast[lane] = lane ? el : -1;
     if (lane == 31) S.misc[2] = int(ia);
+#if APO_K9_PHASES
+    if (lane == 31) {  // slots per call and singleton slots per call (active = the rest)
+      atomicAdd(&k9_phase_cycles[11], (unsigned long long)n);
+      atomicAdd(&k9_phase_cycles[12], (unsigned long long)ib);
+    }
+#endif
     const u32 fb = __ballot_sync(0xffffffffu, (S.hbits[lane * kWItems] & 1u) != 0u);
     if (lane == 0) S.wfirst = fb;
   }

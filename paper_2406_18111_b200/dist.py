@@ -54,35 +54,22 @@ def gather_traces(tokens: torch.Tensor, off: np.ndarray, group=None):
     return all_tok, all_off
 
 
-class TraceExchange:
-    """The multi-GPU union over NVLink peer memory (SURVEY.md §8(e)).
+class SymmetricTransport:
+    """Peer-memory transport of TraceExchange on GPUs: one buffer per rank,
+    allocated with torch symmetric memory and mapped into every peer
+    (plumbing); the library kernel reads the peers' buffers over NVLink."""
 
-    Each rank copies its local trace list into a symmetric buffer (one
-    allocation per rank, mapped into every peer by torch's symmetric memory:
-    plumbing), the ranks exchange their (small) host offsets, and every rank
-    calls apo_trie_build_traces_multi with the peers' mapped pointers: the
-    library kernel pulls the remote lists over NVLink in the same pass that
-    hashes them, so there is no separate all-gather buffer, padding or
-    concatenation.  Device barriers on the symmetric handle order the copies
-    before the pulls and the pulls before the next step's copies.
-
-    The buffer is reused across steps and regrown (collectively: every rank
-    sees the same global maximum) when a list no longer fits.
-    """
-
-    def __init__(self, ctx, group=None):
+    def __init__(self, dev, group):
         import torch.distributed._symmetric_memory as symm_mem
         self._symm = symm_mem
-        self.ctx = ctx
-        self.group = group if group is not None else dist.group.WORLD
-        self.world = dist.get_world_size(self.group)
-        self.rank = dist.get_rank(self.group)
-        self.dev = ctx.device if isinstance(ctx.device, torch.device) else torch.device("cuda", ctx.device)
+        self.dev = dev
+        self.group = group
         self.cap = 0
         self.buf = None
         self.hdl = None
 
-    def _ensure(self, need: int):
+    def ensure(self, need: int):
+        """Collective: every rank passes the same global maximum."""
         if need <= self.cap:
             return
         cap = int(need * 1.25) + 4096
@@ -90,28 +77,78 @@ class TraceExchange:
         self.hdl = self._symm.rendezvous(self.buf, self.group)
         self.cap = cap
 
-    def union(self, trie):
-        """-> the union Trie of every rank's `trie` (identical on all ranks)."""
-        T, n, _ = trie.info()
+    def barrier(self):
+        self.hdl.barrier(channel=0)
+
+    def publish(self, trie):
+        """Copy the local trace list into this rank's buffer -> host offsets."""
+        _, off = trie.traces(out=self.buf)
+        return off
+
+    def sources(self):
+        """Per rank: its buffer, readable from this rank's device."""
+        return list(self.hdl.buffer_ptrs)
+
+
+class TraceExchange:
+    """The multi-GPU union over NVLink peer memory (SURVEY.md §8(e)).
+
+    Each rank copies its local trace list into its exchange buffer (one per
+    rank, mapped into every peer by the transport), the ranks exchange their
+    (small) list sizes and trace lengths over the process group, and every
+    rank calls apo_trie_build_traces_multi with every rank's buffer: the
+    library kernel pulls the remote lists over NVLink in the same pass that
+    hashes them, so there is no separate all-gather buffer, padding or
+    concatenation.  Transport barriers order the copies before the pulls and
+    the pulls before the next step's copies.
+
+    The transport is a seam: on GPUs it is SymmetricTransport (the product);
+    the world-size-2 gloo test (tests/test_dist_cpu.py) runs this same
+    union() with a host shared-memory transport and a CPU builder.  The
+    buffer is reused across steps and regrown (collectively: every rank sees
+    the same global maximum) when a list no longer fits.
+    """
+
+    def __init__(self, ctx, group=None, transport=None):
+        self.ctx = ctx
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        dev = getattr(ctx, "device", "cpu")
+        self.dev = dev if isinstance(dev, torch.device) else (
+            torch.device("cuda", dev) if isinstance(dev, int) else torch.device(dev))
+        self.transport = transport if transport is not None else SymmetricTransport(self.dev, self.group)
+        self.last_pulled_tokens = 0  # tokens this rank pulled from peers in the last union (bench report)
+
+    def gather_sizes(self, T: int, n: int) -> np.ndarray:
+        """Collective: every rank's (tokens, traces) -> int64[world, 2]."""
         sizes = torch.tensor([n, T], dtype=torch.int64, device=self.dev)
         all_sizes = torch.empty(self.world * 2, dtype=torch.int64, device=self.dev)
         dist.all_gather_into_tensor(all_sizes, sizes, group=self.group)
-        all_sizes = all_sizes.view(self.world, 2).cpu().numpy()
-        self._ensure(max(int(all_sizes[:, 0].max()), 1))
-        self.hdl.barrier(channel=0)          # peers are done reading the previous step's lists
-        _, off = trie.traces(out=self.buf)   # local list -> own symmetric buffer
+        return all_sizes.view(self.world, 2).cpu().numpy()
+
+    def gather_offsets(self, all_sizes: np.ndarray, lengths) -> list:
+        """Collective: every rank's trace lengths -> per-rank host offsets."""
+        T = int(all_sizes[self.rank, 1])
         max_tr = max(int(all_sizes[:, 1].max()), 1)
         lens = torch.zeros(max_tr, dtype=torch.int64, device=self.dev)
         if T:
-            lens[:T] = torch.from_numpy(np.diff(off)).to(self.dev)
+            lens[:T] = torch.from_numpy(np.asarray(lengths, dtype=np.int64)).to(self.dev)
         gl = torch.empty(self.world * max_tr, dtype=torch.int64, device=self.dev)
         dist.all_gather_into_tensor(gl, lens, group=self.group)
         gl = gl.view(self.world, max_tr).cpu().numpy()
-        self.hdl.barrier(channel=0)          # every rank's copy is complete
-        ptrs = self.hdl.buffer_ptrs
-        sources = []
-        for r in range(self.world):
-            nr = int(all_sizes[r, 1])
-            o = np.concatenate([[0], np.cumsum(gl[r, :nr])]).astype(np.int64)
-            sources.append((ptrs[r], o))
-        return self.ctx.trie_build_traces_multi(sources)
+        return [np.concatenate([[0], np.cumsum(gl[r, :int(all_sizes[r, 1])])]).astype(np.int64)
+                for r in range(self.world)]
+
+    def union(self, trie):
+        """-> the union Trie of every rank's `trie` (identical on all ranks)."""
+        T, n, _ = trie.info()
+        all_sizes = self.gather_sizes(T, n)
+        self.transport.ensure(max(int(all_sizes[:, 0].max()), 1))
+        self.transport.barrier()              # peers are done reading the previous step's lists
+        off = self.transport.publish(trie)    # local list -> own exchange buffer
+        offs = self.gather_offsets(all_sizes, np.diff(off))
+        self.transport.barrier()              # every rank's copy is complete
+        ptrs = self.transport.sources()
+        self.last_pulled_tokens = int(all_sizes[:, 0].sum() - all_sizes[self.rank, 0])
+        return self.ctx.trie_build_traces_multi([(ptrs[r], offs[r]) for r in range(self.world)])

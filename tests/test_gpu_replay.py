@@ -85,26 +85,30 @@ def random_cases():
 
 
 @pytest.mark.parametrize("params", [{}, dict(count_cap=3), dict(decay_period=2), dict(bonus_num=1, bonus_den=1),
-                                    dict(count_cap=1, decay_q16=65536, bonus_num=1, bonus_den=1)])
+                                    dict(count_cap=1, decay_q16=65536, bonus_num=1, bonus_den=1),
+                                    dict(count_cap=200), dict(decay_period=7, count_cap=1000)])
 def test_replay_random(ctx, params):
     for streams, traces in random_cases():
         got, want, *_ = run_case(ctx, streams, traces, **params)
         assert np.array_equal(got, want)
 
 
-def test_replay_long_streams_global_state(ctx):
+@pytest.mark.parametrize("params", [{}, dict(count_cap=200)])
+def test_replay_long_streams_global_state(ctx, params):
     """Streams longer than the on-chip matcher limit: hits come from the
-    sorted-key path with slot = trace id, and streams with more than 2,048
-    slots keep their trace states in global memory."""
+    sorted-key path with slot = trace id, and streams with more slots than
+    the on-chip state table (8,192 narrow u32 states, or 4,096 wide u64
+    states when count_cap > 127) keep their trace states in global memory."""
     streams = [gen.periodic(7, 40000, 97, 6, noise=0.01), gen.periodic(8, 20000, 31, 3, noise=0.02)]
     rng = gen.Rng(77)
     traces = set()
-    for _ in range(3000):
+    for _ in range(30000):
         s = streams[rng.below(2)]
-        a = rng.below(len(s) - 40)
-        traces.add(tuple(int(x) for x in s[a:a + 2 + rng.below(38)]))
+        a = rng.below(len(s) - 60)
+        traces.add(tuple(int(x) for x in s[a:a + 2 + rng.below(58)]))
     traces = sorted(traces, key=lambda t: (-len(t), t))
-    got, want, *_ = run_case(ctx, streams, traces)
+    assert len(traces) > 8192
+    got, want, *_ = run_case(ctx, streams, traces, **params)
     assert len(want) > 100 and np.array_equal(got, want)
 
 

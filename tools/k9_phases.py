@@ -33,3 +33,5 @@ for k, nm in enumerate(names):
     print(f"{nm:16s} {buf[k] / W:12.0f} cycles/window  {100.0 * buf[k] / tot:5.1f} %")
 print(f"rounds with 1 pass: {buf[9] / W:.2f}/window, 2 passes: {buf[10] / W:.2f}/window")
 print(f"total {tot / W:.0f} cycles/window")
+print(f"singleton slots: {buf[12] / max(buf[11], 1):.3f} of all slots over the head/group calls "
+      f"(active fraction {1 - buf[12] / max(buf[11], 1):.3f})")

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+python -c "from paper_2406_18111_b200 import build; build.build()" > gpurun_out/r02_build.log 2>&1; echo "build rc=$?"
+python tools/replay_diag.py 2>&1 | tail -8
+python tools/k9_phases.py 2>&1 | tail -12
