@@ -403,6 +403,8 @@ class History:
 
     def __init__(self, ctx: Context, capacity_B: int, scale_C: int):
         self.ctx = ctx
+        self.capacity_B = int(capacity_B)
+        self.scale_C = int(scale_C)
         h = ctypes.c_void_p()
         st = ctx.lib.apo_history_create(ctx.h, int(capacity_B), int(scale_C), ctypes.byref(h))
         ctx._raise(st)

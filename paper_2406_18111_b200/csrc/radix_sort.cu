@@ -57,9 +57,11 @@ __device__ __forceinline__ u32 peers_ballot(u32 mask, u32 d) {
   return peers;
 }
 
+// match.any: one instruction instead of BITS ballots (measured 4 % faster
+// on the C5 sort passes, 1 % on C3)
 template <int BITS>
 __device__ __forceinline__ u32 peers_of(u32 mask, u32 d) {
-  return peers_ballot<BITS>(mask, d);
+  return __match_any_sync(mask, d);
 }
 
 __device__ __forceinline__ u32 lanemask_lt() {

@@ -203,25 +203,25 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs a) {
     frontier = i64(e0) + 1;
     have = false;
   };
-  // software pipeline: records 6 chunks ahead, trace lengths 4 chunks ahead
-  // (every load is issued several chunk-iterations before its use)
-  int4 r1 = replay_rec(a, hb + lane, he), r2 = replay_rec(a, hb + 32 + lane, he),
-       r3 = replay_rec(a, hb + 64 + lane, he), r4 = replay_rec(a, hb + 96 + lane, he),
-       r5 = replay_rec(a, hb + 128 + lane, he), r6 = replay_rec(a, hb + 160 + lane, he);
-  u32 L1 = replay_len(a, r1), L2 = replay_len(a, r2), L3 = replay_len(a, r3), L4 = replay_len(a, r4);
+  // software pipeline: records kRecAhead chunks ahead, trace lengths
+  // kLenAhead chunks ahead (a record has kRecAhead - kLenAhead iterations to
+  // arrive before its trace length is looked up)
+  constexpr int kRecAhead = 10, kLenAhead = 5;
+  int4 R[kRecAhead];
+  u32 LS[kLenAhead];
+#pragma unroll
+  for (int k = 0; k < kRecAhead; ++k) R[k] = replay_rec(a, hb + 32 * k + lane, he);
+#pragma unroll
+  for (int k = 0; k < kLenAhead; ++k) LS[k] = replay_len(a, R[k]);
   for (i64 p = hb; p < he; p += 32) {
-    const int4 r = r1;
-    const u32 L = L1;
-    r1 = r2;
-    r2 = r3;
-    r3 = r4;
-    r4 = r5;
-    r5 = r6;
-    L1 = L2;
-    L2 = L3;
-    L3 = L4;
-    L4 = replay_len(a, r4);
-    r6 = replay_rec(a, p + 192 + lane, he);
+    const int4 r = R[0];
+    const u32 L = LS[0];
+#pragma unroll
+    for (int k = 0; k + 1 < kRecAhead; ++k) R[k] = R[k + 1];
+#pragma unroll
+    for (int k = 0; k + 1 < kLenAhead; ++k) LS[k] = LS[k + 1];
+    LS[kLenAhead - 1] = replay_len(a, R[kLenAhead - 1]);
+    R[kRecAhead - 1] = replay_rec(a, p + 32 * kRecAhead + lane, he);
     const bool valid = p + lane < he;
     // a carried end that does not continue here is decided first (before
     // this chunk reads its trace states: the replay sets a replayed bit)

@@ -24,7 +24,7 @@
 // j < h, which have no predecessor i = j - h; all but i = n - h are
 // singletons, and a low key bit of 0 puts i = n - h first in its group.
 //
-// A pass ranks 512 items per warp with ballot-derived peer masks into a
+// A pass ranks 512 items per warp with match.any peer masks into a
 // per-warp u16 digit histogram, one block scan gives digit starts, and items
 // are scattered; the last pass of a round scatters straight to the item's new
 // slot (group start of its non-singleton group + rank inside it).  Group
@@ -138,7 +138,9 @@ __device__ __forceinline__ void lsd_pass(Smem &S, DigitF digit, MoveF move) {
 #pragma unroll
   for (int j = 0; j < kWItems; ++j) {
     const u32 d = digit(base + j * 32);
-    const u32 peers = peers_of<BITS>(d);
+    // peers with the same digit: one match.any for 2+ bit digits (measured
+    // 15 % faster over the whole kernel than BITS ballots), a ballot for 1 bit
+    const u32 peers = BITS >= 2 ? __match_any_sync(0xffffffffu, d) : peers_of<BITS>(d);
     const u32 old = wh[d];
     __syncwarp();
     if (lane == __ffs(peers) - 1) wh[d] = u16(old + __popc(peers));

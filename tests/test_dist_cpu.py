@@ -194,3 +194,135 @@ def test_trace_exchange_union_gloo_world2():
         for k, e in enumerate(log):
             if e[0] == "publish":
                 assert log[k - 1][0] == "barrier" and log[k + 1][0] == "barrier"
+
+
+# ---------------------------------------------------------------------------
+# TraceFinder ingestion agreement (reading R25) on two
+# gloo ranks whose analyses finish at different times: both ranks must
+# ingest the same analyses at the same op counts and grow the agreed delay
+# together whenever either one had to wait.
+
+class _HostHistory:
+    """The history's schedule on the host: apo_ruler_slices (pure host
+    function of libapo) over a numpy token list (test stand-in for the
+    device ring)."""
+
+    def __init__(self, B, C):
+        self.capacity_B, self.scale_C = B, C
+        self.tok = np.zeros(0, np.uint64)
+
+    @property
+    def count(self):
+        return len(self.tok)
+
+    def ingest(self, piece):
+        from paper_2406_18111_b200.apo import ruler_slices
+        k0 = self.count
+        self.tok = np.concatenate([self.tok, piece])
+        return ruler_slices(k0, len(piece), self.scale_C, self.capacity_B)
+
+    def window(self, b, e):
+        return self.tok[b:e]
+
+
+class _ScriptedFuture:
+    def __init__(self, clock, ready_at, win):
+        self.clock, self.ready_at, self.win = clock, ready_at, win
+        self.waited = False
+
+    def done(self):
+        return self.clock() >= self.ready_at
+
+    def result(self):
+        if not self.done():
+            self.waited = True  # the replica blocks here until the analysis completes
+        return self.win
+
+
+class _ScriptedAnalyzer:
+    """Analysis i of this rank completes lag(i) ops after its launch."""
+
+    def __init__(self, lag):
+        self.lag = lag
+        self.n = 0
+        self.clock = None
+
+    def submit(self, win, ready):
+        f = _ScriptedFuture(self.clock, self.clock() + self.lag(self.n), win)
+        self.n += 1
+        return f
+
+
+class _SetBuilder:
+    """IngestCandidates on the host for the test: the analysis's repeat
+    contents by the oracle, the set union."""
+
+    def from_analysis(self, win):
+        import oracle
+        rep = oracle.find_repeats(np.asarray(win), 5, tier=1)["repeats"]
+        return {tuple(int(x) for x in win[s:s + l]) for s, l in rep[:, :2]}
+
+    def union(self, a, b):
+        return a | b
+
+    @staticmethod
+    def size(t):
+        return 0 if t is None else len(t)
+
+
+def _agree_stream():
+    from workloads import gen
+    return np.concatenate([gen.periodic(3, 3000, 37, 24, noise=0.1), gen.periodic(4, 3000, 53, 24, noise=0.1)])
+
+
+def _finder_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2406_18111_b200.finder import TraceFinder
+    # rank 1's first analyses are slow (1,300 ops), later ones fast
+    an = _ScriptedAnalyzer((lambda i: 10) if rank == 0 else (lambda i: 1300 if i < 3 else 10))
+    fi = TraceFinder(_HostHistory(1024, 128), an, _SetBuilder(), delay=128)
+    an.clock = lambda: fi.count
+    S = _agree_stream()
+    rng = np.random.default_rng(rank)  # ranks feed the same ops in different piece sizes
+    pos = 0
+    while pos < len(S):
+        k = int(rng.integers(1, 700))
+        fi.ingest(S[pos:pos + k])
+        pos += k
+    q.put((rank, fi.events, sorted(fi.trie) if fi.trie else []))
+    dist.destroy_process_group()
+
+
+def test_trace_finder_agreement_gloo_world2():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_finder_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, ev, tr = q.get(timeout=180)
+        res[r] = (ev, tr)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ev0, tr0 = res[0]
+    ev1, tr1 = res[1]
+    assert ev0 == ev1 and tr0 == tr1 and len(ev0) > 10
+    # the delay doubles exactly when someone waited, and only then
+    d = 128
+    for count, anyw, size, delay in ev0:
+        if anyw:
+            d *= 2
+        assert delay == d
+    assert any(e[1] for e in ev0) and not ev0[-1][1]
+    # rank 1's three slow analyses (1,300 ops > every delay in force) are the
+    # only waits; after them the agreed delay stays at 128 * 2^3
+    assert sum(e[1] for e in ev0) == 3 and all(e[1] for e in ev0[:3]) and ev0[-1][3] == 1024
+    # every analysis is ingested exactly delay-at-launch ops after its launch
+    # (launch points: multiples of C = 128), in launch order
+    counts = [e[0] for e in ev0]
+    assert counts == sorted(counts)

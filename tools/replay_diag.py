@@ -31,3 +31,16 @@ for _ in range(3):
     e1.record()
     torch.cuda.synchronize()
     print(f"apo_replay: {e0.elapsed_time(e1):.2f} ms, {r.shape[0]} replays")
+# the heaviest stream alone (its sequential walk bounds the kernel)
+qs = int(torch.argmax(nh).item())
+sel = hits[hits[:, 0] == qs].clone()
+sel[:, 0] = 0
+L = int(so[qs + 1] - so[qs])
+for _ in range(2):
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    r1 = ctx.replay(trie, sel, [L])
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"heaviest stream {qs} alone ({sel.shape[0]} hits): {e0.elapsed_time(e1):.2f} ms, {r1.shape[0]} replays")
