@@ -305,6 +305,49 @@ apo_status apo_replay(apo_ctx *ctx, const apo_trie *trie, const apo_match_rec *d
                       const int64_t *h_len, int32_t nstreams, const apo_replay_params *params,
                       apo_replay_rec *d_out, int64_t cap, int64_t *d_count, void *stream);
 
+/* ---------------------------------------------------------------------- */
+/* Distributed suffix array: one window split into       */
+/* contiguous position blocks over G ranks, prefix doubling ("SA <-         */
+/* SuffixArray(S)") with a sample-sort exchange.  These are the      */
+/* per-rank compute steps; paper_2406_18111_b200/dsa.py moves the data      */
+/* between ranks (NCCL all-to-all / all-gather).  Ranks of a round are      */
+/* group-head indices + 1 in [1, n] (0 = past the end); n < 2^32 - 1.       */
+/* ---------------------------------------------------------------------- */
+
+/* Round keys of the owned suffixes i = base .. base+m-1: d_keys[k] =
+ * rank[i] * (n + 1) + rank2 with rank2 = d_rank2[k] (the rank of suffix
+ * i + h) for k < m2 and 0 ("end of string") for k >= m2; d_vals[k] = i. */
+apo_status apo_dsa_keys(apo_ctx *ctx, const uint32_t *d_rank, const uint32_t *d_rank2, int64_t m, int64_t m2,
+                        int64_t base, int64_t n, uint64_t *d_keys, uint32_t *d_vals, void *stream);
+
+/* s evenly spaced (key, value) samples of a block sorted by (key, value)
+ * (all-ones samples when m == 0). */
+apo_status apo_dsa_samples(apo_ctx *ctx, const uint64_t *d_keys, const uint32_t *d_vals, int64_t m, int32_t s,
+                           uint64_t *d_skeys, uint32_t *d_svals, void *stream);
+
+/* Partition of a block sorted by (key, value) by g-1 ascending (key, value)
+ * splitters: d_counts[d] (device int64[g]) = number of pairs p with
+ * splitter[d-1] <= p < splitter[d] (splitter[-1] = -inf, splitter[g-1] =
+ * +inf). */
+apo_status apo_dsa_split(apo_ctx *ctx, const uint64_t *d_keys, const uint32_t *d_vals, int64_t m,
+                         const uint64_t *d_split_keys, const uint32_t *d_split_vals, int32_t g, int64_t *d_counts,
+                         void *stream);
+
+/* New ranks of a block of the globally sorted key sequence whose first
+ * element has global index gbase: element k heads a group iff its key
+ * differs from the previous key (prev_key, the previous rank's last key,
+ * for k = 0 when has_prev); d_rank[k] = global index of its group's head + 1
+ * (carry = global index of the last head before the block, -1 none).
+ * d_stats (device int64[2]) <- {heads in the block, global index of the
+ * last head or -1}.  Synchronises `stream`. */
+apo_status apo_dsa_heads(apo_ctx *ctx, const uint64_t *d_keys, int64_t m, uint64_t prev_key, int32_t has_prev,
+                         int64_t gbase, int64_t carry, uint32_t *d_rank, int64_t *d_stats, void *stream);
+
+/* d_rank[d_pos[k] - base] = d_rank_in[k] for k < m (positions owned by the
+ * calling rank). */
+apo_status apo_dsa_scatter(apo_ctx *ctx, const uint32_t *d_pos, const uint32_t *d_rank_in, int64_t m, int64_t base,
+                           uint32_t *d_rank, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

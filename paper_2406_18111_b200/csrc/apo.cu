@@ -69,34 +69,6 @@ void Ctx::prof_end(cudaStream_t s) { APO_CUDA(cudaEventRecord(prof_recs.back().b
 
 namespace {
 
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur;
-    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
-  }
-};
-
-template <class Fn>
-apo_status guarded(apo_ctx *ctx, Fn &&fn) {
-  if (ctx == nullptr) return APO_ERR_INVALID;
-  ctx->c.err.clear();
-  try {
-    DeviceGuard g(ctx->c.device);
-    fn(ctx->c);
-    return APO_OK;
-  } catch (const Error &e) {
-    ctx->c.err = e.msg;
-    return e.code;
-  } catch (const std::exception &e) {
-    ctx->c.err = e.what();
-    return APO_ERR_CUDA;
-  }
-}
 
 // position -> window map: one CTA per window fills its range (coalesced)
 __global__ void k_fill_wid(const i64 *__restrict__ off, int W, i64 N, i32 *__restrict__ wid) {
@@ -149,22 +121,22 @@ struct Plan {
   size_t bytes = 0;
 };
 
-void plan_all(Carver &cv, Batch &b, Plan &p, bool want_lcp, bool want_select) {
+void plan_all(Carver &cv, Batch &b, Plan &p, bool want_lcp, bool want_select, int nsmid) {
   if (b.W > 1) {
     p.d_off = cv.take<i64>(size_t(b.W) + 1);
     p.d_wid = cv.take<i32>(size_t(b.N));
   }
-  plan_sa(cv, b, p.sa, want_lcp || want_select);
+  plan_sa(cv, b, p.sa, want_lcp || want_select, nsmid);
   if (want_select) plan_select(cv, b, p.sel);
 }
 
 Plan setup(Ctx &c, Batch &b, const i64 *h_off, bool want_lcp, bool want_select, cudaStream_t s) {
   Plan p;
   Carver dry(nullptr);
-  plan_all(dry, b, p, want_lcp, want_select);
+  plan_all(dry, b, p, want_lcp, want_select, c.nsmid);
   c.arena.reserve(dry.off, s);
   Carver cv(c.arena.base);
-  plan_all(cv, b, p, want_lcp, want_select);
+  plan_all(cv, b, p, want_lcp, want_select, c.nsmid);
   if (b.W > 1) {
     APO_CUDA(cudaMemcpyAsync(p.d_off, h_off, sizeof(i64) * (b.W + 1), cudaMemcpyHostToDevice, s));
     k_fill_wid<<<b.W, 256, 0, s>>>(p.d_off, b.W, b.N, p.d_wid);
@@ -193,6 +165,7 @@ apo_status apo_ctx_create(int cuda_device, apo_ctx **out) {
   apo_status st = guarded(ctx, [&](Ctx &c) {
     APO_CUDA(cudaSetDevice(cuda_device));
     APO_CUDA(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, cuda_device));
+    c.nsmid = query_nsmid(cuda_device);
     APO_CUDA(cudaMalloc(&c.counters, sizeof(u32) * kNumCounterSlots));
     APO_CUDA(cudaMemset(c.counters, 0, sizeof(u32) * kNumCounterSlots));
     APO_CUDA(cudaMalloc(&c.d_misc, 64 * 1024));

@@ -111,6 +111,7 @@ struct ProfRec {
 struct Ctx {
   int device = 0;
   int num_sms = 148;
+  int nsmid = 0;  // %nsmid: SM ids are < nsmid (K9's per-SM scratch)
   std::string err;
   Arena arena;  // per-call scratch
   Arena aux;    // second per-call scratch (trie pieces, match hit keys)
@@ -388,3 +389,36 @@ size_t radix_status_words(i64 n);
 struct apo_ctx {
   apo::Ctx c;
 };
+
+namespace apo {
+// Entry-point wrapper: selects the context's device, maps exceptions to
+// status codes and the context's error text.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <class Fn>
+apo_status guarded(apo_ctx *ctx, Fn &&fn) {
+  if (ctx == nullptr) return APO_ERR_INVALID;
+  ctx->c.err.clear();
+  try {
+    DeviceGuard g(ctx->c.device);
+    fn(ctx->c);
+    return APO_OK;
+  } catch (const Error &e) {
+    ctx->c.err = e.msg;
+    return e.code;
+  } catch (const std::exception &e) {
+    ctx->c.err = e.what();
+    return APO_ERR_CUDA;
+  }
+}
+}  // namespace apo

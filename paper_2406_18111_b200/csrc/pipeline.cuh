@@ -53,17 +53,16 @@ struct SAWork {
   int unit = 1;           // level r ranks the (unit * 2^r)-token prefixes (token packing, K3)
 };
 
-void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp);
+void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp, int nsmid);
 // K2 (hash path): dense order-preserving token ids; returns K or -1 when
 // the distinct count exceeds cap / 2.
 size_t token_ids_scratch_bytes(i64 n, u32 cap);
 i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scratch, cudaStream_t s);
 // K9: per-window on-chip suffix array + LCP (windows <= 16,384 ops, not
-// generalized): persistent CTAs (at most kWindowSACtasMax), each with its own
-// level scratch of window_sa_scratch_bytes(b) / CTAs bytes.
-constexpr int kWindowSACtasMax = 256;
+// generalized): one CTA per window, a level scratch per SM id.
 bool window_sa_supported(const Batch &b);
-size_t window_sa_scratch_bytes(const Batch &b);
+size_t window_sa_scratch_bytes(int nsmid);
+int query_nsmid(int device);
 void run_window_sa(Ctx &c, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s);
 void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s);
 

@@ -11,20 +11,38 @@
 // fix what the paper leaves open; the constants are declared
 // defaults (apo_replay_params).
 //
-// Streams are independent; within a stream the decisions are a left-to-right
-// chain (a replay moves the frontier every later decision depends on), so
-// one warp walks one stream's hits (k_replay below):
-//   * the hits are read 32 records at a time, the next chunk prefetched, and
-//     each record's trace state (appearance count, last end) is updated in
-//     parallel in shared memory indexed by the record's stream-local slot;
-//   * only the choice per end is sequential: a warp arg-max (score, length,
-//     -id) over the end's completions that start at or after the frontier;
-//   * decay factors d_k come from a table the host computes with the same
-//     integer recurrence (exact, no floating point);
-//   * replays are staged per stream (at most one per stream position) and
-//     compacted in stream order after a scan of the per-stream counts.
-// A stream whose slots exceed the on-chip table keeps its state in global
-// memory instead (same code, other pointer).
+// Streams are independent, and within a stream only the choice of replays is
+// a left-to-right chain (a replay moves the frontier every later decision
+// depends on).  Everything else is computed in parallel, so no stream's
+// sequential walk touches more than the few chunks where a replay happens
+// (a stream can hold a million hits: a one-warp walk over all of them was
+// the whole kernel's critical path):
+//   A (k_rp_local, CTA per part of 2,048 consecutive records of a stream):
+//     a stable sort of the part's records by slot (the stream-local trace
+//     key) gives each record its appearance count and previous end WITHIN
+//     the part; per run of equal slots the part stores (slot, count, last
+//     end);
+//   B (k_rp_prefix, CTA per stream): walks the stream's parts in order with
+//     a per-slot table (count so far, last end), replacing each run's
+//     (count, last end) with the table's values before the part -- the state
+//     the part starts from -- and updating the table;
+//   C (k_rp_scores, CTA per part): the same sort again; per record
+//     count = min(count before the part + count in the part, cap) and gap =
+//     end - previous end (in the part, else before it), the score before the
+//     bonus len x count x d_k (u64; d_k from a host table built with the
+//     oracle's integer recurrence); per chunk of 32 records the latest start
+//     (end - len + 1);
+//   D (k_rp_decide, warp per stream): the decision walk.  A record is
+//     eligible iff it starts at or after the frontier; a chunk whose latest
+//     start is before the frontier is skipped with one ballot per 32 chunks.
+//     In an eligible chunk the first eligible record marks the next end
+//     where a replay happens; an end's records are in trace-id order (length
+//     descending), so its eligible records are the rest of that end's run:
+//     bonus (replayed bitset), arg-max (score, length, -id), merged with a
+//     running best when the end continues into the next chunk; the replay
+//     moves the frontier.
+// Replays are staged per stream (at most one per stream position) and
+// compacted in stream order after a scan of the per-stream counts.
 #include <algorithm>
 #include <vector>
 
@@ -33,35 +51,55 @@
 namespace apo {
 namespace {
 
-constexpr int kReplayStateBytes = 32768;  // on-chip per-stream trace states (up to 32 KB per warp)
-constexpr int kReplayThreads = 32;  // one warp per stream
+constexpr int kPart = 2048;                     // records per part
+constexpr int kPartThreads = 256;               // 8 warps
+constexpr int kPartItems = kPart / kPartThreads;
+constexpr int kPartWarps = kPartThreads / 32;
+constexpr int kChunksPerPart = kPart / 32;
+constexpr int kMaxDigit = 9;                    // slot sort digits <= 9 bits
+constexpr int kPrefixThreads = 512;
+constexpr int kStateBytesMax = 192 * 1024;      // phase B per-stream table on chip up to here
 
-struct ReplayArgs {
+struct RP {
   const int4 *hits;
-  i64 nhits;
-  int nstreams;
   const i64 *tlen_off;   // trace offsets (T+1): len(t) = off[t+1] - off[t]
   const u32 *dq;         // decay table d_k, k < ndq
   int ndq;
   int count_cap, period;
   double inv_period;     // 1 / period (the quotient is corrected to the exact one)
   u32 bonus_num, bonus_den;
-  const i64 *hbeg;       // per stream: first hit (nstreams + 1, from k_replay_ranges)
-  const u32 *maxslot;    // per stream: max slot + 1
-  void *gstate;          // global fallback states
-  const i64 *gstate_off; // per stream offset into gstate (nstreams + 1)
+  int nstreams;
+  int slot_bits;         // slots < 2^slot_bits
+  const i64 *hbeg;       // per stream: first hit (nstreams + 1)
+  const i64 *pbeg;       // per stream: first part (nstreams + 1)
+  const int *pstream;    // per part: its stream
+  u32 *maxslot;          // per stream: max slot + 1 (phase A)
+  u32 *run_slot;         // per part, per run (slot order): slot
+  u32 *run_cnt;          // A: records of the run; B: count before the part (saturated)
+  i32 *run_last;         // A: last end in the run; B: last end before the part (-1: none)
+  u32 *nruns;            // per part
+  u64 *sc;               // per record: score before the bonus
+  i32 *cmax;             // per part, per chunk: latest start (-1: empty)
+  const int *order;      // phase D: block -> stream (streams with the most hits first)
+  void *gstate;          // phase B/D global fallback tables
+  const i64 *gstate_off; // per stream offset (u32 words) into gstate (nstreams + 1)
+  u32 on_chip_slots;     // phase B: streams with maxslot above this use gstate
+  u32 on_chip_bits;      // phase D: bitsets above this many words use gstate
   const i64 *soff;       // per stream staging offset (stream position base)
   int4 *stage;           // staged replays
   u32 *rcnt;             // per stream replay count
-  const int *order;      // block -> stream (streams with the most hits first)
 };
 
-// Per stream: its hit range (hits sorted by stream) and its largest slot.
-__global__ void k_replay_ranges(const int4 *__restrict__ hits, i64 nhits, int nstreams, i64 *__restrict__ hbeg,
-                                u32 *__restrict__ maxslot) {
-  const int q = blockIdx.x;
+__device__ __forceinline__ u32 lanemask_lt_() {
+  u32 m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Per stream: its hit range (hits sorted by stream).
+__global__ void k_replay_ranges(const int4 *__restrict__ hits, i64 nhits, int nstreams, i64 *__restrict__ hbeg) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q > nstreams) return;
-  // lower bound of stream q (every lane does the same search)
   i64 lo = 0, hi = nhits;
   while (lo < hi) {
     const i64 mid = (lo + hi) >> 1;
@@ -70,26 +108,283 @@ __global__ void k_replay_ranges(const int4 *__restrict__ hits, i64 nhits, int ns
     else
       hi = mid;
   }
-  if (threadIdx.x == 0) hbeg[q] = lo;
-  if (q == nstreams) return;
-  i64 e = lo, hi2 = nhits;  // upper bound
-  while (e < hi2) {
-    const i64 mid = (e + hi2) >> 1;
-    if (__ldg(&hits[mid].x) <= q)
-      e = mid + 1;
-    else
-      hi2 = mid;
+  hbeg[q] = lo;
+}
+
+// ---------------------------------------------------------------------------
+// The part's records sorted by slot (stable): 8 warps x 256 records, LSD
+// passes of up to 9 bits with match.any peer masks into per-warp u16 digit
+// counts.  On return sk[k] / sv[k] hold the k-th record's slot / part-local
+// index in (slot, index) order (pads: slot 0xffffffff at the end).
+struct PartSmem {
+  u32 ka[kPart], kb[kPart];
+  unsigned short va[kPart], vb[kPart];
+  i32 end[kPart];
+  u32 len[kPart];
+  unsigned short hist[kPartWarps][1 << kMaxDigit];
+  u32 start[1 << kMaxDigit];
+  u32 wsum[kPartWarps];
+  u32 wmax[kPartWarps];
+};
+
+template <int BITS>
+__device__ void part_pass(PartSmem &S, const u32 *kin, const unsigned short *vin, u32 *kout, unsigned short *vout,
+                          int shift) {
+  constexpr int RADIX = 1 << BITS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned short *wh = S.hist[warp];
+  for (int i = lane; i < RADIX; i += 32) wh[i] = 0;
+  __syncwarp();
+  const u32 lt = lanemask_lt_();
+  u32 rk[kPartItems];
+#pragma unroll
+  for (int j = 0; j < kPartItems; ++j) {
+    const int q = warp * (32 * kPartItems) + j * 32 + lane;
+    const u32 d = (kin[q] >> shift) & u32(RADIX - 1);
+    const u32 peers = __match_any_sync(0xffffffffu, d);
+    const u32 old = wh[d];
+    __syncwarp();
+    if (lane == __ffs(peers) - 1) wh[d] = (unsigned short)(old + __popc(peers));
+    __syncwarp();
+    rk[j] = old + __popc(peers & lt);
   }
-  u32 m = 0;
-  for (i64 k = lo + threadIdx.x; k < e; k += blockDim.x) m = max(m, u32(__ldg(&hits[k].w)) + 1u);
-  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-  __shared__ u32 s_m[8];
-  if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
   __syncthreads();
+  // per digit: exclusive prefix over warps (in place), digit totals
+  for (int d = tid; d < RADIX; d += kPartThreads) {
+    u32 t = 0;
+#pragma unroll
+    for (int w = 0; w < kPartWarps; ++w) {
+      const u32 c = S.hist[w][d];
+      S.hist[w][d] = (unsigned short)t;
+      t += c;
+    }
+    S.start[d] = t;
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the digit totals
+    u32 carry = 0;
+    for (int d0 = 0; d0 < RADIX; d0 += 32) {
+      const u32 v = d0 + lane < RADIX ? S.start[d0 + lane] : 0u;
+      u32 x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (d0 + lane < RADIX) S.start[d0 + lane] = carry + x - v;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kPartItems; ++j) {
+    const int q = warp * (32 * kPartItems) + j * 32 + lane;
+    const u32 d = (kin[q] >> shift) & u32(RADIX - 1);
+    const u32 to = S.start[d] + wh[d] + rk[j];
+    kout[to] = kin[q];
+    vout[to] = vin[q];
+  }
+  __syncthreads();
+}
+
+__device__ void part_pass_bits(int bits, PartSmem &S, const u32 *kin, const unsigned short *vin, u32 *kout,
+                               unsigned short *vout, int shift) {
+  switch (bits) {
+    case 1: part_pass<1>(S, kin, vin, kout, vout, shift); break;
+    case 2: part_pass<2>(S, kin, vin, kout, vout, shift); break;
+    case 3: part_pass<3>(S, kin, vin, kout, vout, shift); break;
+    case 4: part_pass<4>(S, kin, vin, kout, vout, shift); break;
+    case 5: part_pass<5>(S, kin, vin, kout, vout, shift); break;
+    case 6: part_pass<6>(S, kin, vin, kout, vout, shift); break;
+    case 7: part_pass<7>(S, kin, vin, kout, vout, shift); break;
+    case 8: part_pass<8>(S, kin, vin, kout, vout, shift); break;
+    default: part_pass<9>(S, kin, vin, kout, vout, shift); break;
+  }
+}
+
+// Loads part p's records (slots, ends, trace lengths) and sorts them by slot.
+// Returns (first record, record count); sorted keys/indices in (*sk, *sv).
+__device__ void part_load_sort(const RP &a, PartSmem &S, i64 p, i64 &r0, int &m, const u32 *&sk,
+                               const unsigned short *&sv, bool want_len) {
+  const int q = a.pstream[p];
+  r0 = a.hbeg[q] + (p - a.pbeg[q]) * kPart;
+  m = int(min(i64(kPart), a.hbeg[q + 1] - r0));
+  for (int i = threadIdx.x; i < kPart; i += kPartThreads) {
+    if (i < m) {
+      const int4 r = a.hits[r0 + i];
+      S.ka[i] = u32(r.w);
+      S.end[i] = r.y;
+      if (want_len) S.len[i] = u32(__ldg(&a.tlen_off[r.z + 1]) - __ldg(&a.tlen_off[r.z]));
+    } else {
+      S.ka[i] = 0xffffffffu;  // pads sort last
+    }
+    S.va[i] = (unsigned short)i;
+  }
+  __syncthreads();
+  const int np = (a.slot_bits + kMaxDigit - 1) / kMaxDigit;
+  const int bpp = (a.slot_bits + np - 1) / np;
+  u32 *ks = S.ka, *kd = S.kb;
+  unsigned short *vs = S.va, *vd = S.vb;
+  for (int k = 0; k < np; ++k) {
+    part_pass_bits(bpp, S, ks, vs, kd, vd, k * bpp);
+    u32 *t = ks; ks = kd; kd = t;
+    unsigned short *tv = vs; vs = vd; vd = tv;
+  }
+  sk = ks;
+  sv = vs;
+}
+
+// Run structure of the sorted part: thread t owns sorted positions
+// [8t, 8t + 8).  For each: run id (number of run heads before it), run start.
+__device__ void part_runs(PartSmem &S, const u32 *sk, int m, int (&rid)[kPartItems], int (&rst)[kPartItems],
+                          int &nruns) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int k0 = tid * kPartItems;
+  int heads = 0, lastpos = -1;
+  bool hd[kPartItems];
+#pragma unroll
+  for (int j = 0; j < kPartItems; ++j) {
+    const int k = k0 + j;
+    hd[j] = k < m && (k == 0 || sk[k] != sk[k - 1]);
+    heads += hd[j];
+    if (hd[j]) lastpos = k;
+  }
+  // block exclusive sum of heads and exclusive max of the last head position
+  int hs = heads, hm = lastpos;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, hs, o), z = __shfl_up_sync(0xffffffffu, hm, o);
+    if (lane >= o) {
+      hs += y;
+      hm = max(hm, z);
+    }
+  }
+  if (lane == 31) {
+    S.wsum[warp] = u32(hs);
+    S.wmax[warp] = u32(hm + 1);
+  }
+  __syncthreads();
+  int bs = 0, bm = -1;
+  for (int w = 0; w < warp; ++w) {
+    bs += int(S.wsum[w]);
+    bm = max(bm, int(S.wmax[w]) - 1);
+  }
+  const int ex_s = bs + hs - heads;
+  const int up = __shfl_up_sync(0xffffffffu, hm, 1);
+  const int ex_m = lane == 0 ? bm : max(bm, up);
+  int cur = ex_m, cnt = ex_s;
+#pragma unroll
+  for (int j = 0; j < kPartItems; ++j) {
+    if (hd[j]) {
+      cur = k0 + j;
+      ++cnt;
+    }
+    rst[j] = cur;
+    rid[j] = cnt - 1;
+  }
+  nruns = 0;
+  for (int w = 0; w < kPartWarps; ++w) nruns += int(S.wsum[w]);
+  __syncthreads();
+}
+
+// Phase A: per part, runs of equal slots (slot, records, last end).
+__global__ void __launch_bounds__(kPartThreads) k_rp_local(RP a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  PartSmem &S = *reinterpret_cast<PartSmem *>(smraw);
+  const i64 p = blockIdx.x;
+  i64 r0;
+  int m;
+  const u32 *sk;
+  const unsigned short *sv;
+  part_load_sort(a, S, p, r0, m, sk, sv, false);
+  int rid[kPartItems], rst[kPartItems], nr;
+  part_runs(S, sk, m, rid, rst, nr);
+  const int k0 = threadIdx.x * kPartItems;
+  const i64 rb = p * kPart;
+#pragma unroll
+  for (int j = 0; j < kPartItems; ++j) {
+    const int k = k0 + j;
+    if (k >= m) break;
+    const bool last = k + 1 == m || sk[k + 1] != sk[k];
+    if (last) {
+      a.run_slot[rb + rid[j]] = sk[k];
+      a.run_cnt[rb + rid[j]] = u32(k - rst[j] + 1);
+      a.run_last[rb + rid[j]] = S.end[sv[k]];
+    }
+  }
   if (threadIdx.x == 0) {
-    u32 r = 0;
-    for (int w = 0; w < int(blockDim.x >> 5); ++w) r = max(r, s_m[w]);
-    maxslot[q] = r;
+    a.nruns[p] = u32(nr);
+    if (m > 0) atomicMax(&a.maxslot[a.pstream[p]], sk[m - 1] + 1u);
+  }
+}
+
+// Phase B: per stream, the state each part starts from.
+__global__ void __launch_bounds__(kPrefixThreads) k_rp_prefix(RP a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int q = blockIdx.x;
+  const u32 ms = a.maxslot[q];
+  const bool onchip = ms <= a.on_chip_slots;
+  u32 *cnt = onchip ? reinterpret_cast<u32 *>(smraw) : static_cast<u32 *>(a.gstate) + a.gstate_off[q];
+  i32 *last = reinterpret_cast<i32 *>(cnt + ms);
+  for (u32 i = threadIdx.x; i < ms; i += kPrefixThreads) {
+    cnt[i] = 0;
+    last[i] = -1;
+  }
+  __syncthreads();
+  for (i64 p = a.pbeg[q]; p < a.pbeg[q + 1]; ++p) {
+    const u32 nr = a.nruns[p];
+    const i64 rb = p * kPart;
+    for (u32 r = threadIdx.x; r < nr; r += kPrefixThreads) {  // runs of a part have distinct slots
+      const u32 z = a.run_slot[rb + r];
+      const u32 c0 = cnt[z];
+      const i32 l0 = last[z];
+      const u32 cr = a.run_cnt[rb + r];
+      const i32 lr = a.run_last[rb + r];
+      a.run_cnt[rb + r] = c0;
+      a.run_last[rb + r] = l0;
+      cnt[z] = min(c0 + cr, u32(a.count_cap));
+      last[z] = lr;
+    }
+    __syncthreads();
+  }
+}
+
+// Phase C: scores before the bonus, per chunk the latest start.
+__global__ void __launch_bounds__(kPartThreads) k_rp_scores(RP a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  PartSmem &S = *reinterpret_cast<PartSmem *>(smraw);
+  const i64 p = blockIdx.x;
+  i64 r0;
+  int m;
+  const u32 *sk;
+  const unsigned short *sv;
+  part_load_sort(a, S, p, r0, m, sk, sv, true);
+  int rid[kPartItems], rst[kPartItems], nr;
+  part_runs(S, sk, m, rid, rst, nr);
+  const int k0 = threadIdx.x * kPartItems;
+  const i64 rb = p * kPart;
+#pragma unroll
+  for (int j = 0; j < kPartItems; ++j) {
+    const int k = k0 + j;
+    if (k >= m) break;
+    const int i = sv[k];
+    const u32 c = min(a.run_cnt[rb + rid[j]] + u32(k - rst[j] + 1), u32(a.count_cap));
+    const i32 prev = k > rst[j] ? S.end[sv[k - 1]] : a.run_last[rb + rid[j]];
+    const u32 gap = prev >= 0 ? u32(S.end[i] - prev) : 0u;
+    // gap / period by a reciprocal, corrected to the exact quotient
+    u32 kk = u32(double(gap) * a.inv_period);
+    if (u64(kk) * u64(a.period) > u64(gap)) --kk;
+    if (u64(kk + 1u) * u64(a.period) <= u64(gap)) ++kk;
+    const u64 d = __ldg(&a.dq[kk < u32(a.ndq) ? kk : u32(a.ndq - 1)]);
+    a.sc[r0 + i] = u64(S.len[i]) * u64(c) * d;
+  }
+  // per chunk of 32 records (original order): the latest start
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int ch = warp; ch < kChunksPerPart; ch += kPartWarps) {
+    const int i = ch * 32 + lane;
+    const int st = i < m ? S.end[i] - int(S.len[i]) + 1 : -1;
+    const int mx = __reduce_max_sync(0xffffffffu, st);
+    if (lane == 0) a.cmax[p * kChunksPerPart + ch] = mx;
   }
 }
 
@@ -100,31 +395,8 @@ __device__ __forceinline__ bool beats(u64 sa, u32 la, u32 ta, u64 sb, u32 lb, u3
   return ta < tb;
 }
 
-// Per-slot trace state: replayed bit, appearance count (saturated at the
-// cap: min(count, cap) is all the score uses) and last end + 1 (0 = never).
-// Wide: u64 [replayed:1][count:31][last end + 1:32]; narrow (count_cap <=
-// 127 and stream lengths < 2^24 - 1): u32 [replayed:1][count:7][last+1:24],
-// twice the slots on chip.
-template <class W>
-struct StateWord;
-template <>
-struct StateWord<u64> {
-  static constexpr u64 kRep = 1ull << 63;
-  __device__ static u32 count(u64 w) { return u32(w >> 32) & 0x7fffffffu; }
-  __device__ static u32 last1(u64 w) { return u32(w); }
-  __device__ static u64 make(u64 rep, u32 c, u32 l1) { return rep | (u64(c) << 32) | u64(l1); }
-};
-template <>
-struct StateWord<u32> {
-  static constexpr u32 kRep = 1u << 31;
-  __device__ static u32 count(u32 w) { return (w >> 24) & 0x7fu; }
-  __device__ static u32 last1(u32 w) { return w & 0xffffffu; }
-  __device__ static u32 make(u32 rep, u32 c, u32 l1) { return rep | (c << 24) | l1; }
-};
-
-// Warp arg-max of (score, len, -id) over the lanes with ok set: four
-// warp reductions (redux.sync) on the score's high and low words, the length
-// and the id; returns the winning lane (-1 if no lane is ok).
+// Warp arg-max of (score, len, -id) over the lanes with ok set: four warp
+// reductions (redux.sync); returns the winning lane (-1 if no lane is ok).
 __device__ __forceinline__ int warp_best(bool ok, u64 sc, u32 L, u32 t) {
   const u32 any = __ballot_sync(0xffffffffu, ok);
   if (!any) return -1;
@@ -143,50 +415,18 @@ __device__ __forceinline__ int warp_best(bool ok, u64 sc, u32 L, u32 t) {
   return __ffs(c) - 1;
 }
 
-// One warp per stream.  The hits are read in chunks of 32 consecutive
-// records, the next chunk (record + trace length) prefetched while the
-// current one is processed, so no global load sits on the sequential chain.
-// Per chunk, in parallel: each record's appearance count and gap (its
-// trace's previous appearance is the previous lane with the same slot in the
-// chunk -- __match_any_sync -- or the saved state) and its score before the
-// replay bonus; the last lane of each slot writes the state back.  Then the
-// decisions: a record is eligible iff it starts at or after the frontier;
-// the first eligible record of the chunk marks the next end where a replay
-// happens, and since an end's records are in trace-id order (length
-// descending) its eligible records are the rest of that end's run.  Only
-// such ends are visited: the bonus (the replayed bit may have been set by an
-// earlier end of the chunk), the arg-max over the eligible records, merged
-// with the running best when the end continues into the next chunk; the
-// replay moves the frontier and eligibility is re-evaluated for the later
-// records of the chunk.  Ends without an eligible record cost one ballot per
-// chunk.
-__device__ __forceinline__ int4 replay_rec(const ReplayArgs &a, i64 k, i64 he) {
-  return k < he ? a.hits[k] : make_int4(-1, -1, -1, -1);
-}
-__device__ __forceinline__ u32 replay_len(const ReplayArgs &a, int4 r) {
-  return r.z >= 0 ? u32(__ldg(&a.tlen_off[r.z + 1]) - __ldg(&a.tlen_off[r.z])) : 0u;
-}
-
-template <class W>
-__global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs a) {
-  using SW = StateWord<W>;
-  constexpr W kReplayed = SW::kRep;
-  constexpr u32 kSlots = kReplayStateBytes / sizeof(W);
-  extern __shared__ __align__(8) unsigned char s_raw[];
-  W *s_state = reinterpret_cast<W *>(s_raw);
+// Phase D: one warp per stream, the decisions.
+__global__ void __launch_bounds__(32) k_rp_decide(RP a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
   const int q = a.order[blockIdx.x], lane = threadIdx.x;
-  const u32 lt = (1u << lane) - 1u;
   const i64 hb = a.hbeg[q], he = a.hbeg[q + 1];
-  const u32 ms = a.maxslot[q];
-  const bool onchip = ms <= kSlots;
-  W *st = onchip ? s_state : static_cast<W *>(a.gstate) + a.gstate_off[q];
-  for (u32 i = lane; i < ms; i += 32) st[i] = 0;
+  const u32 nw = (a.maxslot[q] + 31) / 32;
+  u32 *rep = nw <= a.on_chip_bits ? reinterpret_cast<u32 *>(smraw) : static_cast<u32 *>(a.gstate) + a.gstate_off[q];
+  for (u32 i = lane; i < nw; i += 32) rep[i] = 0u;
   __syncwarp();
   i64 frontier = 0;
   u32 nrep = 0;
   int4 *stage = a.stage + a.soff[q];
-  // running best of an eligible end that reaches the chunk's last lane: it
-  // may continue into the next chunk, which decides it
   bool have = false;
   int carry_e = -1;
   u64 bs = 0;
@@ -194,100 +434,76 @@ __global__ void __launch_bounds__(kReplayThreads) k_replay(ReplayArgs a) {
   auto commit = [&](int e0) {
     __syncwarp();
     if (lane == 0) {
-      const W sw = st[bslot];
-      stage[nrep] = make_int4(q, e0, int(bt), (sw & kReplayed) ? 0 : 1);
-      st[bslot] = sw | kReplayed;
+      const u32 mk = 1u << (bslot & 31);
+      const u32 old = rep[bslot >> 5];
+      stage[nrep] = make_int4(q, e0, int(bt), (old & mk) ? 0 : 1);
+      rep[bslot >> 5] = old | mk;
     }
     __syncwarp();
     ++nrep;
     frontier = i64(e0) + 1;
     have = false;
   };
-  // software pipeline: records kRecAhead chunks ahead, trace lengths
-  // kLenAhead chunks ahead (a record has kRecAhead - kLenAhead iterations to
-  // arrive before its trace length is looked up)
-  constexpr int kRecAhead = 10, kLenAhead = 5;
-  int4 R[kRecAhead];
-  u32 LS[kLenAhead];
-#pragma unroll
-  for (int k = 0; k < kRecAhead; ++k) R[k] = replay_rec(a, hb + 32 * k + lane, he);
-#pragma unroll
-  for (int k = 0; k < kLenAhead; ++k) LS[k] = replay_len(a, R[k]);
-  for (i64 p = hb; p < he; p += 32) {
-    const int4 r = R[0];
-    const u32 L = LS[0];
-#pragma unroll
-    for (int k = 0; k + 1 < kRecAhead; ++k) R[k] = R[k + 1];
-#pragma unroll
-    for (int k = 0; k + 1 < kLenAhead; ++k) LS[k] = LS[k + 1];
-    LS[kLenAhead - 1] = replay_len(a, R[kLenAhead - 1]);
-    R[kRecAhead - 1] = replay_rec(a, p + 32 * kRecAhead + lane, he);
-    const bool valid = p + lane < he;
-    // a carried end that does not continue here is decided first (before
-    // this chunk reads its trace states: the replay sets a replayed bit)
-    if (have && __shfl_sync(0xffffffffu, r.y, 0) != carry_e) commit(carry_e);
-    // ---- appearance counts, gaps and scores (parallel) ----
-    const u32 slot = valid ? u32(r.w) : 0xffffffffu;
-    const u32 peers = __match_any_sync(0xffffffffu, slot);
-    const u32 before = peers & lt;
-    u64 sc0 = 0;
-    const W w = valid ? st[slot] : W(0);
-    const int prev_lane = before ? 31 - __clz(before) : -1;
-    const int prev_e = __shfl_sync(0xffffffffu, r.y, prev_lane < 0 ? lane : prev_lane);
-    const u32 c0 = SW::count(w);
-    if (valid) {
-      const u32 c = min(c0 + u32(__popc(before)) + 1u, u32(a.count_cap));
-      u32 gap = 0;
-      if (prev_lane >= 0)
-        gap = u32(r.y - prev_e);
-      else if (SW::last1(w))
-        gap = u32(r.y) - (SW::last1(w) - 1u);
-      // gap / period by a reciprocal, corrected to the exact quotient
-      u32 kk = u32(double(gap) * a.inv_period);
-      if (u64(kk) * u64(a.period) > u64(gap)) --kk;
-      if (u64(kk + 1u) * u64(a.period) <= u64(gap)) ++kk;
-      const u64 d = __ldg(&a.dq[kk < u32(a.ndq) ? kk : u32(a.ndq - 1)]);
-      sc0 = u64(L) * u64(c) * d;
-    }
-    __syncwarp();
-    if (valid && (peers >> lane) == 1u)  // the slot's last record in the chunk
-      st[slot] = SW::make(w & kReplayed, min(c0 + u32(__popc(peers)), u32(a.count_cap)), u32(r.y) + 1u);
-    __syncwarp();
-    // ---- decisions at the ends with an eligible record ----
-    u32 done = 0;  // lanes at or before the last decided end of this chunk
-    for (;;) {
-      const bool elig = valid && !((done >> lane) & 1u) && i64(r.y) - i64(L) + 1 >= frontier;
-      const u32 em = __ballot_sync(0xffffffffu, elig);
-      if (!em) break;
-      // the end to decide: the first eligible record's (with a carried end,
-      // that is the same end: its records lead this chunk)
-      const int a0 = __ffs(em) - 1;
-      const int e0 = __shfl_sync(0xffffffffu, r.y, a0);
-      const bool run = valid && r.y == e0;
-      const u32 rm = __ballot_sync(0xffffffffu, run);
-      const int a1 = 32 - __clz(rm);  // one past the run's last lane
-      const bool ok = elig && run;
-      u64 sc = sc0;
-      if (ok && (st[slot] & kReplayed)) sc = sc * a.bonus_num / a.bonus_den;
-      const int b = warp_best(ok, sc, L, u32(r.z));
-      if (b >= 0) {
-        const u64 s1 = __shfl_sync(0xffffffffu, sc, b);
-        const u32 l1 = __shfl_sync(0xffffffffu, L, b), t1 = __shfl_sync(0xffffffffu, u32(r.z), b);
-        const u32 z1 = __shfl_sync(0xffffffffu, slot, b);
-        if (!have || beats(s1, l1, t1, bs, bl, bt)) {
-          bs = s1;
-          bl = l1;
-          bt = t1;
-          bslot = z1;
-          have = true;
+  const i64 nch = (he - hb + 31) / 32;
+  const i64 p0 = a.pbeg[q];
+  for (i64 c0 = 0; c0 < nch; c0 += 32) {
+    const i64 c = c0 + lane;
+    const int mx = c < nch ? a.cmax[(p0 + c / kChunksPerPart) * kChunksPerPart + c % kChunksPerPart] : -1;
+    u32 pend = __ballot_sync(0xffffffffu, c < nch);
+    while (pend) {
+      // next chunk with a record starting at or after the frontier
+      const u32 cand = pend & __ballot_sync(0xffffffffu, i64(mx) >= frontier);
+      const int l = cand ? __ffs(cand) - 1 : 32;
+      // a carried end does not continue into a skipped chunk: decide it
+      if (have && (l == 32 || l != __ffs(pend) - 1)) commit(carry_e);
+      if (l == 32) break;
+      pend &= ~((2u << l) - 1u);
+      // the chunk's records
+      const i64 k = hb + (c0 + l) * 32 + lane;
+      const bool valid = k < he;
+      int4 r = make_int4(-1, -1, -1, 0);
+      u64 sc0 = 0;
+      u32 L = 0;
+      if (valid) {
+        r = a.hits[k];
+        sc0 = a.sc[k];
+        L = u32(__ldg(&a.tlen_off[r.z + 1]) - __ldg(&a.tlen_off[r.z]));
+      }
+      if (have && __shfl_sync(0xffffffffu, r.y, 0) != carry_e) commit(carry_e);
+      const u32 slot = u32(r.w);
+      u32 done = 0;
+      for (;;) {
+        const bool elig = valid && !((done >> lane) & 1u) && i64(r.y) - i64(L) + 1 >= frontier;
+        const u32 em = __ballot_sync(0xffffffffu, elig);
+        if (!em) break;
+        const int a0 = __ffs(em) - 1;
+        const int e0 = __shfl_sync(0xffffffffu, r.y, a0);
+        const bool run = valid && r.y == e0;
+        const u32 rm = __ballot_sync(0xffffffffu, run);
+        const int a1 = 32 - __clz(rm);
+        const bool ok = elig && run;
+        u64 sc = sc0;
+        if (ok && ((rep[slot >> 5] >> (slot & 31)) & 1u)) sc = sc * a.bonus_num / a.bonus_den;
+        const int b = warp_best(ok, sc, L, u32(r.z));
+        if (b >= 0) {
+          const u64 s1 = __shfl_sync(0xffffffffu, sc, b);
+          const u32 l1 = __shfl_sync(0xffffffffu, L, b), t1 = __shfl_sync(0xffffffffu, u32(r.z), b);
+          const u32 z1 = __shfl_sync(0xffffffffu, slot, b);
+          if (!have || beats(s1, l1, t1, bs, bl, bt)) {
+            bs = s1;
+            bl = l1;
+            bt = t1;
+            bslot = z1;
+            have = true;
+          }
         }
+        done |= rm | ((1u << a1) - 1u);
+        if (a1 == 32) {  // the end may continue into the next chunk
+          carry_e = e0;
+          break;
+        }
+        commit(e0);
       }
-      done |= rm | ((1u << a1) - 1u);
-      if (a1 == 32) {  // the end may continue into the next chunk
-        carry_e = e0;
-        break;
-      }
-      commit(e0);
     }
   }
   if (have) commit(carry_e);
@@ -328,6 +544,8 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
           "invalid replay parameters");
   APO_CUDA(cudaMemsetAsync(d_count, 0, sizeof(i64), s));
   if (nhits == 0 || nstreams == 0) return;
+  const int slot_bits = std::max(1, bits_for(u64(std::max<i64>(tr->T, 2) - 1)));
+  require(slot_bits <= 3 * kMaxDigit, "too many traces for REPLAY (slots must fit 27 bits)");
   // decay table d_k = d_{k-1} * decay >> 16 (the oracle's recurrence), up to
   // the longest possible gap / period, or until it stops changing
   i64 maxlen = 0, tot = 0;
@@ -345,21 +563,59 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
     dq.push_back(nx);
     if (nx == dq[dq.size() - 2]) break;  // fixed point (0, or no decay): later entries equal it
   }
+  // stream ranges (device binary searches), then the part plan on the host
+  const size_t hb_bytes = sizeof(i64) * (size_t(nstreams) + 1);
+  i64 *hbeg0 = static_cast<i64 *>(c.pool_get(hb_bytes));
+  k_replay_ranges<<<grid_for(i64(nstreams) + 1, 256), 256, 0, s>>>(reinterpret_cast<const int4 *>(d_hits), nhits,
+                                                                  nstreams, hbeg0);
+  APO_CHECK_LAUNCH();
+  c.launches++;
+  std::vector<i64> h_hb(size_t(nstreams) + 1);
+  APO_CUDA(cudaMemcpyAsync(h_hb.data(), hbeg0, hb_bytes, cudaMemcpyDeviceToHost, s));
+  APO_CUDA(cudaStreamSynchronize(s));
+  std::vector<i64> h_pb(size_t(nstreams) + 1);
+  i64 nparts = 0;
+  for (int q = 0; q < nstreams; ++q) {
+    h_pb[q] = nparts;
+    nparts += (h_hb[q + 1] - h_hb[q] + kPart - 1) / kPart;
+  }
+  h_pb[nstreams] = nparts;
+  if (nparts == 0) {
+    c.pool_put(hbeg0, hb_bytes);
+    return;
+  }
+  std::vector<int> h_ps(static_cast<size_t>(nparts));
+  for (int q = 0; q < nstreams; ++q)
+    for (i64 p = h_pb[q]; p < h_pb[q + 1]; ++p) h_ps[p] = q;
+  std::vector<int> h_order(static_cast<size_t>(nstreams));
+  for (int q = 0; q < nstreams; ++q) h_order[q] = q;
+  std::stable_sort(h_order.begin(), h_order.end(),
+                   [&](int x, int y) { return h_hb[x + 1] - h_hb[x] > h_hb[y + 1] - h_hb[y]; });
   // workspace
-  i64 *hbeg, *soff, *tbase, *gso;
-  u32 *maxslot, *rcnt, *rbase, *ddq;
-  int *order;
+  i64 *hbeg, *pbeg, *soff, *gso;
+  int *pstream, *order;
+  u32 *maxslot, *run_slot, *run_cnt, *nruns, *rcnt, *rbase, *ddq;
+  i32 *run_last, *cmax;
+  u64 *sc;
   int4 *stage;
+  const size_t npart_rec = size_t(nparts) * kPart;
   auto plan = [&](Carver &cv) {
     hbeg = cv.take<i64>(size_t(nstreams) + 1);
+    pbeg = cv.take<i64>(size_t(nstreams) + 1);
     soff = cv.take<i64>(size_t(nstreams) + 1);
     gso = cv.take<i64>(size_t(nstreams) + 1);
-    tbase = cv.take<i64>(4);
+    pstream = cv.take<int>(size_t(nparts));
+    order = cv.take<int>(size_t(nstreams));
     maxslot = cv.take<u32>(size_t(nstreams));
     rcnt = cv.take<u32>(size_t(nstreams));
     rbase = cv.take<u32>(size_t(nstreams));
-    order = cv.take<int>(size_t(nstreams));
+    nruns = cv.take<u32>(size_t(nparts));
     ddq = cv.take<u32>(dq.size());
+    cmax = cv.take<i32>(size_t(nparts) * kChunksPerPart);
+    run_slot = cv.take<u32>(npart_rec);
+    run_cnt = cv.take<u32>(npart_rec);
+    run_last = cv.take<i32>(npart_rec);
+    sc = cv.take<u64>(size_t(nhits));
     stage = cv.take<int4>(size_t(tot));
   };
   Carver dry(nullptr);
@@ -367,49 +623,52 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   c.arena.reserve(dry.off, s);
   Carver cv(c.arena.base);
   plan(cv);
-  APO_CUDA(cudaMemcpyAsync(soff, h_soff.data(), sizeof(i64) * (size_t(nstreams) + 1), cudaMemcpyHostToDevice, s));
+  APO_CUDA(cudaMemcpyAsync(hbeg, hbeg0, hb_bytes, cudaMemcpyDeviceToDevice, s));
+  APO_CUDA(cudaMemcpyAsync(pbeg, h_pb.data(), hb_bytes, cudaMemcpyHostToDevice, s));
+  APO_CUDA(cudaMemcpyAsync(soff, h_soff.data(), hb_bytes, cudaMemcpyHostToDevice, s));
+  APO_CUDA(cudaMemcpyAsync(pstream, h_ps.data(), sizeof(int) * size_t(nparts), cudaMemcpyHostToDevice, s));
+  APO_CUDA(cudaMemcpyAsync(order, h_order.data(), sizeof(int) * size_t(nstreams), cudaMemcpyHostToDevice, s));
   APO_CUDA(cudaMemcpyAsync(ddq, dq.data(), sizeof(u32) * dq.size(), cudaMemcpyHostToDevice, s));
-  const int4 *hits = reinterpret_cast<const int4 *>(d_hits);
-  k_replay_ranges<<<nstreams + 1, 256, 0, s>>>(hits, nhits, nstreams, hbeg, maxslot);
+  APO_CUDA(cudaMemsetAsync(maxslot, 0, sizeof(u32) * size_t(nstreams), s));
+  RP a{reinterpret_cast<const int4 *>(d_hits), tr->d_off, ddq, int(dq.size()), prm.count_cap, prm.decay_period,
+       1.0 / double(prm.decay_period), u32(prm.bonus_num), u32(prm.bonus_den), nstreams, slot_bits, hbeg, pbeg,
+       pstream, maxslot, run_slot, run_cnt, run_last, nruns, sc, cmax, order, nullptr, gso, 0u, 0u, soff, stage,
+       rcnt};
+  const size_t psmem = sizeof(PartSmem);
+  c.smem_optin(reinterpret_cast<const void *>(k_rp_local), psmem);
+  c.smem_optin(reinterpret_cast<const void *>(k_rp_scores), psmem);
+  k_rp_local<<<unsigned(nparts), kPartThreads, psmem, s>>>(a);
   APO_CHECK_LAUNCH();
-  c.launches++;
-  // global state only for streams whose slots do not fit on chip
+  // per-stream tables: on chip when they fit, else in a global block
   std::vector<u32> h_ms(static_cast<size_t>(nstreams));
   APO_CUDA(cudaMemcpyAsync(h_ms.data(), maxslot, sizeof(u32) * size_t(nstreams), cudaMemcpyDeviceToHost, s));
   APO_CUDA(cudaStreamSynchronize(s));
-  const bool narrow = prm.count_cap <= 127 && maxlen < (i64(1) << 24) - 1;
-  const size_t wbytes = narrow ? sizeof(u32) : sizeof(u64);
-  const u32 kslots = u32(kReplayStateBytes / wbytes);
+  const u32 slots_on_chip = u32(kStateBytesMax / 8);
   std::vector<i64> h_gso(size_t(nstreams) + 1);
-  i64 gtot = 0;
+  i64 gw = 0;
+  u32 smax_b = 1, smax_d = 1;
   for (int q = 0; q < nstreams; ++q) {
-    h_gso[q] = gtot;
-    if (h_ms[q] > kslots) gtot += h_ms[q];
+    h_gso[q] = gw;
+    if (h_ms[q] > slots_on_chip)
+      gw += 2 * i64(h_ms[q]);  // phase B's (count, last) table; phase D's bitset fits in it
+    else
+      smax_b = std::max(smax_b, h_ms[q]);
+    if ((h_ms[q] + 31) / 32 <= slots_on_chip / 32) smax_d = std::max(smax_d, (h_ms[q] + 31) / 32);
   }
-  h_gso[nstreams] = gtot;
+  h_gso[nstreams] = gw;
   void *gstate = nullptr;
-  if (gtot > 0) gstate = c.pool_get(wbytes * size_t(gtot));
-  APO_CUDA(cudaMemcpyAsync(gso, h_gso.data(), sizeof(i64) * (size_t(nstreams) + 1), cudaMemcpyHostToDevice, s));
-  // streams with the most hits first (the per-stream walks are sequential:
-  // the longest ones must start in the first wave)
-  std::vector<i64> h_hb(size_t(nstreams) + 1);
-  APO_CUDA(cudaMemcpy(h_hb.data(), hbeg, sizeof(i64) * (size_t(nstreams) + 1), cudaMemcpyDeviceToHost));
-  std::vector<int> h_order(static_cast<size_t>(nstreams));
-  for (int q = 0; q < nstreams; ++q) h_order[q] = q;
-  std::stable_sort(h_order.begin(), h_order.end(),
-                   [&](int x, int y) { return h_hb[x + 1] - h_hb[x] > h_hb[y + 1] - h_hb[y]; });
-  APO_CUDA(cudaMemcpyAsync(order, h_order.data(), sizeof(int) * size_t(nstreams), cudaMemcpyHostToDevice, s));
-  ReplayArgs a{hits, nhits, nstreams, tr->d_off, ddq, int(dq.size()), prm.count_cap, prm.decay_period,
-               1.0 / double(prm.decay_period), u32(prm.bonus_num), u32(prm.bonus_den), hbeg, maxslot, gstate,
-               gso, soff, stage, rcnt, order};
-  u32 smax = 0;
-  for (int q = 0; q < nstreams; ++q)
-    if (h_ms[q] <= kslots) smax = std::max(smax, h_ms[q]);
-  const size_t rsmem = wbytes * std::max<size_t>(smax, 2);
-  if (narrow)
-    k_replay<u32><<<nstreams, kReplayThreads, rsmem, s>>>(a);
-  else
-    k_replay<u64><<<nstreams, kReplayThreads, rsmem, s>>>(a);
+  if (gw > 0) gstate = c.pool_get(sizeof(u32) * size_t(gw));
+  APO_CUDA(cudaMemcpyAsync(gso, h_gso.data(), hb_bytes, cudaMemcpyHostToDevice, s));
+  a.gstate = gstate;
+  a.on_chip_slots = slots_on_chip;
+  a.on_chip_bits = slots_on_chip / 32;
+  const size_t bsmem = size_t(smax_b) * 8;
+  c.smem_optin(reinterpret_cast<const void *>(k_rp_prefix), bsmem);
+  k_rp_prefix<<<nstreams, kPrefixThreads, bsmem, s>>>(a);
+  APO_CHECK_LAUNCH();
+  k_rp_scores<<<unsigned(nparts), kPartThreads, psmem, s>>>(a);
+  APO_CHECK_LAUNCH();
+  k_rp_decide<<<nstreams, 32, size_t(smax_d) * 4, s>>>(a);
   APO_CHECK_LAUNCH();
   ReplayScanF f{rcnt, rbase, nstreams, d_count};
   launch_scan<false>(c, nstreams, f, s);
@@ -417,9 +676,10 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
     k_replay_compact<<<nstreams, 128, 0, s>>>(stage, soff, rcnt, rbase, cap, reinterpret_cast<int4 *>(d_out));
     APO_CHECK_LAUNCH();
   }
-  c.launches += 2;
+  c.launches += 5;
   APO_CUDA(cudaStreamSynchronize(s));
-  if (gstate) c.pool_put(gstate, wbytes * size_t(gtot));
+  if (gstate) c.pool_put(gstate, sizeof(u32) * size_t(gw));
+  c.pool_put(hbeg0, hb_bytes);
 }
 
 }  // namespace apo

@@ -229,7 +229,7 @@ __global__ void k_lcp_gather(const u32 *__restrict__ sa, const i32 *__restrict__
 
 }  // namespace
 
-void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp) {
+void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp, int nsmid) {
   const i64 N = b.N;
   w.keys = cv.take<u64>(N);
   w.keys_alt = cv.take<u64>(N);
@@ -244,7 +244,7 @@ void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp) {
   for (int r = 0; r < w.max_levels; ++r) w.levels[r] = cv.take<i32>(N);
   w.sa = cv.take<i32>(N);
   w.rw = k9 ? cv.take<i32>(size_t(b.W)) : nullptr;
-  w.win_scratch = k9 ? cv.take<char>(window_sa_scratch_bytes(b)) : nullptr;
+  w.win_scratch = k9 ? cv.take<char>(window_sa_scratch_bytes(nsmid)) : nullptr;
   w.ids = cv.take<u32>(N);
   w.ids_valid = false;
   w.ht_cap = 1u << 21;  // up to 1M distinct tokens; 24 MB of L2-friendly tables

@@ -295,10 +295,10 @@ struct GenPlan {
   i32 *d_wid = nullptr;
 };
 
-void plan_gen(Carver &cv, Batch &b, GenPlan &g, bool lcp) {
+void plan_gen(Carver &cv, Batch &b, GenPlan &g, bool lcp, int nsmid) {
   g.d_off = cv.take<i64>(size_t(b.W) + 1);
   g.d_wid = cv.take<i32>(size_t(b.N));
-  plan_sa(cv, b, g.sa, lcp);
+  plan_sa(cv, b, g.sa, lcp, nsmid);
 }
 
 void upload_batch(Ctx &c, Batch &b, GenPlan &g, const std::vector<i64> &h_off, cudaStream_t s) {
@@ -1689,7 +1689,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       // streams that fit on chip are matched in reversed form (see k_stream_emit)
       const bool rev = maxs <= kSMMax;
       auto plan = [&](Carver &cv) {
-        plan_gen(cv, b, g, true);
+        plan_gen(cv, b, g, true, c.nsmid);
         if (rev) d_rs = cv.take<u64>(Ns);
         e_tok = cv.take<u64>(Ns);
         e_tok_alt = cv.take<u64>(Ns);
@@ -1932,7 +1932,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
     i64 *ilo = nullptr, *scal = nullptr;
     u32 *ibase = nullptr, *icnt = nullptr;
     auto plan = [&](Carver &cv) {
-      plan_gen(cv, b, g, false);
+      plan_gen(cv, b, g, false, c.nsmid);
       ilo = cv.take<i64>(T);
       ibase = cv.take<u32>(T);
       icnt = cv.take<u32>(T);

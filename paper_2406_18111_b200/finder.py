@@ -99,7 +99,8 @@ class TraceFinder:
     """Online history + ruler-scheduled asynchronous analyses + ingestion at
     agreed op counts.  `ingest(tokens)` appends ops and returns the
     ingestion events of the call: (op count, anyone waited, traces in the set
-    after, delay after).  `trie` is the current candidate trace set."""
+    after, delay after, launch op count of the analysis).  `trie` is the
+    current candidate trace set."""
 
     def __init__(self, history, analyzer, builder, delay: int, group=None, allreduce_max=None):
         if int(delay) < 1:
@@ -140,7 +141,7 @@ class TraceFinder:
             if anyw:
                 self.delay *= 2
             self._take(fut)
-            self.events.append((self.count, anyw, self.builder.size(self.trie), self.delay))
+            self.events.append((self.count, anyw, self.builder.size(self.trie), self.delay, k0))
 
     def ingest(self, tokens) -> list:
         """Append ops in pieces that stop at every due point and at every
@@ -172,3 +173,129 @@ class TraceFinder:
         """End of the stream: wait for every pending analysis and ingest it."""
         while self.pending:
             self._take(self.pending.popleft()[2])
+
+
+class BatchPipeline:
+    """Batches of independent windows and their matching streams with the
+    analysis of batch k+1 overlapped with the trace set, matching and replay
+    of batch k ("async FindRepeats").
+
+    The analysis (apo_find_repeats_batched) runs on its own library context
+    and CUDA stream, driven by a worker thread; the rest of a batch (trace
+    set, optional cross-GPU union, apo_match) runs on the caller's current
+    stream, which waits for the batch's analysis with a CUDA event.  Two
+    output buffer sets alternate between batches.  Results are identical to
+    running the batches one after the other (the same library calls on the
+    same inputs; only their overlap changes).
+
+    run(batches) takes an iterable of (tok, off, streams, soff, ready) --
+    device tokens and host offsets; `ready` is a CUDA event the inputs are
+    complete at (or None) -- and yields, per batch, (repeats, repeat
+    offsets, occurrences, counts, match result): repeats etc. as
+    find_repeats_batched(sync=False) returns them (valid until the loop asks
+    for the next batch: the analysis after next reuses them), the match
+    result as Context.match(mode=...) returns it.
+    """
+
+    def __init__(self, ctx, min_len: int, min_count: int = 1, max_len: int = 0, mode: int = 1, exchange=None):
+        from .apo import Context
+        self.ctx = ctx
+        self.min_len, self.min_count, self.max_len, self.mode = min_len, min_count, max_len, mode
+        self.exchange = exchange
+        dev = ctx.device if isinstance(ctx.device, torch.device) else torch.device("cuda", ctx.device)
+        self.dev = dev
+        self.actx = Context(dev.index)
+        # the analysis runs at the lowest stream priority, the rest of a
+        # batch at the highest: when a CTA slot frees up, the block
+        # scheduler serves matching / replay first, the analysis fills the
+        # rest (K9 is not persistent, so it yields SMs window by window)
+        least, greatest = torch.cuda.Stream.priority_range()
+        self.astream = torch.cuda.Stream(dev, priority=least)
+        self.hstream = torch.cuda.Stream(dev, priority=greatest)
+        self.pool = ThreadPoolExecutor(1)
+        self.bufs = [None, None]
+        self.match_cap = 1 << 20
+        self.hit_cap = 1 << 22
+        self.last_hits = 0
+        self.last_traces = 0
+
+    def _buffers(self, k: int, n: int, W: int):
+        b = self.bufs[k]
+        cap = n // max(self.min_len, 1) + 1
+        if b is None or b[0].shape[0] < cap or b[1].numel() != W + 1:
+            b = (torch.empty((cap, 4), dtype=torch.int32, device=self.dev),
+                 torch.empty(W + 1, dtype=torch.int64, device=self.dev),
+                 torch.empty(cap, dtype=torch.int32, device=self.dev),
+                 torch.zeros(2, dtype=torch.int64, device=self.dev))
+            self.bufs[k] = b
+        return b
+
+    def _analyse(self, k: int, tok, off, ready):
+        out = self._buffers(k, int(off[-1]), len(off) - 1)
+
+        def run():
+            with torch.cuda.stream(self.astream):
+                if ready is not None:
+                    self.astream.wait_event(ready)
+                r = self.actx.find_repeats_batched(tok, off, self.min_len, self.min_count, sync=False, out=out)
+                done = torch.cuda.Event()
+                done.record(self.astream)
+            return r, done
+        return self.pool.submit(run)
+
+    def run(self, batches):
+        it = iter(batches)
+        cur = next(it, None)
+        if cur is None:
+            return
+        caller = torch.cuda.current_stream(self.dev)
+        s = self.hstream
+        s.wait_stream(caller)
+        self.astream.wait_stream(caller)
+        fut = self._analyse(0, cur[0], cur[1], cur[4])
+        k = 0
+        while cur is not None:
+            (rep, roff, occ, counts), done = fut.result()  # batch k analysed (enqueued and host-complete)
+            nxt = next(it, None)
+            tok, off, streams, soff, ready = cur
+            s.wait_event(done)
+            if ready is not None:
+                s.wait_event(ready)
+            res = None
+            launched = False
+            torch.cuda.set_stream(s)
+            if streams is not None:
+                trie = self.ctx.trie_build(tok, off, rep, roff, self.min_len, self.max_len)
+                if self.exchange is not None:
+                    trie = self.exchange.union(trie)
+                if self.mode == 1:
+                    # MATCH_ALL, then the next batch's analysis is launched
+                    # while REPLAY runs: the replay's per-stream walks are
+                    # sequential, so as light streams finish their SMs go to
+                    # the analysis kernels (both saturate the SMs otherwise)
+                    hits = self.ctx.match(trie, streams, soff, full=True, cap=self.hit_cap)
+                    self.hit_cap = max(int(hits.shape[0]), 1)
+                    if nxt is not None:
+                        fut = self._analyse((k + 1) % 2, nxt[0], nxt[1], nxt[4])
+                        launched = True
+                    rp = self.ctx.replay(trie, hits, np.diff(np.asarray(soff, dtype=np.int64)), cap=self.match_cap)
+                    self.match_cap = max(int(rp.shape[0]), 1)
+                    self.last_hits = int(hits.shape[0])
+                    res = (rp, self.last_hits)
+                    del hits
+                else:
+                    if nxt is not None:
+                        fut = self._analyse((k + 1) % 2, nxt[0], nxt[1], nxt[4])
+                        launched = True
+                    res = self.ctx.match(trie, streams, soff, mode=self.mode, cap=self.match_cap)
+                self.last_traces = trie.info()[0]
+            if nxt is not None and not launched:
+                fut = self._analyse((k + 1) % 2, nxt[0], nxt[1], nxt[4])
+            torch.cuda.set_stream(caller)
+            caller.wait_stream(s)  # the caller's later work sees this batch's results
+            yield rep, roff, occ, counts, res
+            cur = nxt
+            k += 1
+
+    def close(self):
+        self.pool.shutdown(wait=True)

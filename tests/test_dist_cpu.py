@@ -4,6 +4,7 @@ import os
 import socket
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -314,7 +315,7 @@ def test_trace_finder_agreement_gloo_world2():
     assert ev0 == ev1 and tr0 == tr1 and len(ev0) > 10
     # the delay doubles exactly when someone waited, and only then
     d = 128
-    for count, anyw, size, delay in ev0:
+    for count, anyw, size, delay, k0 in ev0:
         if anyw:
             d *= 2
         assert delay == d
@@ -326,3 +327,110 @@ def test_trace_finder_agreement_gloo_world2():
     # (launch points: multiples of C = 128), in launch order
     counts = [e[0] for e in ev0]
     assert counts == sorted(counts)
+
+
+# ---------------------------------------------------------------------------
+# Distributed suffix array: DistSuffixArray's
+# orchestration -- the rank2 shift exchange, the sample sort (samples,
+# splitters, all-to-all), the head/rank carry across rank boundaries, the
+# return to the position owners -- on 2 and 3 gloo ranks, with numpy
+# stand-ins for the library steps (test infrastructure: each mirrors the
+# documented contract of its apo_dsa_* call).  Expected: the oracle's suffix
+# array (naive comparison sort, tier 0).
+
+class _NpDsaOps:
+    device = torch.device("cpu")
+
+    def empty(self, n, dtype):
+        return torch.empty(max(int(n), 0), dtype=dtype)
+
+    def sort(self, keys, vals, bits):
+        k = keys.view(torch.int64).numpy().view(np.uint64)
+        mk = k & np.uint64((1 << bits) - 1) if bits < 64 else k
+        o = np.argsort(mk, kind="stable")
+        kk, vv = k[o].copy(), vals.numpy()[o].copy()
+        keys.view(torch.int64).numpy()[:] = kk.view(np.int64)
+        vals.numpy()[:] = vv
+
+    def keys(self, rank, rank2, base, n):
+        m = rank.numel()
+        r2 = np.zeros(m, np.uint64)
+        r2[:rank2.numel()] = rank2.numpy().astype(np.uint64)
+        k = rank.numpy().astype(np.uint64) * np.uint64(n + 1) + r2
+        return torch.from_numpy(k.view(np.int64)).view(torch.uint64), torch.arange(base, base + m, dtype=torch.int32)
+
+    def samples(self, keys, vals, s):
+        m = keys.numel()
+        k = keys.view(torch.int64).numpy().view(np.uint64)
+        v = vals.numpy()
+        idx = [min((j * m) // s + (m // s) // 2, m - 1) for j in range(s)]
+        sk = np.array([k[i] if m else np.uint64((1 << 64) - 1) for i in idx], dtype=np.uint64)
+        sv = np.array([v[i] if m else -1 for i in idx], dtype=np.int32)
+        return torch.from_numpy(sk.view(np.int64)).view(torch.uint64), torch.from_numpy(sv)
+
+    def split(self, keys, vals, spk, spv, g):
+        k = [int(x) for x in keys.view(torch.int64).numpy().view(np.uint64)]
+        v = [int(x) & 0xffffffff for x in vals.numpy()]
+        sp = list(zip([int(x) for x in spk.view(torch.int64).numpy().view(np.uint64)],
+                      [int(x) & 0xffffffff for x in spv.numpy()]))
+        bounds = [0] + [sum(1 for p in zip(k, v) if p < s) for s in sp] + [len(k)]
+        return torch.tensor([max(bounds[d + 1] - bounds[d], 0) for d in range(g)], dtype=torch.int64)
+
+    def heads(self, keys, prev_key, has_prev, gbase, carry):
+        k = [int(x) for x in keys.view(torch.int64).numpy().view(np.uint64)]
+        rank, cur, h, last = [], carry, 0, -1
+        for i, x in enumerate(k):
+            if (i == 0 and (not has_prev or x != prev_key)) or (i > 0 and x != k[i - 1]):
+                cur = gbase + i
+                h += 1
+                last = cur
+            rank.append(cur + 1)
+        return torch.tensor(rank, dtype=torch.int32), h, last
+
+    def scatter(self, pos, rank_in, base, rank):
+        rank.numpy()[pos.numpy() - base] = rank_in.numpy()
+
+
+def _dsa_strings():
+    from workloads import gen
+    return [gen.random_string(5, 300, 3), gen.periodic(6, 257, 7, 4, noise=0.05),
+            gen.fibonacci_word(200), gen.high_bit_string(7, 150, 5), gen.random_string(8, 1, 2)]
+
+
+def _dsa_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2406_18111_b200.dsa import DistSuffixArray
+    out = []
+    for S in _dsa_strings():
+        n = len(S)
+        a = [r * n // world for r in range(world + 1)]
+        blk = torch.from_numpy(S[a[rank]:a[rank + 1]].view(np.int64).copy()).view(torch.uint64)
+        d = DistSuffixArray(_NpDsaOps(), oversample=8)
+        part, g = d.run(blk, n)
+        out.append((g, part.numpy().copy(), d.rounds))
+    q.put((rank, out))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_dist_suffix_array_gloo(world):
+    import oracle
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dsa_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, out = q.get(timeout=240)
+        res[r] = out
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for i, S in enumerate(_dsa_strings()):
+        parts = sorted(((res[r][i][0], res[r][i][1]) for r in range(world)), key=lambda x: x[0])
+        got = np.concatenate([p for _, p in parts])
+        assert [g for g, _ in parts] == list(np.cumsum([0] + [len(p) for _, p in parts[:-1]]))
+        assert np.array_equal(got, oracle.sa_naive(S)), i
