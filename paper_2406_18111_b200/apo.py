@@ -82,6 +82,11 @@ _SIGS = {
     "apo_trie_copy": (ctypes.c_int, [_VP, _VP, _P_I64, _VP]),
     "apo_match": (ctypes.c_int, [_VP, _VP, _VP, _P_I64, _I32, _I32, _VP, _I64, _VP, _VP]),
     "apo_replay": (ctypes.c_int, [_VP, _VP, _VP, _I64, _P_I64, _I32, _VP, _VP, _I64, _VP, _VP]),
+    "apo_dsa_keys": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _I64, _I64, _VP, _VP, _VP]),
+    "apo_dsa_samples": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I32, _VP, _VP, _VP]),
+    "apo_dsa_split": (ctypes.c_int, [_VP, _VP, _VP, _I64, _VP, _VP, _I32, _VP, _VP]),
+    "apo_dsa_heads": (ctypes.c_int, [_VP, _VP, _I64, ctypes.c_uint64, _I32, _I64, _I64, _VP, _VP, _VP]),
+    "apo_dsa_scatter": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _VP, _VP]),
 }
 
 _lib = None

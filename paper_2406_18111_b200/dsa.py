@@ -46,21 +46,11 @@ class CudaDsaOps:
     """The per-rank compute steps on the GPU (libapo's apo_dsa_* and K1)."""
 
     def __init__(self, ctx):
-        import ctypes
         from . import apo
         self.ctx = ctx
-        self.lib = ctx.lib
+        self.lib = ctx.lib  # signatures set by apo.load_library
         self.apo = apo
         self.device = ctx.device if isinstance(ctx.device, torch.device) else torch.device("cuda", ctx.device)
-        L = self.lib
-        VP, I64, I32, U64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64
-        L.apo_dsa_keys.argtypes = [VP, VP, VP, I64, I64, I64, I64, VP, VP, VP]
-        L.apo_dsa_samples.argtypes = [VP, VP, VP, I64, I32, VP, VP, VP]
-        L.apo_dsa_split.argtypes = [VP, VP, VP, I64, VP, VP, I32, VP, VP]
-        L.apo_dsa_heads.argtypes = [VP, VP, I64, U64, I32, I64, I64, VP, VP, VP]
-        L.apo_dsa_scatter.argtypes = [VP, VP, VP, I64, I64, VP, VP]
-        for f in ("apo_dsa_keys", "apo_dsa_samples", "apo_dsa_split", "apo_dsa_heads", "apo_dsa_scatter"):
-            getattr(L, f).restype = ctypes.c_int
 
     def _s(self):
         return self.apo._stream(self.device)
