@@ -88,6 +88,13 @@ struct RP {
   const i64 *soff;       // per stream staging offset (stream position base)
   int4 *stage;           // staged replays
   u32 *rcnt;             // per stream replay count
+  // matcher index (apo_match mode 1, on-chip path): see ReplayIndex
+  const i64 *ix_off;
+  const i32 *ix_sa;
+  const u64 *ix_tkey;
+  const u32 *ix_toff;
+  const int *wq;         // wavelet work items: stream
+  const i64 *wr0;        // wavelet work items: first record (nitems + 1 ends)
 };
 
 __device__ __forceinline__ u32 lanemask_lt_() {
@@ -388,6 +395,151 @@ __global__ void __launch_bounds__(kPartThreads) k_rp_scores(RP a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Phases A-C from the matcher's index (apo_match mode 1, streams matched on
+// chip).  A hit (e, z) is an occurrence of slot z's trace ending at e; the
+// trace's occurrences are the ranks [lo_z, hi_z) of z's interval in the
+// REVERSED stream's suffix array, ending at E[r] = n - 1 - SA_rev[r].  So
+//   count(z, e) = #{r in [lo_z, hi_z) : E[r] <= e}   (appearances so far),
+//   prev(z, e)  = the (count - 1)-th smallest E[r] in the range (1-based),
+// two wavelet-matrix queries over E (14 levels for n <= 16,384, built in
+// shared memory per stream) -- no per-part sort, no cross-part prefix.  One
+// CTA per work item of <= 65,536 records of one stream (heavy streams get
+// several CTAs, each building the stream's matrix).
+constexpr int kWvThreads = 1024;
+constexpr int kWvMaxN = 16384;
+constexpr int kWvLevels = 14;
+constexpr int kWvWords = kWvMaxN / 32 + 1;
+constexpr i64 kWvPart = 65536;  // records per work item (a multiple of kPart)
+
+struct WvSmem {
+  u32 bits[kWvLevels][kWvWords];
+  unsigned short pre[kWvLevels][kWvWords];  // ones before each word
+  u32 zeros[kWvLevels];
+  unsigned short cur[kWvMaxN], nxt[kWvMaxN];
+  u32 wtot[kWvThreads / 32];
+};
+
+__device__ __forceinline__ u32 wv_rank1(const WvSmem &S, int l, u32 i) {
+  const u32 w = i >> 5, b = i & 31u;
+  return u32(S.pre[l][w]) + __popc(S.bits[l][w] & ((1u << b) - 1u));
+}
+
+__global__ void __launch_bounds__(kWvThreads) k_rp_wavelet(RP a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  WvSmem &S = *reinterpret_cast<WvSmem *>(smraw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = a.wq[blockIdx.x];
+  const i64 r0 = a.wr0[blockIdx.x], r1 = a.wr0[blockIdx.x + 1];
+  const i64 beg = a.ix_off[q];
+  const int n = int(a.ix_off[q + 1] - beg);
+  const u32 ntrees = a.ix_toff[q + 1] - a.ix_toff[q];
+  if (tid == 0 && r0 == a.hbeg[q]) a.maxslot[q] = ntrees;
+  const int L = max(1, 32 - __clz(u32(max(n - 1, 1))));
+  const int nw = (n + 31) / 32;
+  for (int r = tid; r < n; r += kWvThreads) S.cur[r] = (unsigned short)(n - 1 - (a.ix_sa[beg + r] - int(beg)));
+  __syncthreads();
+  unsigned short *cur = S.cur, *nxt = S.nxt;
+  for (int l = L - 1; l >= 0; --l) {
+    for (int w = warp; w <= nw; w += kWvThreads / 32) {
+      const int i = w * 32 + lane;
+      const u32 m = __ballot_sync(0xffffffffu, i < n && ((cur[i] >> l) & 1u));
+      if (lane == 0) S.bits[l][w] = m;
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive prefix of the ones per word, total zeros
+      u32 carry = 0;
+      for (int w0 = 0; w0 <= nw; w0 += 32) {
+        const u32 v = w0 + lane <= nw ? u32(__popc(S.bits[l][w0 + lane])) : 0u;
+        u32 x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (w0 + lane <= nw) S.pre[l][w0 + lane] = (unsigned short)(carry + x - v);
+        carry += __shfl_sync(0xffffffffu, x, 31);
+      }
+      if (lane == 0) S.zeros[l] = u32(n) - carry;
+    }
+    __syncthreads();
+    if (l > 0) {  // stable partition for the next level: zeros, then ones
+      const u32 Z = S.zeros[l];
+      for (int i = tid; i < n; i += kWvThreads) {
+        const u32 r1 = wv_rank1(S, l, u32(i));
+        const bool b = (cur[i] >> l) & 1u;
+        nxt[b ? Z + r1 : u32(i) - r1] = cur[i];
+      }
+      __syncthreads();
+      unsigned short *t = cur; cur = nxt; nxt = t;
+    }
+  }
+  // queries: warp-aligned chunks of 32 records of the stream
+  const u64 *tk = a.ix_tkey + a.ix_toff[q];
+  const i64 hb = a.hbeg[q], p0 = a.pbeg[q];
+  for (i64 kb = r0 + i64(warp) * 32; kb < r1; kb += kWvThreads) {
+    const i64 k = kb + lane;
+    int st = -1;
+    if (k < r1) {
+      const int4 rec = a.hits[k];
+      const u32 e = u32(rec.y);
+      const u64 kk = tk[rec.w];
+      u32 lo = u32(kk >> 15) & 32767u, hi = 32767u - (u32(kk) & 32767u);
+      // count of ends <= e in [lo, hi)
+      u32 cnt = 0;
+      const u32 x = e + 1u;
+      if (x >= (1u << L)) {
+        cnt = hi - lo;
+      } else {
+        u32 l0 = lo, h0 = hi;
+        for (int l = L - 1; l >= 0; --l) {
+          const u32 a1 = wv_rank1(S, l, l0), b1 = wv_rank1(S, l, h0);
+          if ((x >> l) & 1u) {
+            cnt += (h0 - l0) - (b1 - a1);
+            l0 = S.zeros[l] + a1;
+            h0 = S.zeros[l] + b1;
+          } else {
+            l0 -= a1;
+            h0 -= b1;
+          }
+        }
+      }
+      // previous end: the (cnt - 2)-th smallest (0-based) end in [lo, hi)
+      u32 gap = 0;
+      if (cnt >= 2) {
+        u32 kq = cnt - 2, v = 0, l0 = lo, h0 = hi;
+        for (int l = L - 1; l >= 0; --l) {
+          const u32 a1 = wv_rank1(S, l, l0), b1 = wv_rank1(S, l, h0);
+          const u32 zc = (h0 - l0) - (b1 - a1);
+          if (kq < zc) {
+            l0 -= a1;
+            h0 -= b1;
+          } else {
+            kq -= zc;
+            v |= 1u << l;
+            l0 = S.zeros[l] + a1;
+            h0 = S.zeros[l] + b1;
+          }
+        }
+        gap = e - v;
+      }
+      const u32 len = u32(__ldg(&a.tlen_off[rec.z + 1]) - __ldg(&a.tlen_off[rec.z]));
+      const u32 c = min(cnt, u32(a.count_cap));
+      u32 kq = u32(double(gap) * a.inv_period);
+      if (u64(kq) * u64(a.period) > u64(gap)) --kq;
+      if (u64(kq + 1u) * u64(a.period) <= u64(gap)) ++kq;
+      const u64 d = __ldg(&a.dq[kq < u32(a.ndq) ? kq : u32(a.ndq - 1)]);
+      a.sc[k] = u64(len) * u64(c) * d;
+      st = int(e) - int(len) + 1;
+    }
+    const int mx = __reduce_max_sync(0xffffffffu, st);
+    if (lane == 0) {
+      const i64 ch = (kb - hb) / 32;
+      a.cmax[(p0 + ch / kChunksPerPart) * kChunksPerPart + ch % kChunksPerPart] = mx;
+    }
+  }
+}
+
 // (score, len, -id) order: true iff a beats b
 __device__ __forceinline__ bool beats(u64 sa, u32 la, u32 ta, u64 sb, u32 lb, u32 tb) {
   if (sa != sb) return sa > sb;
@@ -538,7 +690,8 @@ __global__ void k_replay_compact(const int4 *__restrict__ stage, const i64 *__re
 
 void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhits, const i64 *h_len,
                 int nstreams, const apo_replay_params &prm, apo_replay_rec *d_out, i64 cap, i64 *d_count,
-                cudaStream_t s) {
+                cudaStream_t s, const ReplayIndex *ri) {
+  const bool fast = ri != nullptr && ri->ok;
   require(prm.count_cap >= 1 && prm.decay_q16 >= 0 && prm.decay_q16 <= 65536 && prm.decay_period >= 1 &&
               prm.bonus_num >= 0 && prm.bonus_den >= 1,
           "invalid replay parameters");
@@ -591,14 +744,26 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   for (int q = 0; q < nstreams; ++q) h_order[q] = q;
   std::stable_sort(h_order.begin(), h_order.end(),
                    [&](int x, int y) { return h_hb[x + 1] - h_hb[x] > h_hb[y + 1] - h_hb[y]; });
-  // workspace
-  i64 *hbeg, *pbeg, *soff, *gso;
-  int *pstream, *order;
-  u32 *maxslot, *run_slot, *run_cnt, *nruns, *rcnt, *rbase, *ddq;
-  i32 *run_last, *cmax;
+  // wavelet work items (fast path): <= kWvPart records of one stream each
+  std::vector<int> h_wq;
+  std::vector<i64> h_wr;
+  if (fast) {
+    for (int q = 0; q < nstreams; ++q)
+      for (i64 r = h_hb[q]; r < h_hb[q + 1]; r += kWvPart) {
+        h_wq.push_back(q);
+        h_wr.push_back(r);
+      }
+    h_wr.push_back(h_hb[nstreams]);
+  }
+  const i64 nitems = i64(h_wq.size());
+  // workspace (a pooled block: the arenas may hold the matcher's index)
+  i64 *hbeg, *pbeg, *soff, *gso, *wr0 = nullptr;
+  int *pstream, *order, *wq = nullptr;
+  u32 *maxslot, *run_slot = nullptr, *run_cnt = nullptr, *nruns = nullptr, *rcnt, *rbase, *ddq;
+  i32 *run_last = nullptr, *cmax;
   u64 *sc;
   int4 *stage;
-  const size_t npart_rec = size_t(nparts) * kPart;
+  const size_t npart_rec = fast ? 0 : size_t(nparts) * kPart;
   auto plan = [&](Carver &cv) {
     hbeg = cv.take<i64>(size_t(nstreams) + 1);
     pbeg = cv.take<i64>(size_t(nstreams) + 1);
@@ -609,19 +774,25 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
     maxslot = cv.take<u32>(size_t(nstreams));
     rcnt = cv.take<u32>(size_t(nstreams));
     rbase = cv.take<u32>(size_t(nstreams));
-    nruns = cv.take<u32>(size_t(nparts));
     ddq = cv.take<u32>(dq.size());
     cmax = cv.take<i32>(size_t(nparts) * kChunksPerPart);
-    run_slot = cv.take<u32>(npart_rec);
-    run_cnt = cv.take<u32>(npart_rec);
-    run_last = cv.take<i32>(npart_rec);
+    if (fast) {
+      wq = cv.take<int>(size_t(nitems));
+      wr0 = cv.take<i64>(size_t(nitems) + 1);
+    } else {
+      nruns = cv.take<u32>(size_t(nparts));
+      run_slot = cv.take<u32>(npart_rec);
+      run_cnt = cv.take<u32>(npart_rec);
+      run_last = cv.take<i32>(npart_rec);
+    }
     sc = cv.take<u64>(size_t(nhits));
     stage = cv.take<int4>(size_t(tot));
   };
   Carver dry(nullptr);
   plan(dry);
-  c.arena.reserve(dry.off, s);
-  Carver cv(c.arena.base);
+  const size_t ws_bytes = dry.off + 256;
+  char *ws = static_cast<char *>(c.pool_get(ws_bytes));
+  Carver cv(ws);
   plan(cv);
   APO_CUDA(cudaMemcpyAsync(hbeg, hbeg0, hb_bytes, cudaMemcpyDeviceToDevice, s));
   APO_CUDA(cudaMemcpyAsync(pbeg, h_pb.data(), hb_bytes, cudaMemcpyHostToDevice, s));
@@ -633,12 +804,25 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   RP a{reinterpret_cast<const int4 *>(d_hits), tr->d_off, ddq, int(dq.size()), prm.count_cap, prm.decay_period,
        1.0 / double(prm.decay_period), u32(prm.bonus_num), u32(prm.bonus_den), nstreams, slot_bits, hbeg, pbeg,
        pstream, maxslot, run_slot, run_cnt, run_last, nruns, sc, cmax, order, nullptr, gso, 0u, 0u, soff, stage,
-       rcnt};
+       rcnt, nullptr, nullptr, nullptr, nullptr, wq, wr0};
   const size_t psmem = sizeof(PartSmem);
-  c.smem_optin(reinterpret_cast<const void *>(k_rp_local), psmem);
-  c.smem_optin(reinterpret_cast<const void *>(k_rp_scores), psmem);
-  k_rp_local<<<unsigned(nparts), kPartThreads, psmem, s>>>(a);
-  APO_CHECK_LAUNCH();
+  if (fast) {
+    APO_CUDA(cudaMemcpyAsync(wq, h_wq.data(), sizeof(int) * size_t(nitems), cudaMemcpyHostToDevice, s));
+    APO_CUDA(cudaMemcpyAsync(wr0, h_wr.data(), sizeof(i64) * (size_t(nitems) + 1), cudaMemcpyHostToDevice, s));
+    a.ix_off = ri->off;
+    a.ix_sa = ri->sa;
+    a.ix_tkey = ri->tkey;
+    a.ix_toff = ri->toff;
+    const size_t wsmem = sizeof(WvSmem);
+    c.smem_optin(reinterpret_cast<const void *>(k_rp_wavelet), wsmem);
+    k_rp_wavelet<<<unsigned(nitems), kWvThreads, wsmem, s>>>(a);
+    APO_CHECK_LAUNCH();
+  } else {
+    c.smem_optin(reinterpret_cast<const void *>(k_rp_local), psmem);
+    c.smem_optin(reinterpret_cast<const void *>(k_rp_scores), psmem);
+    k_rp_local<<<unsigned(nparts), kPartThreads, psmem, s>>>(a);
+    APO_CHECK_LAUNCH();
+  }
   // per-stream tables: on chip when they fit, else in a global block
   std::vector<u32> h_ms(static_cast<size_t>(nstreams));
   APO_CUDA(cudaMemcpyAsync(h_ms.data(), maxslot, sizeof(u32) * size_t(nstreams), cudaMemcpyDeviceToHost, s));
@@ -662,12 +846,14 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   a.gstate = gstate;
   a.on_chip_slots = slots_on_chip;
   a.on_chip_bits = slots_on_chip / 32;
-  const size_t bsmem = size_t(smax_b) * 8;
-  c.smem_optin(reinterpret_cast<const void *>(k_rp_prefix), bsmem);
-  k_rp_prefix<<<nstreams, kPrefixThreads, bsmem, s>>>(a);
-  APO_CHECK_LAUNCH();
-  k_rp_scores<<<unsigned(nparts), kPartThreads, psmem, s>>>(a);
-  APO_CHECK_LAUNCH();
+  if (!fast) {
+    const size_t bsmem = size_t(smax_b) * 8;
+    c.smem_optin(reinterpret_cast<const void *>(k_rp_prefix), bsmem);
+    k_rp_prefix<<<nstreams, kPrefixThreads, bsmem, s>>>(a);
+    APO_CHECK_LAUNCH();
+    k_rp_scores<<<unsigned(nparts), kPartThreads, psmem, s>>>(a);
+    APO_CHECK_LAUNCH();
+  }
   k_rp_decide<<<nstreams, 32, size_t(smax_d) * 4, s>>>(a);
   APO_CHECK_LAUNCH();
   ReplayScanF f{rcnt, rbase, nstreams, d_count};
@@ -680,6 +866,7 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   APO_CUDA(cudaStreamSynchronize(s));
   if (gstate) c.pool_put(gstate, sizeof(u32) * size_t(gw));
   c.pool_put(hbeg0, hb_bytes);
+  c.pool_put(ws, ws_bytes);
 }
 
 }  // namespace apo

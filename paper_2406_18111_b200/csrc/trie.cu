@@ -1656,7 +1656,8 @@ apo_status apo_trie_copy(const apo_trie *tr, uint64_t *d_tokens, int64_t *h_off,
 namespace {
 // MATCH_ALL (apo_match mode 0) into d_out[0..cap); *d_count <- hits.
 void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int64_t *h_off, int32_t nstreams,
-               apo_match_rec *d_out, int64_t cap, int64_t *d_count, cudaStream_t s) {
+               apo_match_rec *d_out, int64_t cap, int64_t *d_count, cudaStream_t s, ReplayIndex *ri = nullptr) {
+  if (ri) ri->ok = false;
   {
     APO_CUDA(cudaMemsetAsync(d_count, 0, sizeof(i64), s));
     const i64 Ns = h_off[nstreams];
@@ -1860,6 +1861,13 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
               k_stream_emit<<<nstreams, kEmitThreads, esmem, s>>>(sm, stk, tof, qbase, cap, d_out, qorder, gpar, otr,
                                                                   gdep, pair32);
               APO_CHECK_LAUNCH();
+              if (ri && rev && nh <= cap) {
+                ri->ok = true;
+                ri->off = g.d_off;
+                ri->sa = g.sa.sa;
+                ri->tkey = stk;
+                ri->toff = tof;
+              }
               c.launches += 4;
             }
           } else {
@@ -2002,9 +2010,10 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
     // REPLAY: MATCH_ALL into a cached library buffer (grown and re-run if
     // too small), then the replay selection consumes the hits on the device
     i64 nh = 0;
+    ReplayIndex ri;
     for (;;) {
       match_all(c, tr, d_streams, h_off, nstreams, static_cast<apo_match_rec *>(c.hitbuf),
-                i64(c.hitbuf_cap / sizeof(apo_match_rec)), d_count, s);
+                i64(c.hitbuf_cap / sizeof(apo_match_rec)), d_count, s, &ri);
       nh = i64(c.read_u64(reinterpret_cast<const u64 *>(d_count), s));
       if (size_t(nh) * sizeof(apo_match_rec) <= c.hitbuf_cap) break;
       if (c.hitbuf) c.pool_put(c.hitbuf, c.hitbuf_cap);
@@ -2015,7 +2024,7 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams
     for (int q = 0; q < nstreams; ++q) len[q] = h_off[q + 1] - h_off[q];
     const apo_replay_params prm{100, 64881, 100, 11, 10, 0};
     run_replay(c, tr, static_cast<const apo_match_rec *>(c.hitbuf), nh, len.data(), nstreams, prm,
-               reinterpret_cast<apo_replay_rec *>(d_out), cap, d_count, s);
+               reinterpret_cast<apo_replay_rec *>(d_out), cap, d_count, s, &ri);
     APO_CUDA(cudaMemcpyAsync(d_count + 1, &nh, sizeof(i64), cudaMemcpyHostToDevice, s));
     APO_CUDA(cudaStreamSynchronize(s));
   });

@@ -19,8 +19,21 @@ struct apo_trie {
 
 
 namespace apo {
-// REPLAY selection over MATCH_ALL hits (replay.cu); synchronises s.
+// What the on-chip matcher leaves behind for REPLAY (apo_match mode 1): the
+// REVERSED streams' suffix arrays and every stream's matched intervals in
+// preorder (the hit records' slot = preorder id).  The pointers live in the
+// context's arenas: valid until the next call reserves them.
+struct ReplayIndex {
+  bool ok = false;
+  const i64 *off = nullptr;   // stream offsets (nstreams + 1)
+  const i32 *sa = nullptr;    // reversed streams' suffix arrays (global positions)
+  const u64 *tkey = nullptr;  // per interval (preorder): (stream << 30) | (lo << 15) | (32767 - hi)
+  const u32 *toff = nullptr;  // per stream: first interval (nstreams + 1)
+};
+// REPLAY selection over MATCH_ALL hits (replay.cu); synchronises s.  With
+// ri->ok the trace states come from the matcher's index (no per-part
+// sorting of the hits).
 void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhits, const i64 *h_len,
                 int nstreams, const apo_replay_params &prm, apo_replay_rec *d_out, i64 cap, i64 *d_count,
-                cudaStream_t s);
+                cudaStream_t s, const ReplayIndex *ri = nullptr);
 }  // namespace apo

@@ -215,7 +215,6 @@ class BatchPipeline:
         self.pool = ThreadPoolExecutor(1)
         self.bufs = [None, None]
         self.match_cap = 1 << 20
-        self.hit_cap = 1 << 22
         self.last_hits = 0
         self.last_traces = 0
 
@@ -268,26 +267,13 @@ class BatchPipeline:
                 trie = self.ctx.trie_build(tok, off, rep, roff, self.min_len, self.max_len)
                 if self.exchange is not None:
                     trie = self.exchange.union(trie)
+                if nxt is not None:
+                    fut = self._analyse((k + 1) % 2, nxt[0], nxt[1], nxt[4])
+                    launched = True
+                res = self.ctx.match(trie, streams, soff, mode=self.mode, cap=self.match_cap)
                 if self.mode == 1:
-                    # MATCH_ALL, then the next batch's analysis is launched
-                    # while REPLAY runs: the replay's per-stream walks are
-                    # sequential, so as light streams finish their SMs go to
-                    # the analysis kernels (both saturate the SMs otherwise)
-                    hits = self.ctx.match(trie, streams, soff, full=True, cap=self.hit_cap)
-                    self.hit_cap = max(int(hits.shape[0]), 1)
-                    if nxt is not None:
-                        fut = self._analyse((k + 1) % 2, nxt[0], nxt[1], nxt[4])
-                        launched = True
-                    rp = self.ctx.replay(trie, hits, np.diff(np.asarray(soff, dtype=np.int64)), cap=self.match_cap)
-                    self.match_cap = max(int(rp.shape[0]), 1)
-                    self.last_hits = int(hits.shape[0])
-                    res = (rp, self.last_hits)
-                    del hits
-                else:
-                    if nxt is not None:
-                        fut = self._analyse((k + 1) % 2, nxt[0], nxt[1], nxt[4])
-                        launched = True
-                    res = self.ctx.match(trie, streams, soff, mode=self.mode, cap=self.match_cap)
+                    self.match_cap = max(int(res[0].shape[0]), 1)
+                    self.last_hits = res[1]
                 self.last_traces = trie.info()[0]
             if nxt is not None and not launched:
                 fut = self._analyse((k + 1) % 2, nxt[0], nxt[1], nxt[4])

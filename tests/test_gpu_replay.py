@@ -134,3 +134,38 @@ def test_replay_c4_shaped_vs_oracle(ctx):
     got, want, *_ = run_case(ctx, [st[so[q]:so[q + 1]] for q in range(W)],
                              [tt[to[t]:to[t + 1]] for t in range(len(to) - 1)])
     assert len(want) > 0 and np.array_equal(got, want)
+
+
+def test_match_mode_replay_heavy_streams(ctx):
+    """apo_match mode 1 takes the trace states from the matcher's index
+    (wavelet queries over the reversed streams' suffix arrays, several work
+    items per stream beyond 65,536 hits); it must equal MATCH_ALL + the
+    general apo_replay path, and the oracle on a sampled stream."""
+    streams = [gen.periodic(41 + k, 16384, p, 12, noise=0.01) for k, p in enumerate((5, 13, 40))]
+    streams.append(gen.random_string(44, 3000, 50))
+    rng = gen.Rng(45)
+    traces = set()
+    for _ in range(4000):
+        s = streams[rng.below(3)]
+        a = rng.below(len(s) - 64)
+        traces.add(tuple(int(x) for x in s[a:a + 3 + rng.below(60)]))
+    traces = sorted(traces, key=lambda t: (-len(t), t))
+    tt = np.concatenate([np.asarray(t, dtype=np.uint64) for t in traces])
+    to = np.cumsum([0] + [len(t) for t in traces]).astype(np.int64)
+    st = np.concatenate(streams)
+    so = np.cumsum([0] + [len(s) for s in streams]).astype(np.int64)
+    trie = ctx.trie_build_traces(dev(tt), to)
+    hits = ctx.match(trie, dev(st), so, full=True, cap=1 << 26)
+    per = np.bincount(hits[:, 0].cpu().numpy(), minlength=len(streams))
+    assert per.max() > 65536  # several wavelet work items for a stream
+    two = ctx.replay(trie, hits, np.diff(so))
+    one, nh = ctx.match(trie, dev(st), so, mode=1)
+    assert nh == hits.shape[0] and torch.equal(one, two) and one.shape[0] > 0
+    # the oracle on the third stream (brute-force hits of that stream alone)
+    q = 2
+    oh, _ = oracle.match_brute(streams[q], np.array([0, len(streams[q])], dtype=np.int64), tt, to)
+    want = oracle.replay(oh, [len(t) for t in traces])
+    g = one.cpu().numpy()
+    g = g[g[:, 0] == q].copy()
+    g[:, 0] = 0
+    assert np.array_equal(as_oracle_rows(g, [len(t) for t in traces]), want)
