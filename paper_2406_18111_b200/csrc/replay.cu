@@ -95,6 +95,7 @@ struct RP {
   const u32 *ix_toff;
   const int *wq;         // wavelet work items: stream
   const i64 *wr0;        // wavelet work items: first record (nitems + 1 ends)
+  struct WvMat *wv;      // per stream: its wavelet matrix (lazy scores in phase D)
 };
 
 __device__ __forceinline__ u32 lanemask_lt_() {
@@ -402,10 +403,12 @@ __global__ void __launch_bounds__(kPartThreads) k_rp_scores(RP a) {
 // REVERSED stream's suffix array, ending at E[r] = n - 1 - SA_rev[r].  So
 //   count(z, e) = #{r in [lo_z, hi_z) : E[r] <= e}   (appearances so far),
 //   prev(z, e)  = the (count - 1)-th smallest E[r] in the range (1-based),
-// two wavelet-matrix queries over E (14 levels for n <= 16,384, built in
-// shared memory per stream) -- no per-part sort, no cross-part prefix.  One
-// CTA per work item of <= 65,536 records of one stream (heavy streams get
-// several CTAs, each building the stream's matrix).
+// two wavelet-matrix queries over E (14 levels for n <= 16,384; one matrix
+// per stream, built in shared memory by k_rp_wvbuild and stored).  The
+// decisions only ever look at the eligible records of the ends where a
+// replay happens, so phase D evaluates exactly those scores (wv_score) and
+// nothing is computed for the other ~99 % of the hits; k_rp_cmax gives the
+// per-chunk latest starts the decision walk skips by.
 constexpr int kWvThreads = 1024;
 constexpr int kWvMaxN = 16384;
 constexpr int kWvLevels = 14;
@@ -425,21 +428,92 @@ __device__ __forceinline__ u32 wv_rank1(const WvSmem &S, int l, u32 i) {
   return u32(S.pre[l][w]) + __popc(S.bits[l][w] & ((1u << b) - 1u));
 }
 
-__global__ void __launch_bounds__(kWvThreads) k_rp_wavelet(RP a) {
+// The matrix of one stream in global memory, (bits, ones before) per word
+// interleaved so a rank is one 8-byte load: phase D evaluates the scores of
+// the few records it examines (eligible records at decision ends) from it.
+struct WvMat {
+  uint2 bp[kWvLevels][kWvWords];
+  u32 zeros[kWvLevels];
+  int L;
+};
+
+__device__ __forceinline__ u32 wvg_rank1(const WvMat *M, int l, u32 i) {
+  const uint2 v = __ldg(&M->bp[l][i >> 5]);
+  return v.y + __popc(v.x & ((1u << (i & 31u)) - 1u));
+}
+
+// Score before the bonus of hit `rec` (trace length len) of stream q:
+// count = #{E[r] <= e in [lo, hi)}, previous end = the (count - 1)-th
+// smallest E in the range (1-based).
+__device__ u64 wv_score(const RP &a, int q, int4 rec, u32 len) {
+  const WvMat *M = a.wv + q;
+  const int L = M->L;
+  const u64 kk = __ldg(&a.ix_tkey[a.ix_toff[q] + rec.w]);
+  const u32 lo = u32(kk >> 15) & 32767u, hi = 32767u - (u32(kk) & 32767u);
+  const u32 e = u32(rec.y);
+  u32 cnt = 0;
+  const u32 x = e + 1u;
+  if (x >= (1u << L)) {
+    cnt = hi - lo;
+  } else {
+    u32 l0 = lo, h0 = hi;
+    for (int l = L - 1; l >= 0; --l) {
+      const u32 a1 = wvg_rank1(M, l, l0), b1 = wvg_rank1(M, l, h0);
+      const u32 Z = __ldg(&M->zeros[l]);
+      if ((x >> l) & 1u) {
+        cnt += (h0 - l0) - (b1 - a1);
+        l0 = Z + a1;
+        h0 = Z + b1;
+      } else {
+        l0 -= a1;
+        h0 -= b1;
+      }
+    }
+  }
+  u32 gap = 0;
+  if (cnt >= 2) {
+    u32 kq = cnt - 2, v = 0, l0 = lo, h0 = hi;
+    for (int l = L - 1; l >= 0; --l) {
+      const u32 a1 = wvg_rank1(M, l, l0), b1 = wvg_rank1(M, l, h0);
+      const u32 Z = __ldg(&M->zeros[l]);
+      const u32 zc = (h0 - l0) - (b1 - a1);
+      if (kq < zc) {
+        l0 -= a1;
+        h0 -= b1;
+      } else {
+        kq -= zc;
+        v |= 1u << l;
+        l0 = Z + a1;
+        h0 = Z + b1;
+      }
+    }
+    gap = e - v;
+  }
+  const u32 c = min(cnt, u32(a.count_cap));
+  u32 kq = u32(double(gap) * a.inv_period);
+  if (u64(kq) * u64(a.period) > u64(gap)) --kq;
+  if (u64(kq + 1u) * u64(a.period) <= u64(gap)) ++kq;
+  const u64 d = __ldg(&a.dq[kq < u32(a.ndq) ? kq : u32(a.ndq - 1)]);
+  return u64(len) * u64(c) * d;
+}
+
+// Builds every stream's matrix in shared memory (ballots + stable
+// partitions), then stores it to the stream's WvMat.
+__global__ void __launch_bounds__(kWvThreads) k_rp_wvbuild(RP a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   WvSmem &S = *reinterpret_cast<WvSmem *>(smraw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int q = a.wq[blockIdx.x];
-  const i64 r0 = a.wr0[blockIdx.x], r1 = a.wr0[blockIdx.x + 1];
+  const int q = blockIdx.x;
   const i64 beg = a.ix_off[q];
   const int n = int(a.ix_off[q + 1] - beg);
-  const u32 ntrees = a.ix_toff[q + 1] - a.ix_toff[q];
-  if (tid == 0 && r0 == a.hbeg[q]) a.maxslot[q] = ntrees;
+  if (tid == 0) a.maxslot[q] = a.ix_toff[q + 1] - a.ix_toff[q];
+  if (a.hbeg[q] == a.hbeg[q + 1] || n == 0) return;  // no hits: no scores needed
   const int L = max(1, 32 - __clz(u32(max(n - 1, 1))));
   const int nw = (n + 31) / 32;
   for (int r = tid; r < n; r += kWvThreads) S.cur[r] = (unsigned short)(n - 1 - (a.ix_sa[beg + r] - int(beg)));
   __syncthreads();
   unsigned short *cur = S.cur, *nxt = S.nxt;
+  WvMat *M = a.wv + q;
   for (int l = L - 1; l >= 0; --l) {
     for (int w = warp; w <= nw; w += kWvThreads / 32) {
       const int i = w * 32 + lane;
@@ -460,9 +534,13 @@ __global__ void __launch_bounds__(kWvThreads) k_rp_wavelet(RP a) {
         if (w0 + lane <= nw) S.pre[l][w0 + lane] = (unsigned short)(carry + x - v);
         carry += __shfl_sync(0xffffffffu, x, 31);
       }
-      if (lane == 0) S.zeros[l] = u32(n) - carry;
+      if (lane == 0) {
+        S.zeros[l] = u32(n) - carry;
+        M->zeros[l] = u32(n) - carry;
+      }
     }
     __syncthreads();
+    for (int w = tid; w <= nw; w += kWvThreads) M->bp[l][w] = make_uint2(S.bits[l][w], u32(S.pre[l][w]));
     if (l > 0) {  // stable partition for the next level: zeros, then ones
       const u32 Z = S.zeros[l];
       for (int i = tid; i < n; i += kWvThreads) {
@@ -474,63 +552,21 @@ __global__ void __launch_bounds__(kWvThreads) k_rp_wavelet(RP a) {
       unsigned short *t = cur; cur = nxt; nxt = t;
     }
   }
-  // queries: warp-aligned chunks of 32 records of the stream
-  const u64 *tk = a.ix_tkey + a.ix_toff[q];
+  if (tid == 0) M->L = L;
+}
+
+// Per chunk of 32 records (stream-aligned): the latest start end - len + 1.
+__global__ void __launch_bounds__(256) k_rp_cmax(RP a) {
+  const int lane = threadIdx.x & 31;
+  const int q = a.wq[blockIdx.x];
+  const i64 r0 = a.wr0[blockIdx.x], r1 = a.wr0[blockIdx.x + 1];
   const i64 hb = a.hbeg[q], p0 = a.pbeg[q];
-  for (i64 kb = r0 + i64(warp) * 32; kb < r1; kb += kWvThreads) {
+  for (i64 kb = r0 + i64(threadIdx.x >> 5) * 32; kb < r1; kb += 256) {
     const i64 k = kb + lane;
     int st = -1;
     if (k < r1) {
       const int4 rec = a.hits[k];
-      const u32 e = u32(rec.y);
-      const u64 kk = tk[rec.w];
-      u32 lo = u32(kk >> 15) & 32767u, hi = 32767u - (u32(kk) & 32767u);
-      // count of ends <= e in [lo, hi)
-      u32 cnt = 0;
-      const u32 x = e + 1u;
-      if (x >= (1u << L)) {
-        cnt = hi - lo;
-      } else {
-        u32 l0 = lo, h0 = hi;
-        for (int l = L - 1; l >= 0; --l) {
-          const u32 a1 = wv_rank1(S, l, l0), b1 = wv_rank1(S, l, h0);
-          if ((x >> l) & 1u) {
-            cnt += (h0 - l0) - (b1 - a1);
-            l0 = S.zeros[l] + a1;
-            h0 = S.zeros[l] + b1;
-          } else {
-            l0 -= a1;
-            h0 -= b1;
-          }
-        }
-      }
-      // previous end: the (cnt - 2)-th smallest (0-based) end in [lo, hi)
-      u32 gap = 0;
-      if (cnt >= 2) {
-        u32 kq = cnt - 2, v = 0, l0 = lo, h0 = hi;
-        for (int l = L - 1; l >= 0; --l) {
-          const u32 a1 = wv_rank1(S, l, l0), b1 = wv_rank1(S, l, h0);
-          const u32 zc = (h0 - l0) - (b1 - a1);
-          if (kq < zc) {
-            l0 -= a1;
-            h0 -= b1;
-          } else {
-            kq -= zc;
-            v |= 1u << l;
-            l0 = S.zeros[l] + a1;
-            h0 = S.zeros[l] + b1;
-          }
-        }
-        gap = e - v;
-      }
-      const u32 len = u32(__ldg(&a.tlen_off[rec.z + 1]) - __ldg(&a.tlen_off[rec.z]));
-      const u32 c = min(cnt, u32(a.count_cap));
-      u32 kq = u32(double(gap) * a.inv_period);
-      if (u64(kq) * u64(a.period) > u64(gap)) --kq;
-      if (u64(kq + 1u) * u64(a.period) <= u64(gap)) ++kq;
-      const u64 d = __ldg(&a.dq[kq < u32(a.ndq) ? kq : u32(a.ndq - 1)]);
-      a.sc[k] = u64(len) * u64(c) * d;
-      st = int(e) - int(len) + 1;
+      st = rec.y - int(__ldg(&a.tlen_off[rec.z + 1]) - __ldg(&a.tlen_off[rec.z])) + 1;
     }
     const int mx = __reduce_max_sync(0xffffffffu, st);
     if (lane == 0) {
@@ -618,7 +654,7 @@ __global__ void __launch_bounds__(32) k_rp_decide(RP a) {
       u32 L = 0;
       if (valid) {
         r = a.hits[k];
-        sc0 = a.sc[k];
+        if (a.wv == nullptr) sc0 = a.sc[k];
         L = u32(__ldg(&a.tlen_off[r.z + 1]) - __ldg(&a.tlen_off[r.z]));
       }
       if (have && __shfl_sync(0xffffffffu, r.y, 0) != carry_e) commit(carry_e);
@@ -635,6 +671,7 @@ __global__ void __launch_bounds__(32) k_rp_decide(RP a) {
         const int a1 = 32 - __clz(rm);
         const bool ok = elig && run;
         u64 sc = sc0;
+        if (ok && a.wv != nullptr) sc = wv_score(a, q, r, L);  // lazily: only examined records
         if (ok && ((rep[slot >> 5] >> (slot & 31)) & 1u)) sc = sc * a.bonus_num / a.bonus_den;
         const int b = warp_best(ok, sc, L, u32(r.z));
         if (b >= 0) {
@@ -761,7 +798,8 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   int *pstream, *order, *wq = nullptr;
   u32 *maxslot, *run_slot = nullptr, *run_cnt = nullptr, *nruns = nullptr, *rcnt, *rbase, *ddq;
   i32 *run_last = nullptr, *cmax;
-  u64 *sc;
+  u64 *sc = nullptr;
+  WvMat *wv = nullptr;
   int4 *stage;
   const size_t npart_rec = fast ? 0 : size_t(nparts) * kPart;
   auto plan = [&](Carver &cv) {
@@ -779,13 +817,14 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
     if (fast) {
       wq = cv.take<int>(size_t(nitems));
       wr0 = cv.take<i64>(size_t(nitems) + 1);
+      wv = cv.take<WvMat>(size_t(nstreams));
     } else {
       nruns = cv.take<u32>(size_t(nparts));
       run_slot = cv.take<u32>(npart_rec);
       run_cnt = cv.take<u32>(npart_rec);
       run_last = cv.take<i32>(npart_rec);
+      sc = cv.take<u64>(size_t(nhits));
     }
-    sc = cv.take<u64>(size_t(nhits));
     stage = cv.take<int4>(size_t(tot));
   };
   Carver dry(nullptr);
@@ -804,7 +843,7 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   RP a{reinterpret_cast<const int4 *>(d_hits), tr->d_off, ddq, int(dq.size()), prm.count_cap, prm.decay_period,
        1.0 / double(prm.decay_period), u32(prm.bonus_num), u32(prm.bonus_den), nstreams, slot_bits, hbeg, pbeg,
        pstream, maxslot, run_slot, run_cnt, run_last, nruns, sc, cmax, order, nullptr, gso, 0u, 0u, soff, stage,
-       rcnt, nullptr, nullptr, nullptr, nullptr, wq, wr0};
+       rcnt, nullptr, nullptr, nullptr, nullptr, wq, wr0, wv};
   const size_t psmem = sizeof(PartSmem);
   if (fast) {
     APO_CUDA(cudaMemcpyAsync(wq, h_wq.data(), sizeof(int) * size_t(nitems), cudaMemcpyHostToDevice, s));
@@ -813,10 +852,14 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
     a.ix_sa = ri->sa;
     a.ix_tkey = ri->tkey;
     a.ix_toff = ri->toff;
+    // the matrices once per stream; scores are evaluated lazily in phase D
     const size_t wsmem = sizeof(WvSmem);
-    c.smem_optin(reinterpret_cast<const void *>(k_rp_wavelet), wsmem);
-    k_rp_wavelet<<<unsigned(nitems), kWvThreads, wsmem, s>>>(a);
+    c.smem_optin(reinterpret_cast<const void *>(k_rp_wvbuild), wsmem);
+    k_rp_wvbuild<<<nstreams, kWvThreads, wsmem, s>>>(a);
     APO_CHECK_LAUNCH();
+    k_rp_cmax<<<unsigned(nitems), 256, 0, s>>>(a);
+    APO_CHECK_LAUNCH();
+    c.launches++;
   } else {
     c.smem_optin(reinterpret_cast<const void *>(k_rp_local), psmem);
     c.smem_optin(reinterpret_cast<const void *>(k_rp_scores), psmem);

@@ -117,6 +117,34 @@ __global__ void k_double_keys(const i32 *__restrict__ rank, Batch b, i64 h, int 
   vals[i] = u32(i);
 }
 
+// Manber-Myers order for a single window (the global path's rounds after
+// the first): walking the previous order SA (sorted by the first h tokens)
+// and emitting i = SA[q] - h lists the suffixes by their SECOND key
+// rank[i + h]; the suffixes i >= n - h (second key "end of string", the
+// smallest) take the slots of j = SA[q] < h.  All of those but i = n - h
+// are singletons (shorter than h: their h-prefix includes the end), so only
+// i = n - h must lead: it goes to slot 0 and the slots before its own shift
+// up by one.  A stable sort of this list by the FIRST key alone (the high
+// key bits) then orders by the full (rank[i], rank[i + h]) key: half the key
+// bits per round.
+__global__ void k_pos_of_zero(const u32 *__restrict__ sa, i64 n, u32 *__restrict__ out) {
+  const i64 q = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q < n && sa[q] == 0u) *out = u32(q);
+}
+
+__global__ void k_mm_keys(const u32 *__restrict__ sa_prev, const i32 *__restrict__ rank, i64 n, i64 h, int lob,
+                          const u32 *__restrict__ q0p, u64 *__restrict__ keys, u32 *__restrict__ vals) {
+  const i64 q = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const i64 q0 = *q0p;
+  const i64 j = sa_prev[q];
+  const i64 i = j >= h ? j - h : n - h + j;
+  const i64 dst = q == q0 ? 0 : (q < q0 ? q + 1 : q);
+  const u64 lo = i + h < n ? u64(rank[i + h] + 1) : 0ull;
+  keys[dst] = (u64(u32(rank[i])) << lob) | lo;
+  vals[dst] = u32(i);
+}
+
 // Next rank level from the sorted keys; flags "not done" if any group has
 // more than one member.
 struct DoubleRankF {
@@ -361,12 +389,31 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   for (i64 h = h0; !done; h <<= 1) {
     if (r + 1 >= w.max_levels) throw Error{APO_ERR_INVALID, "prefix doubling exceeded its level budget"};
     APO_CUDA(cudaMemsetAsync(notdone, 0, sizeof(u32), s));
-    k_double_keys<<<G, T, 0, s>>>(w.levels[r], b, h, lob, w.keys, w.vals);
-    APO_CHECK_LAUNCH();
-    c.launches++;
-    bool a = radix_sort_u64_u32(c, w.keys, w.vals, w.keys_alt, w.vals_alt, N, 0, hib + lob, s);
-    const u64 *key = a ? w.keys_alt : w.keys;
-    const u32 *sa = a ? w.vals_alt : w.vals;
+    const u64 *key;
+    const u32 *sa;
+    if (final_sa != nullptr && !b.gen && b.W == 1 && b.sort_depth == 0 && h < N) {
+      // Manber-Myers round: keys listed in second-key order, sorted by the
+      // first key's bits only (the pair not holding the previous SA)
+      const bool in_main = final_sa == w.vals;
+      u64 *k0 = in_main ? w.keys_alt : w.keys, *k1 = in_main ? w.keys : w.keys_alt;
+      u32 *v0 = in_main ? w.vals_alt : w.vals, *v1 = in_main ? w.vals : w.vals_alt;
+      u32 *q0 = notdone + 1;
+      k_pos_of_zero<<<G, T, 0, s>>>(final_sa, N, q0);
+      APO_CHECK_LAUNCH();
+      k_mm_keys<<<G, T, 0, s>>>(final_sa, w.levels[r], N, h, lob, q0, k0, v0);
+      APO_CHECK_LAUNCH();
+      c.launches += 2;
+      bool a = radix_sort_u64_u32(c, k0, v0, k1, v1, N, lob, hib + lob, s);
+      key = a ? k1 : k0;
+      sa = a ? v1 : v0;
+    } else {
+      k_double_keys<<<G, T, 0, s>>>(w.levels[r], b, h, lob, w.keys, w.vals);
+      APO_CHECK_LAUNCH();
+      c.launches++;
+      bool a = radix_sort_u64_u32(c, w.keys, w.vals, w.keys_alt, w.vals_alt, N, 0, hib + lob, s);
+      key = a ? w.keys_alt : w.keys;
+      sa = a ? w.vals_alt : w.vals;
+    }
     DoubleRankF f{key, sa, w.levels[r + 1], notdone};
     launch_scan<true>(c, N, f, s);
     ++r;

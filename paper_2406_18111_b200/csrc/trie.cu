@@ -702,17 +702,34 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
     }
     i64 cnt = 0;
     if (lhi >= L) {
-      cnt = 1;
-      for (i64 k0 = hi; k0 + 1 < hi0; k0 += 32) {
-        const i64 k = k0 + lane;
-        const bool ok = (k + 1 < hi0) && i64(LC[k]) >= L;
-        const u32 bad = __ballot_sync(0xffffffffu, !ok);
-        if (bad) {
-          cnt += __ffs(bad) - 1;
-          break;
-        }
-        cnt += 32;
+      // the interval extends while LC[k] >= L (k + 1 < hi0): first the rest
+      // of hi's 32-entry block, then 32 blocks per step by their minima
+      const i64 kend = hi0 - 1;
+      i64 k = hi, stop = -1;
+      {
+        const i64 bend = min(((k >> 5) + 1) << 5, kend);
+        const i64 kk = k + lane;
+        const u32 bad = __ballot_sync(0xffffffffu, kk < bend && i64(LC[kk]) < L);
+        if (bad)
+          stop = k + __ffs(bad) - 1;
+        else
+          k = bend;
       }
+      while (stop < 0 && k < kend) {  // k is block aligned here
+        const i64 b = (k >> 5) + lane;
+        const bool cand = (b << 5) < kend && ((b << 5) + 32 > kend || i64(s_bmin[b]) < L);
+        const u32 cb = __ballot_sync(0xffffffffu, cand);
+        if (!cb) {
+          k += 32 * 32;
+          continue;
+        }
+        const i64 fb = (k >> 5) + __ffs(cb) - 1;
+        const i64 kk = (fb << 5) + lane;
+        const u32 bad = __ballot_sync(0xffffffffu, kk < kend && i64(LC[kk]) < L);
+        stop = bad ? (fb << 5) + __ffs(bad) - 1 : min((fb << 5) + 32, kend);
+      }
+      if (stop < 0) stop = kend;
+      cnt = 1 + (stop - hi);
     }
     u32 nx = 0;
     if (lane == 0) {
@@ -1867,6 +1884,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
                 ri->sa = g.sa.sa;
                 ri->tkey = stk;
                 ri->toff = tof;
+                ri->nint = P;
               }
               c.launches += 4;
             }

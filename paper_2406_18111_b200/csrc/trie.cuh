@@ -29,6 +29,7 @@ struct ReplayIndex {
   const i32 *sa = nullptr;    // reversed streams' suffix arrays (global positions)
   const u64 *tkey = nullptr;  // per interval (preorder): (stream << 30) | (lo << 15) | (32767 - hi)
   const u32 *toff = nullptr;  // per stream: first interval (nstreams + 1)
+  i64 nint = 0;               // intervals of all streams
 };
 // REPLAY selection over MATCH_ALL hits (replay.cu); synchronises s.  With
 // ri->ok the trace states come from the matcher's index (no per-part
