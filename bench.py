@@ -327,6 +327,7 @@ def main():
     bufs = (torch.empty((cap, 4), dtype=torch.int32, device=dev), torch.empty(W + 1, dtype=torch.int64, device=dev),
             torch.empty(cap, dtype=torch.int32, device=dev), torch.zeros(2, dtype=torch.int64, device=dev))
     s = torch.cuda.current_stream(dev)
+    # "gather": the NVLink union at N > 1 (overlapped with the stream index)
     stage_names = ["analysis", "trace_set", "gather", "match"]
     stage_ms = {k: 0.0 for k in stage_names}
     last = {}
@@ -345,13 +346,22 @@ def main():
             trie = ctx.trie_build(tok, off, rep, roff, MIN_LEN, 0)
             if timed:
                 evs[2].record(s)
+            idx = None
             if world > 1:
-                trie = exchange.union(trie)
+                # the union of the ranks' lists: the peers' lists are pulled
+                # by the copy engines while the SMs build the trace-independent
+                # stream index (reversed streams' SA + LCP, buckets)
+                exchange.start(trie)
+                idx = ctx.match_index(streams, soff)
+                trie = exchange.finish()
             if timed:
                 evs[3].record(s)
             # MATCH_ALL, then REPLAY selection consuming the hits on the device
             # (Alg. 1 SelectReplayTrace / ExecuteAndReplay)
-            hits, nall = ctx.match(trie, streams, soff, mode=1, cap=last.get("replays", 1 << 20))
+            if idx is not None:
+                hits, nall = ctx.match_indexed(trie, idx, mode=1, cap=last.get("replays", 1 << 20))
+            else:
+                hits, nall = ctx.match(trie, streams, soff, mode=1, cap=last.get("replays", 1 << 20))
             last["replays"] = max(int(hits.shape[0]), 1)
             last["hits"] = nall
             last["traces"] = trie.info()[0]

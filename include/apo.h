@@ -3,7 +3,7 @@
  * (arXiv 2406.18111, "Apophenia: automatic trace identification").
  *
  * Library: paper_2406_18111_b200/libapo.so (hand-written sm_100a CUDA).
- * Citations "P:n" are lines of the paper text; R1..R17 are the
+ * Citations "P:n" are lines of the paper text; R1..R25 are the
  * readings of the paper listed in DESIGN.md §3.
  *
  * General conventions
@@ -16,6 +16,11 @@
  *    work is enqueued on it.  Data-dependent loop trip counts (prefix-doubling
  *    rounds, greedy rounds) are currently resolved with a small host read of a
  *    device flag, so the calls return with their results complete on `stream`.
+ *  - Asynchrony: the calls return with their results complete, so a caller
+ *    that wants analysis to overlap other GPU work runs it on another
+ *    context + stream from another host thread (finder.py's StreamAnalyzer
+ *    and BatchPipeline); apo_match_index lets the trace-independent half of
+ *    matching run before the trace set exists.
  *  - Tokens are uint64 op hashes ordered as unsigned integers (R1).  A suffix
  *    that is a proper prefix of another sorts first (R2).
  *  - Positions, lengths and counts on the device are int32 unless stated.
@@ -116,10 +121,10 @@ int64_t apo_launch_count(const apo_ctx *ctx);
  * kernel class `kind` (0 = radix-sort digit pass, 1 = radix histogram,
  * 2 = single-pass scans, 3 = other, 4 = per-window on-chip suffix sort K9,
  * 5 = per-stream trace search), the summed device time in ms, the number
- * of launches and the summed ALGORITHMIC bytes: HBM bytes for kind 0 (each
- * key/value read once and written once), shared-memory bytes for kind 4
- * (20 B per item per LSD pass + 18 B per item per round, counted by the
- * kernel).  Any output pointer may be NULL. */
+ * of launches and, for kind 0, the summed ALGORITHMIC HBM bytes (each
+ * key/value read once and written once; 0 for the other kinds: bench.py
+ * applies SURVEY.md §8(d)'s per-op model to them).  Any output pointer may
+ * be NULL. */
 apo_status apo_profile(apo_ctx *ctx, int enable);
 apo_status apo_profile_read(apo_ctx *ctx, int kind, double *ms, int64_t *launches, double *bytes);
 
@@ -288,6 +293,21 @@ apo_status apo_trie_copy(const apo_trie *trie, uint64_t *d_tokens, int64_t *h_of
 apo_status apo_match(apo_ctx *ctx, const apo_trie *trie, const uint64_t *d_streams,
                      const int64_t *h_off, int32_t nstreams, int32_t mode, apo_match_rec *d_out,
                      int64_t cap, int64_t *d_count, void *stream);
+
+/* The trace-independent half of apo_match, for callers that overlap it with
+ * building the trace set (e.g. the multi-GPU union): the REVERSED streams,
+ * their suffix arrays + LCP arrays and first-token buckets.  The handle owns
+ * device workspace of ctx (free with apo_stream_index_destroy); d_streams
+ * (and h_off's values) must stay unchanged until its last use.
+ * Synchronises `stream`. */
+typedef struct apo_stream_index apo_stream_index;
+apo_status apo_match_index(apo_ctx *ctx, const uint64_t *d_streams, const int64_t *h_off, int32_t nstreams,
+                           apo_stream_index **out, void *stream);
+/* apo_match on the streams of `idx` (same output, modes and capacity rules);
+ * idx must come from apo_match_index on the same ctx. */
+apo_status apo_match_indexed(apo_ctx *ctx, const apo_trie *trie, const apo_stream_index *idx, int32_t mode,
+                             apo_match_rec *d_out, int64_t cap, int64_t *d_count, void *stream);
+void apo_stream_index_destroy(apo_stream_index *idx);
 
 /* REPLAY selection (Alg. 1 SelectReplayTrace / ExecuteAndReplay, P:429-443;
  * scoring P:694-713; readings R20-R24) over MATCH_ALL hits d_hits[0..nhits)

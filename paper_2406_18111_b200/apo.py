@@ -82,6 +82,9 @@ _SIGS = {
     "apo_trie_copy": (ctypes.c_int, [_VP, _VP, _P_I64, _VP]),
     "apo_match": (ctypes.c_int, [_VP, _VP, _VP, _P_I64, _I32, _I32, _VP, _I64, _VP, _VP]),
     "apo_replay": (ctypes.c_int, [_VP, _VP, _VP, _I64, _P_I64, _I32, _VP, _VP, _I64, _VP, _VP]),
+    "apo_match_index": (ctypes.c_int, [_VP, _VP, _P_I64, _I32, ctypes.POINTER(_VP), _VP]),
+    "apo_match_indexed": (ctypes.c_int, [_VP, _VP, _VP, _I32, _VP, _I64, _VP, _VP]),
+    "apo_stream_index_destroy": (None, [_VP]),
     "apo_dsa_keys": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _I64, _I64, _VP, _VP, _VP]),
     "apo_dsa_samples": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I32, _VP, _VP, _VP]),
     "apo_dsa_split": (ctypes.c_int, [_VP, _VP, _VP, _I64, _VP, _VP, _I32, _VP, _VP]),
@@ -359,6 +362,38 @@ class Context:
                 return out[:n] if full else out[:n, :3]
             cap = n
 
+    def match_index(self, streams: torch.Tensor, off) -> "StreamIndex":
+        """apo_match_index: the trace-independent half of match() (reversed
+        streams, their suffix arrays + LCP, first-token buckets), to overlap
+        with building the trace set; use with match_indexed()."""
+        streams = _check_tok(streams, self.device)
+        o = _host_off(off)
+        h = ctypes.c_void_p()
+        self._raise(self.lib.apo_match_index(self.h, _ptr(streams), o.ctypes.data_as(_P_I64), len(o) - 1,
+                                             ctypes.byref(h), _stream(self.device)))
+        return StreamIndex(self, h, streams, o)
+
+    def match_indexed(self, trie: "Trie", idx: "StreamIndex", cap: int | None = None, full: bool = False,
+                      mode: int = 0):
+        """match() on the streams of `idx` (same results)."""
+        if idx.ctx is not self:
+            raise ValueError("the stream index belongs to another context")
+        d = self.device
+        if cap is None:
+            cap = 1 << 22 if mode == 0 else max(int(idx.off[-1]) // 8, 1024)
+        while True:
+            out = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=d)
+            cnt = torch.zeros(2, dtype=torch.int64, device=d)
+            self._raise(self.lib.apo_match_indexed(self.h, trie.h, idx.h, int(mode), _ptr(out), cap, _ptr(cnt),
+                                                   _stream(d)))
+            c = cnt.tolist()
+            n = int(c[0])
+            if n <= cap:
+                if mode == 1:
+                    return out[:n], int(c[1])
+                return out[:n] if full else out[:n, :3]
+            cap = n
+
     def replay(self, trie: "Trie", hits: torch.Tensor, stream_lengths, cap: int | None = None, **params):
         """REPLAY selection over MATCH_ALL hits (int32[h,4] from match(..., full=True))
         -> int32[r,4] rows (stream, end_pos, trace_id, first)."""
@@ -445,6 +480,21 @@ class History:
         self.ctx._raise(self.ctx.lib.apo_history_window(self.h, int(begin), int(end), _ptr(out),
                                                         _stream(self.ctx.device)))
         return out
+
+
+class StreamIndex:
+    """apo_stream_index: keeps the streams tensor alive while it is used."""
+
+    def __init__(self, ctx: Context, h, streams: torch.Tensor, off: np.ndarray):
+        self.ctx, self.h, self.streams, self.off = ctx, h, streams, off
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.ctx.lib.apo_stream_index_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
 
 
 class Trie:

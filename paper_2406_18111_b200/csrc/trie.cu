@@ -1673,10 +1673,11 @@ apo_status apo_trie_copy(const apo_trie *tr, uint64_t *d_tokens, int64_t *h_off,
 namespace {
 // MATCH_ALL (apo_match mode 0) into d_out[0..cap); *d_count <- hits.
 void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int64_t *h_off, int32_t nstreams,
-               apo_match_rec *d_out, int64_t cap, int64_t *d_count, cudaStream_t s, ReplayIndex *ri = nullptr) {
+               apo_match_rec *d_out, int64_t cap, int64_t *d_count, cudaStream_t s, ReplayIndex *ri = nullptr,
+               apo_stream_index *build_idx = nullptr, const apo_stream_index *pre = nullptr) {
   if (ri) ri->ok = false;
   {
-    APO_CUDA(cudaMemsetAsync(d_count, 0, sizeof(i64), s));
+    if (d_count) APO_CUDA(cudaMemsetAsync(d_count, 0, sizeof(i64), s));
     const i64 Ns = h_off[nstreams];
     require(h_off[0] == 0, "h_off[0] must be 0");
     i64 maxs = 0;
@@ -1684,11 +1685,12 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       require(h_off[q + 1] >= h_off[q], "h_off must be non-decreasing");
       maxs = std::max<i64>(maxs, h_off[q + 1] - h_off[q]);
     }
-    if (tr->T == 0 || Ns == 0) return;
+    const i64 T = tr ? tr->T : 0;
+    if (Ns == 0 || (!build_idx && T == 0)) return;
     require(d_streams != nullptr, "NULL device pointer");
-    const i64 T = tr->T;
     require(Ns < (i64(1) << 31) - 1, "streams longer than 2^31-1 tokens");
-    const int bT = bits_for(u64(T - 1)), bE = bits_for(u64(maxs - 1)), bS = bits_for(u64(nstreams - 1));
+    const int bT = bits_for(u64(std::max<i64>(T, 1) - 1)), bE = bits_for(u64(maxs - 1)),
+              bS = bits_for(u64(nstreams - 1));
     require(bT + bE + bS <= 64, "match key does not fit 64 bits");
     std::vector<i64> h_s(h_off, h_off + nstreams + 1);
     u64 *keys = nullptr, *keys_alt = nullptr;
@@ -1701,11 +1703,43 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       b.W = nstreams;
       b.maxwin = maxs;
       GenPlan g;
-      u64 *e_tok, *e_tok_alt, *d_rs = nullptr;
-      u32 *e_lo, *e_q, *e_hi, *e_idx, *e_idx_alt, *ea, *ecnt, *pbase;
+      u64 *e_tok = nullptr, *e_tok_alt, *d_rs = nullptr;
+      u32 *e_lo = nullptr, *e_q = nullptr, *e_hi = nullptr, *e_idx, *e_idx_alt, *ea, *ecnt, *pbase;
       i64 *scal;
       // streams that fit on chip are matched in reversed form (see k_stream_emit)
       const bool rev = maxs <= kSMMax;
+      // the stream index: reversed streams, their suffix arrays + LCP,
+      // first-token buckets (trace-independent; precomputed when `pre`)
+      const i64 *p_off;
+      const i32 *p_wid, *p_sa, *p_lcp;
+      const u64 *mtok, *stok;
+      const u32 *sord;
+      i64 E;
+      if (pre) {
+        auto plan = [&](Carver &cv) {
+          ea = cv.take<u32>(T);
+          ecnt = cv.take<u32>(T);
+          pbase = cv.take<u32>(T);
+          scal = cv.take<i64>(4);
+        };
+        Carver dry(nullptr);
+        plan(dry);
+        c.arena.reserve(dry.off, s);
+        Carver cv(c.arena.base);
+        plan(cv);
+        APO_CUDA(cudaMemsetAsync(scal, 0, sizeof(i64) * 4, s));
+        p_off = pre->d_off;
+        p_wid = pre->d_wid;
+        p_sa = pre->sa;
+        p_lcp = pre->lcp;
+        mtok = pre->rev ? pre->rs : d_streams;
+        stok = pre->stok;
+        sord = pre->sord;
+        e_lo = pre->e_lo;
+        e_q = pre->e_q;
+        e_hi = pre->e_hi;
+        E = pre->E;
+      } else {
       auto plan = [&](Carver &cv) {
         plan_gen(cv, b, g, true, c.nsmid);
         if (rev) d_rs = cv.take<u64>(Ns);
@@ -1731,28 +1765,77 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
         k_reverse_by_wid<<<grid_for(Ns, T256), T256, 0, s>>>(d_streams, g.d_off, g.d_wid, Ns, d_rs);
         APO_CHECK_LAUNCH();
         c.launches++;
-        if (!tr->d_rtok) {
-          tr->d_rtok = static_cast<u64 *>(c.pool_get(tr->tok_bytes));
-          k_reverse_traces<<<grid_for(T * 32, T256), T256, 0, s>>>(tr->d_tok, tr->d_off, T, tr->d_rtok);
-          APO_CHECK_LAUNCH();
-          c.launches++;
-        }
       }
-      const u64 *mtok = rev ? d_rs : d_streams;
+      mtok = rev ? d_rs : d_streams;
       build_sa(c, mtok, b, g.sa, true, s);
-      StreamMatch sm{g.d_off, g.d_wid, g.sa.sa, g.sa.lcp, mtok, rev ? tr->d_rtok : tr->d_tok, tr->d_off, Ns, T};
+      p_off = g.d_off;
+      p_wid = g.d_wid;
+      p_sa = g.sa.sa;
+      p_lcp = g.sa.lcp;
+      StreamMatch sm0{p_off, p_wid, p_sa, p_lcp, mtok, nullptr, nullptr, Ns, T};
       APO_CUDA(cudaMemsetAsync(scal, 0, sizeof(i64) * 4, s));
-      BucketF bf{sm, e_tok, e_lo, e_q, scal};
+      BucketF bf{sm0, e_tok, e_lo, e_q, scal};
       launch_scan<false>(c, Ns, bf, s);
-      const i64 E = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
+      E = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
       k_bucket_hi<<<grid_for(E, T256), T256, 0, s>>>(e_lo, e_q, E, g.d_off, e_hi, e_idx);
       APO_CHECK_LAUNCH();
       bool ae = radix_sort_u64_u32(c, e_tok, e_idx, e_tok_alt, e_idx_alt, E, 0, 64, s);
-      const u64 *stok = ae ? e_tok_alt : e_tok;
-      const u32 *sord = ae ? e_idx_alt : e_idx;
+      stok = ae ? e_tok_alt : e_tok;
+      sord = ae ? e_idx_alt : e_idx;
+      c.launches++;
+      if (build_idx) {  // apo_match_index: keep the index in a pooled block
+        apo_stream_index &x = *build_idx;
+        x.d_streams = d_streams;
+        x.h_off = h_s;
+        x.nstreams = nstreams;
+        x.Ns = Ns;
+        x.maxs = maxs;
+        x.E = E;
+        x.rev = rev;
+        Carver kd(nullptr);
+        auto carve = [&](Carver &k) {
+          x.d_off = k.take<i64>(size_t(nstreams) + 1);
+          x.d_wid = k.take<i32>(size_t(Ns));
+          x.sa = k.take<i32>(size_t(Ns));
+          x.lcp = k.take<i32>(size_t(Ns));
+          x.rs = rev ? k.take<u64>(size_t(Ns)) : nullptr;
+          x.stok = k.take<u64>(size_t(std::max<i64>(E, 1)));
+          x.sord = k.take<u32>(size_t(std::max<i64>(E, 1)));
+          x.e_lo = k.take<u32>(size_t(std::max<i64>(E, 1)));
+          x.e_q = k.take<u32>(size_t(std::max<i64>(E, 1)));
+          x.e_hi = k.take<u32>(size_t(std::max<i64>(E, 1)));
+        };
+        carve(kd);
+        x.bytes = kd.off + 256;
+        x.blk = c.pool_get(x.bytes);
+        Carver kc(static_cast<char *>(x.blk));
+        carve(kc);
+        auto cp = [&](void *dst, const void *src, size_t n) {
+          if (n) APO_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, s));
+        };
+        cp(x.d_off, g.d_off, sizeof(i64) * (size_t(nstreams) + 1));
+        cp(x.d_wid, g.d_wid, sizeof(i32) * size_t(Ns));
+        cp(x.sa, g.sa.sa, sizeof(i32) * size_t(Ns));
+        cp(x.lcp, g.sa.lcp, sizeof(i32) * size_t(Ns));
+        if (rev) cp(x.rs, d_rs, sizeof(u64) * size_t(Ns));
+        cp(x.stok, stok, sizeof(u64) * size_t(E));
+        cp(x.sord, sord, sizeof(u32) * size_t(E));
+        cp(x.e_lo, e_lo, sizeof(u32) * size_t(E));
+        cp(x.e_q, e_q, sizeof(u32) * size_t(E));
+        cp(x.e_hi, e_hi, sizeof(u32) * size_t(E));
+        return;
+      }
+      }  // index computed here (not pre)
+      if (rev && !tr->d_rtok) {
+        tr->d_rtok = static_cast<u64 *>(c.pool_get(tr->tok_bytes));
+        k_reverse_traces<<<grid_for(T * 32, T256), T256, 0, s>>>(tr->d_tok, tr->d_off, T, tr->d_rtok);
+        APO_CHECK_LAUNCH();
+        c.launches++;
+      }
+      StreamMatch sm{p_off, p_wid, p_sa, p_lcp, mtok, rev ? tr->d_rtok : tr->d_tok, tr->d_off, Ns, T};
       k_trace_buckets<<<grid_for(T, T256), T256, 0, s>>>(sm, stok, E, ea, ecnt);
       APO_CHECK_LAUNCH();
-      c.launches += 2;
+      c.launches++;
       PairBaseF pf{ecnt, pbase, T, scal + 1};
       launch_scan<false>(c, T, pf, s);
       const i64 P = i64(c.read_u64(reinterpret_cast<const u64 *>(scal + 1), s));
@@ -1855,7 +1938,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
             emitted = true;
             if (nh > 0 && cap > 0) {
               // interval forest of every stream (preorder sort + stack sweep)
-              k_tree_keys<<<grid_for(P, T256), T256, 0, s>>>(sqk, sqv, ilo, icnt, g.d_off, ptr, P, bS, tk, tv, gtr);
+              k_tree_keys<<<grid_for(P, T256), T256, 0, s>>>(sqk, sqv, ilo, icnt, p_off, ptr, P, bS, tk, tv, gtr);
               APO_CHECK_LAUNCH();
               const bool at = radix_sort_u64_u32(c, tk, tv, tk_alt, tv_alt, P, 0, bS + 31, s);
               const u64 *stk = at ? tk_alt : tk;
@@ -1880,8 +1963,8 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
               APO_CHECK_LAUNCH();
               if (ri && rev && nh <= cap) {
                 ri->ok = true;
-                ri->off = g.d_off;
-                ri->sa = g.sa.sa;
+                ri->off = p_off;
+                ri->sa = p_sa;
                 ri->tkey = stk;
                 ri->toff = tof;
                 ri->nint = P;
@@ -1918,7 +2001,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
               // pool run on the same stream, after it)
               i64 *ilo2 = reinterpret_cast<i64 *>(e_tok);
               u32 *hb2 = e_lo, *pt2 = e_q;
-              if (P > Ns) {
+              if (P > Ns || pre != nullptr) {  // (a precomputed index is not scratch)
                 spill_bytes = (sizeof(i64) + 2 * sizeof(u32)) * size_t(P) + 256;
                 spill = c.pool_get(spill_bytes);
                 ilo2 = reinterpret_cast<i64 *>(spill);
@@ -2010,42 +2093,94 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
 }
 }  // namespace
 
+namespace apo {
+namespace {
+// apo_match / apo_match_indexed: MATCH_ALL (mode 0) or MATCH_ALL + REPLAY
+// (mode 1) with the stream index computed here or taken from `pre`.
+void match_entry(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int64_t *h_off, int32_t nstreams,
+                 int32_t mode, apo_match_rec *d_out, int64_t cap, int64_t *d_count, cudaStream_t s,
+                 const apo_stream_index *pre) {
+  require(tr != nullptr && d_count != nullptr && cap >= 0 && nstreams >= 1 && h_off != nullptr, "invalid argument");
+  require(mode == 0 || mode == 1, "mode must be 0 (MATCH_ALL) or 1 (REPLAY)");
+  require(cap == 0 || d_out != nullptr, "d_out is NULL");
+  require((reinterpret_cast<uintptr_t>(d_out) & 15) == 0, "d_out must be 16-byte aligned");
+  if (mode == 0) {
+    match_all(c, tr, d_streams, h_off, nstreams, d_out, cap, d_count, s, nullptr, nullptr, pre);
+    return;
+  }
+  // REPLAY: MATCH_ALL into a cached library buffer (grown and re-run if
+  // too small), then the replay selection consumes the hits on the device
+  i64 nh = 0;
+  ReplayIndex ri;
+  for (;;) {
+    match_all(c, tr, d_streams, h_off, nstreams, static_cast<apo_match_rec *>(c.hitbuf),
+              i64(c.hitbuf_cap / sizeof(apo_match_rec)), d_count, s, &ri, nullptr, pre);
+    nh = i64(c.read_u64(reinterpret_cast<const u64 *>(d_count), s));
+    if (size_t(nh) * sizeof(apo_match_rec) <= c.hitbuf_cap) break;
+    if (c.hitbuf) c.pool_put(c.hitbuf, c.hitbuf_cap);
+    c.hitbuf_cap = (size_t(nh) + size_t(nh) / 16 + 1024) * sizeof(apo_match_rec);
+    c.hitbuf = c.pool_get(c.hitbuf_cap);
+  }
+  std::vector<i64> len(static_cast<size_t>(nstreams));
+  for (int q = 0; q < nstreams; ++q) len[q] = h_off[q + 1] - h_off[q];
+  const apo_replay_params prm{100, 64881, 100, 11, 10, 0};
+  run_replay(c, tr, static_cast<const apo_match_rec *>(c.hitbuf), nh, len.data(), nstreams, prm,
+             reinterpret_cast<apo_replay_rec *>(d_out), cap, d_count, s, &ri);
+  APO_CUDA(cudaMemcpyAsync(d_count + 1, &nh, sizeof(i64), cudaMemcpyHostToDevice, s));
+  APO_CUDA(cudaStreamSynchronize(s));
+}
+}  // namespace
+}  // namespace apo
+
 extern "C" {
 
 apo_status apo_match(apo_ctx *ctx, const apo_trie *tr, const uint64_t *d_streams, const int64_t *h_off,
                      int32_t nstreams, int32_t mode, apo_match_rec *d_out, int64_t cap, int64_t *d_count,
                      void *stream) {
   return trie_guard(ctx, [&](Ctx &c) {
-    require(tr != nullptr && d_count != nullptr && cap >= 0 && nstreams >= 1 && h_off != nullptr, "invalid argument");
-    require(mode == 0 || mode == 1, "mode must be 0 (MATCH_ALL) or 1 (REPLAY)");
-    require(cap == 0 || d_out != nullptr, "d_out is NULL");
-    require((reinterpret_cast<uintptr_t>(d_out) & 15) == 0, "d_out must be 16-byte aligned");
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (mode == 0) {
-      match_all(c, tr, d_streams, h_off, nstreams, d_out, cap, d_count, s);
-      return;
-    }
-    // REPLAY: MATCH_ALL into a cached library buffer (grown and re-run if
-    // too small), then the replay selection consumes the hits on the device
-    i64 nh = 0;
-    ReplayIndex ri;
-    for (;;) {
-      match_all(c, tr, d_streams, h_off, nstreams, static_cast<apo_match_rec *>(c.hitbuf),
-                i64(c.hitbuf_cap / sizeof(apo_match_rec)), d_count, s, &ri);
-      nh = i64(c.read_u64(reinterpret_cast<const u64 *>(d_count), s));
-      if (size_t(nh) * sizeof(apo_match_rec) <= c.hitbuf_cap) break;
-      if (c.hitbuf) c.pool_put(c.hitbuf, c.hitbuf_cap);
-      c.hitbuf_cap = (size_t(nh) + size_t(nh) / 16 + 1024) * sizeof(apo_match_rec);
-      c.hitbuf = c.pool_get(c.hitbuf_cap);
-    }
-    std::vector<i64> len(static_cast<size_t>(nstreams));
-    for (int q = 0; q < nstreams; ++q) len[q] = h_off[q + 1] - h_off[q];
-    const apo_replay_params prm{100, 64881, 100, 11, 10, 0};
-    run_replay(c, tr, static_cast<const apo_match_rec *>(c.hitbuf), nh, len.data(), nstreams, prm,
-               reinterpret_cast<apo_replay_rec *>(d_out), cap, d_count, s, &ri);
-    APO_CUDA(cudaMemcpyAsync(d_count + 1, &nh, sizeof(i64), cudaMemcpyHostToDevice, s));
-    APO_CUDA(cudaStreamSynchronize(s));
+    match_entry(c, tr, d_streams, h_off, nstreams, mode, d_out, cap, d_count, static_cast<cudaStream_t>(stream),
+                nullptr);
   });
+}
+
+apo_status apo_match_index(apo_ctx *ctx, const uint64_t *d_streams, const int64_t *h_off, int32_t nstreams,
+                           apo_stream_index **out, void *stream) {
+  return trie_guard(ctx, [&](Ctx &c) {
+    require(out != nullptr && nstreams >= 1 && h_off != nullptr, "invalid argument");
+    *out = nullptr;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    auto *x = new apo_stream_index();
+    x->ctx = ctx;
+    try {
+      match_all(c, nullptr, d_streams, h_off, nstreams, nullptr, 0, nullptr, s, nullptr, x, nullptr);
+      APO_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      if (x->blk) c.pool_put(x->blk, x->bytes);
+      delete x;
+      throw;
+    }
+    if (x->nstreams == 0) {  // empty streams: an index with nothing to search
+      x->d_streams = d_streams;
+      x->h_off.assign(h_off, h_off + nstreams + 1);
+      x->nstreams = nstreams;
+    }
+    *out = x;
+  });
+}
+
+apo_status apo_match_indexed(apo_ctx *ctx, const apo_trie *tr, const apo_stream_index *idx, int32_t mode,
+                             apo_match_rec *d_out, int64_t cap, int64_t *d_count, void *stream) {
+  return trie_guard(ctx, [&](Ctx &c) {
+    require(idx != nullptr && idx->ctx == ctx, "the index belongs to another context");
+    match_entry(c, tr, idx->d_streams, idx->h_off.data(), idx->nstreams, mode, d_out, cap, d_count,
+                static_cast<cudaStream_t>(stream), idx->blk ? idx : nullptr);
+  });
+}
+
+void apo_stream_index_destroy(apo_stream_index *idx) {
+  if (!idx) return;
+  if (idx->blk && idx->ctx) idx->ctx->c.pool_put(idx->blk, idx->bytes);
+  delete idx;
 }
 
 }  // extern "C"

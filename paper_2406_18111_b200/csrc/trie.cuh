@@ -18,6 +18,24 @@ struct apo_trie {
 };
 
 
+// The trace-independent half of apo_match (apo_match_index): the reversed
+// streams, their suffix arrays + LCP and first-token buckets, in one pooled
+// block of the creating context.  d_streams stays the caller's.
+struct apo_stream_index {
+  apo_ctx *ctx = nullptr;
+  const apo::u64 *d_streams = nullptr;
+  std::vector<apo::i64> h_off;
+  int nstreams = 0;
+  apo::i64 Ns = 0, maxs = 0, E = 0;
+  bool rev = false;
+  void *blk = nullptr;
+  size_t bytes = 0;
+  apo::i64 *d_off = nullptr;
+  apo::i32 *d_wid = nullptr, *sa = nullptr, *lcp = nullptr;
+  apo::u64 *rs = nullptr, *stok = nullptr;
+  apo::u32 *sord = nullptr, *e_lo = nullptr, *e_q = nullptr, *e_hi = nullptr;
+};
+
 namespace apo {
 // What the on-chip matcher leaves behind for REPLAY (apo_match mode 1): the
 // REVERSED streams' suffix arrays and every stream's matched intervals in

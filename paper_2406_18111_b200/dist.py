@@ -67,6 +67,9 @@ class SymmetricTransport:
         self.cap = 0
         self.buf = None
         self.hdl = None
+        self.stage = None
+        self.cstream = None
+        self.pulled = None
 
     def ensure(self, need: int):
         """Collective: every rank passes the same global maximum."""
@@ -88,6 +91,36 @@ class SymmetricTransport:
     def sources(self):
         """Per rank: its buffer, readable from this rank's device."""
         return list(self.hdl.buffer_ptrs)
+
+    def pull(self, ntok):
+        """Copy every peer's list (ntok[r] tokens) into local staging with the
+        copy engines, on a side stream that first waits for the caller's
+        stream (the barrier that follows the peers' publishes); returns per
+        rank a local pointer (own list: own buffer).  wait() joins."""
+        me = self.hdl.rank
+        need = sum(int(n) for r, n in enumerate(ntok) if r != me)
+        if self.stage is None or self.stage.numel() < need:
+            self.stage = torch.empty(max(int(need * 1.25), 1), dtype=torch.int64, device=self.dev)
+        if self.cstream is None:
+            self.cstream = torch.cuda.Stream(self.dev)
+        self.cstream.wait_stream(torch.cuda.current_stream(self.dev))
+        ptrs, o = [], 0
+        with torch.cuda.stream(self.cstream):
+            for r, n in enumerate(ntok):
+                n = int(n)
+                if r == me:
+                    ptrs.append(self.buf.data_ptr())
+                    continue
+                if n:
+                    self.stage[o:o + n].copy_(self.hdl.get_buffer(r, (n,), torch.int64), non_blocking=True)
+                ptrs.append(self.stage.data_ptr() + 8 * o)
+                o += n
+        self.pulled = torch.cuda.Event()
+        self.pulled.record(self.cstream)
+        return ptrs
+
+    def wait(self):
+        torch.cuda.current_stream(self.dev).wait_event(self.pulled)
 
 
 class TraceExchange:
@@ -141,14 +174,33 @@ class TraceExchange:
                 for r in range(self.world)]
 
     def union(self, trie):
-        """-> the union Trie of every rank's `trie` (identical on all ranks)."""
+        """-> the union Trie of every rank's `trie` (identical on all ranks):
+        the library kernel pulls the peers' lists over NVLink while it hashes
+        them."""
+        self._publish(trie)
+        ptrs = self.transport.sources()
+        return self.ctx.trie_build_traces_multi([(ptrs[r], self._offs[r]) for r in range(self.world)])
+
+    def start(self, trie):
+        """First half of an overlapped union: publish, exchange sizes, and
+        start pulling the peers' lists into local memory with the copy
+        engines (no SMs), so the caller's stream can run other work (e.g.
+        apo_match_index of its streams) meanwhile; finish() builds the union."""
+        self._publish(trie)
+        self._ptrs = self.transport.pull([int(x) for x in self._sizes[:, 0]])
+
+    def finish(self):
+        """-> the union Trie (after start())."""
+        self.transport.wait()
+        return self.ctx.trie_build_traces_multi([(self._ptrs[r], self._offs[r]) for r in range(self.world)])
+
+    def _publish(self, trie):
         T, n, _ = trie.info()
         all_sizes = self.gather_sizes(T, n)
         self.transport.ensure(max(int(all_sizes[:, 0].max()), 1))
         self.transport.barrier()              # peers are done reading the previous step's lists
         off = self.transport.publish(trie)    # local list -> own exchange buffer
-        offs = self.gather_offsets(all_sizes, np.diff(off))
+        self._offs = self.gather_offsets(all_sizes, np.diff(off))
         self.transport.barrier()              # every rank's copy is complete
-        ptrs = self.transport.sources()
+        self._sizes = all_sizes
         self.last_pulled_tokens = int(all_sizes[:, 0].sum() - all_sizes[self.rank, 0])
-        return self.ctx.trie_build_traces_multi([(ptrs[r], offs[r]) for r in range(self.world)])

@@ -265,12 +265,16 @@ class BatchPipeline:
             torch.cuda.set_stream(s)
             if streams is not None:
                 trie = self.ctx.trie_build(tok, off, rep, roff, self.min_len, self.max_len)
-                if self.exchange is not None:
-                    trie = self.exchange.union(trie)
                 if nxt is not None:
                     fut = self._analyse((k + 1) % 2, nxt[0], nxt[1], nxt[4])
                     launched = True
-                res = self.ctx.match(trie, streams, soff, mode=self.mode, cap=self.match_cap)
+                if self.exchange is not None:  # copy-engine pulls overlap the stream index
+                    self.exchange.start(trie)
+                    idx = self.ctx.match_index(streams, soff)
+                    trie = self.exchange.finish()
+                    res = self.ctx.match_indexed(trie, idx, mode=self.mode, cap=self.match_cap)
+                else:
+                    res = self.ctx.match(trie, streams, soff, mode=self.mode, cap=self.match_cap)
                 if self.mode == 1:
                     self.match_cap = max(int(res[0].shape[0]), 1)
                     self.last_hits = res[1]

@@ -122,6 +122,14 @@ class _ShmTransport:
     def sources(self):
         return [np.ndarray((self.cap,), dtype=np.uint64, buffer=p.buf) for p in self.peers]
 
+    def pull(self, ntok):  # the copy-engine pull: peers' lists copied out, own list in place
+        self.log.append(("pull",))
+        return [np.ndarray((self.cap,), dtype=np.uint64, buffer=p.buf)[:n].copy() if r != self.rank
+                else np.ndarray((self.cap,), dtype=np.uint64, buffer=p.buf) for r, (p, n) in enumerate(zip(self.peers, ntok))]
+
+    def wait(self):
+        self.log.append(("wait",))
+
     def close(self):
         for p in self.peers:
             p.close()
@@ -157,9 +165,13 @@ def _exchange_worker(rank, world, port, q):
     tr = _ShmTransport(port, rank, world)
     ex = TraceExchange(_CpuBuilder(), transport=tr)
     out = []
-    for step in range(3):
+    for step in range(4):
         tok, off = _exchange_lists(rank, min(step, 1))
-        out.append((ex.union(_HostTrie(tok, off)), ex.last_pulled_tokens))
+        if step < 3:
+            out.append((ex.union(_HostTrie(tok, off)), ex.last_pulled_tokens))
+        else:  # the overlapped form bench.py uses: start (pull), other work, finish
+            ex.start(_HostTrie(tok, off))
+            out.append((ex.finish(), ex.last_pulled_tokens))
     q.put((rank, out, tr.log))
     tr.close()
     dist.destroy_process_group()
@@ -180,7 +192,7 @@ def test_trace_exchange_union_gloo_world2():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    for step in range(3):
+    for step in range(4):
         lists = [_exchange_lists(r, min(step, 1)) for r in range(world)]
         want = sorted({tuple(int(x) for x in tok[off[t]:off[t + 1]]) for tok, off in lists
                        for t in range(len(off) - 1)}, key=lambda c: (-len(c), c))

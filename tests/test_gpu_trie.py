@@ -315,3 +315,25 @@ def test_match_long_streams(ctx):
     want, cnt = oracle.match_brute(sflat, soff, tt.cpu().numpy(), to)
     assert cnt == len(hits) and np.array_equal(hits, want)
     assert len(hits) > 0
+
+
+def test_match_indexed_equals_match():
+    """apo_match_index + apo_match_indexed (the stream index built before and
+    independently of the trace set, reused for two trace sets and both
+    modes) == apo_match."""
+    from paper_2406_18111_b200 import Context
+    ctx = Context(0)
+    tok, off, st, so = gen.c4(seed=71, windows=32, window=4096, templates=8)
+    d, ds = torch.from_numpy(tok).cuda(), torch.from_numpy(st).cuda()
+    idx = ctx.match_index(ds, so)
+    for half in (slice(0, 16), slice(16, 32)):
+        o = off[half.start:half.stop + 1] - off[half.start]
+        dd = d[int(off[half.start]):int(off[half.stop])]
+        rep, roff, occ = ctx.find_repeats_batched(dd, o, 25)
+        trie = ctx.trie_build(dd, o, rep, roff, 25, 0)
+        a = ctx.match(trie, ds, so, full=True)
+        b = ctx.match_indexed(trie, idx, full=True)
+        assert a.shape[0] > 0 and torch.equal(a, b)
+        ra, na = ctx.match(trie, ds, so, mode=1)
+        rb, nb = ctx.match_indexed(trie, idx, mode=1)
+        assert na == nb and torch.equal(ra, rb)
