@@ -337,3 +337,31 @@ def test_match_indexed_equals_match():
         ra, na = ctx.match(trie, ds, so, mode=1)
         rb, nb = ctx.match_indexed(trie, idx, mode=1)
         assert na == nb and torch.equal(ra, rb)
+
+
+def test_match_indexed_long_streams_and_empty_trie():
+    """The split matcher on streams longer than the on-chip limit (the
+    global per-stream search path, not reversed) and against an empty-ish
+    trace set: equal to apo_match."""
+    from paper_2406_18111_b200 import Context
+    ctx = Context(0)
+    streams = [gen.periodic(81, 40000, 97, 6, noise=0.01), gen.periodic(82, 9000, 31, 4, noise=0.02)]
+    st = np.concatenate(streams)
+    so = np.cumsum([0] + [len(x) for x in streams]).astype(np.int64)
+    ds = torch.from_numpy(st).cuda()
+    rng = gen.Rng(83)
+    traces = sorted({tuple(int(x) for x in streams[rng.below(2)][a:a + 3 + rng.below(40)])
+                     for a in (rng.below(8000) for _ in range(300))}, key=lambda t: (-len(t), t))
+    tt = np.concatenate([np.asarray(t, dtype=np.uint64) for t in traces])
+    to = np.cumsum([0] + [len(t) for t in traces]).astype(np.int64)
+    trie = ctx.trie_build_traces(torch.from_numpy(tt).cuda(), to)
+    idx = ctx.match_index(ds, so)
+    a = ctx.match(trie, ds, so, full=True, cap=1 << 24)
+    b = ctx.match_indexed(trie, idx, full=True, cap=1 << 24)
+    assert a.shape[0] > 0 and torch.equal(a, b)
+    ra, na = ctx.match(trie, ds, so, mode=1)
+    rb, nb = ctx.match_indexed(trie, idx, mode=1)
+    assert na == nb and torch.equal(ra, rb)
+    one = ctx.trie_build_traces(torch.from_numpy(np.array([1, 2, 3], dtype=np.uint64)).cuda(),
+                                np.array([0, 3], dtype=np.int64))
+    assert ctx.match_indexed(one, idx).shape[0] == ctx.match(one, ds, so).shape[0] == 0
