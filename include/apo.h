@@ -368,6 +368,27 @@ apo_status apo_dsa_heads(apo_ctx *ctx, const uint64_t *d_keys, int64_t m, uint64
 apo_status apo_dsa_scatter(apo_ctx *ctx, const uint32_t *d_pos, const uint32_t *d_rank_in, int64_t m, int64_t base,
                            uint32_t *d_rank, void *stream);
 
+/* LCP of the distributed SA ("SA, LCP <- SuffixArray(S)"; R3) by
+ * galloping over the saved rank levels, level j = ranks by the first 2^j
+ * tokens, from the highest level down: equal level-j ranks at i + l and
+ * i' + l <=> the next 2^j tokens agree, then l += 2^j.  Per level:
+ *  - apo_dsa_lcp_requests: pair p = (d_a[p], d_b[p]) with lcp d_l[p] asks
+ *    for the ranks at d_a[p] + l and d_b[p] + l: d_keys[2p], d_keys[2p+1] =
+ *    those positions (n when past the end: not to be sent), d_vals = 2p,
+ *    2p + 1;
+ *  - apo_dsa_gather (owner side): d_out[k] = d_rank[d_pos[k] - base];
+ *  - apo_dsa_lcp_update: the first nvalid answers d_resp (in the order of
+ *    the sorted requests d_req) go back to their pairs through d_by_req
+ *    (uint32[2 np], all 0xffffffff / 0xfffffffe pairs before the first
+ *    level; reset by the call); d_l[p] += step where both answers exist and
+ *    agree. */
+apo_status apo_dsa_lcp_requests(apo_ctx *ctx, const uint32_t *d_a, const uint32_t *d_b, const uint32_t *d_l,
+                                int64_t np, int64_t n, uint64_t *d_keys, uint32_t *d_vals, void *stream);
+apo_status apo_dsa_gather(apo_ctx *ctx, const uint32_t *d_pos, int64_t m, int64_t base, const uint32_t *d_rank,
+                          uint32_t *d_out, void *stream);
+apo_status apo_dsa_lcp_update(apo_ctx *ctx, const uint32_t *d_resp, const uint32_t *d_req, int64_t nvalid,
+                              int64_t np, uint32_t step, uint32_t *d_by_req, uint32_t *d_l, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -90,6 +90,9 @@ _SIGS = {
     "apo_dsa_split": (ctypes.c_int, [_VP, _VP, _VP, _I64, _VP, _VP, _I32, _VP, _VP]),
     "apo_dsa_heads": (ctypes.c_int, [_VP, _VP, _I64, ctypes.c_uint64, _I32, _I64, _I64, _VP, _VP, _VP]),
     "apo_dsa_scatter": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, _VP, _VP]),
+    "apo_dsa_lcp_requests": (ctypes.c_int, [_VP, _VP, _VP, _VP, _I64, _I64, _VP, _VP, _VP]),
+    "apo_dsa_gather": (ctypes.c_int, [_VP, _VP, _I64, _I64, _VP, _VP, _VP]),
+    "apo_dsa_lcp_update": (ctypes.c_int, [_VP, _VP, _VP, _I64, _I64, ctypes.c_uint32, _VP, _VP, _VP]),
 }
 
 _lib = None

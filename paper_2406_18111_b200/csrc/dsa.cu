@@ -18,7 +18,12 @@
 //                    rank = global index of the head + 1, heads before the
 //                    block carried in; also the number of heads and the
 //                    last head's global index;
-//   apo_dsa_scatter  received (position, rank) pairs into the owned block.
+//   apo_dsa_scatter  received (position, rank) pairs into the owned block;
+//   apo_dsa_lcp_requests / apo_dsa_gather / apo_dsa_lcp_update
+//                    the LCP of the distributed SA by galloping over the
+//                    saved rank levels (equal level-j ranks <=> equal 2^j-token
+//                    prefixes): per level, every adjacent pair asks the
+//                    owners of i + l and i' + l for their level ranks.
 #include "pipeline.cuh"
 
 namespace apo {
@@ -116,6 +121,43 @@ __global__ void k_dsa_scatter(const u32 *__restrict__ pos, const u32 *__restrict
   if (k < m) rank[i64(pos[k]) - base] = rk[k];
 }
 
+// LCP galloping step requests: pair p = (a[p], b[p]) at current lcp l[p]
+// asks for the level ranks at a + l and b + l (request 2p and 2p + 1;
+// key = position, or n when past the end: such requests are not sent).
+__global__ void k_dsa_lcp_req(const u32 *__restrict__ a, const u32 *__restrict__ b, const u32 *__restrict__ l,
+                              i64 np, i64 n, u64 *__restrict__ keys, u32 *__restrict__ vals) {
+  const i64 p = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  const i64 pa = i64(a[p]) + l[p], pb = i64(b[p]) + l[p];
+  keys[2 * p] = u64(pa < n ? pa : n);
+  keys[2 * p + 1] = u64(pb < n ? pb : n);
+  vals[2 * p] = u32(2 * p);
+  vals[2 * p + 1] = u32(2 * p + 1);
+}
+
+__global__ void k_dsa_gather(const u32 *__restrict__ pos, i64 m, i64 base, const u32 *__restrict__ rank,
+                             u32 *__restrict__ out) {
+  const i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < m) out[k] = rank[i64(pos[k]) - base];
+}
+
+// Answers (in sorted request order, the first nvalid requests) back to the
+// pairs; a pair extends its lcp by `step` iff both answers exist and agree.
+__global__ void k_dsa_lcp_fill(const u32 *__restrict__ resp, const u32 *__restrict__ req, i64 nvalid,
+                               u32 *__restrict__ by_req) {
+  const i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < nvalid) by_req[req[k]] = resp[k];
+}
+
+__global__ void k_dsa_lcp_step(u32 *__restrict__ by_req, i64 np, u32 step, u32 *__restrict__ l) {
+  const i64 p = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  const u32 x = by_req[2 * p], y = by_req[2 * p + 1];
+  if (x == y && x != 0xffffffffu) l[p] += step;
+  by_req[2 * p] = 0xffffffffu;  // reset for the next level (past-the-end answers stay unequal)
+  by_req[2 * p + 1] = 0xfffffffeu;
+}
+
 }  // namespace
 }  // namespace apo
 
@@ -191,6 +233,49 @@ apo_status apo_dsa_scatter(apo_ctx *ctx, const uint32_t *d_pos, const uint32_t *
                                                                                     d_rank);
     APO_CHECK_LAUNCH();
     c.launches++;
+  });
+}
+
+apo_status apo_dsa_lcp_requests(apo_ctx *ctx, const uint32_t *d_a, const uint32_t *d_b, const uint32_t *d_l,
+                                int64_t np, int64_t n, uint64_t *d_keys, uint32_t *d_vals, void *stream) {
+  return guarded(ctx, [&](Ctx &c) {
+    require(np >= 0 && n >= 0 && (np == 0 || (d_a && d_b && d_l && d_keys && d_vals)) && 2 * np < (i64(1) << 32),
+            "invalid argument");
+    if (np == 0) return;
+    k_dsa_lcp_req<<<grid_for(np, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(d_a, d_b, d_l, np, n, d_keys,
+                                                                                     d_vals);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+  });
+}
+
+apo_status apo_dsa_gather(apo_ctx *ctx, const uint32_t *d_pos, int64_t m, int64_t base, const uint32_t *d_rank,
+                          uint32_t *d_out, void *stream) {
+  return guarded(ctx, [&](Ctx &c) {
+    require(m >= 0 && base >= 0 && (m == 0 || (d_pos && d_rank && d_out)), "invalid argument");
+    if (m == 0) return;
+    k_dsa_gather<<<grid_for(m, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(d_pos, m, base, d_rank, d_out);
+    APO_CHECK_LAUNCH();
+    c.launches++;
+  });
+}
+
+apo_status apo_dsa_lcp_update(apo_ctx *ctx, const uint32_t *d_resp, const uint32_t *d_req, int64_t nvalid,
+                              int64_t np, uint32_t step, uint32_t *d_by_req, uint32_t *d_l, void *stream) {
+  return guarded(ctx, [&](Ctx &c) {
+    require(nvalid >= 0 && np >= 0 && nvalid <= 2 * np && (np == 0 || (d_by_req && d_l)) &&
+                (nvalid == 0 || (d_resp && d_req)),
+            "invalid argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (nvalid > 0) {
+      k_dsa_lcp_fill<<<grid_for(nvalid, 256), 256, 0, s>>>(d_resp, d_req, nvalid, d_by_req);
+      APO_CHECK_LAUNCH();
+    }
+    if (np > 0) {
+      k_dsa_lcp_step<<<grid_for(np, 256), 256, 0, s>>>(d_by_req, np, step, d_l);
+      APO_CHECK_LAUNCH();
+    }
+    c.launches += 2;
   });
 }
 

@@ -2,7 +2,9 @@
 group (a window larger than one GPU).
 
 "SA, LCP <- SuffixArray(S)" (Alg. 2) by prefix doubling
-where every round is a distributed sample sort.  Rank r owns the contiguous
+where every round is a distributed sample sort; the LCP (`lcp()`) by
+galloping over the saved rank levels with one request/answer exchange per
+level.  Rank r owns the contiguous
 positions [a_r, a_{r+1}) of S, a_r = r * n // G.  Round 0 sorts the
 suffixes by their first token; round j by their first 2^j tokens:
 
@@ -98,6 +100,23 @@ class CudaDsaOps:
     def scatter(self, pos, rank_in, base: int, rank):
         self.ctx._raise(self.lib.apo_dsa_scatter(self.ctx.h, self._p(pos), self._p(rank_in), pos.numel(), base,
                                                  self._p(rank), self._s()))
+
+    def lcp_requests(self, a, b, l, n: int):
+        np_ = a.numel()
+        k, v = self.empty(2 * np_, torch.uint64), self.empty(2 * np_, torch.int32)
+        self.ctx._raise(self.lib.apo_dsa_lcp_requests(self.ctx.h, self._p(a), self._p(b), self._p(l), np_, n,
+                                                      self._p(k), self._p(v), self._s()))
+        return k, v
+
+    def gather(self, pos, base: int, rank):
+        out = self.empty(pos.numel(), torch.int32)
+        self.ctx._raise(self.lib.apo_dsa_gather(self.ctx.h, self._p(pos), pos.numel(), base, self._p(rank),
+                                                self._p(out), self._s()))
+        return out
+
+    def lcp_update(self, resp, req, nvalid: int, step: int, by_req, l):
+        self.ctx._raise(self.lib.apo_dsa_lcp_update(self.ctx.h, self._p(resp), self._p(req), nvalid, l.numel(), step,
+                                                    self._p(by_req), self._p(l), self._s()))
 
 
 class DistSuffixArray:
@@ -213,6 +232,7 @@ class DistSuffixArray:
         rank_new, heads, gbase = self._new_ranks(keys)
         rank_block = ops.empty(m, torch.int32)
         self._to_owners(vals, rank_new, a, n, rank_block, base)
+        self.levels = [rank_block.clone()]  # level j: ranks by the first 2^j tokens (for the LCP)
         self.rounds = 1
         h = 1
         kbits = bits_for((n + 1) * (n + 1) - 1)
@@ -237,5 +257,52 @@ class DistSuffixArray:
             self.rounds += 1
             if heads < n:
                 self._to_owners(vals, rank_new, a, n, rank_block, base)
+                self.levels.append(rank_block.clone())
             h *= 2
+        self.n, self.a, self.sa_part, self.gbase = n, a, vals, gbase
         return vals, gbase
+
+    def lcp(self):
+        """After run(): this rank's part of the LCP array, lcp[k] =
+        LCP(SA[k], SA[k+1]) for its SA entries (0 for the global last, R3),
+        by galloping over the saved levels from the highest down: per level
+        every adjacent pair asks the owners of i + l and i' + l for their
+        level ranks (one all-to-all each way) and extends l by 2^j where they
+        agree (equal level-j ranks <=> equal 2^j-token prefixes)."""
+        ops, G, r = self.ops, self.G, self.r
+        n, a, sa = self.n, self.a, self.sa_part
+        base = a[r]
+        m = sa.numel()
+        first = int(sa[0].item()) if m else -1
+        info = self._all_gather_i64([m, first])
+        nxt = next((info[q][1] for q in range(r + 1, G) if info[q][0] > 0), -1)
+        if m == 0:  # no pairs here, but every level's collectives still run
+            pa = b = ops.empty(0, torch.int32)
+        elif nxt >= 0:
+            b = torch.cat([sa[1:], torch.tensor([nxt], dtype=torch.int32, device=ops.device)])
+            pa = sa
+        else:
+            b = sa[1:].contiguous()
+            pa = sa[:-1].contiguous()
+        npairs = pa.numel()
+        lv = torch.zeros(npairs, dtype=torch.int32, device=ops.device)
+        by_req = torch.tensor([-1, -2], dtype=torch.int32, device=ops.device).repeat(max(npairs, 1))[:2 * npairs]
+        bk = torch.tensor(a[1:G] + [n], dtype=torch.int64, device=ops.device).view(torch.uint64)
+        bv = torch.zeros(G, dtype=torch.int32, device=ops.device)
+        for j in reversed(range(len(self.levels))):
+            keys, vals = ops.lcp_requests(pa, b.contiguous(), lv, n)
+            ops.sort(keys, vals, bits_for(n))
+            cnt = ops.split(keys, vals, bk, bv, G + 1)  # per owner, then the past-the-end requests
+            if G > 1:
+                send, recv = self._exchange_counts(cnt[:G])
+            else:
+                send = recv = [int(cnt[0].item())]
+            nvalid = int(sum(send))
+            pos = self._u64(keys[:nvalid]).to(torch.int32)
+            pos_in = self._all_to_all(pos, send, recv) if G > 1 else pos
+            ans = ops.gather(pos_in, base, self.levels[j])
+            resp = self._all_to_all(ans, recv, send) if G > 1 else ans
+            ops.lcp_update(resp, vals[:nvalid].contiguous(), nvalid, 1 << j, by_req, lv)
+        if nxt < 0 and m > 0:
+            lv = torch.cat([lv, torch.zeros(1, dtype=torch.int32, device=ops.device)])
+        return lv

@@ -402,6 +402,23 @@ class _NpDsaOps:
     def scatter(self, pos, rank_in, base, rank):
         rank.numpy()[pos.numpy() - base] = rank_in.numpy()
 
+    def lcp_requests(self, a, b, l, n):
+        pa = np.minimum(a.numpy().astype(np.int64) + l.numpy(), n)
+        pb = np.minimum(b.numpy().astype(np.int64) + l.numpy(), n)
+        k = np.empty(2 * len(pa), np.uint64)
+        k[0::2], k[1::2] = pa, pb
+        return torch.from_numpy(k.view(np.int64)).view(torch.uint64), torch.arange(2 * len(pa), dtype=torch.int32)
+
+    def gather(self, pos, base, rank):
+        return torch.from_numpy(rank.numpy()[pos.numpy() - base].copy())
+
+    def lcp_update(self, resp, req, nvalid, step, by_req, l):
+        br = by_req.numpy()
+        br[req.numpy()[:nvalid]] = resp.numpy()[:nvalid]
+        x, y = br[0::2], br[1::2]
+        l.numpy()[(x == y) & (x != -1)] += step
+        br[0::2], br[1::2] = -1, -2
+
 
 def _dsa_strings():
     from workloads import gen
@@ -420,7 +437,7 @@ def _dsa_worker(rank, world, port, q):
         blk = torch.from_numpy(S[a[rank]:a[rank + 1]].view(np.int64).copy()).view(torch.uint64)
         d = DistSuffixArray(_NpDsaOps(), oversample=8)
         part, g = d.run(blk, n)
-        out.append((g, part.numpy().copy(), d.rounds))
+        out.append((g, part.numpy().copy(), d.rounds, d.lcp().numpy().copy()))
     q.put((rank, out))
     dist.destroy_process_group()
 
@@ -442,7 +459,11 @@ def test_dist_suffix_array_gloo(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     for i, S in enumerate(_dsa_strings()):
-        parts = sorted(((res[r][i][0], res[r][i][1]) for r in range(world)), key=lambda x: x[0])
-        got = np.concatenate([p for _, p in parts])
-        assert [g for g, _ in parts] == list(np.cumsum([0] + [len(p) for _, p in parts[:-1]]))
-        assert np.array_equal(got, oracle.sa_naive(S)), i
+        parts = sorted(((res[r][i][0], res[r][i][1], res[r][i][3]) for r in range(world)), key=lambda x: x[0])
+        got = np.concatenate([p for _, p, _ in parts])
+        assert [g for g, _, _ in parts] == list(np.cumsum([0] + [len(p) for _, p, _ in parts[:-1]]))
+        sa = oracle.sa_naive(S)
+        assert np.array_equal(got, sa), i
+        lcp = np.concatenate([c for _, _, c in parts])
+        want = np.append(oracle.lcp_naive(S, sa), 0)  # LCP(SA[k], SA[k+1]); 0 for the last (R3)
+        assert np.array_equal(lcp, want), i

@@ -1,5 +1,5 @@
-"""Distributed suffix array on the GPU: DistSuffixArray
-with the library's apo_dsa_* steps and K1, NCCL collectives.  One process
+"""Distributed suffix array + LCP on the GPU:
+DistSuffixArray with the library's apo_dsa_* steps and K1, NCCL collectives.  One process
 (world 1: the doubling loop, keys, heads and scatter kernels) and, on a box
 with two GPUs, two ranks (the sample-sort exchange over NVLink).  Expected:
 the oracle's suffix array (tier 0 naive sort on small inputs; the O(n)
@@ -47,7 +47,7 @@ def _worker(rank, world, port, q):
         blk = torch.from_numpy(S[a[rank]:a[rank + 1]].copy()).cuda()
         d = DistSuffixArray(CudaDsaOps(ctx))
         part, g = d.run(blk, n)
-        out.append((g, part.cpu().numpy().copy(), d.rounds))
+        out.append((g, part.cpu().numpy().copy(), d.rounds, d.lcp().cpu().numpy().copy()))
     q.put((rank, out))
     dist.barrier()
     dist.destroy_process_group()
@@ -69,13 +69,17 @@ def _run(world):
         p.join(timeout=120)
         assert p.exitcode == 0
     for i, (name, S) in enumerate(_cases()):
-        parts = sorted(((res[r][i][0], res[r][i][1]) for r in range(world)), key=lambda x: x[0])
-        sa = np.concatenate([p for _, p in parts]).astype(np.int64)
-        assert [g for g, _ in parts] == list(np.cumsum([0] + [len(p) for _, p in parts[:-1]])), name
+        parts = sorted(((res[r][i][0], res[r][i][1], res[r][i][3]) for r in range(world)), key=lambda x: x[0])
+        sa = np.concatenate([p for _, p, _ in parts]).astype(np.int64)
+        assert [g for g, _, _ in parts] == list(np.cumsum([0] + [len(p) for _, p, _ in parts[:-1]])), name
+        lcp = np.concatenate([c for _, _, c in parts]).astype(np.int64)
         if len(S) <= 5000:
             assert np.array_equal(sa, oracle.sa_naive(S)), name
+            want = oracle.lcp_naive(S, sa)
         else:
             assert oracle.sa_check(S, sa), name  # the suffix array is unique: certified == oracle
+            want = oracle.lcp_kasai(S, sa)
+        assert np.array_equal(lcp, np.append(np.asarray(want, dtype=np.int64), 0)), name
 
 
 def test_dist_suffix_array_one_gpu():

@@ -23,7 +23,7 @@ n = len(S)
 a = [r * n // world for r in range(world + 1)]
 blk = torch.from_numpy(S[a[rank]:a[rank + 1]].copy()).cuda()
 d = DistSuffixArray(CudaDsaOps(ctx))
-ts = []
+ts, tl = [], []
 for it in range(3):
     dist.barrier()
     torch.cuda.synchronize()
@@ -35,21 +35,32 @@ for it in range(3):
     t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ts.append(float(t.item()))
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0.record()
+    lcp = d.lcp()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tl.append(float(t.item()))
 # spot check against the single-GPU suffix array on rank 0
 sizes = torch.tensor([part.numel()], device="cuda")
 allsz = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(world)]
 dist.all_gather(allsz, sizes)
-out = {"config": cfg, "n": n, "ranks": world, "rounds": d.rounds, "ms": ts, "part_sizes": [int(x.item()) for x in allsz]}
+out = {"config": cfg, "n": n, "ranks": world, "rounds": d.rounds, "sa_ms": ts, "lcp_ms": tl,
+       "part_sizes": [int(x.item()) for x in allsz]}
 if rank == 0:
     full = torch.from_numpy(S).cuda()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    sa1 = ctx.suffix_array(full, lcp=False)
+    sa1, lcp1 = ctx.suffix_array(full, lcp=True)
     e1.record()
     torch.cuda.synchronize()
-    out["single_gpu_sa_ms"] = e0.elapsed_time(e1)
-    out["rank0_part_matches_single_gpu"] = bool(torch.equal(sa1[:part.numel()], part))
+    out["single_gpu_sa_lcp_ms"] = e0.elapsed_time(e1)
+    out["rank0_part_matches_single_gpu"] = bool(torch.equal(sa1[:part.numel()], part)) and bool(
+        torch.equal(lcp1[:lcp.numel()], lcp[:lcp1.numel()][:lcp.numel()]))
     print(json.dumps(out), flush=True)
 dist.barrier()
 dist.destroy_process_group()
