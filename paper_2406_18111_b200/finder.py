@@ -208,7 +208,7 @@ class BatchPipeline:
         # the analysis runs at the lowest stream priority, the rest of a
         # batch at the highest: when a CTA slot frees up, the block
         # scheduler serves matching / replay first, the analysis fills the
-        # rest (K9 is not persistent, so it yields SMs window by window)
+        # rest
         least, greatest = torch.cuda.Stream.priority_range()
         self.astream = torch.cuda.Stream(dev, priority=least)
         self.hstream = torch.cuda.Stream(dev, priority=greatest)
