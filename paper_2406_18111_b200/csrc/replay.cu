@@ -96,6 +96,8 @@ struct RP {
   const int *wq;         // wavelet work items: stream
   const i64 *wr0;        // wavelet work items: first record (nitems + 1 ends)
   struct WvMat *wv;      // per stream: its wavelet matrix (lazy scores in phase D)
+  const u32 *endoff;     // per stream position: first hit record (mode 1, from the emitter)
+  const unsigned short *endml;  // per stream position: shortest trace ending there (0xffff: none)
 };
 
 __device__ __forceinline__ u32 lanemask_lt_() {
@@ -699,6 +701,91 @@ __global__ void __launch_bounds__(32) k_rp_decide(RP a) {
   if (lane == 0) a.rcnt[q] = nrep;
 }
 
+// Phase D by ends (mode 1 with the emitter's per-end index): lanes test 32
+// ends at a time -- an end has an eligible record iff its shortest trace
+// starts at or after the frontier (e - minlen + 1 >= frontier) -- and the
+// first such end is decided over its whole record run (records in trace-id
+// order = length descending; the eligible ones are a suffix), scores
+// evaluated lazily as in k_rp_decide; the replay moves the frontier and the
+// scan continues after that end.
+__global__ void __launch_bounds__(32) k_rp_decide_ends(RP a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int q = a.order[blockIdx.x], lane = threadIdx.x;
+  const i64 hb = a.hbeg[q], he = a.hbeg[q + 1];
+  if (lane == 0) a.rcnt[q] = 0;
+  if (hb == he) return;
+  const u32 nw = (a.maxslot[q] + 31) / 32;
+  u32 *rep = nw <= a.on_chip_bits ? reinterpret_cast<u32 *>(smraw) : static_cast<u32 *>(a.gstate) + a.gstate_off[q];
+  for (u32 i = lane; i < nw; i += 32) rep[i] = 0u;
+  __syncwarp();
+  const i64 beg = a.ix_off[q];
+  const int n = int(a.ix_off[q + 1] - beg);
+  i64 frontier = 0;
+  u32 nrep = 0;
+  int4 *stage = a.stage + a.soff[q];
+  for (int e0 = 0; e0 < n; e0 += 32) {
+    const int e = e0 + lane;
+    const u32 ml = e < n ? u32(a.endml[beg + e]) : 0xffffu;
+    u32 pend = __ballot_sync(0xffffffffu, e < n);
+    while (pend) {
+      const u32 cand = pend & __ballot_sync(0xffffffffu, ml != 0xffffu && i64(e) - i64(ml) + 1 >= frontier);
+      if (!cand) break;
+      const int l = __ffs(cand) - 1;
+      pend &= ~((2u << l) - 1u);
+      const int ed = e0 + l;
+      const i64 r0 = a.endoff[beg + ed];
+      const i64 r1 = ed + 1 < n ? i64(a.endoff[beg + ed + 1]) : he;
+      // the end's records, 32 at a time; keep the best eligible one
+      bool have = false;
+      u64 bs = 0;
+      u32 bl = 0, bt = 0, bslot = 0;
+      for (i64 k0 = r0; k0 < r1; k0 += 32) {
+        const i64 k = k0 + lane;
+        const bool valid = k < r1;
+        int4 r = make_int4(-1, -1, -1, 0);
+        u32 L = 0;
+        if (valid) {
+          r = a.hits[k];
+          L = u32(__ldg(&a.tlen_off[r.z + 1]) - __ldg(&a.tlen_off[r.z]));
+        }
+        const bool ok = valid && i64(ed) - i64(L) + 1 >= frontier;
+        const u32 slot = u32(r.w);
+        u64 sc = 0;
+        if (ok) {
+          sc = wv_score(a, q, r, L);
+          if ((rep[slot >> 5] >> (slot & 31)) & 1u) sc = sc * a.bonus_num / a.bonus_den;
+        }
+        const int b = warp_best(ok, sc, L, u32(r.z));
+        if (b >= 0) {
+          const u64 s1 = __shfl_sync(0xffffffffu, sc, b);
+          const u32 l1 = __shfl_sync(0xffffffffu, L, b), t1 = __shfl_sync(0xffffffffu, u32(r.z), b);
+          const u32 z1 = __shfl_sync(0xffffffffu, slot, b);
+          if (!have || beats(s1, l1, t1, bs, bl, bt)) {
+            bs = s1;
+            bl = l1;
+            bt = t1;
+            bslot = z1;
+            have = true;
+          }
+        }
+      }
+      if (have) {  // always: the end had an eligible record
+        __syncwarp();
+        if (lane == 0) {
+          const u32 mk = 1u << (bslot & 31);
+          const u32 old = rep[bslot >> 5];
+          stage[nrep] = make_int4(q, ed, int(bt), (old & mk) ? 0 : 1);
+          rep[bslot >> 5] = old | mk;
+        }
+        __syncwarp();
+        ++nrep;
+        frontier = i64(ed) + 1;
+      }
+    }
+  }
+  if (lane == 0) a.rcnt[q] = nrep;
+}
+
 struct ReplayScanF {
   const u32 *cnt;
   u32 *base;
@@ -843,7 +930,8 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   RP a{reinterpret_cast<const int4 *>(d_hits), tr->d_off, ddq, int(dq.size()), prm.count_cap, prm.decay_period,
        1.0 / double(prm.decay_period), u32(prm.bonus_num), u32(prm.bonus_den), nstreams, slot_bits, hbeg, pbeg,
        pstream, maxslot, run_slot, run_cnt, run_last, nruns, sc, cmax, order, nullptr, gso, 0u, 0u, soff, stage,
-       rcnt, nullptr, nullptr, nullptr, nullptr, wq, wr0, wv};
+       rcnt, nullptr, nullptr, nullptr, nullptr, wq, wr0, wv, nullptr, nullptr};
+  const bool by_ends = fast && ri->endoff != nullptr && ri->endml != nullptr;
   const size_t psmem = sizeof(PartSmem);
   if (fast) {
     APO_CUDA(cudaMemcpyAsync(wq, h_wq.data(), sizeof(int) * size_t(nitems), cudaMemcpyHostToDevice, s));
@@ -857,9 +945,14 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
     c.smem_optin(reinterpret_cast<const void *>(k_rp_wvbuild), wsmem);
     k_rp_wvbuild<<<nstreams, kWvThreads, wsmem, s>>>(a);
     APO_CHECK_LAUNCH();
-    k_rp_cmax<<<unsigned(nitems), 256, 0, s>>>(a);
-    APO_CHECK_LAUNCH();
-    c.launches++;
+    if (by_ends) {  // the emitter's per-end index replaces the per-chunk latest starts
+      a.endoff = ri->endoff;
+      a.endml = ri->endml;
+    } else {
+      k_rp_cmax<<<unsigned(nitems), 256, 0, s>>>(a);
+      APO_CHECK_LAUNCH();
+      c.launches++;
+    }
   } else {
     c.smem_optin(reinterpret_cast<const void *>(k_rp_local), psmem);
     c.smem_optin(reinterpret_cast<const void *>(k_rp_scores), psmem);
@@ -897,7 +990,10 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
     k_rp_scores<<<unsigned(nparts), kPartThreads, psmem, s>>>(a);
     APO_CHECK_LAUNCH();
   }
-  k_rp_decide<<<nstreams, 32, size_t(smax_d) * 4, s>>>(a);
+  if (by_ends)
+    k_rp_decide_ends<<<nstreams, 32, size_t(smax_d) * 4, s>>>(a);
+  else
+    k_rp_decide<<<nstreams, 32, size_t(smax_d) * 4, s>>>(a);
   APO_CHECK_LAUNCH();
   ReplayScanF f{rcnt, rbase, nstreams, d_count};
   launch_scan<false>(c, nstreams, f, s);
@@ -910,6 +1006,10 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   if (gstate) c.pool_put(gstate, sizeof(u32) * size_t(gw));
   c.pool_put(hbeg0, hb_bytes);
   c.pool_put(ws, ws_bytes);
+  if (fast) {
+    c.pool_put(ri->endoff, ri->endoff_bytes);
+    c.pool_put(ri->endml, ri->endml_bytes);
+  }
 }
 
 }  // namespace apo

@@ -977,7 +977,9 @@ __global__ void __launch_bounds__(kEmitThreads, 1) k_stream_emit(StreamMatch m, 
                                                                  const u32 *__restrict__ qorder,
                                                                  const u32 *__restrict__ opar,
                                                                  const u32 *__restrict__ otr,
-                                                                 const u32 *__restrict__ odep, bool pair32) {
+                                                                 const u32 *__restrict__ odep, bool pair32,
+                                                                 u32 *__restrict__ endoff,
+                                                                 unsigned short *__restrict__ endml) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ u32 s_warp[33];
   const int q = int(qorder[blockIdx.x]);
@@ -1073,12 +1075,21 @@ __global__ void __launch_bounds__(kEmitThreads, 1) k_stream_emit(StreamMatch m, 
   };
 #pragma unroll 1
   for (int j = 0; j < kPer; ++j) {
-    if (!ce[j]) continue;
     const i64 e = b0 + j;
-    u32 z = deep[RISA[n - 1 - e]] - 1u;
+    if (endoff != nullptr && e < n) endoff[beg + e] = u32(pos);  // REPLAY (mode 1): the end's first record
+    if (!ce[j]) {
+      if (endml != nullptr && e < n) endml[beg + e] = 0xffffu;
+      continue;
+    }
+    u32 z = deep[RISA[n - 1 - e]] - 1u, zl = z;
     for (u32 k = 0; k < ce[j]; ++k, ++pos) {
       put(pos, make_int4(q, i32(e), i32(trs[z]), i32(z)));  // slot = stream-local interval id
+      zl = z;
       z = par[z];
+    }
+    if (endml != nullptr) {  // the end's shortest trace (its root-most interval): the latest start is e - len + 1
+      const u32 t = trs[zl];
+      endml[beg + e] = (unsigned short)min(i64(0xfffe), m.toff[t + 1] - m.toff[t]);
     }
   }
   if (have) reinterpret_cast<int4 *>(out)[hpos] = held;
@@ -1958,8 +1969,16 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
               const size_t esmem = sizeof(u32) * (kSMMax + 3 * kEmitPairs) + sizeof(unsigned short) * kSMMax;
               c.smem_optin(reinterpret_cast<const void *>(k_stream_emit), esmem);
               const bool pair32 = (reinterpret_cast<uintptr_t>(d_out) & 31) == 0;
+              u32 *endoff = nullptr;
+              unsigned short *endml = nullptr;
+              if (ri && rev && nh <= cap && Ns < (i64(1) << 32)) {  // REPLAY's per-end index (mode 1)
+                ri->endoff_bytes = sizeof(u32) * size_t(Ns);
+                ri->endml_bytes = sizeof(unsigned short) * size_t(Ns);
+                endoff = static_cast<u32 *>(c.pool_get(ri->endoff_bytes));
+                endml = static_cast<unsigned short *>(c.pool_get(ri->endml_bytes));
+              }
               k_stream_emit<<<nstreams, kEmitThreads, esmem, s>>>(sm, stk, tof, qbase, cap, d_out, qorder, gpar, otr,
-                                                                  gdep, pair32);
+                                                                  gdep, pair32, endoff, endml);
               APO_CHECK_LAUNCH();
               if (ri && rev && nh <= cap) {
                 ri->ok = true;
@@ -1968,6 +1987,8 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
                 ri->tkey = stk;
                 ri->toff = tof;
                 ri->nint = P;
+                ri->endoff = endoff;
+                ri->endml = endml;
               }
               c.launches += 4;
             }

@@ -48,6 +48,12 @@ struct ReplayIndex {
   const u64 *tkey = nullptr;  // per interval (preorder): (stream << 30) | (lo << 15) | (32767 - hi)
   const u32 *toff = nullptr;  // per stream: first interval (nstreams + 1)
   i64 nint = 0;               // intervals of all streams
+  // per stream position (end): the index of its first hit record and the
+  // length of the shortest trace ending there (0xffff: no hit); pooled
+  // blocks written by the emitter, returned by run_replay
+  u32 *endoff = nullptr;
+  unsigned short *endml = nullptr;
+  size_t endoff_bytes = 0, endml_bytes = 0;
 };
 // REPLAY selection over MATCH_ALL hits (replay.cu); synchronises s.  With
 // ri->ok the trace states come from the matcher's index (no per-part
