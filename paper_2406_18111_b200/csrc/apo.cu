@@ -121,22 +121,23 @@ struct Plan {
   size_t bytes = 0;
 };
 
-void plan_all(Carver &cv, Batch &b, Plan &p, bool want_lcp, bool want_select, int nsmid) {
+void plan_all(Carver &cv, Batch &b, Plan &p, bool want_lcp, bool want_select, int nsmid, int min_len) {
   if (b.W > 1) {
     p.d_off = cv.take<i64>(size_t(b.W) + 1);
     p.d_wid = cv.take<i32>(size_t(b.N));
   }
   plan_sa(cv, b, p.sa, want_lcp || want_select, nsmid);
-  if (want_select) plan_select(cv, b, p.sel);
+  if (want_select) plan_select(cv, b, p.sel, min_len);
 }
 
-Plan setup(Ctx &c, Batch &b, const i64 *h_off, bool want_lcp, bool want_select, cudaStream_t s) {
+Plan setup(Ctx &c, Batch &b, const i64 *h_off, bool want_lcp, bool want_select, cudaStream_t s,
+           int min_len = 1) {
   Plan p;
   Carver dry(nullptr);
-  plan_all(dry, b, p, want_lcp, want_select, c.nsmid);
+  plan_all(dry, b, p, want_lcp, want_select, c.nsmid, min_len);
   c.arena.reserve(dry.off, s);
   Carver cv(c.arena.base);
-  plan_all(cv, b, p, want_lcp, want_select, c.nsmid);
+  plan_all(cv, b, p, want_lcp, want_select, c.nsmid, min_len);
   if (b.W > 1) {
     APO_CUDA(cudaMemcpyAsync(p.d_off, h_off, sizeof(i64) * (b.W + 1), cudaMemcpyHostToDevice, s));
     k_fill_wid<<<b.W, 256, 0, s>>>(p.d_off, b.W, b.N, p.d_wid);
@@ -304,7 +305,7 @@ apo_status apo_candidates(apo_ctx *ctx, const uint64_t *d_tok, int32_t n, int32_
     require(d_tok != nullptr, "NULL device pointer");
     int64_t off[2] = {0, n};
     Batch b = describe(off, 1);
-    Plan p = setup(c, b, off, true, true, s);
+    Plan p = setup(c, b, off, true, true, s, min_len);
     build_sa(c, d_tok, b, p.sa, true, s);
     select_candidates(c, d_tok, b, p.sa, min_len, p.sel, s);
     emit_candidates(c, b, p.sel, d_len, d_id, d_start, d_kept, cap, d_count, s);
@@ -334,7 +335,7 @@ static apo_status find_common(apo_ctx *ctx, const uint64_t *d_tok, const int64_t
       return;
     }
     require(d_tok != nullptr, "NULL device pointer");
-    Plan p = setup(c, b, h_off, true, true, s);
+    Plan p = setup(c, b, h_off, true, true, s, min_len);
     build_sa(c, d_tok, b, p.sa, true, s);
     select_candidates(c, d_tok, b, p.sa, min_len, p.sel, s);
     emit_repeats(c, b, p.sel, prm.min_count, d_out, cap, d_out_off, d_occ, occ_cap, d_counts, s);

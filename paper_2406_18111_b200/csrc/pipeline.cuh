@@ -87,10 +87,14 @@ struct SelWork {
   u32 *oidx;              // 2N occurrence index per candidate
   u32 *wcnt;              // W+1 repeats per window
   u64 *scal;              // small device scalars
+  // the per-window greedy's kept candidates: per window up to kcap indices
+  // (in candidate order) and their count, then compacted to klist (K entries)
+  u32 *kwin = nullptr, *kcnt = nullptr, *kbase = nullptr, *klist = nullptr;
+  i64 kcap = 0, K = -1;   // K: kept candidates (-1: no compact list, scan all candidates)
   i64 m = 0, G = 0;       // host copies of candidate / group counts
 };
 
-void plan_select(Carver &cv, const Batch &b, SelWork &w);
+void plan_select(Carver &cv, const Batch &b, SelWork &w, int min_len);
 // Runs K5..K7 (candidates, ordering, greedy).  After return, w.m and w.G are
 // valid and w.cl/cs/cg/state hold the candidates in the paper's order.
 void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa, int min_len,

@@ -593,7 +593,9 @@ constexpr int kGreedyWarps = 8;
 
 __global__ void __launch_bounds__(kGreedyWarps * 32) k_greedy_window(Batch b, const i32 *__restrict__ cl,
                                                                      const i32 *__restrict__ cs, i64 m,
-                                                                     u8 *__restrict__ state) {
+                                                                     u8 *__restrict__ state, u32 *__restrict__ kwin,
+                                                                     u32 *__restrict__ kcnt, i64 kcap,
+                                                                     u32 *__restrict__ kover) {
   __shared__ u32 marks[kGreedyWarps][kGreedyMaxWin / 32];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const i64 w = i64(blockIdx.x) * kGreedyWarps + wl;
@@ -619,6 +621,7 @@ __global__ void __launch_bounds__(kGreedyWarps * 32) k_greedy_window(Batch b, co
     c1 = lo;
   }
   __syncwarp();
+  u32 nk = 0;
   for (i64 base = c0; base < c1; base += 32) {
     const i64 my = base + lane;
     i32 ml = 0, ms = 0;
@@ -657,12 +660,79 @@ __global__ void __launch_bounds__(kGreedyWarps * 32) k_greedy_window(Batch b, co
       __syncwarp();
     }
     if (my < c1) state[my] = ((keep_bits >> lane) & 1u) ? 1 : 2;
+    if (kwin != nullptr) {  // the window's kept candidates, in candidate order
+      if ((keep_bits >> lane) & 1u) {
+        const u32 j = nk + __popc(keep_bits & ((1u << lane) - 1u));
+        if (i64(j) < kcap) kwin[w * kcap + j] = u32(my);
+      }
+      nk += __popc(keep_bits);
+    }
+  }
+  if (kwin != nullptr && lane == 0) {
+    kcnt[w] = i64(nk) <= kcap ? nk : 0u;
+    if (i64(nk) > kcap) atomicOr(kover, 1u);  // cannot happen for non-overlapping kept repeats; scan all if it does
   }
 }
 
+struct KeptBaseF {  // exclusive scan of the per-window kept counts
+  const u32 *cnt;
+  u32 *base;
+  i64 n;
+  i64 *total;
+  __device__ u32 load(i64 i) const { return cnt[i]; }
+  __device__ bool store(i64 i, u32 incl, u32 excl) const {
+    base[i] = excl;
+    if (i == n - 1) *total = i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+__global__ void k_kept_compact(const u32 *__restrict__ kwin, const u32 *__restrict__ kcnt,
+                               const u32 *__restrict__ kbase, i64 kcap, u32 *__restrict__ klist) {
+  const i64 w = blockIdx.x;
+  const u32 n = kcnt[w], b = kbase[w];
+  for (u32 j = threadIdx.x; j < n; j += blockDim.x) klist[b + j] = kwin[w * kcap + j];
+}
+
+// K8 over the compact kept list: group counts and first kept candidate
+__global__ void k_gstats_kept(const u32 *__restrict__ klist, i64 K, const i32 *__restrict__ cg,
+                              u32 *__restrict__ gcnt, u32 *__restrict__ gfirst) {
+  const i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const u32 c = klist[k];
+  const i32 g = cg[c];
+  atomicAdd(&gcnt[g], 1u);
+  atomicMin(&gfirst[g], c);
+}
+
+// occurrence list over the kept candidates in candidate order
+struct OccKeptF {
+  const u32 *klist;
+  const i32 *cg, *cs, *gbase;
+  const u32 *gcnt;
+  u32 minc;
+  u32 *oidx;
+  i32 *occ;
+  i64 occ_cap;
+  i64 K;
+  i64 *total;
+  __device__ u32 load(i64 k) const { return gcnt[cg[klist[k]]] >= minc ? 1u : 0u; }
+  __device__ bool store(i64 k, u32 incl, u32 excl) const {
+    if (incl != excl) {
+      const u32 c = klist[k];
+      oidx[c] = excl;
+      if (occ != nullptr && i64(excl) < occ_cap) occ[excl] = cs[c] - gbase[cg[c]];  // window-local start
+    }
+    if (k == K - 1) *total = i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
 }  // namespace
 
-void plan_select(Carver &cv, const Batch &b, SelWork &w) {
+void plan_select(Carver &cv, const Batch &b, SelWork &w, int min_len) {
   const i64 N = b.N, M = N > 1 ? 2 * (N - 1) : 1;
   w.k1 = cv.take<u32>(M);
   w.k1_alt = cv.take<u32>(M);
@@ -696,6 +766,13 @@ void plan_select(Carver &cv, const Batch &b, SelWork &w) {
   w.oidx = cv.take<u32>(M);
   w.wcnt = cv.take<u32>(size_t(b.W) + 1);
   w.scal = cv.take<u64>(16);
+  if (b.maxwin <= kGreedyMaxWin && b.W >= 8) {  // the per-window greedy keeps <= maxwin / min_len per window
+    w.kcap = b.maxwin / std::max(min_len, 1) + 1;
+    w.kwin = cv.take<u32>(size_t(b.W) * size_t(w.kcap));
+    w.kcnt = cv.take<u32>(size_t(b.W) + 1);
+    w.kbase = cv.take<u32>(size_t(b.W) + 1);
+    w.klist = cv.take<u32>(size_t(b.W) * size_t(w.kcap));
+  }
 }
 
 void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa, int min_len, SelWork &w,
@@ -781,9 +858,20 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
   if (b.maxwin <= kGreedyMaxWin && b.W >= 8) {
     // many small windows: the paper's sequential marked-array greedy, one
     // warp per window, all windows at once
-    k_greedy_window<<<grid_for(b.W, kGreedyWarps), kGreedyWarps * 32, 0, s>>>(b, w.cl, w.cs, m, w.state);
+    if (w.kwin != nullptr) APO_CUDA(cudaMemsetAsync(w.scal + 4, 0, sizeof(u64), s));
+    k_greedy_window<<<grid_for(b.W, kGreedyWarps), kGreedyWarps * 32, 0, s>>>(b, w.cl, w.cs, m, w.state, w.kwin,
+                                                                               w.kcnt, w.kcap,
+                                                                               reinterpret_cast<u32 *>(w.scal + 4));
     APO_CHECK_LAUNCH();
     c.launches++;
+    if (w.kwin != nullptr) {  // compact the kept candidates (window-major, candidate order)
+      KeptBaseF f{w.kcnt, w.kbase, b.W, reinterpret_cast<i64 *>(w.scal + 3)};
+      launch_scan<false>(c, b.W, f, s);
+      k_kept_compact<<<b.W, 128, 0, s>>>(w.kwin, w.kcnt, w.kbase, w.kcap, w.klist);
+      APO_CHECK_LAUNCH();
+      c.launches++;
+      w.K = c.read_u64(w.scal + 4, s) != 0 ? -1 : i64(c.read_u64(w.scal + 3, s));
+    }
     return;
   }
   // large windows: exact round-parallel greedy
@@ -820,12 +908,22 @@ void emit_repeats(Ctx &c, const Batch &b, SelWork &w, int min_count, apo_repeat 
   if (m > 0) {
     APO_CUDA(cudaMemsetAsync(w.gcnt, 0, sizeof(u32) * G, s));
     APO_CUDA(cudaMemsetAsync(w.gfirst, 0xff, sizeof(u32) * G, s));
-    k_gstats<<<grid_for(m, T), T, 0, s>>>(w.cg, w.state, m, w.gcnt, w.gfirst);
-    APO_CHECK_LAUNCH();
-    c.launches++;
     const u32 minc = u32(min_count < 1 ? 1 : min_count);
-    OccF of{b, w.cg, w.cs, w.gbase, w.state, w.gcnt, minc, w.oidx, occ, occ_cap, m, counts + 1};
-    launch_scan<false>(c, m, of, s);
+    if (w.K >= 0) {  // the per-window greedy's compact kept list: K entries instead of m
+      if (w.K > 0) {
+        k_gstats_kept<<<grid_for(w.K, T), T, 0, s>>>(w.klist, w.K, w.cg, w.gcnt, w.gfirst);
+        APO_CHECK_LAUNCH();
+        c.launches++;
+        OccKeptF of{w.klist, w.cg, w.cs, w.gbase, w.gcnt, minc, w.oidx, occ, occ_cap, w.K, counts + 1};
+        launch_scan<false>(c, w.K, of, s);
+      }
+    } else {
+      k_gstats<<<grid_for(m, T), T, 0, s>>>(w.cg, w.state, m, w.gcnt, w.gfirst);
+      APO_CHECK_LAUNCH();
+      c.launches++;
+      OccF of{b, w.cg, w.cs, w.gbase, w.state, w.gcnt, minc, w.oidx, occ, occ_cap, m, counts + 1};
+      launch_scan<false>(c, m, of, s);
+    }
     RepF rf{b, w.gcnt, w.gfirst, w.oidx, w.glen, w.cs, w.gbase, w.gwin, minc, out, cap, w.wcnt, G, counts};
     launch_scan<false>(c, G, rf, s);
   }
