@@ -46,6 +46,10 @@ struct SAWork {
   bool ids_valid;
   char *ht_scratch;       // hash-table scratch of dense_token_ids
   u32 ht_cap;
+  i64 K = -1;             // distinct tokens (K2 hash path; -1 otherwise)
+  const u64 *dkeys = nullptr;  // their sorted values except ~0 (dk_n of them; in ht_scratch)
+  i64 dk_n = 0;
+  bool dk_max = false;    // the token ~0 occurs (id dk_n)
   // results
   i32 *sa;                // N (global positions, window-major suffix order)
   i32 *lcp;               // N (pair k = (k, k+1); 0 at the end of each window)
@@ -57,7 +61,8 @@ void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp, int nsmid);
 // K2 (hash path): dense order-preserving token ids; returns K or -1 when
 // the distinct count exceeds cap / 2.
 size_t token_ids_scratch_bytes(i64 n, u32 cap);
-i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scratch, cudaStream_t s);
+i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scratch, cudaStream_t s,
+                    const u64 **dkeys = nullptr, i64 *dk_n = nullptr, bool *dk_max = nullptr);
 // K9: per-window on-chip suffix array + LCP (windows <= 16,384 ops, not
 // generalized): one CTA per window, a level scratch per SM id.
 bool window_sa_supported(const Batch &b);

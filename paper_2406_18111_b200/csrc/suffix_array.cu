@@ -301,11 +301,14 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   // large) the 64-bit radix sort of (token, position).
   w.ids_valid = false;
   w.unit = 1;
+  w.K = -1;
+  w.dkeys = nullptr;
   i64 packK = -1;
   if (b.gen || b.W == 1 || w.rw != nullptr) {
-    const i64 K = dense_token_ids(c, tok, N, w.ids, w.ht_cap, w.ht_scratch, s);
+    const i64 K = dense_token_ids(c, tok, N, w.ids, w.ht_cap, w.ht_scratch, s, &w.dkeys, &w.dk_n, &w.dk_max);
     if (K >= 0) {
       w.ids_valid = true;
+      w.K = K;
       packK = K;
       const int bt0 = bits_for(u64(K));
       const bool will_pack = !b.gen && b.W == 1 && w.rw == nullptr && b.sort_depth == 0 && 64 / bt0 >= 2;

@@ -105,7 +105,8 @@ size_t token_ids_scratch_bytes(i64 n, u32 cap) {
 // Returns K (number of distinct tokens) or -1 if more than cap/2 distinct
 // tokens were found (ids are then undefined).  `scratch` must hold
 // token_ids_scratch_bytes(n, cap) bytes.
-i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scratch, cudaStream_t s) {
+i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scratch, cudaStream_t s,
+                    const u64 **dkeys, i64 *dk_n, bool *dk_max) {
   Carver cv(scratch);
   u64 *table = cv.take<u64>(cap);
   u32 *slot_rank = cv.take<u32>(cap + 1);
@@ -127,8 +128,14 @@ i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scra
   i64 K = nkeys;
   if (K > 1) {
     bool a = radix_sort_u64_u32(c, dk, ds, dk_alt, ds_alt, K, 0, 64, s);
-    if (a) ds = ds_alt;
+    if (a) {
+      ds = ds_alt;
+      dk = dk_alt;
+    }
   }
+  if (dkeys) *dkeys = dk;
+  if (dk_n) *dk_n = K;
+  if (dk_max) *dk_max = has_max != 0;
   if (K > 0) {
     k_slot_rank<<<grid_for(K, 256), 256, 0, s>>>(ds, K, slot_rank);
     APO_CHECK_LAUNCH();

@@ -544,6 +544,21 @@ __global__ void k_q_offsets(const u64 *__restrict__ qkey, i64 P, int S, u32 *__r
 
 constexpr int kCmpChunks = 8;  // trace tokens fetched per round trip: 8 x 32
 
+// Matcher statistics (diagnostics only; compiled out unless APO_MATCH_STATS
+// is 1): lane 0 of each searching warp adds event counts to match_stats.
+#ifndef APO_MATCH_STATS
+#define APO_MATCH_STATS 0
+#endif
+#if APO_MATCH_STATS
+__device__ unsigned long long match_stats[16];
+#define MS_ADD(i, v)                                                         \
+  do {                                                                       \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&match_stats[i], (unsigned long long)(v)); \
+  } while (0)
+#else
+#define MS_ADD(i, v)
+#endif
+
 // Warp-cooperative compare of trace t with the on-chip stream suffix at p;
 // the trace's first 64 tokens live in registers (r0 = t[lane],
 // r1 = t[32 + lane]), later tokens come from global memory.  Each 32-token
@@ -566,6 +581,7 @@ __device__ __forceinline__ int warp_cmp_smem(const u64 *__restrict__ S, i64 p, i
     const u64 x = k < 32 ? a : (k < 64 ? b : (k < L ? t[k] : 0ull));
     const bool ne = k < L && (p + k >= n || x != S[p + k]);
     const u32 m = __ballot_sync(0xffffffffu, ne);
+    MS_ADD(5, 1);
     if (m) {
       const int f = __ffs(m) - 1;
       *lcp = base + f;
@@ -574,6 +590,7 @@ __device__ __forceinline__ int warp_cmp_smem(const u64 *__restrict__ S, i64 p, i
   }
   // later tokens: kCmpChunks 32-token chunks per round trip to L2/HBM
   for (; base < L; base += 32 * kCmpChunks) {
+    MS_ADD(6, 1);
     u64 x[kCmpChunks];
 #pragma unroll
     for (int c = 0; c < kCmpChunks; ++c) {
@@ -585,6 +602,7 @@ __device__ __forceinline__ int warp_cmp_smem(const u64 *__restrict__ S, i64 p, i
       const i64 k = base + c * 32 + lane;
       const bool ne = k < L && (p + k >= n || x[c] != S[p + k]);
       const u32 m = __ballot_sync(0xffffffffu, ne);
+      MS_ADD(7, 1);
       if (m) {
         const int f = __ffs(m) - 1;
         *lcp = base + c * 32 + f;
@@ -668,7 +686,11 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
     // min over the on-chip LCP array) decides the step without comparing
     // tokens; tokens are compared only from the known lcp onwards.
     i64 lo = lo0 - 1, hi = hi0, llo = 1, lhi = -1;
+    MS_ADD(0, 1);
+    MS_ADD(1, L);
+    MS_ADD(10, hi0 - lo0);
     while (hi - lo > 1) {
+      MS_ADD(2, 1);
       const i64 mid = lo + ((hi - lo) >> 1);
       const bool real = lo >= lo0 && lhi >= 0;
       i64 st = 1;
@@ -676,6 +698,7 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
         const bool left = llo > lhi;
         const i64 a = left ? lo : mid, b = left ? mid : hi;  // lcp(S_a, S_b) = min LC[a..b-1]
         const i64 x = range_min(a, b);
+        MS_ADD(3, 1);
         if (left) {
           if (x > llo) { lo = mid; continue; }            // S_mid < t, lcp(t, S_mid) = llo
           if (x < llo) { hi = mid; lhi = x; continue; }   // t < S_mid, lcp = x
@@ -692,6 +715,8 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
       }
       i64 l;
       const int c = warp_cmp_smem(S, SA[mid], n, tt, r0, r1, L, st, &l);
+      MS_ADD(4, 1);
+      MS_ADD(11, l - st);
       if (c <= 0) {
         hi = mid;
         lhi = l;
@@ -731,6 +756,8 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
       if (stop < 0) stop = kend;
       cnt = 1 + (stop - hi);
     }
+    MS_ADD(8, cnt > 0);
+    MS_ADD(9, cnt);
     u32 nx = 0;
     if (lane == 0) {
       ilo[z] = beg + hi;
@@ -739,6 +766,251 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
       nx = atomicAdd(&s_next, 1u);
     }
     i = z0 + __shfl_sync(0xffffffffu, nx, 0);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) qtot[q] = s_tot;
+}
+
+// ---- the same matcher over dense token ids (the common path) ----
+// When the stream batch's dictionary holds at most 65,534 distinct tokens,
+// K2's order-preserving ids stand in for the 64-bit tokens:
+//  * stream token -> y = id + 1 (u16, in shared memory; y = 0 past the end),
+//  * trace token  -> 2 * (id + 1) if the token occurs in the batch, else
+//    2 * (number of batch tokens below it) + 1; 0xffffffff past the trace end.
+// Equal tokens give x == 2y, and x < 2y exactly when the token is smaller, so
+// every comparison decides as on the raw tokens (the past-the-end values sort
+// as a shorter suffix / an exhausted trace do).  Per pair the search needs
+// one 16-byte record (k_pair_meta) instead of a chain of dependent lookups,
+// the stream half of each 32-token step is one 64-B shared-memory wavefront,
+// and the CTA fits twice per SM (512 threads, ~109 KB).
+constexpr int kSMIThreads = 512;
+constexpr int kSMIWarps = kSMIThreads / 32;
+constexpr int kSMIPad = 256;    // zero entries past the stream end (a trip reads <= 256 past its start)
+constexpr int kSMICache = 128;  // leading trace ids per warp kept in shared memory
+constexpr u32 kTraceEnd = 0xffffffffu;
+
+__global__ void k_stream_id16(const u32 *__restrict__ ids, i64 n, unsigned short *__restrict__ out) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (unsigned short)(ids[i] + 1u);
+}
+
+// trace token -> comparison value against the batch dictionary dk[0..K0)
+// (sorted distinct tokens except ~0, which has id K0 when `has_max`)
+__global__ void k_trace_ids(const u64 *__restrict__ tok, i64 n, const u64 *__restrict__ dk, i64 K0, int has_max,
+                            u32 *__restrict__ out) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u64 v = tok[i];
+  if (v == ~0ull) {
+    out[i] = has_max ? u32(2 * (K0 + 1)) : u32(2 * K0 + 1);
+    return;
+  }
+  i64 lo = 0, hi = K0;
+  while (lo < hi) {
+    const i64 mid = (lo + hi) >> 1;
+    if (__ldg(&dk[mid]) < v) lo = mid + 1; else hi = mid;
+  }
+  out[i] = (lo < K0 && __ldg(&dk[lo]) == v) ? u32(2 * (lo + 1)) : u32(2 * lo + 1);
+}
+
+// per stream-sorted pair i: (lo | hi << 16) local to the stream, pair id z,
+// trace offset, trace length
+__global__ void k_pair_meta(const u64 *__restrict__ sqk, const u32 *__restrict__ sqv, i64 P,
+                            const u32 *__restrict__ pair_e, const u32 *__restrict__ ptrace,
+                            const u32 *__restrict__ e_lo, const u32 *__restrict__ e_hi, const i64 *__restrict__ off,
+                            const i64 *__restrict__ toff, uint4 *__restrict__ meta) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  const u32 z = sqv[i];
+  const u32 e = pair_e[z], t = ptrace[z];
+  const i64 beg = off[sqk[i]];
+  const i64 a = toff[t], b = toff[t + 1];
+  meta[i] = make_uint4(u32(e_lo[e] - beg) | (u32(e_hi[e] - beg) << 16), z, u32(a), u32(b - a));
+}
+
+// Warp compare of the trace (ids: Tc = the first kSMICache in shared memory,
+// tg = all in global memory) with the stream suffix at p, from token `from`
+// on (the known common prefix).  Returns -1 / 1 (t < / > suffix) or 0 (t is
+// a prefix of the suffix); *lcp = the common prefix length (capped at L).
+template <int CH>
+__device__ __forceinline__ bool ids_trip(const unsigned short *__restrict__ S, int p, const u32 *__restrict__ Tc,
+                                         const u32 *__restrict__ tg, int L, int &base, int *lcp, int *res) {
+  const int lane = threadIdx.x & 31;
+  u32 x[CH], y[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const int k = base + c * 32 + lane;
+    x[c] = k < kSMICache ? Tc[k] : (k < L ? __ldg(&tg[k]) : kTraceEnd);
+    y[c] = u32(S[p + k]) << 1;
+  }
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const u32 m = __ballot_sync(0xffffffffu, x[c] != y[c]);
+    if (m) {
+      const int f = __ffs(m) - 1;
+      const int k = base + c * 32 + f;
+      const int r = __shfl_sync(0xffffffffu, x[c] < y[c] ? -1 : 1, f);
+      *lcp = k < L ? k : L;
+      *res = k < L ? r : 0;
+      return true;
+    }
+  }
+  base += CH * 32;
+  return false;
+}
+
+__device__ __forceinline__ int warp_cmp_ids(const unsigned short *__restrict__ S, int p, const u32 *__restrict__ Tc,
+                                            const u32 *__restrict__ tg, int L, int from, int *lcp) {
+  int base = from, res = 0;
+  while (base < kSMICache) {  // the cached head: two chunks per trip
+    if (ids_trip<2>(S, p, Tc, tg, L, base, lcp, &res)) return res;
+  }
+  while (true) {  // later tokens: eight chunks per round trip to L2/HBM
+    if (ids_trip<8>(S, p, Tc, tg, L, base, lcp, &res)) return res;
+  }
+}
+
+__global__ void __launch_bounds__(kSMIThreads, 2)
+    k_stream_match_ids(const i64 *__restrict__ soff, const i32 *__restrict__ sa, const i32 *__restrict__ lcpa,
+                       const unsigned short *__restrict__ sid, const u32 *__restrict__ tid,
+                       const uint4 *__restrict__ meta, const u32 *__restrict__ qoff, i64 *__restrict__ ilo,
+                       u32 *__restrict__ icnt, u32 *__restrict__ qtot, const u32 *__restrict__ qorder) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ u32 s_tot, s_next;
+  __shared__ unsigned short s_bmin[kSMMax / 32];
+  const int q = int(qorder[blockIdx.x]);
+  const u32 z0 = qoff[q], z1 = qoff[q + 1];
+  if (z0 == z1) {
+    if (threadIdx.x == 0) qtot[q] = 0;
+    return;
+  }
+  if (threadIdx.x == 0) {
+    s_tot = 0;
+    s_next = kSMIWarps;
+  }
+  const i64 beg = soff[q];
+  const int n = int(soff[q + 1] - beg);
+  unsigned short *S = reinterpret_cast<unsigned short *>(smem);
+  unsigned short *SA = S + kSMMax + kSMIPad;
+  unsigned short *LC = SA + kSMMax;
+  u32 *Tc = reinterpret_cast<u32 *>(LC + kSMMax);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < ((n + 31) & ~31); i += kSMIThreads) {
+    u32 v = 0xffffu;
+    if (i < n) {
+      S[i] = sid[beg + i];
+      SA[i] = (unsigned short)(sa[beg + i] - beg);
+      v = u32(lcpa[beg + i]);
+      LC[i] = (unsigned short)v;
+    }
+    v = __reduce_min_sync(0xffffffffu, v);
+    if (lane == 0) s_bmin[i >> 5] = (unsigned short)v;
+  }
+  for (int i = n + threadIdx.x; i < n + kSMIPad; i += kSMIThreads) S[i] = 0;
+  __syncthreads();
+  u32 *tc = Tc + warp * kSMICache;
+  auto range_min = [&](int a, int b) -> u32 {  // lcp(S_a, S_b) = min LC[a .. b-1]
+    u32 mn = 0xffffu;
+    const int ba = (a + 31) >> 5, bb = b >> 5;
+    if (ba >= bb) {
+      for (int k = a + lane; k < b; k += 32) mn = min(mn, u32(LC[k]));
+    } else {
+      const int k1 = a + lane, k2 = (bb << 5) + lane;
+      if (k1 < (ba << 5)) mn = min(mn, u32(LC[k1]));
+      if (k2 < b) mn = min(mn, u32(LC[k2]));
+      for (int k = ba + lane; k < bb; k += 32) mn = min(mn, u32(s_bmin[k]));
+    }
+    return __reduce_min_sync(0xffffffffu, mn);
+  };
+  u32 i = z0 + warp;
+  uint4 mc = i < z1 ? meta[i] : make_uint4(0, 0, 0, 0);
+  while (i < z1) {
+    u32 nx = 0;
+    if (lane == 0) nx = atomicAdd(&s_next, 1u);
+    const u32 ni = z0 + __shfl_sync(0xffffffffu, nx, 0);
+    const uint4 mn = ni < z1 ? meta[ni] : make_uint4(0, 0, 0, 0);  // consumed next iteration
+    const u32 *tg = tid + mc.z;
+    const int L = int(mc.w);
+    const int lo0 = int(mc.x & 0xffffu), hi0 = int(mc.x >> 16);
+    {
+      u32 v[kSMICache / 32];
+#pragma unroll
+      for (int j = 0; j < kSMICache / 32; ++j) v[j] = 32 * j + lane < L ? __ldg(&tg[32 * j + lane]) : kTraceEnd;
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < kSMICache / 32; ++j) tc[32 * j + lane] = v[j];
+      __syncwarp();
+    }
+    // lower bound with LCP-LR skips, as in k_stream_match
+    int lo = lo0 - 1, hi = hi0, llo = 1, lhi = -1;
+    while (hi - lo > 1) {
+      const int mid = lo + ((hi - lo) >> 1);
+      const bool real = lo >= lo0 && lhi >= 0;
+      int st = 1;
+      if (real && llo != lhi) {
+        const bool left = llo > lhi;
+        const int a = left ? lo : mid, b = left ? mid : hi;
+        const int x = int(range_min(a, b));
+        if (left) {
+          if (x > llo) { lo = mid; continue; }
+          if (x < llo) { hi = mid; lhi = x; continue; }
+          st = llo;
+        } else {
+          if (x > lhi) { hi = mid; continue; }
+          if (x < lhi) { lo = mid; llo = x; continue; }
+          st = lhi;
+        }
+      } else if (real) {
+        st = llo;
+      } else if (lhi >= 0) {
+        st = 1;
+      }
+      int l;
+      const int c = warp_cmp_ids(S, SA[mid], tc, tg, L, st, &l);
+      if (c <= 0) {
+        hi = mid;
+        lhi = l;
+      } else {
+        lo = mid;
+        llo = l;
+      }
+    }
+    int cnt = 0;
+    if (lhi >= L) {  // extend while LC[k] >= L (k + 1 < hi0)
+      const int kend = hi0 - 1;
+      int k = hi, stop = -1;
+      {
+        const int bend = min(((k >> 5) + 1) << 5, kend);
+        const int kk = k + lane;
+        const u32 bad = __ballot_sync(0xffffffffu, kk < bend && int(LC[kk]) < L);
+        if (bad)
+          stop = k + __ffs(bad) - 1;
+        else
+          k = bend;
+      }
+      while (stop < 0 && k < kend) {
+        const int b = (k >> 5) + lane;
+        const bool cand = (b << 5) < kend && ((b << 5) + 32 > kend || int(s_bmin[b]) < L);
+        const u32 cb = __ballot_sync(0xffffffffu, cand);
+        if (!cb) {
+          k += 32 * 32;
+          continue;
+        }
+        const int fb = (k >> 5) + __ffs(cb) - 1;
+        const int kk = (fb << 5) + lane;
+        const u32 bad = __ballot_sync(0xffffffffu, kk < kend && int(LC[kk]) < L);
+        stop = bad ? (fb << 5) + __ffs(bad) - 1 : min((fb << 5) + 32, kend);
+      }
+      if (stop < 0) stop = kend;
+      cnt = 1 + (stop - hi);
+    }
+    if (lane == 0) {
+      ilo[mc.y] = beg + hi;
+      icnt[mc.y] = u32(cnt);
+      if (cnt) atomicAdd(&s_tot, u32(cnt));
+    }
+    i = ni;
+    mc = mn;
   }
   __syncthreads();
   if (threadIdx.x == 0) qtot[q] = s_tot;
@@ -1715,6 +1987,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       b.maxwin = maxs;
       GenPlan g;
       u64 *e_tok = nullptr, *e_tok_alt, *d_rs = nullptr;
+      unsigned short *sid16 = nullptr;
       u32 *e_lo = nullptr, *e_q = nullptr, *e_hi = nullptr, *e_idx, *e_idx_alt, *ea, *ecnt, *pbase;
       i64 *scal;
       // streams that fit on chip are matched in reversed form (see k_stream_emit)
@@ -1726,6 +1999,11 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       const u64 *mtok, *stok;
       const u32 *sord;
       i64 E;
+      // dense-id matcher (k_stream_match_ids): stream ids + the batch dictionary
+      const unsigned short *p_sid = nullptr;
+      const u64 *p_dk = nullptr;
+      i64 p_dkn = 0;
+      bool p_dkmax = false;
       if (pre) {
         auto plan = [&](Carver &cv) {
           ea = cv.take<u32>(T);
@@ -1750,6 +2028,10 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
         e_q = pre->e_q;
         e_hi = pre->e_hi;
         E = pre->E;
+        p_sid = pre->sid;
+        p_dk = pre->dk;
+        p_dkn = pre->dk_n;
+        p_dkmax = pre->dk_max;
       } else {
       auto plan = [&](Carver &cv) {
         plan_gen(cv, b, g, true, c.nsmid);
@@ -1761,6 +2043,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
         e_hi = cv.take<u32>(Ns);
         e_idx = cv.take<u32>(Ns);
         e_idx_alt = cv.take<u32>(Ns);
+        sid16 = rev ? cv.take<unsigned short>(Ns) : nullptr;
         ea = cv.take<u32>(T);
         ecnt = cv.take<u32>(T);
         pbase = cv.take<u32>(T);
@@ -1779,6 +2062,15 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       }
       mtok = rev ? d_rs : d_streams;
       build_sa(c, mtok, b, g.sa, true, s);
+      if (rev && g.sa.ids_valid && g.sa.K >= 1 && g.sa.K <= 65534 && g.sa.dkeys) {
+        k_stream_id16<<<grid_for(Ns, T256), T256, 0, s>>>(g.sa.ids, Ns, sid16);
+        APO_CHECK_LAUNCH();
+        c.launches++;
+        p_sid = sid16;
+        p_dk = g.sa.dkeys;
+        p_dkn = g.sa.dk_n;
+        p_dkmax = g.sa.dk_max;
+      }
       p_off = g.d_off;
       p_wid = g.d_wid;
       p_sa = g.sa.sa;
@@ -1815,6 +2107,8 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
           x.e_lo = k.take<u32>(size_t(std::max<i64>(E, 1)));
           x.e_q = k.take<u32>(size_t(std::max<i64>(E, 1)));
           x.e_hi = k.take<u32>(size_t(std::max<i64>(E, 1)));
+          x.sid = p_sid ? k.take<unsigned short>(size_t(Ns)) : nullptr;
+          x.dk = p_sid ? k.take<u64>(size_t(std::max<i64>(p_dkn, 1))) : nullptr;
         };
         carve(kd);
         x.bytes = kd.off + 256;
@@ -1834,6 +2128,12 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
         cp(x.e_lo, e_lo, sizeof(u32) * size_t(E));
         cp(x.e_q, e_q, sizeof(u32) * size_t(E));
         cp(x.e_hi, e_hi, sizeof(u32) * size_t(E));
+        if (p_sid) {
+          cp(x.sid, p_sid, sizeof(unsigned short) * size_t(Ns));
+          cp(x.dk, p_dk, sizeof(u64) * size_t(p_dkn));
+          x.dk_n = p_dkn;
+          x.dk_max = p_dkmax;
+        }
         return;
       }
       }  // index computed here (not pre)
@@ -1898,6 +2198,8 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
             full.take<u32>(P);
             full.take<u32>(P);
             full.take<u32>(size_t(nstreams));
+            const bool use_ids = p_sid != nullptr && tr->ntok < (i64(1) << 32);
+            if (use_ids) full.take<uint4>(P);
             if (full.off > c.aux.cap) {
               c.aux.reserve(full.off, s);
               Carver cb(c.aux.base);
@@ -1922,6 +2224,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
             u32 *gpar = cz.take<u32>(P), *ghi = cz.take<u32>(P), *gtr = cz.take<u32>(P), *gdep = cz.take<u32>(P);
             u32 *otr = cz.take<u32>(P);
             u32 *tbig = cz.take<u32>(size_t(nstreams));
+            uint4 *meta = use_ids ? cz.take<uint4>(P) : nullptr;
             k_pair_list<<<grid_for(T * 32, T256), T256, 0, s>>>(pbase, ea, ecnt, sord, e_q, T, pair_e, ptr, qk, qv);
             APO_CHECK_LAUNCH();
             bool aq = radix_sort_u64_u32(c, qk, qv, qk_alt, qv_alt, P, 0, bits_for(u64(nstreams - 1)), s);
@@ -1934,14 +2237,36 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
             c.launches += 2;
             const bool as = radix_sort_u64_u32(c, sk, sv, sk_alt, sv_alt, nstreams, 0, bits_for(u64(T)), s);
             const u32 *qorder = as ? sv_alt : sv;
-            const size_t smem = sizeof(u64) * kSMMax + 2 * sizeof(unsigned short) * kSMMax;
-            c.smem_optin(reinterpret_cast<const void *>(k_stream_match), smem);
-            if (c.prof) c.prof_begin(kProfMatch, 0.0, s);
-            k_stream_match<<<nstreams, kSMThreads, smem, s>>>(sm, sqv, qoff, pair_e, ptr, e_lo, e_hi, ilo, icnt,
-                                                              qtot, qorder);
-            APO_CHECK_LAUNCH();
-            if (c.prof) c.prof_end(s);
-            c.launches += 3;
+            if (use_ids) {
+              // trace tokens as comparison values against the batch dictionary
+              const size_t tid_bytes = sizeof(u32) * size_t(std::max<i64>(tr->ntok, 1));
+              u32 *tid = static_cast<u32 *>(c.pool_get(tid_bytes));
+              k_trace_ids<<<grid_for(std::max<i64>(tr->ntok, 1), T256), T256, 0, s>>>(
+                  tr->d_rtok, tr->ntok, p_dk, p_dkn, p_dkmax ? 1 : 0, tid);
+              APO_CHECK_LAUNCH();
+              k_pair_meta<<<grid_for(P, T256), T256, 0, s>>>(sqk, sqv, P, pair_e, ptr, e_lo, e_hi, p_off, tr->d_off,
+                                                             meta);
+              APO_CHECK_LAUNCH();
+              const size_t smem = sizeof(unsigned short) * (3 * size_t(kSMMax) + kSMIPad) +
+                                  sizeof(u32) * size_t(kSMIWarps) * kSMICache;
+              c.smem_optin(reinterpret_cast<const void *>(k_stream_match_ids), smem);
+              if (c.prof) c.prof_begin(kProfMatch, 0.0, s);
+              k_stream_match_ids<<<nstreams, kSMIThreads, smem, s>>>(p_off, p_sa, p_lcp, p_sid, tid, meta, qoff, ilo,
+                                                                     icnt, qtot, qorder);
+              APO_CHECK_LAUNCH();
+              if (c.prof) c.prof_end(s);
+              c.pool_put(tid, tid_bytes);  // later pool users run on this stream, after the matcher
+              c.launches += 5;
+            } else {
+              const size_t smem = sizeof(u64) * kSMMax + 2 * sizeof(unsigned short) * kSMMax;
+              c.smem_optin(reinterpret_cast<const void *>(k_stream_match), smem);
+              if (c.prof) c.prof_begin(kProfMatch, 0.0, s);
+              k_stream_match<<<nstreams, kSMThreads, smem, s>>>(sm, sqv, qoff, pair_e, ptr, e_lo, e_hi, ilo, icnt,
+                                                                qtot, qorder);
+              APO_CHECK_LAUNCH();
+              if (c.prof) c.prof_end(s);
+              c.launches += 3;
+            }
             // hits in final order straight from the per-stream emitter
             PairBaseF qf{qtot, qbase, nstreams, scal + 3};
             launch_scan<false>(c, nstreams, qf, s);
@@ -2205,3 +2530,14 @@ void apo_stream_index_destroy(apo_stream_index *idx) {
 }
 
 }  // extern "C"
+
+#if APO_MATCH_STATS
+extern "C" int apo_debug_match_stats(unsigned long long *out, int reset) {
+  if (cudaMemcpyFromSymbol(out, apo::match_stats, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(apo::match_stats, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -34,6 +34,11 @@ struct apo_stream_index {
   apo::i32 *d_wid = nullptr, *sa = nullptr, *lcp = nullptr;
   apo::u64 *rs = nullptr, *stok = nullptr;
   apo::u32 *sord = nullptr, *e_lo = nullptr, *e_q = nullptr, *e_hi = nullptr;
+  // dense-id matcher inputs (when the batch has <= 65,534 distinct tokens)
+  unsigned short *sid = nullptr;  // reversed streams' ids + 1
+  apo::u64 *dk = nullptr;         // sorted distinct tokens except ~0
+  apo::i64 dk_n = 0;
+  bool dk_max = false;
 };
 
 namespace apo {

@@ -365,3 +365,71 @@ def test_match_indexed_long_streams_and_empty_trie():
     one = ctx.trie_build_traces(torch.from_numpy(np.array([1, 2, 3], dtype=np.uint64)).cuda(),
                                 np.array([0, 3], dtype=np.int64))
     assert ctx.match_indexed(one, idx).shape[0] == ctx.match(one, ds, so).shape[0] == 0
+
+
+def test_match_dense_id_order_edges(ctx):
+    """The dense-id matcher (k_stream_match_ids): stream tokens include 0,
+    2^63 and ~0; traces diverge from stream substrings at tokens that are
+    absent from the streams and fall below, between and above the stream
+    vocabulary (their comparison values are odd), and run past stream ends.
+    Both modes against the oracle."""
+    rng = gen.Rng(91)
+    M = (1 << 64) - 1
+    alpha = np.array([0, 7, 9, 1 << 63, M - 1, M], dtype=np.uint64)
+    absent = [1, 8, 10, (1 << 63) - 1, (1 << 63) + 1, M - 2]
+    lens = [300, 1, 2, 777, 2000, 16384, 33, 1500]
+    streams = [alpha[gen.Rng(900 + q).below_np(len(alpha), n).astype(np.int64)] for q, n in enumerate(lens)]
+    traces = set()
+    for j in range(400):
+        s = streams[rng.below(len(streams))]
+        a = rng.below(len(s))
+        L = 1 + rng.below(40)
+        t = [int(x) for x in s[a:a + L]]
+        if j % 3 == 1 and len(t) > 1:  # diverge at an absent token
+            t[rng.below(len(t))] = absent[rng.below(len(absent))]
+        elif j % 3 == 2:  # run past the stream end / extend
+            t = t + [int(alpha[rng.below(len(alpha))]) for _ in range(rng.below(5))]
+        traces.add(tuple(t))
+    traces = sorted(traces, key=lambda t: (-len(t), t))
+    tt = np.array([x for t in traces for x in t], dtype=np.uint64)
+    to = np.cumsum([0] + [len(t) for t in traces]).astype(np.int64)
+    trie = ctx.trie_build_traces(dev(tt), to)
+    gt, go = trie.traces()
+    sflat = np.concatenate(streams)
+    soff = np.cumsum([0] + lens).astype(np.int64)
+    hits = ctx.match(trie, dev(sflat), soff, cap=1 << 24).cpu().numpy()
+    want, cnt = oracle.match_brute(sflat, soff, gt.cpu().numpy(), go)
+    assert cnt == len(hits) and np.array_equal(hits, want) and cnt > 0
+    rp, nall = ctx.match(trie, dev(sflat), soff, mode=1)
+    tlen = np.diff(go)
+    want_rp = oracle.replay(want, tlen)
+    g = rp.cpu().numpy().astype(np.int64)
+    got_rp = np.stack([g[:, 0], g[:, 1] - tlen[g[:, 2]] + 1, g[:, 1], g[:, 2], g[:, 3]], axis=1)
+    assert nall == cnt and np.array_equal(got_rp, want_rp)
+
+
+def test_match_large_vocabulary_raw_token_path(ctx):
+    """More than 65,534 distinct tokens in the stream batch: the matcher
+    compares raw 64-bit tokens (k_stream_match); against the oracle."""
+    lens = [15000, 16384, 14000, 12000, 16000]
+    streams = [gen.random_string(950 + q, n, 1 << 40) for q, n in enumerate(lens)]
+    assert len(np.unique(np.concatenate(streams))) > 65534
+    rng = gen.Rng(96)
+    traces = set()
+    for j in range(500):
+        s = streams[rng.below(len(streams))]
+        a = rng.below(len(s) - 60)
+        t = [int(x) for x in s[a:a + 1 + rng.below(50)]]
+        if j % 4 == 3:
+            t[-1] = int(streams[0][rng.below(100)])
+        traces.add(tuple(t))
+    traces = sorted(traces, key=lambda t: (-len(t), t))
+    tt = np.array([x for t in traces for x in t], dtype=np.uint64)
+    to = np.cumsum([0] + [len(t) for t in traces]).astype(np.int64)
+    trie = ctx.trie_build_traces(dev(tt), to)
+    gt, go = trie.traces()
+    sflat = np.concatenate(streams)
+    soff = np.cumsum([0] + lens).astype(np.int64)
+    hits = ctx.match(trie, dev(sflat), soff).cpu().numpy()
+    want, cnt = oracle.match_brute(sflat, soff, gt.cpu().numpy(), go)
+    assert cnt == len(hits) and np.array_equal(hits, want) and cnt >= 300
