@@ -46,6 +46,7 @@
 #include <algorithm>
 #include <vector>
 
+#include <cstdlib>
 #include "trie.cuh"
 
 namespace apo {
@@ -98,6 +99,12 @@ struct RP {
   struct WvMat *wv;      // per stream: its wavelet matrix (lazy scores in phase D)
   const u32 *endoff;     // per stream position: first hit record (mode 1, from the emitter)
   const unsigned short *endml;  // per stream position: shortest trace ending there (0xffff: none)
+  // phase D by ends: per decision its winner (single eligible record) or its
+  // staged candidates; the candidate pool and its fill counter
+  uint2 *dwin = nullptr;
+  struct RpCand *cand = nullptr;
+  i64 ccap = 0;
+  unsigned long long *ccnt = nullptr;
 };
 
 __device__ __forceinline__ u32 lanemask_lt_() {
@@ -701,89 +708,222 @@ __global__ void __launch_bounds__(32) k_rp_decide(RP a) {
   if (lane == 0) a.rcnt[q] = nrep;
 }
 
-// Phase D by ends (mode 1 with the emitter's per-end index): lanes test 32
-// ends at a time -- an end has an eligible record iff its shortest trace
-// starts at or after the frontier (e - minlen + 1 >= frontier) -- and the
-// first such end is decided over its whole record run (records in trace-id
-// order = length descending; the eligible ones are a suffix), scores
-// evaluated lazily as in k_rp_decide; the replay moves the frontier and the
-// scan continues after that end.
-__global__ void __launch_bounds__(32) k_rp_decide_ends(RP a) {
+// Phase D by ends (mode 1 with the emitter's per-end index).  Which ends are
+// decided does not depend on any score: an end is decided iff its shortest
+// trace starts at or after the frontier (e - minlen + 1 >= frontier), and a
+// replay at e moves the frontier to e + 1 whichever record wins.  So the
+// phase runs in three kernels:
+//  * k_rp_dec_find (warp per stream): the decision ends and the frontier each
+//    was decided under, from the shortest-length column alone (register
+//    ballots over 32 ends at a time; no record is read);
+//  * k_rp_dec_cands (all decisions in parallel): the eligible records of a
+//    decision are a suffix of its end's run (trace-id order = length
+//    descending); ~90 % of the decisions have exactly one, which wins without
+//    a score; the others get their scores evaluated (wavelet queries; scores
+//    do not depend on earlier decisions) and staged in a candidate pool;
+//  * k_rp_dec_pick (warp per stream): the winners in end order -- only the
+//    bonus depends on the slots replayed so far -- and the replay records.
+// A decision whose candidates do not fit the pool is decided by the whole
+// warp in k_rp_dec_pick (rp_decide_end, scores evaluated there).
+struct RpCand {
+  u64 sc;
+  u32 len, t, slot, pad;
+};
+constexpr u32 kDecMulti = 0x80000000u;  // dwin.x flag: (count, pool offset) follow
+constexpr u32 kDecOver = 0xffffffffu;   // dwin.x: candidates not staged
+
+// One decision at end ed (frontier fr) with the whole warp: the best
+// eligible record (score with the bonus, then length, then smaller id).
+__device__ void rp_decide_end(const RP &a, int q, i64 beg, i64 he, int n, const u32 *rep, int ed, i64 fr,
+                              u32 *bt_out, u32 *bslot_out) {
+  const int lane = threadIdx.x & 31;
+  const i64 r0 = a.endoff[beg + ed];
+  const i64 r1 = ed + 1 < n ? i64(a.endoff[beg + ed + 1]) : he;
+  bool have = false;
+  u64 bs = 0;
+  u32 bl = 0, bt = 0, bslot = 0;
+  for (i64 k0 = r0; k0 < r1; k0 += 32) {
+    const i64 k = k0 + lane;
+    const bool valid = k < r1;
+    int4 r = make_int4(-1, -1, -1, 0);
+    u32 L = 0;
+    if (valid) {
+      r = a.hits[k];
+      L = u32(__ldg(&a.tlen_off[r.z + 1]) - __ldg(&a.tlen_off[r.z]));
+    }
+    const bool ok = valid && i64(ed) - i64(L) + 1 >= fr;
+    const u32 slot = u32(r.w);
+    u64 sc = 0;
+    if (ok) {
+      sc = wv_score(a, q, r, L);
+      if ((rep[slot >> 5] >> (slot & 31)) & 1u) sc = sc * a.bonus_num / a.bonus_den;
+    }
+    const int b = warp_best(ok, sc, L, u32(r.z));
+    if (b >= 0) {
+      const u64 s1 = __shfl_sync(0xffffffffu, sc, b);
+      const u32 l1 = __shfl_sync(0xffffffffu, L, b), t1 = __shfl_sync(0xffffffffu, u32(r.z), b);
+      const u32 z1 = __shfl_sync(0xffffffffu, slot, b);
+      if (!have || beats(s1, l1, t1, bs, bl, bt)) {
+        bs = s1;
+        bl = l1;
+        bt = t1;
+        bslot = z1;
+        have = true;
+      }
+    }
+  }
+  *bt_out = bt;
+  *bslot_out = bslot;
+}
+
+constexpr int kFindWarps = 4;
+
+__global__ void __launch_bounds__(kFindWarps * 32) k_rp_dec_find(RP a) {
+  const int lane = threadIdx.x & 31;
+  const int qi = blockIdx.x * kFindWarps + (threadIdx.x >> 5);
+  if (qi >= a.nstreams) return;
+  const int q = a.order[qi];
+  const i64 hb = a.hbeg[q], he = a.hbeg[q + 1];
+  u32 nrep = 0;
+  if (hb < he) {
+    const i64 beg = a.ix_off[q];
+    const int n = int(a.ix_off[q + 1] - beg);
+    int4 *stage = a.stage + a.soff[q];
+    i64 frontier = 0;
+    u32 mln = lane < n ? u32(a.endml[beg + lane]) : 0xffffu;
+    for (int e0 = 0; e0 < n; e0 += 32) {
+      const int e = e0 + lane;
+      const u32 ml = mln;
+      mln = e + 32 < n ? u32(a.endml[beg + e + 32]) : 0xffffu;  // next window, in flight meanwhile
+      u32 dm = 0, pend = __ballot_sync(0xffffffffu, ml != 0xffffu);
+      i64 f = frontier;
+      while (pend) {
+        const u32 cm = pend & __ballot_sync(0xffffffffu, i64(e) - i64(ml) + 1 >= f);
+        if (!cm) break;
+        const int l = __ffs(cm) - 1;
+        dm |= 1u << l;
+        f = i64(e0 + l) + 1;
+        pend &= ~((2u << l) - 1u);
+      }
+      if ((dm >> lane) & 1u) {
+        const u32 below = dm & lanemask_lt_();
+        const i64 fr = below ? i64(e0 + 31 - __clz(below)) + 1 : frontier;
+        stage[nrep + __popc(below)] = make_int4(q, e, int(fr), 0);
+      }
+      nrep += __popc(dm);
+      frontier = f;
+    }
+  }
+  if (lane == 0) a.rcnt[q] = nrep;
+}
+
+constexpr int kCandThreads = 128;
+
+__global__ void __launch_bounds__(kCandThreads) k_rp_dec_cands(RP a) {
+  const int q = blockIdx.x;
+  const u32 R = a.rcnt[q];
+  if (R == 0) return;
+  const i64 he = a.hbeg[q + 1];
+  const i64 beg = a.ix_off[q];
+  const int n = int(a.ix_off[q + 1] - beg);
+  const int4 *stage = a.stage + a.soff[q];
+  uint2 *dwin = a.dwin + a.soff[q];
+  for (u32 j = threadIdx.x; j < R; j += kCandThreads) {
+    const int4 d = stage[j];
+    const int e = d.y;
+    const i64 fr = d.z;
+    const i64 r0 = a.endoff[beg + e];
+    const i64 r1 = e + 1 < n ? i64(a.endoff[beg + e + 1]) : he;
+    // the shortest record is eligible by construction; count the others
+    const int4 last = a.hits[r1 - 1];
+    u32 ne = 1;
+    for (i64 k = r1 - 2; k >= r0; --k) {
+      const int z = __ldg(&a.hits[k].z);
+      const u32 L = u32(__ldg(&a.tlen_off[z + 1]) - __ldg(&a.tlen_off[z]));
+      if (i64(e) - i64(L) + 1 < fr) break;
+      ++ne;
+    }
+    if (ne == 1) {
+      dwin[j] = make_uint2(u32(last.z), u32(last.w));
+      continue;
+    }
+    const unsigned long long o = atomicAdd(a.ccnt, (unsigned long long)ne);
+    if (i64(o + ne) > a.ccap) {
+      dwin[j] = make_uint2(kDecOver, 0u);
+      continue;
+    }
+    for (u32 i = 0; i < ne; ++i) {
+      const int4 r = a.hits[r1 - ne + i];
+      const u32 L = u32(__ldg(&a.tlen_off[r.z + 1]) - __ldg(&a.tlen_off[r.z]));
+      a.cand[o + i] = RpCand{wv_score(a, q, r, L), L, u32(r.z), u32(r.w), 0u};
+    }
+    dwin[j] = make_uint2(kDecMulti | ne, u32(o));
+  }
+}
+
+__global__ void __launch_bounds__(32) k_rp_dec_pick(RP a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   const int q = a.order[blockIdx.x], lane = threadIdx.x;
-  const i64 hb = a.hbeg[q], he = a.hbeg[q + 1];
-  if (lane == 0) a.rcnt[q] = 0;
-  if (hb == he) return;
+  const u32 R = a.rcnt[q];
+  if (R == 0) return;
   const u32 nw = (a.maxslot[q] + 31) / 32;
   u32 *rep = nw <= a.on_chip_bits ? reinterpret_cast<u32 *>(smraw) : static_cast<u32 *>(a.gstate) + a.gstate_off[q];
   for (u32 i = lane; i < nw; i += 32) rep[i] = 0u;
   __syncwarp();
+  const i64 he = a.hbeg[q + 1];
   const i64 beg = a.ix_off[q];
   const int n = int(a.ix_off[q + 1] - beg);
-  i64 frontier = 0;
-  u32 nrep = 0;
   int4 *stage = a.stage + a.soff[q];
-  for (int e0 = 0; e0 < n; e0 += 32) {
-    const int e = e0 + lane;
-    const u32 ml = e < n ? u32(a.endml[beg + e]) : 0xffffu;
-    u32 pend = __ballot_sync(0xffffffffu, e < n);
-    while (pend) {
-      const u32 cand = pend & __ballot_sync(0xffffffffu, ml != 0xffffu && i64(e) - i64(ml) + 1 >= frontier);
-      if (!cand) break;
-      const int l = __ffs(cand) - 1;
-      pend &= ~((2u << l) - 1u);
-      const int ed = e0 + l;
-      const i64 r0 = a.endoff[beg + ed];
-      const i64 r1 = ed + 1 < n ? i64(a.endoff[beg + ed + 1]) : he;
-      // the end's records, 32 at a time; keep the best eligible one
-      bool have = false;
-      u64 bs = 0;
-      u32 bl = 0, bt = 0, bslot = 0;
-      for (i64 k0 = r0; k0 < r1; k0 += 32) {
-        const i64 k = k0 + lane;
-        const bool valid = k < r1;
-        int4 r = make_int4(-1, -1, -1, 0);
-        u32 L = 0;
-        if (valid) {
-          r = a.hits[k];
-          L = u32(__ldg(&a.tlen_off[r.z + 1]) - __ldg(&a.tlen_off[r.z]));
-        }
-        const bool ok = valid && i64(ed) - i64(L) + 1 >= frontier;
-        const u32 slot = u32(r.w);
-        u64 sc = 0;
-        if (ok) {
-          sc = wv_score(a, q, r, L);
-          if ((rep[slot >> 5] >> (slot & 31)) & 1u) sc = sc * a.bonus_num / a.bonus_den;
-        }
-        const int b = warp_best(ok, sc, L, u32(r.z));
-        if (b >= 0) {
-          const u64 s1 = __shfl_sync(0xffffffffu, sc, b);
-          const u32 l1 = __shfl_sync(0xffffffffu, L, b), t1 = __shfl_sync(0xffffffffu, u32(r.z), b);
-          const u32 z1 = __shfl_sync(0xffffffffu, slot, b);
-          if (!have || beats(s1, l1, t1, bs, bl, bt)) {
-            bs = s1;
-            bl = l1;
-            bt = t1;
-            bslot = z1;
-            have = true;
+  const uint2 *dwin = a.dwin + a.soff[q];
+  for (u32 j0 = 0; j0 < R; j0 += 32) {
+    const u32 j = j0 + lane;
+    const int4 d = j < R ? stage[j] : make_int4(0, 0, 0, 0);
+    const uint2 w = j < R ? dwin[j] : make_uint2(0, 0);
+    const int m = int(min(32u, R - j0));
+    for (int l = 0; l < m; ++l) {
+      const u32 wx = __shfl_sync(0xffffffffu, w.x, l), wy = __shfl_sync(0xffffffffu, w.y, l);
+      const int e = __shfl_sync(0xffffffffu, d.y, l);
+      u32 bt = wx, bslot = wy;
+      if (wx & kDecMulti) {
+        if (wx == kDecOver) {
+          rp_decide_end(a, q, beg, he, n, rep, e, i64(__shfl_sync(0xffffffffu, d.z, l)), &bt, &bslot);
+        } else {
+          const u32 nl = wx & ~kDecMulti;
+          bool have = false;
+          u64 bs = 0;
+          u32 bl = 0;
+          for (u32 i0 = 0; i0 < nl; i0 += 32) {
+            const u32 i = i0 + lane;
+            const bool ok = i < nl;
+            const RpCand c = ok ? a.cand[wy + i] : RpCand{0, 0, 0, 0, 0};
+            u64 sc = c.sc;
+            if (ok && ((rep[c.slot >> 5] >> (c.slot & 31)) & 1u)) sc = sc * a.bonus_num / a.bonus_den;
+            const int b = warp_best(ok, sc, c.len, c.t);
+            if (b >= 0) {
+              const u64 s1 = __shfl_sync(0xffffffffu, sc, b);
+              const u32 l1 = __shfl_sync(0xffffffffu, c.len, b), t1 = __shfl_sync(0xffffffffu, c.t, b);
+              const u32 z1 = __shfl_sync(0xffffffffu, c.slot, b);
+              if (!have || beats(s1, l1, t1, bs, bl, bt)) {
+                bs = s1;
+                bl = l1;
+                bt = t1;
+                bslot = z1;
+                have = true;
+              }
+            }
           }
         }
-      }
-      if (have) {  // always: the end had an eligible record
         __syncwarp();
-        if (lane == 0) {
-          const u32 mk = 1u << (bslot & 31);
-          const u32 old = rep[bslot >> 5];
-          stage[nrep] = make_int4(q, ed, int(bt), (old & mk) ? 0 : 1);
-          rep[bslot >> 5] = old | mk;
-        }
-        __syncwarp();
-        ++nrep;
-        frontier = i64(ed) + 1;
       }
+      if (lane == 0) {
+        const u32 mk = 1u << (bslot & 31);
+        const u32 old = rep[bslot >> 5];
+        stage[j0 + l] = make_int4(q, e, int(bt), (old & mk) ? 0 : 1);
+        rep[bslot >> 5] = old | mk;
+      }
+      __syncwarp();
     }
   }
-  if (lane == 0) a.rcnt[q] = nrep;
 }
 
 struct ReplayScanF {
@@ -889,6 +1029,14 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   WvMat *wv = nullptr;
   int4 *stage;
   const size_t npart_rec = fast ? 0 : size_t(nparts) * kPart;
+  const bool by_ends = fast && ri->endoff != nullptr && ri->endml != nullptr;
+  uint2 *dwin = nullptr;
+  RpCand *cand = nullptr;
+  unsigned long long *ccnt = nullptr;
+  // candidate pool (decisions beyond it are decided by the whole warp in
+  // k_rp_dec_pick); APO_REPLAY_CCAP (tests) shrinks it to force that path
+  i64 ccap = std::min<i64>(std::max<i64>(tot, 1), std::max<i64>(i64(1) << 16, tot / 64));
+  if (const char *cc = std::getenv("APO_REPLAY_CCAP")) ccap = std::max<i64>(1, std::atoll(cc));
   auto plan = [&](Carver &cv) {
     hbeg = cv.take<i64>(size_t(nstreams) + 1);
     pbeg = cv.take<i64>(size_t(nstreams) + 1);
@@ -913,6 +1061,11 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
       sc = cv.take<u64>(size_t(nhits));
     }
     stage = cv.take<int4>(size_t(tot));
+    if (by_ends) {
+      dwin = cv.take<uint2>(size_t(tot));
+      cand = cv.take<RpCand>(size_t(ccap));
+      ccnt = cv.take<unsigned long long>(1);
+    }
   };
   Carver dry(nullptr);
   plan(dry);
@@ -931,8 +1084,12 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
        1.0 / double(prm.decay_period), u32(prm.bonus_num), u32(prm.bonus_den), nstreams, slot_bits, hbeg, pbeg,
        pstream, maxslot, run_slot, run_cnt, run_last, nruns, sc, cmax, order, nullptr, gso, 0u, 0u, soff, stage,
        rcnt, nullptr, nullptr, nullptr, nullptr, wq, wr0, wv, nullptr, nullptr};
-  const bool by_ends = fast && ri->endoff != nullptr && ri->endml != nullptr;
   const size_t psmem = sizeof(PartSmem);
+  a.dwin = dwin;
+  a.cand = cand;
+  a.ccap = ccap;
+  a.ccnt = ccnt;
+  if (by_ends) APO_CUDA(cudaMemsetAsync(ccnt, 0, sizeof(unsigned long long), s));
   if (fast) {
     APO_CUDA(cudaMemcpyAsync(wq, h_wq.data(), sizeof(int) * size_t(nitems), cudaMemcpyHostToDevice, s));
     APO_CUDA(cudaMemcpyAsync(wr0, h_wr.data(), sizeof(i64) * (size_t(nitems) + 1), cudaMemcpyHostToDevice, s));
@@ -990,10 +1147,16 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
     k_rp_scores<<<unsigned(nparts), kPartThreads, psmem, s>>>(a);
     APO_CHECK_LAUNCH();
   }
-  if (by_ends)
-    k_rp_decide_ends<<<nstreams, 32, size_t(smax_d) * 4, s>>>(a);
-  else
+  if (by_ends) {
+    k_rp_dec_find<<<(nstreams + kFindWarps - 1) / kFindWarps, kFindWarps * 32, 0, s>>>(a);
+    APO_CHECK_LAUNCH();
+    k_rp_dec_cands<<<nstreams, kCandThreads, 0, s>>>(a);
+    APO_CHECK_LAUNCH();
+    k_rp_dec_pick<<<nstreams, 32, size_t(smax_d) * 4, s>>>(a);
+    c.launches += 2;
+  } else {
     k_rp_decide<<<nstreams, 32, size_t(smax_d) * 4, s>>>(a);
+  }
   APO_CHECK_LAUNCH();
   ReplayScanF f{rcnt, rbase, nstreams, d_count};
   launch_scan<false>(c, nstreams, f, s);

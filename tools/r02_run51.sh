@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+python tools/replay_counts.py 2>&1 | tail -8
