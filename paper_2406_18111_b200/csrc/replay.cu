@@ -105,6 +105,10 @@ struct RP {
   struct RpCand *cand = nullptr;
   i64 ccap = 0;
   unsigned long long *ccnt = nullptr;
+  u32 *pend = nullptr;                 // candidates left for the wavelet queries
+  unsigned long long *pcnt = nullptr;
+  unsigned char *need_wv = nullptr;    // per stream: build its wavelet matrix
+  u32 scan_max = 0;                    // longest occurrence range scored by a scan
 };
 
 __device__ __forceinline__ u32 lanemask_lt_() {
@@ -451,6 +455,17 @@ __device__ __forceinline__ u32 wvg_rank1(const WvMat *M, int l, u32 i) {
   return v.y + __popc(v.x & ((1u << (i & 31u)) - 1u));
 }
 
+// Score before the bonus from the appearance count and the gap since the
+// previous appearance (R20-R22): len * min(count, cap) * d_k, k = gap / period.
+__device__ __forceinline__ u64 score_of(const RP &a, u32 cnt, u32 gap, u32 len) {
+  const u32 c = min(cnt, u32(a.count_cap));
+  u32 kq = u32(double(gap) * a.inv_period);
+  if (u64(kq) * u64(a.period) > u64(gap)) --kq;
+  if (u64(kq + 1u) * u64(a.period) <= u64(gap)) ++kq;
+  const u64 d = __ldg(&a.dq[kq < u32(a.ndq) ? kq : u32(a.ndq - 1)]);
+  return u64(len) * u64(c) * d;
+}
+
 // Score before the bonus of hit `rec` (trace length len) of stream q:
 // count = #{E[r] <= e in [lo, hi)}, previous end = the (count - 1)-th
 // smallest E in the range (1-based).
@@ -498,12 +513,7 @@ __device__ u64 wv_score(const RP &a, int q, int4 rec, u32 len) {
     }
     gap = e - v;
   }
-  const u32 c = min(cnt, u32(a.count_cap));
-  u32 kq = u32(double(gap) * a.inv_period);
-  if (u64(kq) * u64(a.period) > u64(gap)) --kq;
-  if (u64(kq + 1u) * u64(a.period) <= u64(gap)) ++kq;
-  const u64 d = __ldg(&a.dq[kq < u32(a.ndq) ? kq : u32(a.ndq - 1)]);
-  return u64(len) * u64(c) * d;
+  return score_of(a, cnt, gap, len);
 }
 
 // Builds every stream's matrix in shared memory (ballots + stable
@@ -517,6 +527,7 @@ __global__ void __launch_bounds__(kWvThreads) k_rp_wvbuild(RP a) {
   const int n = int(a.ix_off[q + 1] - beg);
   if (tid == 0) a.maxslot[q] = a.ix_toff[q + 1] - a.ix_toff[q];
   if (a.hbeg[q] == a.hbeg[q + 1] || n == 0) return;  // no hits: no scores needed
+  if (a.need_wv != nullptr && !a.need_wv[q]) return;  // by ends: no wavelet query in this stream
   const int L = max(1, 32 - __clz(u32(max(n - 1, 1))));
   const int nw = (n + 31) / 32;
   for (int r = tid; r < n; r += kWvThreads) S.cur[r] = (unsigned short)(n - 1 - (a.ix_sa[beg + r] - int(beg)));
@@ -727,8 +738,9 @@ __global__ void __launch_bounds__(32) k_rp_decide(RP a) {
 // warp in k_rp_dec_pick (rp_decide_end, scores evaluated there).
 struct RpCand {
   u64 sc;
-  u32 len, t, slot, pad;
+  u32 len, t, slot, q, e, pad;
 };
+constexpr u32 kScanMax = 4096;  // occurrence ranges up to this are scanned, longer ones queried (default)
 constexpr u32 kDecMulti = 0x80000000u;  // dwin.x flag: (count, pool offset) follow
 constexpr u32 kDecOver = 0xffffffffu;   // dwin.x: candidates not staged
 
@@ -850,14 +862,60 @@ __global__ void __launch_bounds__(kCandThreads) k_rp_dec_cands(RP a) {
     const unsigned long long o = atomicAdd(a.ccnt, (unsigned long long)ne);
     if (i64(o + ne) > a.ccap) {
       dwin[j] = make_uint2(kDecOver, 0u);
+      a.need_wv[q] = 1;  // decided in k_rp_dec_pick with wavelet queries
       continue;
     }
     for (u32 i = 0; i < ne; ++i) {
       const int4 r = a.hits[r1 - ne + i];
       const u32 L = u32(__ldg(&a.tlen_off[r.z + 1]) - __ldg(&a.tlen_off[r.z]));
-      a.cand[o + i] = RpCand{wv_score(a, q, r, L), L, u32(r.z), u32(r.w), 0u};
+      a.cand[o + i] = RpCand{0ull, L, u32(r.z), u32(r.w), u32(q), u32(e), 0u};
     }
     dwin[j] = make_uint2(kDecMulti | ne, u32(o));
+  }
+}
+
+// Scores of the staged candidates, a warp per candidate: count = the
+// trace's occurrences ending at or before e, previous end = the largest
+// occurrence end below e -- one pass over the trace's occurrence range in the
+// reversed stream's suffix array (ends E[r] = n - 1 - SA_rev[r]).  Ranges
+// longer than kScanMax are left to the wavelet queries (k_rp_cand_wv).
+__global__ void __launch_bounds__(256) k_rp_cand_score(RP a) {
+  const int lane = threadIdx.x & 31;
+  const i64 nc = min(i64(*a.ccnt), a.ccap);
+  for (i64 i = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < nc; i += (i64(gridDim.x) * blockDim.x) >> 5) {
+    RpCand &c = a.cand[i];
+    const int q = int(c.q);
+    const u64 kk = __ldg(&a.ix_tkey[a.ix_toff[q] + c.slot]);
+    const u32 lo = u32(kk >> 15) & 32767u, hi = 32767u - (u32(kk) & 32767u);
+    if (hi - lo > a.scan_max) {
+      if (lane == 0) {
+        a.pend[atomicAdd(a.pcnt, 1ull)] = u32(i);
+        a.need_wv[q] = 1;
+      }
+      continue;
+    }
+    const i64 beg = a.ix_off[q];
+    const int n1 = int(a.ix_off[q + 1] - beg) - 1;
+    const int e = int(c.e);
+    u32 cnt = 0;
+    int pm = -1;
+    for (u32 r = lo + lane; r < hi; r += 32) {
+      const int E = n1 - (__ldg(&a.ix_sa[beg + r]) - int(beg));
+      cnt += E <= e ? 1u : 0u;
+      if (E < e) pm = max(pm, E);
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    pm = __reduce_max_sync(0xffffffffu, pm);
+    if (lane == 0) c.sc = score_of(a, cnt, cnt >= 2 ? u32(e - pm) : 0u, c.len);
+  }
+}
+
+// The candidates with long occurrence ranges: wavelet-matrix queries.
+__global__ void k_rp_cand_wv(RP a) {
+  const i64 np = i64(*a.pcnt);
+  for (i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x; i < np; i += i64(gridDim.x) * blockDim.x) {
+    RpCand &c = a.cand[a.pend[i]];
+    c.sc = wv_score(a, int(c.q), make_int4(int(c.q), int(c.e), int(c.t), int(c.slot)), c.len);
   }
 }
 
@@ -1033,6 +1091,8 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   uint2 *dwin = nullptr;
   RpCand *cand = nullptr;
   unsigned long long *ccnt = nullptr;
+  u32 *pend = nullptr;
+  unsigned char *need_wv = nullptr;
   // candidate pool (decisions beyond it are decided by the whole warp in
   // k_rp_dec_pick); APO_REPLAY_CCAP (tests) shrinks it to force that path
   i64 ccap = std::min<i64>(std::max<i64>(tot, 1), std::max<i64>(i64(1) << 16, tot / 64));
@@ -1064,7 +1124,9 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
     if (by_ends) {
       dwin = cv.take<uint2>(size_t(tot));
       cand = cv.take<RpCand>(size_t(ccap));
-      ccnt = cv.take<unsigned long long>(1);
+      ccnt = cv.take<unsigned long long>(2);
+      pend = cv.take<u32>(size_t(ccap));
+      need_wv = cv.take<unsigned char>(size_t(nstreams));
     }
   };
   Carver dry(nullptr);
@@ -1089,7 +1151,15 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   a.cand = cand;
   a.ccap = ccap;
   a.ccnt = ccnt;
-  if (by_ends) APO_CUDA(cudaMemsetAsync(ccnt, 0, sizeof(unsigned long long), s));
+  a.pcnt = by_ends ? ccnt + 1 : nullptr;
+  a.pend = pend;
+  a.need_wv = need_wv;
+  a.scan_max = kScanMax;
+  if (const char *sm = std::getenv("APO_REPLAY_SCANMAX")) a.scan_max = u32(std::atoll(sm));  // tests
+  if (by_ends) {
+    APO_CUDA(cudaMemsetAsync(ccnt, 0, 2 * sizeof(unsigned long long), s));
+    APO_CUDA(cudaMemsetAsync(need_wv, 0, size_t(nstreams), s));
+  }
   if (fast) {
     APO_CUDA(cudaMemcpyAsync(wq, h_wq.data(), sizeof(int) * size_t(nitems), cudaMemcpyHostToDevice, s));
     APO_CUDA(cudaMemcpyAsync(wr0, h_wr.data(), sizeof(i64) * (size_t(nitems) + 1), cudaMemcpyHostToDevice, s));
@@ -1097,15 +1167,29 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
     a.ix_sa = ri->sa;
     a.ix_tkey = ri->tkey;
     a.ix_toff = ri->toff;
-    // the matrices once per stream; scores are evaluated lazily in phase D
     const size_t wsmem = sizeof(WvSmem);
     c.smem_optin(reinterpret_cast<const void *>(k_rp_wvbuild), wsmem);
-    k_rp_wvbuild<<<nstreams, kWvThreads, wsmem, s>>>(a);
-    APO_CHECK_LAUNCH();
-    if (by_ends) {  // the emitter's per-end index replaces the per-chunk latest starts
+    if (by_ends) {
+      // the emitter's per-end index: decision ends, their candidates and the
+      // candidates' scores (scans; wavelet matrices only for the streams with
+      // long occurrence ranges or pool overflows)
       a.endoff = ri->endoff;
       a.endml = ri->endml;
+      k_rp_dec_find<<<(nstreams + kFindWarps - 1) / kFindWarps, kFindWarps * 32, 0, s>>>(a);
+      APO_CHECK_LAUNCH();
+      k_rp_dec_cands<<<nstreams, kCandThreads, 0, s>>>(a);
+      APO_CHECK_LAUNCH();
+      k_rp_cand_score<<<c.num_sms * 8, 256, 0, s>>>(a);
+      APO_CHECK_LAUNCH();
+      k_rp_wvbuild<<<nstreams, kWvThreads, wsmem, s>>>(a);
+      APO_CHECK_LAUNCH();
+      k_rp_cand_wv<<<c.num_sms * 4, 256, 0, s>>>(a);
+      APO_CHECK_LAUNCH();
+      c.launches += 4;
     } else {
+      // the matrices once per stream; scores are evaluated lazily in phase D
+      k_rp_wvbuild<<<nstreams, kWvThreads, wsmem, s>>>(a);
+      APO_CHECK_LAUNCH();
       k_rp_cmax<<<unsigned(nitems), 256, 0, s>>>(a);
       APO_CHECK_LAUNCH();
       c.launches++;
@@ -1148,12 +1232,7 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
     APO_CHECK_LAUNCH();
   }
   if (by_ends) {
-    k_rp_dec_find<<<(nstreams + kFindWarps - 1) / kFindWarps, kFindWarps * 32, 0, s>>>(a);
-    APO_CHECK_LAUNCH();
-    k_rp_dec_cands<<<nstreams, kCandThreads, 0, s>>>(a);
-    APO_CHECK_LAUNCH();
     k_rp_dec_pick<<<nstreams, 32, size_t(smax_d) * 4, s>>>(a);
-    c.launches += 2;
   } else {
     k_rp_decide<<<nstreams, 32, size_t(smax_d) * 4, s>>>(a);
   }

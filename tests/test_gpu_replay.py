@@ -171,17 +171,22 @@ def test_match_mode_replay_heavy_streams(ctx):
     assert np.array_equal(as_oracle_rows(g, [len(t) for t in traces]), want)
 
 
-@pytest.mark.parametrize("ccap", ["1", "5"])
-def test_match_mode_replay_candidate_pool_overflow(ctx, ccap, monkeypatch):
-    """REPLAY by ends with a tiny candidate pool: decisions with several
+@pytest.mark.parametrize("ccap,scan_max", [("1", None), ("5", None), (None, "0"), ("7", "40")])
+def test_match_mode_replay_candidate_pool_overflow(ctx, ccap, scan_max, monkeypatch):
+    """REPLAY by ends with a tiny candidate pool (decisions with several
     eligible records that do not fit are decided by the whole warp in
-    k_rp_dec_pick; the replays equal MATCH_ALL + the general apo_replay."""
+    k_rp_dec_pick) and with short scan limits (candidates scored by wavelet
+    queries instead of occurrence-range scans): the replays equal MATCH_ALL +
+    the general apo_replay."""
     tok, off, st, so = gen.c4(seed=23, windows=24, window=4096, templates=8)
     d = dev(tok)
     rep, roff, occ = ctx.find_repeats_batched(d, off, 25)
     trie = ctx.trie_build(d, off, rep, roff, 25, 0)
     hits = ctx.match(trie, dev(st), so, full=True)
     two = ctx.replay(trie, hits, np.diff(so))
-    monkeypatch.setenv("APO_REPLAY_CCAP", ccap)
+    if ccap:
+        monkeypatch.setenv("APO_REPLAY_CCAP", ccap)
+    if scan_max:
+        monkeypatch.setenv("APO_REPLAY_SCANMAX", scan_max)
     one, nh = ctx.match(trie, dev(st), so, mode=1)
     assert nh == hits.shape[0] and torch.equal(one, two) and one.shape[0] > 0
