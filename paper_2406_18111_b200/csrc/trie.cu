@@ -794,9 +794,33 @@ __global__ void k_stream_id16(const u32 *__restrict__ ids, i64 n, unsigned short
   if (i < n) out[i] = (unsigned short)(ids[i] + 1u);
 }
 
-// trace token -> comparison value against the batch dictionary dk[0..K0)
-// (sorted distinct tokens except ~0, which has id K0 when `has_max`)
+// Open-addressing table of the batch dictionary dk[0..K0) (sorted distinct
+// tokens except ~0): key -> rank, for k_trace_ids.  `mask` + 1 slots, at most
+// half full; empty slots hold ~0 (the token ~0 is handled aside).
+__device__ __forceinline__ u32 dict_hash(u64 z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return u32(z ^ (z >> 31));
+}
+
+__global__ void k_dict_build(const u64 *__restrict__ dk, i64 K0, u64 *__restrict__ tkey, u32 *__restrict__ tval,
+                             u32 mask) {
+  const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= K0) return;
+  const u64 v = dk[r];
+  for (u32 h = dict_hash(v) & mask;; h = (h + 1) & mask) {
+    if (atomicCAS(reinterpret_cast<unsigned long long *>(&tkey[h]), ~0ull, v) == ~0ull) {
+      tval[h] = u32(r);
+      return;
+    }
+  }
+}
+
+// trace token -> comparison value against the batch dictionary: 2 (rank + 1)
+// for a token of the batch (one table probe), else 2 (tokens below it) + 1
+// (binary search over dk; tokens absent from the batch are rare)
 __global__ void k_trace_ids(const u64 *__restrict__ tok, i64 n, const u64 *__restrict__ dk, i64 K0, int has_max,
+                            const u64 *__restrict__ tkey, const u32 *__restrict__ tval, u32 mask,
                             u32 *__restrict__ out) {
   const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -804,6 +828,14 @@ __global__ void k_trace_ids(const u64 *__restrict__ tok, i64 n, const u64 *__res
   if (v == ~0ull) {
     out[i] = has_max ? u32(2 * (K0 + 1)) : u32(2 * K0 + 1);
     return;
+  }
+  for (u32 h = dict_hash(v) & mask;; h = (h + 1) & mask) {
+    const u64 k = __ldg(&tkey[h]);
+    if (k == v) {
+      out[i] = 2u * (__ldg(&tval[h]) + 1u);
+      return;
+    }
+    if (k == ~0ull) break;
   }
   i64 lo = 0, hi = K0;
   while (lo < hi) {
@@ -2241,8 +2273,19 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
               // trace tokens as comparison values against the batch dictionary
               const size_t tid_bytes = sizeof(u32) * size_t(std::max<i64>(tr->ntok, 1));
               u32 *tid = static_cast<u32 *>(c.pool_get(tid_bytes));
+              u32 tslots = 1024;
+              while (i64(tslots) < 2 * p_dkn) tslots <<= 1;
+              const size_t dict_bytes = (sizeof(u64) + sizeof(u32)) * size_t(tslots) + 256;
+              char *dict = static_cast<char *>(c.pool_get(dict_bytes));
+              u64 *tkey = reinterpret_cast<u64 *>(dict);
+              u32 *tval = reinterpret_cast<u32 *>(tkey + tslots);
+              APO_CUDA(cudaMemsetAsync(tkey, 0xff, sizeof(u64) * tslots, s));
+              if (p_dkn > 0) {
+                k_dict_build<<<grid_for(p_dkn, T256), T256, 0, s>>>(p_dk, p_dkn, tkey, tval, tslots - 1);
+                APO_CHECK_LAUNCH();
+              }
               k_trace_ids<<<grid_for(std::max<i64>(tr->ntok, 1), T256), T256, 0, s>>>(
-                  tr->d_rtok, tr->ntok, p_dk, p_dkn, p_dkmax ? 1 : 0, tid);
+                  tr->d_rtok, tr->ntok, p_dk, p_dkn, p_dkmax ? 1 : 0, tkey, tval, tslots - 1, tid);
               APO_CHECK_LAUNCH();
               k_pair_meta<<<grid_for(P, T256), T256, 0, s>>>(sqk, sqv, P, pair_e, ptr, e_lo, e_hi, p_off, tr->d_off,
                                                              meta);
@@ -2256,6 +2299,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
               APO_CHECK_LAUNCH();
               if (c.prof) c.prof_end(s);
               c.pool_put(tid, tid_bytes);  // later pool users run on this stream, after the matcher
+              c.pool_put(dict, dict_bytes);
               c.launches += 5;
             } else {
               const size_t smem = sizeof(u64) * kSMMax + 2 * sizeof(unsigned short) * kSMMax;
