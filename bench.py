@@ -9,7 +9,12 @@ One step = one pass of the whole hot path over
 one batch, inputs resident in HBM: apo_find_repeats_batched over every window
 (SA, LCP, candidates, ordering, greedy selection, dedup/output), the
 candidate trace set (apo_trie_build), and MATCH_ALL matching of every
-window's next 16,384 ops (apo_match).  Multi-GPU (torchrun, one process per
+window's next 16,384 ops with REPLAY selection over the completions
+(apo_match mode 1: every trace's occurrence interval in the reversed stream's
+suffix array, the interval forest, per end its deepest matched interval --
+the end's completions are that interval's chain of parents -- and the
+replay decisions, which walk the chains of the ends they decide; the
+MATCH_ALL count is returned, the 474 M records are not written out).  Multi-GPU (torchrun, one process per
 GPU): every rank analyses its own C4-shaped batch (weak scaling); the only
 exchange is the union of the candidate trace lists: each rank stages its list
 in a symmetric (NVLink-mapped) buffer and apo_trie_build_traces_multi pulls
@@ -503,8 +508,8 @@ def main():
             r, o = (int(x) for x in c.tolist())
             # the step's result read back: the analysis output (repeats, their
             # per-window offsets, occurrence lists) and the replay decisions;
-            # the MATCH_ALL records (~7.6 GB for C4) are consumed on the
-            # device by the REPLAY selection
+            # MATCH_ALL stays implicit on the device (per-end chains of the
+            # interval forest) and is consumed there by the REPLAY selection
             # (ctx.match already read the 16-byte {replays, hits} count back)
             return to_host(bufs[0][:r], bufs[1], bufs[2][:o], h)
 

@@ -109,12 +109,23 @@ struct RP {
   unsigned long long *pcnt = nullptr;
   unsigned char *need_wv = nullptr;    // per stream: build its wavelet matrix
   u32 scan_max = 0;                    // longest occurrence range scored by a scan
+  // lazy MATCH_ALL (ReplayIndex::lazy): endoff = 1 + deepest interval per
+  // end; an end's records are its chain of parents (ids local to ix_toff[q])
+  bool lazy = false;
+  const u32 *opar = nullptr, *otr = nullptr, *odep = nullptr;
 };
 
 __device__ __forceinline__ u32 lanemask_lt_() {
   u32 m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
+}
+
+// Per stream: its hit range from the matcher's per-stream hit bases (lazy
+// MATCH_ALL: no records to search).
+__global__ void k_replay_ranges_q(const u32 *__restrict__ qbase, i64 nhits, int nstreams, i64 *__restrict__ hbeg) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q <= nstreams) hbeg[q] = q < nstreams ? i64(qbase[q]) : nhits;
 }
 
 // Per stream: its hit range (hits sorted by stream).
@@ -743,12 +754,55 @@ struct RpCand {
 constexpr u32 kScanMax = 4096;  // occurrence ranges up to this are scanned, longer ones queried (default)
 constexpr u32 kDecMulti = 0x80000000u;  // dwin.x flag: (count, pool offset) follow
 constexpr u32 kDecOver = 0xffffffffu;   // dwin.x: candidates not staged
+constexpr u32 kNoParR = 0xffffffffu;    // no parent (the matcher's kNoPar)
 
 // One decision at end ed (frontier fr) with the whole warp: the best
 // eligible record (score with the bonus, then length, then smaller id).
 __device__ void rp_decide_end(const RP &a, int q, i64 beg, i64 he, int n, const u32 *rep, int ed, i64 fr,
                               u32 *bt_out, u32 *bslot_out) {
   const int lane = threadIdx.x & 31;
+  if (a.lazy) {  // the end's chain, 32 links at a time (lane i takes the i-th)
+    const u32 a0 = a.ix_toff[q];
+    u32 z = a.endoff[beg + ed] - 1u;
+    bool have = false;
+    u64 bs = 0;
+    u32 bl = 0, bt = 0, bslot = 0;
+    while (z != kNoParR) {
+      u32 mine = kNoParR;
+      for (int i = 0; i < 32 && z != kNoParR; ++i) {
+        if (lane == i) mine = z;
+        z = __ldg(&a.opar[a0 + z]);
+      }
+      const bool valid = mine != kNoParR;
+      u32 L = 0, t = 0;
+      if (valid) {
+        t = __ldg(&a.otr[a0 + mine]);
+        L = u32(__ldg(&a.tlen_off[t + 1]) - __ldg(&a.tlen_off[t]));
+      }
+      const bool ok = valid && i64(ed) - i64(L) + 1 >= fr;
+      u64 sc = 0;
+      if (ok) {
+        sc = wv_score(a, q, make_int4(q, ed, int(t), int(mine)), L);
+        if ((rep[mine >> 5] >> (mine & 31)) & 1u) sc = sc * a.bonus_num / a.bonus_den;
+      }
+      const int b = warp_best(ok, sc, L, t);
+      if (b >= 0) {
+        const u64 s1 = __shfl_sync(0xffffffffu, sc, b);
+        const u32 l1 = __shfl_sync(0xffffffffu, L, b), t1 = __shfl_sync(0xffffffffu, t, b);
+        const u32 z1 = __shfl_sync(0xffffffffu, mine, b);
+        if (!have || beats(s1, l1, t1, bs, bl, bt)) {
+          bs = s1;
+          bl = l1;
+          bt = t1;
+          bslot = z1;
+          have = true;
+        }
+      }
+    }
+    *bt_out = bt;
+    *bslot_out = bslot;
+    return;
+  }
   const i64 r0 = a.endoff[beg + ed];
   const i64 r1 = ed + 1 < n ? i64(a.endoff[beg + ed + 1]) : he;
   bool have = false;
@@ -844,6 +898,39 @@ __global__ void __launch_bounds__(kCandThreads) k_rp_dec_cands(RP a) {
     const int4 d = stage[j];
     const int e = d.y;
     const i64 fr = d.z;
+    if (a.lazy) {
+      // the chain from the deepest interval outwards is length-descending:
+      // skip its ineligible head, the rest (odep links) is eligible
+      const u32 a0 = a.ix_toff[q];
+      u32 z = a.endoff[beg + e] - 1u, t = __ldg(&a.otr[a0 + z]);
+      u32 L = u32(__ldg(&a.tlen_off[t + 1]) - __ldg(&a.tlen_off[t]));
+      while (i64(e) - i64(L) + 1 < fr) {
+        z = __ldg(&a.opar[a0 + z]);
+        t = __ldg(&a.otr[a0 + z]);
+        L = u32(__ldg(&a.tlen_off[t + 1]) - __ldg(&a.tlen_off[t]));
+      }
+      const u32 ne = __ldg(&a.odep[a0 + z]);
+      if (ne == 1) {
+        dwin[j] = make_uint2(t, z);
+        continue;
+      }
+      const unsigned long long o = atomicAdd(a.ccnt, (unsigned long long)ne);
+      if (i64(o + ne) > a.ccap) {
+        dwin[j] = make_uint2(kDecOver, 0u);
+        a.need_wv[q] = 1;
+        continue;
+      }
+      for (u32 i = 0; i < ne; ++i) {
+        a.cand[o + i] = RpCand{0ull, L, t, z, u32(q), u32(e), 0u};
+        if (i + 1 < ne) {
+          z = __ldg(&a.opar[a0 + z]);
+          t = __ldg(&a.otr[a0 + z]);
+          L = u32(__ldg(&a.tlen_off[t + 1]) - __ldg(&a.tlen_off[t]));
+        }
+      }
+      dwin[j] = make_uint2(kDecMulti | ne, u32(o));
+      continue;
+    }
     const i64 r0 = a.endoff[beg + e];
     const i64 r1 = e + 1 < n ? i64(a.endoff[beg + e + 1]) : he;
     // the shortest record is eligible by construction; count the others
@@ -1041,8 +1128,11 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   // stream ranges (device binary searches), then the part plan on the host
   const size_t hb_bytes = sizeof(i64) * (size_t(nstreams) + 1);
   i64 *hbeg0 = static_cast<i64 *>(c.pool_get(hb_bytes));
-  k_replay_ranges<<<grid_for(i64(nstreams) + 1, 256), 256, 0, s>>>(reinterpret_cast<const int4 *>(d_hits), nhits,
-                                                                  nstreams, hbeg0);
+  if (fast && ri->lazy)
+    k_replay_ranges_q<<<grid_for(i64(nstreams) + 1, 256), 256, 0, s>>>(ri->qbase, nhits, nstreams, hbeg0);
+  else
+    k_replay_ranges<<<grid_for(i64(nstreams) + 1, 256), 256, 0, s>>>(reinterpret_cast<const int4 *>(d_hits), nhits,
+                                                                    nstreams, hbeg0);
   APO_CHECK_LAUNCH();
   c.launches++;
   std::vector<i64> h_hb(size_t(nstreams) + 1);
@@ -1167,6 +1257,10 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
     a.ix_sa = ri->sa;
     a.ix_tkey = ri->tkey;
     a.ix_toff = ri->toff;
+    a.lazy = ri->lazy;
+    a.opar = ri->opar;
+    a.otr = ri->otr;
+    a.odep = ri->odep;
     const size_t wsmem = sizeof(WvSmem);
     c.smem_optin(reinterpret_cast<const void *>(k_rp_wvbuild), wsmem);
     if (by_ends) {

@@ -1151,7 +1151,7 @@ __global__ void __launch_bounds__(32) k_tree_sweep(const u64 *__restrict__ key, 
                                                    const u32 *__restrict__ toff, const u32 *__restrict__ gtr,
                                                    u32 *__restrict__ opar, u32 *__restrict__ ohi,
                                                    u32 *__restrict__ odep, u32 *__restrict__ otr,
-                                                   const u32 *__restrict__ only) {
+                                                   u32 *__restrict__ oroot, const u32 *__restrict__ only) {
   __shared__ u64 s_key[kTreeChunk];
   __shared__ u32 s_idx[kTreeDepth], s_hi[kTreeDepth];
   const int q = blockIdx.x, lane = threadIdx.x;
@@ -1186,6 +1186,7 @@ __global__ void __launch_bounds__(32) k_tree_sweep(const u64 *__restrict__ key, 
         opar[a + id] = cur;
         ohi[a + id] = hi;
         odep[a + id] = cur != kNoPar ? depth + 2 : 1;
+        oroot[a + id] = cur != kNoPar ? oroot[a + cur] : id;
         if (cur != kNoPar) {  // push the open interval below the new one
           s_idx[depth % kTreeDepth] = cur;
           s_hi[depth % kTreeDepth] = curhi;
@@ -1216,7 +1217,7 @@ __global__ void __launch_bounds__(32) k_tree_par(const u64 *__restrict__ key, co
                                                  const u32 *__restrict__ toff, const u32 *__restrict__ gtr,
                                                  u32 *__restrict__ opar, u32 *__restrict__ ohi,
                                                  u32 *__restrict__ odep, u32 *__restrict__ otr,
-                                                 u32 *__restrict__ big) {
+                                                 u32 *__restrict__ oroot, u32 *__restrict__ big) {
   __shared__ u32 s_id[kParDepth + 1];
   __shared__ unsigned short s_hi[kParDepth + 1];
   const int q = blockIdx.x, lane = threadIdx.x;
@@ -1256,10 +1257,25 @@ __global__ void __launch_bounds__(32) k_tree_par(const u64 *__restrict__ key, co
       }
     }
     const u32 depth = acc;
+    // root (the depth-1 ancestor): the stack bottom, or itself, for an
+    // interval whose parent precedes the chunk; else its in-chunk parent's
+    u32 rt = P >= 0 ? 0u : (pid == kNoPar ? k - a : s_id[1]);
+    int rp = P;
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+      const int src = rp >= 0 ? rp : lane;
+      const u32 prt = __shfl_sync(0xffffffffu, rt, src);
+      const int prp = __shfl_sync(0xffffffffu, rp, src);
+      if (rp >= 0) {
+        if (prp < 0) rt = prt;
+        rp = prp;
+      }
+    }
     if (v) {
       opar[k] = P >= 0 ? c0 + u32(P) - a : pid;
       ohi[k] = hi;
       odep[k] = depth;
+      oroot[k] = rt;
       otr[k] = gtr[val[k]];
       if (depth > kParDepth) deep_stream = true;
     }
@@ -1397,6 +1413,71 @@ __global__ void __launch_bounds__(kEmitThreads, 1) k_stream_emit(StreamMatch m, 
     }
   }
   if (have) reinterpret_cast<int4 *>(out)[hpos] = held;
+}
+
+// MATCH_ALL kept implicit for REPLAY (apo_match mode 1): the hits ending at e
+// are the chain of intervals from the deepest one containing rank
+// RISA[n-1-e] out to its root (trace-id order), so instead of writing every
+// record this stores, per end, 1 + that deepest interval (0: no hit) and the
+// length of the chain's root trace (the end's shortest; 0xffff: none).
+// REPLAY walks the chains of the ends it decides (~0.3 % of the hits).
+constexpr int kEndsThreads = 1024;
+
+__global__ void __launch_bounds__(kEndsThreads, 2) k_stream_ends(StreamMatch m, const u64 *__restrict__ tkey,
+                                                                 const u32 *__restrict__ toff,
+                                                                 const u32 *__restrict__ otr,
+                                                                 const u32 *__restrict__ oroot,
+                                                                 u32 *__restrict__ deepz,
+                                                                 unsigned short *__restrict__ endml) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int q = blockIdx.x;
+  const i64 beg = m.off[q], n = m.off[q + 1] - beg;
+  const i64 a = toff[q], M = i64(toff[q + 1]) - a;
+  if (M == 0) {
+    for (i64 e = threadIdx.x; e < n; e += kEndsThreads) {
+      deepz[beg + e] = 0u;
+      endml[beg + e] = 0xffffu;
+    }
+    return;
+  }
+  u32 *deep = reinterpret_cast<u32 *>(smem);                                  // [kSMMax]
+  unsigned short *RISA = reinterpret_cast<unsigned short *>(deep + kSMMax);  // [kSMMax]
+  for (i64 r = threadIdx.x; r < n; r += kEndsThreads) {
+    deep[r] = 0;
+    RISA[m.sa[beg + r] - beg] = (unsigned short)r;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // deepest interval per rank (largest preorder id containing it), as in k_stream_emit
+  for (i64 kb = i64(warp) * 32; kb < M; kb += i64(kEndsThreads)) {
+    const i64 k = kb + lane;
+    u32 lo = 0, hi = 0;
+    if (k < M) {
+      const u64 kk = tkey[a + k];
+      lo = u32(kk >> 15) & 32767u;
+      hi = 32767u - (u32(kk) & 32767u);
+    }
+    u32 live = __ballot_sync(0xffffffffu, hi > lo);
+    while (live) {
+      const int src = __ffs(live) - 1;
+      live &= live - 1;
+      const u32 l0 = __shfl_sync(0xffffffffu, lo, src), h0 = __shfl_sync(0xffffffffu, hi, src);
+      const u32 id1 = u32(kb + src) + 1u;
+      for (u32 r = l0 + lane; r < h0; r += 32)
+        if (deep[r] < id1) atomicMax(&deep[r], id1);
+    }
+  }
+  __syncthreads();
+  for (i64 e = threadIdx.x; e < n; e += kEndsThreads) {
+    const u32 d1 = deep[RISA[n - 1 - e]];
+    u32 ml = 0xffffu;
+    if (d1) {
+      const u32 t = otr[a + oroot[a + d1 - 1]];
+      ml = u32(min(i64(0xfffe), m.toff[t + 1] - m.toff[t]));
+    }
+    deepz[beg + e] = d1;
+    endml[beg + e] = (unsigned short)ml;
+  }
 }
 
 // warp per pair: its hits are the contiguous SA range [ilo, ilo + cnt) of
@@ -2230,6 +2311,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
             full.take<u32>(P);
             full.take<u32>(P);
             full.take<u32>(size_t(nstreams));
+            full.take<u32>(P);
             const bool use_ids = p_sid != nullptr && tr->ntok < (i64(1) << 32);
             if (use_ids) full.take<uint4>(P);
             if (full.off > c.aux.cap) {
@@ -2254,6 +2336,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
             u32 *tv = cz.take<u32>(P), *tv_alt = cz.take<u32>(P);
             u32 *tof = cz.take<u32>(size_t(nstreams) + 1);
             u32 *gpar = cz.take<u32>(P), *ghi = cz.take<u32>(P), *gtr = cz.take<u32>(P), *gdep = cz.take<u32>(P);
+            u32 *groot = cz.take<u32>(P);
             u32 *otr = cz.take<u32>(P);
             u32 *tbig = cz.take<u32>(size_t(nstreams));
             uint4 *meta = use_ids ? cz.take<uint4>(P) : nullptr;
@@ -2316,7 +2399,10 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
             launch_scan<false>(c, nstreams, qf, s);
             nh = i64(c.read_u64(reinterpret_cast<const u64 *>(scal + 3), s));
             emitted = true;
-            if (nh > 0 && cap > 0) {
+            // REPLAY (mode 1) keeps MATCH_ALL implicit (k_stream_ends) unless
+            // APO_REPLAY_EAGER is set (tests: the emitted-records path)
+            const bool lazy = ri && rev && Ns < (i64(1) << 32) && std::getenv("APO_REPLAY_EAGER") == nullptr;
+            if (nh > 0 && (cap > 0 || lazy)) {
               // interval forest of every stream (preorder sort + stack sweep)
               k_tree_keys<<<grid_for(P, T256), T256, 0, s>>>(sqk, sqv, ilo, icnt, p_off, ptr, P, bS, tk, tv, gtr);
               APO_CHECK_LAUNCH();
@@ -2329,12 +2415,36 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
               static const bool tree_seq = std::getenv("APO_TREE_SEQ") != nullptr;
               APO_CUDA(cudaMemsetAsync(tbig, tree_seq ? 0xff : 0, sizeof(u32) * size_t(nstreams), s));
               if (!tree_seq) {
-                k_tree_par<<<nstreams, 32, 0, s>>>(stk, stv, tof, gtr, gpar, ghi, gdep, otr, tbig);
+                k_tree_par<<<nstreams, 32, 0, s>>>(stk, stv, tof, gtr, gpar, ghi, gdep, otr, groot, tbig);
                 APO_CHECK_LAUNCH();
               }
-              k_tree_sweep<<<nstreams, 32, 0, s>>>(stk, stv, tof, gtr, gpar, ghi, gdep, otr, tbig);
+              k_tree_sweep<<<nstreams, 32, 0, s>>>(stk, stv, tof, gtr, gpar, ghi, gdep, otr, groot, tbig);
               APO_CHECK_LAUNCH();
               c.launches++;
+              if (lazy) {
+                ri->endoff_bytes = sizeof(u32) * size_t(Ns);
+                ri->endml_bytes = sizeof(unsigned short) * size_t(Ns);
+                u32 *deepz = static_cast<u32 *>(c.pool_get(ri->endoff_bytes));
+                unsigned short *endml = static_cast<unsigned short *>(c.pool_get(ri->endml_bytes));
+                const size_t nsmem = (sizeof(u32) + sizeof(unsigned short)) * size_t(kSMMax);
+                c.smem_optin(reinterpret_cast<const void *>(k_stream_ends), nsmem);
+                k_stream_ends<<<nstreams, kEndsThreads, nsmem, s>>>(sm, stk, tof, otr, groot, deepz, endml);
+                APO_CHECK_LAUNCH();
+                ri->ok = true;
+                ri->lazy = true;
+                ri->off = p_off;
+                ri->sa = p_sa;
+                ri->tkey = stk;
+                ri->toff = tof;
+                ri->nint = P;
+                ri->endoff = deepz;
+                ri->endml = endml;
+                ri->opar = gpar;
+                ri->otr = otr;
+                ri->odep = gdep;
+                ri->qbase = qbase;
+                c.launches += 4;
+              } else {
               const size_t esmem = sizeof(u32) * (kSMMax + 3 * kEmitPairs) + sizeof(unsigned short) * kSMMax;
               c.smem_optin(reinterpret_cast<const void *>(k_stream_emit), esmem);
               const bool pair32 = (reinterpret_cast<uintptr_t>(d_out) & 31) == 0;
@@ -2360,6 +2470,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
                 ri->endml = endml;
               }
               c.launches += 4;
+              }
             }
           } else {
             const i64 chunks = (P + kPairChunk - 1) / kPairChunk;
@@ -2506,7 +2617,7 @@ void match_entry(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const in
     match_all(c, tr, d_streams, h_off, nstreams, static_cast<apo_match_rec *>(c.hitbuf),
               i64(c.hitbuf_cap / sizeof(apo_match_rec)), d_count, s, &ri, nullptr, pre);
     nh = i64(c.read_u64(reinterpret_cast<const u64 *>(d_count), s));
-    if (size_t(nh) * sizeof(apo_match_rec) <= c.hitbuf_cap) break;
+    if ((ri.ok && ri.lazy) || size_t(nh) * sizeof(apo_match_rec) <= c.hitbuf_cap) break;
     if (c.hitbuf) c.pool_put(c.hitbuf, c.hitbuf_cap);
     c.hitbuf_cap = (size_t(nh) + size_t(nh) / 16 + 1024) * sizeof(apo_match_rec);
     c.hitbuf = c.pool_get(c.hitbuf_cap);

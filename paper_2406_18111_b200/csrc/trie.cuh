@@ -59,6 +59,13 @@ struct ReplayIndex {
   u32 *endoff = nullptr;
   unsigned short *endml = nullptr;
   size_t endoff_bytes = 0, endml_bytes = 0;
+  // lazy (MATCH_ALL not written): endoff holds, per end, 1 + the deepest
+  // interval containing its rank (0: no hit); an end's hits are the chain of
+  // parents from there (interval ids local to the stream, base toff[q]):
+  // opar = parent (kNoPar at a root), otr = trace id, odep = chain length;
+  // qbase = per stream, its first hit in MATCH_ALL order
+  bool lazy = false;
+  const u32 *opar = nullptr, *otr = nullptr, *odep = nullptr, *qbase = nullptr;
 };
 // REPLAY selection over MATCH_ALL hits (replay.cu); synchronises s.  With
 // ri->ok the trace states come from the matcher's index (no per-part

@@ -190,3 +190,21 @@ def test_match_mode_replay_candidate_pool_overflow(ctx, ccap, scan_max, monkeypa
         monkeypatch.setenv("APO_REPLAY_SCANMAX", scan_max)
     one, nh = ctx.match(trie, dev(st), so, mode=1)
     assert nh == hits.shape[0] and torch.equal(one, two) and one.shape[0] > 0
+
+
+@pytest.mark.parametrize("ccap", [None, "3"])
+def test_match_mode_replay_eager_equals_lazy(ctx, ccap, monkeypatch):
+    """apo_match mode 1 keeps MATCH_ALL implicit (per end the deepest matched
+    interval; decisions walk their chains); APO_REPLAY_EAGER=1 writes every
+    hit record and REPLAY reads the records instead.  Both give the same
+    replays and hit count, also with a tiny candidate pool."""
+    tok, off, st, so = gen.c4(seed=27, windows=32, window=4096, templates=8)
+    d = dev(tok)
+    rep, roff, occ = ctx.find_repeats_batched(d, off, 25)
+    trie = ctx.trie_build(d, off, rep, roff, 25, 0)
+    if ccap:
+        monkeypatch.setenv("APO_REPLAY_CCAP", ccap)
+    lazy, nl = ctx.match(trie, dev(st), so, mode=1)
+    monkeypatch.setenv("APO_REPLAY_EAGER", "1")
+    eager, ne = ctx.match(trie, dev(st), so, mode=1)
+    assert nl == ne and torch.equal(lazy, eager) and lazy.shape[0] > 0
