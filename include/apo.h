@@ -286,9 +286,13 @@ apo_status apo_trie_copy(const apo_trie *trie, uint64_t *d_tokens, int64_t *h_of
  *    16-byte aligned; 32-byte alignment lets the library store consecutive
  *    records in pairs); d_count: device int64[1] <- number of hits; at most
  *    cap records are stored.
- *  mode 1 = REPLAY: MATCH_ALL into library workspace, then apo_replay with
- *    default parameters; d_out receives apo_replay_rec[cap] (cast), d_count:
- *    device int64[2] <- {replays, MATCH_ALL hits}.
+ *  mode 1 = REPLAY: MATCH_ALL, then apo_replay with default parameters;
+ *    d_out receives apo_replay_rec[cap] (cast), d_count: device int64[2] <-
+ *    {replays, MATCH_ALL hits}.  On the on-chip path (streams <= 16,384 ops)
+ *    the hits stay implicit in library workspace -- per end the deepest
+ *    matched interval of the interval forest; the end's hits are its chain
+ *    of parents -- and the selection walks the chains of the ends it
+ *    decides; otherwise the records are written to library workspace.
  * Other modes: APO_ERR_INVALID.  Synchronises `stream`. */
 apo_status apo_match(apo_ctx *ctx, const apo_trie *trie, const uint64_t *d_streams,
                      const int64_t *h_off, int32_t nstreams, int32_t mode, apo_match_rec *d_out,
