@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libapo.so")
-SOURCES = ["radix_sort.cu", "token_ids.cu", "suffix_array.cu", "select.cu", "window_sa.cu", "history.cu", "trie.cu", "replay.cu", "dsa.cu", "apo.cu"]
+SOURCES = ["radix_sort.cu", "token_ids.cu", "suffix_array.cu", "select.cu", "window_select.cu", "window_sa.cu", "history.cu", "trie.cu", "replay.cu", "dsa.cu", "apo.cu"]
 HEADERS = ["common.cuh", "pipeline.cuh", "trie.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

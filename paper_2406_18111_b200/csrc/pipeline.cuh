@@ -100,6 +100,10 @@ struct SelWork {
 };
 
 void plan_select(Carver &cv, const Batch &b, SelWork &w, int min_len);
+// K5 + K6 fused per window (window_select.cu): true when it produced the
+// candidates (false: a group too large for it; run the global path).
+bool window_select_supported(const Batch &b, int min_len);
+bool window_select(Ctx &c, const Batch &b, const SAWork &sa, int min_len, SelWork &w, cudaStream_t s);
 // Runs K5..K7 (candidates, ordering, greedy).  After return, w.m and w.G are
 // valid and w.cl/cs/cg/state hold the candidates in the paper's order.
 void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa, int min_len,

@@ -29,6 +29,8 @@
 //    candidates with the marked array as a shared-memory bitset
 //    (k_greedy_window), every window at once.
 // K8 dedup/output (R10, R11).
+#include <cstdlib>
+
 #include "pipeline.cuh"
 
 namespace apo {
@@ -791,12 +793,19 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
   u32 *undecided = reinterpret_cast<u32 *>(w.scal + 2);
   APO_CUDA(cudaMemsetAsync(w.scal, 0, sizeof(u64) * 16, s));
 
+  // ---- K5 + K6 per window on chip (batches of small windows) ----
+  const bool no_fused = std::getenv("APO_SELECT_GLOBAL") != nullptr;  // tests: the global path
+  i64 m = 0;
+  if (!no_fused && window_select_supported(b, min_len) && window_select(c, b, sa, min_len, w, s)) {
+    m = w.m;
+    if (m == 0) return;
+  } else {
   // ---- K5 ----
   {
     CandF f{b, sa.sa, sa.lcp, min_len, bl, maxl, N - 1, w.k1, w.v1, m_dev};
     launch_scan<false>(c, N - 1, f, s);
   }
-  const i64 m = i64(c.read_u64(reinterpret_cast<u64 *>(m_dev), s));
+  m = i64(c.read_u64(reinterpret_cast<u64 *>(m_dev), s));
   w.m = m;
   if (m == 0) return;
 
@@ -852,6 +861,7 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
     k_unpack<<<grid_for(m, T), T, 0, s>>>(k2, m, bL, w.glen, w.gbase, w.cl, w.cs, w.cg, w.state);
     APO_CHECK_LAUNCH();
     c.launches++;
+  }
   }
 
   // ---- K7 ----

@@ -316,3 +316,37 @@ def test_batch_window_size_boundary(ctx):
         want = oracle.sa_doubling(S)
         assert np.array_equal(sa[off[w]:off[w + 1]], want)
         assert np.array_equal(lcp[off[w]:off[w + 1]][:len(S) - 1], oracle.lcp_kasai(S, want))
+
+
+@pytest.mark.parametrize("with_big_group", [False, True])
+def test_batched_fused_select_equals_global(ctx, with_big_group, monkeypatch):
+    """Batches of small windows take the fused per-window K5+K6 kernel
+    (window_select.cu); APO_SELECT_GLOBAL=1 forces the global path (CandF,
+    segment sort, RMQ heads, HeadF, unpack).  Repeats, offsets and
+    occurrences must be identical, and equal to the oracle on sampled
+    windows.  A window made of 200 copies of one block has sub-string groups
+    of more than 64 members: the fused kernel hands the batch back to the
+    global path."""
+    tok, off, _, _ = gen.c4(seed=77, windows=40, window=4096, templates=8, with_streams=False)
+    wins = [tok[off[w]:off[w + 1]] for w in range(len(off) - 1)]
+    if with_big_group:
+        wins.insert(7, np.tile(gen.random_string(5, 30, 1000), 200)[:6000])
+    wins.append(gen.random_string(9, 16384, 3))  # a full-size window
+    tok = np.concatenate(wins)
+    off = np.cumsum([0] + [len(x) for x in wins]).astype(np.int64)
+    for min_len in (5, 25):
+        got = [t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t)
+               for t in ctx.find_repeats_batched(dev(tok), off, min_len)]
+        monkeypatch.setenv("APO_SELECT_GLOBAL", "1")
+        ref = [t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t)
+               for t in ctx.find_repeats_batched(dev(tok), off, min_len)]
+        monkeypatch.delenv("APO_SELECT_GLOBAL")
+        for a, b in zip(got, ref):
+            assert np.array_equal(a, b)
+        rep, roff, occ = got
+        for w in (0, 7, len(wins) - 1):
+            want = oracle.find_repeats(wins[w], min_len, tier=1)
+            g = rep[roff[w]:roff[w + 1]]
+            assert np.array_equal(g[:, :3], want["repeats"][:, :3]), w
+            for row, wrow in zip(g, want["repeats"]):
+                assert np.array_equal(occ[row[3]:row[3] + row[2]], want["occ"][wrow[3]:wrow[3] + wrow[2]])
