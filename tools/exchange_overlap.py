@@ -54,10 +54,29 @@ def overlapped():
     return idx, u
 
 
+def publish_only():
+    ex._publish(trie)
+
+
+def pulled_build_only():
+    ex.start(trie)
+    ex.transport.wait()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    u = ex.finish()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
 for name, f in (("sm_union", sm_union), ("ce_union", ce_union), ("index_only", index_only),
-                ("ce_union+index overlapped", overlapped)):
+                ("ce_union+index overlapped", overlapped), ("publish_only", publish_only)):
     ts = [timed(f)[0] for _ in range(4)]
     if rank == 0:
         print(f"{name}: {[round(t, 2) for t in ts]} ms", flush=True)
-dist.barrier()
+bt = torch.tensor([pulled_build_only() for _ in range(3)][-1], device="cuda")
+dist.all_reduce(bt, op=dist.ReduceOp.MAX)
+if rank == 0:
+    print("union build from pulled lists (finish after wait)", round(float(bt.item()), 3), "ms", flush=True)
 dist.destroy_process_group()
