@@ -337,9 +337,12 @@ def main():
     stage_ms = {k: 0.0 for k in stage_names}
     last = {}
 
-    def step(tok, streams, timed=False):
+    def step(tok, streams, timed=False, after_trie=None):
         """One pass of the whole hot path: FindRepeats on every window, the
-        candidate trace set (+ the cross-GPU union), batched matching."""
+        candidate trace set (+ the cross-GPU union), batched matching.
+        after_trie: called once the trace set is built (the e2e loop starts
+        the next step's input upload there, so it overlaps matching's long
+        kernels rather than the analysis's many short ones)."""
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)] if timed else None
         if timed:
             evs[0].record(s)
@@ -349,6 +352,8 @@ def main():
         hits = None
         if streams is not None:
             trie = ctx.trie_build(tok, off, rep, roff, MIN_LEN, 0)
+            if after_trie is not None:
+                after_trie()
             if timed:
                 evs[2].record(s)
             idx = None
@@ -489,23 +494,29 @@ def main():
         copied = [torch.cuda.Event() for _ in range(2)]
         consumed = [torch.cuda.Event() for _ in range(2)]
 
+        CHUNK = 2 << 20  # elements (16 MB): the library's own small uploads interleave between chunks
+
         def enqueue_copy(i):
             bi = i % 2
             cs.wait_event(consumed[bi])  # the buffer's previous step is done with it
             with torch.cuda.stream(cs):
-                dbuf[bi][0].copy_(tok_host, non_blocking=True)
-                if st_host is not None:
-                    dbuf[bi][1].copy_(st_host, non_blocking=True)
+                for dst, src in ((dbuf[bi][0], tok_host), (dbuf[bi][1], st_host)):
+                    if src is None:
+                        continue
+                    for a in range(0, src.numel(), CHUNK):
+                        dst[a:a + CHUNK].copy_(src[a:a + CHUNK], non_blocking=True)
             copied[bi].record(cs)
 
         def e2e_step(i, last):
             bi = i % 2
             s.wait_event(copied[bi])
-            if not last:
-                enqueue_copy(i + 1)
-            c, h = step(dbuf[bi][0], dbuf[bi][1])
+            nxt = None if last else (lambda: enqueue_copy(i + 1))
+            if nxt is not None and dbuf[bi][1] is None:  # no matching stage: upload at once
+                nxt()
+                nxt = None
+            c, h = step(dbuf[bi][0], dbuf[bi][1], after_trie=nxt)
             consumed[bi].record(s)
-            r, o = (int(x) for x in c.tolist())
+            r, o = (int(x) for x in ctx._read(c))
             # the step's result read back: the analysis output (repeats, their
             # per-window offsets, occurrence lists) and the replay decisions;
             # MATCH_ALL stays implicit on the device (per-end chains of the
@@ -533,7 +544,7 @@ def main():
             return sum(x.numel() * x.element_size() for x in outs) + 16 + (16 if h is not None else 0)
 
         def readback(rep, roff, occ, counts, h):
-            r, o = (int(x) for x in counts.tolist())
+            r, o = (int(x) for x in ctx._read(counts))
             return to_host(rep[:r], roff, occ[:o], h)
 
         def inputs(K):

@@ -147,6 +147,7 @@ class Context:
         if not torch.cuda.is_available():
             raise RuntimeError("libapo needs a CUDA device (no CPU fallback)")
         self.lib = load_library()
+        self._pinned = {}
         self.device = torch.device("cuda", device if isinstance(device, int) else device.index or 0)
         h = ctypes.c_void_p()
         torch.cuda.init()
@@ -165,6 +166,18 @@ class Context:
             self.close()
         except Exception:
             pass
+
+    def _read(self, t: torch.Tensor) -> list:
+        """Small device tensor -> Python list through a cached pinned buffer (a
+        pageable copy waits behind any host -> device transfer in flight)."""
+        key = (t.dtype, t.numel())
+        buf = self._pinned.get(key)
+        if buf is None:
+            buf = torch.empty(t.numel(), dtype=t.dtype).pin_memory()
+            self._pinned[key] = buf
+        buf.copy_(t.reshape(-1), non_blocking=True)
+        torch.cuda.current_stream(t.device).synchronize()
+        return buf.tolist()
 
     def _raise(self, st: int):
         if st not in (APO_OK,):
@@ -233,7 +246,7 @@ class Context:
         cnt = torch.zeros(1, dtype=torch.int64, device=d)
         self._raise(self.lib.apo_candidates(self.h, _ptr(tok), n, int(min_len), _ptr(ln), _ptr(cid), _ptr(st),
                                             _ptr(kept), cap, _ptr(cnt), _stream(d)))
-        m = int(cnt.item())
+        m = int(self._read(cnt)[0])
         return dict(cand_len=ln[:m], cand_id=cid[:m], cand_start=st[:m], keep=kept[:m])
 
     # ------------------------------------------------------- FindRepeats --
@@ -255,7 +268,7 @@ class Context:
                                               _ptr(occ), cap, _ptr(counts), _stream(d)))
         if not sync:
             return out, occ, counts
-        r, o = (int(x) for x in counts.tolist())
+        r, o = (int(x) for x in self._read(counts))
         return out[:r], occ[:o]
 
     def find_repeats_batched(self, tok: torch.Tensor, off, min_len: int, min_count: int = 1, sync: bool = True,
@@ -277,7 +290,7 @@ class Context:
                                                       _ptr(occ), occ.shape[0], _ptr(counts), _stream(d)))
         if not sync:
             return rep, roff, occ, counts
-        r, oc = (int(x) for x in counts.tolist())
+        r, oc = (int(x) for x in self._read(counts))
         return rep[:r], roff, occ[:oc]
 
     def find_repeats_batched_host(self, tok_host: torch.Tensor, off, min_len: int, min_count: int = 1):
@@ -357,7 +370,7 @@ class Context:
             cnt = torch.zeros(2, dtype=torch.int64, device=d)
             self._raise(self.lib.apo_match(self.h, trie.h, _ptr(streams), o.ctypes.data_as(_P_I64), len(o) - 1,
                                            int(mode), _ptr(out), cap, _ptr(cnt), _stream(d)))
-            c = cnt.tolist()
+            c = self._read(cnt)
             n = int(c[0])
             if n <= cap:
                 if mode == 1:
@@ -389,7 +402,7 @@ class Context:
             cnt = torch.zeros(2, dtype=torch.int64, device=d)
             self._raise(self.lib.apo_match_indexed(self.h, trie.h, idx.h, int(mode), _ptr(out), cap, _ptr(cnt),
                                                    _stream(d)))
-            c = cnt.tolist()
+            c = self._read(cnt)
             n = int(c[0])
             if n <= cap:
                 if mode == 1:
@@ -414,7 +427,7 @@ class Context:
             cnt = torch.zeros(1, dtype=torch.int64, device=d)
             self._raise(self.lib.apo_replay(self.h, trie.h, _ptr(hits), hits.shape[0], lens.ctypes.data_as(_P_I64),
                                             len(lens), ctypes.byref(prm), _ptr(out), cap, _ptr(cnt), _stream(d)))
-            n = int(cnt.item())
+            n = int(self._read(cnt)[0])
             if n <= cap:
                 return out[:n]
             cap = n

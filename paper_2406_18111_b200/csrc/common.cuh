@@ -169,6 +169,23 @@ struct Ctx {
   u32 *take_counter(cudaStream_t s);
   u32 read_u32(const u32 *d_ptr, cudaStream_t s);
   u64 read_u64(const u64 *d_ptr, cudaStream_t s);
+  // up to 16 consecutive u32 words from the device (synchronises s)
+  void read_words(u32 *out, const void *d_src, int nwords, cudaStream_t s);
+  // small host -> device uploads (offset tables, scalars): staged in a
+  // mapped pinned ring and read by a kernel on `s`.  A copy-engine copy
+  // (pageable or pinned) would queue behind any large host -> device
+  // transfer other streams have in flight.
+  char *h_ring = nullptr;
+  size_t ring_off = 0;
+  void h2d(void *d_dst, const void *h_src, size_t bytes, cudaStream_t s);
+  // device -> pageable host: through a pinned bounce buffer (a pageable
+  // copy would wait behind any host -> device transfer in flight), then
+  // synchronises `s`
+  char *h_bounce = nullptr;
+  size_t bounce_cap = 0;
+  void d2h(void *h_dst, const void *d_src, size_t bytes, cudaStream_t s);
+  // device -> device copies by a kernel on `s` (no copy-engine queue)
+  void d2d(void *d_dst, const void *d_src, size_t bytes, cudaStream_t s);
   // dynamic shared-memory opt-ins already applied on THIS context's device
   // (the attribute is per device, so it is tracked per context, not per
   // process)

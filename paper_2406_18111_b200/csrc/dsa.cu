@@ -212,7 +212,7 @@ apo_status apo_dsa_heads(apo_ctx *ctx, const uint64_t *d_keys, int64_t m, uint64
             "invalid argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const i64 init[2] = {0, -1};
-    APO_CUDA(cudaMemcpyAsync(d_stats, init, sizeof(init), cudaMemcpyHostToDevice, s));
+    c.h2d(d_stats, init, sizeof(init), s);
     if (m == 0) return;
     DsaHeadF f{d_keys, m, prev_key, has_prev, gbase, carry, d_rank, d_stats};
     launch_scan<true>(c, m, f, s);

@@ -1136,8 +1136,7 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   APO_CHECK_LAUNCH();
   c.launches++;
   std::vector<i64> h_hb(size_t(nstreams) + 1);
-  APO_CUDA(cudaMemcpyAsync(h_hb.data(), hbeg0, hb_bytes, cudaMemcpyDeviceToHost, s));
-  APO_CUDA(cudaStreamSynchronize(s));
+  c.d2h(h_hb.data(), hbeg0, hb_bytes, s);
   std::vector<i64> h_pb(size_t(nstreams) + 1);
   i64 nparts = 0;
   for (int q = 0; q < nstreams; ++q) {
@@ -1225,12 +1224,12 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   char *ws = static_cast<char *>(c.pool_get(ws_bytes));
   Carver cv(ws);
   plan(cv);
-  APO_CUDA(cudaMemcpyAsync(hbeg, hbeg0, hb_bytes, cudaMemcpyDeviceToDevice, s));
-  APO_CUDA(cudaMemcpyAsync(pbeg, h_pb.data(), hb_bytes, cudaMemcpyHostToDevice, s));
-  APO_CUDA(cudaMemcpyAsync(soff, h_soff.data(), hb_bytes, cudaMemcpyHostToDevice, s));
-  APO_CUDA(cudaMemcpyAsync(pstream, h_ps.data(), sizeof(int) * size_t(nparts), cudaMemcpyHostToDevice, s));
-  APO_CUDA(cudaMemcpyAsync(order, h_order.data(), sizeof(int) * size_t(nstreams), cudaMemcpyHostToDevice, s));
-  APO_CUDA(cudaMemcpyAsync(ddq, dq.data(), sizeof(u32) * dq.size(), cudaMemcpyHostToDevice, s));
+  c.d2d(hbeg, hbeg0, hb_bytes, s);
+  c.h2d(pbeg, h_pb.data(), hb_bytes, s);
+  c.h2d(soff, h_soff.data(), hb_bytes, s);
+  c.h2d(pstream, h_ps.data(), sizeof(int) * size_t(nparts), s);
+  c.h2d(order, h_order.data(), sizeof(int) * size_t(nstreams), s);
+  c.h2d(ddq, dq.data(), sizeof(u32) * dq.size(), s);
   APO_CUDA(cudaMemsetAsync(maxslot, 0, sizeof(u32) * size_t(nstreams), s));
   RP a{reinterpret_cast<const int4 *>(d_hits), tr->d_off, ddq, int(dq.size()), prm.count_cap, prm.decay_period,
        1.0 / double(prm.decay_period), u32(prm.bonus_num), u32(prm.bonus_den), nstreams, slot_bits, hbeg, pbeg,
@@ -1251,8 +1250,8 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
     APO_CUDA(cudaMemsetAsync(need_wv, 0, size_t(nstreams), s));
   }
   if (fast) {
-    APO_CUDA(cudaMemcpyAsync(wq, h_wq.data(), sizeof(int) * size_t(nitems), cudaMemcpyHostToDevice, s));
-    APO_CUDA(cudaMemcpyAsync(wr0, h_wr.data(), sizeof(i64) * (size_t(nitems) + 1), cudaMemcpyHostToDevice, s));
+    c.h2d(wq, h_wq.data(), sizeof(int) * size_t(nitems), s);
+    c.h2d(wr0, h_wr.data(), sizeof(i64) * (size_t(nitems) + 1), s);
     a.ix_off = ri->off;
     a.ix_sa = ri->sa;
     a.ix_tkey = ri->tkey;
@@ -1296,8 +1295,7 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   }
   // per-stream tables: on chip when they fit, else in a global block
   std::vector<u32> h_ms(static_cast<size_t>(nstreams));
-  APO_CUDA(cudaMemcpyAsync(h_ms.data(), maxslot, sizeof(u32) * size_t(nstreams), cudaMemcpyDeviceToHost, s));
-  APO_CUDA(cudaStreamSynchronize(s));
+  c.d2h(h_ms.data(), maxslot, sizeof(u32) * size_t(nstreams), s);
   const u32 slots_on_chip = u32(kStateBytesMax / 8);
   std::vector<i64> h_gso(size_t(nstreams) + 1);
   i64 gw = 0;
@@ -1313,7 +1311,7 @@ void run_replay(Ctx &c, const apo_trie *tr, const apo_match_rec *d_hits, i64 nhi
   h_gso[nstreams] = gw;
   void *gstate = nullptr;
   if (gw > 0) gstate = c.pool_get(sizeof(u32) * size_t(gw));
-  APO_CUDA(cudaMemcpyAsync(gso, h_gso.data(), hb_bytes, cudaMemcpyHostToDevice, s));
+  c.h2d(gso, h_gso.data(), hb_bytes, s);
   a.gstate = gstate;
   a.on_chip_slots = slots_on_chip;
   a.on_chip_bits = slots_on_chip / 32;

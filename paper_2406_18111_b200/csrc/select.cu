@@ -945,7 +945,7 @@ void emit_repeats(Ctx &c, const Batch &b, SelWork &w, int min_count, apo_repeat 
 
 void emit_candidates(Ctx &c, const Batch &b, const SelWork &w, i32 *len, i32 *id, i32 *start, u8 *kept, i64 cap,
                      i64 *count, cudaStream_t s) {
-  APO_CUDA(cudaMemcpyAsync(count, &w.m, sizeof(i64), cudaMemcpyHostToDevice, s));
+  c.h2d(count, &w.m, sizeof(i64), s);
   if (w.m > 0) {
     k_emit_cands<<<grid_for(w.m, T), T, 0, s>>>(b, w.cl, w.cs, w.cg, w.state, w.m, cap, len, id, start, kept);
     APO_CHECK_LAUNCH();

@@ -341,7 +341,7 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
     APO_CHECK_LAUNCH();
     c.launches++;
     // copy values so the (key, value) pair lives in (ok, ov)
-    APO_CUDA(cudaMemcpyAsync(ov, sv, sizeof(u32) * N, cudaMemcpyDeviceToDevice, s));
+    c.d2d(ov, sv, sizeof(u32) * N, s);
     bool a2 = radix_sort_u64_u32(c, ok, ov, sk, sv, N, 0, bits_for(u64(b.W - 1)), s);
     u32 *idx = a2 ? sv : ov;
     k_gather_tok<<<G, T, 0, s>>>(idx, tok, N, w.tok_sorted);
@@ -426,7 +426,7 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
     if (h > b.maxwin) throw Error{APO_ERR_CUDA, "prefix doubling did not converge"};
   }
   w.R = r;
-  APO_CUDA(cudaMemcpyAsync(w.sa, final_sa, sizeof(i32) * N, cudaMemcpyDeviceToDevice, s));
+  c.d2d(w.sa, final_sa, sizeof(i32) * N, s);
   }
 
   if (!want_lcp) return;

@@ -119,9 +119,9 @@ i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scra
   k_ht_insert<<<grid_for(n, 256), 256, 0, s>>>(tok, n, table, cap, ids, cnt, cnt + 1);
   APO_CHECK_LAUNCH();
   c.launches++;
-  APO_CUDA(cudaMemcpyAsync(c.h_flag, cnt, sizeof(u32) * 3, cudaMemcpyDeviceToHost, s));
-  APO_CUDA(cudaStreamSynchronize(s));
-  const u32 nkeys = c.h_flag[0], has_max = c.h_flag[1], over = c.h_flag[2];
+  u32 hv[3];
+  c.read_words(hv, cnt, 3, s);
+  const u32 nkeys = hv[0], has_max = hv[1], over = hv[2];
   if (over) return -1;
   HtCompactF f{table, dk, ds, i64(cap), tot};
   launch_scan<false>(c, i64(cap), f, s);
@@ -143,7 +143,7 @@ i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scra
   }
   if (has_max) {  // the token ~0 is the largest value
     const u32 r = u32(K);
-    APO_CUDA(cudaMemcpyAsync(slot_rank + cap, &r, sizeof(u32), cudaMemcpyHostToDevice, s));
+    c.h2d(slot_rank + cap, &r, sizeof(u32), s);
     ++K;
   }
   k_ids_from_slots<<<grid_for(n, 256), 256, 0, s>>>(ids, n, slot_rank);

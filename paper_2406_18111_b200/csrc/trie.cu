@@ -302,7 +302,7 @@ void plan_gen(Carver &cv, Batch &b, GenPlan &g, bool lcp, int nsmid) {
 }
 
 void upload_batch(Ctx &c, Batch &b, GenPlan &g, const std::vector<i64> &h_off, cudaStream_t s) {
-  APO_CUDA(cudaMemcpyAsync(g.d_off, h_off.data(), sizeof(i64) * h_off.size(), cudaMemcpyHostToDevice, s));
+  c.h2d(g.d_off, h_off.data(), sizeof(i64) * h_off.size(), s);
   k_fill_wid_t<<<b.W, T256, 0, s>>>(g.d_off, b.W, b.N, g.d_wid);
   APO_CHECK_LAUNCH();
   c.launches++;
@@ -1771,14 +1771,14 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
   c.arena.reserve(dry.off, s);
   Carver cv(c.arena.base);
   plan(cv);
-  APO_CUDA(cudaMemcpyAsync(d_poff, h_poff.data(), sizeof(i64) * (np + 1), cudaMemcpyHostToDevice, s));
+  c.h2d(d_poff, h_poff.data(), sizeof(i64) * (np + 1), s);
   // 1. merge identical pieces
   if (src)
     k_piece_hash<true><<<grid_for(np * 32, T256), T256, 0, s>>>(d_ptok, d_poff, np, hk, hv, pk, *src);
   else
     k_piece_hash<false><<<grid_for(np * 32, T256), T256, 0, s>>>(d_ptok, d_poff, np, hk, hv, pk, PieceSrc{});
   APO_CHECK_LAUNCH();
-  APO_CUDA(cudaMemcpyAsync(hk_keep, hk, sizeof(u64) * np, cudaMemcpyDeviceToDevice, s));
+  c.d2d(hk_keep, hk, sizeof(u64) * np, s);
   // grouping only needs equal hashes together: 32 hash bits suffice (a rare
   // split group is caught by the exact neighbour check of step 3)
   bool a1 = radix_sort_u64_u32(c, hk, hv, hk_alt, hv_alt, np, 0, 32, s);
@@ -1824,7 +1824,7 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
     c.launches += 4;
     const u32 worst = c.read_u32(reinterpret_cast<const u32 *>(scal + 2), s);
     if (worst <= u32(kMaxTie)) {
-      APO_CUDA(cudaMemcpyAsync(order, rv, sizeof(u32) * U, cudaMemcpyDeviceToDevice, s));
+      c.d2d(order, rv, sizeof(u32) * U, s);
     } else {
       i64 PU = 1;
       while (PU < U) PU <<= 1;
@@ -1850,8 +1850,7 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
   std::vector<i64> h_uoff(size_t(T) + 1, 0);
   {
     std::vector<i32> hl(static_cast<size_t>(T));
-    APO_CUDA(cudaMemcpyAsync(hl.data(), ulen, sizeof(i32) * T, cudaMemcpyDeviceToHost, s));
-    APO_CUDA(cudaStreamSynchronize(s));
+    c.d2h(hl.data(), ulen, sizeof(i32) * T, s);
     for (i64 t = 0; t < T; ++t) h_uoff[t + 1] = h_uoff[t] + hl[t];
   }
   const i64 ntok = h_uoff[T];
@@ -1859,7 +1858,7 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
   tr->off_bytes = sizeof(i64) * size_t(T + 1);
   tr->d_tok = static_cast<u64 *>(c.pool_get(tr->tok_bytes));
   tr->d_off = static_cast<i64 *>(c.pool_get(tr->off_bytes));
-  APO_CUDA(cudaMemcpyAsync(tr->d_off, h_uoff.data(), sizeof(i64) * (T + 1), cudaMemcpyHostToDevice, s));
+  c.h2d(tr->d_off, h_uoff.data(), sizeof(i64) * (T + 1), s);
   k_src_of<<<grid_for(T, T256), T256, 0, s>>>(uniq, d_poff, T, d_src);
   k_copy_pieces<<<grid_for(T * 32, T256), T256, 0, s>>>(d_ptok, d_src, tr->d_off, T, tr->d_tok);
   APO_CHECK_LAUNCH();
@@ -1909,8 +1908,7 @@ apo_status apo_trie_build(apo_ctx *ctx, const uint64_t *d_tok, const int64_t *h_
             "invalid argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     i64 nrep = 0;
-    APO_CUDA(cudaMemcpyAsync(&nrep, d_rep_off + nwin, sizeof(i64), cudaMemcpyDeviceToHost, s));
-    APO_CUDA(cudaStreamSynchronize(s));
+    c.d2h(&nrep, d_rep_off + nwin, sizeof(i64), s);
     if (nrep == 0) {
       tr->h_off.assign(1, 0);
       return;
@@ -1940,7 +1938,7 @@ apo_status apo_trie_build(apo_ctx *ctx, const uint64_t *d_tok, const int64_t *h_
     c.aux.reserve(dry.off, s);
     Carver cv(c.aux.base);
     plan(cv);
-    APO_CUDA(cudaMemcpyAsync(d_src_off, h_off, sizeof(i64) * (nwin + 1), cudaMemcpyHostToDevice, s));
+    c.h2d(d_src_off, h_off, sizeof(i64) * (nwin + 1), s);
     SrcRep sr{d_rep, d_rep_off, d_src_off, nwin, nrep, min_len, max_len};
     PieceCountF pf{sr, pbase, scal};
     launch_scan<false>(c, nrep, pf, s);
@@ -1950,12 +1948,11 @@ apo_status apo_trie_build(apo_ctx *ctx, const uint64_t *d_tok, const int64_t *h_
     APO_CHECK_LAUNCH();
     c.launches++;
     std::vector<i32> hl(static_cast<size_t>(np));
-    APO_CUDA(cudaMemcpyAsync(hl.data(), p_len, sizeof(i32) * np, cudaMemcpyDeviceToHost, s));
-    APO_CUDA(cudaStreamSynchronize(s));
+    c.d2h(hl.data(), p_len, sizeof(i32) * np, s);
     std::vector<i64> h_poff(size_t(np) + 1, 0);
     for (i64 q = 0; q < np; ++q) h_poff[q + 1] = h_poff[q] + hl[q];
     require(h_poff[np] <= Nsrc, "piece tokens exceed their bound");
-    APO_CUDA(cudaMemcpyAsync(p_off, h_poff.data(), sizeof(i64) * (np + 1), cudaMemcpyHostToDevice, s));
+    c.h2d(p_off, h_poff.data(), sizeof(i64) * (np + 1), s);
     k_copy_pieces<<<grid_for(np * 32, T256), T256, 0, s>>>(d_tok, p_src, p_off, np, ptok);
     APO_CHECK_LAUNCH();
     c.launches++;
@@ -2229,7 +2226,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
         Carver kc(static_cast<char *>(x.blk));
         carve(kc);
         auto cp = [&](void *dst, const void *src, size_t n) {
-          if (n) APO_CUDA(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, s));
+          if (n) c.d2d(dst, src, n, s);
         };
         cp(x.d_off, g.d_off, sizeof(i64) * (size_t(nstreams) + 1));
         cp(x.d_wid, g.d_wid, sizeof(i32) * size_t(Ns));
@@ -2509,9 +2506,9 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
                 hb2 = reinterpret_cast<u32 *>(ilo2 + P);
                 pt2 = hb2 + P;
               }
-              APO_CUDA(cudaMemcpyAsync(ilo2, ilo, sizeof(i64) * P, cudaMemcpyDeviceToDevice, s));
-              APO_CUDA(cudaMemcpyAsync(hb2, hbase, sizeof(u32) * P, cudaMemcpyDeviceToDevice, s));
-              APO_CUDA(cudaMemcpyAsync(pt2, ptr, sizeof(u32) * P, cudaMemcpyDeviceToDevice, s));
+              c.d2d(ilo2, ilo, sizeof(i64) * P, s);
+              c.d2d(hb2, hbase, sizeof(u32) * P, s);
+              c.d2d(pt2, ptr, sizeof(u32) * P, s);
               c.aux.reserve(need, s);
               ilo = ilo2;
               hbase = hb2;
@@ -2573,7 +2570,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
     }
     }
     if (emitted) {
-      APO_CUDA(cudaMemcpyAsync(d_count, &nh, sizeof(i64), cudaMemcpyHostToDevice, s));
+      c.h2d(d_count, &nh, sizeof(i64), s);
       APO_CUDA(cudaStreamSynchronize(s));
       return;
     }
@@ -2588,7 +2585,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       APO_CHECK_LAUNCH();
       c.launches++;
     }
-    APO_CUDA(cudaMemcpyAsync(d_count, &nh, sizeof(i64), cudaMemcpyHostToDevice, s));
+    c.h2d(d_count, &nh, sizeof(i64), s);
     APO_CUDA(cudaStreamSynchronize(s));
   }
 }
@@ -2627,7 +2624,7 @@ void match_entry(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const in
   const apo_replay_params prm{100, 64881, 100, 11, 10, 0};
   run_replay(c, tr, static_cast<const apo_match_rec *>(c.hitbuf), nh, len.data(), nstreams, prm,
              reinterpret_cast<apo_replay_rec *>(d_out), cap, d_count, s, &ri);
-  APO_CUDA(cudaMemcpyAsync(d_count + 1, &nh, sizeof(i64), cudaMemcpyHostToDevice, s));
+  c.h2d(d_count + 1, &nh, sizeof(i64), s);
   APO_CUDA(cudaStreamSynchronize(s));
 }
 }  // namespace

@@ -409,9 +409,8 @@ bool window_select(Ctx &c, const Batch &b, const SAWork &sa, int min_len, SelWor
                                          w.gbase, w.gwin, w.gpos, m_dev, G_dev, big, c.status, ctr, ep);
   APO_CHECK_LAUNCH();
   c.launches++;
-  APO_CUDA(cudaMemcpyAsync(c.h_flag, w.scal, sizeof(u64) * 6, cudaMemcpyDeviceToHost, s));
-  APO_CUDA(cudaStreamSynchronize(s));
-  const u64 *h = reinterpret_cast<const u64 *>(c.h_flag);
+  u64 h[6];
+  c.read_words(reinterpret_cast<u32 *>(h), w.scal, 12, s);
   if (u32(h[5]) != 0) return false;
   w.m = i64(h[0]);
   w.G = i64(h[1]);
