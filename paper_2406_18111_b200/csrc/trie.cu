@@ -350,6 +350,7 @@ struct BucketF {
   u64 *e_tok;
   u32 *e_lo, *e_q;
   i64 *total;
+  const unsigned short *sid = nullptr;  // dense ids + 1 of the streams: buckets keyed by id, not token
   // a bucket starts at a stream's first rank or where the first token
   // changes, i.e. where the LCP with the previous suffix is 0 (sequential
   // reads only: the SA is stream-major, so rank k is in the stream of
@@ -361,7 +362,7 @@ struct BucketF {
   }
   __device__ bool store(i64 k, u32 incl, u32 excl) const {
     if (incl != excl) {
-      e_tok[excl] = m.tok[m.sa[k]];
+      e_tok[excl] = sid ? u64(sid[m.sa[k]]) : m.tok[m.sa[k]];
       e_lo[excl] = u32(k);
       e_q[excl] = u32(m.wid[k]);
     }
@@ -381,10 +382,21 @@ __global__ void k_bucket_hi(const u32 *__restrict__ e_lo, const u32 *__restrict_
 
 // per trace: range [ea, eb) of token-sorted buckets with the trace's first token
 __global__ void k_trace_buckets(StreamMatch m, const u64 *__restrict__ sorted_tok, i64 E, u32 *__restrict__ ea,
-                                u32 *__restrict__ ecnt) {
+                                u32 *__restrict__ ecnt, const u32 *__restrict__ tid) {
   const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= m.T) return;
-  const u64 a = m.ttok[m.toff[t]];
+  u64 a;
+  if (tid != nullptr) {  // buckets keyed by dense id + 1; a token absent from the batch has none
+    const u32 x = tid[m.toff[t]];
+    if (x & 1u) {
+      ea[t] = 0;
+      ecnt[t] = 0;
+      return;
+    }
+    a = u64(x >> 1);
+  } else {
+    a = m.ttok[m.toff[t]];
+  }
   i64 lo = 0, hi = E;
   while (lo < hi) {
     i64 mid = (lo + hi) >> 1;
@@ -2187,12 +2199,14 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       p_lcp = g.sa.lcp;
       StreamMatch sm0{p_off, p_wid, p_sa, p_lcp, mtok, nullptr, nullptr, Ns, T};
       APO_CUDA(cudaMemsetAsync(scal, 0, sizeof(i64) * 4, s));
-      BucketF bf{sm0, e_tok, e_lo, e_q, scal};
+      BucketF bf{sm0, e_tok, e_lo, e_q, scal, p_sid};
       launch_scan<false>(c, Ns, bf, s);
       E = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
       k_bucket_hi<<<grid_for(E, T256), T256, 0, s>>>(e_lo, e_q, E, g.d_off, e_hi, e_idx);
       APO_CHECK_LAUNCH();
-      bool ae = radix_sort_u64_u32(c, e_tok, e_idx, e_tok_alt, e_idx_alt, E, 0, 64, s);
+      // ids + 1 <= K need bits(K) bits; raw tokens all 64
+      const int ebits = p_sid ? bits_for(u64(p_dkn + (p_dkmax ? 1 : 0))) : 64;
+      bool ae = radix_sort_u64_u32(c, e_tok, e_idx, e_tok_alt, e_idx_alt, E, 0, ebits, s);
       stok = ae ? e_tok_alt : e_tok;
       sord = ae ? e_idx_alt : e_idx;
       c.launches++;
@@ -2254,7 +2268,43 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
         c.launches++;
       }
       StreamMatch sm{p_off, p_wid, p_sa, p_lcp, mtok, rev ? tr->d_rtok : tr->d_tok, tr->d_off, Ns, T};
-      k_trace_buckets<<<grid_for(T, T256), T256, 0, s>>>(sm, stok, E, ea, ecnt);
+      // dense-id matching: the traces' comparison values against the batch
+      // dictionary (the buckets are keyed by id too)
+      u32 *tid = nullptr;
+      char *dict = nullptr;
+      size_t tid_bytes = 0, dict_bytes = 0;
+      struct PoolBack {  // returned once this block's launches are enqueued (pool users are stream-ordered)
+        Ctx &c;
+        void *&p;
+        size_t &n;
+        ~PoolBack() {
+          if (p) c.pool_put(p, n);
+        }
+      };
+      void *tid_v = nullptr, *dict_v = nullptr;
+      PoolBack back_tid{c, tid_v, tid_bytes}, back_dict{c, dict_v, dict_bytes};
+      if (p_sid != nullptr) {
+        tid_bytes = sizeof(u32) * size_t(std::max<i64>(tr->ntok, 1));
+        tid = static_cast<u32 *>(c.pool_get(tid_bytes));
+        u32 tslots = 1024;
+        while (i64(tslots) < 2 * p_dkn) tslots <<= 1;
+        dict_bytes = (sizeof(u64) + sizeof(u32)) * size_t(tslots) + 256;
+        dict = static_cast<char *>(c.pool_get(dict_bytes));
+        u64 *tkey = reinterpret_cast<u64 *>(dict);
+        u32 *tval = reinterpret_cast<u32 *>(tkey + tslots);
+        APO_CUDA(cudaMemsetAsync(tkey, 0xff, sizeof(u64) * tslots, s));
+        if (p_dkn > 0) {
+          k_dict_build<<<grid_for(p_dkn, T256), T256, 0, s>>>(p_dk, p_dkn, tkey, tval, tslots - 1);
+          APO_CHECK_LAUNCH();
+        }
+        k_trace_ids<<<grid_for(std::max<i64>(tr->ntok, 1), T256), T256, 0, s>>>(
+            tr->d_rtok, tr->ntok, p_dk, p_dkn, p_dkmax ? 1 : 0, tkey, tval, tslots - 1, tid);
+        APO_CHECK_LAUNCH();
+        c.launches += 2;
+        tid_v = tid;
+        dict_v = dict;
+      }
+      k_trace_buckets<<<grid_for(T, T256), T256, 0, s>>>(sm, stok, E, ea, ecnt, tid);
       APO_CHECK_LAUNCH();
       c.launches++;
       PairBaseF pf{ecnt, pbase, T, scal + 1};
@@ -2350,23 +2400,6 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
             const bool as = radix_sort_u64_u32(c, sk, sv, sk_alt, sv_alt, nstreams, 0, bits_for(u64(T)), s);
             const u32 *qorder = as ? sv_alt : sv;
             if (use_ids) {
-              // trace tokens as comparison values against the batch dictionary
-              const size_t tid_bytes = sizeof(u32) * size_t(std::max<i64>(tr->ntok, 1));
-              u32 *tid = static_cast<u32 *>(c.pool_get(tid_bytes));
-              u32 tslots = 1024;
-              while (i64(tslots) < 2 * p_dkn) tslots <<= 1;
-              const size_t dict_bytes = (sizeof(u64) + sizeof(u32)) * size_t(tslots) + 256;
-              char *dict = static_cast<char *>(c.pool_get(dict_bytes));
-              u64 *tkey = reinterpret_cast<u64 *>(dict);
-              u32 *tval = reinterpret_cast<u32 *>(tkey + tslots);
-              APO_CUDA(cudaMemsetAsync(tkey, 0xff, sizeof(u64) * tslots, s));
-              if (p_dkn > 0) {
-                k_dict_build<<<grid_for(p_dkn, T256), T256, 0, s>>>(p_dk, p_dkn, tkey, tval, tslots - 1);
-                APO_CHECK_LAUNCH();
-              }
-              k_trace_ids<<<grid_for(std::max<i64>(tr->ntok, 1), T256), T256, 0, s>>>(
-                  tr->d_rtok, tr->ntok, p_dk, p_dkn, p_dkmax ? 1 : 0, tkey, tval, tslots - 1, tid);
-              APO_CHECK_LAUNCH();
               k_pair_meta<<<grid_for(P, T256), T256, 0, s>>>(sqk, sqv, P, pair_e, ptr, e_lo, e_hi, p_off, tr->d_off,
                                                              meta);
               APO_CHECK_LAUNCH();
@@ -2378,9 +2411,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
                                                                      icnt, qtot, qorder);
               APO_CHECK_LAUNCH();
               if (c.prof) c.prof_end(s);
-              c.pool_put(tid, tid_bytes);  // later pool users run on this stream, after the matcher
-              c.pool_put(dict, dict_bytes);
-              c.launches += 5;
+              c.launches += 3;
             } else {
               const size_t smem = sizeof(u64) * kSMMax + 2 * sizeof(unsigned short) * kSMMax;
               c.smem_optin(reinterpret_cast<const void *>(k_stream_match), smem);
