@@ -345,40 +345,101 @@ struct StreamMatch {
   i64 N, T;
 };
 
-struct BucketF {
-  StreamMatch m;
-  u64 *e_tok;
-  u32 *e_lo, *e_q;
-  i64 *total;
-  const unsigned short *sid = nullptr;  // dense ids + 1 of the streams: buckets keyed by id, not token
-  // a bucket starts at a stream's first rank or where the first token
-  // changes, i.e. where the LCP with the previous suffix is 0 (sequential
-  // reads only: the SA is stream-major, so rank k is in the stream of
-  // position k)
-  __device__ u32 load(i64 k) const {
-    const int q = m.wid[k];
-    if (k == m.off[q]) return 1;
-    return m.lcp[k - 1] == 0 ? 1u : 0u;
-  }
-  __device__ bool store(i64 k, u32 incl, u32 excl) const {
-    if (incl != excl) {
-      e_tok[excl] = sid ? u64(sid[m.sa[k]]) : m.tok[m.sa[k]];
-      e_lo[excl] = u32(k);
-      e_q[excl] = u32(m.wid[k]);
-    }
-    if (k == m.N - 1) *total = i64(incl);
-    return false;
-  }
-  __device__ u32 *flag() const { return nullptr; }
-};
 
-__global__ void k_bucket_hi(const u32 *__restrict__ e_lo, const u32 *__restrict__ e_q, i64 E,
-                            const i64 *__restrict__ off, u32 *__restrict__ e_hi, u32 *__restrict__ e_idx) {
-  const i64 e = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= E) return;
-  e_hi[e] = (e + 1 < E && e_q[e + 1] == e_q[e]) ? e_lo[e + 1] : u32(off[e_q[e] + 1]);
-  e_idx[e] = u32(e);
+// The same buckets, one CTA per stream (streams claimed in order; their
+// bucket counts combined by a decoupled look-back): heads counted, the
+// stream's base found, then the heads written in rank order with their end
+// (the next head of the stream, or the stream's end) -- two sequential reads
+// of the stream's LCP instead of a device-wide scan with random window-id
+// lookups.
+constexpr int kBkThreads = 1024;
+constexpr int kBkPer = 16;  // consecutive ranks per thread in the write pass
+
+__global__ void __launch_bounds__(kBkThreads) k_stream_buckets(StreamMatch m, const unsigned short *__restrict__ sid,
+                                                              u64 *__restrict__ e_tok, u32 *__restrict__ e_lo,
+                                                              u32 *__restrict__ e_q, u32 *__restrict__ e_hi,
+                                                              u32 *__restrict__ e_idx, i64 *__restrict__ total,
+                                                              int W, u64 *status, u32 *counter, u32 epoch) {
+  __shared__ u32 s_w, s_base, s_wsum[kBkThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_w = atomicAdd(counter, 1u);
+  __syncthreads();
+  const int w = int(s_w);
+  const i64 beg = m.off[w], n = m.off[w + 1] - beg;
+  auto head = [&](i64 r) -> u32 { return (r == 0 || m.lcp[beg + r - 1] == 0) ? 1u : 0u; };
+  u32 cnt = 0;
+  for (i64 r = tid; r < n; r += kBkThreads) cnt += head(r);
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if (lane == 0) s_wsum[warp] = cnt;
+  __syncthreads();
+  if (warp == 0) {
+    u32 v = s_wsum[lane];
+    v = __reduce_add_sync(0xffffffffu, v);
+    if (lane == 0) {
+      u32 pre = 0;
+      if (w == 0) {
+        lb_store(status, lb_pack(epoch, kFlagInc, v));
+      } else {
+        lb_store(status + w, lb_pack(epoch, kFlagAgg, v));
+        pre = lb_lookback<false>(status, 1, 0, w, epoch);
+        lb_store(status + w, lb_pack(epoch, kFlagInc, pre + v));
+      }
+      s_base = pre;
+      if (w == W - 1) *total = i64(pre + v);
+    }
+  }
+  __syncthreads();
+  const u32 base = s_base;
+  u32 run = base;  // heads written so far
+  for (i64 t0 = 0; t0 < n; t0 += i64(kBkThreads) * kBkPer) {
+    const i64 r0 = t0 + i64(tid) * kBkPer;
+    u32 bits = 0;
+#pragma unroll
+    for (int j = 0; j < kBkPer; ++j)
+      if (r0 + j < n && head(r0 + j)) bits |= 1u << j;
+    const u32 c = __popc(bits);
+    u32 incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u32 o = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += o;
+    }
+    if (lane == 31) s_wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const u32 x = s_wsum[lane];
+      u32 y = x;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const u32 o = __shfl_up_sync(0xffffffffu, y, d);
+        if (lane >= d) y += o;
+      }
+      s_wsum[lane] = y - x;
+    }
+    __syncthreads();
+    u32 o = run + s_wsum[warp] + incl - c;
+    const u32 tile_total = __shfl_sync(0xffffffffu, incl, 31);  // (this warp's; the CTA total follows)
+    (void)tile_total;
+    while (bits) {
+      const int j = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const i64 k = beg + r0 + j;
+      const i64 p = m.sa[k];
+      e_tok[o] = sid ? u64(sid[p]) : m.tok[p];
+      e_lo[o] = u32(k);
+      e_q[o] = u32(w);
+      e_idx[o] = o;
+      ++o;
+    }
+    __syncthreads();
+    if (tid == kBkThreads - 1) s_base = o;  // the last thread's end = heads through this tile
+    __syncthreads();
+    run = s_base;
+  }
+  __syncthreads();  // every head's e_lo is written and visible to the CTA
+  for (u32 e = base + tid; e < run; e += kBkThreads) e_hi[e] = e + 1 < run ? e_lo[e + 1] : u32(beg + n);
 }
+
 
 // per trace: range [ea, eb) of token-sorted buckets with the trace's first token
 __global__ void k_trace_buckets(StreamMatch m, const u64 *__restrict__ sorted_tok, i64 E, u32 *__restrict__ ea,
@@ -2199,11 +2260,16 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       p_lcp = g.sa.lcp;
       StreamMatch sm0{p_off, p_wid, p_sa, p_lcp, mtok, nullptr, nullptr, Ns, T};
       APO_CUDA(cudaMemsetAsync(scal, 0, sizeof(i64) * 4, s));
-      BucketF bf{sm0, e_tok, e_lo, e_q, scal, p_sid};
-      launch_scan<false>(c, Ns, bf, s);
+      {
+        c.ensure_status(size_t(nstreams), s);
+        u32 *ctr = c.take_counter(s);
+        const u32 ep = c.next_epoch();
+        k_stream_buckets<<<nstreams, kBkThreads, 0, s>>>(sm0, p_sid, e_tok, e_lo, e_q, e_hi, e_idx, scal, nstreams,
+                                                       c.status, ctr, ep);
+        APO_CHECK_LAUNCH();
+        c.launches++;
+      }
       E = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
-      k_bucket_hi<<<grid_for(E, T256), T256, 0, s>>>(e_lo, e_q, E, g.d_off, e_hi, e_idx);
-      APO_CHECK_LAUNCH();
       // ids + 1 <= K need bits(K) bits; raw tokens all 64
       const int ebits = p_sid ? bits_for(u64(p_dkn + (p_dkmax ? 1 : 0))) : 64;
       bool ae = radix_sort_u64_u32(c, e_tok, e_idx, e_tok_alt, e_idx_alt, E, 0, ebits, s);
