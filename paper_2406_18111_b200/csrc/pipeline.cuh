@@ -61,15 +61,33 @@ void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp, int nsmid);
 // K2 (hash path): dense order-preserving token ids; returns K or -1 when
 // the distinct count exceeds cap / 2.
 size_t token_ids_scratch_bytes(i64 n, u32 cap);
+// Mirrored ids (the matcher's reversed streams without reversing tokens):
+// the table is built from the tokens as given, and id of position i goes to
+// ids[off[w] + off[w+1] - 1 - i] (w = wid[i]); with id16, also id + 1 as u16
+// when K <= 65,534 (*id16_ok says whether it was written).
+struct IdsMirror {
+  const i64 *off;
+  const i32 *wid;
+  u32 *slots;             // n scratch words
+  unsigned short *id16;   // or nullptr
+  bool id16_ok = false;
+};
 i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scratch, cudaStream_t s,
-                    const u64 **dkeys = nullptr, i64 *dk_n = nullptr, bool *dk_max = nullptr);
+                    const u64 **dkeys = nullptr, i64 *dk_n = nullptr, bool *dk_max = nullptr,
+                    IdsMirror *mir = nullptr);
 // K9: per-window on-chip suffix array + LCP (windows <= 16,384 ops, not
 // generalized): one CTA per window, a level scratch per SM id.
 bool window_sa_supported(const Batch &b);
 size_t window_sa_scratch_bytes(int nsmid);
 int query_nsmid(int device);
 void run_window_sa(Ctx &c, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s);
-void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s);
+void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s,
+              IdsMirror *mir = nullptr);
+// build_sa of the REVERSED windows of tok (K9 path only) without reversing
+// the tokens: the dense ids are mirrored.  false (nothing done) when the
+// ids cannot be formed (vocabulary over the table budget) or K9 does not apply.
+bool build_sa_mirrored(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s,
+                       IdsMirror &mir);
 
 // ----- candidate generation, ordering, greedy, output (K5-K8) -----
 struct SelWork {

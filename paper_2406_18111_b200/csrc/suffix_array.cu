@@ -287,7 +287,23 @@ void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp, int nsmid) {
   }
 }
 
-void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s) {
+bool build_sa_mirrored(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s,
+                       IdsMirror &mir) {
+  if (w.rw == nullptr || b.N == 0) return false;  // K9 path only
+  w.ids_valid = false;
+  w.unit = 1;
+  w.R = 0;
+  w.dkeys = nullptr;
+  const i64 K = dense_token_ids(c, tok, b.N, w.ids, w.ht_cap, w.ht_scratch, s, &w.dkeys, &w.dk_n, &w.dk_max, &mir);
+  if (K < 0) return false;
+  w.ids_valid = true;
+  w.K = K;
+  run_window_sa(c, b, w, want_lcp, s);
+  return true;
+}
+
+void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, cudaStream_t s, IdsMirror *mir) {
+  (void)mir;
   const i64 N = b.N;
   const int T = 256;
   const int G = grid_for(N, T);

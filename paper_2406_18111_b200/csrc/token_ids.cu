@@ -86,6 +86,18 @@ __global__ void k_ids_from_slots(u32 *__restrict__ ids, i64 n, const u32 *__rest
   if (i < n) ids[i] = slot_rank[ids[i]];
 }
 
+__global__ void k_ids_mirror(const u32 *__restrict__ slots, i64 n, const u32 *__restrict__ slot_rank,
+                             const i64 *__restrict__ off, const i32 *__restrict__ wid, u32 *__restrict__ ids,
+                             unsigned short *__restrict__ id16) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int w = wid[i];
+  const i64 j = off[w] + off[w + 1] - 1 - i;
+  const u32 id = slot_rank[slots[i]];
+  ids[j] = id;
+  if (id16 != nullptr) id16[j] = (unsigned short)(id + 1u);
+}
+
 }  // namespace
 
 size_t token_ids_scratch_bytes(i64 n, u32 cap) {
@@ -106,7 +118,7 @@ size_t token_ids_scratch_bytes(i64 n, u32 cap) {
 // tokens were found (ids are then undefined).  `scratch` must hold
 // token_ids_scratch_bytes(n, cap) bytes.
 i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scratch, cudaStream_t s,
-                    const u64 **dkeys, i64 *dk_n, bool *dk_max) {
+                    const u64 **dkeys, i64 *dk_n, bool *dk_max, IdsMirror *mir) {
   Carver cv(scratch);
   u64 *table = cv.take<u64>(cap);
   u32 *slot_rank = cv.take<u32>(cap + 1);
@@ -116,7 +128,8 @@ i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scra
   i64 *tot = cv.take<i64>(2);
   APO_CUDA(cudaMemsetAsync(table, 0xff, sizeof(u64) * cap, s));
   APO_CUDA(cudaMemsetAsync(cnt, 0, sizeof(u32) * 8, s));
-  k_ht_insert<<<grid_for(n, 256), 256, 0, s>>>(tok, n, table, cap, ids, cnt, cnt + 1);
+  u32 *slots = mir ? mir->slots : ids;  // table slot of every position
+  k_ht_insert<<<grid_for(n, 256), 256, 0, s>>>(tok, n, table, cap, slots, cnt, cnt + 1);
   APO_CHECK_LAUNCH();
   c.launches++;
   u32 hv[3];
@@ -146,7 +159,13 @@ i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scra
     c.h2d(slot_rank + cap, &r, sizeof(u32), s);
     ++K;
   }
-  k_ids_from_slots<<<grid_for(n, 256), 256, 0, s>>>(ids, n, slot_rank);
+  if (mir) {
+    mir->id16_ok = mir->id16 != nullptr && K >= 1 && K <= 65534;
+    k_ids_mirror<<<grid_for(n, 256), 256, 0, s>>>(slots, n, slot_rank, mir->off, mir->wid, ids,
+                                                 mir->id16_ok ? mir->id16 : nullptr);
+  } else {
+    k_ids_from_slots<<<grid_for(n, 256), 256, 0, s>>>(ids, n, slot_rank);
+  }
   APO_CHECK_LAUNCH();
   c.launches++;
   APO_CUDA(cudaStreamSynchronize(s));  // `r` above lives on the host stack

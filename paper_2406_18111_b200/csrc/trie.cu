@@ -862,10 +862,6 @@ constexpr int kSMIPad = 256;    // zero entries past the stream end (a trip read
 constexpr int kSMICache = 128;  // leading trace ids per warp kept in shared memory
 constexpr u32 kTraceEnd = 0xffffffffu;
 
-__global__ void k_stream_id16(const u32 *__restrict__ ids, i64 n, unsigned short *__restrict__ out) {
-  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = (unsigned short)(ids[i] + 1u);
-}
 
 // Open-addressing table of the batch dictionary dk[0..K0) (sorted distinct
 // tokens except ~0): key -> rank, for k_trace_ids.  `mask` + 1 slots, at most
@@ -2180,6 +2176,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       const i64 *p_off;
       const i32 *p_wid, *p_sa, *p_lcp;
       const u64 *mtok, *stok;
+      bool d_rs_used = false;  // the reversed token copy exists (raw-token paths)
       const u32 *sord;
       i64 E;
       // dense-id matcher (k_stream_match_ids): stream ids + the batch dictionary
@@ -2238,17 +2235,22 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       Carver cv(c.arena.base);
       plan(cv);
       upload_batch(c, b, g, h_s, s);
-      if (rev) {
+      // the reversed streams' suffix arrays: K9 over MIRRORED dense ids (no
+      // reversed token copy); the reversed tokens are materialised only
+      // for the raw-token paths (vocabulary over 65,534 or no dense ids)
+      bool mirrored = false;
+      IdsMirror mir{g.d_off, g.d_wid, reinterpret_cast<u32 *>(g.sa.vals), sid16};
+      if (rev) mirrored = build_sa_mirrored(c, d_streams, b, g.sa, true, s, mir);
+      const bool ids16 = mirrored && mir.id16_ok && g.sa.dkeys;
+      if (rev && !ids16) {
         k_reverse_by_wid<<<grid_for(Ns, T256), T256, 0, s>>>(d_streams, g.d_off, g.d_wid, Ns, d_rs);
         APO_CHECK_LAUNCH();
         c.launches++;
       }
-      mtok = rev ? d_rs : d_streams;
-      build_sa(c, mtok, b, g.sa, true, s);
-      if (rev && g.sa.ids_valid && g.sa.K >= 1 && g.sa.K <= 65534 && g.sa.dkeys) {
-        k_stream_id16<<<grid_for(Ns, T256), T256, 0, s>>>(g.sa.ids, Ns, sid16);
-        APO_CHECK_LAUNCH();
-        c.launches++;
+      mtok = rev ? (ids16 ? nullptr : d_rs) : d_streams;
+      d_rs_used = rev && !ids16;
+      if (!mirrored) build_sa(c, mtok, b, g.sa, true, s);
+      if (ids16) {
         p_sid = sid16;
         p_dk = g.sa.dkeys;
         p_dkn = g.sa.dk_n;
@@ -2291,7 +2293,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
           x.d_wid = k.take<i32>(size_t(Ns));
           x.sa = k.take<i32>(size_t(Ns));
           x.lcp = k.take<i32>(size_t(Ns));
-          x.rs = rev ? k.take<u64>(size_t(Ns)) : nullptr;
+          x.rs = (rev && d_rs_used) ? k.take<u64>(size_t(Ns)) : nullptr;
           x.stok = k.take<u64>(size_t(std::max<i64>(E, 1)));
           x.sord = k.take<u32>(size_t(std::max<i64>(E, 1)));
           x.e_lo = k.take<u32>(size_t(std::max<i64>(E, 1)));
@@ -2312,7 +2314,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
         cp(x.d_wid, g.d_wid, sizeof(i32) * size_t(Ns));
         cp(x.sa, g.sa.sa, sizeof(i32) * size_t(Ns));
         cp(x.lcp, g.sa.lcp, sizeof(i32) * size_t(Ns));
-        if (rev) cp(x.rs, d_rs, sizeof(u64) * size_t(Ns));
+        if (x.rs) cp(x.rs, d_rs, sizeof(u64) * size_t(Ns));
         cp(x.stok, stok, sizeof(u64) * size_t(E));
         cp(x.sord, sord, sizeof(u32) * size_t(E));
         cp(x.e_lo, e_lo, sizeof(u32) * size_t(E));

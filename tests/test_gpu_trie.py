@@ -433,3 +433,34 @@ def test_match_large_vocabulary_raw_token_path(ctx):
     hits = ctx.match(trie, dev(sflat), soff).cpu().numpy()
     want, cnt = oracle.match_brute(sflat, soff, gt.cpu().numpy(), go)
     assert cnt == len(hits) and np.array_equal(hits, want) and cnt >= 300
+
+
+def test_match_vocabulary_over_id_table_budget(ctx):
+    """A stream batch with more distinct tokens than the dense-id table holds
+    (~1.6 M distinct in 100 streams of 16,384): no dense ids, the matcher
+    reverses the raw tokens and runs K9 from the 64-bit level-0 sort; mode 0
+    and mode 1 against the oracle."""
+    lens = [16384] * 100
+    streams = [gen.random_string(3000 + q, n, 1 << 62) for q, n in enumerate(lens)]
+    rng = gen.Rng(97)
+    traces = set()
+    for j in range(300):
+        s = streams[rng.below(len(streams))]
+        a = rng.below(len(s) - 40)
+        traces.add(tuple(int(x) for x in s[a:a + 1 + rng.below(30)]))
+    traces = sorted(traces, key=lambda t: (-len(t), t))
+    tt = np.array([x for t in traces for x in t], dtype=np.uint64)
+    to = np.cumsum([0] + [len(t) for t in traces]).astype(np.int64)
+    trie = ctx.trie_build_traces(dev(tt), to)
+    gt, go = trie.traces()
+    sflat = np.concatenate(streams)
+    soff = np.cumsum([0] + lens).astype(np.int64)
+    hits = ctx.match(trie, dev(sflat), soff).cpu().numpy()
+    want, cnt = oracle.match_brute(sflat, soff, gt.cpu().numpy(), go)
+    assert cnt == len(hits) and np.array_equal(hits, want) and cnt >= 300
+    rp, nall = ctx.match(trie, dev(sflat), soff, mode=1)
+    tlen = np.diff(go)
+    want_rp = oracle.replay(want, tlen)
+    g = rp.cpu().numpy().astype(np.int64)
+    got_rp = np.stack([g[:, 0], g[:, 1] - tlen[g[:, 2]] + 1, g[:, 1], g[:, 2], g[:, 3]], axis=1)
+    assert nall == cnt and np.array_equal(got_rp, want_rp)
