@@ -624,13 +624,24 @@ __global__ void __launch_bounds__(kGreedyWarps * 32) k_greedy_window(Batch b, co
   }
   __syncwarp();
   u32 nk = 0;
+  // the next two batches' (length, start) are in flight while one is decided
+  auto fetch = [&](i64 q, i32 &l, i32 &st) {
+    l = 0;
+    st = 0;
+    if (q < c1) {
+      l = cl[q];
+      st = i32(cs[q] - beg);
+    }
+  };
+  i32 l1, s1, l2, s2;
+  fetch(c0 + lane, l1, s1);
+  fetch(c0 + 32 + lane, l2, s2);
   for (i64 base = c0; base < c1; base += 32) {
     const i64 my = base + lane;
-    i32 ml = 0, ms = 0;
-    if (my < c1) {
-      ml = cl[my];
-      ms = i32(cs[my] - beg);
-    }
+    const i32 ml = l1, ms = s1;
+    l1 = l2;
+    s1 = s2;
+    fetch(base + 64 + lane, l2, s2);
     // marks only grow, so a candidate whose end bits are already set now is
     // rejected whatever the earlier candidates of this batch do: only the
     // survivors of this parallel pre-check are walked in order
@@ -697,29 +708,40 @@ __global__ void k_kept_compact(const u32 *__restrict__ kwin, const u32 *__restri
   for (u32 j = threadIdx.x; j < n; j += blockDim.x) klist[b + j] = kwin[w * kcap + j];
 }
 
-// K8 over the compact kept list: group counts and first kept candidate
-__global__ void k_gstats_kept(const u32 *__restrict__ klist, i64 K, const i32 *__restrict__ cg,
-                              u32 *__restrict__ gcnt, u32 *__restrict__ gfirst) {
-  const i64 k = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= K) return;
-  const u32 c = klist[k];
-  const i32 g = cg[c];
-  atomicAdd(&gcnt[g], 1u);
-  atomicMin(&gfirst[g], c);
+// K8 over the compact kept list without per-group tables: the kept
+// candidates are in candidate order, where a sub-string group's members are
+// contiguous, so a group's kept members form one run of the list -- its
+// count is the run's length and its first occurrence the run's head.
+struct KeptRunF {  // run ordinal of every kept candidate; each run's first index
+  const u32 *klist;
+  const i32 *cg;
+  u32 *rid, *hpos;
+  i64 K;
+  i64 *total;
+  __device__ u32 load(i64 k) const { return (k == 0 || cg[klist[k]] != cg[klist[k - 1]]) ? 1u : 0u; }
+  __device__ bool store(i64 k, u32 incl, u32 excl) const {
+    rid[k] = incl - 1;
+    if (incl != excl) hpos[excl] = u32(k);
+    if (k == K - 1) *total = i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+__device__ __forceinline__ u32 run_len(const u32 *hpos, i64 R, i64 K, u32 r) {
+  return u32((i64(r) + 1 < R ? i64(hpos[r + 1]) : K) - i64(hpos[r]));
 }
 
-// occurrence list over the kept candidates in candidate order
-struct OccKeptF {
-  const u32 *klist;
+struct OccRunF {  // occurrence list over the kept candidates of runs with count >= minc
+  const u32 *klist, *rid, *hpos;
+  i64 R, K;
   const i32 *cg, *cs, *gbase;
-  const u32 *gcnt;
   u32 minc;
   u32 *oidx;
   i32 *occ;
   i64 occ_cap;
-  i64 K;
   i64 *total;
-  __device__ u32 load(i64 k) const { return gcnt[cg[klist[k]]] >= minc ? 1u : 0u; }
+  __device__ u32 load(i64 k) const { return run_len(hpos, R, K, rid[k]) >= minc ? 1u : 0u; }
   __device__ bool store(i64 k, u32 incl, u32 excl) const {
     if (incl != excl) {
       const u32 c = klist[k];
@@ -727,6 +749,37 @@ struct OccKeptF {
       if (occ != nullptr && i64(excl) < occ_cap) occ[excl] = cs[c] - gbase[cg[c]];  // window-local start
     }
     if (k == K - 1) *total = i64(incl);
+    return false;
+  }
+  __device__ u32 *flag() const { return nullptr; }
+};
+
+struct RepRunF {  // one repeat per run with count >= minc, in run (= group) order
+  const u32 *klist, *hpos;
+  i64 R, K;
+  const i32 *cg, *cs, *glen, *gbase, *gwin;
+  const u32 *oidx;
+  u32 minc;
+  apo_repeat *out;
+  i64 cap;
+  u32 *wcnt;
+  i64 *total;
+  __device__ u32 load(i64 r) const { return run_len(hpos, R, K, u32(r)) >= minc ? 1u : 0u; }
+  __device__ bool store(i64 r, u32 incl, u32 excl) const {
+    if (incl != excl) {
+      const u32 c0 = klist[hpos[r]];
+      const i32 g = cg[c0];
+      if (i64(excl) < cap && out != nullptr) {
+        apo_repeat rr;
+        rr.start = i32(cs[c0] - gbase[g]);
+        rr.length = glen[g];
+        rr.count = i32(run_len(hpos, R, K, u32(r)));
+        rr.first_occ = i32(oidx[c0]);
+        out[excl] = rr;
+      }
+      atomicAdd(&wcnt[gwin[g]], 1u);
+    }
+    if (r == R - 1) *total = i64(incl);
     return false;
   }
   __device__ u32 *flag() const { return nullptr; }
@@ -915,19 +968,26 @@ void emit_repeats(Ctx &c, const Batch &b, SelWork &w, int min_count, apo_repeat 
   const i64 m = w.m, G = w.G;
   APO_CUDA(cudaMemsetAsync(counts, 0, sizeof(i64) * 2, s));
   APO_CUDA(cudaMemsetAsync(w.wcnt, 0, sizeof(u32) * (b.W + 1), s));
-  if (m > 0) {
+  if (m > 0 && w.K >= 0) {
+    // the per-window greedy's compact kept list: runs of equal groups
+    const u32 minc = u32(min_count < 1 ? 1 : min_count);
+    const i64 K = w.K;
+    if (K > 0) {
+      u32 *rid = w.gcnt, *hpos = w.gfirst;  // (per-group tables are not needed here)
+      i64 *R_dev = reinterpret_cast<i64 *>(w.scal + 6);
+      KeptRunF kr{w.klist, w.cg, rid, hpos, K, R_dev};
+      launch_scan<false>(c, K, kr, s);
+      const i64 R = i64(c.read_u64(w.scal + 6, s));
+      OccRunF of{w.klist, rid, hpos, R, K, w.cg, w.cs, w.gbase, minc, w.oidx, occ, occ_cap, counts + 1};
+      launch_scan<false>(c, K, of, s);
+      RepRunF rf{w.klist, hpos, R, K, w.cg, w.cs, w.glen, w.gbase, w.gwin, w.oidx, minc, out, cap, w.wcnt, counts};
+      launch_scan<false>(c, R, rf, s);
+    }
+  } else if (m > 0) {
     APO_CUDA(cudaMemsetAsync(w.gcnt, 0, sizeof(u32) * G, s));
     APO_CUDA(cudaMemsetAsync(w.gfirst, 0xff, sizeof(u32) * G, s));
     const u32 minc = u32(min_count < 1 ? 1 : min_count);
-    if (w.K >= 0) {  // the per-window greedy's compact kept list: K entries instead of m
-      if (w.K > 0) {
-        k_gstats_kept<<<grid_for(w.K, T), T, 0, s>>>(w.klist, w.K, w.cg, w.gcnt, w.gfirst);
-        APO_CHECK_LAUNCH();
-        c.launches++;
-        OccKeptF of{w.klist, w.cg, w.cs, w.gbase, w.gcnt, minc, w.oidx, occ, occ_cap, w.K, counts + 1};
-        launch_scan<false>(c, w.K, of, s);
-      }
-    } else {
+    {
       k_gstats<<<grid_for(m, T), T, 0, s>>>(w.cg, w.state, m, w.gcnt, w.gfirst);
       APO_CHECK_LAUNCH();
       c.launches++;
