@@ -50,6 +50,7 @@ struct SAWork {
   const u64 *dkeys = nullptr;  // their sorted values except ~0 (dk_n of them; in ht_scratch)
   i64 dk_n = 0;
   bool dk_max = false;    // the token ~0 occurs (id dk_n)
+  const u32 *slot_rank = nullptr;  // set: ids[] holds table slots, id = slot_rank[slot] (K9 maps them)
   // results
   i32 *sa;                // N (global positions, window-major suffix order)
   i32 *lcp;               // N (pair k = (k, k+1); 0 at the end of each window)
@@ -74,7 +75,7 @@ struct IdsMirror {
 };
 i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scratch, cudaStream_t s,
                     const u64 **dkeys = nullptr, i64 *dk_n = nullptr, bool *dk_max = nullptr,
-                    IdsMirror *mir = nullptr);
+                    IdsMirror *mir = nullptr, const u32 **slots_only = nullptr);
 // K9: per-window on-chip suffix array + LCP (windows <= 16,384 ops, not
 // generalized): one CTA per window, a level scratch per SM id.
 bool window_sa_supported(const Batch &b);

@@ -294,6 +294,7 @@ bool build_sa_mirrored(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool w
   w.unit = 1;
   w.R = 0;
   w.dkeys = nullptr;
+  w.slot_rank = nullptr;
   const i64 K = dense_token_ids(c, tok, b.N, w.ids, w.ht_cap, w.ht_scratch, s, &w.dkeys, &w.dk_n, &w.dk_max, &mir);
   if (K < 0) return false;
   w.ids_valid = true;
@@ -319,9 +320,12 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   w.unit = 1;
   w.K = -1;
   w.dkeys = nullptr;
+  w.slot_rank = nullptr;
   i64 packK = -1;
   if (b.gen || b.W == 1 || w.rw != nullptr) {
-    const i64 K = dense_token_ids(c, tok, N, w.ids, w.ht_cap, w.ht_scratch, s, &w.dkeys, &w.dk_n, &w.dk_max);
+    // K9 maps table slots to ids itself (w.slot_rank); others need the ids
+    const i64 K = dense_token_ids(c, tok, N, w.ids, w.ht_cap, w.ht_scratch, s, &w.dkeys, &w.dk_n, &w.dk_max,
+                                  nullptr, w.rw != nullptr ? &w.slot_rank : nullptr);
     if (K >= 0) {
       w.ids_valid = true;
       w.K = K;

@@ -118,7 +118,7 @@ size_t token_ids_scratch_bytes(i64 n, u32 cap) {
 // tokens were found (ids are then undefined).  `scratch` must hold
 // token_ids_scratch_bytes(n, cap) bytes.
 i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scratch, cudaStream_t s,
-                    const u64 **dkeys, i64 *dk_n, bool *dk_max, IdsMirror *mir) {
+                    const u64 **dkeys, i64 *dk_n, bool *dk_max, IdsMirror *mir, const u32 **slots_only) {
   Carver cv(scratch);
   u64 *table = cv.take<u64>(cap);
   u32 *slot_rank = cv.take<u32>(cap + 1);
@@ -158,6 +158,12 @@ i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scra
     const u32 r = u32(K);
     c.h2d(slot_rank + cap, &r, sizeof(u32), s);
     ++K;
+  }
+  if (slots_only != nullptr && mir == nullptr) {
+    // the caller maps slots itself (K9's level-0 load): ids[] keeps the slots
+    *slots_only = slot_rank;
+    APO_CUDA(cudaStreamSynchronize(s));  // `r` above lives on the host stack
+    return K;
   }
   if (mir) {
     mir->id16_ok = mir->id16 != nullptr && K >= 1 && K <= 65534;

@@ -360,7 +360,8 @@ __global__ void k_nsmid(int *out) {
 // ids: global dense order-preserving token ids (K2), or nullptr: level 0
 // from level0 (global group starts of the (window, token) order).
 __global__ void __launch_bounds__(kWT, 1)
-    k_window_sa(Batch b, const u32 *__restrict__ ids, const i32 *__restrict__ level0, u16 *__restrict__ scratch,
+    k_window_sa(Batch b, const u32 *__restrict__ ids, const u32 *__restrict__ slot_rank,
+                const i32 *__restrict__ level0, u16 *__restrict__ scratch,
                 u32 nslots, u32 *__restrict__ next_win, i32 *__restrict__ sa_out, i32 *__restrict__ lcp_out,
                 i32 *__restrict__ rw) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -396,18 +397,26 @@ __global__ void __launch_bounds__(kWT, 1)
     // ---------------- level 0: sort the window by token ----------------
     if (ids != nullptr) {
       // keys ping-pong X <-> Y, positions ping-pong rank <-> nsk
+      // ids[] holds K2's table slots when slot_rank is given (the id is
+      // slot_rank[slot]: no separate id pass over the batch)
       u32 mx = 0;
-      for (int q = tid; q < n; q += kWT) mx = max(mx, ids[beg + q]);
-      mx = __reduce_max_sync(0xffffffffu, mx);
       if (tid == 0) S.misc[1] = 0;
+      for (int q = tid; q < n; q += kWT) {
+        u32 v = ids[beg + q];
+        if (slot_rank != nullptr) v = __ldg(&slot_rank[v]);
+        S.X[q] = v;
+        S.rank[q] = u16(q);
+        mx = max(mx, v);
+      }
+      mx = __reduce_max_sync(0xffffffffu, mx);
       __syncthreads();
       if (lane == 0) atomicMax(reinterpret_cast<u32 *>(&S.misc[1]), mx);
       __syncthreads();
       const int kv = max(bits_for(u64(u32(S.misc[1]))), 1);
       const int kb = kv + (n < kWMax ? 1 : 0);  // pad slots (key 2^kv, above every id) need one more bit
       const u32 pad = 1u << kv;
-      for (int q = tid; q < kWMax; q += kWT) {
-        S.X[q] = q < n ? ids[beg + q] : pad;
+      for (int q = n + tid; q < kWMax; q += kWT) {
+        S.X[q] = pad;
         S.rank[q] = u16(q);
       }
       __syncthreads();
@@ -604,7 +613,8 @@ void run_window_sa(Ctx &c, const Batch &b, SAWork &w, bool want_lcp, cudaStream_
   // window: no per-window CTA launch and teardown)
   const int grid = int(std::min<i64>(b.W, c.num_sms));
   u32 *ctr = c.take_counter(s);
-  k_window_sa<<<grid, kWT, smem, s>>>(b, w.ids_valid ? w.ids : nullptr, w.levels[0],
+  k_window_sa<<<grid, kWT, smem, s>>>(b, w.ids_valid ? w.ids : nullptr, w.ids_valid ? w.slot_rank : nullptr,
+                                      w.levels[0],
                                       reinterpret_cast<u16 *>(w.win_scratch), u32(c.nsmid), ctr, w.sa,
                                       want_lcp ? w.lcp : nullptr, w.rw);
   APO_CHECK_LAUNCH();
