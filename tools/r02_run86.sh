@@ -1,0 +1,10 @@
+mkdir -p gpurun_out
+python -c "from paper_2406_18111_b200 import build; build.build()" > gpurun_out/r02_build.log 2>&1; echo "build rc=$?"
+timeout 1500 python -m pytest tests -q -m gpu -x > gpurun_out/r02_pytest_86.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/r02_pytest_86.log
+for C in C3 C2 C5; do timeout 600 python bench.py --config $C --steps 10 --warmup 3 --no-e2e --cpu-budget 0.1 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$C', round(d['value']/1e6,1), round(d['ms_per_step'],3))"; done
+timeout 900 python bench.py --cpu-budget 2 --no-c3 > gpurun_out/r02_bench86.json 2> gpurun_out/r02_bench86.err; echo "bench rc=$?"
+python - <<'PY'
+import json
+d=json.loads(open('gpurun_out/r02_bench86.json').read().strip().splitlines()[-1])
+print('value', d['value']/1e6, 'ms', d['ms_per_step'], 'e2e', d['e2e']['value']/1e6, 'cfg', {k: d['config'].get(k) for k in ('stage_ms_per_step',)})
+PY
