@@ -458,6 +458,22 @@ __global__ void k_pull(const u32 *__restrict__ up, u32 *__restrict__ down, i64 n
   if (v < down[y]) down[y] = v;
 }
 
+// two levels of the pull-down in one pass: level q-2 from levels q-1 and q
+// (level q-1's pulled value at y is min(up1[y], up2[y], up2[y - h1]))
+__global__ void k_pull2(const u32 *__restrict__ up2, const u32 *__restrict__ up1, u32 *__restrict__ down, i64 n,
+                        i64 h1, i64 h2) {
+  const i64 y = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (y >= n) return;
+  auto lvl1 = [&](i64 x) -> u32 {
+    u32 v = min(up1[x], up2[x]);
+    if (x >= h1) v = min(v, up2[x - h1]);
+    return v;
+  };
+  u32 v = min(down[y], lvl1(y));
+  if (y >= h2) v = min(v, lvl1(y - h2));
+  down[y] = v;
+}
+
 __global__ void k_select(const i32 *__restrict__ cl, const i32 *__restrict__ cs, u8 *__restrict__ state, i64 m,
                          const u32 *__restrict__ first, u32 *__restrict__ diff) {
   i64 c = i64(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -944,11 +960,19 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
   const int gm = grid_for(m, T), gn = grid_for(N, T);
   for (int round = 0;; ++round) {
     if (round > 100000) throw Error{APO_ERR_CUDA, "greedy selection did not converge"};
-    for (int q = 0; q < w.tab_levels; ++q) APO_CUDA(cudaMemsetAsync(w.tab[q], 0xff, sizeof(u32) * N, s));
+    // the levels are consecutive carves: one fill for all of them
+    const size_t tab_bytes = size_t(reinterpret_cast<char *>(w.tab[w.tab_levels - 1] + N) -
+                                    reinterpret_cast<char *>(w.tab[0]));
+    APO_CUDA(cudaMemsetAsync(w.tab[0], 0xff, tab_bytes, s));
     k_mark<<<gm, T, 0, s>>>(w.cl, w.cs, w.state, m, tab);
     APO_CHECK_LAUNCH();
-    for (int q = w.tab_levels - 1; q >= 1; --q) {
-      k_pull<<<gn, T, 0, s>>>(w.tab[q], w.tab[q - 1], N, i64(1) << (q - 1));
+    int q = w.tab_levels - 1;
+    for (; q >= 2; q -= 2) {
+      k_pull2<<<gn, T, 0, s>>>(w.tab[q], w.tab[q - 1], w.tab[q - 2], N, i64(1) << (q - 1), i64(1) << (q - 2));
+      APO_CHECK_LAUNCH();
+    }
+    if (q == 1) {
+      k_pull<<<gn, T, 0, s>>>(w.tab[1], w.tab[0], N, 1);
       APO_CHECK_LAUNCH();
     }
     k_select<<<gm, T, 0, s>>>(w.cl, w.cs, w.state, m, w.tab[0], w.diff);
@@ -958,7 +982,7 @@ void select_candidates(Ctx &c, const u64 *tok, const Batch &b, const SAWork &sa,
     APO_CUDA(cudaMemsetAsync(undecided, 0, sizeof(u32), s));
     k_reject<<<gm, T, 0, s>>>(w.cl, w.cs, w.state, m, w.cov, undecided);
     APO_CHECK_LAUNCH();
-    c.launches += 3 + (w.tab_levels - 1);
+    c.launches += 3 + w.tab_levels / 2;
     if (c.read_u32(undecided, s) == 0) break;
   }
 }
