@@ -328,13 +328,19 @@ __device__ __forceinline__ int groups_phase(Smem &S, const u32 *ord, int n) {
 
 // Equal level-r ranks <=> equal 2^r-token prefixes: greedy descent over the
 // levels from a known lower bound l of lcp(i, j), valid because
-// lcp(i, j) - l < 2^R (level R is all distinct).
-__device__ __forceinline__ int gallop(const u16 *__restrict__ lv, int R, int n, int i, int j, int l) {
-  for (int r = R - 1; r >= 0; --r) {
+// lcp(i, j) - l < 2^R (level R is all distinct).  Levels 1 .. kLvlSkip-1 are
+// not kept (less scratch traffic): below level kLvlSkip the last < 2^kLvlSkip
+// tokens are compared directly on the level-0 ranks in shared memory.
+constexpr int kLvlSkip = 4;
+
+__device__ __forceinline__ int gallop(const u16 *__restrict__ lv, const u16 *__restrict__ tok0, int R, int n, int i,
+                                      int j, int l) {
+  for (int r = R - 1; r >= kLvlSkip; --r) {
     if (i + l >= n || j + l >= n) break;
     const u16 *L = lv + size_t(r) * kWMax;
     if (__ldcg(L + i + l) == __ldcg(L + j + l)) l += 1 << r;
   }
+  while (i + l < n && j + l < n && tok0[i + l] == tok0[j + l]) ++l;  // < 2^kLvlSkip steps
   return l;
 }
 
@@ -463,7 +469,8 @@ __global__ void __launch_bounds__(kWT, 1)
         break;
       }
       // level r (prefix length h = 2^r) to the scratch for the LCP stage
-      {
+      // (levels 1 .. kLvlSkip-1 are not needed: see gallop)
+      if (r == 0 || r >= kLvlSkip) {
         const u32 *src = reinterpret_cast<const u32 *>(S.rank);
         u32 *dst = reinterpret_cast<u32 *>(lv + size_t(r) * kWMax);
         for (int q = tid; q < kWMax / 2; q += kWT) __stcg(dst + q, src[q]);
@@ -559,14 +566,14 @@ __global__ void __launch_bounds__(kWT, 1)
         if (R == 0) {
           l = 0;  // all first tokens distinct
         } else if (l < 0) {
-          l = gallop(lv, R, n, i, j, 0);
+          l = gallop(lv, tok0, R, n, i, j, 0);
         } else {
           l = l > 0 ? l - 1 : 0;
           int steps = 0;
           while (i + l < n && j + l < n && tok0[i + l] == tok0[j + l]) {
             ++l;
             if (++steps == kKasaiSteps) {
-              l = gallop(lv, R, n, i, j, l);
+              l = gallop(lv, tok0, R, n, i, j, l);
               break;
             }
           }
