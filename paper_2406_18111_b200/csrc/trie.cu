@@ -359,14 +359,16 @@ __global__ void __launch_bounds__(kBkThreads) k_stream_buckets(StreamMatch m, co
                                                               u64 *__restrict__ e_tok, u32 *__restrict__ e_lo,
                                                               u32 *__restrict__ e_q, u32 *__restrict__ e_hi,
                                                               u32 *__restrict__ e_idx, i64 *__restrict__ total,
-                                                              int W, u64 *status, u32 *counter, u32 epoch) {
+                                                              int W, u64 *status, u32 *counter, u32 epoch,
+                                                              int depth) {
   __shared__ u32 s_w, s_base, s_wsum[kBkThreads / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_w = atomicAdd(counter, 1u);
   __syncthreads();
   const int w = int(s_w);
   const i64 beg = m.off[w], n = m.off[w + 1] - beg;
-  auto head = [&](i64 r) -> u32 { return (r == 0 || m.lcp[beg + r - 1] == 0) ? 1u : 0u; };
+  // depth 1: a bucket per first token; depth 2 (ids): per first two tokens
+  auto head = [&](i64 r) -> u32 { return (r == 0 || m.lcp[beg + r - 1] < depth) ? 1u : 0u; };
   u32 cnt = 0;
   for (i64 r = tid; r < n; r += kBkThreads) cnt += head(r);
   cnt = __reduce_add_sync(0xffffffffu, cnt);
@@ -425,7 +427,10 @@ __global__ void __launch_bounds__(kBkThreads) k_stream_buckets(StreamMatch m, co
       bits &= bits - 1;
       const i64 k = beg + r0 + j;
       const i64 p = m.sa[k];
-      e_tok[o] = sid ? u64(sid[p]) : m.tok[p];
+      if (depth == 2)  // (id0 + 1, id1 + 1 or 0 past the stream end)
+        e_tok[o] = (u64(sid[p]) << 17) | u64(p + 1 < beg + n ? sid[p + 1] : 0u);
+      else
+        e_tok[o] = sid ? u64(sid[p]) : m.tok[p];
       e_lo[o] = u32(k);
       e_q[o] = u32(w);
       e_idx[o] = o;
@@ -443,18 +448,19 @@ __global__ void __launch_bounds__(kBkThreads) k_stream_buckets(StreamMatch m, co
 
 // per trace: range [ea, eb) of token-sorted buckets with the trace's first token
 __global__ void k_trace_buckets(StreamMatch m, const u64 *__restrict__ sorted_tok, i64 E, u32 *__restrict__ ea,
-                                u32 *__restrict__ ecnt, const u32 *__restrict__ tid) {
+                                u32 *__restrict__ ecnt, const u32 *__restrict__ tid, int depth) {
   const i64 t = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= m.T) return;
   u64 a;
   if (tid != nullptr) {  // buckets keyed by dense id + 1; a token absent from the batch has none
     const u32 x = tid[m.toff[t]];
-    if (x & 1u) {
+    const u32 y = depth == 2 ? tid[m.toff[t] + 1] : 0u;  // (traces are >= 2 long at depth 2)
+    if ((x | y) & 1u) {
       ea[t] = 0;
       ecnt[t] = 0;
       return;
     }
-    a = u64(x >> 1);
+    a = depth == 2 ? (u64(x >> 1) << 17) | u64(y >> 1) : u64(x >> 1);
   } else {
     a = m.ttok[m.toff[t]];
   }
@@ -975,7 +981,8 @@ __global__ void __launch_bounds__(kSMIThreads, 2)
     k_stream_match_ids(const i64 *__restrict__ soff, const i32 *__restrict__ sa, const i32 *__restrict__ lcpa,
                        const unsigned short *__restrict__ sid, const u32 *__restrict__ tid,
                        const uint4 *__restrict__ meta, const u32 *__restrict__ qoff, i64 *__restrict__ ilo,
-                       u32 *__restrict__ icnt, u32 *__restrict__ qtot, const u32 *__restrict__ qorder) {
+                       u32 *__restrict__ icnt, u32 *__restrict__ qtot, const u32 *__restrict__ qorder,
+                       int depth) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ u32 s_tot, s_next;
   __shared__ unsigned short s_bmin[kSMMax / 32];
@@ -1042,12 +1049,13 @@ __global__ void __launch_bounds__(kSMIThreads, 2)
       for (int j = 0; j < kSMICache / 32; ++j) tc[32 * j + lane] = v[j];
       __syncwarp();
     }
-    // lower bound with LCP-LR skips, as in k_stream_match
-    int lo = lo0 - 1, hi = hi0, llo = 1, lhi = -1;
+    // lower bound with LCP-LR skips, as in k_stream_match; a bucket's
+    // members share the trace's first `depth` tokens
+    int lo = lo0 - 1, hi = hi0, llo = depth, lhi = -1;
     while (hi - lo > 1) {
       const int mid = lo + ((hi - lo) >> 1);
       const bool real = lo >= lo0 && lhi >= 0;
-      int st = 1;
+      int st = depth;
       if (real && llo != lhi) {
         const bool left = llo > lhi;
         const int a = left ? lo : mid, b = left ? mid : hi;
@@ -1064,7 +1072,7 @@ __global__ void __launch_bounds__(kSMIThreads, 2)
       } else if (real) {
         st = llo;
       } else if (lhi >= 0) {
-        st = 1;
+        st = depth;
       }
       int l;
       const int c = warp_cmp_ids(S, SA[mid], tc, tg, L, st, &l);
@@ -1936,6 +1944,8 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
   tr->T = T;
   tr->ntok = ntok;
   tr->maxlen = maxlen;
+  tr->minlen = T > 0 ? maxlen : 0;
+  for (i64 t = 0; t < T; ++t) tr->minlen = std::min<i64>(tr->minlen, h_uoff[t + 1] - h_uoff[t]);
   tr->h_off = std::move(h_uoff);
 }
 
@@ -2177,6 +2187,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       const i32 *p_wid, *p_sa, *p_lcp;
       const u64 *mtok, *stok;
       bool d_rs_used = false;  // the reversed token copy exists (raw-token paths)
+      int depth = 1;           // tokens keying the buckets
       const u32 *sord;
       i64 E;
       // dense-id matcher (k_stream_match_ids): stream ids + the batch dictionary
@@ -2184,12 +2195,45 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       const u64 *p_dk = nullptr;
       i64 p_dkn = 0;
       bool p_dkmax = false;
+      // the streams' buckets (one CTA per stream, look-back offsets), sorted
+      // by key; keys are ids + 1 (bits(K)), two of them at depth 2, or raw
+      // tokens (64 bits)
+      auto make_buckets = [&](const StreamMatch &smb, int dep, u64 *et, u64 *et_alt, u32 *elo, u32 *eq, u32 *ehi,
+                              u32 *eidx, u32 *eidx_alt, const u64 **out_tok, const u32 **out_ord, i64 *out_E) {
+        c.ensure_status(size_t(nstreams), s);
+        u32 *ctr = c.take_counter(s);
+        const u32 ep = c.next_epoch();
+        k_stream_buckets<<<nstreams, kBkThreads, 0, s>>>(smb, p_sid, et, elo, eq, ehi, eidx, scal, nstreams, c.status,
+                                                       ctr, ep, dep);
+        APO_CHECK_LAUNCH();
+        c.launches++;
+        const i64 En = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
+        const int idb = bits_for(u64(p_dkn + (p_dkmax ? 1 : 0)));
+        const int ebits = p_sid ? (dep == 2 ? 17 + idb : idb) : 64;
+        const bool ae = radix_sort_u64_u32(c, et, eidx, et_alt, eidx_alt, En, 0, ebits, s);
+        *out_tok = ae ? et_alt : et;
+        *out_ord = ae ? eidx_alt : eidx;
+        *out_E = En;
+        c.launches++;
+      };
+      u64 *rb_tok = nullptr, *rb_tok_alt = nullptr;  // bucket rebuild (pre index at depth 2, 1-token traces)
+      u32 *rb_lo = nullptr, *rb_q = nullptr, *rb_hi = nullptr, *rb_idx = nullptr, *rb_idx_alt = nullptr;
       if (pre) {
+        const bool rebuild = pre->depth == 2 && tr->minlen < 2;
         auto plan = [&](Carver &cv) {
           ea = cv.take<u32>(T);
           ecnt = cv.take<u32>(T);
           pbase = cv.take<u32>(T);
           scal = cv.take<i64>(4);
+          if (rebuild) {
+            rb_tok = cv.take<u64>(Ns);
+            rb_tok_alt = cv.take<u64>(Ns);
+            rb_lo = cv.take<u32>(Ns);
+            rb_q = cv.take<u32>(Ns);
+            rb_hi = cv.take<u32>(Ns);
+            rb_idx = cv.take<u32>(Ns);
+            rb_idx_alt = cv.take<u32>(Ns);
+          }
         };
         Carver dry(nullptr);
         plan(dry);
@@ -2212,6 +2256,17 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
         p_dk = pre->dk;
         p_dkn = pre->dk_n;
         p_dkmax = pre->dk_max;
+        depth = pre->depth;
+        if (depth == 2 && tr->minlen < 2) {
+          // 1-token traces: rebuild the buckets by first token only
+          u64 *rt = rb_tok, *rt_alt = rb_tok_alt;
+          StreamMatch smb{p_off, p_wid, p_sa, p_lcp, mtok, nullptr, nullptr, Ns, T};
+          depth = 1;
+          make_buckets(smb, 1, rt, rt_alt, rb_lo, rb_q, rb_hi, rb_idx, rb_idx_alt, &stok, &sord, &E);
+          e_lo = rb_lo;
+          e_q = rb_q;
+          e_hi = rb_hi;
+        }
       } else {
       auto plan = [&](Carver &cv) {
         plan_gen(cv, b, g, true, c.nsmid);
@@ -2262,22 +2317,10 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       p_lcp = g.sa.lcp;
       StreamMatch sm0{p_off, p_wid, p_sa, p_lcp, mtok, nullptr, nullptr, Ns, T};
       APO_CUDA(cudaMemsetAsync(scal, 0, sizeof(i64) * 4, s));
-      {
-        c.ensure_status(size_t(nstreams), s);
-        u32 *ctr = c.take_counter(s);
-        const u32 ep = c.next_epoch();
-        k_stream_buckets<<<nstreams, kBkThreads, 0, s>>>(sm0, p_sid, e_tok, e_lo, e_q, e_hi, e_idx, scal, nstreams,
-                                                       c.status, ctr, ep);
-        APO_CHECK_LAUNCH();
-        c.launches++;
-      }
-      E = i64(c.read_u64(reinterpret_cast<const u64 *>(scal), s));
-      // ids + 1 <= K need bits(K) bits; raw tokens all 64
-      const int ebits = p_sid ? bits_for(u64(p_dkn + (p_dkmax ? 1 : 0))) : 64;
-      bool ae = radix_sort_u64_u32(c, e_tok, e_idx, e_tok_alt, e_idx_alt, E, 0, ebits, s);
-      stok = ae ? e_tok_alt : e_tok;
-      sord = ae ? e_idx_alt : e_idx;
-      c.launches++;
+      // buckets by the first two tokens on the id path (fewer, tighter
+      // pairs), unless the trace set has 1-token traces
+      depth = (p_sid != nullptr && (build_idx != nullptr || (tr != nullptr && tr->minlen >= 2))) ? 2 : 1;
+      make_buckets(sm0, depth, e_tok, e_tok_alt, e_lo, e_q, e_hi, e_idx, e_idx_alt, &stok, &sord, &E);
       if (build_idx) {  // apo_match_index: keep the index in a pooled block
         apo_stream_index &x = *build_idx;
         x.d_streams = d_streams;
@@ -2287,6 +2330,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
         x.maxs = maxs;
         x.E = E;
         x.rev = rev;
+        x.depth = depth;
         Carver kd(nullptr);
         auto carve = [&](Carver &k) {
           x.d_off = k.take<i64>(size_t(nstreams) + 1);
@@ -2372,7 +2416,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
         tid_v = tid;
         dict_v = dict;
       }
-      k_trace_buckets<<<grid_for(T, T256), T256, 0, s>>>(sm, stok, E, ea, ecnt, tid);
+      k_trace_buckets<<<grid_for(T, T256), T256, 0, s>>>(sm, stok, E, ea, ecnt, tid, depth);
       APO_CHECK_LAUNCH();
       c.launches++;
       PairBaseF pf{ecnt, pbase, T, scal + 1};
@@ -2476,7 +2520,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
               c.smem_optin(reinterpret_cast<const void *>(k_stream_match_ids), smem);
               if (c.prof) c.prof_begin(kProfMatch, 0.0, s);
               k_stream_match_ids<<<nstreams, kSMIThreads, smem, s>>>(p_off, p_sa, p_lcp, p_sid, tid, meta, qoff, ilo,
-                                                                     icnt, qtot, qorder);
+                                                                     icnt, qtot, qorder, depth);
               APO_CHECK_LAUNCH();
               if (c.prof) c.prof_end(s);
               c.launches += 3;

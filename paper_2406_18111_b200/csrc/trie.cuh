@@ -10,6 +10,7 @@ struct apo_trie {
   apo::i64 T = 0;      // distinct traces
   apo::i64 ntok = 0;   // total tokens
   apo::i64 maxlen = 0;
+  apo::i64 minlen = 0;
   apo::u64 *d_tok = nullptr;  // traces in id order, back to back
   mutable apo::u64 *d_rtok = nullptr;  // the same traces, each reversed (built by the first apo_match)
   apo::i64 *d_off = nullptr;  // T+1
@@ -34,6 +35,7 @@ struct apo_stream_index {
   apo::i32 *d_wid = nullptr, *sa = nullptr, *lcp = nullptr;
   apo::u64 *rs = nullptr, *stok = nullptr;
   apo::u32 *sord = nullptr, *e_lo = nullptr, *e_q = nullptr, *e_hi = nullptr;
+  int depth = 1;  // tokens that key the buckets (2 on the dense-id path)
   // dense-id matcher inputs (when the batch has <= 65,534 distinct tokens)
   unsigned short *sid = nullptr;  // reversed streams' ids + 1
   apo::u64 *dk = nullptr;         // sorted distinct tokens except ~0

@@ -464,3 +464,34 @@ def test_match_vocabulary_over_id_table_budget(ctx):
     g = rp.cpu().numpy().astype(np.int64)
     got_rp = np.stack([g[:, 0], g[:, 1] - tlen[g[:, 2]] + 1, g[:, 1], g[:, 2], g[:, 3]], axis=1)
     assert nall == cnt and np.array_equal(got_rp, want_rp)
+
+
+def test_match_indexed_one_token_traces():
+    """A stream index keys its buckets by the first two tokens; a trace set
+    with 1-token traces makes the search rebuild them by the first token:
+    match_indexed == match == the oracle, both modes."""
+    from paper_2406_18111_b200 import Context
+    ctx = Context(0)
+    streams = [gen.random_string(700 + q, 3000 + 17 * q, 40) for q in range(6)]
+    st = np.concatenate(streams)
+    so = np.cumsum([0] + [len(x) for x in streams]).astype(np.int64)
+    ds = torch.from_numpy(st).cuda()
+    idx = ctx.match_index(ds, so)
+    rng = gen.Rng(701)
+    traces = {(int(streams[0][5]),), (int(streams[1][9]),)}
+    for _ in range(200):
+        s = streams[rng.below(len(streams))]
+        a = rng.below(len(s) - 10)
+        traces.add(tuple(int(x) for x in s[a:a + 1 + rng.below(8)]))
+    traces = sorted(traces, key=lambda t: (-len(t), t))
+    tt = np.array([x for t in traces for x in t], dtype=np.uint64)
+    to = np.cumsum([0] + [len(t) for t in traces]).astype(np.int64)
+    trie = ctx.trie_build_traces(torch.from_numpy(tt).cuda(), to)
+    gt, go = trie.traces()
+    a = ctx.match(trie, ds, so, full=True, cap=1 << 22)
+    b = ctx.match_indexed(trie, idx, full=True, cap=1 << 22)
+    want, cnt = oracle.match_brute(st, so, gt.cpu().numpy(), go)
+    assert torch.equal(a, b) and cnt == a.shape[0] and np.array_equal(a[:, :3].cpu().numpy(), want)
+    ra, na = ctx.match(trie, ds, so, mode=1)
+    rb, nb = ctx.match_indexed(trie, idx, mode=1)
+    assert na == nb == cnt and torch.equal(ra, rb)
