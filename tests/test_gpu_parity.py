@@ -350,3 +350,26 @@ def test_batched_fused_select_equals_global(ctx, with_big_group, monkeypatch):
             assert np.array_equal(g[:, :3], want["repeats"][:, :3]), w
             for row, wrow in zip(g, want["repeats"]):
                 assert np.array_equal(occ[row[3]:row[3] + row[2]], want["occ"][wrow[3]:wrow[3] + wrow[2]])
+
+
+def test_batched_edge_windows_fused_and_global(ctx, monkeypatch):
+    """Empty, 1-, 2- and 3-op windows, a window of one repeated token and a
+    full 16,384-op window in one batch: the fused per-window candidate stage
+    and the global path give the oracle's repeats and occurrences."""
+    wins = [np.zeros(0, np.uint64), gen.random_string(1, 1, 3), gen.random_string(2, 2, 1),
+            gen.random_string(3, 3, 2), np.full(700, 5, np.uint64), gen.random_string(4, 25, 2),
+            np.zeros(0, np.uint64), gen.random_string(6, 16384, 4)]
+    tok = np.concatenate(wins)
+    off = np.cumsum([0] + [len(x) for x in wins]).astype(np.int64)
+    for mode in ("fused", "global"):
+        if mode == "global":
+            monkeypatch.setenv("APO_SELECT_GLOBAL", "1")
+        for min_len in (1, 2, 25):
+            rep, roff, occ = ctx.find_repeats_batched(dev(tok), off, min_len)
+            rep, roff, occ = rep.cpu().numpy(), roff.cpu().numpy(), occ.cpu().numpy()
+            for w in range(len(wins)):
+                want = oracle.find_repeats(wins[w], min_len, tier=1)
+                g = rep[roff[w]:roff[w + 1]]
+                assert np.array_equal(g[:, :3], want["repeats"][:, :3]), (mode, min_len, w)
+                for row, wrow in zip(g, want["repeats"]):
+                    assert np.array_equal(occ[row[3]:row[3] + row[2]], want["occ"][wrow[3]:wrow[3] + wrow[2]])
