@@ -507,7 +507,40 @@ def main():
                         dst[a:a + CHUNK].copy_(src[a:a + CHUNK], non_blocking=True)
             copied[bi].record(cs)
 
+        # N = 1 with matching: the window tokens of step i+1 are uploaded
+        # while step i matches, the streams of step i while step i analyses
+        # (each half fits its phase; the analysis' many host syncs then see
+        # only half the transfer)
+        split = world == 1 and st_host is not None
+        tok_copied = [torch.cuda.Event() for _ in range(2)]
+        st_copied = [torch.cuda.Event() for _ in range(2)]
+
+        def enqueue_part(i, which):
+            bi = i % 2
+            cs.wait_event(consumed[bi])
+            src = tok_host if which == 0 else st_host
+            with torch.cuda.stream(cs):
+                for a in range(0, src.numel(), CHUNK):
+                    dbuf[bi][which][a:a + CHUNK].copy_(src[a:a + CHUNK], non_blocking=True)
+            (tok_copied if which == 0 else st_copied)[bi].record(cs)
+
+        def e2e_step_split(i, last):
+            bi = i % 2
+            s.wait_event(tok_copied[bi])
+            enqueue_part(i, 1)  # this step's streams, during its analysis
+
+            def after_trie():
+                s.wait_event(st_copied[bi])
+                if not last:
+                    enqueue_part(i + 1, 0)  # the next step's windows, during this step's matching
+            c, h = step(dbuf[bi][0], dbuf[bi][1], after_trie=after_trie)
+            consumed[bi].record(s)
+            r, o = (int(x) for x in ctx._read(c))
+            return to_host(bufs[0][:r], bufs[1], bufs[2][:o], h)
+
         def e2e_step(i, last):
+            if split:
+                return e2e_step_split(i, last)
             bi = i % 2
             s.wait_event(copied[bi])
             nxt = None if last else (lambda: enqueue_copy(i + 1))
@@ -565,7 +598,7 @@ def main():
         if pipe is not None:
             e2e_pipelined(2)
         else:
-            enqueue_copy(0)
+            enqueue_part(0, 0) if split else enqueue_copy(0)
             e2e_step(0, True)
         torch.cuda.synchronize()
         barrier()
@@ -575,7 +608,7 @@ def main():
         if pipe is not None:
             d2h = e2e_pipelined(args.steps)
         else:
-            enqueue_copy(0)
+            enqueue_part(0, 0) if split else enqueue_copy(0)
             for i in range(args.steps):
                 d2h = e2e_step(i, i + 1 == args.steps)
         e1.record(s)
