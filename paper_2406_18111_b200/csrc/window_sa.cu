@@ -155,7 +155,7 @@ __device__ __forceinline__ void lsd_pass(Smem &S, DigitF digit, MoveF move) {
   // per digit: exclusive prefix over warps (in place) and the digit total
   u32 total = 0;
   if (tid < RADIX) {
-#pragma unroll 8
+#pragma unroll
     for (int w = 0; w < kWWarps; ++w) {
       const u32 c = S.u.hist[w][tid];
       S.u.hist[w][tid] = u16(total);
@@ -219,7 +219,7 @@ __device__ __forceinline__ void heads_phase(Smem &S, int n, KeyF key) {
   u32 cn = 0, cs = 0;
   int last = -1;
   u32 hb_prev = 0;
-#pragma unroll 2
+#pragma unroll 8
   for (int j = 0; j <= kWItems; ++j) {
     u32 hb = 0;
     if (j < kWItems) {
@@ -298,7 +298,7 @@ __device__ __forceinline__ int groups_phase(Smem &S, const u32 *ord, int n) {
   const u32 le = lt | (1u << lane);
   u32 nb = S.u.g.wsum[warp][0], sb = S.u.g.wsum[warp][1];
   int carry = S.u.g.wlast[warp];
-#pragma unroll 4
+#pragma unroll
   for (int j = 0; j < kWItems; ++j) {
     const int row = warp * (32 * kWItems) + j * 32;
     const int q = row + lane;
@@ -487,6 +487,7 @@ __global__ void __launch_bounds__(kWT, 1)
       // (position 0xffff).
       {
         const int q0 = S.misc[3];
+#pragma unroll
         for (int q = tid; q < kWMax; q += kWT) {
           if (q < n) {
             const int j = int(ord[q] & 0xffffu);
