@@ -865,7 +865,7 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
 constexpr int kSMIThreads = 512;
 constexpr int kSMIWarps = kSMIThreads / 32;
 constexpr int kSMIPad = 256;    // zero entries past the stream end (a trip reads <= 256 past its start)
-constexpr int kSMICache = 128;  // leading trace ids per warp kept in shared memory
+constexpr int kSMICache = 64;  // leading trace ids per warp kept in shared memory (measured: 64 beats 128)
 constexpr u32 kTraceEnd = 0xffffffffu;
 
 
