@@ -883,7 +883,7 @@ __global__ void __launch_bounds__(kFindWarps * 32) k_rp_dec_find(RP a) {
   if (lane == 0) a.rcnt[q] = nrep;
 }
 
-constexpr int kCandThreads = 128;
+constexpr int kCandThreads = 1024;  // (measured: 1,024 > 512 > 256 > 128)
 
 __global__ void __launch_bounds__(kCandThreads) k_rp_dec_cands(RP a) {
   const int q = blockIdx.x;
