@@ -318,6 +318,10 @@ __global__ void __launch_bounds__(kXT, 1)
     if (tid < nw) S.hpre[tid] = u16(e2);
     if (tid == kXT - 1) S.misc[2] = e2 + v;
   }
+  // every candidate's start, once (T and U -- the range-minimum tables --
+  // are free now and hold 2 x kXW u16 together)
+  u16 *ST = S.T;
+  for (int c = tid; c < m; c += kXT) ST[c] = u16(pair_start(S, S.P[c >> 1], u32(c & 1)));
   __syncthreads();
   const u32 Gw = S.misc[2];
   // window offsets: decoupled look-back over (candidates, groups)
@@ -366,10 +370,10 @@ __global__ void __launch_bounds__(kXT, 1)
     }
     const int k = S.P[c >> 1];
     const u32 l = S.plen[k];
-    const u32 st = pair_start(S, k, u32(c & 1));
+    const u32 st = ST[c];
     u32 r = 0;
     for (int j = gs; j < ge; ++j) {
-      const u32 sj = pair_start(S, S.P[j >> 1], u32(j & 1));
+      const u32 sj = ST[j];
       r += (sj < st || (sj == st && j < c)) ? 1u : 0u;
     }
     const u32 gid = u32(S.hpre[wd]) + __popc(below) - 1u;
