@@ -51,6 +51,7 @@ struct SAWork {
   i64 dk_n = 0;
   bool dk_max = false;    // the token ~0 occurs (id dk_n)
   const u32 *slot_rank = nullptr;  // set: ids[] holds table slots, id = slot_rank[slot] (K9 maps them)
+  bool mirror = false;    // K9 reads each window's ids back to front (the reversed windows)
   // results
   i32 *sa;                // N (global positions, window-major suffix order)
   i32 *lcp;               // N (pair k = (k, k+1); 0 at the end of each window)
@@ -72,6 +73,7 @@ struct IdsMirror {
   u32 *slots;             // n scratch words
   unsigned short *id16;   // or nullptr
   bool id16_ok = false;
+  int nwin = 0;           // windows (off has nwin + 1 entries)
 };
 i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scratch, cudaStream_t s,
                     const u64 **dkeys = nullptr, i64 *dk_n = nullptr, bool *dk_max = nullptr,

@@ -295,11 +295,17 @@ bool build_sa_mirrored(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool w
   w.R = 0;
   w.dkeys = nullptr;
   w.slot_rank = nullptr;
-  const i64 K = dense_token_ids(c, tok, b.N, w.ids, w.ht_cap, w.ht_scratch, s, &w.dkeys, &w.dk_n, &w.dk_max, &mir);
+  mir.nwin = b.W;
+  // the table slots of the FORWARD windows; K9 maps them to ids and reads
+  // every window back to front
+  const i64 K = dense_token_ids(c, tok, b.N, w.ids, w.ht_cap, w.ht_scratch, s, &w.dkeys, &w.dk_n, &w.dk_max, &mir,
+                                &w.slot_rank);
   if (K < 0) return false;
   w.ids_valid = true;
   w.K = K;
+  w.mirror = true;
   run_window_sa(c, b, w, want_lcp, s);
+  w.mirror = false;
   return true;
 }
 
@@ -321,6 +327,7 @@ void build_sa(Ctx &c, const u64 *tok, const Batch &b, SAWork &w, bool want_lcp, 
   w.K = -1;
   w.dkeys = nullptr;
   w.slot_rank = nullptr;
+  w.mirror = false;
   i64 packK = -1;
   if (b.gen || b.W == 1 || w.rw != nullptr) {
     // K9 maps table slots to ids itself (w.slot_rank); others need the ids

@@ -86,6 +86,15 @@ __global__ void k_ids_from_slots(u32 *__restrict__ ids, i64 n, const u32 *__rest
   if (i < n) ids[i] = slot_rank[ids[i]];
 }
 
+// id + 1 of every position as u16, mirrored inside each window; a CTA per
+// window (no per-position window lookups); slots[] read forward
+__global__ void k_id16_mirror(const u32 *__restrict__ slots, const u32 *__restrict__ slot_rank,
+                              const i64 *__restrict__ off, unsigned short *__restrict__ id16) {
+  const i64 beg = off[blockIdx.x], n = off[blockIdx.x + 1] - beg;
+  for (i64 i = threadIdx.x; i < n; i += blockDim.x)
+    id16[beg + n - 1 - i] = (unsigned short)(__ldg(&slot_rank[slots[beg + i]]) + 1u);
+}
+
 __global__ void k_ids_mirror(const u32 *__restrict__ slots, i64 n, const u32 *__restrict__ slot_rank,
                              const i64 *__restrict__ off, const i32 *__restrict__ wid, u32 *__restrict__ ids,
                              unsigned short *__restrict__ id16) {
@@ -128,7 +137,9 @@ i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scra
   i64 *tot = cv.take<i64>(2);
   APO_CUDA(cudaMemsetAsync(table, 0xff, sizeof(u64) * cap, s));
   APO_CUDA(cudaMemsetAsync(cnt, 0, sizeof(u32) * 8, s));
-  u32 *slots = mir ? mir->slots : ids;  // table slot of every position
+  // table slot of every position (with slots_only the caller maps slots to
+  // ids itself, e.g. K9 on its level-0 load, mirrored or not)
+  u32 *slots = (mir && !slots_only) ? mir->slots : ids;
   k_ht_insert<<<grid_for(n, 256), 256, 0, s>>>(tok, n, table, cap, slots, cnt, cnt + 1);
   APO_CHECK_LAUNCH();
   c.launches++;
@@ -159,9 +170,17 @@ i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scra
     c.h2d(slot_rank + cap, &r, sizeof(u32), s);
     ++K;
   }
-  if (slots_only != nullptr && mir == nullptr) {
+  if (slots_only != nullptr) {
     // the caller maps slots itself (K9's level-0 load): ids[] keeps the slots
     *slots_only = slot_rank;
+    if (mir) {
+      mir->id16_ok = mir->id16 != nullptr && K >= 1 && K <= 65534;
+      if (mir->id16_ok) {
+        k_id16_mirror<<<mir->nwin, 256, 0, s>>>(ids, slot_rank, mir->off, mir->id16);
+        APO_CHECK_LAUNCH();
+        c.launches++;
+      }
+    }
     APO_CUDA(cudaStreamSynchronize(s));  // `r` above lives on the host stack
     return K;
   }

@@ -366,7 +366,7 @@ __global__ void k_nsmid(int *out) {
 // ids: global dense order-preserving token ids (K2), or nullptr: level 0
 // from level0 (global group starts of the (window, token) order).
 __global__ void __launch_bounds__(kWT, 1)
-    k_window_sa(Batch b, const u32 *__restrict__ ids, const u32 *__restrict__ slot_rank,
+    k_window_sa(Batch b, const u32 *__restrict__ ids, const u32 *__restrict__ slot_rank, int mirror,
                 const i32 *__restrict__ level0, u16 *__restrict__ scratch,
                 u32 nslots, u32 *__restrict__ next_win, i32 *__restrict__ sa_out, i32 *__restrict__ lcp_out,
                 i32 *__restrict__ rw) {
@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(kWT, 1)
       u32 mx = 0;
       if (tid == 0) S.misc[1] = 0;
       for (int q = tid; q < n; q += kWT) {
-        u32 v = ids[beg + q];
+        u32 v = ids[beg + (mirror ? n - 1 - q : q)];
         if (slot_rank != nullptr) v = __ldg(&slot_rank[v]);
         S.X[q] = v;
         S.rank[q] = u16(q);
@@ -622,6 +622,7 @@ void run_window_sa(Ctx &c, const Batch &b, SAWork &w, bool want_lcp, cudaStream_
   const int grid = int(std::min<i64>(b.W, c.num_sms));
   u32 *ctr = c.take_counter(s);
   k_window_sa<<<grid, kWT, smem, s>>>(b, w.ids_valid ? w.ids : nullptr, w.ids_valid ? w.slot_rank : nullptr,
+                                      w.ids_valid && w.mirror ? 1 : 0,
                                       w.levels[0],
                                       reinterpret_cast<u16 *>(w.win_scratch), u32(c.nsmid), ctr, w.sa,
                                       want_lcp ? w.lcp : nullptr, w.rw);
