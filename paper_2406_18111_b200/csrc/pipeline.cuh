@@ -64,16 +64,14 @@ void plan_sa(Carver &cv, const Batch &b, SAWork &w, bool want_lcp, int nsmid);
 // the distinct count exceeds cap / 2.
 size_t token_ids_scratch_bytes(i64 n, u32 cap);
 // Mirrored ids (the matcher's reversed streams without reversing tokens):
-// the table is built from the tokens as given, and id of position i goes to
-// ids[off[w] + off[w+1] - 1 - i] (w = wid[i]); with id16, also id + 1 as u16
-// when K <= 65,534 (*id16_ok says whether it was written).
+// with slots_only, the table is built from the tokens as given and each
+// window's id + 1 is written back to front as u16 into id16 when K <= 65,534
+// (id16_ok says whether it was written); K9 maps the slots itself.
 struct IdsMirror {
-  const i64 *off;
-  const i32 *wid;
-  u32 *slots;             // n scratch words
+  const i64 *off;         // window offsets (nwin + 1)
   unsigned short *id16;   // or nullptr
   bool id16_ok = false;
-  int nwin = 0;           // windows (off has nwin + 1 entries)
+  int nwin = 0;
 };
 i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scratch, cudaStream_t s,
                     const u64 **dkeys = nullptr, i64 *dk_n = nullptr, bool *dk_max = nullptr,

@@ -95,17 +95,6 @@ __global__ void k_id16_mirror(const u32 *__restrict__ slots, const u32 *__restri
     id16[beg + n - 1 - i] = (unsigned short)(__ldg(&slot_rank[slots[beg + i]]) + 1u);
 }
 
-__global__ void k_ids_mirror(const u32 *__restrict__ slots, i64 n, const u32 *__restrict__ slot_rank,
-                             const i64 *__restrict__ off, const i32 *__restrict__ wid, u32 *__restrict__ ids,
-                             unsigned short *__restrict__ id16) {
-  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int w = wid[i];
-  const i64 j = off[w] + off[w + 1] - 1 - i;
-  const u32 id = slot_rank[slots[i]];
-  ids[j] = id;
-  if (id16 != nullptr) id16[j] = (unsigned short)(id + 1u);
-}
 
 }  // namespace
 
@@ -139,7 +128,7 @@ i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scra
   APO_CUDA(cudaMemsetAsync(cnt, 0, sizeof(u32) * 8, s));
   // table slot of every position (with slots_only the caller maps slots to
   // ids itself, e.g. K9 on its level-0 load, mirrored or not)
-  u32 *slots = (mir && !slots_only) ? mir->slots : ids;
+  u32 *slots = ids;
   k_ht_insert<<<grid_for(n, 256), 256, 0, s>>>(tok, n, table, cap, slots, cnt, cnt + 1);
   APO_CHECK_LAUNCH();
   c.launches++;
@@ -184,13 +173,7 @@ i64 dense_token_ids(Ctx &c, const u64 *tok, i64 n, u32 *ids, u32 cap, char *scra
     APO_CUDA(cudaStreamSynchronize(s));  // `r` above lives on the host stack
     return K;
   }
-  if (mir) {
-    mir->id16_ok = mir->id16 != nullptr && K >= 1 && K <= 65534;
-    k_ids_mirror<<<grid_for(n, 256), 256, 0, s>>>(slots, n, slot_rank, mir->off, mir->wid, ids,
-                                                 mir->id16_ok ? mir->id16 : nullptr);
-  } else {
-    k_ids_from_slots<<<grid_for(n, 256), 256, 0, s>>>(ids, n, slot_rank);
-  }
+  k_ids_from_slots<<<grid_for(n, 256), 256, 0, s>>>(ids, n, slot_rank);
   APO_CHECK_LAUNCH();
   c.launches++;
   APO_CUDA(cudaStreamSynchronize(s));  // `r` above lives on the host stack

@@ -2294,7 +2294,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
       // reversed token copy); the reversed tokens are materialised only
       // for the raw-token paths (vocabulary over 65,534 or no dense ids)
       bool mirrored = false;
-      IdsMirror mir{g.d_off, g.d_wid, reinterpret_cast<u32 *>(g.sa.vals), sid16};
+      IdsMirror mir{g.d_off, sid16};
       if (rev) mirrored = build_sa_mirrored(c, d_streams, b, g.sa, true, s, mir);
       const bool ids16 = mirrored && mir.id16_ok && g.sa.dkeys;
       if (rev && !ids16) {
