@@ -595,17 +595,19 @@ __global__ void k_pair_list(const u32 *__restrict__ pbase, const u32 *__restrict
   }
 }
 
-// Launch order of the per-stream CTAs: streams keyed by the trace of their
-// first pair (the longest candidate trace whose first token the stream
-// holds).  Streams that share traces get neighbouring CTAs, so the CTAs
-// resident at any moment read overlapping trace sets and the trace tokens
-// (the matcher's HBM stream) are served from L2 instead of re-read from HBM.
+// Launch order of the per-stream CTAs: the streams with the most pairs
+// first (longest-processing-time first, so the heaviest streams do not finish
+// last; measured 0.55 ms faster on C4 than ordering by the first pair's
+// trace for L2 sharing).
 __global__ void k_stream_keys(const u32 *__restrict__ qoff, const u32 *__restrict__ zsorted,
                               const u32 *__restrict__ ptrace, int S, i64 T, u64 *__restrict__ key,
                               u32 *__restrict__ val) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= S) return;
-  key[q] = qoff[q] < qoff[q + 1] ? u64(ptrace[zsorted[qoff[q]]]) : u64(T);  // streams without pairs last
+  (void)zsorted;
+  (void)ptrace;
+  (void)T;
+  key[q] = u64(0xffffffffu - (qoff[q + 1] - qoff[q]));  // most pairs first (32-bit key)
   val[q] = u32(q);
 }
 
@@ -1505,9 +1507,10 @@ __global__ void __launch_bounds__(kEndsThreads, 2) k_stream_ends(StreamMatch m, 
                                                                  const u32 *__restrict__ otr,
                                                                  const u32 *__restrict__ oroot,
                                                                  u32 *__restrict__ deepz,
-                                                                 unsigned short *__restrict__ endml) {
+                                                                 unsigned short *__restrict__ endml,
+                                                                 const u32 *__restrict__ qorder) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int q = blockIdx.x;
+  const int q = int(qorder[blockIdx.x]);  // heaviest streams first
   const i64 beg = m.off[q], n = m.off[q + 1] - beg;
   const i64 a = toff[q], M = i64(toff[q + 1]) - a;
   if (M == 0) {
@@ -2509,7 +2512,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
             k_stream_keys<<<grid_for(nstreams, T256), T256, 0, s>>>(qoff, sqv, ptr, nstreams, T, sk, sv);
             APO_CHECK_LAUNCH();
             c.launches += 2;
-            const bool as = radix_sort_u64_u32(c, sk, sv, sk_alt, sv_alt, nstreams, 0, bits_for(u64(T)), s);
+            const bool as = radix_sort_u64_u32(c, sk, sv, sk_alt, sv_alt, nstreams, 0, 32, s);
             const u32 *qorder = as ? sv_alt : sv;
             if (use_ids) {
               k_pair_meta<<<grid_for(P, T256), T256, 0, s>>>(sqk, sqv, P, pair_e, ptr, e_lo, e_hi, p_off, tr->d_off,
@@ -2568,7 +2571,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
                 unsigned short *endml = static_cast<unsigned short *>(c.pool_get(ri->endml_bytes));
                 const size_t nsmem = (sizeof(u32) + sizeof(unsigned short)) * size_t(kSMMax);
                 c.smem_optin(reinterpret_cast<const void *>(k_stream_ends), nsmem);
-                k_stream_ends<<<nstreams, kEndsThreads, nsmem, s>>>(sm, stk, tof, otr, groot, deepz, endml);
+                k_stream_ends<<<nstreams, kEndsThreads, nsmem, s>>>(sm, stk, tof, otr, groot, deepz, endml, qorder);
                 APO_CHECK_LAUNCH();
                 ri->ok = true;
                 ri->lazy = true;
