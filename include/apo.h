@@ -300,8 +300,10 @@ apo_status apo_match(apo_ctx *ctx, const apo_trie *trie, const uint64_t *d_strea
 
 /* The trace-independent half of apo_match, for callers that overlap it with
  * building the trace set (e.g. the multi-GPU union): the REVERSED streams,
- * their suffix arrays + LCP arrays and their buckets (by the first two tokens when the batch has <= 65,534 distinct tokens, else by the first).    The handle owns
- * device workspace of ctx (free with apo_stream_index_destroy); d_streams
+ * their suffix arrays + LCP arrays and their buckets (by the first two
+ * tokens when the batch has <= 65,534 distinct tokens, else by the first).
+ * The handle owns device workspace of ctx (free with
+ * apo_stream_index_destroy); d_streams
  * (and h_off's values) must stay unchanged until its last use.
  * Synchronises `stream`. */
 typedef struct apo_stream_index apo_stream_index;
