@@ -289,7 +289,9 @@ __device__ __forceinline__ u32 scan_op(u32 a, u32 b) {
 // coalesce); the values are transposed through shared memory so each thread
 // scans a contiguous run of kScanItems elements.
 template <bool IS_MAX, class F>
-__global__ void __launch_bounds__(kScanThreads) k_scan(i64 n, F f, u64 *status, u32 *counter, u32 epoch) {
+__global__ void __launch_bounds__(kScanThreads) k_scan(i64 n, F f, u64 *status, u32 *counter, u32 epoch,
+                                                        const u32 *gate) {
+  if (gate != nullptr && *gate == 0u) return;  // speculative round after convergence
   // one pad word per 16 keeps both the striped and the blocked accesses
   // bank-conflict free
   __shared__ u32 s_v[kScanTile + kScanTile / 16];  // values
@@ -376,14 +378,14 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(i64 n, F f, u64 *status, 
 }
 
 template <bool IS_MAX, class F>
-void launch_scan(Ctx &c, i64 n, const F &f, cudaStream_t s) {
+void launch_scan(Ctx &c, i64 n, const F &f, cudaStream_t s, const u32 *gate = nullptr) {
   if (n <= 0) return;
   i64 tiles = (n + kScanTile - 1) / kScanTile;
   c.ensure_status(size_t(tiles), s);
   u32 *ctr = c.take_counter(s);
   u32 ep = c.next_epoch();
   if (c.prof) c.prof_begin(kProfScan, 0.0, s);
-  k_scan<IS_MAX, F><<<int(tiles), kScanThreads, 0, s>>>(n, f, c.status, ctr, ep);
+  k_scan<IS_MAX, F><<<int(tiles), kScanThreads, 0, s>>>(n, f, c.status, ctr, ep, gate);
   APO_CHECK_LAUNCH();
   if (c.prof) c.prof_end(s);
   c.launches++;
@@ -393,8 +395,9 @@ void launch_scan(Ctx &c, i64 n, const F &f, cudaStream_t s) {
 // LSD onesweep radix sort of (u64 key, V value) pairs (V = u32, u64, or
 // void for keys only) over key bits [begin_bit, end_bit).  Stable.  Returns
 // true iff the result ended in the *_alt buffers.
+// gate (optional, device): the whole sort is skipped when *gate == 0
 bool radix_sort_u64_u32(Ctx &c, u64 *keys, u32 *vals, u64 *keys_alt, u32 *vals_alt, i64 n,
-                        int begin_bit, int end_bit, cudaStream_t s);
+                        int begin_bit, int end_bit, cudaStream_t s, const u32 *gate = nullptr);
 bool radix_sort_u64_keys(Ctx &c, u64 *keys, u64 *keys_alt, i64 n, int begin_bit, int end_bit,
                          cudaStream_t s);
 bool radix_sort_u32_u64(Ctx &c, u32 *keys, u64 *vals, u32 *keys_alt, u64 *vals_alt, i64 n,

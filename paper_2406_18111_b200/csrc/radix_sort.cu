@@ -72,7 +72,8 @@ __device__ __forceinline__ u32 lanemask_lt() {
 
 template <class K>
 __global__ void __launch_bounds__(kSortThreads) k_hist(const K *__restrict__ keys, i64 n, PassPlan plan,
-                                                       u32 *__restrict__ ghist) {
+                                                       u32 *__restrict__ ghist, const u32 *gate) {
+  if (gate != nullptr && *gate == 0u) return;  // speculative round after convergence
   __shared__ u32 sh[kMaxPasses * kMaxRadix];
   for (int i = threadIdx.x; i < plan.npass * kMaxRadix; i += kSortThreads) sh[i] = 0;
   __syncthreads();
@@ -127,7 +128,8 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(const K *__restric
                                                            const V *__restrict__ vin, V *__restrict__ vout,
                                                            i64 n, int shift, int pbits,
                                                            const u32 *__restrict__ ghist, u64 *status,
-                                                           u32 *counter, u32 epoch) {
+                                                           u32 *counter, u32 epoch, const u32 *gate) {
+  if (gate != nullptr && *gate == 0u) return;  // speculative round after convergence
   constexpr bool HAS_V = !std::is_same<V, NoVal>::value;
   constexpr int RADIX = 1 << BITS;
   constexpr int BPT = RADIX / kSortThreads;
@@ -276,7 +278,7 @@ PassPlan plan_passes(int begin_bit, int end_bit) {
 
 template <class K, class V, int BITS>
 void launch_pass(Ctx &c, const K *kin, K *kout, const V *vin, V *vout, i64 n, int shift, int pbits,
-                 const u32 *ghist, cudaStream_t s) {
+                 const u32 *ghist, cudaStream_t s, const u32 *gate) {
   constexpr bool HAS_V = !std::is_same<V, NoVal>::value;
   constexpr int RADIX = 1 << BITS;
   const size_t smem = (sizeof(K) + (HAS_V ? sizeof(V) : 0)) * kSortTile + sizeof(u32) * kSortWarps * RADIX;
@@ -288,7 +290,7 @@ void launch_pass(Ctx &c, const K *kin, K *kout, const V *vin, V *vout, i64 n, in
   // algorithmic bytes: every (key, value) read once and written once
   if (c.prof) c.prof_begin(kProfRadixPass, 2.0 * double(n) * double(sizeof(K) + (HAS_V ? sizeof(V) : 0)), s);
   k_onesweep<K, V, BITS><<<int(tiles), kSortThreads, smem, s>>>(kin, kout, vin, vout, n, shift, pbits, ghist,
-                                                                 c.status, ctr, ep);
+                                                                 c.status, ctr, ep, gate);
   APO_CHECK_LAUNCH();
   if (c.prof) c.prof_end(s);
   c.launches++;
@@ -296,14 +298,14 @@ void launch_pass(Ctx &c, const K *kin, K *kout, const V *vin, V *vout, i64 n, in
 
 template <class K, class V>
 bool radix_sort(Ctx &c, K *keys, V *vals, K *keys_alt, V *vals_alt, i64 n, int begin_bit, int end_bit,
-                cudaStream_t s) {
+                cudaStream_t s, const u32 *gate = nullptr) {
   if (n <= 1 || end_bit <= begin_bit) return false;
   PassPlan plan = plan_passes(begin_bit, end_bit);
   u32 *ghist = reinterpret_cast<u32 *>(c.d_misc + 64);  // kMaxPasses * kMaxRadix u32
   APO_CUDA(cudaMemsetAsync(ghist, 0, sizeof(u32) * kMaxPasses * kMaxRadix, s));
   int hg = grid_for(n, kSortThreads * 16, c.num_sms * 8);
   if (c.prof) c.prof_begin(kProfRadixHist, double(n) * sizeof(K), s);
-  k_hist<K><<<hg, kSortThreads, 0, s>>>(keys, n, plan, ghist);
+  k_hist<K><<<hg, kSortThreads, 0, s>>>(keys, n, plan, ghist, gate);
   APO_CHECK_LAUNCH();
   if (c.prof) c.prof_end(s);
   c.launches++;
@@ -312,9 +314,9 @@ bool radix_sort(Ctx &c, K *keys, V *vals, K *keys_alt, V *vals_alt, i64 n, int b
   for (int p = 0; p < plan.npass; ++p) {
     const u32 *gh = ghist + p * kMaxRadix;
     if (plan.bits[p] > 8)
-      launch_pass<K, V, 9>(c, ki, ko, vi, vo, n, plan.shift[p], plan.bits[p], gh, s);
+      launch_pass<K, V, 9>(c, ki, ko, vi, vo, n, plan.shift[p], plan.bits[p], gh, s, gate);
     else
-      launch_pass<K, V, 8>(c, ki, ko, vi, vo, n, plan.shift[p], plan.bits[p], gh, s);
+      launch_pass<K, V, 8>(c, ki, ko, vi, vo, n, plan.shift[p], plan.bits[p], gh, s, gate);
     std::swap(ki, ko);
     std::swap(vi, vo);
   }
@@ -326,8 +328,8 @@ bool radix_sort(Ctx &c, K *keys, V *vals, K *keys_alt, V *vals_alt, i64 n, int b
 size_t radix_status_words(i64 n) { return size_t((n + kSortTile - 1) / kSortTile) * kMaxRadix; }
 
 bool radix_sort_u64_u32(Ctx &c, u64 *keys, u32 *vals, u64 *keys_alt, u32 *vals_alt, i64 n, int begin_bit,
-                        int end_bit, cudaStream_t s) {
-  return radix_sort<u64, u32>(c, keys, vals, keys_alt, vals_alt, n, begin_bit, end_bit, s);
+                        int end_bit, cudaStream_t s, const u32 *gate) {
+  return radix_sort<u64, u32>(c, keys, vals, keys_alt, vals_alt, n, begin_bit, end_bit, s, gate);
 }
 bool radix_sort_u64_keys(Ctx &c, u64 *keys, u64 *keys_alt, i64 n, int begin_bit, int end_bit, cudaStream_t s) {
   return radix_sort<u64, NoVal>(c, keys, (NoVal *)nullptr, keys_alt, (NoVal *)nullptr, n, begin_bit, end_bit, s);

@@ -104,6 +104,21 @@ def test_edge_cases(ctx):
     assert sa.tolist() == [0] and lcp.numel() == 0
 
 
+
+@pytest.mark.parametrize("spec", [1, 2, 3, 8])
+@pytest.mark.parametrize("case", range(4))
+def test_sa_lcp_speculative_rounds(ctx, case, spec, monkeypatch):
+    """Global doubling path (> 16,384 tokens) with 1-8 Manber-Myers rounds
+    launched per host convergence read: the rounds after convergence are
+    gated off on the device, the SA/LCP must equal the oracle's."""
+    S = [gen.c2()[:20000], gen.c3()[:17000], gen.periodic(6, 40000, 7, 3),
+         gen.fibonacci_word(30000)][case]
+    monkeypatch.setenv("APO_SPEC_ROUNDS", str(spec))
+    sa, lcp = ctx.suffix_array(dev(S))
+    want = oracle.sa_doubling(S)
+    assert np.array_equal(sa.cpu().numpy(), want)
+    assert np.array_equal(lcp.cpu().numpy(), oracle.lcp_kasai(S, want))
+
 def test_config_c1_full(ctx):
     check_find(ctx, gen.c1(), 5, tier=0)
 
