@@ -896,22 +896,11 @@ __global__ void k_dict_build(const u64 *__restrict__ dk, i64 K0, u64 *__restrict
 // trace token -> comparison value against the batch dictionary: 2 (rank + 1)
 // for a token of the batch (one table probe), else 2 (tokens below it) + 1
 // (binary search over dk; tokens absent from the batch are rare)
-__global__ void k_trace_ids(const u64 *__restrict__ tok, i64 n, const u64 *__restrict__ dk, i64 K0, int has_max,
-                            const u64 *__restrict__ tkey, const u32 *__restrict__ tval, u32 mask,
-                            u32 *__restrict__ out) {
-  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const u64 v = tok[i];
-  if (v == ~0ull) {
-    out[i] = has_max ? u32(2 * (K0 + 1)) : u32(2 * K0 + 1);
-    return;
-  }
-  for (u32 h = dict_hash(v) & mask;; h = (h + 1) & mask) {
+__device__ __noinline__ u32 trace_id_slow(u64 v, u32 h, const u64 *__restrict__ dk, i64 K0,
+                                          const u64 *__restrict__ tkey, const u32 *__restrict__ tval, u32 mask) {
+  for (;; h = (h + 1) & mask) {
     const u64 k = __ldg(&tkey[h]);
-    if (k == v) {
-      out[i] = 2u * (__ldg(&tval[h]) + 1u);
-      return;
-    }
+    if (k == v) return 2u * (__ldg(&tval[h]) + 1u);
     if (k == ~0ull) break;
   }
   i64 lo = 0, hi = K0;
@@ -919,7 +908,41 @@ __global__ void k_trace_ids(const u64 *__restrict__ tok, i64 n, const u64 *__res
     const i64 mid = (lo + hi) >> 1;
     if (__ldg(&dk[mid]) < v) lo = mid + 1; else hi = mid;
   }
-  out[i] = (lo < K0 && __ldg(&dk[lo]) == v) ? u32(2 * (lo + 1)) : u32(2 * lo + 1);
+  return (lo < K0 && __ldg(&dk[lo]) == v) ? u32(2 * (lo + 1)) : u32(2 * lo + 1);
+}
+
+// kTidItems tokens per thread, their first probes and values loaded together
+// (the dependent token -> key -> value loads are latency-bound)
+constexpr int kTidItems = 4;
+__global__ void __launch_bounds__(256) k_trace_ids(const u64 *__restrict__ tok, i64 n, const u64 *__restrict__ dk,
+                                                   i64 K0, int has_max, const u64 *__restrict__ tkey,
+                                                   const u32 *__restrict__ tval, u32 mask, u32 *__restrict__ out) {
+  const i64 base = i64(blockIdx.x) * (256 * kTidItems) + threadIdx.x;
+  u64 v[kTidItems], k[kTidItems];
+  u32 h[kTidItems], r[kTidItems];
+#pragma unroll
+  for (int j = 0; j < kTidItems; ++j) {
+    const i64 i = base + j * 256;
+    v[j] = i < n ? __ldg(&tok[i]) : ~0ull;
+  }
+#pragma unroll
+  for (int j = 0; j < kTidItems; ++j) {
+    h[j] = dict_hash(v[j]) & mask;
+    k[j] = v[j] != ~0ull ? __ldg(&tkey[h[j]]) : 0ull;
+  }
+#pragma unroll
+  for (int j = 0; j < kTidItems; ++j) r[j] = (v[j] != ~0ull && k[j] == v[j]) ? __ldg(&tval[h[j]]) : 0u;
+#pragma unroll
+  for (int j = 0; j < kTidItems; ++j) {
+    const i64 i = base + j * 256;
+    if (i >= n) break;
+    if (v[j] == ~0ull)
+      out[i] = has_max ? u32(2 * (K0 + 1)) : u32(2 * K0 + 1);
+    else if (k[j] == v[j])
+      out[i] = 2u * (r[j] + 1u);
+    else
+      out[i] = trace_id_slow(v[j], h[j], dk, K0, tkey, tval, mask);
+  }
 }
 
 // per stream-sorted pair i: (lo | hi << 16) local to the stream, pair id z,
@@ -2412,7 +2435,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
           k_dict_build<<<grid_for(p_dkn, T256), T256, 0, s>>>(p_dk, p_dkn, tkey, tval, tslots - 1);
           APO_CHECK_LAUNCH();
         }
-        k_trace_ids<<<grid_for(std::max<i64>(tr->ntok, 1), T256), T256, 0, s>>>(
+        k_trace_ids<<<grid_for(std::max<i64>(tr->ntok, 1), T256 * kTidItems), T256, 0, s>>>(
             tr->d_rtok, tr->ntok, p_dk, p_dkn, p_dkmax ? 1 : 0, tkey, tval, tslots - 1, tid);
         APO_CHECK_LAUNCH();
         c.launches += 2;
