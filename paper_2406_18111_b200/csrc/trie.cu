@@ -856,11 +856,13 @@ __global__ void __launch_bounds__(kSMThreads, 1) k_stream_match(StreamMatch m, c
 // When the stream batch's dictionary holds at most 65,534 distinct tokens,
 // K2's order-preserving ids stand in for the 64-bit tokens:
 //  * stream token -> y = id + 1 (u16, in shared memory; y = 0 past the end),
-//  * trace token  -> 2 * (id + 1) if the token occurs in the batch, else
-//    2 * (number of batch tokens below it) + 1; 0xffffffff past the trace end.
-// Equal tokens give x == 2y, and x < 2y exactly when the token is smaller, so
-// every comparison decides as on the raw tokens (the past-the-end values sort
-// as a shorter suffix / an exhausted trace do).  Per pair the search needs
+//  * trace token  -> 2 * (id + 1) if the token occurs in the batch, else 1;
+//    0xffffffff past the trace end.
+// Equal tokens give x == 2y, and for tokens of the batch x < 2y exactly when
+// the token is smaller, so every comparison of a trace made of batch tokens
+// decides as on the raw tokens (the past-the-end values sort as a shorter
+// suffix / an exhausted trace do); a trace holding another token matches
+// nowhere, and its search only has to end (k_trace_ids).  Per pair the search needs
 // one 16-byte record (k_pair_meta) instead of a chain of dependent lookups,
 // the stream half of each 32-token step is one 64-B shared-memory wavefront,
 // and the CTA fits twice per SM (512 threads, ~109 KB).
@@ -871,77 +873,55 @@ constexpr int kSMICache = 64;  // leading trace ids per warp kept in shared memo
 constexpr u32 kTraceEnd = 0xffffffffu;
 
 
-// Open-addressing table of the batch dictionary dk[0..K0) (sorted distinct
-// tokens except ~0): key -> rank, for k_trace_ids.  `mask` + 1 slots, at most
-// half full; empty slots hold ~0 (the token ~0 is handled aside).
+// trace token -> comparison value against the batch dictionary dk[0..K0)
+// (sorted distinct tokens except ~0): 2 (rank + 1) for a token of the batch,
+// else 1.  A trace holding a token absent from the stream batch occurs
+// nowhere in it: its comparisons with stream suffixes (stream values 2 (id +
+// 1), 0 past the end) never reach its full length, so it gets no bucket, no
+// interval and no hit whatever order its absent tokens take -- they only
+// need a value that equals no stream value.  One probe of an open-addressing
+// table of 16-B (token, rank) slots, at most a quarter full: one L2 request
+// for a token of the batch, ~1.4 for an absent one (at N > 1 most of the
+// peers' trace tokens).  N = 4 union, 184 M trace tokens: 0.99 ms; 2.99 ms
+// with a (token) + (rank) table and a binary search over dk for the exact
+// rank of an absent token, 3.1 ms with a two-level search for every token.
 __device__ __forceinline__ u32 dict_hash(u64 z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return u32(z ^ (z >> 31));
 }
 
-__global__ void k_dict_build(const u64 *__restrict__ dk, i64 K0, u64 *__restrict__ tkey, u32 *__restrict__ tval,
-                             u32 mask) {
+__global__ void k_dict_build(const u64 *__restrict__ dk, i64 K0, ulonglong2 *__restrict__ slot, u32 mask) {
   const i64 r = i64(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= K0) return;
   const u64 v = dk[r];
   for (u32 h = dict_hash(v) & mask;; h = (h + 1) & mask) {
-    if (atomicCAS(reinterpret_cast<unsigned long long *>(&tkey[h]), ~0ull, v) == ~0ull) {
-      tval[h] = u32(r);
+    if (atomicCAS(reinterpret_cast<unsigned long long *>(&slot[h].x), ~0ull, v) == ~0ull) {
+      slot[h].y = u64(r);
       return;
     }
   }
 }
 
-// trace token -> comparison value against the batch dictionary: 2 (rank + 1)
-// for a token of the batch (one table probe), else 2 (tokens below it) + 1
-// (binary search over dk; tokens absent from the batch are rare)
-__device__ __noinline__ u32 trace_id_slow(u64 v, u32 h, const u64 *__restrict__ dk, i64 K0,
-                                          const u64 *__restrict__ tkey, const u32 *__restrict__ tval, u32 mask) {
-  for (;; h = (h + 1) & mask) {
-    const u64 k = __ldg(&tkey[h]);
-    if (k == v) return 2u * (__ldg(&tval[h]) + 1u);
-    if (k == ~0ull) break;
+__global__ void k_trace_ids(const u64 *__restrict__ tok, i64 n, i64 K0, int has_max,
+                            const ulonglong2 *__restrict__ slot, u32 mask, u32 *__restrict__ out) {
+  const i64 i = i64(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const u64 v = tok[i];
+  if (v == ~0ull) {
+    out[i] = has_max ? u32(2 * (K0 + 1)) : 1u;
+    return;
   }
-  i64 lo = 0, hi = K0;
-  while (lo < hi) {
-    const i64 mid = (lo + hi) >> 1;
-    if (__ldg(&dk[mid]) < v) lo = mid + 1; else hi = mid;
-  }
-  return (lo < K0 && __ldg(&dk[lo]) == v) ? u32(2 * (lo + 1)) : u32(2 * lo + 1);
-}
-
-// kTidItems tokens per thread, their first probes and values loaded together
-// (the dependent token -> key -> value loads are latency-bound)
-constexpr int kTidItems = 4;
-__global__ void __launch_bounds__(256) k_trace_ids(const u64 *__restrict__ tok, i64 n, const u64 *__restrict__ dk,
-                                                   i64 K0, int has_max, const u64 *__restrict__ tkey,
-                                                   const u32 *__restrict__ tval, u32 mask, u32 *__restrict__ out) {
-  const i64 base = i64(blockIdx.x) * (256 * kTidItems) + threadIdx.x;
-  u64 v[kTidItems], k[kTidItems];
-  u32 h[kTidItems], r[kTidItems];
-#pragma unroll
-  for (int j = 0; j < kTidItems; ++j) {
-    const i64 i = base + j * 256;
-    v[j] = i < n ? __ldg(&tok[i]) : ~0ull;
-  }
-#pragma unroll
-  for (int j = 0; j < kTidItems; ++j) {
-    h[j] = dict_hash(v[j]) & mask;
-    k[j] = v[j] != ~0ull ? __ldg(&tkey[h[j]]) : 0ull;
-  }
-#pragma unroll
-  for (int j = 0; j < kTidItems; ++j) r[j] = (v[j] != ~0ull && k[j] == v[j]) ? __ldg(&tval[h[j]]) : 0u;
-#pragma unroll
-  for (int j = 0; j < kTidItems; ++j) {
-    const i64 i = base + j * 256;
-    if (i >= n) break;
-    if (v[j] == ~0ull)
-      out[i] = has_max ? u32(2 * (K0 + 1)) : u32(2 * K0 + 1);
-    else if (k[j] == v[j])
-      out[i] = 2u * (r[j] + 1u);
-    else
-      out[i] = trace_id_slow(v[j], h[j], dk, K0, tkey, tval, mask);
+  for (u32 h = dict_hash(v) & mask;; h = (h + 1) & mask) {
+    const ulonglong2 e = __ldg(&slot[h]);
+    if (e.x == v) {
+      out[i] = 2u * (u32(e.y) + 1u);
+      return;
+    }
+    if (e.x == ~0ull) {
+      out[i] = 1u;
+      return;
+    }
   }
 }
 
@@ -2425,18 +2405,17 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
         tid_bytes = sizeof(u32) * size_t(std::max<i64>(tr->ntok, 1));
         tid = static_cast<u32 *>(c.pool_get(tid_bytes));
         u32 tslots = 1024;
-        while (i64(tslots) < 2 * p_dkn) tslots <<= 1;
-        dict_bytes = (sizeof(u64) + sizeof(u32)) * size_t(tslots) + 256;
+        while (i64(tslots) < 4 * p_dkn) tslots <<= 1;
+        dict_bytes = sizeof(ulonglong2) * size_t(tslots);
         dict = static_cast<char *>(c.pool_get(dict_bytes));
-        u64 *tkey = reinterpret_cast<u64 *>(dict);
-        u32 *tval = reinterpret_cast<u32 *>(tkey + tslots);
-        APO_CUDA(cudaMemsetAsync(tkey, 0xff, sizeof(u64) * tslots, s));
+        ulonglong2 *slot = reinterpret_cast<ulonglong2 *>(dict);
+        APO_CUDA(cudaMemsetAsync(slot, 0xff, dict_bytes, s));
         if (p_dkn > 0) {
-          k_dict_build<<<grid_for(p_dkn, T256), T256, 0, s>>>(p_dk, p_dkn, tkey, tval, tslots - 1);
+          k_dict_build<<<grid_for(p_dkn, T256), T256, 0, s>>>(p_dk, p_dkn, slot, tslots - 1);
           APO_CHECK_LAUNCH();
         }
-        k_trace_ids<<<grid_for(std::max<i64>(tr->ntok, 1), T256 * kTidItems), T256, 0, s>>>(
-            tr->d_rtok, tr->ntok, p_dk, p_dkn, p_dkmax ? 1 : 0, tkey, tval, tslots - 1, tid);
+        k_trace_ids<<<grid_for(std::max<i64>(tr->ntok, 1), T256), T256, 0, s>>>(tr->d_rtok, tr->ntok, p_dkn,
+                                                                                p_dkmax ? 1 : 0, slot, tslots - 1, tid);
         APO_CHECK_LAUNCH();
         c.launches += 2;
         tid_v = tid;

@@ -495,3 +495,41 @@ def test_match_indexed_one_token_traces():
     ra, na = ctx.match(trie, ds, so, mode=1)
     rb, nb = ctx.match_indexed(trie, idx, mode=1)
     assert na == nb == cnt and torch.equal(ra, rb)
+
+
+def test_match_dense_ids_many_absent_trace_tokens(ctx):
+    """Dense-id matcher with a dictionary of ~30 K stream tokens and traces
+    whose tokens are mostly absent from the streams (as the peers' traces
+    are at N > 1): the absent tokens' comparison values come from the
+    on-chip dictionary sample (k_trace_ids).  Both modes against the oracle."""
+    rng = gen.Rng(93)
+    vocab = np.unique(gen.H_np(3, gen.Rng(94).below_np(1 << 40, 40000)))
+    lens = [4000, 16384, 2500, 1, 7000, 3000]
+    streams = [vocab[gen.Rng(950 + q).below_np(len(vocab), n).astype(np.int64)] for q, n in enumerate(lens)]
+    traces = set()
+    for j in range(3000):
+        if j % 4 == 3:  # entirely foreign tokens (between, below and above the vocabulary)
+            t = [int(x) for x in gen.H_np(5 + j, gen.Rng(960 + j).below_np(1 << 40, 1 + rng.below(30)))]
+        else:
+            s = streams[rng.below(len(streams))]
+            a = rng.below(len(s))
+            t = [int(x) for x in s[a:a + 1 + rng.below(40)]]
+            if j % 4 == 1:  # one absent token
+                t[rng.below(len(t))] = int(gen.H_np(7, np.array([j], dtype=np.uint64))[0])
+        traces.add(tuple(t))
+    traces = sorted(traces, key=lambda t: (-len(t), t))
+    tt = np.array([x for t in traces for x in t], dtype=np.uint64)
+    to = np.cumsum([0] + [len(t) for t in traces]).astype(np.int64)
+    trie = ctx.trie_build_traces(dev(tt), to)
+    gt, go = trie.traces()
+    sflat = np.concatenate(streams)
+    soff = np.cumsum([0] + lens).astype(np.int64)
+    hits = ctx.match(trie, dev(sflat), soff, cap=1 << 24).cpu().numpy()
+    want, cnt = oracle.match_brute(sflat, soff, gt.cpu().numpy(), go)
+    assert cnt == len(hits) and np.array_equal(hits, want) and cnt > 0
+    rp, nall = ctx.match(trie, dev(sflat), soff, mode=1)
+    tlen = np.diff(go)
+    want_rp = oracle.replay(want, tlen)
+    g = rp.cpu().numpy().astype(np.int64)
+    got_rp = np.stack([g[:, 0], g[:, 1] - tlen[g[:, 2]] + 1, g[:, 1], g[:, 2], g[:, 3]], axis=1)
+    assert nall == cnt and np.array_equal(got_rp, want_rp)
