@@ -104,6 +104,18 @@ __global__ void k_copy_pieces(const u64 *__restrict__ src_tok, const i64 *__rest
   for (i64 k = lane; k < n; k += 32) dst[o + k] = src_tok[a + k];
 }
 
+// the same, each piece written back to front (the trace set keeps only its
+// reversed traces, the form the matcher reads; the forward form is made on
+// demand by trie_forward)
+__global__ void k_copy_pieces_rev(const u64 *__restrict__ src_tok, const i64 *__restrict__ p_src,
+                                  const i64 *__restrict__ p_off, i64 np, u64 *__restrict__ dst) {
+  i64 p = (i64(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (p >= np) return;
+  i64 a = p_src[p], o = p_off[p], n = p_off[p + 1] - o;
+  for (i64 k = lane; k < n; k += 32) dst[o + n - 1 - k] = src_tok[a + k];
+}
+
 // ------------------------------------------------ order + dedup ----
 // warp per sorted neighbour pair: same length and same content -> not a head
 __global__ void k_trace_heads(const u64 *__restrict__ tok, const i64 *__restrict__ off, const u32 *__restrict__ order,
@@ -327,6 +339,16 @@ __global__ void k_reverse_traces(const u64 *__restrict__ src, const i64 *__restr
   const int lane = threadIdx.x & 31;
   const i64 o = off[t], L = off[t + 1] - o;
   for (i64 k = lane; k < L; k += 32) dst[o + k] = src[o + L - 1 - k];
+}
+
+// the forward traces (the trace set keeps the reversed ones): made once, on
+// the first use by a path that reads them (streams > 16,384 tokens)
+void trie_forward(Ctx &c, const apo_trie *tr, cudaStream_t s) {
+  if (tr->d_tok || tr->T == 0) return;
+  tr->d_tok = static_cast<u64 *>(c.pool_get(tr->tok_bytes));
+  k_reverse_traces<<<grid_for(tr->T * 32, T256), T256, 0, s>>>(tr->d_rtok, tr->d_off, tr->T, tr->d_tok);
+  APO_CHECK_LAUNCH();
+  c.launches++;
 }
 
 // ------------------------------------------- per-stream matching path ----
@@ -1939,11 +1961,11 @@ void build_trace_set(Ctx &c, apo_trie *tr, const u64 *d_ptok, const std::vector<
   const i64 ntok = h_uoff[T];
   tr->tok_bytes = sizeof(u64) * size_t(std::max<i64>(ntok, 1));
   tr->off_bytes = sizeof(i64) * size_t(T + 1);
-  tr->d_tok = static_cast<u64 *>(c.pool_get(tr->tok_bytes));
+  tr->d_rtok = static_cast<u64 *>(c.pool_get(tr->tok_bytes));
   tr->d_off = static_cast<i64 *>(c.pool_get(tr->off_bytes));
   c.h2d(tr->d_off, h_uoff.data(), sizeof(i64) * (T + 1), s);
   k_src_of<<<grid_for(T, T256), T256, 0, s>>>(uniq, d_poff, T, d_src);
-  k_copy_pieces<<<grid_for(T * 32, T256), T256, 0, s>>>(d_ptok, d_src, tr->d_off, T, tr->d_tok);
+  k_copy_pieces_rev<<<grid_for(T * 32, T256), T256, 0, s>>>(d_ptok, d_src, tr->d_off, T, tr->d_rtok);
   APO_CHECK_LAUNCH();
   c.launches += 2;
   APO_CUDA(cudaStreamSynchronize(s));
@@ -2120,7 +2142,7 @@ apo_status apo_trie_build_traces_multi(apo_ctx *ctx, int32_t nsrc, const uint64_
 void apo_trie_destroy(apo_trie *tr) {
   if (!tr) return;
   if (tr->ctx) {
-    tr->ctx->c.pool_put(tr->d_tok, tr->tok_bytes);
+    if (tr->d_tok) tr->ctx->c.pool_put(tr->d_tok, tr->tok_bytes);
     if (tr->d_rtok) tr->ctx->c.pool_put(tr->d_rtok, tr->tok_bytes);
     tr->ctx->c.pool_put(tr->d_off, tr->off_bytes);
   }
@@ -2139,9 +2161,15 @@ apo_status apo_trie_copy(const apo_trie *tr, uint64_t *d_tokens, int64_t *h_off,
   if (!tr) return APO_ERR_INVALID;
   if (h_off) std::copy(tr->h_off.begin(), tr->h_off.end(), h_off);
   if (tr->ntok > 0 && d_tokens) {
-    cudaError_t e = cudaMemcpyAsync(d_tokens, tr->d_tok, sizeof(u64) * tr->ntok, cudaMemcpyDeviceToDevice,
-                                    static_cast<cudaStream_t>(stream));
-    if (e != cudaSuccess) return APO_ERR_CUDA;
+    if (tr->d_tok) {
+      cudaError_t e = cudaMemcpyAsync(d_tokens, tr->d_tok, sizeof(u64) * tr->ntok, cudaMemcpyDeviceToDevice,
+                                      static_cast<cudaStream_t>(stream));
+      if (e != cudaSuccess) return APO_ERR_CUDA;
+    } else {  // the forward form straight from the kept reversed traces
+      k_reverse_traces<<<grid_for(tr->T * 32, T256), T256, 0, static_cast<cudaStream_t>(stream)>>>(
+          tr->d_rtok, tr->d_off, tr->T, d_tokens);
+      if (cudaGetLastError() != cudaSuccess) return APO_ERR_CUDA;
+    }
   }
   return APO_OK;
 }
@@ -2379,12 +2407,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
         return;
       }
       }  // index computed here (not pre)
-      if (rev && !tr->d_rtok) {
-        tr->d_rtok = static_cast<u64 *>(c.pool_get(tr->tok_bytes));
-        k_reverse_traces<<<grid_for(T * 32, T256), T256, 0, s>>>(tr->d_tok, tr->d_off, T, tr->d_rtok);
-        APO_CHECK_LAUNCH();
-        c.launches++;
-      }
+      if (!rev) trie_forward(c, tr, s);
       StreamMatch sm{p_off, p_wid, p_sa, p_lcp, mtok, rev ? tr->d_rtok : tr->d_tok, tr->d_off, Ns, T};
       // dense-id matching: the traces' comparison values against the batch
       // dictionary (the buckets are keyed by id too)
@@ -2700,6 +2723,7 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
     plan(cv);
     upload_batch(c, b, g, h_s, s);
     build_sa(c, d_streams, b, g.sa, false, s);
+    trie_forward(c, tr, s);
     MatchSetup m{Ns, nstreams, T, g.d_off, g.d_wid, g.sa.sa, d_streams, tr->d_tok, tr->d_off};
     k_trace_search<<<grid_for(T * 32, 256), 256, 0, s>>>(m, ilo, icnt);
     APO_CHECK_LAUNCH();

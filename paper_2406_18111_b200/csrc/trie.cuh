@@ -11,8 +11,10 @@ struct apo_trie {
   apo::i64 ntok = 0;   // total tokens
   apo::i64 maxlen = 0;
   apo::i64 minlen = 0;
-  apo::u64 *d_tok = nullptr;  // traces in id order, back to back
-  mutable apo::u64 *d_rtok = nullptr;  // the same traces, each reversed (built by the first apo_match)
+  // traces in id order, back to back, each reversed (what the matcher reads);
+  // the forward form is made on first use (trie_forward, apo_trie_copy)
+  apo::u64 *d_rtok = nullptr;
+  mutable apo::u64 *d_tok = nullptr;
   apo::i64 *d_off = nullptr;  // T+1
   size_t tok_bytes = 0, off_bytes = 0;  // pooled blocks (returned to the context on destroy)
   std::vector<apo::i64> h_off;
