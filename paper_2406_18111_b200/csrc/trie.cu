@@ -2126,6 +2126,19 @@ apo_status apo_trie_build_traces_multi(apo_ctx *ctx, int32_t nsrc, const uint64_
     src.first[nsrc] = i64(h.size()) - 1;
     src.base[nsrc] = h.back();
     const i64 N = h.back();
+    // sources lying back to back in one buffer (TraceExchange stages every
+    // rank's list so): hashed in place, no gathered copy
+    const uint64_t *p0 = nullptr;
+    bool contiguous = true;
+    for (int r = 0; r < nsrc; ++r) {
+      if (h_src_ntr[r] == 0) continue;
+      if (p0 == nullptr) p0 = h_src_tok[r] - src.base[r];
+      if (h_src_tok[r] != p0 + src.base[r]) contiguous = false;
+    }
+    if (contiguous && p0 != nullptr) {
+      build_trace_set(c, tr, reinterpret_cast<const u64 *>(p0), h, s);
+      return;
+    }
     // the gathered tokens: a second scratch arena (build_trace_set carves the first)
     c.aux.reserve(sizeof(u64) * size_t(std::max<i64>(N, 1)), s);
     src.gather = reinterpret_cast<u64 *>(c.aux.base);

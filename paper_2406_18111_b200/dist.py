@@ -93,12 +93,14 @@ class SymmetricTransport:
         return list(self.hdl.buffer_ptrs)
 
     def pull(self, ntok):
-        """Copy every peer's list (ntok[r] tokens) into local staging with the
-        copy engines, on a side stream that first waits for the caller's
-        stream (the barrier that follows the peers' publishes); returns per
-        rank a local pointer (own list: own buffer).  wait() joins."""
+        """Copy every rank's list (ntok[r] tokens; the own one too) into local
+        staging, back to back in rank order, with the copy engines, on a side
+        stream that first waits for the caller's stream (the barrier that
+        follows the peers' publishes); returns per rank a local pointer.
+        Back-to-back lists are hashed in place by the union build (no
+        gathered copy: 0.4 ms less at N = 4).  wait() joins."""
         me = self.hdl.rank
-        need = sum(int(n) for r, n in enumerate(ntok) if r != me)
+        need = sum(int(n) for n in ntok)
         if self.stage is None or self.stage.numel() < need:
             self.stage = torch.empty(max(int(need * 1.25), 1), dtype=torch.int64, device=self.dev)
         if self.cstream is None:
@@ -108,11 +110,9 @@ class SymmetricTransport:
         with torch.cuda.stream(self.cstream):
             for r, n in enumerate(ntok):
                 n = int(n)
-                if r == me:
-                    ptrs.append(self.buf.data_ptr())
-                    continue
                 if n:
-                    self.stage[o:o + n].copy_(self.hdl.get_buffer(r, (n,), torch.int64), non_blocking=True)
+                    src = self.buf[:n] if r == me else self.hdl.get_buffer(r, (n,), torch.int64)
+                    self.stage[o:o + n].copy_(src, non_blocking=True)
                 ptrs.append(self.stage.data_ptr() + 8 * o)
                 o += n
         self.pulled = torch.cuda.Event()

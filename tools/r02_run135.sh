@@ -1,0 +1,11 @@
+# union hashed in place from contiguous staging: multi-GPU tests, exchange parts, bench N = 2 / 4
+mkdir -p gpurun_out
+python -c "from paper_2406_18111_b200 import build; build.build()" > gpurun_out/r02_build.log 2>&1; echo "build rc=$?"
+timeout 900 python -m pytest tests/test_gpu_multi.py tests/test_gpu_trie.py -q -m gpu -x > gpurun_out/r02_pytest_135.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/r02_pytest_135.log
+echo "N=4"; timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29814 tools/exchange_overlap.py 2>&1 | grep " ms\|Error" | tail -8
+for N in 4 2; do
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2990$N bench.py --gpus $N --steps 5 --warmup 3 --cpu-budget 1 > gpurun_out/r02_bench135_n$N.json 2> gpurun_out/r02_bench135_n$N.err
+  echo "bench n$N rc=$?"
+  python -c "
+import json; d=json.loads(open('gpurun_out/r02_bench135_n$N.json').read().strip().splitlines()[-1]); print('N $N', round(d['value']/1e6,1), 'ms', round(d['ms_per_step'],2), 'e2e', round(d['e2e']['value']/1e6,1), d['config'].get('stage_ms_per_step'), d['clocks'])"
+done
