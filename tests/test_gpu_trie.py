@@ -192,6 +192,17 @@ def test_trie_build_traces_multi_sources(ctx):
     b, bo = ref.traces()
     assert np.array_equal(ao, bo) and torch.equal(a, b)
     assert u.info()[0] < sum(len(o) - 1 for _, o in lists)  # source 3 repeats source 0
+    # the same lists back to back in one buffer (as TraceExchange stages
+    # them): hashed in place, same union; and a union trie's forward traces
+    # come from its reversed ones
+    bases = np.cumsum([0] + [int(o[-1]) for _, o in lists])
+    u2 = ctx.trie_build_traces_multi([(flat.data_ptr() + 8 * int(bases[r]), o) for r, (_, o) in enumerate(lists)])
+    c, co = u2.traces()
+    assert np.array_equal(co, bo) and torch.equal(c, b)
+    r2 = [(flat[int(bases[r]):int(bases[r + 1])].clone(), o) for r, (_, o) in enumerate(lists)]  # gathered
+    hits1 = ctx.match(u2, flat, np.asarray(bases, np.int64), cap=1 << 22)
+    hits2 = ctx.match(ctx.trie_build_traces_multi(r2), flat, np.asarray(bases, np.int64), cap=1 << 22)
+    assert torch.equal(hits1, hits2) and hits1.shape[0] > 0
 
 
 def test_match_large_end_bins(ctx):
