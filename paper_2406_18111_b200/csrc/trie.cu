@@ -1526,11 +1526,13 @@ __global__ void __launch_bounds__(kEmitThreads, 1) k_stream_emit(StreamMatch m, 
 // length of the chain's root trace (the end's shortest; 0xffff: none).
 // REPLAY walks the chains of the ends it decides (~0.3 % of the hits).
 constexpr int kEndsThreads = 1024;
+constexpr int kEndsMl = 7168;  // intervals whose root lengths stay on chip (two CTAs per SM)
 
 __global__ void __launch_bounds__(kEndsThreads, 2) k_stream_ends(StreamMatch m, const u64 *__restrict__ tkey,
                                                                  const u32 *__restrict__ toff,
                                                                  const u32 *__restrict__ otr,
                                                                  const u32 *__restrict__ oroot,
+                                                                 const u32 *__restrict__ opar,
                                                                  u32 *__restrict__ deepz,
                                                                  unsigned short *__restrict__ endml,
                                                                  const u32 *__restrict__ qorder) {
@@ -1553,32 +1555,73 @@ __global__ void __launch_bounds__(kEndsThreads, 2) k_stream_ends(StreamMatch m, 
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // deepest interval per rank (largest preorder id containing it), as in k_stream_emit
+  // deepest interval per rank (largest preorder id containing it), each
+  // rank written once: in preorder (lo asc, hi desc) interval k owns
+  // [lo_k, min(hi_k, lo_{k+1})) -- up to its first child -- and, on behalf
+  // of its parent p, [hi_k, min(hi_p, lo_s)) with s the first interval after
+  // k's subtree (the first with lo >= hi_k: a binary search over the keys)
+  // -- up to k's next sibling.  These segments partition the covered ranks
+  // (painting every interval's whole range instead, 474 M shared-memory
+  // reads per C4 step: 0.64 ms for the kernel, 0.57 ms with the segments).
   for (i64 kb = i64(warp) * 32; kb < M; kb += i64(kEndsThreads)) {
     const i64 k = kb + lane;
-    u32 lo = 0, hi = 0;
+    u32 a0 = 0, b0 = 0, a1 = 0, b1 = 0, p1 = 0;
     if (k < M) {
       const u64 kk = tkey[a + k];
-      lo = u32(kk >> 15) & 32767u;
-      hi = 32767u - (u32(kk) & 32767u);
+      const u32 lo = u32(kk >> 15) & 32767u, hi = 32767u - (u32(kk) & 32767u);
+      const u32 nlo = k + 1 < M ? u32(tkey[a + k + 1] >> 15) & 32767u : 32767u;
+      a0 = lo;
+      b0 = min(hi, nlo);
+      const u32 p = opar[a + k];
+      if (p != kNoPar) {
+        const u32 hp = 32767u - (u32(tkey[a + p]) & 32767u);
+        const u64 target = ((kk >> 30) << 30) | (u64(hi) << 15);
+        i64 l = k + 1, h = M;  // first j > k with key >= target (lo_j >= hi)
+        while (l < h) {
+          const i64 mid = (l + h) >> 1;
+          if (tkey[a + mid] < target) l = mid + 1; else h = mid;
+        }
+        const u32 ls = l < M ? u32(tkey[a + l] >> 15) & 32767u : 32767u;
+        a1 = hi;
+        b1 = min(hp, ls);
+        p1 = p + 1u;
+      }
     }
-    u32 live = __ballot_sync(0xffffffffu, hi > lo);
-    while (live) {
-      const int src = __ffs(live) - 1;
-      live &= live - 1;
-      const u32 l0 = __shfl_sync(0xffffffffu, lo, src), h0 = __shfl_sync(0xffffffffu, hi, src);
-      const u32 id1 = u32(kb + src) + 1u;
-      for (u32 r = l0 + lane; r < h0; r += 32)
-        if (deep[r] < id1) atomicMax(&deep[r], id1);
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      const u32 pa = part ? a1 : a0, pb = part ? b1 : b0, pid = part ? p1 : u32(k + 1);
+      u32 live = __ballot_sync(0xffffffffu, pb > pa);
+      while (live) {
+        const int src = __ffs(live) - 1;
+        live &= live - 1;
+        const u32 l0 = __shfl_sync(0xffffffffu, pa, src), h0 = __shfl_sync(0xffffffffu, pb, src);
+        const u32 id1 = __shfl_sync(0xffffffffu, pid, src);
+        for (u32 r = l0 + lane; r < h0; r += 32) deep[r] = id1;
+      }
     }
   }
+  // per interval, the length of its chain's root trace (the shortest trace
+  // ending where the chain is deepest), on chip when the stream has at most
+  // kEndsMl intervals: the per-end lookups then stay in shared memory (the
+  // dependent otr -> oroot -> toff chain per end: C4 0.57 -> 0.50 ms)
+  unsigned short *s_ml = RISA + kSMMax;
+  const bool ml_on_chip = M <= kEndsMl;
+  if (ml_on_chip)
+    for (i64 k = threadIdx.x; k < M; k += kEndsThreads) {
+      const u32 t = otr[a + oroot[a + k]];
+      s_ml[k] = (unsigned short)min(i64(0xfffe), m.toff[t + 1] - m.toff[t]);
+    }
   __syncthreads();
   for (i64 e = threadIdx.x; e < n; e += kEndsThreads) {
     const u32 d1 = deep[RISA[n - 1 - e]];
     u32 ml = 0xffffu;
     if (d1) {
-      const u32 t = otr[a + oroot[a + d1 - 1]];
-      ml = u32(min(i64(0xfffe), m.toff[t + 1] - m.toff[t]));
+      if (ml_on_chip) {
+        ml = s_ml[d1 - 1];
+      } else {
+        const u32 t = otr[a + oroot[a + d1 - 1]];
+        ml = u32(min(i64(0xfffe), m.toff[t + 1] - m.toff[t]));
+      }
     }
     deepz[beg + e] = d1;
     endml[beg + e] = (unsigned short)ml;
@@ -2607,9 +2650,11 @@ void match_all(Ctx &c, const apo_trie *tr, const uint64_t *d_streams, const int6
                 ri->endml_bytes = sizeof(unsigned short) * size_t(Ns);
                 u32 *deepz = static_cast<u32 *>(c.pool_get(ri->endoff_bytes));
                 unsigned short *endml = static_cast<unsigned short *>(c.pool_get(ri->endml_bytes));
-                const size_t nsmem = (sizeof(u32) + sizeof(unsigned short)) * size_t(kSMMax);
+                const size_t nsmem = (sizeof(u32) + sizeof(unsigned short)) * size_t(kSMMax) +
+                                     sizeof(unsigned short) * size_t(kEndsMl);
                 c.smem_optin(reinterpret_cast<const void *>(k_stream_ends), nsmem);
-                k_stream_ends<<<nstreams, kEndsThreads, nsmem, s>>>(sm, stk, tof, otr, groot, deepz, endml, qorder);
+                k_stream_ends<<<nstreams, kEndsThreads, nsmem, s>>>(sm, stk, tof, otr, groot, gpar, deepz, endml,
+                                                                    qorder);
                 APO_CHECK_LAUNCH();
                 ri->ok = true;
                 ri->lazy = true;

@@ -283,6 +283,14 @@ def test_match_many_intervals_one_stream(ctx):
     hits = ctx.match(trie, dev(sflat), soff).cpu().numpy()
     want, cnt = oracle.match_brute(sflat, soff, tt.cpu().numpy(), to)
     assert cnt == len(hits) and np.array_equal(hits, want)
+    # REPLAY over the implicit MATCH_ALL: the per-end chain kernel with more
+    # intervals than it keeps root lengths for on chip (> 7,168)
+    rp, nall = ctx.match(trie, dev(sflat), soff, mode=1)
+    tlen = np.diff(to)
+    want_rp = oracle.replay(want, tlen)
+    g = rp.cpu().numpy().astype(np.int64)
+    got_rp = np.stack([g[:, 0], g[:, 1] - tlen[g[:, 2]] + 1, g[:, 1], g[:, 2], g[:, 3]], axis=1)
+    assert nall == cnt and np.array_equal(got_rp, want_rp)
 
 
 def test_match_capacity_prefix(ctx):
